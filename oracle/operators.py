@@ -1,0 +1,149 @@
+"""The user operator: ``matvec`` / ``cmatvec``.  TEST INFRASTRUCTURE ONLY.
+
+P:95 (§5): "All the communication to matvec, cmatvec is set in module
+arraymodule.  User can implement his/her own sparse matrix scheme in matvec
+and cmatvec."  P:17 (abstract): the matrix-vector product is "separated from
+the conjugate gradient iterations itself".
+
+Each operator exposes
+
+* ``apply(x)``   = A·x                 (matvec)
+* ``apply_h(x)`` = Aᴴ·x                (cmatvec)
+* ``apply_t(x)`` = Aᵀ·x (unconjugated)
+
+and counts its applications (work accounting).
+
+Dense storage is row-major.  Aᴴx is formed as conj(conj(x)ᵀ·A) so that the
+matrix is never copied or conjugated.  CSR uses
+scipy.sparse for floating dtypes (library primitive) and a plain double loop
+for object dtypes (exact / mpmath modes) and the CSR pins.
+"""
+
+import numpy as np
+
+
+class _Counted:
+    def __init__(self):
+        self.n_a = 0
+        self.n_ah = 0
+        self.n_at = 0
+
+    def reset_counts(self):
+        self.n_a = self.n_ah = self.n_at = 0
+
+
+class DenseOp(_Counted):
+    """Dense row-major n×n operator."""
+
+    def __init__(self, A):
+        super().__init__()
+        A = np.asarray(A)
+        if A.ndim != 2 or A.shape[0] != A.shape[1]:
+            raise ValueError("DenseOp needs a square matrix")
+        self.A = A
+        self.n = A.shape[0]
+        self.dtype = A.dtype
+
+    def apply(self, x):
+        self.n_a += 1
+        return self.A.dot(x)
+
+    def apply_h(self, x):
+        self.n_ah += 1
+        return np.conj(np.conj(x).dot(self.A))
+
+    def apply_t(self, x):
+        self.n_at += 1
+        return x.dot(self.A)
+
+
+class CsrOp(_Counted):
+    """CSR operator: rowptr (n+1), colind (nnz), vals (nnz)."""
+
+    def __init__(self, rowptr, colind, vals, n=None):
+        super().__init__()
+        self.rowptr = np.asarray(rowptr)
+        self.colind = np.asarray(colind)
+        self.vals = np.asarray(vals)
+        self.n = len(self.rowptr) - 1 if n is None else n
+        self.dtype = self.vals.dtype
+        if self.vals.dtype != object:
+            import scipy.sparse as sp
+            self._M = sp.csr_matrix((self.vals, self.colind, self.rowptr),
+                                    shape=(self.n, self.n))
+        else:
+            self._M = None
+
+    def _loop(self, x, conj_vals, transpose):
+        out = np.zeros(self.n, dtype=x.dtype) if x.dtype != object else \
+            np.array([0] * self.n, dtype=object)
+        for i in range(self.n):
+            for k in range(self.rowptr[i], self.rowptr[i + 1]):
+                v = self.vals[k]
+                if conj_vals:
+                    v = v.conjugate()
+                j = self.colind[k]
+                if transpose:
+                    out[j] = out[j] + v * x[i]
+                else:
+                    out[i] = out[i] + v * x[j]
+        return out
+
+    def apply(self, x):
+        self.n_a += 1
+        if self._M is None:
+            return self._loop(x, False, False)
+        return self._M.dot(x)
+
+    def apply_h(self, x):
+        self.n_ah += 1
+        if self._M is None:
+            return self._loop(x, True, True)
+        return np.conj(self._M.T.dot(np.conj(x)))
+
+    def apply_t(self, x):
+        self.n_at += 1
+        if self._M is None:
+            return self._loop(x, False, True)
+        return self._M.T.dot(x)
+
+    def apply_loop(self, x, op="A"):
+        """Plain double-loop product (no scipy) — used to pin the scipy path."""
+        return self._loop(x, op == "AH", op in ("AH", "AT"))
+
+    def to_dense(self):
+        D = np.zeros((self.n, self.n), dtype=self.vals.dtype)
+        for i in range(self.n):
+            for k in range(self.rowptr[i], self.rowptr[i + 1]):
+                D[i, self.colind[k]] += self.vals[k]
+        return D
+
+
+def reference_apply(A, x, op="A"):
+    """Per-matvec parity reference.
+
+    Accumulated more accurately than the working precision: complex64
+    inputs are promoted to complex128 and the product is taken with numpy
+    (BLAS zgemv); complex128 inputs go straight to zgemv.  ``A`` may be a
+    dense array or a CsrOp."""
+    if isinstance(A, CsrOp):
+        op_ = CsrOp(A.rowptr, A.colind, A.vals.astype(np.complex128), A.n)
+        xx = np.asarray(x, dtype=np.complex128)
+        return {"A": op_.apply, "AH": op_.apply_h, "AT": op_.apply_t}[op](xx)
+    A = np.asarray(A)
+    xx = np.asarray(x, dtype=np.complex128)
+    AA = A.astype(np.complex128, copy=False)
+    if op == "A":
+        return AA.dot(xx)
+    if op == "AH":
+        return np.conj(np.conj(xx).dot(AA))
+    if op == "AT":
+        return xx.dot(AA)
+    raise ValueError(op)
+
+
+def check_complex_symmetric(A, tol=0.0):
+    """max|A_ij − A_ji| ≤ tol·max|A| (unconjugated)."""
+    A = np.asarray(A)
+    m = np.max(np.abs(A)) if A.size else 0.0
+    return bool(np.max(np.abs(A - A.T)) <= tol * m) if A.size else True

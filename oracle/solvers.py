@@ -1,0 +1,495 @@
+"""The five hot-path Krylov recurrences, step by step.  TEST INFRASTRUCTURE ONLY.
+
+The paper names the methods and cites their sources but writes none of them
+down (BiCGSTAB, CGNE, QMR: PIM90 set, §2.1, QMR "changed" per P:57 and
+Chaumet's corrected version P:101 §6; BiCOR / CORS: Carpentieri, Jing & Huang
+2011, §2.4).  The recurrences below follow SURVEY.md §8(c) O1-O5
+line by line, in that notation, with the readings Q1-Q16 listed in
+DESIGN.md §"Readings of the paper".  BiCG, CGS and COCR (§3.4) are
+included only as independent pins: BiCOR ≡ BiCG(shadow Aᴴr₀*), CORS ≡
+CGS(shadow Aᴴr₀*), BiCOR(r₀* = conj r₀) ≡ COCR on complex-symmetric A.
+
+Common rules (SURVEY.md §8(c) "Common rules"):
+
+* x₀ = 0 unless given; r₀ = y − A·x₀.
+* stop when the recurrence residual satisfies ‖r_k‖² ≤ tol²·‖r₀‖²
+  (equivalent to ‖r_k‖ ≤ tol·‖r₀‖; squared so that exact rational
+  arithmetic needs no square root);
+* ‖r₀‖ = 0 → CONVERGED with 0 iterations;
+* a divisor that is exactly 0 → BREAKDOWN(name) (Q6), iterations =
+  completed iterations; any non-finite scalar → NONFINITE;
+* at exit the true residual ‖y − A·x̂‖/‖r₀‖ is recomputed;
+  CONVERGED with true residual > 10·tol → FALSE_CONVERGENCE;
+* ``iterations`` counts outer steps; ``matvecs_a/_ah`` count every
+  operator application of the recurrence (setup included, the final
+  true-residual check excluded).
+
+Arithmetic is in the working precision of the inputs (complex64 or
+complex128 numpy arrays), or exact (object arrays of
+``exact.GaussianRational``), or mpmath (object arrays of ``mpmath.mpc``).
+"""
+
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+
+from .numerics import dotc, dotu, norm_sq, sqrt
+
+CONVERGED, MAXIT, BREAKDOWN, FALSE_CONVERGENCE, NONFINITE = 0, 1, 2, 3, 4
+STATUS_NAMES = {0: "CONVERGED", 1: "MAXIT", 2: "BREAKDOWN",
+                3: "FALSE_CONVERGENCE", 4: "NONFINITE"}
+# breakdown codes (shared *numbering* with include/ccg.h; no code is shared)
+BREAKDOWN_CODES = {None: 0, "rho": 1, "sigma": 2, "tt": 3, "omega": 4,
+                   "pi": 5, "delta": 6, "epsilon": 7, "beta": 8, "xi": 9,
+                   "vnorm": 10, "wnorm": 11, "gamma": 12}
+
+
+@dataclass
+class Result:
+    x: np.ndarray
+    status: int
+    iterations: int
+    matvecs_a: int
+    matvecs_ah: int
+    breakdown: Optional[str] = None
+    rec_rel_res: float = float("nan")
+    true_rel_res: float = float("nan")
+    history: list = field(default_factory=list)   # ‖r_k‖ (recurrence), k = 0..
+    half_step: bool = False                        # BiCGSTAB exit on ‖s‖
+
+    @property
+    def status_name(self):
+        return STATUS_NAMES[self.status]
+
+
+class _Breakdown(Exception):
+    def __init__(self, name):
+        super().__init__(name)
+        self.name = name
+
+
+class _NonFinite(Exception):
+    pass
+
+
+class _Ctx:
+    """Per-solve scalar policy: keeps every scalar in the working precision."""
+
+    def __init__(self, y):
+        self.obj = (y.dtype == object)
+        if not self.obj:
+            self.ctype = y.dtype.type                       # complex64/128
+            self.rtype = np.finfo(y.dtype).dtype.type       # float32/64
+
+    def c(self, s):
+        return s if self.obj else self.ctype(s)
+
+    def r(self, s):
+        return s if self.obj else self.rtype(s)
+
+    def check(self, *vals):
+        if self.obj:
+            return
+        for v in vals:
+            if not np.isfinite(v):
+                raise _NonFinite()
+
+    def div(self, num, den, name):
+        if den == 0:
+            raise _Breakdown(name)
+        q = num / den
+        self.check(q)
+        return q
+
+
+def _zero_like(y):
+    if y.dtype == object:
+        return np.array([0 * y[0]] * len(y), dtype=object) if len(y) else y.copy()
+    return np.zeros_like(y)
+
+
+def _init(op, y, x0):
+    """x₀ and r₀ = y − A·x₀ (x₀ = 0 → r₀ = y with no matvec)."""
+    if x0 is None:
+        return _zero_like(y), y.copy()
+    x = np.array(x0, dtype=y.dtype, copy=True)
+    return x, y - op.apply(x)
+
+
+def _finish(op, y, res, r0sq, tol, ctx):
+    """True residual and FALSE_CONVERGENCE guard."""
+    x = res.x
+    rt = y - op.apply(x)
+    if op is not None:                       # not counted as work
+        op.n_a -= 1
+    if ctx.obj:
+        tr = float(norm_sq(rt)) ** 0.5
+        r0 = float(r0sq) ** 0.5
+    else:
+        tr = float(np.linalg.norm(rt.astype(np.complex128)))
+        r0 = float(np.sqrt(np.float64(r0sq)))
+    res.true_rel_res = tr / r0 if r0 > 0 else 0.0
+    if res.history:
+        res.rec_rel_res = float(res.history[-1]) / r0 if r0 > 0 else 0.0
+    if not ctx.obj and not np.all(np.isfinite(x)):
+        res.status = NONFINITE
+    if res.status == CONVERGED and res.true_rel_res > 10 * tol:
+        res.status = FALSE_CONVERGENCE
+    res.matvecs_a = op.n_a
+    res.matvecs_ah = op.n_ah
+    return res
+
+
+def _run(body, op, y, tol, maxit, x0, **kw):
+    """Shared driver: setup, r0 check, exception → status mapping, finalize."""
+    y = np.asarray(y)
+    ctx = _Ctx(y)
+    op.reset_counts()
+    x, r = _init(op, y, x0)
+    r0sq = norm_sq(r)
+    tol2 = tol * tol
+    hist = [sqrt(r0sq)]
+    state = {"x": x, "k": 0}
+    res = Result(x=x, status=MAXIT, iterations=0, matvecs_a=0, matvecs_ah=0,
+                 history=hist)
+    if r0sq == 0:
+        res.status = CONVERGED
+        return _finish(op, y, res, r0sq, tol, ctx)
+    try:
+        status, k, half = body(op, y, x, r, r0sq, tol2, maxit, ctx, hist, state, **kw)
+        res.status, res.iterations, res.half_step = status, k, half
+    except _Breakdown as e:
+        res.status, res.breakdown = BREAKDOWN, e.name
+        res.iterations = state["k"] - 1
+    except _NonFinite:
+        res.status = NONFINITE
+        res.iterations = state["k"] - 1
+    res.x = state["x"]
+    return _finish(op, y, res, r0sq, tol, ctx)
+
+
+def _conv(rr, tol2, r0sq):
+    return rr <= tol2 * r0sq
+
+
+# ---------------------------------------------------------------------------
+# O1 BiCGSTAB (van der Vorst).  Only A·x.  Shadow r̃ = r₀.
+# ---------------------------------------------------------------------------
+def _bicgstab(op, y, x, r, r0sq, tol2, maxit, ctx, hist, st, shadow=None):
+    rt = r.copy() if shadow is None else np.asarray(shadow, dtype=y.dtype)
+    one = ctx.c(1)
+    rho_prev = alpha = omega = one
+    p = v = None
+    for k in range(1, maxit + 1):
+        st["k"] = k
+        rho = ctx.c(dotc(rt, r))                               # ρ = ⟨r̃, r⟩
+        ctx.check(rho)
+        if rho == 0:
+            raise _Breakdown("rho")
+        if k == 1:
+            p = r.copy()                                        # p = r
+        else:
+            beta = ctx.c((rho / rho_prev) * (alpha / omega))
+            p = r + beta * (p - omega * v)                      # p = r + β(p − ωv)
+        v = op.apply(p)                                         # v = A p
+        sigma = ctx.c(dotc(rt, v))                              # σ = ⟨r̃, v⟩
+        alpha = ctx.c(ctx.div(rho, sigma, "sigma"))             # α = ρ/σ
+        s = r - alpha * v                                       # s = r − αv
+        ss = ctx.r(norm_sq(s))
+        ctx.check(ss)
+        if _conv(ss, tol2, r0sq):                               # half-step exit (Q4)
+            st["x"] = x = x + alpha * p
+            hist.append(sqrt(ss))
+            return CONVERGED, k, True
+        t = op.apply(s)                                         # t = A s
+        tt = ctx.r(norm_sq(t))
+        ts = ctx.c(dotc(t, s))
+        omega = ctx.c(ctx.div(ts, tt, "tt"))                    # ω = ⟨t,s⟩/⟨t,t⟩
+        if omega == 0:
+            raise _Breakdown("omega")
+        st["x"] = x = x + alpha * p + omega * s                 # x += αp + ωs
+        r = s - omega * t                                       # r = s − ωt
+        rr = ctx.r(norm_sq(r))
+        ctx.check(rr)
+        hist.append(sqrt(rr))
+        if _conv(rr, tol2, r0sq):
+            return CONVERGED, k, False
+        rho_prev = rho
+    return MAXIT, maxit, False
+
+
+# ---------------------------------------------------------------------------
+# O2 CGNE (Craig's method = CG on AAᴴu = y, x = Aᴴu; Q1).
+# ---------------------------------------------------------------------------
+def _cgne(op, y, x, r, r0sq, tol2, maxit, ctx, hist, st):
+    p = op.apply_h(r)                                           # p = Aᴴ r
+    rho = ctx.r(r0sq)                                           # ρ = ‖r‖²
+    for k in range(1, maxit + 1):
+        st["k"] = k
+        pi = ctx.r(norm_sq(p))                                  # π = ‖p‖²
+        alpha = ctx.r(ctx.div(rho, pi, "pi"))                   # α = ρ/π
+        st["x"] = x = x + alpha * p                             # x += αp
+        q = op.apply(p)
+        r = r - alpha * q                                       # r −= α A p
+        rho_new = ctx.r(norm_sq(r))
+        ctx.check(rho_new)
+        hist.append(sqrt(rho_new))
+        if _conv(rho_new, tol2, r0sq):
+            return CONVERGED, k, False
+        beta = ctx.r(rho_new / rho)
+        p = op.apply_h(r) + beta * p                            # p = Aᴴr + βp
+        rho = rho_new
+    return MAXIT, maxit, False
+
+
+# ---------------------------------------------------------------------------
+# O3 QMR (Freund–Nachtigal without look-ahead, Templates form,
+# M = I, Q2).  form="H": conjugated products and Aᴴ, w̃₁ = r₀.
+# form="T": bilinear products and Aᵀ, w̃₁ = conj(r₀) (pin: identical iterates).
+# ---------------------------------------------------------------------------
+def _qmr(op, y, x, r, r0sq, tol2, maxit, ctx, hist, st, form="H", shadow=None):
+    if form == "H":
+        ip, adj, cj = dotc, op.apply_h, (lambda z: z.conjugate())
+        wt = r.copy() if shadow is None else np.asarray(shadow, dtype=y.dtype)
+    else:
+        ip, adj, cj = dotu, op.apply_t, (lambda z: z)
+        wt = np.conj(r) if shadow is None else np.asarray(shadow, dtype=y.dtype)
+    vt = r.copy()                                               # ṽ = r
+    rho = ctx.r(sqrt(norm_sq(vt)))                              # ρ = ‖ṽ‖
+    xi = ctx.r(sqrt(norm_sq(wt)))                               # ξ = ‖w̃‖
+    gamma_prev = ctx.r(1)
+    eta = ctx.c(-1)
+    theta_prev = ctx.r(0)
+    eps = None
+    p = q = d = s = None
+    for i in range(1, maxit + 1):
+        st["k"] = i
+        if rho == 0:
+            raise _Breakdown("vnorm")
+        if xi == 0:
+            raise _Breakdown("wnorm")
+        v = vt / rho                                            # v = ṽ/ρ
+        w = wt / xi                                             # w = w̃/ξ
+        delta = ctx.c(ip(w, v))                                 # δ = ⟨w, v⟩
+        ctx.check(delta)
+        if delta == 0:
+            raise _Breakdown("delta")
+        if i == 1:
+            p = v.copy()
+            q = w.copy()
+        else:
+            p = v - ctx.c(xi * delta / eps) * p                 # p = v − (ξδ/ε)p
+            q = w - ctx.c(cj(rho * delta / eps)) * q            # q = w − conj(ρδ/ε)q
+        pt = op.apply(p)                                        # p̃ = A p
+        eps = ctx.c(ip(q, pt))                                  # ε = ⟨q, p̃⟩
+        ctx.check(eps)
+        if eps == 0:
+            raise _Breakdown("epsilon")
+        beta = ctx.c(eps / delta)                               # β = ε/δ
+        if beta == 0:
+            raise _Breakdown("beta")
+        vt = pt - beta * v                                      # ṽ = p̃ − βv
+        rho_next = ctx.r(sqrt(norm_sq(vt)))
+        wt = adj(q) - ctx.c(cj(beta)) * w                       # w̃ = Aᴴq − conj(β)w
+        xi_next = ctx.r(sqrt(norm_sq(wt)))
+        theta = ctx.r(rho_next / (gamma_prev * abs(beta)))      # θ = ρ'/(γ_prev|β|)
+        gamma = ctx.r(1 / sqrt(1 + theta * theta))              # γ = 1/√(1+θ²)
+        ctx.check(theta, gamma)
+        if gamma == 0:
+            raise _Breakdown("gamma")
+        eta = ctx.c(-eta * rho * gamma * gamma /
+                    (beta * gamma_prev * gamma_prev))           # η
+        if i == 1:
+            d = eta * p
+            s = eta * pt
+        else:
+            c2 = ctx.r((theta_prev * gamma) * (theta_prev * gamma))
+            d = eta * p + c2 * d                                # d = ηp + (θ_prev γ)² d
+            s = eta * pt + c2 * s                               # s = ηp̃ + (θ_prev γ)² s
+        st["x"] = x = x + d                                     # x += d
+        r = r - s                                               # r −= s
+        rr = ctx.r(norm_sq(r))
+        ctx.check(rr)
+        hist.append(sqrt(rr))
+        if _conv(rr, tol2, r0sq):
+            return CONVERGED, i, False
+        rho, xi, gamma_prev, theta_prev = rho_next, xi_next, gamma, theta
+    return MAXIT, maxit, False
+
+
+# ---------------------------------------------------------------------------
+# O4 BiCOR (Carpentieri–Jing–Huang).  Shadow r₀* = r₀ (Q3).
+# ---------------------------------------------------------------------------
+def _bicor(op, y, x, r, r0sq, tol2, maxit, ctx, hist, st, shadow=None):
+    rs = r.copy() if shadow is None else np.array(shadow, dtype=y.dtype, copy=True)
+    p = ps = q = None
+    rho_prev = None
+    for k in range(1, maxit + 1):
+        st["k"] = k
+        rh = op.apply(r)                                        # r̂ = A r
+        rho = ctx.c(dotc(rs, rh))                               # ρ = ⟨r*, r̂⟩
+        ctx.check(rho)
+        if rho == 0:
+            raise _Breakdown("rho")
+        if k == 1:
+            p, ps, q = r.copy(), rs.copy(), rh.copy()
+        else:
+            beta = ctx.c(rho / rho_prev)
+            p = r + beta * p                                    # p = r + βp
+            ps = rs + ctx.c(beta.conjugate()) * ps              # p* = r* + conj(β)p*
+            q = rh + beta * q                                   # q = r̂ + βq
+        qs = op.apply_h(ps)                                     # q* = Aᴴ p*
+        xi = ctx.c(dotc(qs, q))                                 # ξ = ⟨q*, q⟩
+        alpha = ctx.c(ctx.div(rho, xi, "xi"))                   # α = ρ/ξ
+        st["x"] = x = x + alpha * p                             # x += αp
+        r = r - alpha * q                                       # r −= αq
+        rs = rs - ctx.c(alpha.conjugate()) * qs                 # r* −= conj(α)q*
+        rr = ctx.r(norm_sq(r))
+        ctx.check(rr)
+        hist.append(sqrt(rr))
+        if _conv(rr, tol2, r0sq):
+            return CONVERGED, k, False
+        rho_prev = rho
+    return MAXIT, maxit, False
+
+
+# ---------------------------------------------------------------------------
+# O5 CORS.  BiCOR "squared"; transpose-free (Q15).  r₀* = r₀.
+# ---------------------------------------------------------------------------
+def _cors(op, y, x, r, r0sq, tol2, maxit, ctx, hist, st, shadow=None):
+    r0s = r.copy() if shadow is None else np.asarray(shadow, dtype=y.dtype)
+    e = eh = qh = h = hh = None
+    rho_prev = None
+    for k in range(1, maxit + 1):
+        st["k"] = k
+        rh = op.apply(r)                                        # r̂ = A r
+        rho = ctx.c(dotc(r0s, rh))                              # ρ = ⟨r₀*, r̂⟩
+        ctx.check(rho)
+        if rho == 0:
+            raise _Breakdown("rho")
+        if k == 1:
+            e, eh, qh = r.copy(), rh.copy(), rh.copy()
+        else:
+            beta = ctx.c(rho / rho_prev)
+            e = r + beta * h                                    # e = r + βh
+            eh = rh + beta * hh                                 # ê = r̂ + βĥ
+            qh = eh + beta * (hh + beta * qh)                   # q̂ = ê + β(ĥ + βq̂)
+        q = op.apply(qh)                                        # q = A q̂
+        xi = ctx.c(dotc(r0s, q))                                # ξ = ⟨r₀*, q⟩
+        alpha = ctx.c(ctx.div(rho, xi, "xi"))                   # α = ρ/ξ
+        h = e - alpha * qh                                      # h = e − αq̂
+        hh = eh - alpha * q                                     # ĥ = ê − αq
+        st["x"] = x = x + alpha * (e + h)                       # x += α(e + h)
+        r = r - alpha * (eh + hh)                               # r −= α(ê + ĥ)
+        rr = ctx.r(norm_sq(r))
+        ctx.check(rr)
+        hist.append(sqrt(rr))
+        if _conv(rr, tol2, r0sq):
+            return CONVERGED, k, False
+        rho_prev = rho
+    return MAXIT, maxit, False
+
+
+# ---------------------------------------------------------------------------
+# Pins only (not on the hot path): BiCG, CGS, COCR (§3.4).
+# ---------------------------------------------------------------------------
+def _bicg(op, y, x, r, r0sq, tol2, maxit, ctx, hist, st, shadow=None):
+    rt = r.copy() if shadow is None else np.array(shadow, dtype=y.dtype, copy=True)
+    p = pt = None
+    rho_prev = None
+    for k in range(1, maxit + 1):
+        st["k"] = k
+        rho = ctx.c(dotc(rt, r))
+        if rho == 0:
+            raise _Breakdown("rho")
+        if k == 1:
+            p, pt = r.copy(), rt.copy()
+        else:
+            beta = ctx.c(rho / rho_prev)
+            p = r + beta * p
+            pt = rt + ctx.c(beta.conjugate()) * pt
+        q = op.apply(p)
+        qt = op.apply_h(pt)
+        alpha = ctx.c(ctx.div(rho, dotc(pt, q), "sigma"))
+        st["x"] = x = x + alpha * p
+        r = r - alpha * q
+        rt = rt - ctx.c(alpha.conjugate()) * qt
+        rr = ctx.r(norm_sq(r))
+        hist.append(sqrt(rr))
+        if _conv(rr, tol2, r0sq):
+            return CONVERGED, k, False
+        rho_prev = rho
+    return MAXIT, maxit, False
+
+
+def _cgs(op, y, x, r, r0sq, tol2, maxit, ctx, hist, st, shadow=None):
+    rt = r.copy() if shadow is None else np.asarray(shadow, dtype=y.dtype)
+    u = p = q = None
+    rho_prev = None
+    for k in range(1, maxit + 1):
+        st["k"] = k
+        rho = ctx.c(dotc(rt, r))
+        if rho == 0:
+            raise _Breakdown("rho")
+        if k == 1:
+            u = r.copy()
+            p = u.copy()
+        else:
+            beta = ctx.c(rho / rho_prev)
+            u = r + beta * q
+            p = u + beta * (q + beta * p)
+        v = op.apply(p)
+        alpha = ctx.c(ctx.div(rho, dotc(rt, v), "sigma"))
+        q = u - alpha * v
+        uq = u + q
+        st["x"] = x = x + alpha * uq
+        r = r - alpha * op.apply(uq)
+        rr = ctx.r(norm_sq(r))
+        hist.append(sqrt(rr))
+        if _conv(rr, tol2, r0sq):
+            return CONVERGED, k, False
+        rho_prev = rho
+    return MAXIT, maxit, False
+
+
+def _cocr(op, y, x, r, r0sq, tol2, maxit, ctx, hist, st):
+    Ar = op.apply(r)
+    p, Ap = r.copy(), Ar.copy()
+    mu = ctx.c(dotu(r, Ar))
+    for k in range(1, maxit + 1):
+        st["k"] = k
+        if k > 1:
+            p = r + beta * p
+            Ap = Ar + beta * Ap
+        alpha = ctx.c(ctx.div(mu, dotu(Ap, Ap), "xi"))
+        st["x"] = x = x + alpha * p
+        r = r - alpha * Ap
+        rr = ctx.r(norm_sq(r))
+        hist.append(sqrt(rr))
+        if _conv(rr, tol2, r0sq):
+            return CONVERGED, k, False
+        Ar = op.apply(r)
+        mu_new = ctx.c(dotu(r, Ar))
+        beta = ctx.c(ctx.div(mu_new, mu, "rho"))
+        mu = mu_new
+    return MAXIT, maxit, False
+
+
+METHODS = {
+    "bicgstab": _bicgstab, "cgne": _cgne, "qmr": _qmr, "bicor": _bicor,
+    "cors": _cors,
+    # pins only
+    "bicg": _bicg, "cgs": _cgs, "cocr": _cocr,
+}
+HOT_PATH = ("bicgstab", "cgne", "qmr", "bicor", "cors")
+
+
+def solve(method, op, y, tol, maxit, x0=None, **kw):
+    """Run ``method`` on A x = y (A given as an operator with apply/apply_h/apply_t).
+
+    Returns a :class:`Result`.  ``kw`` passes method options (``shadow`` for
+    BiCGSTAB/BiCOR/CORS/BiCG/CGS/QMR, ``form`` for QMR)."""
+    if method not in METHODS:
+        raise ValueError(f"unknown method {method!r}")
+    return _run(METHODS[method], op, y, tol, maxit, x0, **kw)
