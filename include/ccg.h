@@ -1,0 +1,202 @@
+/*
+ * ccg.h — C-ABI of libccg.so, the B200 (sm_100a) hot path of the complex
+ * conjugate-gradient family catalogued by CCGPAK (Flatau, arXiv:1208.4869).
+ *
+ * Citations: "P:<n>" = /root/reference/PAPER.md line n (its section in
+ * brackets); "S:<n>" = SPEC.md line n; "SURVEY §x" = /root/repo/SURVEY.md.
+ *
+ * The paper's contract is a user-supplied matrix-vector product kept apart
+ * from the Krylov iteration (P:17 [abstract]: "mechanism for matrix times
+ * vector multiplication which is separated from the conjugate gradient
+ * iterations itself"; P:95 [§5]: matvec / cmatvec in module arraymodule), a
+ * configuration record carrying the tolerance epsilon_err and maxit (P:95
+ * [§5], module cgmodule), and a single/double precision switch (P:17, P:95
+ * [§5], ddprecision.f90).  This header maps them to:
+ *
+ *   ccg_create             precision switch (CCG_C64 / CCG_C128) + device/comm
+ *   ccg_set_matvec_dense   matvec/cmatvec over a dense row-major matrix
+ *   ccg_set_matvec_csr     matvec over a CSR matrix ("own sparse matrix scheme")
+ *   ccg_apply              one product A·x, Aᴴ·x or Aᵀ·x (per-matvec parity hook)
+ *   ccg_solve              one solve by BiCGSTAB / CGNE / QMR (P:57 [§2.1]) or
+ *                          BiCOR / CORS (P:69 [§2.4]) with epsilon_err, maxit
+ *   ccg_destroy
+ *
+ * Conventions for every function:
+ *  - Complex numbers are interleaved (re, im) pairs: CCG_C64 = 2 x float
+ *    (8 bytes), CCG_C128 = 2 x double (16 bytes).  Vectors are contiguous.
+ *  - Return value: a ccg_err (0 = CCG_OK).  On error nothing is half-done
+ *    that the caller must undo; ccg_last_error(h) gives a one-line reason.
+ *    Solver OUTCOMES (max iterations, breakdown, ...) are not errors: they
+ *    are reported in ccg_result.status.
+ *  - Multi-GPU: one process per GPU (world ranks).  Every rank calls
+ *    ccg_apply / ccg_solve collectively with the same arguments except the
+ *    vector pointers, which hold that rank's row slice; every rank receives
+ *    the same ccg_result.
+ *  - No CPU fallback: every arithmetic step runs in libccg's CUDA kernels.
+ *    Without a usable CUDA device ccg_create returns CCG_E_CUDA.
+ */
+#ifndef CCG_H_
+#define CCG_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct ccg_ctx* ccg_handle;
+
+/* Working precision ("simple to switch between single and double
+ * precisions"; ddprecision.f90).  Matrix, vectors and matvec
+ * arithmetic are in this precision; reductions (dot products, norms) are
+ * accumulated in fp64 and the recurrence scalars are kept in fp64. */
+typedef enum { CCG_C64 = 0, CCG_C128 = 1 } ccg_dtype;
+
+/* Methods on the hot path (BASELINE.json north_star).  BiCGSTAB, CGNE, QMR:
+ * PIM90 set (P:57 [§2.1]; QMR as corrected, P:101 [§6]).  BiCOR, CORS:
+ * Carpentieri-Jing-Huang (P:69 [§2.4]).  Recurrences: SURVEY §8(c) O1-O5 /
+ * DESIGN.md.  Operator needs: BiCGSTAB, CORS -> A·x only; CGNE, QMR, BiCOR ->
+ * A·x and Aᴴ·x. */
+typedef enum {
+  CCG_BICGSTAB = 0,
+  CCG_CGNE = 1,
+  CCG_QMR = 2,
+  CCG_BICOR = 3,
+  CCG_CORS = 4
+} ccg_method;
+
+/* The three products of the operator module: A·x (matvec),
+ * Aᴴ·x (cmatvec, conjugate transpose), Aᵀ·x (unconjugated transpose). */
+typedef enum { CCG_OP_A = 0, CCG_OP_AH = 1, CCG_OP_AT = 2 } ccg_op;
+
+/* Flags for ccg_set_matvec_*.  CCG_FLAG_SYMMETRIC: caller asserts A == Aᵀ
+ * (complex symmetric, unconjugated).  Not verified by the
+ * library.  For CSR it enables Aᴴ·x = conj(A·conj(x)) (single GPU only). */
+enum { CCG_FLAG_SYMMETRIC = 1 };
+
+typedef enum {
+  CCG_OK = 0,
+  CCG_E_ARG = -1,        /* NULL handle/pointer, bad enum, tol < 0, maxit < 1, misaligned */
+  CCG_E_DIM = -2,        /* sizes inconsistent with the handle (n, nloc, row0, lda, nnz) */
+  CCG_E_CAPABILITY = -3, /* method/op needs Aᴴ (or Aᵀ) the operator cannot provide */
+  CCG_E_STATE = -4,      /* ccg_apply/ccg_solve before any ccg_set_matvec_* */
+  CCG_E_CUDA = -5,       /* CUDA runtime error (text in ccg_last_error) */
+  CCG_E_NCCL = -6,       /* NCCL error or NCCL unavailable with world > 1 */
+  CCG_E_OOM = -7         /* device allocation failed */
+} ccg_err;
+
+/* Solve outcome (mirrors SPEC SolverOutcome). */
+typedef enum {
+  CCG_CONVERGED = 0,         /* ‖r_k‖ ≤ tol·‖r_0‖ on the recurrence residual */
+  CCG_MAXIT = 1,             /* maxit outer iterations without convergence */
+  CCG_BREAKDOWN = 2,         /* a recurrence divisor was exactly 0 (breakdown_code names it) */
+  CCG_FALSE_CONVERGENCE = 3, /* converged on the recurrence but true residual > 10·tol */
+  CCG_NONFINITE = 4          /* a NaN/Inf reached a recurrence scalar */
+} ccg_status;
+
+/* Breakdown codes: which divisor vanished (SURVEY §8(c) O1-O5 names). */
+typedef enum {
+  CCG_BD_NONE = 0, CCG_BD_RHO = 1, CCG_BD_SIGMA = 2, CCG_BD_TT = 3, CCG_BD_OMEGA = 4,
+  CCG_BD_PI = 5, CCG_BD_DELTA = 6, CCG_BD_EPSILON = 7, CCG_BD_BETA = 8, CCG_BD_XI = 9,
+  CCG_BD_VNORM = 10, CCG_BD_WNORM = 11, CCG_BD_GAMMA = 12
+} ccg_breakdown;
+
+typedef struct {
+  int32_t status;         /* ccg_status */
+  int32_t iterations;     /* outer iterations completed; BiCGSTAB half-step exit counts k */
+  int32_t matvecs_a;      /* A·x applications by the recurrence (setup included, final check excluded) */
+  int32_t matvecs_ah;     /* Aᴴ·x applications */
+  int32_t breakdown_code; /* ccg_breakdown */
+  int32_t half_step;      /* 1 if BiCGSTAB exited on ‖s‖ */
+  double rec_rel_res;     /* last recurrence residual ‖r_k‖/‖r_0‖ */
+  double true_rel_res;    /* ‖y − A·x̂‖/‖r_0‖ recomputed at exit */
+  double wall_ms;         /* host wall time of the call */
+} ccg_result;
+
+/* NCCL unique id for world > 1: rank 0 calls this, the caller broadcasts the
+ * 128 bytes (e.g. over a torch.distributed process group) and every rank
+ * passes them to ccg_create.  Returns CCG_E_NCCL if NCCL is unavailable. */
+int ccg_get_unique_id(uint8_t id[128]);
+
+/* Create a handle for an n×n system in precision dt.
+ *   world, rank : number of ranks (one GPU each) and this rank; world = 1 for a
+ *                 single GPU.  With world > 1 rank r owns rows
+ *                 [r·n/world, (r+1)·n/world) (n % world == 0 required, else CCG_E_DIM).
+ *   nccl_id     : 128 bytes from ccg_get_unique_id (NULL iff world == 1).
+ *   device      : CUDA device ordinal this handle uses.
+ *   cuda_stream : cudaStream_t to order work on, or NULL for a private stream.
+ * Ownership: the library owns all workspace (Krylov vectors, reduction slots,
+ * NCCL communicator, CUDA graphs) and frees it in ccg_destroy. */
+int ccg_create(ccg_handle* h, ccg_dtype dt, int64_t n, int world, int rank,
+               const uint8_t* nccl_id, int device, void* cuda_stream);
+
+/* Dense operator (matvec + cmatvec of a row-major matrix; P:95 [§5]).
+ *   A_local : DEVICE pointer to this rank's rows, row-major, nloc × n with
+ *             leading dimension lda ≥ n (elements).  Borrowed: the caller keeps
+ *             it alive and unmodified until ccg_destroy or the next set_matvec.
+ *   row0, nloc : must equal the handle's row range (rank·n/world, n/world).
+ *   flags   : CCG_FLAG_SYMMETRIC or 0 (informational for dense).
+ * Supports CCG_OP_A, CCG_OP_AH, CCG_OP_AT. */
+int ccg_set_matvec_dense(ccg_handle h, const void* A_local, int64_t row0, int64_t nloc,
+                         int64_t lda, uint32_t flags);
+
+/* CSR operator, rows [row0, row0+nloc) of the global matrix.
+ *   rowptr : DEVICE int32[nloc+1], rowptr[0] == 0, nondecreasing, rowptr[nloc] == nnz_local.
+ *   colind : DEVICE int32[nnz_local], GLOBAL column indices in [0, n).  With world > 1
+ *            every column must lie within [row0 − h, row0 + nloc + h) for a halo
+ *            width h ≤ nloc (neighbour ranks only), else CCG_E_ARG.
+ *   vals   : DEVICE complex[nnz_local] in the handle's precision.
+ *   Borrowed like the dense matrix.  Supports CCG_OP_A; CCG_OP_AH / CCG_OP_AT
+ *   only with CCG_FLAG_SYMMETRIC and world == 1, else CCG_E_CAPABILITY. */
+int ccg_set_matvec_csr(ccg_handle h, const int32_t* rowptr, const int32_t* colind,
+                       const void* vals, int64_t row0, int64_t nloc, int64_t nnz_local,
+                       uint32_t flags);
+
+/* y_local = (op(A)·x)[row0 : row0+nloc] from x_local = x[row0 : row0+nloc].
+ * x_local / y_local may be HOST or DEVICE pointers (detected); nloc elements.
+ * Collective over ranks.  Blocks until y_local is written. */
+int ccg_apply(ccg_handle h, ccg_op op, const void* x_local, void* y_local);
+
+/* Solve A x = y with `method` (stopping rule ‖r_k‖ ≤ tol·‖r_0‖
+ * on the recurrence residual, r_0 = y − A·x0; true residual recomputed at exit).
+ *   x0_local : initial guess slice (NULL => 0), y_local: right-hand side slice,
+ *   x_local_out : solution slice.  HOST or DEVICE pointers (detected), nloc elements.
+ *   tol ≥ 0 (epsilon_err), maxit ≥ 1.  tol = 0 runs exactly maxit iterations
+ *   unless the recurrence residual is exactly 0 or a breakdown occurs.
+ *   res : caller-owned, filled on CCG_OK.
+ * Collective over ranks.  Blocks until the result is final. */
+int ccg_solve(ccg_handle h, ccg_method method, const void* x0_local, const void* y_local,
+              void* x_local_out, double tol, int32_t maxit, ccg_result* res);
+
+/* Recurrence residual history ‖r_k‖/‖r_0‖, k = 0..iterations, of the last solve
+ * (S:440-448).  Copies min(cap, available) doubles into rel_res (host), sets *len. */
+int ccg_get_history(ccg_handle h, double* rel_res, int32_t cap, int32_t* len);
+
+/* Device time of the matvec kernels of the last ccg_solve / ccg_apply when
+ * timing is enabled (CUDA events on the handle's stream around every matvec
+ * launch; disables graph capture while on).  ms_a/ms_ah: summed milliseconds of
+ * the A·x and Aᴴ·x kernels, n_a/n_ah: launch counts.  Any pointer may be NULL. */
+int ccg_set_timing(ccg_handle h, int enable);
+int ccg_get_timing(ccg_handle h, double* ms_a, int32_t* n_a, double* ms_ah, int32_t* n_ah);
+
+/* Number of libccg kernel launches issued by the last ccg_solve / ccg_apply
+ * (graph-launched kernels included; early-exit kernels after convergence
+ * are counted because they are launched). */
+int64_t ccg_last_launch_count(ccg_handle h);
+
+/* cudaStream_t of the handle (for callers that order their own work). */
+void* ccg_get_stream(ccg_handle h);
+
+/* Text of the last error on h (or of the last ccg_create failure if h is NULL).
+ * Valid until the next call on h. */
+const char* ccg_last_error(ccg_handle h);
+
+int ccg_destroy(ccg_handle h);
+
+/* Library version string "ccg-b200 <major>.<minor> sm_100a". */
+const char* ccg_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CCG_H_ */

@@ -1,0 +1,930 @@
+// ccg.cu — libccg.so: C-ABI (include/ccg.h), matvec engine dispatch, the
+// per-method iteration schedules, CUDA-graph iteration loop and the NCCL
+// row-sharded multi-GPU path.
+//
+// Paper mapping (PAPER.md = P:<line>):  matvec / cmatvec separated from the
+// iteration (P:17, P:95 [§5]) -> ccg_set_matvec_* + the kernels of
+// matvec.cuh; cgmodule's epsilon_err / maxit -> ccg_solve(tol, maxit);
+// ddprecision.f90 single/double switch -> ccg_dtype.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <string>
+#include <vector>
+
+#include "../../include/ccg.h"
+#include "common.cuh"
+#include "matvec.cuh"
+#include "methods.cuh"
+#include "nccl.h"
+
+using namespace ccg;
+
+// ===========================================================================
+// NCCL, loaded on demand (only world > 1 needs it)
+// ===========================================================================
+namespace {
+struct NcclApi {
+  bool loaded = false;
+  std::string err;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*ReduceScatter)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                                cudaStream_t) = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+NcclApi g_nccl;
+
+bool nccl_load() {
+  if (g_nccl.loaded) return true;
+  void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) {
+    const char* p = getenv("CCG_NCCL_LIB");
+    if (p) h = dlopen(p, RTLD_NOW | RTLD_GLOBAL);
+  }
+  if (!h) { g_nccl.err = "cannot dlopen libnccl.so.2 (set CCG_NCCL_LIB)"; return false; }
+#define LOADSYM(field, name)                                              \
+  g_nccl.field = reinterpret_cast<decltype(g_nccl.field)>(dlsym(h, name)); \
+  if (!g_nccl.field) { g_nccl.err = std::string("missing NCCL symbol ") + name; return false; }
+  LOADSYM(GetUniqueId, "ncclGetUniqueId");
+  LOADSYM(CommInitRank, "ncclCommInitRank");
+  LOADSYM(CommDestroy, "ncclCommDestroy");
+  LOADSYM(AllGather, "ncclAllGather");
+  LOADSYM(ReduceScatter, "ncclReduceScatter");
+  LOADSYM(Send, "ncclSend");
+  LOADSYM(Recv, "ncclRecv");
+  LOADSYM(GroupStart, "ncclGroupStart");
+  LOADSYM(GroupEnd, "ncclGroupEnd");
+  LOADSYM(GetErrorString, "ncclGetErrorString");
+#undef LOADSYM
+  g_nccl.loaded = true;
+  return true;
+}
+
+thread_local std::string g_create_err;
+
+struct Err {
+  int code;
+};
+}  // namespace
+
+// ===========================================================================
+// context
+// ===========================================================================
+enum { NLOCAL = 12, NFULL = 3 };
+enum { OPK_NONE = 0, OPK_DENSE = 1, OPK_CSR = 2 };
+
+struct ccg_ctx {
+  int dtype = 0;
+  int64_t n = 0, nloc = 0, row0 = 0;
+  int world = 1, rank = 0, device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  size_t esz = 8;  // bytes per complex
+  // operator
+  int opk = OPK_NONE;
+  const void* A = nullptr;
+  int64_t lda = 0;
+  uint32_t flags = 0;
+  const int32_t* rowptr = nullptr;
+  const int32_t* colind = nullptr;
+  const void* vals = nullptr;
+  int64_t nnz = 0, halo = 0;
+  bool vec_ok = true;
+  // workspace
+  State* st = nullptr;
+  State* st_host = nullptr;  // pinned
+  double2* part = nullptr;
+  size_t part_cap = 0;  // in double2
+  unsigned* ticket = nullptr;
+  double2* rank_sum = nullptr;
+  double2* all_sums = nullptr;
+  int* zero_gate = nullptr;
+  void* loc[NLOCAL] = {};
+  void* full[NFULL] = {};
+  void* hpart = nullptr;
+  size_t hpart_bytes = 0;
+  void* wfull = nullptr;
+  double* hist = nullptr;
+  int hist_cap = 0;
+  int hist_len = 0;
+  void* stage_in = nullptr;  // pinned staging (host pointer I/O)
+  size_t stage_bytes = 0;
+  // comm
+  ncclComm_t comm = nullptr;
+  // graphs per method
+  cudaGraphExec_t gexec[5] = {};
+  int64_t graph_launches_per_iter[5] = {};
+  // launch parameters
+  int sm_count = 148;
+  int gemv_grid = 0, ah_S = 1, ah_strips = 1, pass_grid = 0, stage2_grid = 0, spmv_grid = 0;
+  // timing
+  bool timing = false;
+  std::vector<cudaEvent_t> ev;
+  size_t ev_used = 0;
+  std::vector<int> ev_kind;
+  double ms_a = 0, ms_ah = 0;
+  int n_a = 0, n_ah = 0;
+  int64_t launches = 0;
+  bool capturing = false;
+  std::string err;
+};
+
+#define FAIL(c, code, msg)       \
+  do {                           \
+    (c)->err = (msg);            \
+    return (code);               \
+  } while (0)
+
+#define CK(c, call)                                                                        \
+  do {                                                                                     \
+    cudaError_t e_ = (call);                                                               \
+    if (e_ != cudaSuccess) {                                                               \
+      (c)->err = std::string(#call) + ": " + cudaGetErrorString(e_);                       \
+      return CCG_E_CUDA;                                                                   \
+    }                                                                                      \
+  } while (0)
+
+#define NK(c, call)                                                                        \
+  do {                                                                                     \
+    ncclResult_t r_ = (call);                                                              \
+    if (r_ != ncclSuccess) {                                                               \
+      (c)->err = std::string(#call) + ": " + g_nccl.GetErrorString(r_);                    \
+      return CCG_E_NCCL;                                                                   \
+    }                                                                                      \
+  } while (0)
+
+#define TRY(expr)            \
+  do {                       \
+    int rc_ = (expr);        \
+    if (rc_ != CCG_OK) return rc_; \
+  } while (0)
+
+static bool is_device_ptr(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+static Red make_red(ccg_ctx* c) {
+  Red r;
+  r.part = c->part;
+  r.ticket = c->ticket;
+  r.rank_sum = c->rank_sum;
+  r.fuse = c->world == 1 ? 1 : 0;
+  return r;
+}
+
+// ---------------------------------------------------------------------------
+// timing events around matvec launches (kind 0 = A, 1 = AH)
+// ---------------------------------------------------------------------------
+static void tev_begin(ccg_ctx* c, int kind) {
+  if (!c->timing) return;
+  if (c->ev_used + 2 > c->ev.size()) {
+    for (int i = 0; i < 256; ++i) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      c->ev.push_back(e);
+    }
+  }
+  cudaEventRecord(c->ev[c->ev_used], c->stream);
+  c->ev_kind.push_back(kind);
+}
+static void tev_end(ccg_ctx* c) {
+  if (!c->timing) return;
+  cudaEventRecord(c->ev[c->ev_used + 1], c->stream);
+  c->ev_used += 2;
+}
+static void tev_collect(ccg_ctx* c) {
+  if (!c->timing) return;
+  cudaStreamSynchronize(c->stream);
+  for (size_t p = 0; p < c->ev_kind.size(); ++p) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, c->ev[2 * p], c->ev[2 * p + 1]);
+    if (c->ev_kind[p] == 0) { c->ms_a += ms; c->n_a++; } else { c->ms_ah += ms; c->n_ah++; }
+  }
+  c->ev_used = 0;
+  c->ev_kind.clear();
+}
+
+// ===========================================================================
+// Engine<T>: launches
+// ===========================================================================
+template <typename T>
+struct Engine {
+  using C = typename CT<T>::c;
+  static constexpr int NT = 256;
+  static constexpr int R = 8;
+  static constexpr int UR = 8;
+  static constexpr int LPR = 8;
+
+  static C* L(ccg_ctx* c, int i) { return reinterpret_cast<C*>(c->loc[i]); }
+  static C* F(ccg_ctx* c, int i) { return reinterpret_cast<C*>(c->full[i]); }
+  static C* Fs(ccg_ctx* c, int i) { return reinterpret_cast<C*>(c->full[i]) + c->row0; }  // own slice
+
+  static ncclDataType_t ndt() { return sizeof(T) == 4 ? ncclFloat32 : ncclFloat64; }
+
+  // -------------------- collectives --------------------
+  static int allgather(ccg_ctx* c, int fi) {
+    if (c->world == 1) return CCG_OK;
+    C* buf = F(c, fi);
+    if (c->opk == OPK_CSR) return halo_exchange(c, buf);
+    NK(c, g_nccl.AllGather(buf + c->row0, buf, (size_t)c->nloc * 2, ndt(), c->comm, c->stream));
+    return CCG_OK;
+  }
+  static int halo_exchange(ccg_ctx* c, C* buf) {
+    const int64_t h = c->halo;
+    if (h == 0) return CCG_OK;
+    NK(c, g_nccl.GroupStart());
+    if (c->rank > 0) {
+      NK(c, g_nccl.Send(buf + c->row0, (size_t)h * 2, ndt(), c->rank - 1, c->comm, c->stream));
+      NK(c, g_nccl.Recv(buf + c->row0 - h, (size_t)h * 2, ndt(), c->rank - 1, c->comm, c->stream));
+    }
+    if (c->rank < c->world - 1) {
+      NK(c, g_nccl.Send(buf + c->row0 + c->nloc - h, (size_t)h * 2, ndt(), c->rank + 1, c->comm, c->stream));
+      NK(c, g_nccl.Recv(buf + c->row0 + c->nloc, (size_t)h * 2, ndt(), c->rank + 1, c->comm, c->stream));
+    }
+    NK(c, g_nccl.GroupEnd());
+    return CCG_OK;
+  }
+  // scalar phase for world > 1: allgather this rank's K sums, sum in rank order
+  template <class Fin>
+  static int post(ccg_ctx* c, const int* gate) {
+    constexpr int K = Fin::K;
+    if constexpr (K > 0) {
+      if (c->world > 1) {
+        NK(c, g_nccl.AllGather(c->rank_sum, c->all_sums, (size_t)K * 2, ncclFloat64, c->comm, c->stream));
+        scalar_kernel<K, Fin><<<1, 1, 0, c->stream>>>(c->all_sums, c->world, c->st, gate);
+        c->launches++;
+      }
+    }
+    return CCG_OK;
+  }
+
+  // -------------------- kernels --------------------
+  template <class Op>
+  static int pass(ccg_ctx* c, Op op, const int* gate) {
+    pass_kernel<NT, Op><<<c->pass_grid, NT, 0, c->stream>>>(op, c->nloc, make_red(c), c->st, gate);
+    c->launches++;
+    CK(c, cudaGetLastError());
+    return post<Op>(c, gate);
+  }
+
+  // y_local = A · xfull (full-length buffer, own slice + gathered/halo parts)
+  template <class Epi>
+  static int matvec_a(ccg_ctx* c, const C* xfull, Epi epi, const int* gate) {
+    tev_begin(c, 0);
+    if (c->opk == OPK_DENSE) {
+      const C* A = reinterpret_cast<const C*>(c->A);
+      if (c->vec_ok)
+        gemv_n_kernel<T, R, NT, true, Epi><<<c->gemv_grid, NT, 0, c->stream>>>(
+            A, c->lda, xfull, c->n, c->nloc, epi, make_red(c), c->st, gate);
+      else
+        gemv_n_kernel<T, R, NT, false, Epi><<<c->gemv_grid, NT, 0, c->stream>>>(
+            A, c->lda, xfull, c->n, c->nloc, epi, make_red(c), c->st, gate);
+    } else {
+      spmv_csr_kernel<T, LPR, NT, false, Epi><<<c->spmv_grid, NT, 0, c->stream>>>(
+          c->rowptr, c->colind, reinterpret_cast<const C*>(c->vals), xfull, c->nloc, epi, make_red(c),
+          c->st, gate);
+    }
+    c->launches++;
+    tev_end(c);
+    CK(c, cudaGetLastError());
+    return post<Epi>(c, gate);
+  }
+
+  // y_local = op(A) · x_local, op = Aᴴ (conj) or Aᵀ
+  template <class Epi>
+  static int matvec_h(ccg_ctx* c, const C* xloc, bool conj, Epi epi, const int* gate) {
+    if (c->opk == OPK_CSR) {
+      // complex-symmetric CSR, single GPU: Aᴴx = conj(A conj x), Aᵀx = A x
+      tev_begin(c, 1);
+      if (conj)
+        spmv_csr_kernel<T, LPR, NT, true, Epi><<<c->spmv_grid, NT, 0, c->stream>>>(
+            c->rowptr, c->colind, reinterpret_cast<const C*>(c->vals), xloc, c->nloc, epi, make_red(c),
+            c->st, gate);
+      else
+        spmv_csr_kernel<T, LPR, NT, false, Epi><<<c->spmv_grid, NT, 0, c->stream>>>(
+            c->rowptr, c->colind, reinterpret_cast<const C*>(c->vals), xloc, c->nloc, epi, make_red(c),
+            c->st, gate);
+      c->launches++;
+      tev_end(c);
+      CK(c, cudaGetLastError());
+      return post<Epi>(c, gate);
+    }
+    const C* A = reinterpret_cast<const C*>(c->A);
+    C* part = reinterpret_cast<C*>(c->hpart);
+    dim3 g1(c->ah_strips, c->ah_S);
+    tev_begin(c, 1);
+    if (c->vec_ok) {
+      if (conj)
+        gemv_h_stage1<T, true, NT, UR, true><<<g1, NT, 0, c->stream>>>(A, c->lda, xloc, c->nloc, c->n, part, gate);
+      else
+        gemv_h_stage1<T, false, NT, UR, true><<<g1, NT, 0, c->stream>>>(A, c->lda, xloc, c->nloc, c->n, part, gate);
+    } else {
+      if (conj)
+        gemv_h_stage1<T, true, NT, UR, false><<<g1, NT, 0, c->stream>>>(A, c->lda, xloc, c->nloc, c->n, part, gate);
+      else
+        gemv_h_stage1<T, false, NT, UR, false><<<g1, NT, 0, c->stream>>>(A, c->lda, xloc, c->nloc, c->n, part, gate);
+    }
+    c->launches++;
+    CK(c, cudaGetLastError());
+    if (c->world == 1) {
+      gemv_h_stage2<T, NT, Epi><<<c->stage2_grid, NT, 0, c->stream>>>(part, c->ah_S, c->n, 0, c->n, epi,
+                                                                       make_red(c), c->st, gate);
+      c->launches++;
+      tev_end(c);
+      CK(c, cudaGetLastError());
+      return CCG_OK;
+    }
+    // multi GPU: full-length partial of this rank -> reduce-scatter -> epilogue pass
+    Store<T> stv{reinterpret_cast<C*>(c->wfull)};
+    gemv_h_stage2<T, NT, Store<T>><<<c->stage2_grid, NT, 0, c->stream>>>(part, c->ah_S, c->n, 0, c->n, stv,
+                                                                         make_red(c), c->st, gate);
+    c->launches++;
+    tev_end(c);
+    CK(c, cudaGetLastError());
+    C* wl = L(c, NLOCAL - 1);
+    NK(c, g_nccl.ReduceScatter(c->wfull, wl, (size_t)c->nloc * 2, ndt(), ncclSum, c->comm, c->stream));
+    EpiPass<C, Epi> ep{epi, wl};
+    return pass(c, ep, gate);
+  }
+
+  // ==================== method schedules ====================
+  // local vector slots (NLOCAL-1 is reserved for the multi-GPU Aᴴ result)
+  enum { X = 0 };
+
+  static int init_residual(ccg_ctx* c, bool has_x0, C* d0, C* d1, C* d2, C* d3) {
+    const int* g = c->zero_gate;
+    C* y = L(c, 1);  // y is staged in loc[1] by solve()
+    InitR<T> ir{y, d0, d1, d2, d3};
+    if (has_x0) {
+      // x0 already copied into loc[X]; gather it into full[2]
+      Copy<T> cp{L(c, X), Fs(c, 2)};
+      TRY(pass(c, cp, g));
+      TRY(allgather(c, 2));
+      return matvec_a(c, F(c, 2), ir, g);
+    }
+    return pass(c, ir, g);
+  }
+
+  // ---- BiCGSTAB: loc: 0 x, 1 y, 2 r, 3 rt, 4 v, 5 t ; full: 0 p, 1 s
+  static int bicgstab_setup(ccg_ctx* c, bool x0) { return init_residual(c, x0, L(c, 2), L(c, 3), nullptr, nullptr); }
+  static int bicgstab_iter(ccg_ctx* c) {
+    const int* g = &c->st->done;
+    const int* g2 = &c->st->gate2;
+    TRY(pass(c, BsP<T>{L(c, 2), Fs(c, 0), L(c, 4)}, g));
+    TRY(allgather(c, 0));
+    TRY(matvec_a(c, F(c, 0), BsV<T>{L(c, 4), L(c, 3)}, g));
+    TRY(pass(c, BsS<T>{L(c, 2), L(c, 4), Fs(c, 1)}, g));
+    TRY(allgather(c, 1));
+    TRY(matvec_a(c, F(c, 1), BsT<T>{L(c, 5), Fs(c, 1)}, g2));
+    return pass(c, BsX<T>{L(c, X), L(c, 2), Fs(c, 0), Fs(c, 1), L(c, 5), L(c, 3)}, g);
+  }
+
+  // ---- CGNE: loc: 0 x, 1 y, 2 r ; full: 0 p
+  static int cgne_setup(ccg_ctx* c, bool x0) {
+    TRY(init_residual(c, x0, L(c, 2), nullptr, nullptr, nullptr));
+    return matvec_h(c, L(c, 2), true, CgP0<T>{Fs(c, 0)}, &c->st->done);
+  }
+  static int cgne_iter(ccg_ctx* c) {
+    const int* g = &c->st->done;
+    TRY(allgather(c, 0));
+    TRY(matvec_a(c, F(c, 0), CgQ<T>{L(c, 2), L(c, X), Fs(c, 0)}, g));
+    return matvec_h(c, L(c, 2), true, CgP<T>{Fs(c, 0)}, g);
+  }
+
+  // ---- QMR: loc: 0 x, 1 y, 2 r, 3 vt, 4 wt, 5 v, 6 w, 7 q, 8 pt, 9 d, 10 s ; full: 0 p
+  static int qmr_setup(ccg_ctx* c, bool x0) {
+    TRY(init_residual(c, x0, L(c, 2), L(c, 3), L(c, 4), nullptr));
+    return pass(c, QmV<T>{L(c, 3), L(c, 4), L(c, 5), L(c, 6)}, &c->st->done);
+  }
+  static int qmr_iter(ccg_ctx* c) {
+    const int* g = &c->st->done;
+    TRY(pass(c, QmP<T>{L(c, 5), L(c, 6), Fs(c, 0), L(c, 7)}, g));
+    TRY(allgather(c, 0));
+    TRY(matvec_a(c, F(c, 0), QmPt<T>{L(c, 8), L(c, 7)}, g));
+    TRY(matvec_h(c, L(c, 7), true, QmVW<T>{L(c, 3), L(c, 4), L(c, 8), L(c, 5), L(c, 6)}, g));
+    return pass(c, QmDV<T>{L(c, 9), L(c, 10), L(c, X), L(c, 2), Fs(c, 0), L(c, 8), L(c, 3), L(c, 4), L(c, 5),
+                           L(c, 6)},
+                g);
+  }
+
+  // ---- BiCOR: loc: 0 x, 1 y, 2 rs, 3 rh, 4 p, 5 ps, 6 q, 7 qs ; full: 0 r
+  static int bicor_setup(ccg_ctx* c, bool x0) { return init_residual(c, x0, Fs(c, 0), L(c, 2), nullptr, nullptr); }
+  static int bicor_iter(ccg_ctx* c) {
+    const int* g = &c->st->done;
+    TRY(allgather(c, 0));
+    TRY(matvec_a(c, F(c, 0), RhoEpi<T>{L(c, 3), L(c, 2)}, g));
+    TRY(pass(c, BcP<T>{Fs(c, 0), L(c, 2), L(c, 3), L(c, 4), L(c, 5), L(c, 6)}, g));
+    TRY(matvec_h(c, L(c, 5), true, BcQs<T>{L(c, 7), L(c, 6)}, g));
+    return pass(c, BcX<T>{L(c, X), Fs(c, 0), L(c, 2), L(c, 4), L(c, 6), L(c, 7)}, g);
+  }
+
+  // ---- CORS: loc: 0 x, 1 y, 2 r0s, 3 rh, 4 e, 5 eh, 6 h, 7 hh, 8 q ; full: 0 r, 1 qh
+  static int cors_setup(ccg_ctx* c, bool x0) { return init_residual(c, x0, Fs(c, 0), L(c, 2), nullptr, nullptr); }
+  static int cors_iter(ccg_ctx* c) {
+    const int* g = &c->st->done;
+    TRY(allgather(c, 0));
+    TRY(matvec_a(c, F(c, 0), RhoEpi<T>{L(c, 3), L(c, 2)}, g));
+    TRY(pass(c, CoP<T>{Fs(c, 0), L(c, 3), L(c, 6), L(c, 7), L(c, 4), L(c, 5), Fs(c, 1)}, g));
+    TRY(allgather(c, 1));
+    TRY(matvec_a(c, F(c, 1), CoQ<T>{L(c, 8), L(c, 2)}, g));
+    return pass(c, CoH<T>{L(c, 4), L(c, 5), Fs(c, 1), L(c, 8), L(c, 6), L(c, 7), L(c, X), Fs(c, 0)}, g);
+  }
+
+  static int setup(ccg_ctx* c, int m, bool x0) {
+    switch (m) {
+      case M_BICGSTAB: return bicgstab_setup(c, x0);
+      case M_CGNE: return cgne_setup(c, x0);
+      case M_QMR: return qmr_setup(c, x0);
+      case M_BICOR: return bicor_setup(c, x0);
+      default: return cors_setup(c, x0);
+    }
+  }
+  static int iter(ccg_ctx* c, int m) {
+    switch (m) {
+      case M_BICGSTAB: return bicgstab_iter(c);
+      case M_CGNE: return cgne_iter(c);
+      case M_QMR: return qmr_iter(c);
+      case M_BICOR: return bicor_iter(c);
+      default: return cors_iter(c);
+    }
+  }
+
+  // true residual ‖y − A x‖²
+  static int true_residual(ccg_ctx* c) {
+    const int* g = c->zero_gate;
+    TRY(pass(c, Copy<T>{L(c, X), Fs(c, 2)}, g));
+    TRY(allgather(c, 2));
+    return matvec_a(c, F(c, 2), TrueRes<T>{L(c, 1)}, g);
+  }
+
+  // ccg_apply
+  static int apply(ccg_ctx* c, int op, const C* xin, C* yout) {
+    const int* g = c->zero_gate;
+    if (op == CCG_OP_A || (op == CCG_OP_AT && c->opk == OPK_CSR)) {
+      CK(c, cudaMemcpyAsync(Fs(c, 2), xin, c->nloc * sizeof(C), cudaMemcpyDeviceToDevice, c->stream));
+      TRY(allgather(c, 2));
+      return matvec_a(c, F(c, 2), Store<T>{yout}, g);
+    }
+    CK(c, cudaMemcpyAsync(L(c, 2), xin, c->nloc * sizeof(C), cudaMemcpyDeviceToDevice, c->stream));
+    return matvec_h(c, L(c, 2), op == CCG_OP_AH, Store<T>{yout}, g);
+  }
+};
+
+// ===========================================================================
+// launch-parameter selection
+// ===========================================================================
+template <typename T>
+static int choose_launch(ccg_ctx* c) {
+  using E = Engine<T>;
+  using C = typename CT<T>::c;
+  const int NT = E::NT;
+  int occ = 0;
+  if (c->vec_ok)
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gemv_n_kernel<T, E::R, E::NT, true, Store<T>>, NT, 0);
+  else
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gemv_n_kernel<T, E::R, E::NT, false, Store<T>>, NT, 0);
+  if (occ < 1) occ = 1;
+  const int64_t groups = (c->nloc + E::R - 1) / E::R;
+  c->gemv_grid = (int)std::max<int64_t>(1, std::min<int64_t>(groups, (int64_t)c->sm_count * occ));
+  // Aᴴ stage 1: strips of NT*V columns, S row splits, ~ whole waves
+  const int V = c->vec_ok ? CT<T>::V : 1;
+  const int64_t nv = c->n / V;
+  c->ah_strips = (int)std::max<int64_t>(1, (nv + NT - 1) / NT);
+  int occ1 = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1, gemv_h_stage1<T, true, E::NT, E::UR, true>, NT, 0);
+  if (occ1 < 1) occ1 = 1;
+  const int64_t slots = (int64_t)c->sm_count * occ1;
+  int64_t S = slots / c->ah_strips;
+  S = std::max<int64_t>(1, std::min<int64_t>(S, 128));
+  S = std::min<int64_t>(S, std::max<int64_t>(1, c->nloc / 16));
+  c->ah_S = (int)S;
+  c->stage2_grid = (int)std::max<int64_t>(1, std::min<int64_t>((c->n + NT - 1) / NT, (int64_t)c->sm_count * 4));
+  c->pass_grid = (int)std::max<int64_t>(1, std::min<int64_t>((c->nloc + NT - 1) / NT, (int64_t)c->sm_count * 8));
+  c->spmv_grid = (int)std::max<int64_t>(
+      1, std::min<int64_t>((c->nloc + NT / E::LPR - 1) / (NT / E::LPR), (int64_t)c->sm_count * 8));
+  // workspace sized for the chosen grids
+  size_t need_hpart = (size_t)c->ah_S * (size_t)c->n * sizeof(C);
+  if (c->opk == OPK_DENSE && need_hpart > c->hpart_bytes) {
+    if (c->hpart) cudaFree(c->hpart);
+    c->hpart = nullptr;
+    CK(c, cudaMalloc(&c->hpart, need_hpart));
+    c->hpart_bytes = need_hpart;
+  }
+  int64_t maxgrid = std::max<int64_t>({(int64_t)c->gemv_grid, (int64_t)c->ah_strips * c->ah_S,
+                                       (int64_t)c->stage2_grid, (int64_t)c->pass_grid, (int64_t)c->spmv_grid});
+  size_t need_part = (size_t)maxgrid * 4;
+  if (need_part > c->part_cap) {
+    if (c->part) cudaFree(c->part);
+    c->part = nullptr;
+    CK(c, cudaMalloc(&c->part, need_part * sizeof(double2)));
+    c->part_cap = need_part;
+  }
+  return CCG_OK;
+}
+
+static void invalidate_graphs(ccg_ctx* c) {
+  for (int m = 0; m < 5; ++m) {
+    if (c->gexec[m]) cudaGraphExecDestroy(c->gexec[m]);
+    c->gexec[m] = nullptr;
+  }
+}
+
+// ===========================================================================
+// C-ABI
+// ===========================================================================
+template <typename T>
+static int run_iterations(ccg_ctx* c, int m, int maxit) {
+  using E = Engine<T>;
+  int done = 0;
+  auto read_done = [&]() -> int {
+    CK(c, cudaMemcpyAsync(&c->st_host->done, &c->st->done, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    CK(c, cudaStreamSynchronize(c->stream));
+    done = c->st_host->done;
+    return CCG_OK;
+  };
+  TRY(read_done());
+  if (done) return CCG_OK;
+  if (c->timing) {
+    for (int k = 0; k < maxit && !done; ++k) {
+      TRY(E::iter(c, m));
+      TRY(read_done());
+      tev_collect(c);
+    }
+    return CCG_OK;
+  }
+  if (!c->gexec[m]) {
+    cudaGraph_t graph;
+    int64_t l0 = c->launches;
+    CK(c, cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+    int rc = E::iter(c, m);
+    cudaError_t e2 = cudaStreamEndCapture(c->stream, &graph);
+    if (rc) return rc;
+    if (e2 != cudaSuccess) FAIL(c, CCG_E_CUDA, std::string("graph capture: ") + cudaGetErrorString(e2));
+    c->graph_launches_per_iter[m] = c->launches - l0;
+    c->launches = l0;
+    CK(c, cudaGraphInstantiate(&c->gexec[m], graph, 0));
+    cudaGraphDestroy(graph);
+  }
+  // adaptive chunk: sync every `chunk` iterations (kernels after convergence
+  // are gated and return immediately)
+  int k = 0, chunk = 1;
+  while (k < maxit && !done) {
+    const int todo = std::min(chunk, maxit - k);
+    auto t0 = std::chrono::steady_clock::now();
+    for (int i = 0; i < todo; ++i) {
+      CK(c, cudaGraphLaunch(c->gexec[m], c->stream));
+      c->launches += c->graph_launches_per_iter[m];
+    }
+    k += todo;
+    TRY(read_done());
+    const double us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
+    const double per = us / todo;
+    chunk = per > 0 ? (int)std::max(1.0, std::min(32.0, 200.0 / per)) : 32;
+  }
+  return CCG_OK;
+}
+
+extern "C" {
+
+const char* ccg_version(void) { return "ccg-b200 0.1 sm_100a"; }
+
+int ccg_get_unique_id(uint8_t id[128]) {
+  if (!id) { g_create_err = "id is NULL"; return CCG_E_ARG; }
+  if (!nccl_load()) { g_create_err = g_nccl.err; return CCG_E_NCCL; }
+  ncclUniqueId u;
+  ncclResult_t r = g_nccl.GetUniqueId(&u);
+  if (r != ncclSuccess) { g_create_err = g_nccl.GetErrorString(r); return CCG_E_NCCL; }
+  memcpy(id, u.internal, 128);
+  return CCG_OK;
+}
+
+int ccg_create(ccg_handle* h, ccg_dtype dt, int64_t n, int world, int rank, const uint8_t* nccl_id, int device,
+               void* cuda_stream) {
+  if (!h) { g_create_err = "h is NULL"; return CCG_E_ARG; }
+  *h = nullptr;
+  if (dt != CCG_C64 && dt != CCG_C128) { g_create_err = "bad dtype"; return CCG_E_ARG; }
+  if (n < 1 || world < 1 || rank < 0 || rank >= world) { g_create_err = "bad n/world/rank"; return CCG_E_ARG; }
+  if (n % world != 0) { g_create_err = "n must be divisible by world"; return CCG_E_DIM; }
+  if (world > 1 && !nccl_id) { g_create_err = "nccl_id required for world > 1"; return CCG_E_ARG; }
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess || ndev == 0) {
+    g_create_err = std::string("no CUDA device: ") + cudaGetErrorString(e);
+    cudaGetLastError();
+    return CCG_E_CUDA;
+  }
+  if (device < 0 || device >= ndev) { g_create_err = "bad device ordinal"; return CCG_E_ARG; }
+  ccg_ctx* c = new ccg_ctx();
+  c->dtype = dt;
+  c->esz = dt == CCG_C64 ? 8 : 16;
+  c->n = n;
+  c->world = world;
+  c->rank = rank;
+  c->nloc = n / world;
+  c->row0 = (int64_t)rank * c->nloc;
+  c->device = device;
+  auto bail = [&](int code) {
+    g_create_err = c->err;
+    ccg_destroy(c);
+    return code;
+  };
+#define CKC(call)                                                                   \
+  do {                                                                              \
+    cudaError_t e_ = (call);                                                        \
+    if (e_ != cudaSuccess) {                                                        \
+      c->err = std::string(#call) + ": " + cudaGetErrorString(e_);                  \
+      return bail(e_ == cudaErrorMemoryAllocation ? CCG_E_OOM : CCG_E_CUDA);        \
+    }                                                                               \
+  } while (0)
+  CKC(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  CKC(cudaGetDeviceProperties(&prop, device));
+  c->sm_count = prop.multiProcessorCount;
+  if (cuda_stream) {
+    c->stream = reinterpret_cast<cudaStream_t>(cuda_stream);
+  } else {
+    CKC(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    c->own_stream = true;
+  }
+  CKC(cudaMalloc(&c->st, sizeof(State)));
+  CKC(cudaMallocHost(&c->st_host, sizeof(State)));
+  CKC(cudaMalloc(&c->ticket, sizeof(unsigned)));
+  CKC(cudaMemset(c->ticket, 0, sizeof(unsigned)));
+  CKC(cudaMalloc(&c->rank_sum, 8 * sizeof(double2)));
+  CKC(cudaMalloc(&c->all_sums, (size_t)8 * world * sizeof(double2)));
+  CKC(cudaMalloc(&c->zero_gate, sizeof(int)));
+  CKC(cudaMemset(c->zero_gate, 0, sizeof(int)));
+  for (int i = 0; i < NLOCAL; ++i) {
+    CKC(cudaMalloc(&c->loc[i], (size_t)c->nloc * c->esz));
+    CKC(cudaMemset(c->loc[i], 0, (size_t)c->nloc * c->esz));
+  }
+  for (int i = 0; i < NFULL; ++i) {
+    CKC(cudaMalloc(&c->full[i], (size_t)n * c->esz));
+    CKC(cudaMemset(c->full[i], 0, (size_t)n * c->esz));
+  }
+  if (world > 1) {
+    CKC(cudaMalloc(&c->wfull, (size_t)n * c->esz));
+    if (!nccl_load()) { c->err = g_nccl.err; return bail(CCG_E_NCCL); }
+    ncclUniqueId u;
+    memcpy(u.internal, nccl_id, 128);
+    ncclResult_t r = g_nccl.CommInitRank(&c->comm, world, u, rank);
+    if (r != ncclSuccess) { c->err = std::string("ncclCommInitRank: ") + g_nccl.GetErrorString(r); return bail(CCG_E_NCCL); }
+  }
+#undef CKC
+  *h = c;
+  return CCG_OK;
+}
+
+int ccg_set_matvec_dense(ccg_handle c, const void* A_local, int64_t row0, int64_t nloc, int64_t lda, uint32_t flags) {
+  if (!c) return CCG_E_ARG;
+  if (!A_local) FAIL(c, CCG_E_ARG, "A_local is NULL");
+  if (row0 != c->row0 || nloc != c->nloc) FAIL(c, CCG_E_DIM, "row0/nloc differ from the handle's row range");
+  if (lda < c->n) FAIL(c, CCG_E_DIM, "lda < n");
+  if (!is_device_ptr(A_local)) FAIL(c, CCG_E_ARG, "A_local must be a device pointer");
+  if (((uintptr_t)A_local) % c->esz) FAIL(c, CCG_E_ARG, "A_local misaligned");
+  CK(c, cudaSetDevice(c->device));
+  c->opk = OPK_DENSE;
+  c->A = A_local;
+  c->lda = lda;
+  c->flags = flags;
+  c->vec_ok = (c->esz == 16) || (((uintptr_t)A_local % 16) == 0 && (lda % 2) == 0);
+  invalidate_graphs(c);
+  return c->dtype == CCG_C64 ? choose_launch<float>(c) : choose_launch<double>(c);
+}
+
+int ccg_set_matvec_csr(ccg_handle c, const int32_t* rowptr, const int32_t* colind, const void* vals, int64_t row0,
+                       int64_t nloc, int64_t nnz_local, uint32_t flags) {
+  if (!c) return CCG_E_ARG;
+  if (!rowptr || !colind || !vals) FAIL(c, CCG_E_ARG, "NULL CSR pointer");
+  if (row0 != c->row0 || nloc != c->nloc) FAIL(c, CCG_E_DIM, "row0/nloc differ from the handle's row range");
+  if (nnz_local < 0 || nnz_local > INT32_MAX) FAIL(c, CCG_E_DIM, "nnz out of range");
+  if (!is_device_ptr(rowptr) || !is_device_ptr(colind) || !is_device_ptr(vals))
+    FAIL(c, CCG_E_ARG, "CSR arrays must be device pointers");
+  CK(c, cudaSetDevice(c->device));
+  // validate structure and compute the halo width on the host (one-time copy)
+  std::vector<int32_t> rp(nloc + 1), ci(nnz_local);
+  CK(c, cudaMemcpy(rp.data(), rowptr, (nloc + 1) * sizeof(int32_t), cudaMemcpyDeviceToHost));
+  if (nnz_local) CK(c, cudaMemcpy(ci.data(), colind, nnz_local * sizeof(int32_t), cudaMemcpyDeviceToHost));
+  if (rp[0] != 0 || rp[nloc] != nnz_local) FAIL(c, CCG_E_DIM, "rowptr[0] != 0 or rowptr[nloc] != nnz");
+  int64_t halo = 0;
+  for (int64_t i = 0; i < nloc; ++i) {
+    if (rp[i + 1] < rp[i]) FAIL(c, CCG_E_ARG, "rowptr not nondecreasing");
+    for (int32_t k = rp[i]; k < rp[i + 1]; ++k) {
+      const int64_t j = ci[k];
+      if (j < 0 || j >= c->n) FAIL(c, CCG_E_ARG, "column index out of range");
+      if (j < row0) halo = std::max<int64_t>(halo, row0 - j);
+      if (j >= row0 + nloc) halo = std::max<int64_t>(halo, j - (row0 + nloc) + 1);
+    }
+  }
+  if (c->world > 1 && halo > nloc) FAIL(c, CCG_E_ARG, "CSR columns reach beyond the neighbour ranks (halo > nloc)");
+  if (c->world > 1) {
+    // all ranks use the same (maximum) halo width so that sends match receives
+    int64_t* dh = nullptr;
+    CK(c, cudaMalloc(&dh, sizeof(int64_t) * c->world));
+    CK(c, cudaMemcpy(dh + c->rank, &halo, sizeof(int64_t), cudaMemcpyHostToDevice));
+    ncclResult_t r = g_nccl.AllGather(dh + c->rank, dh, 1, ncclInt64, c->comm, c->stream);
+    if (r != ncclSuccess) { cudaFree(dh); FAIL(c, CCG_E_NCCL, g_nccl.GetErrorString(r)); }
+    std::vector<int64_t> hs(c->world);
+    CK(c, cudaStreamSynchronize(c->stream));
+    CK(c, cudaMemcpy(hs.data(), dh, sizeof(int64_t) * c->world, cudaMemcpyDeviceToHost));
+    cudaFree(dh);
+    for (auto v : hs) halo = std::max(halo, v);
+    if (halo > nloc) FAIL(c, CCG_E_ARG, "halo > nloc on some rank");
+  }
+  c->opk = OPK_CSR;
+  c->rowptr = rowptr;
+  c->colind = colind;
+  c->vals = vals;
+  c->nnz = nnz_local;
+  c->halo = halo;
+  c->flags = flags;
+  c->vec_ok = true;
+  invalidate_graphs(c);
+  return c->dtype == CCG_C64 ? choose_launch<float>(c) : choose_launch<double>(c);
+}
+
+static int stage_in(ccg_ctx* c, void* dst, const void* src, size_t bytes) {
+  if (is_device_ptr(src)) {
+    CK(c, cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, c->stream));
+  } else {
+    CK(c, cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, c->stream));
+  }
+  return CCG_OK;
+}
+static int stage_out(ccg_ctx* c, void* dst, const void* src, size_t bytes) {
+  if (is_device_ptr(dst)) {
+    CK(c, cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, c->stream));
+  } else {
+    CK(c, cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, c->stream));
+  }
+  return CCG_OK;
+}
+
+static bool needs_ah(int m) { return m == CCG_CGNE || m == CCG_QMR || m == CCG_BICOR; }
+
+int ccg_apply(ccg_handle c, ccg_op op, const void* x_local, void* y_local) {
+  if (!c) return CCG_E_ARG;
+  if (!x_local || !y_local) FAIL(c, CCG_E_ARG, "NULL vector");
+  if (op != CCG_OP_A && op != CCG_OP_AH && op != CCG_OP_AT) FAIL(c, CCG_E_ARG, "bad op");
+  if (c->opk == OPK_NONE) FAIL(c, CCG_E_STATE, "no operator set (call ccg_set_matvec_*)");
+  if (c->opk == OPK_CSR && op != CCG_OP_A && (!(c->flags & CCG_FLAG_SYMMETRIC) || c->world > 1))
+    FAIL(c, CCG_E_CAPABILITY, "CSR Aᴴ/Aᵀ needs CCG_FLAG_SYMMETRIC and world == 1");
+  CK(c, cudaSetDevice(c->device));
+  c->launches = 0;
+  c->ms_a = c->ms_ah = 0;
+  c->n_a = c->n_ah = 0;
+  const size_t bytes = (size_t)c->nloc * c->esz;
+  void* xin = c->loc[3];
+  void* yout = c->loc[4];
+  TRY(stage_in(c, xin, x_local, bytes));
+  int rc = c->dtype == CCG_C64
+               ? Engine<float>::apply(c, op, (const float2*)xin, (float2*)yout)
+               : Engine<double>::apply(c, op, (const double2*)xin, (double2*)yout);
+  if (rc) return rc;
+  TRY(stage_out(c, y_local, yout, bytes));
+  CK(c, cudaStreamSynchronize(c->stream));
+  tev_collect(c);
+  return CCG_OK;
+}
+
+int ccg_solve(ccg_handle c, ccg_method method, const void* x0_local, const void* y_local, void* x_local_out, double tol,
+              int32_t maxit, ccg_result* res) {
+  auto t_start = std::chrono::steady_clock::now();
+  if (!c) return CCG_E_ARG;
+  if (!y_local || !x_local_out || !res) FAIL(c, CCG_E_ARG, "NULL y/x_out/res");
+  if ((int)method < 0 || (int)method > 4) FAIL(c, CCG_E_ARG, "bad method");
+  if (!(tol >= 0.0) || maxit < 1) FAIL(c, CCG_E_ARG, "tol must be >= 0 and maxit >= 1");
+  if (c->opk == OPK_NONE) FAIL(c, CCG_E_STATE, "no operator set (call ccg_set_matvec_*)");
+  if (needs_ah(method) && c->opk == OPK_CSR && (!(c->flags & CCG_FLAG_SYMMETRIC) || c->world > 1))
+    FAIL(c, CCG_E_CAPABILITY, "method needs Aᴴ; CSR provides it only with CCG_FLAG_SYMMETRIC and world == 1");
+  CK(c, cudaSetDevice(c->device));
+  c->launches = 0;
+  c->ms_a = c->ms_ah = 0;
+  c->n_a = c->n_ah = 0;
+  const size_t bytes = (size_t)c->nloc * c->esz;
+  // history buffer
+  if (maxit + 1 > c->hist_cap) {
+    if (c->hist) cudaFree(c->hist);
+    c->hist = nullptr;
+    CK(c, cudaMalloc(&c->hist, sizeof(double) * (maxit + 1)));
+    c->hist_cap = maxit + 1;
+  }
+  // state
+  State s0;
+  memset(&s0, 0, sizeof(s0));
+  s0.maxit = maxit;
+  s0.method = method;
+  s0.tol2 = tol * tol;
+  s0.hist = c->hist;
+  s0.hist_cap = c->hist_cap;
+  *c->st_host = s0;
+  CK(c, cudaMemcpyAsync(c->st, c->st_host, sizeof(State), cudaMemcpyHostToDevice, c->stream));
+  // inputs: x -> loc[0], y -> loc[1]
+  TRY(stage_in(c, c->loc[1], y_local, bytes));
+  if (x0_local) {
+    TRY(stage_in(c, c->loc[0], x0_local, bytes));
+  } else {
+    CK(c, cudaMemsetAsync(c->loc[0], 0, bytes, c->stream));
+  }
+  const bool has_x0 = x0_local != nullptr;
+  int rc = c->dtype == CCG_C64 ? Engine<float>::setup(c, method, has_x0) : Engine<double>::setup(c, method, has_x0);
+  if (rc) return rc;
+  rc = c->dtype == CCG_C64 ? run_iterations<float>(c, method, maxit) : run_iterations<double>(c, method, maxit);
+  if (rc) return rc;
+  rc = c->dtype == CCG_C64 ? Engine<float>::true_residual(c) : Engine<double>::true_residual(c);
+  if (rc) return rc;
+  CK(c, cudaMemcpyAsync(c->st_host, c->st, sizeof(State), cudaMemcpyDeviceToHost, c->stream));
+  TRY(stage_out(c, x_local_out, c->loc[0], bytes));
+  CK(c, cudaStreamSynchronize(c->stream));
+  tev_collect(c);
+  const State& s = *c->st_host;
+  memset(res, 0, sizeof(*res));
+  res->status = s.done ? s.status : CCG_MAXIT;
+  res->iterations = s.done ? s.iterations : maxit;
+  res->matvecs_a = s.matvecs_a + (has_x0 ? 1 : 0);
+  res->matvecs_ah = s.matvecs_ah;
+  res->breakdown_code = s.breakdown;
+  res->half_step = s.half;
+  const double r0 = sqrt(s.r0sq);
+  res->rec_rel_res = r0 > 0 ? sqrt(s.rr) / r0 : 0.0;
+  res->true_rel_res = r0 > 0 ? sqrt(s.true_rr) / r0 : 0.0;
+  if (!std::isfinite(s.true_rr)) res->status = CCG_NONFINITE;
+  if (res->status == CCG_CONVERGED && res->true_rel_res > 10.0 * tol) res->status = CCG_FALSE_CONVERGENCE;
+  c->hist_len = std::min(c->hist_cap, res->iterations + 1);
+  res->wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count();
+  return CCG_OK;
+}
+
+int ccg_get_history(ccg_handle c, double* rel_res, int32_t cap, int32_t* len) {
+  if (!c || !len) return CCG_E_ARG;
+  if (!c->hist || c->hist_len == 0) { *len = 0; return CCG_OK; }
+  int32_t m = std::min<int32_t>(cap, c->hist_len);
+  if (m > 0 && rel_res) CK(c, cudaMemcpy(rel_res, c->hist, sizeof(double) * m, cudaMemcpyDeviceToHost));
+  *len = m;
+  return CCG_OK;
+}
+
+int ccg_set_timing(ccg_handle c, int enable) {
+  if (!c) return CCG_E_ARG;
+  c->timing = enable != 0;
+  return CCG_OK;
+}
+
+int ccg_get_timing(ccg_handle c, double* ms_a, int32_t* n_a, double* ms_ah, int32_t* n_ah) {
+  if (!c) return CCG_E_ARG;
+  if (ms_a) *ms_a = c->ms_a;
+  if (n_a) *n_a = c->n_a;
+  if (ms_ah) *ms_ah = c->ms_ah;
+  if (n_ah) *n_ah = c->n_ah;
+  return CCG_OK;
+}
+
+int64_t ccg_last_launch_count(ccg_handle c) { return c ? c->launches : -1; }
+
+void* ccg_get_stream(ccg_handle c) { return c ? (void*)c->stream : nullptr; }
+
+const char* ccg_last_error(ccg_handle c) { return c ? c->err.c_str() : g_create_err.c_str(); }
+
+int ccg_destroy(ccg_handle c) {
+  if (!c) return CCG_OK;
+  cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  invalidate_graphs(c);
+  for (auto e : c->ev) cudaEventDestroy(e);
+  if (c->comm && g_nccl.loaded) g_nccl.CommDestroy(c->comm);
+  for (int i = 0; i < NLOCAL; ++i) if (c->loc[i]) cudaFree(c->loc[i]);
+  for (int i = 0; i < NFULL; ++i) if (c->full[i]) cudaFree(c->full[i]);
+  if (c->wfull) cudaFree(c->wfull);
+  if (c->hpart) cudaFree(c->hpart);
+  if (c->part) cudaFree(c->part);
+  if (c->hist) cudaFree(c->hist);
+  if (c->st) cudaFree(c->st);
+  if (c->st_host) cudaFreeHost(c->st_host);
+  if (c->ticket) cudaFree(c->ticket);
+  if (c->rank_sum) cudaFree(c->rank_sum);
+  if (c->all_sums) cudaFree(c->all_sums);
+  if (c->zero_gate) cudaFree(c->zero_gate);
+  if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+  return CCG_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,291 @@
+// matvec.cuh — the matvec engine: dense A·x, dense Aᴴ·x / Aᵀ·x, CSR A·x.
+//
+// PAPER.md P:95 [§5]: "All the communication to matvec, cmatvec is set in
+// module arraymodule" — matvec = A·x, cmatvec = Aᴴ·x.  All three
+// kernels are HBM-bandwidth bound: A is streamed once with
+// 128-bit loads and evict-first caching; the vector is kept in L2/L1.
+//
+// Epilogue functors (method phases, methods.cuh) receive each finished
+// output element (row i, value) and accumulate up to K fp64 partial sums,
+// which finish_reduction() turns into the phase's recurrence scalars.
+#pragma once
+#include <type_traits>
+#include "common.cuh"
+
+namespace ccg {
+
+// streaming 16-byte load (ld.global.cs: evict-first, A is touched once)
+__device__ __forceinline__ float4 ld_stream(const float4* p) { return __ldcs(p); }
+__device__ __forceinline__ double2 ld_stream(const double2* p) { return __ldcs(p); }
+__device__ __forceinline__ float2 ld_stream(const float2* p) { return __ldcs(p); }
+
+// unpack a 16-byte vector into V complex values
+__device__ __forceinline__ void unpack(const float4& v, float2 (&c)[2]) {
+  c[0] = make_float2(v.x, v.y); c[1] = make_float2(v.z, v.w);
+}
+__device__ __forceinline__ void unpack(const double2& v, double2 (&c)[1]) { c[0] = v; }
+__device__ __forceinline__ void unpack(const float2& v, float2 (&c)[1]) { c[0] = v; }
+
+// ---------------------------------------------------------------------------
+// K1 gemv_n: y_i = Σ_j A_ij x_j for local rows [0, nrows), row-major A.
+// Persistent, balanced: CTA b owns rows [b·nrows/G, (b+1)·nrows/G) and walks
+// them in groups of R rows.  Each thread keeps its x chunk in registers and
+// reuses it across the R rows (x is read from L2 once per R rows).
+// VEC: 16-byte loads (c64: 2 elements) — needs lda, n even and 16-B aligned
+// pointers for c64; c128 is always 16 B per element.
+// ---------------------------------------------------------------------------
+template <typename T, int R, int NT, bool VEC, class Epi>
+__global__ void __launch_bounds__(NT)
+gemv_n_kernel(const typename CT<T>::c* __restrict__ A, int64_t lda,
+              const typename CT<T>::c* __restrict__ x, int64_t n, int64_t nrows,
+              Epi epi, Red red, State* st, const int* gate) {
+  using C = typename CT<T>::c;
+  constexpr int V = VEC ? CT<T>::V : 1;
+  using LV = typename std::conditional<VEC, typename CT<T>::v, C>::type;
+  constexpr int KK = Epi::K > 0 ? Epi::K : 1;
+  if (*gate) return;
+  epi.load(st);
+  __shared__ C sm[NT / 32][R];
+  double2 dacc[KK];
+#pragma unroll
+  for (int k = 0; k < KK; ++k) dacc[k] = make_double2(0.0, 0.0);
+
+  const int64_t rb = nrows * (int64_t)blockIdx.x / gridDim.x;
+  const int64_t re = nrows * ((int64_t)blockIdx.x + 1) / gridDim.x;
+  const int64_t nv = n / V;  // vector steps
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+
+  for (int64_t g = rb; g < re; g += R) {
+    const int nr = (int)min((int64_t)R, re - g);
+    const LV* Ar[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) Ar[r] = reinterpret_cast<const LV*>(A + (g + min(r, nr - 1)) * lda);
+    const LV* xv = reinterpret_cast<const LV*>(x);
+    C acc[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) acc[r] = czero<C>();
+#pragma unroll 2
+    for (int64_t j = threadIdx.x; j < nv; j += NT) {
+      C xc[V];
+      unpack(__ldg(xv + j), xc);
+      LV a[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) a[r] = ld_stream(Ar[r] + j);
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        C ac[V];
+        unpack(a[r], ac);
+#pragma unroll
+        for (int v = 0; v < V; ++v) cfma(acc[r], ac[v], xc[v]);
+      }
+    }
+    // scalar tail (odd n with VEC)
+    for (int64_t j = nv * V + threadIdx.x; j < n; j += NT) {
+      C xj = x[j];
+#pragma unroll
+      for (int r = 0; r < R; ++r) cfma(acc[r], A[(g + min(r, nr - 1)) * lda + j], xj);
+    }
+    // block reduction of the R row sums (fixed order => deterministic)
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        acc[r].x += __shfl_xor_sync(0xffffffffu, acc[r].x, o);
+        acc[r].y += __shfl_xor_sync(0xffffffffu, acc[r].y, o);
+      }
+    }
+    if (lane == 0) {
+#pragma unroll
+      for (int r = 0; r < R; ++r) sm[warp][r] = acc[r];
+    }
+    __syncthreads();
+    if (threadIdx.x < nr) {
+      const int r = threadIdx.x;
+      C s = sm[0][r];
+#pragma unroll
+      for (int w = 1; w < NT / 32; ++w) s = cadd(s, sm[w][r]);
+      epi(g + r, s, dacc);
+    }
+    __syncthreads();
+  }
+  if constexpr (Epi::K > 0) finish_reduction<KK, NT, Epi>(dacc, red, st);
+}
+
+// ---------------------------------------------------------------------------
+// K2 stage 1: part[s][j] = Σ_{i in split s} op(A_ij) x_i, op = conj (Aᴴ) or
+// identity (Aᵀ), reading row-major A once (no Aᴴ copy).  Grid (strips, S):
+// CTA (c, s) owns columns [c·NT·V, (c+1)·NT·V) and rows of split s.
+// x (local rows) is staged through shared memory in chunks.
+// ---------------------------------------------------------------------------
+template <typename T, bool CONJ, int NT, int UR, bool VEC>
+__global__ void __launch_bounds__(NT)
+gemv_h_stage1(const typename CT<T>::c* __restrict__ A, int64_t lda,
+              const typename CT<T>::c* __restrict__ x, int64_t nrows, int64_t n,
+              typename CT<T>::c* __restrict__ part, const int* gate) {
+  using C = typename CT<T>::c;
+  constexpr int V = VEC ? CT<T>::V : 1;
+  using LV = typename std::conditional<VEC, typename CT<T>::v, C>::type;
+  constexpr int CH = 512;  // rows of x per smem chunk
+  if (*gate) return;
+  __shared__ C xs[CH];
+  const int S = gridDim.y, s = blockIdx.y;
+  const int64_t i0 = nrows * s / S, i1 = nrows * (s + 1) / S;
+  const int64_t jv = (int64_t)blockIdx.x * NT + threadIdx.x;   // vector column index
+  const int64_t nv = n / V;
+  const bool active = jv < nv;
+  const int64_t jc = active ? jv : 0;
+  C acc[V];
+#pragma unroll
+  for (int v = 0; v < V; ++v) acc[v] = czero<C>();
+
+  for (int64_t c0 = i0; c0 < i1; c0 += CH) {
+    const int cn = (int)min((int64_t)CH, i1 - c0);
+    __syncthreads();
+    for (int t = threadIdx.x; t < cn; t += NT) xs[t] = x[c0 + t];
+    __syncthreads();
+    const LV* Ap = reinterpret_cast<const LV*>(A + c0 * lda) + jc;
+    const int64_t ldv = lda / V;
+    int t = 0;
+    for (; t + UR <= cn; t += UR) {
+      LV a[UR];
+#pragma unroll
+      for (int u = 0; u < UR; ++u) a[u] = ld_stream(Ap + (int64_t)(t + u) * ldv);
+#pragma unroll
+      for (int u = 0; u < UR; ++u) {
+        C ac[V];
+        unpack(a[u], ac);
+        const C xi = xs[t + u];
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+          if (CONJ) cfmac(acc[v], ac[v], xi); else cfma(acc[v], ac[v], xi);
+        }
+      }
+    }
+    for (; t < cn; ++t) {
+      C ac[V];
+      unpack(ld_stream(Ap + (int64_t)t * ldv), ac);
+      const C xi = xs[t];
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        if (CONJ) cfmac(acc[v], ac[v], xi); else cfma(acc[v], ac[v], xi);
+      }
+    }
+  }
+  if (active) {
+#pragma unroll
+    for (int v = 0; v < V; ++v) part[(int64_t)s * n + jv * V + v] = acc[v];
+  }
+  // scalar tail column (odd n with VEC): handled by strip 0, thread 0
+  if (VEC && (n % V) && blockIdx.x == 0 && threadIdx.x == 0) {
+    const int64_t j = n - 1;
+    C a2 = czero<C>();
+    for (int64_t i = i0; i < i1; ++i) {
+      if (CONJ) cfmac(a2, A[i * lda + j], x[i]); else cfma(a2, A[i * lda + j], x[i]);
+    }
+    part[(int64_t)s * n + j] = a2;
+  }
+}
+
+// K2 stage 2: w_j = Σ_s part[s][off + j] in split order, then epilogue.
+template <typename T, int NT, class Epi>
+__global__ void __launch_bounds__(NT)
+gemv_h_stage2(const typename CT<T>::c* __restrict__ part, int S, int64_t n, int64_t off,
+              int64_t nout, Epi epi, Red red, State* st, const int* gate) {
+  using C = typename CT<T>::c;
+  constexpr int KK = Epi::K > 0 ? Epi::K : 1;
+  if (*gate) return;
+  epi.load(st);
+  double2 dacc[KK];
+#pragma unroll
+  for (int k = 0; k < KK; ++k) dacc[k] = make_double2(0.0, 0.0);
+  for (int64_t j = (int64_t)blockIdx.x * NT + threadIdx.x; j < nout; j += (int64_t)gridDim.x * NT) {
+    double2 w = make_double2(0.0, 0.0);
+    for (int s = 0; s < S; ++s) {
+      C p = __ldcs(part + (int64_t)s * n + off + j);
+      w.x += (double)p.x; w.y += (double)p.y;
+    }
+    epi(j, fromd2<C>(w), dacc);
+  }
+  if constexpr (Epi::K > 0) finish_reduction<KK, NT, Epi>(dacc, red, st);
+}
+
+// ---------------------------------------------------------------------------
+// K3 CSR SpMV, LPR lanes per row (LPR = 4 or 8 for ~7 nnz/row stencils,
+// 32 = warp-per-row).  Column indices are GLOBAL; x is a full-length buffer
+// (own slice + halos filled).  CONJ: y = conj(A·conj(x)) (= Aᴴx for
+// complex-symmetric A).
+// ---------------------------------------------------------------------------
+template <typename T, int LPR, int NT, bool CONJ, class Epi>
+__global__ void __launch_bounds__(NT)
+spmv_csr_kernel(const int32_t* __restrict__ rowptr, const int32_t* __restrict__ colind,
+                const typename CT<T>::c* __restrict__ vals, const typename CT<T>::c* __restrict__ x,
+                int64_t nrows, Epi epi, Red red, State* st, const int* gate) {
+  using C = typename CT<T>::c;
+  constexpr int KK = Epi::K > 0 ? Epi::K : 1;
+  if (*gate) return;
+  epi.load(st);
+  double2 dacc[KK];
+#pragma unroll
+  for (int k = 0; k < KK; ++k) dacc[k] = make_double2(0.0, 0.0);
+  const int sub = threadIdx.x % LPR;
+  const int64_t rows_per_iter = (int64_t)gridDim.x * (NT / LPR);
+  for (int64_t i = (int64_t)blockIdx.x * (NT / LPR) + threadIdx.x / LPR; i < nrows; i += rows_per_iter) {
+    const int k0 = __ldg(rowptr + i), k1 = __ldg(rowptr + i + 1);
+    C acc = czero<C>();
+    for (int k = k0 + sub; k < k1; k += LPR) {
+      const C a = __ldcs(vals + k);
+      C xv = __ldg(x + __ldcs(colind + k));
+      if (CONJ) xv = cconj(xv);
+      cfma(acc, a, xv);
+    }
+#pragma unroll
+    for (int o = LPR / 2; o > 0; o >>= 1) {
+      acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o, LPR);
+      acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o, LPR);
+    }
+    if (sub == 0) epi(i, CONJ ? cconj(acc) : acc, dacc);
+  }
+  if constexpr (Epi::K > 0) finish_reduction<KK, NT, Epi>(dacc, red, st);
+}
+
+// ---------------------------------------------------------------------------
+// K4 fused vector pass: one grid-stride sweep applying a method-phase
+// functor to every local element, with up to K fp64 partial sums.
+// ---------------------------------------------------------------------------
+template <int NT, class Op>
+__global__ void __launch_bounds__(NT)
+pass_kernel(Op op, int64_t n, Red red, State* st, const int* gate) {
+  constexpr int KK = Op::K > 0 ? Op::K : 1;
+  if (*gate) return;
+  op.load(st);
+  double2 dacc[KK];
+#pragma unroll
+  for (int k = 0; k < KK; ++k) dacc[k] = make_double2(0.0, 0.0);
+  for (int64_t i = (int64_t)blockIdx.x * NT + threadIdx.x; i < n; i += (int64_t)gridDim.x * NT) op(i, dacc);
+  if constexpr (Op::K > 0) finish_reduction<KK, NT, Op>(dacc, red, st);
+}
+
+// epilogue applied as a pass over a stored vector (multi-GPU Aᴴ: after the
+// reduce-scatter the epilogue runs on the local slice)
+template <typename C, class Epi>
+struct EpiPass {
+  static constexpr int K = Epi::K;
+  Epi epi;
+  const C* w;
+  __device__ void load(const State* st) { epi.load(st); }
+  __device__ void operator()(int64_t i, double2* acc) { epi(i, w[i], acc); }
+  static __device__ void finish(State* st, const double2* s) { Epi::finish(st, s); }
+};
+
+// multi-GPU scalar step: sum the world×K allgathered rank sums in rank order
+template <int K, class Fin>
+__global__ void scalar_kernel(const double2* all, int world, State* st, const int* gate) {
+  if (*gate) return;
+  double2 s[K];
+  for (int k = 0; k < K; ++k) s[k] = make_double2(0.0, 0.0);
+  for (int r = 0; r < world; ++r)
+    for (int k = 0; k < K; ++k) { s[k].x += all[r * K + k].x; s[k].y += all[r * K + k].y; }
+  Fin::finish(st, s);
+}
+
+}  // namespace ccg

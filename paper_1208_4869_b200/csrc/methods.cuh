@@ -1,0 +1,564 @@
+// methods.cuh — the five recurrences of the hot path, split into phases.
+//
+// Each phase is (a) a per-element functor run inside a matvec epilogue or a
+// fused vector pass, accumulating up to K fp64 partial sums, and (b) a
+// single-thread `finish` that turns the sums into the recurrence scalars,
+// applies the stopping / breakdown rules and updates the device State.
+//
+// Recurrences: BiCGSTAB, CGNE, QMR — PIM90 set, PAPER.md P:57 [§2.1] (QMR as
+// corrected, P:101 [§6]); BiCOR, CORS — P:69 [§2.4].  The paper writes none
+// of them down; the formulation followed is SURVEY.md §8(c) O1-O5 (restated
+// in DESIGN.md), with the paper readings Q1-Q16.  Stopping rule
+// ‖r_k‖² ≤ tol²‖r_0‖², breakdown = a divisor exactly 0 (Q6),
+// NaN/Inf scalar => NONFINITE.
+//
+// Vector updates run in the working precision T; scalars are fp64 and are
+// rounded to T once per kernel (load()).
+#pragma once
+#include "common.cuh"
+
+namespace ccg {
+
+template <typename T> using Cx = typename CT<T>::c;
+
+__device__ __forceinline__ void conv_check_common(State* st, int k, double rr, bool& stop) {
+  // rr non-finite -> NONFINITE with k-1 completed; converged -> k; maxit -> k
+  stop = true;
+  if (!isfinite(rr)) { set_done(st, ST_NONFINITE, k - 1); return; }
+  push_hist(st, k, rr);
+  if (rr <= st->tol2r0) { set_done(st, ST_CONVERGED, k); return; }
+  if (k >= st->maxit) { set_done(st, ST_MAXIT, k); return; }
+  stop = false;
+}
+
+// ===========================================================================
+// Generic phases
+// ===========================================================================
+// r = y (pass) or r = y − A·x0 (gemv epilogue); copies r into up to three
+// more vectors (shadow residuals etc.); K=1: ‖r‖².
+template <typename T>
+struct InitR {
+  static constexpr int K = 1;
+  using C = Cx<T>;
+  const C* y;
+  C *d0, *d1, *d2, *d3;
+  __device__ void load(const State*) {}
+  __device__ void put(int64_t i, C r, double2* acc) {
+    if (d0) d0[i] = r;
+    if (d1) d1[i] = r;
+    if (d2) d2[i] = r;
+    if (d3) d3[i] = r;
+    nrm_acc(acc[0], r);
+  }
+  __device__ void operator()(int64_t i, double2* acc) { put(i, y[i], acc); }        // pass
+  __device__ void operator()(int64_t i, C ax, double2* acc) { put(i, csub(y[i], ax), acc); }  // epilogue
+  static __device__ void finish(State* st, const double2* s) {
+    const double rr = s[0].x;
+    st->r0sq = rr;
+    st->tol2r0 = st->tol2 * rr;
+    st->rr = rr;
+    if (st->hist && st->hist_cap > 0) st->hist[0] = rr > 0 ? 1.0 : 0.0;
+    if (!isfinite(rr)) { set_done(st, ST_NONFINITE, 0); return; }
+    if (rr == 0.0) { set_done(st, ST_CONVERGED, 0); return; }
+    switch (st->method) {
+      case M_BICGSTAB: st->rho = make_double2(rr, 0.0); break;
+      case M_CGNE: st->rho_r = rr; break;
+      case M_QMR:
+        st->rnrm = sqrt(rr); st->xnrm = sqrt(rr);
+        st->gamma_prev = 1.0; st->eta = make_double2(-1.0, 0.0); st->theta_prev = 0.0;
+        break;
+      default: break;
+    }
+  }
+};
+
+// out[i] = value (ccg_apply, multi-GPU Aᴴ full-length result)
+template <typename T>
+struct Store {
+  static constexpr int K = 0;
+  using C = Cx<T>;
+  C* out;
+  __device__ void load(const State*) {}
+  __device__ void operator()(int64_t i, C v, double2*) { out[i] = v; }
+  static __device__ void finish(State*, const double2*) {}
+};
+
+// dst[i] = src[i]
+template <typename T>
+struct Copy {
+  static constexpr int K = 0;
+  using C = Cx<T>;
+  const C* src;
+  C* dst;
+  __device__ void load(const State*) {}
+  __device__ void operator()(int64_t i, double2*) { dst[i] = src[i]; }
+  static __device__ void finish(State*, const double2*) {}
+};
+
+// ‖y − A·x‖² at exit
+template <typename T>
+struct TrueRes {
+  static constexpr int K = 1;
+  using C = Cx<T>;
+  const C* y;
+  __device__ void load(const State*) {}
+  __device__ void operator()(int64_t i, C ax, double2* acc) { nrm_acc(acc[0], csub(y[i], ax)); }
+  static __device__ void finish(State* st, const double2* s) { st->true_rr = s[0].x; }
+};
+
+// ===========================================================================
+// O1 BiCGSTAB.  Per iteration: P → [A p → v, σ] → S → [A s → t, ⟨t,s⟩,⟨t,t⟩] → X
+// ===========================================================================
+template <typename T>
+struct BsP {  // p = r (k=1) | p = r + β(p − ωv)
+  static constexpr int K = 0;
+  using C = Cx<T>;
+  const C* r; C* p; const C* v;
+  C beta, omega; int first;
+  __device__ void load(const State* st) {
+    first = st->iter == 0;
+    beta = fromd2<C>(st->beta); omega = fromd2<C>(st->omega);
+  }
+  __device__ void operator()(int64_t i, double2*) {
+    p[i] = first ? r[i] : caxpy(r[i], beta, caxmy(p[i], omega, v[i]));
+  }
+  static __device__ void finish(State*, const double2*) {}
+};
+
+template <typename T>
+struct BsV {  // v = A p ; σ = ⟨r̃, v⟩ ; α = ρ/σ
+  static constexpr int K = 1;
+  using C = Cx<T>;
+  C* v; const C* rt;
+  __device__ void load(const State*) {}
+  __device__ void operator()(int64_t i, C val, double2* acc) { v[i] = val; dotc_acc(acc[0], rt[i], val); }
+  static __device__ void finish(State* st, const double2* s) {
+    const int k = st->iter + 1;
+    st->matvecs_a++;
+    const double2 sigma = s[0];
+    if (zzero(sigma)) { set_done(st, ST_BREAKDOWN, k - 1, BD_SIGMA); return; }
+    st->alpha = zdiv(st->rho, sigma);
+    if (!zfinite(st->alpha)) { set_done(st, ST_NONFINITE, k - 1); return; }
+  }
+};
+
+template <typename T>
+struct BsS {  // s = r − αv ; ‖s‖² ; half-step test (Q4)
+  static constexpr int K = 1;
+  using C = Cx<T>;
+  const C* r; const C* v; C* s;
+  C alpha;
+  __device__ void load(const State* st) { alpha = fromd2<C>(st->alpha); }
+  __device__ void operator()(int64_t i, double2* acc) {
+    const C si = caxmy(r[i], alpha, v[i]);
+    s[i] = si;
+    nrm_acc(acc[0], si);
+  }
+  static __device__ void finish(State* st, const double2* sm) {
+    const int k = st->iter + 1;
+    const double ss = sm[0].x;
+    if (!isfinite(ss)) { set_done(st, ST_NONFINITE, k - 1); return; }
+    st->ss = ss;
+    if (ss <= st->tol2r0) { st->half = 1; st->gate2 = 1; }
+  }
+};
+
+template <typename T>
+struct BsT {  // t = A s ; ⟨t,s⟩, ⟨t,t⟩ ; ω
+  static constexpr int K = 2;
+  using C = Cx<T>;
+  C* t; const C* s;
+  __device__ void load(const State*) {}
+  __device__ void operator()(int64_t i, C val, double2* acc) {
+    t[i] = val;
+    dotc_acc(acc[0], val, s[i]);
+    nrm_acc(acc[1], val);
+  }
+  static __device__ void finish(State* st, const double2* sm) {
+    const int k = st->iter + 1;
+    st->matvecs_a++;
+    const double tt = sm[1].x;
+    if (tt == 0.0) { set_done(st, ST_BREAKDOWN, k - 1, BD_TT); return; }
+    st->omega = make_double2(sm[0].x / tt, sm[0].y / tt);
+    if (!zfinite(st->omega)) { set_done(st, ST_NONFINITE, k - 1); return; }
+    if (zzero(st->omega)) { set_done(st, ST_BREAKDOWN, k - 1, BD_OMEGA); return; }
+  }
+};
+
+template <typename T>
+struct BsX {  // x += αp + ωs ; r = s − ωt ; ‖r‖², ⟨r̃, r⟩   (half-step: x += αp)
+  static constexpr int K = 2;
+  using C = Cx<T>;
+  C* x; C* r; const C* p; const C* s; const C* t; const C* rt;
+  C alpha, omega; int half;
+  __device__ void load(const State* st) {
+    alpha = fromd2<C>(st->alpha); omega = fromd2<C>(st->omega); half = st->half;
+  }
+  __device__ void operator()(int64_t i, double2* acc) {
+    if (half) { x[i] = caxpy(x[i], alpha, p[i]); return; }
+    const C si = s[i];
+    x[i] = caxpy(caxpy(x[i], alpha, p[i]), omega, si);
+    const C ri = caxmy(si, omega, t[i]);
+    r[i] = ri;
+    nrm_acc(acc[0], ri);
+    dotc_acc(acc[1], rt[i], ri);
+  }
+  static __device__ void finish(State* st, const double2* sm) {
+    const int k = st->iter + 1;
+    if (st->half) {
+      push_hist(st, k, st->ss);
+      set_done(st, ST_CONVERGED, k);
+      return;
+    }
+    bool stop;
+    conv_check_common(st, k, sm[0].x, stop);
+    if (stop) return;
+    const double2 rho_new = sm[1];
+    if (!zfinite(rho_new)) { set_done(st, ST_NONFINITE, k); return; }
+    if (zzero(rho_new)) { set_done(st, ST_BREAKDOWN, k, BD_RHO); return; }
+    st->beta = zmul(zdiv(rho_new, st->rho), zdiv(st->alpha, st->omega));
+    st->rho = rho_new;
+    st->iter = k;
+  }
+};
+
+// ===========================================================================
+// O2 CGNE (Craig).  Setup: AH r → P0 (π, α).  Per iteration:
+// [A p → r −= αAp, x += αp, ‖r‖²] → [Aᴴ r → p = Aᴴr + βp, ‖p‖²]
+// ===========================================================================
+__device__ __forceinline__ void cgne_pi(State* st, double pi) {
+  const int k = st->iter + 1;
+  st->matvecs_ah++;
+  if (pi == 0.0) { set_done(st, ST_BREAKDOWN, k - 1, BD_PI); return; }
+  st->pi_r = pi;
+  st->alpha_r = st->rho_r / pi;
+  if (!isfinite(st->alpha_r)) { set_done(st, ST_NONFINITE, k - 1); return; }
+}
+
+template <typename T>
+struct CgP0 {  // p = Aᴴ r (setup)
+  static constexpr int K = 1;
+  using C = Cx<T>;
+  C* p;
+  __device__ void load(const State*) {}
+  __device__ void operator()(int64_t i, C w, double2* acc) { p[i] = w; nrm_acc(acc[0], w); }
+  static __device__ void finish(State* st, const double2* s) { cgne_pi(st, s[0].x); }
+};
+
+template <typename T>
+struct CgP {  // p = Aᴴ r + βp
+  static constexpr int K = 1;
+  using C = Cx<T>;
+  C* p;
+  T beta;
+  __device__ void load(const State* st) { beta = (T)st->beta_r; }
+  __device__ void operator()(int64_t i, C w, double2* acc) {
+    C pi = p[i];
+    C v; v.x = w.x + beta * pi.x; v.y = w.y + beta * pi.y;
+    p[i] = v;
+    nrm_acc(acc[0], v);
+  }
+  static __device__ void finish(State* st, const double2* s) { cgne_pi(st, s[0].x); }
+};
+
+template <typename T>
+struct CgQ {  // r −= α(Ap) ; x += αp ; ‖r‖²
+  static constexpr int K = 1;
+  using C = Cx<T>;
+  C* r; C* x; const C* p;
+  T alpha;
+  __device__ void load(const State* st) { alpha = (T)st->alpha_r; }
+  __device__ void operator()(int64_t i, C q, double2* acc) {
+    C pi = p[i], xi = x[i], ri = r[i];
+    xi.x += alpha * pi.x; xi.y += alpha * pi.y;
+    ri.x -= alpha * q.x; ri.y -= alpha * q.y;
+    x[i] = xi; r[i] = ri;
+    nrm_acc(acc[0], ri);
+  }
+  static __device__ void finish(State* st, const double2* s) {
+    const int k = st->iter + 1;
+    st->matvecs_a++;
+    bool stop;
+    conv_check_common(st, k, s[0].x, stop);
+    if (stop) return;
+    st->beta_r = s[0].x / st->rho_r;
+    st->rho_r = s[0].x;
+    st->iter = k;
+  }
+};
+
+// ===========================================================================
+// O3 QMR (no look-ahead, Aᴴ form).  Setup: V.  Per iteration:
+// P → [A p → p̃, ε] → [Aᴴ q → w̃, ṽ, ‖ṽ‖², ‖w̃‖²] → DV (d, s, x, r, ‖r‖², v, w, δ)
+// ===========================================================================
+__device__ __forceinline__ void qmr_delta(State* st, double2 delta) {
+  // start of iteration k = iter + 1
+  const int k = st->iter + 1;
+  if (st->rnrm == 0.0) { set_done(st, ST_BREAKDOWN, k - 1, BD_VNORM); return; }
+  if (st->xnrm == 0.0) { set_done(st, ST_BREAKDOWN, k - 1, BD_WNORM); return; }
+  if (!zfinite(delta)) { set_done(st, ST_NONFINITE, k - 1); return; }
+  if (zzero(delta)) { set_done(st, ST_BREAKDOWN, k - 1, BD_DELTA); return; }
+  st->delta = delta;
+  if (st->iter > 0) {
+    st->cp = zdiv(zscal(delta, st->xnrm), st->eps);             // ξδ/ε
+    st->cq = zconj(zdiv(zscal(delta, st->rnrm), st->eps));      // conj(ρδ/ε)
+  }
+}
+
+template <typename T>
+struct QmV {  // v = ṽ/ρ ; w = w̃/ξ ; δ = ⟨w, v⟩   (setup)
+  static constexpr int K = 1;
+  using C = Cx<T>;
+  const C* vt; const C* wt; C* v; C* w;
+  T rn, xn;
+  __device__ void load(const State* st) { rn = (T)st->rnrm; xn = (T)st->xnrm; }
+  __device__ void operator()(int64_t i, double2* acc) {
+    const C vi = cdivr(vt[i], rn), wi = cdivr(wt[i], xn);
+    v[i] = vi; w[i] = wi;
+    dotc_acc(acc[0], wi, vi);
+  }
+  static __device__ void finish(State* st, const double2* s) { qmr_delta(st, s[0]); }
+};
+
+template <typename T>
+struct QmP {  // p = v − (ξδ/ε)p ; q = w − conj(ρδ/ε)q   (k=1: p = v, q = w)
+  static constexpr int K = 0;
+  using C = Cx<T>;
+  const C* v; const C* w; C* p; C* q;
+  C cp, cq; int first;
+  __device__ void load(const State* st) {
+    first = st->iter == 0; cp = fromd2<C>(st->cp); cq = fromd2<C>(st->cq);
+  }
+  __device__ void operator()(int64_t i, double2*) {
+    if (first) { p[i] = v[i]; q[i] = w[i]; return; }
+    p[i] = caxmy(v[i], cp, p[i]);
+    q[i] = caxmy(w[i], cq, q[i]);
+  }
+  static __device__ void finish(State*, const double2*) {}
+};
+
+template <typename T>
+struct QmPt {  // p̃ = A p ; ε = ⟨q, p̃⟩ ; β = ε/δ
+  static constexpr int K = 1;
+  using C = Cx<T>;
+  C* pt; const C* q;
+  __device__ void load(const State*) {}
+  __device__ void operator()(int64_t i, C val, double2* acc) { pt[i] = val; dotc_acc(acc[0], q[i], val); }
+  static __device__ void finish(State* st, const double2* s) {
+    const int k = st->iter + 1;
+    st->matvecs_a++;
+    const double2 eps = s[0];
+    if (!zfinite(eps)) { set_done(st, ST_NONFINITE, k - 1); return; }
+    if (zzero(eps)) { set_done(st, ST_BREAKDOWN, k - 1, BD_EPSILON); return; }
+    st->eps = eps;
+    st->beta = zdiv(eps, st->delta);
+    if (zzero(st->beta)) { set_done(st, ST_BREAKDOWN, k - 1, BD_BETA); return; }
+  }
+};
+
+template <typename T>
+struct QmVW {  // w̃ = Aᴴq − conj(β)w ; ṽ = p̃ − βv ; ‖ṽ‖², ‖w̃‖² ; θ, γ, η
+  static constexpr int K = 2;
+  using C = Cx<T>;
+  C* vt; C* wt; const C* pt; const C* v; const C* w;
+  C beta, cbeta;
+  __device__ void load(const State* st) { beta = fromd2<C>(st->beta); cbeta = fromd2<C>(zconj(st->beta)); }
+  __device__ void operator()(int64_t i, C u, double2* acc) {
+    const C wti = caxmy(u, cbeta, w[i]);
+    const C vti = caxmy(pt[i], beta, v[i]);
+    wt[i] = wti; vt[i] = vti;
+    nrm_acc(acc[0], vti);
+    nrm_acc(acc[1], wti);
+  }
+  static __device__ void finish(State* st, const double2* s) {
+    const int k = st->iter + 1;
+    st->matvecs_ah++;
+    const double rn = sqrt(s[0].x), xn = sqrt(s[1].x);
+    st->rnrm_next = rn; st->xnrm_next = xn;
+    const double theta = rn / (st->gamma_prev * zabs(st->beta));
+    const double gamma = 1.0 / sqrt(1.0 + theta * theta);
+    if (!isfinite(theta) || !isfinite(gamma)) { set_done(st, ST_NONFINITE, k - 1); return; }
+    if (gamma == 0.0) { set_done(st, ST_BREAKDOWN, k - 1, BD_GAMMA); return; }
+    // η = −η ρ γ² / (β γ_prev²)
+    const double2 num = zscal(zscal(zscal(zscal(st->eta, -1.0), st->rnrm), gamma), gamma);
+    const double2 den = zscal(zscal(st->beta, st->gamma_prev), st->gamma_prev);
+    st->eta = zdiv(num, den);
+    st->theta = theta; st->gamma = gamma;
+    const double tg = st->theta_prev * gamma;
+    st->c2 = tg * tg;
+  }
+};
+
+template <typename T>
+struct QmDV {  // d, s ; x += d ; r −= s ; ‖r‖² ; v = ṽ/ρ' ; w = w̃/ξ' ; δ' = ⟨w, v⟩
+  static constexpr int K = 2;
+  using C = Cx<T>;
+  C* d; C* sv; C* x; C* r; const C* p; const C* pt;
+  const C* vt; const C* wt; C* v; C* w;
+  C eta; T c2, rn, xn; int first;
+  __device__ void load(const State* st) {
+    eta = fromd2<C>(st->eta); c2 = (T)st->c2; rn = (T)st->rnrm_next; xn = (T)st->xnrm_next;
+    first = st->iter == 0;
+  }
+  __device__ void operator()(int64_t i, double2* acc) {
+    C di = cmul(eta, p[i]), si = cmul(eta, pt[i]);
+    if (!first) {
+      const C dd = d[i], ss = sv[i];
+      di.x += c2 * dd.x; di.y += c2 * dd.y;
+      si.x += c2 * ss.x; si.y += c2 * ss.y;
+    }
+    d[i] = di; sv[i] = si;
+    x[i] = cadd(x[i], di);
+    const C ri = csub(r[i], si);
+    r[i] = ri;
+    nrm_acc(acc[0], ri);
+    const C vi = cdivr(vt[i], rn), wi = cdivr(wt[i], xn);
+    v[i] = vi; w[i] = wi;
+    dotc_acc(acc[1], wi, vi);
+  }
+  static __device__ void finish(State* st, const double2* s) {
+    const int k = st->iter + 1;
+    bool stop;
+    conv_check_common(st, k, s[0].x, stop);
+    if (stop) return;
+    st->rnrm = st->rnrm_next; st->xnrm = st->xnrm_next;
+    st->gamma_prev = st->gamma; st->theta_prev = st->theta;
+    st->iter = k;
+    qmr_delta(st, s[1]);
+  }
+};
+
+// ===========================================================================
+// O4 BiCOR.  Per iteration: [A r → r̂, ρ = ⟨r*, r̂⟩] → P → [Aᴴ p* → q*, ξ = ⟨q*, q⟩] → X
+// ===========================================================================
+__device__ __forceinline__ void rho_step(State* st, double2 rho, bool count_a) {
+  const int k = st->iter + 1;
+  if (count_a) st->matvecs_a++;
+  if (!zfinite(rho)) { set_done(st, ST_NONFINITE, k - 1); return; }
+  if (zzero(rho)) { set_done(st, ST_BREAKDOWN, k - 1, BD_RHO); return; }
+  st->rho = rho;
+  if (st->iter > 0) st->beta = zdiv(rho, st->rho_prev);
+}
+__device__ __forceinline__ void xi_step(State* st, double2 xi) {
+  const int k = st->iter + 1;
+  if (zzero(xi)) { set_done(st, ST_BREAKDOWN, k - 1, BD_XI); return; }
+  st->alpha = zdiv(st->rho, xi);
+  if (!zfinite(st->alpha)) { set_done(st, ST_NONFINITE, k - 1); return; }
+}
+__device__ __forceinline__ void r_step(State* st, double rr) {
+  const int k = st->iter + 1;
+  bool stop;
+  conv_check_common(st, k, rr, stop);
+  if (stop) return;
+  st->rho_prev = st->rho;
+  st->iter = k;
+}
+
+template <typename T>
+struct RhoEpi {  // r̂ = A r ; ρ = ⟨shadow, r̂⟩   (BiCOR and CORS)
+  static constexpr int K = 1;
+  using C = Cx<T>;
+  C* rh; const C* sh;
+  __device__ void load(const State*) {}
+  __device__ void operator()(int64_t i, C val, double2* acc) { rh[i] = val; dotc_acc(acc[0], sh[i], val); }
+  static __device__ void finish(State* st, const double2* s) { rho_step(st, s[0], true); }
+};
+
+template <typename T>
+struct BcP {  // p = r + βp ; p* = r* + conj(β)p* ; q = r̂ + βq   (k=1: copies)
+  static constexpr int K = 0;
+  using C = Cx<T>;
+  const C* r; const C* rs; const C* rh; C* p; C* ps; C* q;
+  C beta, cbeta; int first;
+  __device__ void load(const State* st) {
+    first = st->iter == 0; beta = fromd2<C>(st->beta); cbeta = fromd2<C>(zconj(st->beta));
+  }
+  __device__ void operator()(int64_t i, double2*) {
+    if (first) { p[i] = r[i]; ps[i] = rs[i]; q[i] = rh[i]; return; }
+    p[i] = caxpy(r[i], beta, p[i]);
+    ps[i] = caxpy(rs[i], cbeta, ps[i]);
+    q[i] = caxpy(rh[i], beta, q[i]);
+  }
+  static __device__ void finish(State*, const double2*) {}
+};
+
+template <typename T>
+struct BcQs {  // q* = Aᴴ p* ; ξ = ⟨q*, q⟩ ; α = ρ/ξ
+  static constexpr int K = 1;
+  using C = Cx<T>;
+  C* qs; const C* q;
+  __device__ void load(const State*) {}
+  __device__ void operator()(int64_t i, C w, double2* acc) { qs[i] = w; dotc_acc(acc[0], w, q[i]); }
+  static __device__ void finish(State* st, const double2* s) { st->matvecs_ah++; xi_step(st, s[0]); }
+};
+
+template <typename T>
+struct BcX {  // x += αp ; r −= αq ; r* −= conj(α)q* ; ‖r‖²
+  static constexpr int K = 1;
+  using C = Cx<T>;
+  C* x; C* r; C* rs; const C* p; const C* q; const C* qs;
+  C alpha, calpha;
+  __device__ void load(const State* st) { alpha = fromd2<C>(st->alpha); calpha = fromd2<C>(zconj(st->alpha)); }
+  __device__ void operator()(int64_t i, double2* acc) {
+    x[i] = caxpy(x[i], alpha, p[i]);
+    const C ri = caxmy(r[i], alpha, q[i]);
+    r[i] = ri;
+    rs[i] = caxmy(rs[i], calpha, qs[i]);
+    nrm_acc(acc[0], ri);
+  }
+  static __device__ void finish(State* st, const double2* s) { r_step(st, s[0].x); }
+};
+
+// ===========================================================================
+// O5 CORS (transpose-free).  Per iteration:
+// [A r → r̂, ρ = ⟨r₀*, r̂⟩] → P (e, ê, q̂) → [A q̂ → q, ξ = ⟨r₀*, q⟩] → H (h, ĥ, x, r, ‖r‖²)
+// ===========================================================================
+template <typename T>
+struct CoP {  // e = r + βh ; ê = r̂ + βĥ ; q̂ = ê + β(ĥ + βq̂)   (k=1: e = r, ê = q̂ = r̂)
+  static constexpr int K = 0;
+  using C = Cx<T>;
+  const C* r; const C* rh; const C* h; const C* hh; C* e; C* eh; C* qh;
+  C beta; int first;
+  __device__ void load(const State* st) { first = st->iter == 0; beta = fromd2<C>(st->beta); }
+  __device__ void operator()(int64_t i, double2*) {
+    if (first) { const C v = rh[i]; e[i] = r[i]; eh[i] = v; qh[i] = v; return; }
+    const C hhi = hh[i];
+    e[i] = caxpy(r[i], beta, h[i]);
+    const C ehi = caxpy(rh[i], beta, hhi);
+    eh[i] = ehi;
+    qh[i] = caxpy(ehi, beta, caxpy(hhi, beta, qh[i]));
+  }
+  static __device__ void finish(State*, const double2*) {}
+};
+
+template <typename T>
+struct CoQ {  // q = A q̂ ; ξ = ⟨r₀*, q⟩ ; α = ρ/ξ
+  static constexpr int K = 1;
+  using C = Cx<T>;
+  C* q; const C* r0s;
+  __device__ void load(const State*) {}
+  __device__ void operator()(int64_t i, C val, double2* acc) { q[i] = val; dotc_acc(acc[0], r0s[i], val); }
+  static __device__ void finish(State* st, const double2* s) { st->matvecs_a++; xi_step(st, s[0]); }
+};
+
+template <typename T>
+struct CoH {  // h = e − αq̂ ; ĥ = ê − αq ; x += α(e + h) ; r −= α(ê + ĥ) ; ‖r‖²
+  static constexpr int K = 1;
+  using C = Cx<T>;
+  const C* e; const C* eh; const C* qh; const C* q; C* h; C* hh; C* x; C* r;
+  C alpha;
+  __device__ void load(const State* st) { alpha = fromd2<C>(st->alpha); }
+  __device__ void operator()(int64_t i, double2* acc) {
+    const C ei = e[i], ehi = eh[i];
+    const C hi = caxmy(ei, alpha, qh[i]);
+    const C hhi = caxmy(ehi, alpha, q[i]);
+    h[i] = hi; hh[i] = hhi;
+    x[i] = caxpy(x[i], alpha, cadd(ei, hi));
+    const C ri = caxmy(r[i], alpha, cadd(ehi, hhi));
+    r[i] = ri;
+    nrm_acc(acc[0], ri);
+  }
+  static __device__ void finish(State* st, const double2* s) { r_step(st, s[0].x); }
+};
+
+}  // namespace ccg

@@ -1,0 +1,162 @@
+"""Solver parity: ccg_solve (C-ABI, sm_100a) vs the oracle recurrences.
+
+Bar (north_star): iteration counts within ±2 of the oracle; x compared at an
+EQUAL iteration count (stopping one iteration apart moves x by
+more than the bar) within 1e-9 (c128) / 1e-4 (c64) relative; true residual
+≤ 10·tol.  Plus the method's degenerate cases.
+"""
+
+import numpy as np
+import pytest
+
+import paper_1208_4869_b200 as ccg
+import oracle
+from oracle import DenseOp, CsrOp
+from workloads import cfg1, cfg2, gauss_shifted_rows, cfg3_rhs, helmholtz_csr, helmholtz_rhs, dense_random
+from tests._gpu import Dense, Csr, XTOL, relerr
+
+pytestmark = pytest.mark.gpu
+
+HOT = ("bicgstab", "cgne", "qmr", "bicor", "cors")
+
+
+def _parity(h, op, y, method, tol, maxit, dtype):
+    o = oracle.solve(method, op, y, tol, maxit)
+    g = h.solve(method, y, tol, maxit)
+    assert g["status"] == o.status_name == "CONVERGED", (method, g["status"], o.status_name)
+    assert abs(g["iterations"] - o.iterations) <= 2, (method, g["iterations"], o.iterations)
+    assert g["true_rel_res"] <= 10 * tol
+    k = min(g["iterations"], o.iterations)
+    oe = oracle.solve(method, op, y, 0.0, k)
+    ge = h.solve(method, y, 0.0, k)
+    assert ge["iterations"] == oe.iterations == k
+    err = relerr(ge["x"], oe.x)
+    assert err <= XTOL[dtype], (method, k, err)
+    return o, g
+
+
+@pytest.mark.parametrize("method", HOT)
+def test_cfg1_all_methods(method):
+    A, y = cfg1()
+    with Dense(A) as h:
+        o, g = _parity(h, DenseOp(A), y, method, 1e-10, 500, np.complex128)
+        assert (g["matvecs_a"], g["matvecs_ah"]) == (o.matvecs_a, o.matvecs_ah)
+        assert g["half_step"] == o.half_step
+        hist = ccg.ccg_get_history(h.h)
+        r0 = o.history[0]
+        np.testing.assert_allclose(hist, np.array(o.history, float) / r0, rtol=1e-6, atol=1e-12)
+
+
+@pytest.mark.parametrize("method", HOT)
+def test_cfg2_all_methods(method):
+    A, y = cfg2()
+    with Dense(A) as h:
+        _parity(h, DenseOp(A), y, method, 1e-8, 1000, np.complex128)
+
+
+@pytest.mark.parametrize("method", ["bicgstab", "cgne", "qmr", "bicor", "cors"])
+def test_cfg3_proxy_c64(method):
+    n = 4096                     # cfg3 recipe at a size the oracle finishes quickly
+    A = gauss_shifted_rows(n, 0, n, seed=1)
+    y = cfg3_rhs(n)
+    with Dense(A) as h:
+        _parity(h, DenseOp(A), y, method, 1e-5, 500, np.complex64)
+
+
+@pytest.mark.parametrize("method", ["bicgstab", "cors"])
+def test_cfg5_proxy_csr(method):
+    N = 24
+    rp, ci, v = helmholtz_csr(N, kh=10 / 128)
+    y = helmholtz_rhs(N)
+    with Csr(rp, ci, v, N ** 3) as h:
+        _parity(h, CsrOp(rp, ci, v), y, method, 1e-8, 2000, np.complex128)
+
+
+@pytest.mark.parametrize("n", [1, 7, 257, 1000])
+@pytest.mark.parametrize("method", HOT)
+def test_ragged_sizes(method, n):
+    A = dense_random(n, seed=n, dtype=np.complex128, shift=3 - 1j)
+    y = dense_random(n, seed=n + 1)[:, 0] * 3
+    with Dense(A) as h:
+        _parity(h, DenseOp(A), y, method, 1e-10, 400, np.complex128)
+
+
+@pytest.mark.parametrize("method", HOT)
+def test_scaled_identity(method):
+    c = 3 - 4j
+    n = 10
+    y = np.arange(n) + 1j * np.arange(n)[::-1]
+    with Dense(c * np.eye(n, dtype=np.complex128)) as h:
+        g = h.solve(method, y.astype(np.complex128), 1e-12, 50)
+    assert g["status"] == "CONVERGED" and g["iterations"] == 1
+    np.testing.assert_allclose(g["x"], y / c, rtol=1e-14, atol=1e-14)
+    if method == "bicgstab":
+        assert g["half_step"] and g["matvecs_a"] == 1
+
+
+def test_breakdown_fixture():
+    A = np.array([[0, 1], [-1, 0]], dtype=np.complex128)
+    y = np.array([1, 0], dtype=np.complex128)
+    with Dense(A) as h:
+        g = h.solve("bicgstab", y, 1e-10, 10)
+        assert g["status"] == "BREAKDOWN" and g["breakdown"] == "sigma" and g["iterations"] == 0
+        for m in ("bicor", "cors"):
+            g = h.solve(m, y, 1e-10, 10)
+            assert g["status"] == "BREAKDOWN" and g["breakdown"] == "rho", m
+
+
+@pytest.mark.parametrize("method", HOT)
+def test_zero_rhs_maxit_nonfinite_x0(method):
+    A, y = cfg1(n=32, seed=2)
+    with Dense(A) as h:
+        g = h.solve(method, np.zeros(32, np.complex128), 1e-10, 10)
+        assert g["status"] == "CONVERGED" and g["iterations"] == 0 and not np.any(g["x"])
+        g = h.solve(method, y, 0.0, 3)
+        o = oracle.solve(method, DenseOp(A), y, 0.0, 3)
+        assert g["status"] == "MAXIT" and g["iterations"] == 3
+        assert (g["matvecs_a"], g["matvecs_ah"]) == (o.matvecs_a, o.matvecs_ah)
+        yb = y.copy()
+        yb[5] = np.nan
+        assert h.solve(method, yb, 1e-10, 10)["status"] == "NONFINITE"
+        xs = np.linalg.solve(A, y)
+        g = h.solve(method, y, 1e-6, 10, x0=xs)
+        assert g["status"] == "CONVERGED" and g["iterations"] <= 1
+        o = oracle.solve(method, DenseOp(A), y, 1e-12, 100, x0=0.5 * xs)
+        g = h.solve(method, y, 1e-12, 100, x0=0.5 * xs)
+        assert abs(g["iterations"] - o.iterations) <= 2 and relerr(g["x"], o.x) <= 1e-9
+
+
+def test_capability_and_state_errors():
+    rp, ci, v = helmholtz_csr(6)
+    with Csr(rp, ci, v, 216) as h:
+        for m in ("cgne", "qmr", "bicor"):
+            with pytest.raises(ccg.CcgError) as e:
+                h.solve(m, np.ones(216, np.complex128), 1e-8, 10)
+            assert e.value.code == -3
+    h = ccg.ccg_create("c64", 8)
+    try:
+        with pytest.raises(ccg.CcgError) as e:
+            ccg.ccg_solve(h, "bicgstab", None, np.ones(8, np.complex64), np.empty(8, np.complex64), 1e-5, 10)
+        assert e.value.code == -4
+    finally:
+        ccg.ccg_destroy(h)
+
+
+def test_csr_symmetric_ah_methods():
+    """Complex-symmetric CSR with CCG_FLAG_SYMMETRIC runs the Aᴴ methods (single GPU)."""
+    N = 10
+    rp, ci, v = helmholtz_csr(N, kh=10 / 128)
+    y = helmholtz_rhs(N)
+    with Csr(rp, ci, v, N ** 3, flags=ccg.FLAG_SYMMETRIC) as h:
+        for m in ("cgne", "qmr", "bicor"):
+            _parity(h, CsrOp(rp, ci, v), y, m, 1e-8, 3000, np.complex128)
+
+
+def test_host_pointer_solve_and_determinism():
+    A, y = cfg2()
+    with Dense(A) as h:
+        x1 = np.empty(4096, np.complex128)
+        r1 = ccg.ccg_solve(h.h, "bicgstab", None, y, x1, 1e-8, 1000)
+        r2 = h.solve("bicgstab", y, 1e-8, 1000)
+        assert r1["iterations"] == r2["iterations"]
+        assert np.array_equal(x1, r2["x"])        # bitwise run-to-run determinism
