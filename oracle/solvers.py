@@ -237,6 +237,8 @@ def _cgne(op, y, x, r, r0sq, tol2, maxit, ctx, hist, st):
         hist.append(sqrt(rho_new))
         if _conv(rho_new, tol2, r0sq):
             return CONVERGED, k, False
+        if k == maxit:              # no further iterate needs the next direction
+            break
         beta = ctx.r(rho_new / rho)
         p = op.apply_h(r) + beta * p                            # p = Aᴴr + βp
         rho = rho_new

@@ -16,7 +16,7 @@ import numpy as np
 __all__ = [
     "CONFIGS", "cfg1", "cfg2", "cfg3_rows", "cfg3_rhs", "cfg3", "gauss_shifted_rows",
     "dda_lattice_rows", "dda_lattice_rhs", "cfg2_like", "cfg4_rows", "cfg4_rhs",
-    "helmholtz_csr", "helmholtz_rhs", "cfg5", "dense_random", "lattice_dims",
+    "helmholtz_csr", "helmholtz_rhs", "cfg5", "dense_random", "lattice_dims", "BLOCK",
 ]
 
 # config index -> (dtype, n, methods, tol, maxit)  (BJ:7-11, maxit per Q8)
