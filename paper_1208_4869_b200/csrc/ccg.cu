@@ -85,6 +85,7 @@ struct Err {
 // ===========================================================================
 enum { NLOCAL = 12, NFULL = 3 };
 enum { OPK_NONE = 0, OPK_DENSE = 1, OPK_CSR = 2 };
+enum { GEMV_SPLIT = 0, GEMV_BULK = 1, GEMV_ROWS = 2 };
 
 struct ccg_ctx {
   int dtype = 0;
@@ -103,6 +104,12 @@ struct ccg_ctx {
   const void* vals = nullptr;
   int64_t nnz = 0, halo = 0;
   bool vec_ok = true;
+  bool bulk_ok = false;   // TMA bulk-copy GEMV usable (alignment / n multiple of a 4 KiB tile)
+  int bulk_grid = 0;
+  int gemv_mode = 0;      // GEMV_SPLIT (default) | GEMV_BULK | GEMV_ROWS (env CCG_GEMV)
+  int split_W = 0, split_strips = 1, split_nrb = 1, nstage2_grid = 1, split_ur = 8;
+  void* npart = nullptr;  // [strips][nloc] partial row sums of the split GEMV
+  size_t npart_bytes = 0;
   // workspace
   State* st = nullptr;
   State* st_host = nullptr;  // pinned
@@ -232,6 +239,9 @@ struct Engine {
   static constexpr int R = 8;
   static constexpr int UR = 8;
   static constexpr int LPR = 8;
+  static constexpr int BR = 8;        // rows per group, bulk GEMV
+  static constexpr int BSTAGES = 5;   // pipeline depth, bulk GEMV (5 x 36 KiB smem)
+  static constexpr int SUR = 8;       // 16-byte loads in flight per lane, split GEMV
 
   static C* L(ccg_ctx* c, int i) { return reinterpret_cast<C*>(c->loc[i]); }
   static C* F(ccg_ctx* c, int i) { return reinterpret_cast<C*>(c->full[i]); }
@@ -289,7 +299,48 @@ struct Engine {
   template <class Epi>
   static int matvec_a(ccg_ctx* c, const C* xfull, Epi epi, const int* gate) {
     tev_begin(c, 0);
-    if (c->opk == OPK_DENSE) {
+    if (c->opk == OPK_DENSE && c->gemv_mode == GEMV_SPLIT) {
+      const C* A = reinterpret_cast<const C*>(c->A);
+      C* part = reinterpret_cast<C*>(c->npart);
+      dim3 g(c->split_strips, c->split_nrb);
+      const size_t smem = (size_t)c->split_W * sizeof(C);
+      if (c->split_strips == 1) {
+        if (c->vec_ok)
+          gemv_n_split<T, NT, SUR, true, true, Epi><<<g, NT, smem, c->stream>>>(
+              A, c->lda, xfull, c->n, c->nloc, c->split_W, part, epi, make_red(c), c->st, gate);
+        else
+          gemv_n_split<T, NT, SUR, false, true, Epi><<<g, NT, smem, c->stream>>>(
+              A, c->lda, xfull, c->n, c->nloc, c->split_W, part, epi, make_red(c), c->st, gate);
+      } else {
+        Store<T> none{nullptr};
+        if (c->vec_ok && c->split_ur == 16)
+          gemv_n_split<T, NT, 16, true, false, Store<T>><<<g, NT, smem, c->stream>>>(
+              A, c->lda, xfull, c->n, c->nloc, c->split_W, part, none, make_red(c), c->st, gate);
+        else if (c->vec_ok && c->split_ur == 4)
+          gemv_n_split<T, NT, 4, true, false, Store<T>><<<g, NT, smem, c->stream>>>(
+              A, c->lda, xfull, c->n, c->nloc, c->split_W, part, none, make_red(c), c->st, gate);
+        else if (c->vec_ok)
+          gemv_n_split<T, NT, SUR, true, false, Store<T>><<<g, NT, smem, c->stream>>>(
+              A, c->lda, xfull, c->n, c->nloc, c->split_W, part, none, make_red(c), c->st, gate);
+        else
+          gemv_n_split<T, NT, SUR, false, false, Store<T>><<<g, NT, smem, c->stream>>>(
+              A, c->lda, xfull, c->n, c->nloc, c->split_W, part, none, make_red(c), c->st, gate);
+        c->launches++;
+        CK(c, cudaGetLastError());
+        gemv_h_stage2<T, NT, Epi><<<c->nstage2_grid, NT, 0, c->stream>>>(part, c->split_strips, c->nloc, 0,
+                                                                          c->nloc, epi, make_red(c), c->st, gate);
+      }
+    } else if (c->opk == OPK_DENSE && c->gemv_mode == GEMV_BULK && c->bulk_ok) {
+      constexpr size_t smem = bulk_smem_bytes<BR, BSTAGES>();
+      auto kern = gemv_n_bulk<T, BR, BSTAGES, Epi>;
+      static bool attr_set = false;  // per instantiation
+      if (!attr_set) {
+        CK(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr_set = true;
+      }
+      kern<<<c->bulk_grid, BULK_NT, smem, c->stream>>>(reinterpret_cast<const C*>(c->A), c->lda, xfull, c->n,
+                                                       c->nloc, epi, make_red(c), c->st, gate);
+    } else if (c->opk == OPK_DENSE) {
       const C* A = reinterpret_cast<const C*>(c->A);
       if (c->vec_ok)
         gemv_n_kernel<T, R, NT, true, Epi><<<c->gemv_grid, NT, 0, c->stream>>>(
@@ -504,6 +555,52 @@ static int choose_launch(ccg_ctx* c) {
   if (occ < 1) occ = 1;
   const int64_t groups = (c->nloc + E::R - 1) / E::R;
   c->gemv_grid = (int)std::max<int64_t>(1, std::min<int64_t>(groups, (int64_t)c->sm_count * occ));
+  c->bulk_ok = c->opk == OPK_DENSE && getenv("CCG_NO_BULK") == nullptr &&
+               ((c->n * (int64_t)sizeof(C)) % BULK_TILE == 0) && ((c->lda * (int64_t)sizeof(C)) % 16 == 0) &&
+               (((uintptr_t)c->A) % 16 == 0);
+  c->bulk_grid = (int)std::max<int64_t>(1, std::min<int64_t>((c->nloc + E::BR - 1) / E::BR, c->sm_count));
+  {
+    const char* gm = getenv("CCG_GEMV");
+    c->gemv_mode = (gm && !strcmp(gm, "bulk")) ? GEMV_BULK : (gm && !strcmp(gm, "rows")) ? GEMV_ROWS : GEMV_SPLIT;
+  }
+  if (c->opk == OPK_DENSE && c->gemv_mode == GEMV_SPLIT) {
+    // x strip of 16 KiB in shared memory; whole waves of CTAs (strips × row blocks)
+    // (CCG_SPLIT_KB / CCG_SPLIT_UR / CCG_SPLIT_WAVES: tuning knobs for sweeps)
+    const char* kb = getenv("CCG_SPLIT_KB");
+    const char* ur = getenv("CCG_SPLIT_UR");
+    const char* wv = getenv("CCG_SPLIT_WAVES");
+    const int64_t strip_bytes = kb ? std::max(1, atoi(kb)) * 1024 : 16384;
+    c->split_ur = ur ? atoi(ur) : 8;
+    const int max_waves = wv ? std::max(1, atoi(wv)) : 4;
+    c->split_W = (int)std::min<int64_t>(c->n, strip_bytes / (int64_t)sizeof(C));
+    c->split_strips = (int)((c->n + c->split_W - 1) / c->split_W);
+    int occs = 0;
+    if (c->vec_ok)
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occs, gemv_n_split<T, E::NT, E::SUR, true, false, Store<T>>,
+                                                    NT, (size_t)c->split_W * sizeof(C));
+    else
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occs, gemv_n_split<T, E::NT, E::SUR, false, false, Store<T>>,
+                                                    NT, (size_t)c->split_W * sizeof(C));
+    if (occs < 1) occs = 1;
+    const int64_t slots = (int64_t)c->sm_count * occs;
+    // waves k: row blocks of >= 64 rows (x-strip reuse), CTAs = k·slots
+    int64_t nrb = 1;
+    for (int k = max_waves; k >= 1; --k) {
+      nrb = std::max<int64_t>(1, (k * slots) / c->split_strips);
+      if (c->nloc / nrb >= 64 || k == 1) break;
+    }
+    nrb = std::min<int64_t>(nrb, std::max<int64_t>(1, c->nloc / 8));
+    c->split_nrb = (int)nrb;
+    c->nstage2_grid =
+        (int)std::max<int64_t>(1, std::min<int64_t>((c->nloc + NT - 1) / NT, (int64_t)c->sm_count * 4));
+    size_t need = c->split_strips > 1 ? (size_t)c->split_strips * c->nloc * sizeof(C) : 0;
+    if (need > c->npart_bytes) {
+      if (c->npart) cudaFree(c->npart);
+      c->npart = nullptr;
+      CK(c, cudaMalloc(&c->npart, need));
+      c->npart_bytes = need;
+    }
+  }
   // Aᴴ stage 1: strips of NT*V columns, S row splits, ~ whole waves
   const int V = c->vec_ok ? CT<T>::V : 1;
   const int64_t nv = c->n / V;
@@ -529,7 +626,9 @@ static int choose_launch(ccg_ctx* c) {
     c->hpart_bytes = need_hpart;
   }
   int64_t maxgrid = std::max<int64_t>({(int64_t)c->gemv_grid, (int64_t)c->ah_strips * c->ah_S,
-                                       (int64_t)c->stage2_grid, (int64_t)c->pass_grid, (int64_t)c->spmv_grid});
+                                       (int64_t)c->stage2_grid, (int64_t)c->pass_grid, (int64_t)c->spmv_grid,
+                                       (int64_t)c->split_strips * c->split_nrb, (int64_t)c->nstage2_grid,
+                                       (int64_t)c->bulk_grid});
   size_t need_part = (size_t)maxgrid * 4;
   if (need_part > c->part_cap) {
     if (c->part) cudaFree(c->part);
@@ -914,6 +1013,7 @@ int ccg_destroy(ccg_handle c) {
   for (int i = 0; i < NFULL; ++i) if (c->full[i]) cudaFree(c->full[i]);
   if (c->wfull) cudaFree(c->wfull);
   if (c->hpart) cudaFree(c->hpart);
+  if (c->npart) cudaFree(c->npart);
   if (c->part) cudaFree(c->part);
   if (c->hist) cudaFree(c->hist);
   if (c->st) cudaFree(c->st);

@@ -10,6 +10,7 @@
 // which finish_reduction() turns into the phase's recurrence scalars.
 #pragma once
 #include <type_traits>
+#include "bulk.cuh"
 #include "common.cuh"
 
 namespace ccg {
@@ -109,6 +110,204 @@ gemv_n_kernel(const typename CT<T>::c* __restrict__ A, int64_t lda,
     __syncthreads();
   }
   if constexpr (Epi::K > 0) finish_reduction<KK, NT, Epi>(dacc, red, st);
+}
+
+// ---------------------------------------------------------------------------
+// K1' gemv_n_bulk: the same product with A streamed by the TMA bulk-copy
+// engine into a STAGES-deep shared-memory ring (mbarrier tx-count pipeline),
+// so the bytes in flight do not live in registers.  One CTA per SM
+// (persistent), CTA b owns rows [b·nrows/G, (b+1)·nrows/G), walked in groups
+// of R rows; a tile = R row segments of 4 KiB + the matching 4 KiB of x.
+// Thread t owns the 16-byte column chunk t of every tile and keeps R
+// accumulators; the R row sums are reduced across the CTA once per group.
+// Needs n·sizeof(C) % 4096 == 0, lda·sizeof(C) % 16 == 0 and 16-B aligned A.
+// ---------------------------------------------------------------------------
+constexpr int BULK_TILE = 4096;  // bytes per row segment
+constexpr int BULK_NT = 256;     // threads: 256 x 16 B = one 4 KiB segment
+
+template <int R, int STAGES>
+constexpr size_t bulk_smem_bytes() {
+  return (size_t)STAGES * (R + 1) * BULK_TILE + 2 * STAGES * sizeof(uint64_t) + 128;
+}
+
+template <typename T, int R, int STAGES, class Epi>
+__global__ void __launch_bounds__(BULK_NT, 1)
+gemv_n_bulk(const typename CT<T>::c* __restrict__ A, int64_t lda,
+            const typename CT<T>::c* __restrict__ x, int64_t n, int64_t nrows,
+            Epi epi, Red red, State* st, const int* gate) {
+  using C = typename CT<T>::c;
+  using LV = typename CT<T>::v;
+  constexpr int V = CT<T>::V;
+  constexpr int KK = Epi::K > 0 ? Epi::K : 1;
+  constexpr int TC = BULK_TILE / (int)sizeof(C);   // complex per row segment
+  if (*gate) return;
+  epi.load(st);
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  unsigned char* tiles = smem_raw;                                  // [STAGES][R+1][4096]
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + (size_t)STAGES * (R + 1) * BULK_TILE);
+  uint64_t* empty = full + STAGES;
+  __shared__ C red_sm[BULK_NT / 32][R];
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t rb = nrows * (int64_t)blockIdx.x / gridDim.x;
+  const int64_t re = nrows * ((int64_t)blockIdx.x + 1) / gridDim.x;
+  const int64_t ngroups = (re - rb + R - 1) / R;
+  const int ntiles = (int)(n / TC);
+  const int64_t tot = ngroups * ntiles;
+
+  if (tid == 0) {
+    for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], BULK_NT / 32); }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  uint64_t pol = 0;
+  auto issue = [&](int64_t t) {
+    const int s = (int)(t % STAGES);
+    const int64_t g = t / ntiles;
+    const int ct = (int)(t % ntiles);
+    const int64_t r0 = rb + g * R;
+    const int nr = (int)min((int64_t)R, re - r0);
+    unsigned char* stg = tiles + (size_t)s * (R + 1) * BULK_TILE;
+    mbar_arrive_expect_tx(&full[s], (uint32_t)(nr + 1) * BULK_TILE);
+    for (int r = 0; r < nr; ++r)
+      bulk_g2s(stg + (size_t)r * BULK_TILE, A + (r0 + r) * lda + (int64_t)ct * TC, BULK_TILE, &full[s], pol);
+    bulk_g2s(stg + (size_t)R * BULK_TILE, x + (int64_t)ct * TC, BULK_TILE, &full[s], pol);
+  };
+  if (tid == 0) {
+    pol = policy_evict_first();
+    for (int64_t t = 0; t < tot && t < STAGES; ++t) issue(t);
+  }
+
+  double2 dacc[KK];
+#pragma unroll
+  for (int k = 0; k < KK; ++k) dacc[k] = make_double2(0.0, 0.0);
+  C acc[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) acc[r] = czero<C>();
+
+  for (int64_t t = 0; t < tot; ++t) {
+    const int s = (int)(t % STAGES);
+    const uint32_t ph = (uint32_t)((t / STAGES) & 1);
+    mbar_wait(&full[s], ph);
+    const unsigned char* stg = tiles + (size_t)s * (R + 1) * BULK_TILE;
+    C xc[V];
+    unpack(*reinterpret_cast<const LV*>(stg + (size_t)R * BULK_TILE + tid * 16), xc);
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      C ac[V];
+      unpack(*reinterpret_cast<const LV*>(stg + (size_t)r * BULK_TILE + tid * 16), ac);
+#pragma unroll
+      for (int v = 0; v < V; ++v) cfma(acc[r], ac[v], xc[v]);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+    if (tid == 0 && t + STAGES < tot) {
+      mbar_wait(&empty[s], ph);
+      issue(t + STAGES);
+    }
+    if ((int)(t % ntiles) == ntiles - 1) {
+      // end of a row group: CTA reduction of the R row sums, then epilogue
+      const int64_t r0 = rb + (t / ntiles) * R;
+      const int nr = (int)min((int64_t)R, re - r0);
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          acc[r].x += __shfl_xor_sync(0xffffffffu, acc[r].x, o);
+          acc[r].y += __shfl_xor_sync(0xffffffffu, acc[r].y, o);
+        }
+      }
+      if (lane == 0) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) red_sm[warp][r] = acc[r];
+      }
+      __syncthreads();
+      if (tid < nr) {
+        C sum = red_sm[0][tid];
+#pragma unroll
+        for (int w = 1; w < BULK_NT / 32; ++w) sum = cadd(sum, red_sm[w][tid]);
+        epi(r0 + tid, sum, dacc);
+      }
+      __syncthreads();
+#pragma unroll
+      for (int r = 0; r < R; ++r) acc[r] = czero<C>();
+    }
+  }
+  if constexpr (Epi::K > 0) finish_reduction<KK, BULK_NT, Epi>(dacc, red, st);
+}
+
+// ---------------------------------------------------------------------------
+// K1'' gemv_n_split (default A·x): column strips × row blocks.  CTA (c, b)
+// stages the x strip [c·W, c·W + W) in shared memory once, then each warp
+// streams whole row segments of its rows (lanes 16 B apart, UR independent
+// 16-byte loads in flight per lane, ~40 registers => 8 CTAs/SM, >200 KB of
+// loads in flight per SM) and warp-reduces each row.  With one strip the row
+// sum is final and the epilogue runs here (FUSED); otherwise the partial
+// goes to part[c][i] and gemv_h_stage2 sums the strips in order (fixed
+// order => deterministic) and runs the epilogue.
+// ---------------------------------------------------------------------------
+template <typename T, int NT, int UR, bool VEC, bool FUSED, class Epi>
+__global__ void __launch_bounds__(NT)
+gemv_n_split(const typename CT<T>::c* __restrict__ A, int64_t lda,
+             const typename CT<T>::c* __restrict__ x, int64_t n, int64_t nrows, int W,
+             typename CT<T>::c* __restrict__ part, Epi epi, Red red, State* st, const int* gate) {
+  using C = typename CT<T>::c;
+  constexpr int V = VEC ? CT<T>::V : 1;
+  using LV = typename std::conditional<VEC, typename CT<T>::v, C>::type;
+  constexpr int KK = Epi::K > 0 ? Epi::K : 1;
+  if (*gate) return;
+  if constexpr (FUSED) epi.load(st);
+  extern __shared__ __align__(16) unsigned char xs_raw[];
+  C* xs = reinterpret_cast<C*>(xs_raw);
+  const int strip = blockIdx.x, nrb = gridDim.y, b = blockIdx.y;
+  const int64_t c0 = (int64_t)strip * W;
+  const int cw = (int)min((int64_t)W, n - c0);
+  for (int t = threadIdx.x; t < cw; t += NT) xs[t] = x[c0 + t];
+  __syncthreads();
+  const int64_t i0 = nrows * b / nrb, i1 = nrows * (b + 1) / nrb;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nvec = cw / V;
+  const LV* xv = reinterpret_cast<const LV*>(xs);
+  double2 dacc[KK];
+#pragma unroll
+  for (int k = 0; k < KK; ++k) dacc[k] = make_double2(0.0, 0.0);
+  for (int64_t i = i0 + warp; i < i1; i += NT / 32) {
+    const LV* a = reinterpret_cast<const LV*>(A + i * lda + c0);
+    C acc = czero<C>();
+    int k = lane;
+    for (; k + 32 * (UR - 1) < nvec; k += 32 * UR) {
+      LV av[UR];
+#pragma unroll
+      for (int u = 0; u < UR; ++u) av[u] = ld_stream(a + k + 32 * u);
+#pragma unroll
+      for (int u = 0; u < UR; ++u) {
+        C ac[V], xc[V];
+        unpack(av[u], ac);
+        unpack(xv[k + 32 * u], xc);
+#pragma unroll
+        for (int v = 0; v < V; ++v) cfma(acc, ac[v], xc[v]);
+      }
+    }
+    for (; k < nvec; k += 32) {
+      C ac[V], xc[V];
+      unpack(ld_stream(a + k), ac);
+      unpack(xv[k], xc);
+#pragma unroll
+      for (int v = 0; v < V; ++v) cfma(acc, ac[v], xc[v]);
+    }
+    if (VEC && (cw % V) && lane == 0) cfma(acc, A[i * lda + c0 + cw - 1], xs[cw - 1]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
+      acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+    }
+    if (lane == 0) {
+      if constexpr (FUSED) epi(i, acc, dacc);
+      else part[(int64_t)strip * nrows + i] = acc;
+    }
+  }
+  if constexpr (FUSED && Epi::K > 0) finish_reduction<KK, NT, Epi>(dacc, red, st);
 }
 
 // ---------------------------------------------------------------------------
