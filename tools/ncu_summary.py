@@ -68,12 +68,16 @@ def main():
     for rep in sorted(glob.glob(os.path.join(src, "prof_*.ncu-rep"))):
         name = os.path.basename(rep)[:-8]
         out = report(rep, os.path.join(dst, name + ".txt"))
+        def nbytes(s):
+            parts = s.split()
+            unit = parts[1] if len(parts) > 1 else "byte"
+            return float(parts[0]) * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1)
+
         for o in out:
-            rd = float(o["dram__bytes_read.sum"].split()[0])
-            wr = float(o["dram__bytes_write.sum"].split()[0])
-            unit = o["dram__bytes_read.sum"].split()[1] if len(o["dram__bytes_read.sum"].split()) > 1 else "B"
-            scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "B": 1}.get(unit, 1)
-            traffic[name] = {"kernel": o["kernel"][:120], "dram_bytes_per_launch": (rd + wr) * scale,
+            rd = nbytes(o["dram__bytes_read.sum"])
+            wr = nbytes(o["dram__bytes_write.sum"])
+            traffic[name] = {"kernel": o["kernel"][:120], "dram_bytes_per_launch": rd + wr,
+                             "dram_read": rd, "dram_write": wr,
                              "duration": o["gpu__time_duration.sum"]}
     if "prof_gemv" in traffic:
         t = dict(traffic["prof_gemv"])
