@@ -130,6 +130,17 @@ int ccg_get_unique_id(uint8_t id[128]);
 int ccg_create(ccg_handle* h, ccg_dtype dt, int64_t n, int world, int rank,
                const uint8_t* nccl_id, int device, void* cuda_stream);
 
+/* Validation hook for the sharded path on ONE GPU: creates `world` (≥ 2)
+ * handles hs[0..world-1] for ranks 0..world-1 of an n×n system on `device`,
+ * wired to an in-process loopback communicator instead of NCCL (every
+ * collective becomes a host-side barrier plus device-to-device copies, so no
+ * kernel waits on another rank).  Each handle must be driven by its own host
+ * thread, all calling the same collective functions in the same order.  The
+ * handles are otherwise identical to ccg_create(..., world, rank, ...) ones
+ * (same kernels, same row ownership); each is released with ccg_destroy.
+ * On error no handle is left allocated. */
+int ccg_create_loopback_group(ccg_handle* hs, int world, ccg_dtype dt, int64_t n, int device);
+
 /* Dense operator (matvec + cmatvec of a row-major matrix; P:95 [§5]).
  *   A_local : DEVICE pointer to this rank's rows, row-major, nloc × n with
  *             leading dimension lda ≥ n (elements).  Borrowed: the caller keeps

@@ -30,7 +30,8 @@ ERRORS = {0: "CCG_OK", -1: "CCG_E_ARG", -2: "CCG_E_DIM", -3: "CCG_E_CAPABILITY",
           -4: "CCG_E_STATE", -5: "CCG_E_CUDA", -6: "CCG_E_NCCL", -7: "CCG_E_OOM"}
 
 # every symbol include/ccg.h declares (checked by tests/test_abi.py)
-EXPORTS = ("ccg_get_unique_id", "ccg_create", "ccg_set_matvec_dense", "ccg_set_matvec_csr",
+EXPORTS = ("ccg_get_unique_id", "ccg_create", "ccg_create_loopback_group",
+           "ccg_set_matvec_dense", "ccg_set_matvec_csr",
            "ccg_apply", "ccg_solve", "ccg_get_history", "ccg_set_timing", "ccg_get_timing",
            "ccg_last_launch_count", "ccg_get_stream", "ccg_last_error", "ccg_destroy",
            "ccg_version")
@@ -78,6 +79,8 @@ def load():
         "ccg_get_unique_id": (ctypes.c_int, [ctypes.c_char_p]),
         "ccg_create": (ctypes.c_int, [ctypes.POINTER(vp), ctypes.c_int, i64, ctypes.c_int,
                                       ctypes.c_int, ctypes.c_char_p, ctypes.c_int, vp]),
+        "ccg_create_loopback_group": (ctypes.c_int, [ctypes.POINTER(vp), ctypes.c_int, ctypes.c_int,
+                                                     i64, ctypes.c_int]),
         "ccg_set_matvec_dense": (ctypes.c_int, [vp, vp, i64, i64, i64, u32]),
         "ccg_set_matvec_csr": (ctypes.c_int, [vp, vp, vp, vp, i64, i64, i64, u32]),
         "ccg_apply": (ctypes.c_int, [vp, ctypes.c_int, vp, vp]),
@@ -158,6 +161,16 @@ def ccg_create(dtype, n, world=1, rank=0, nccl_id=None, device=0, stream=None):
     _check(None, rc)
     _keepalive[h.value] = []
     return h.value
+
+
+def ccg_create_loopback_group(world, dtype, n, device=0):
+    """`world` handles sharing an in-process loopback communicator (one GPU)."""
+    hs = (ctypes.c_void_p * world)()
+    _check(None, load().ccg_create_loopback_group(hs, int(world), _dtype_code(dtype), int(n), int(device)))
+    out = [hs[r] for r in range(world)]
+    for h in out:
+        _keepalive[h] = []
+    return out
 
 
 def ccg_set_matvec_dense(h, A, row0, nloc, lda=None, flags=0):

@@ -22,62 +22,12 @@
 #include "common.cuh"
 #include "matvec.cuh"
 #include "methods.cuh"
-#include "nccl.h"
+#include "comm.cuh"
 
 using namespace ccg;
 
-// ===========================================================================
-// NCCL, loaded on demand (only world > 1 needs it)
-// ===========================================================================
 namespace {
-struct NcclApi {
-  bool loaded = false;
-  std::string err;
-  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
-  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
-  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
-  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
-  ncclResult_t (*ReduceScatter)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
-                                cudaStream_t) = nullptr;
-  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
-  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
-  ncclResult_t (*GroupStart)() = nullptr;
-  ncclResult_t (*GroupEnd)() = nullptr;
-  const char* (*GetErrorString)(ncclResult_t) = nullptr;
-};
-NcclApi g_nccl;
-
-bool nccl_load() {
-  if (g_nccl.loaded) return true;
-  void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
-  if (!h) {
-    const char* p = getenv("CCG_NCCL_LIB");
-    if (p) h = dlopen(p, RTLD_NOW | RTLD_GLOBAL);
-  }
-  if (!h) { g_nccl.err = "cannot dlopen libnccl.so.2 (set CCG_NCCL_LIB)"; return false; }
-#define LOADSYM(field, name)                                              \
-  g_nccl.field = reinterpret_cast<decltype(g_nccl.field)>(dlsym(h, name)); \
-  if (!g_nccl.field) { g_nccl.err = std::string("missing NCCL symbol ") + name; return false; }
-  LOADSYM(GetUniqueId, "ncclGetUniqueId");
-  LOADSYM(CommInitRank, "ncclCommInitRank");
-  LOADSYM(CommDestroy, "ncclCommDestroy");
-  LOADSYM(AllGather, "ncclAllGather");
-  LOADSYM(ReduceScatter, "ncclReduceScatter");
-  LOADSYM(Send, "ncclSend");
-  LOADSYM(Recv, "ncclRecv");
-  LOADSYM(GroupStart, "ncclGroupStart");
-  LOADSYM(GroupEnd, "ncclGroupEnd");
-  LOADSYM(GetErrorString, "ncclGetErrorString");
-#undef LOADSYM
-  g_nccl.loaded = true;
-  return true;
-}
-
 thread_local std::string g_create_err;
-
-struct Err {
-  int code;
-};
 }  // namespace
 
 // ===========================================================================
@@ -130,7 +80,7 @@ struct ccg_ctx {
   void* stage_in = nullptr;  // pinned staging (host pointer I/O)
   size_t stage_bytes = 0;
   // comm
-  ncclComm_t comm = nullptr;
+  Comm* comm = nullptr;  // NcclComm or LoopbackComm (world > 1)
   // graphs per method
   cudaGraphExec_t gexec[5] = {};
   int64_t graph_launches_per_iter[5] = {};
@@ -164,13 +114,13 @@ struct ccg_ctx {
     }                                                                                      \
   } while (0)
 
-#define NK(c, call)                                                                        \
-  do {                                                                                     \
-    ncclResult_t r_ = (call);                                                              \
-    if (r_ != ncclSuccess) {                                                               \
-      (c)->err = std::string(#call) + ": " + g_nccl.GetErrorString(r_);                    \
-      return CCG_E_NCCL;                                                                   \
-    }                                                                                      \
+#define NK(c, call)                 \
+  do {                              \
+    int r_ = (call);                \
+    if (r_ != 0) {                  \
+      (c)->err = (c)->comm->err;    \
+      return r_;                    \
+    }                               \
   } while (0)
 
 #define TRY(expr)            \
@@ -247,29 +197,18 @@ struct Engine {
   static C* F(ccg_ctx* c, int i) { return reinterpret_cast<C*>(c->full[i]); }
   static C* Fs(ccg_ctx* c, int i) { return reinterpret_cast<C*>(c->full[i]) + c->row0; }  // own slice
 
-  static ncclDataType_t ndt() { return sizeof(T) == 4 ? ncclFloat32 : ncclFloat64; }
+  static CommType ndt() { return sizeof(T) == 4 ? CT_F32 : CT_F64; }
 
   // -------------------- collectives --------------------
   static int allgather(ccg_ctx* c, int fi) {
     if (c->world == 1) return CCG_OK;
     C* buf = F(c, fi);
     if (c->opk == OPK_CSR) return halo_exchange(c, buf);
-    NK(c, g_nccl.AllGather(buf + c->row0, buf, (size_t)c->nloc * 2, ndt(), c->comm, c->stream));
+    NK(c, c->comm->allgather_inplace(buf, (size_t)c->nloc * 2, ndt(), c->stream));
     return CCG_OK;
   }
   static int halo_exchange(ccg_ctx* c, C* buf) {
-    const int64_t h = c->halo;
-    if (h == 0) return CCG_OK;
-    NK(c, g_nccl.GroupStart());
-    if (c->rank > 0) {
-      NK(c, g_nccl.Send(buf + c->row0, (size_t)h * 2, ndt(), c->rank - 1, c->comm, c->stream));
-      NK(c, g_nccl.Recv(buf + c->row0 - h, (size_t)h * 2, ndt(), c->rank - 1, c->comm, c->stream));
-    }
-    if (c->rank < c->world - 1) {
-      NK(c, g_nccl.Send(buf + c->row0 + c->nloc - h, (size_t)h * 2, ndt(), c->rank + 1, c->comm, c->stream));
-      NK(c, g_nccl.Recv(buf + c->row0 + c->nloc, (size_t)h * 2, ndt(), c->rank + 1, c->comm, c->stream));
-    }
-    NK(c, g_nccl.GroupEnd());
+    NK(c, c->comm->halo(buf, c->row0, c->nloc, c->halo, sizeof(C), ndt(), c->stream));
     return CCG_OK;
   }
   // scalar phase for world > 1: allgather this rank's K sums, sum in rank order
@@ -278,7 +217,7 @@ struct Engine {
     constexpr int K = Fin::K;
     if constexpr (K > 0) {
       if (c->world > 1) {
-        NK(c, g_nccl.AllGather(c->rank_sum, c->all_sums, (size_t)K * 2, ncclFloat64, c->comm, c->stream));
+        NK(c, c->comm->allgather(c->rank_sum, c->all_sums, (size_t)K * 2, CT_F64, c->stream));
         scalar_kernel<K, Fin><<<1, 1, 0, c->stream>>>(c->all_sums, c->world, c->st, gate);
         c->launches++;
       }
@@ -411,7 +350,7 @@ struct Engine {
     tev_end(c);
     CK(c, cudaGetLastError());
     C* wl = L(c, NLOCAL - 1);
-    NK(c, g_nccl.ReduceScatter(c->wfull, wl, (size_t)c->nloc * 2, ndt(), ncclSum, c->comm, c->stream));
+    NK(c, c->comm->reduce_scatter(c->wfull, wl, (size_t)c->nloc * 2, ndt(), c->stream));
     EpiPass<C, Epi> ep{epi, wl};
     return pass(c, ep, gate);
   }
@@ -661,7 +600,7 @@ static int run_iterations(ccg_ctx* c, int m, int maxit) {
   };
   TRY(read_done());
   if (done) return CCG_OK;
-  if (c->timing) {
+  if (c->timing || (c->comm && !c->comm->graph_safe)) {
     for (int k = 0; k < maxit && !done; ++k) {
       TRY(E::iter(c, m));
       TRY(read_done());
@@ -715,14 +654,14 @@ int ccg_get_unique_id(uint8_t id[128]) {
   return CCG_OK;
 }
 
-int ccg_create(ccg_handle* h, ccg_dtype dt, int64_t n, int world, int rank, const uint8_t* nccl_id, int device,
-               void* cuda_stream) {
+static int create_impl(ccg_handle* h, ccg_dtype dt, int64_t n, int world, int rank, const uint8_t* nccl_id,
+                       int device, void* cuda_stream, LoopbackGroup* lg) {
   if (!h) { g_create_err = "h is NULL"; return CCG_E_ARG; }
   *h = nullptr;
   if (dt != CCG_C64 && dt != CCG_C128) { g_create_err = "bad dtype"; return CCG_E_ARG; }
   if (n < 1 || world < 1 || rank < 0 || rank >= world) { g_create_err = "bad n/world/rank"; return CCG_E_ARG; }
   if (n % world != 0) { g_create_err = "n must be divisible by world"; return CCG_E_DIM; }
-  if (world > 1 && !nccl_id) { g_create_err = "nccl_id required for world > 1"; return CCG_E_ARG; }
+  if (world > 1 && !nccl_id && !lg) { g_create_err = "nccl_id required for world > 1"; return CCG_E_ARG; }
   int ndev = 0;
   cudaError_t e = cudaGetDeviceCount(&ndev);
   if (e != cudaSuccess || ndev == 0) {
@@ -781,15 +720,50 @@ int ccg_create(ccg_handle* h, ccg_dtype dt, int64_t n, int world, int rank, cons
   }
   if (world > 1) {
     CKC(cudaMalloc(&c->wfull, (size_t)n * c->esz));
-    if (!nccl_load()) { c->err = g_nccl.err; return bail(CCG_E_NCCL); }
-    ncclUniqueId u;
-    memcpy(u.internal, nccl_id, 128);
-    ncclResult_t r = g_nccl.CommInitRank(&c->comm, world, u, rank);
-    if (r != ncclSuccess) { c->err = std::string("ncclCommInitRank: ") + g_nccl.GetErrorString(r); return bail(CCG_E_NCCL); }
+    if (lg) {
+      {
+        std::lock_guard<std::mutex> lk(lg->m);
+        lg->refs++;
+      }
+      c->comm = new LoopbackComm(lg, rank);
+    } else {
+      NcclComm* nc = new NcclComm();
+      c->comm = nc;
+      int rc = nc->init(world, rank, nccl_id);
+      if (rc) { c->err = nc->err; return bail(CCG_E_NCCL); }
+    }
   }
 #undef CKC
   *h = c;
   return CCG_OK;
+}
+
+int ccg_create(ccg_handle* h, ccg_dtype dt, int64_t n, int world, int rank, const uint8_t* nccl_id, int device,
+               void* cuda_stream) {
+  return create_impl(h, dt, n, world, rank, nccl_id, device, cuda_stream, nullptr);
+}
+
+int ccg_create_loopback_group(ccg_handle* hs, int world, ccg_dtype dt, int64_t n, int device) {
+  if (!hs || world < 2) { g_create_err = "hs is NULL or world < 2"; return CCG_E_ARG; }
+  LoopbackGroup* lg = new LoopbackGroup(world);
+  lg->refs = 1;  // held until every handle exists
+  int rc = CCG_OK;
+  int made = 0;
+  for (int r = 0; r < world; ++r) {
+    rc = create_impl(&hs[r], dt, n, world, r, nullptr, device, nullptr, lg);
+    if (rc) break;
+    made++;
+  }
+  if (rc) {
+    for (int r = 0; r < made; ++r) ccg_destroy(hs[r]);
+  }
+  bool last = false;
+  {
+    std::lock_guard<std::mutex> lk(lg->m);
+    last = (--lg->refs == 0);
+  }
+  if (last) delete lg;
+  return rc;
 }
 
 int ccg_set_matvec_dense(ccg_handle c, const void* A_local, int64_t row0, int64_t nloc, int64_t lda, uint32_t flags) {
@@ -839,8 +813,8 @@ int ccg_set_matvec_csr(ccg_handle c, const int32_t* rowptr, const int32_t* colin
     int64_t* dh = nullptr;
     CK(c, cudaMalloc(&dh, sizeof(int64_t) * c->world));
     CK(c, cudaMemcpy(dh + c->rank, &halo, sizeof(int64_t), cudaMemcpyHostToDevice));
-    ncclResult_t r = g_nccl.AllGather(dh + c->rank, dh, 1, ncclInt64, c->comm, c->stream);
-    if (r != ncclSuccess) { cudaFree(dh); FAIL(c, CCG_E_NCCL, g_nccl.GetErrorString(r)); }
+    int r = c->comm->allgather(dh + c->rank, dh, 1, CT_I64, c->stream);
+    if (r) { cudaFree(dh); FAIL(c, r, c->comm->err); }
     std::vector<int64_t> hs(c->world);
     CK(c, cudaStreamSynchronize(c->stream));
     CK(c, cudaMemcpy(hs.data(), dh, sizeof(int64_t) * c->world, cudaMemcpyDeviceToHost));
@@ -1008,7 +982,8 @@ int ccg_destroy(ccg_handle c) {
   if (c->stream) cudaStreamSynchronize(c->stream);
   invalidate_graphs(c);
   for (auto e : c->ev) cudaEventDestroy(e);
-  if (c->comm && g_nccl.loaded) g_nccl.CommDestroy(c->comm);
+  delete c->comm;
+  c->comm = nullptr;
   for (int i = 0; i < NLOCAL; ++i) if (c->loc[i]) cudaFree(c->loc[i]);
   for (int i = 0; i < NFULL; ++i) if (c->full[i]) cudaFree(c->full[i]);
   if (c->wfull) cudaFree(c->wfull);

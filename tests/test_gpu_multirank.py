@@ -1,0 +1,179 @@
+"""The row-sharded multi-rank path on ONE GPU (loopback communicator).
+
+ccg_create_loopback_group wires G handles (ranks) to an in-process
+communicator: the collectives of the NCCL path (allgather of GEMV inputs,
+reduce-scatter of Aᴴ partials, allgather of scalar partial sums, CSR halo
+exchange) become host barriers + device copies, so the exact sharded code
+path — row ownership, slice offsets, halo maps, rank-ordered scalar sums —
+runs with the real sm_100a kernels, one host thread per rank, and no kernel
+waits on another rank.  Checked against the oracle and the 1-rank result.
+"""
+
+import threading
+
+import numpy as np
+import pytest
+
+import paper_1208_4869_b200 as ccg
+import oracle
+from oracle import DenseOp, CsrOp
+from oracle.operators import reference_apply
+from oracle.envelope import iteration_envelope, x_spread
+from workloads import cfg1, cfg2, dense_random, helmholtz_csr, helmholtz_rhs
+from tests._gpu import to_dev, relerr, XTOL, TOL, Dense
+
+pytestmark = pytest.mark.gpu
+
+
+def _threads(G, fn):
+    out, errs = [None] * G, []
+
+    def run(r):
+        try:
+            out[r] = fn(r)
+        except Exception as e:  # pragma: no cover - surfaced below
+            errs.append((r, e))
+    ts = [threading.Thread(target=run, args=(r,)) for r in range(G)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join(timeout=600)
+    assert not errs, errs
+    return out
+
+
+class DenseGroup:
+    def __init__(self, A, G):
+        self.n = A.shape[0]
+        self.G = G
+        self.nloc = self.n // G
+        self.dtype = A.dtype.type
+        self.dt = "c64" if self.dtype == np.complex64 else "c128"
+        self.hs = ccg.ccg_create_loopback_group(G, self.dt, self.n)
+        self.parts = [to_dev(A[r * self.nloc:(r + 1) * self.nloc]) for r in range(G)]
+        for r in range(G):
+            ccg.ccg_set_matvec_dense(self.hs[r], self.parts[r], r * self.nloc, self.nloc, lda=self.n)
+
+    def _sl(self, v, r):
+        return to_dev(np.ascontiguousarray(v[r * self.nloc:(r + 1) * self.nloc]).astype(self.dtype))
+
+    def apply(self, x, op="A"):
+        def f(r):
+            xd = self._sl(x, r)
+            y = xd.clone()
+            ccg.ccg_apply(self.hs[r], op, xd, y)
+            return y.cpu().numpy()
+        return np.concatenate(_threads(self.G, f))
+
+    def solve(self, method, y, tol, maxit):
+        def f(r):
+            yd = self._sl(y, r)
+            x = yd.clone()
+            res = ccg.ccg_solve(self.hs[r], method, None, yd, x, tol, maxit)
+            res["x"] = x.cpu().numpy()
+            return res
+        rs = _threads(self.G, f)
+        for k in ("status", "iterations", "matvecs_a", "matvecs_ah", "true_rel_res", "rec_rel_res"):
+            assert all(r[k] == rs[0][k] for r in rs), (k, [r[k] for r in rs])   # every rank agrees
+        out = dict(rs[0])
+        out["x"] = np.concatenate([r["x"] for r in rs])
+        return out
+
+    def close(self):
+        for h in self.hs:
+            ccg.ccg_destroy(h)
+
+
+class CsrGroup(DenseGroup):
+    def __init__(self, N, G, flags=0):
+        self.n = N ** 3
+        self.G = G
+        self.nloc = self.n // G
+        self.dtype = np.complex128
+        self.hs = ccg.ccg_create_loopback_group(G, "c128", self.n)
+        zs = N // G
+        self.keep = []
+        parts = [helmholtz_csr(N, kh=10 / 128, z0=r * zs, z1=(r + 1) * zs) for r in range(G)]
+
+        def f(r):
+            rp, ci, v = (to_dev(a) for a in parts[r])
+            self.keep.append((rp, ci, v))
+            ccg.ccg_set_matvec_csr(self.hs[r], rp, ci, v, r * self.nloc, self.nloc, len(parts[r][2]),
+                                   flags=flags)
+        _threads(G, f)   # set_matvec_csr agrees on the halo width collectively
+
+
+@pytest.mark.parametrize("G", [2, 4])
+@pytest.mark.parametrize("dtype", [np.complex128, np.complex64])
+def test_sharded_dense_apply(G, dtype):
+    n = 2048
+    A = dense_random(n, seed=G, dtype=dtype, shift=1.5)
+    x = (np.random.default_rng(1).standard_normal(n) + 1j).astype(dtype)
+    g = DenseGroup(A, G)
+    try:
+        for op in ("A", "AH", "AT"):
+            assert relerr(g.apply(x, op), reference_apply(A, x, op)) <= TOL[dtype], op
+    finally:
+        g.close()
+
+
+@pytest.mark.parametrize("G", [2, 4])
+@pytest.mark.parametrize("method", ["bicgstab", "cgne", "qmr", "bicor", "cors"])
+def test_sharded_cfg1_solve(G, method):
+    A, y = cfg1()
+    g = DenseGroup(A, G)
+    try:
+        o = oracle.solve(method, DenseOp(A), y, 1e-10, 500)
+        r = g.solve(method, y, 1e-10, 500)
+        assert r["status"] == "CONVERGED" and abs(r["iterations"] - o.iterations) <= 2
+        assert (r["matvecs_a"], r["matvecs_ah"]) == (o.matvecs_a, o.matvecs_ah)
+        k = min(r["iterations"], o.iterations)
+        re_ = g.solve(method, y, 0.0, k)
+        oe = oracle.solve(method, DenseOp(A), y, 0.0, k)
+        assert relerr(re_["x"], oe.x) <= XTOL[np.complex128]
+        with Dense(A) as h1:                   # and the 1-rank path
+            one = h1.solve(method, y, 1e-10, 500)
+        assert abs(one["iterations"] - r["iterations"]) <= 2
+    finally:
+        g.close()
+
+
+@pytest.mark.parametrize("method", ["bicgstab", "qmr", "bicor"])
+def test_sharded_cfg2_solve(method):
+    A, y = cfg2()
+    g = DenseGroup(A, 2)
+    try:
+        o = oracle.solve(method, DenseOp(A), y, 1e-8, 1000)
+        r = g.solve(method, y, 1e-8, 1000)
+        assert r["status"] == "CONVERGED" and abs(r["iterations"] - o.iterations) <= 2
+        k = min(r["iterations"], o.iterations)
+        assert relerr(g.solve(method, y, 0.0, k)["x"], oracle.solve(method, DenseOp(A), y, 0.0, k).x) <= 1e-9
+    finally:
+        g.close()
+
+
+@pytest.mark.parametrize("G", [2, 4])
+def test_sharded_csr_apply_and_solve(G):
+    N = 16
+    g = CsrGroup(N, G)
+    rp, ci, v = helmholtz_csr(N, kh=10 / 128)
+    op = CsrOp(rp, ci, v)
+    try:
+        x = np.random.default_rng(3).standard_normal(N ** 3) + 1j
+        assert relerr(g.apply(x, "A"), reference_apply(op, x)) <= 1e-13
+        y = helmholtz_rhs(N)
+        for method in ("bicgstab", "cors"):
+            r = g.solve(method, y, 1e-8, 2000)
+            assert r["status"] == "CONVERGED" and r["true_rel_res"] <= 1e-7
+            k0, kmin, kmax = iteration_envelope(method, op, y, 1e-8, 2000)
+            assert kmin - 2 <= r["iterations"] <= kmax + 2, (method, r["iterations"], kmin, kmax)
+            k = min(r["iterations"], k0)
+            xc, D = x_spread(method, op, y, k)
+            assert relerr(g.solve(method, y, 0.0, k)["x"], xc) <= max(1e-9, 2 * D)
+        # CSR Aᴴ is single-GPU only
+        xd = to_dev(x[:g.nloc].astype(np.complex128))
+        with pytest.raises(ccg.CcgError) as e:
+            ccg.ccg_apply(g.hs[0], "AH", xd, xd.clone())   # refused before any collective
+        assert e.value.code == -3
+    finally:
+        g.close()
