@@ -76,8 +76,12 @@ class _NonFinite(Exception):
 class _Ctx:
     """Per-solve scalar policy: keeps every scalar in the working precision."""
 
-    def __init__(self, y):
+    def __init__(self, y, dots=None):
         self.obj = (y.dtype == object)
+        # inner products (replaceable by a sharded implementation, oracle/sharded.py)
+        self.dotc = dots.dotc if dots is not None else dotc
+        self.dotu = dots.dotu if dots is not None else dotu
+        self.norm_sq = dots.norm_sq if dots is not None else norm_sq
         if not self.obj:
             self.ctype = y.dtype.type                       # complex64/128
             self.rtype = np.finfo(y.dtype).dtype.type       # float32/64
@@ -124,10 +128,10 @@ def _finish(op, y, res, r0sq, tol, ctx):
     if op is not None:                       # not counted as work
         op.n_a -= 1
     if ctx.obj:
-        tr = float(norm_sq(rt)) ** 0.5
+        tr = float(ctx.norm_sq(rt)) ** 0.5
         r0 = float(r0sq) ** 0.5
     else:
-        tr = float(np.linalg.norm(rt.astype(np.complex128)))
+        tr = float(np.sqrt(np.float64(ctx.norm_sq(rt.astype(np.complex128)))))
         r0 = float(np.sqrt(np.float64(r0sq)))
     res.true_rel_res = tr / r0 if r0 > 0 else 0.0
     if res.history:
@@ -141,13 +145,13 @@ def _finish(op, y, res, r0sq, tol, ctx):
     return res
 
 
-def _run(body, op, y, tol, maxit, x0, **kw):
+def _run(body, op, y, tol, maxit, x0, dots=None, **kw):
     """Shared driver: setup, r0 check, exception → status mapping, finalize."""
     y = np.asarray(y)
-    ctx = _Ctx(y)
+    ctx = _Ctx(y, dots)
     op.reset_counts()
     x, r = _init(op, y, x0)
-    r0sq = norm_sq(r)
+    r0sq = ctx.norm_sq(r)
     tol2 = tol * tol
     hist = [sqrt(r0sq)]
     state = {"x": x, "k": 0}
@@ -183,7 +187,7 @@ def _bicgstab(op, y, x, r, r0sq, tol2, maxit, ctx, hist, st, shadow=None):
     p = v = None
     for k in range(1, maxit + 1):
         st["k"] = k
-        rho = ctx.c(dotc(rt, r))                               # ρ = ⟨r̃, r⟩
+        rho = ctx.c(ctx.dotc(rt, r))                               # ρ = ⟨r̃, r⟩
         ctx.check(rho)
         if rho == 0:
             raise _Breakdown("rho")
@@ -193,24 +197,24 @@ def _bicgstab(op, y, x, r, r0sq, tol2, maxit, ctx, hist, st, shadow=None):
             beta = ctx.c((rho / rho_prev) * (alpha / omega))
             p = r + beta * (p - omega * v)                      # p = r + β(p − ωv)
         v = op.apply(p)                                         # v = A p
-        sigma = ctx.c(dotc(rt, v))                              # σ = ⟨r̃, v⟩
+        sigma = ctx.c(ctx.dotc(rt, v))                              # σ = ⟨r̃, v⟩
         alpha = ctx.c(ctx.div(rho, sigma, "sigma"))             # α = ρ/σ
         s = r - alpha * v                                       # s = r − αv
-        ss = ctx.r(norm_sq(s))
+        ss = ctx.r(ctx.norm_sq(s))
         ctx.check(ss)
         if _conv(ss, tol2, r0sq):                               # half-step exit (Q4)
             st["x"] = x = x + alpha * p
             hist.append(sqrt(ss))
             return CONVERGED, k, True
         t = op.apply(s)                                         # t = A s
-        tt = ctx.r(norm_sq(t))
-        ts = ctx.c(dotc(t, s))
+        tt = ctx.r(ctx.norm_sq(t))
+        ts = ctx.c(ctx.dotc(t, s))
         omega = ctx.c(ctx.div(ts, tt, "tt"))                    # ω = ⟨t,s⟩/⟨t,t⟩
         if omega == 0:
             raise _Breakdown("omega")
         st["x"] = x = x + alpha * p + omega * s                 # x += αp + ωs
         r = s - omega * t                                       # r = s − ωt
-        rr = ctx.r(norm_sq(r))
+        rr = ctx.r(ctx.norm_sq(r))
         ctx.check(rr)
         hist.append(sqrt(rr))
         if _conv(rr, tol2, r0sq):
@@ -227,12 +231,12 @@ def _cgne(op, y, x, r, r0sq, tol2, maxit, ctx, hist, st):
     rho = ctx.r(r0sq)                                           # ρ = ‖r‖²
     for k in range(1, maxit + 1):
         st["k"] = k
-        pi = ctx.r(norm_sq(p))                                  # π = ‖p‖²
+        pi = ctx.r(ctx.norm_sq(p))                                  # π = ‖p‖²
         alpha = ctx.r(ctx.div(rho, pi, "pi"))                   # α = ρ/π
         st["x"] = x = x + alpha * p                             # x += αp
         q = op.apply(p)
         r = r - alpha * q                                       # r −= α A p
-        rho_new = ctx.r(norm_sq(r))
+        rho_new = ctx.r(ctx.norm_sq(r))
         ctx.check(rho_new)
         hist.append(sqrt(rho_new))
         if _conv(rho_new, tol2, r0sq):
@@ -252,14 +256,14 @@ def _cgne(op, y, x, r, r0sq, tol2, maxit, ctx, hist, st):
 # ---------------------------------------------------------------------------
 def _qmr(op, y, x, r, r0sq, tol2, maxit, ctx, hist, st, form="H", shadow=None):
     if form == "H":
-        ip, adj, cj = dotc, op.apply_h, (lambda z: z.conjugate())
+        ip, adj, cj = ctx.dotc, op.apply_h, (lambda z: z.conjugate())
         wt = r.copy() if shadow is None else np.asarray(shadow, dtype=y.dtype)
     else:
-        ip, adj, cj = dotu, op.apply_t, (lambda z: z)
+        ip, adj, cj = ctx.dotu, op.apply_t, (lambda z: z)
         wt = np.conj(r) if shadow is None else np.asarray(shadow, dtype=y.dtype)
     vt = r.copy()                                               # ṽ = r
-    rho = ctx.r(sqrt(norm_sq(vt)))                              # ρ = ‖ṽ‖
-    xi = ctx.r(sqrt(norm_sq(wt)))                               # ξ = ‖w̃‖
+    rho = ctx.r(sqrt(ctx.norm_sq(vt)))                              # ρ = ‖ṽ‖
+    xi = ctx.r(sqrt(ctx.norm_sq(wt)))                               # ξ = ‖w̃‖
     gamma_prev = ctx.r(1)
     eta = ctx.c(-1)
     theta_prev = ctx.r(0)
@@ -292,9 +296,9 @@ def _qmr(op, y, x, r, r0sq, tol2, maxit, ctx, hist, st, form="H", shadow=None):
         if beta == 0:
             raise _Breakdown("beta")
         vt = pt - beta * v                                      # ṽ = p̃ − βv
-        rho_next = ctx.r(sqrt(norm_sq(vt)))
+        rho_next = ctx.r(sqrt(ctx.norm_sq(vt)))
         wt = adj(q) - ctx.c(cj(beta)) * w                       # w̃ = Aᴴq − conj(β)w
-        xi_next = ctx.r(sqrt(norm_sq(wt)))
+        xi_next = ctx.r(sqrt(ctx.norm_sq(wt)))
         theta = ctx.r(rho_next / (gamma_prev * abs(beta)))      # θ = ρ'/(γ_prev|β|)
         gamma = ctx.r(1 / sqrt(1 + theta * theta))              # γ = 1/√(1+θ²)
         ctx.check(theta, gamma)
@@ -311,7 +315,7 @@ def _qmr(op, y, x, r, r0sq, tol2, maxit, ctx, hist, st, form="H", shadow=None):
             s = eta * pt + c2 * s                               # s = ηp̃ + (θ_prev γ)² s
         st["x"] = x = x + d                                     # x += d
         r = r - s                                               # r −= s
-        rr = ctx.r(norm_sq(r))
+        rr = ctx.r(ctx.norm_sq(r))
         ctx.check(rr)
         hist.append(sqrt(rr))
         if _conv(rr, tol2, r0sq):
@@ -330,7 +334,7 @@ def _bicor(op, y, x, r, r0sq, tol2, maxit, ctx, hist, st, shadow=None):
     for k in range(1, maxit + 1):
         st["k"] = k
         rh = op.apply(r)                                        # r̂ = A r
-        rho = ctx.c(dotc(rs, rh))                               # ρ = ⟨r*, r̂⟩
+        rho = ctx.c(ctx.dotc(rs, rh))                               # ρ = ⟨r*, r̂⟩
         ctx.check(rho)
         if rho == 0:
             raise _Breakdown("rho")
@@ -342,12 +346,12 @@ def _bicor(op, y, x, r, r0sq, tol2, maxit, ctx, hist, st, shadow=None):
             ps = rs + ctx.c(beta.conjugate()) * ps              # p* = r* + conj(β)p*
             q = rh + beta * q                                   # q = r̂ + βq
         qs = op.apply_h(ps)                                     # q* = Aᴴ p*
-        xi = ctx.c(dotc(qs, q))                                 # ξ = ⟨q*, q⟩
+        xi = ctx.c(ctx.dotc(qs, q))                                 # ξ = ⟨q*, q⟩
         alpha = ctx.c(ctx.div(rho, xi, "xi"))                   # α = ρ/ξ
         st["x"] = x = x + alpha * p                             # x += αp
         r = r - alpha * q                                       # r −= αq
         rs = rs - ctx.c(alpha.conjugate()) * qs                 # r* −= conj(α)q*
-        rr = ctx.r(norm_sq(r))
+        rr = ctx.r(ctx.norm_sq(r))
         ctx.check(rr)
         hist.append(sqrt(rr))
         if _conv(rr, tol2, r0sq):
@@ -366,7 +370,7 @@ def _cors(op, y, x, r, r0sq, tol2, maxit, ctx, hist, st, shadow=None):
     for k in range(1, maxit + 1):
         st["k"] = k
         rh = op.apply(r)                                        # r̂ = A r
-        rho = ctx.c(dotc(r0s, rh))                              # ρ = ⟨r₀*, r̂⟩
+        rho = ctx.c(ctx.dotc(r0s, rh))                              # ρ = ⟨r₀*, r̂⟩
         ctx.check(rho)
         if rho == 0:
             raise _Breakdown("rho")
@@ -378,13 +382,13 @@ def _cors(op, y, x, r, r0sq, tol2, maxit, ctx, hist, st, shadow=None):
             eh = rh + beta * hh                                 # ê = r̂ + βĥ
             qh = eh + beta * (hh + beta * qh)                   # q̂ = ê + β(ĥ + βq̂)
         q = op.apply(qh)                                        # q = A q̂
-        xi = ctx.c(dotc(r0s, q))                                # ξ = ⟨r₀*, q⟩
+        xi = ctx.c(ctx.dotc(r0s, q))                                # ξ = ⟨r₀*, q⟩
         alpha = ctx.c(ctx.div(rho, xi, "xi"))                   # α = ρ/ξ
         h = e - alpha * qh                                      # h = e − αq̂
         hh = eh - alpha * q                                     # ĥ = ê − αq
         st["x"] = x = x + alpha * (e + h)                       # x += α(e + h)
         r = r - alpha * (eh + hh)                               # r −= α(ê + ĥ)
-        rr = ctx.r(norm_sq(r))
+        rr = ctx.r(ctx.norm_sq(r))
         ctx.check(rr)
         hist.append(sqrt(rr))
         if _conv(rr, tol2, r0sq):
@@ -402,7 +406,7 @@ def _bicg(op, y, x, r, r0sq, tol2, maxit, ctx, hist, st, shadow=None):
     rho_prev = None
     for k in range(1, maxit + 1):
         st["k"] = k
-        rho = ctx.c(dotc(rt, r))
+        rho = ctx.c(ctx.dotc(rt, r))
         if rho == 0:
             raise _Breakdown("rho")
         if k == 1:
@@ -413,11 +417,11 @@ def _bicg(op, y, x, r, r0sq, tol2, maxit, ctx, hist, st, shadow=None):
             pt = rt + ctx.c(beta.conjugate()) * pt
         q = op.apply(p)
         qt = op.apply_h(pt)
-        alpha = ctx.c(ctx.div(rho, dotc(pt, q), "sigma"))
+        alpha = ctx.c(ctx.div(rho, ctx.dotc(pt, q), "sigma"))
         st["x"] = x = x + alpha * p
         r = r - alpha * q
         rt = rt - ctx.c(alpha.conjugate()) * qt
-        rr = ctx.r(norm_sq(r))
+        rr = ctx.r(ctx.norm_sq(r))
         hist.append(sqrt(rr))
         if _conv(rr, tol2, r0sq):
             return CONVERGED, k, False
@@ -431,7 +435,7 @@ def _cgs(op, y, x, r, r0sq, tol2, maxit, ctx, hist, st, shadow=None):
     rho_prev = None
     for k in range(1, maxit + 1):
         st["k"] = k
-        rho = ctx.c(dotc(rt, r))
+        rho = ctx.c(ctx.dotc(rt, r))
         if rho == 0:
             raise _Breakdown("rho")
         if k == 1:
@@ -442,12 +446,12 @@ def _cgs(op, y, x, r, r0sq, tol2, maxit, ctx, hist, st, shadow=None):
             u = r + beta * q
             p = u + beta * (q + beta * p)
         v = op.apply(p)
-        alpha = ctx.c(ctx.div(rho, dotc(rt, v), "sigma"))
+        alpha = ctx.c(ctx.div(rho, ctx.dotc(rt, v), "sigma"))
         q = u - alpha * v
         uq = u + q
         st["x"] = x = x + alpha * uq
         r = r - alpha * op.apply(uq)
-        rr = ctx.r(norm_sq(r))
+        rr = ctx.r(ctx.norm_sq(r))
         hist.append(sqrt(rr))
         if _conv(rr, tol2, r0sq):
             return CONVERGED, k, False
@@ -458,21 +462,21 @@ def _cgs(op, y, x, r, r0sq, tol2, maxit, ctx, hist, st, shadow=None):
 def _cocr(op, y, x, r, r0sq, tol2, maxit, ctx, hist, st):
     Ar = op.apply(r)
     p, Ap = r.copy(), Ar.copy()
-    mu = ctx.c(dotu(r, Ar))
+    mu = ctx.c(ctx.dotu(r, Ar))
     for k in range(1, maxit + 1):
         st["k"] = k
         if k > 1:
             p = r + beta * p
             Ap = Ar + beta * Ap
-        alpha = ctx.c(ctx.div(mu, dotu(Ap, Ap), "xi"))
+        alpha = ctx.c(ctx.div(mu, ctx.dotu(Ap, Ap), "xi"))
         st["x"] = x = x + alpha * p
         r = r - alpha * Ap
-        rr = ctx.r(norm_sq(r))
+        rr = ctx.r(ctx.norm_sq(r))
         hist.append(sqrt(rr))
         if _conv(rr, tol2, r0sq):
             return CONVERGED, k, False
         Ar = op.apply(r)
-        mu_new = ctx.c(dotu(r, Ar))
+        mu_new = ctx.c(ctx.dotu(r, Ar))
         beta = ctx.c(ctx.div(mu_new, mu, "rho"))
         mu = mu_new
     return MAXIT, maxit, False
@@ -487,11 +491,11 @@ METHODS = {
 HOT_PATH = ("bicgstab", "cgne", "qmr", "bicor", "cors")
 
 
-def solve(method, op, y, tol, maxit, x0=None, **kw):
+def solve(method, op, y, tol, maxit, x0=None, dots=None, **kw):
     """Run ``method`` on A x = y (A given as an operator with apply/apply_h/apply_t).
 
     Returns a :class:`Result`.  ``kw`` passes method options (``shadow`` for
     BiCGSTAB/BiCOR/CORS/BiCG/CGS/QMR, ``form`` for QMR)."""
     if method not in METHODS:
         raise ValueError(f"unknown method {method!r}")
-    return _run(METHODS[method], op, y, tol, maxit, x0, **kw)
+    return _run(METHODS[method], op, y, tol, maxit, x0, dots=dots, **kw)
