@@ -1,0 +1,127 @@
+"""Throughput of every config × method on one B200.
+
+For each BASELINE config: repeated tolerance-driven ccg_solve calls (graphs on,
+no per-kernel timing), iterations/s = Σ iterations / Σ device time, plus the
+effective bandwidth of the algorithmic bytes (SURVEY §8(a):
+B_iter = m·B_mat + v·n·s).  One JSON line per (config, method).
+
+usage: python tools/bench_all.py [--configs 1,2,3,4,5] [--reps R]
+"""
+
+import argparse
+import json
+import os
+import sys
+import time
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import paper_1208_4869_b200 as ccg  # noqa: E402
+from workloads import (cfg1, cfg2, gauss_shifted_rows, cfg3_rhs, cfg4_rhs, helmholtz_csr,  # noqa: E402
+                       helmholtz_rhs, CONFIGS)
+from workloads.device import cfg4_rows_device  # noqa: E402
+
+V_PASSES = {"bicgstab": 18, "cgne": 10, "qmr": 26, "bicor": 24, "cors": 24}
+M_MATVEC = {"bicgstab": 2, "cgne": 2, "qmr": 2, "bicor": 2, "cors": 2}
+ALL = ("bicgstab", "cgne", "qmr", "bicor", "cors")
+
+
+def timed(h, method, y, x, tol, maxit, reps, stream):
+    r = ccg.ccg_solve(h, method, None, y, x, tol, maxit)          # warm (graph capture)
+    its, ms = 0, 0.0
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for _ in range(reps):
+        e0.record(stream)
+        r = ccg.ccg_solve(h, method, None, y, x, tol, maxit)
+        e1.record(stream)
+        e1.synchronize()
+        its += r["iterations"]
+        ms += e0.elapsed_time(e1)
+    return r, its, ms
+
+
+def run_dense(cfg, A, y, methods, tol, maxit, reps, dtype):
+    n = A.shape[0]
+    s = 8 if dtype == "c64" else 16
+    h = ccg.ccg_create(dtype, n)
+    ccg.ccg_set_matvec_dense(h, A, 0, n)
+    stream = torch.cuda.ExternalStream(ccg.ccg_get_stream(h))
+    x = torch.empty_like(y)
+    for m in methods:
+        r, its, ms = timed(h, m, y, x, tol, maxit, reps, stream)
+        b_iter = M_MATVEC[m] * n * n * s + V_PASSES[m] * n * s
+        ips = its / (ms / 1e3)
+        print(json.dumps({"config": cfg, "method": m, "n": n, "dtype": dtype, "status": r["status"],
+                          "iterations": r["iterations"], "ms_per_solve": ms / reps,
+                          "us_per_iteration": 1e3 * ms / its, "iterations_per_s": ips,
+                          "effective_GBs": b_iter * ips / 1e9, "true_rel_res": r["true_rel_res"],
+                          "reps": reps}), flush=True)
+    ccg.ccg_destroy(h)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--configs", default="1,2,3,4,5")
+    ap.add_argument("--reps", type=int, default=0)
+    ap.add_argument("--methods", default="")
+    a = ap.parse_args()
+    dev = "cuda:0"
+    for c in [int(v) for v in a.configs.split(",")]:
+        cf = CONFIGS[c]
+        t0 = time.time()
+        if c == 1:
+            A, y = cfg1()
+            run_dense(1, torch.from_numpy(A).to(dev), torch.from_numpy(y).to(dev), ALL, cf["tol"],
+                      cf["maxit"], a.reps or 200, "c128")
+        elif c == 2:
+            A, y = cfg2()
+            run_dense(2, torch.from_numpy(A).to(dev), torch.from_numpy(y).to(dev), ALL, cf["tol"],
+                      cf["maxit"], a.reps or 50, "c128")
+        elif c == 3:
+            n = cf["n"]
+            Ad = torch.empty((n, n), dtype=torch.complex64, device=dev)
+            pin = torch.empty((4096, n), dtype=torch.complex64).pin_memory()
+            for r0 in range(0, n, 4096):
+                gauss_shifted_rows(n, r0, r0 + 4096, seed=1, out=pin.numpy())
+                Ad[r0:r0 + 4096].copy_(pin)
+            run_dense(3, Ad, torch.from_numpy(cfg3_rhs(n)).to(dev), ALL, cf["tol"], cf["maxit"],
+                      a.reps or 5, "c64")
+            del Ad
+        elif c == 4:
+            n = cf["n"]
+            Ad = torch.empty((n, n), dtype=torch.complex128, device=dev)
+            for r0 in range(0, n, 4096):
+                cfg4_rows_device(r0, r0 + 4096, Ad[r0:r0 + 4096])
+            torch.cuda.synchronize()
+            print(json.dumps({"config": 4, "generate_s": time.time() - t0}), flush=True)
+            run_dense(4, Ad, torch.from_numpy(cfg4_rhs()).to(dev), ("bicgstab", "qmr", "bicor", "cgne"),
+                      cf["tol"], cf["maxit"], a.reps or 1, "c128")
+            del Ad
+        elif c == 5:
+            rp, ci, v = helmholtz_csr(128)
+            y = torch.from_numpy(helmholtz_rhs(128)).to(dev)
+            n = 128 ** 3
+            h = ccg.ccg_create("c128", n)
+            rpd, cid, vd = (torch.from_numpy(t).to(dev) for t in (rp, ci, v))
+            ccg.ccg_set_matvec_csr(h, rpd, cid, vd, 0, n, len(v))
+            stream = torch.cuda.ExternalStream(ccg.ccg_get_stream(h))
+            x = torch.empty_like(y)
+            b_mat = len(v) * (16 + 4) + 4 * (n + 1)
+            for m in [m for m in ("bicgstab", "cors") if not a.methods or m in a.methods.split(",")]:
+                r, its, ms = timed(h, m, y, x, cf["tol"], cf["maxit"], a.reps or 2, stream)
+                ips = its / (ms / 1e3)
+                b_iter = 2 * b_mat + V_PASSES[m] * n * 16
+                print(json.dumps({"config": 5, "method": m, "n": n, "dtype": "c128", "status": r["status"],
+                                  "iterations": r["iterations"], "ms_per_solve": ms / (a.reps or 2),
+                                  "us_per_iteration": 1e3 * ms / its, "iterations_per_s": ips,
+                                  "effective_GBs": b_iter * ips / 1e9, "true_rel_res": r["true_rel_res"]}),
+                      flush=True)
+            ccg.ccg_destroy(h)
+        torch.cuda.empty_cache()
+
+
+if __name__ == "__main__":
+    main()
