@@ -53,6 +53,13 @@ struct ccg_ctx {
   const int32_t* colind = nullptr;
   const void* vals = nullptr;
   int64_t nnz = 0, halo = 0;
+  int32_t* csr_blocks = nullptr;  // CSR-stream row-block boundaries (device)
+  int csr_nblocks = 0;
+  int64_t* sell_off = nullptr;    // SELL-32 copy of the CSR operator (owned)
+  int32_t* sell_width = nullptr;
+  int32_t* sell_col = nullptr;
+  void* sell_val = nullptr;
+  int sell_grid = 0;
   bool vec_ok = true;
   bool bulk_ok = false;   // TMA bulk-copy GEMV usable (alignment / n multiple of a 4 KiB tile)
   int bulk_grid = 0;
@@ -192,6 +199,7 @@ struct Engine {
   static constexpr int BR = 8;        // rows per group, bulk GEMV
   static constexpr int BSTAGES = 5;   // pipeline depth, bulk GEMV (5 x 36 KiB smem)
   static constexpr int SUR = 8;       // 16-byte loads in flight per lane, split GEMV
+  static constexpr int SNNZ = 2048;   // nonzeros per CSR-stream block
 
   static C* L(ccg_ctx* c, int i) { return reinterpret_cast<C*>(c->loc[i]); }
   static C* F(ccg_ctx* c, int i) { return reinterpret_cast<C*>(c->full[i]); }
@@ -232,6 +240,22 @@ struct Engine {
     c->launches++;
     CK(c, cudaGetLastError());
     return post<Op>(c, gate);
+  }
+
+  // CSR SpMV: CSR-stream blocks (default) or LPR lanes per row (CCG_SPMV=lanes)
+  template <bool CONJ, class Epi>
+  static void spmv(ccg_ctx* c, const C* x, Epi epi, const int* gate) {
+    const C* vals = reinterpret_cast<const C*>(c->vals);
+    if (c->sell_col)
+      spmv_sell_kernel<T, NT, CONJ, Epi><<<c->sell_grid, NT, 0, c->stream>>>(
+          c->sell_off, c->sell_width, c->sell_col, reinterpret_cast<const C*>(c->sell_val), x, c->nloc, epi,
+          make_red(c), c->st, gate);
+    else if (c->csr_blocks)
+      spmv_stream_kernel<T, NT, SNNZ, CONJ, Epi><<<c->spmv_grid, NT, 0, c->stream>>>(
+          c->rowptr, c->colind, vals, x, c->csr_blocks, c->csr_nblocks, epi, make_red(c), c->st, gate);
+    else
+      spmv_csr_kernel<T, LPR, NT, CONJ, Epi><<<c->spmv_grid, NT, 0, c->stream>>>(
+          c->rowptr, c->colind, vals, x, c->nloc, epi, make_red(c), c->st, gate);
   }
 
   // y_local = A · xfull (full-length buffer, own slice + gathered/halo parts)
@@ -288,9 +312,7 @@ struct Engine {
         gemv_n_kernel<T, R, NT, false, Epi><<<c->gemv_grid, NT, 0, c->stream>>>(
             A, c->lda, xfull, c->n, c->nloc, epi, make_red(c), c->st, gate);
     } else {
-      spmv_csr_kernel<T, LPR, NT, false, Epi><<<c->spmv_grid, NT, 0, c->stream>>>(
-          c->rowptr, c->colind, reinterpret_cast<const C*>(c->vals), xfull, c->nloc, epi, make_red(c),
-          c->st, gate);
+      spmv<false>(c, xfull, epi, gate);
     }
     c->launches++;
     tev_end(c);
@@ -305,13 +327,9 @@ struct Engine {
       // complex-symmetric CSR, single GPU: Aᴴx = conj(A conj x), Aᵀx = A x
       tev_begin(c, 1);
       if (conj)
-        spmv_csr_kernel<T, LPR, NT, true, Epi><<<c->spmv_grid, NT, 0, c->stream>>>(
-            c->rowptr, c->colind, reinterpret_cast<const C*>(c->vals), xloc, c->nloc, epi, make_red(c),
-            c->st, gate);
+        spmv<true>(c, xloc, epi, gate);
       else
-        spmv_csr_kernel<T, LPR, NT, false, Epi><<<c->spmv_grid, NT, 0, c->stream>>>(
-            c->rowptr, c->colind, reinterpret_cast<const C*>(c->vals), xloc, c->nloc, epi, make_red(c),
-            c->st, gate);
+        spmv<false>(c, xloc, epi, gate);
       c->launches++;
       tev_end(c);
       CK(c, cudaGetLastError());
@@ -556,6 +574,20 @@ static int choose_launch(ccg_ctx* c) {
   c->pass_grid = (int)std::max<int64_t>(1, std::min<int64_t>((c->nloc + NT - 1) / NT, (int64_t)c->sm_count * 8));
   c->spmv_grid = (int)std::max<int64_t>(
       1, std::min<int64_t>((c->nloc + NT / E::LPR - 1) / (NT / E::LPR), (int64_t)c->sm_count * 8));
+  if (c->sell_col) {
+    int occ4 = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ4, spmv_sell_kernel<T, E::NT, false, Store<T>>, NT, 0);
+    if (occ4 < 1) occ4 = 1;
+    const int64_t thr = ((c->nloc + 31) / 32) * 32;
+    c->sell_grid = (int)std::max<int64_t>(1, std::min<int64_t>((thr + NT - 1) / NT, (int64_t)c->sm_count * occ4));
+  }
+  if (c->csr_blocks) {
+    int occ3 = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ3, spmv_stream_kernel<T, E::NT, E::SNNZ, false, Store<T>>,
+                                                  NT, 0);
+    if (occ3 < 1) occ3 = 1;
+    c->spmv_grid = (int)std::max<int64_t>(1, std::min<int64_t>(c->csr_nblocks, (int64_t)c->sm_count * occ3));
+  }
   // workspace sized for the chosen grids
   size_t need_hpart = (size_t)c->ah_S * (size_t)c->n * sizeof(C);
   if (c->opk == OPK_DENSE && need_hpart > c->hpart_bytes) {
@@ -567,7 +599,7 @@ static int choose_launch(ccg_ctx* c) {
   int64_t maxgrid = std::max<int64_t>({(int64_t)c->gemv_grid, (int64_t)c->ah_strips * c->ah_S,
                                        (int64_t)c->stage2_grid, (int64_t)c->pass_grid, (int64_t)c->spmv_grid,
                                        (int64_t)c->split_strips * c->split_nrb, (int64_t)c->nstage2_grid,
-                                       (int64_t)c->bulk_grid});
+                                       (int64_t)c->bulk_grid, (int64_t)c->sell_grid});
   size_t need_part = (size_t)maxgrid * 4;
   if (need_part > c->part_cap) {
     if (c->part) cudaFree(c->part);
@@ -576,6 +608,20 @@ static int choose_launch(ccg_ctx* c) {
     c->part_cap = need_part;
   }
   return CCG_OK;
+}
+
+static void free_csr_copies(ccg_ctx* c) {
+  if (c->csr_blocks) cudaFree(c->csr_blocks);
+  if (c->sell_off) cudaFree(c->sell_off);
+  if (c->sell_width) cudaFree(c->sell_width);
+  if (c->sell_col) cudaFree(c->sell_col);
+  if (c->sell_val) cudaFree(c->sell_val);
+  c->csr_blocks = nullptr;
+  c->csr_nblocks = 0;
+  c->sell_off = nullptr;
+  c->sell_width = nullptr;
+  c->sell_col = nullptr;
+  c->sell_val = nullptr;
 }
 
 static void invalidate_graphs(ccg_ctx* c) {
@@ -822,6 +868,56 @@ int ccg_set_matvec_csr(ccg_handle c, const int32_t* rowptr, const int32_t* colin
     for (auto v : hs) halo = std::max(halo, v);
     if (halo > nloc) FAIL(c, CCG_E_ARG, "halo > nloc on some rank");
   }
+  // CSR-stream row blocks: ≤ 256 rows and ≤ 2048 nonzeros each (long rows alone)
+  free_csr_copies(c);
+  const char* sp = getenv("CCG_SPMV");
+  // SELL-32 copy when the padding is small (regular rows, e.g. stencils)
+  {
+    const int64_t nsl = (nloc + 31) / 32;
+    std::vector<int64_t> off(nsl);
+    std::vector<int32_t> wid(nsl);
+    int64_t tot = 0;
+    for (int64_t sl = 0; sl < nsl; ++sl) {
+      int32_t w = 0;
+      for (int64_t i = sl * 32; i < std::min<int64_t>(nloc, sl * 32 + 32); ++i) w = std::max(w, rp[i + 1] - rp[i]);
+      off[sl] = tot;
+      wid[sl] = w;
+      tot += 32 * (int64_t)w;
+    }
+    const bool want = sp ? !strcmp(sp, "sell") : (tot <= nnz_local + nnz_local / 4 + 1024);
+    if (want && nloc > 0) {
+      CK(c, cudaMalloc(&c->sell_off, nsl * sizeof(int64_t)));
+      CK(c, cudaMalloc(&c->sell_width, nsl * sizeof(int32_t)));
+      CK(c, cudaMalloc(&c->sell_col, std::max<int64_t>(tot, 1) * sizeof(int32_t)));
+      CK(c, cudaMalloc(&c->sell_val, std::max<int64_t>(tot, 1) * c->esz));
+      CK(c, cudaMemcpy(c->sell_off, off.data(), nsl * sizeof(int64_t), cudaMemcpyHostToDevice));
+      CK(c, cudaMemcpy(c->sell_width, wid.data(), nsl * sizeof(int32_t), cudaMemcpyHostToDevice));
+      const int64_t thr = nsl * 32;
+      const int g = (int)((thr + 255) / 256);
+      if (c->esz == 8)
+        csr_to_sell<float2><<<g, 256, 0, c->stream>>>(rowptr, colind, (const float2*)vals, c->sell_off,
+                                                      c->sell_width, nloc, c->sell_col, (float2*)c->sell_val);
+      else
+        csr_to_sell<double2><<<g, 256, 0, c->stream>>>(rowptr, colind, (const double2*)vals, c->sell_off,
+                                                        c->sell_width, nloc, c->sell_col, (double2*)c->sell_val);
+      CK(c, cudaGetLastError());
+      CK(c, cudaStreamSynchronize(c->stream));
+    }
+  }
+  if (!c->sell_col && (sp == nullptr || strcmp(sp, "lanes") != 0)) {
+    std::vector<int32_t> bl;
+    bl.push_back(0);
+    int64_t r = 0;
+    while (r < nloc) {
+      int64_t e = r + 1;
+      while (e < nloc && e - r < 256 && rp[e + 1] - rp[r] <= 2048) ++e;
+      bl.push_back((int32_t)e);
+      r = e;
+    }
+    c->csr_nblocks = (int)bl.size() - 1;
+    CK(c, cudaMalloc(&c->csr_blocks, bl.size() * sizeof(int32_t)));
+    CK(c, cudaMemcpy(c->csr_blocks, bl.data(), bl.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+  }
   c->opk = OPK_CSR;
   c->rowptr = rowptr;
   c->colind = colind;
@@ -989,6 +1085,7 @@ int ccg_destroy(ccg_handle c) {
   if (c->wfull) cudaFree(c->wfull);
   if (c->hpart) cudaFree(c->hpart);
   if (c->npart) cudaFree(c->npart);
+  free_csr_copies(c);
   if (c->part) cudaFree(c->part);
   if (c->hist) cudaFree(c->hist);
   if (c->st) cudaFree(c->st);

@@ -448,6 +448,171 @@ spmv_csr_kernel(const int32_t* __restrict__ rowptr, const int32_t* __restrict__ 
 }
 
 // ---------------------------------------------------------------------------
+// K3' CSR-stream SpMV (default): the rows are cut on the host into blocks of
+// ≤ NT rows and ≤ NNZ_MAX nonzeros (a row longer than NNZ_MAX is a block of
+// its own).  A CTA streams its block's vals/colind coalesced, 8 independent
+// (val, col) pairs then 8 independent x gathers per thread, writes the
+// products to shared memory, and thread t sums row t's products in CSR order
+// (deterministic).  All loads of a block are in flight at once instead of one
+// dependent rowptr → colind → x chain per row.
+// ---------------------------------------------------------------------------
+template <typename T, int NT, int NNZ_MAX, bool CONJ, class Epi>
+__global__ void __launch_bounds__(NT)
+spmv_stream_kernel(const int32_t* __restrict__ rowptr, const int32_t* __restrict__ colind,
+                   const typename CT<T>::c* __restrict__ vals, const typename CT<T>::c* __restrict__ x,
+                   const int32_t* __restrict__ blocks, int nblocks, Epi epi, Red red, State* st,
+                   const int* gate) {
+  using C = typename CT<T>::c;
+  constexpr int KK = Epi::K > 0 ? Epi::K : 1;
+  constexpr int U = 8;
+  if (*gate) return;
+  epi.load(st);
+  __shared__ C prod[NNZ_MAX];
+  __shared__ int32_t rp[NT + 1];
+  __shared__ double2 lsum[NT / 32];
+  double2 dacc[KK];
+#pragma unroll
+  for (int k = 0; k < KK; ++k) dacc[k] = make_double2(0.0, 0.0);
+  const int t = threadIdx.x;
+  for (int b = blockIdx.x; b < nblocks; b += gridDim.x) {
+    const int r0 = __ldg(blocks + b), r1 = __ldg(blocks + b + 1);
+    const int nr = r1 - r0;
+    const int k0 = __ldg(rowptr + r0), k1 = __ldg(rowptr + r1);
+    if (k1 - k0 > NNZ_MAX) {
+      // one long row: strided partial sums, fixed-order CTA reduction
+      C acc = czero<C>();
+      for (int k = k0 + t; k < k1; k += NT) {
+        C xv = __ldg(x + __ldcs(colind + k));
+        if (CONJ) xv = cconj(xv);
+        cfma(acc, __ldcs(vals + k), xv);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
+        acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+      }
+      if ((t & 31) == 0) lsum[t >> 5] = make_double2((double)acc.x, (double)acc.y);
+      __syncthreads();
+      if (t == 0) {
+        C s = czero<C>();
+        for (int w = 0; w < NT / 32; ++w) { s.x += lsum[w].x; s.y += lsum[w].y; }
+        epi(r0, CONJ ? cconj(s) : s, dacc);
+      }
+      __syncthreads();
+      continue;
+    }
+    const int nk = k1 - k0;
+    for (int j = t; j <= nr; j += NT) rp[j] = __ldg(rowptr + r0 + j) - k0;
+    for (int kb = t; kb < nk; kb += NT * U) {
+      int col[U];
+      C v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int k = kb + u * NT;
+        col[u] = k < nk ? __ldcs(colind + k0 + k) : 0;
+        v[u] = k < nk ? __ldcs(vals + k0 + k) : czero<C>();
+      }
+      C xv[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) xv[u] = __ldg(x + col[u]);
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int k = kb + u * NT;
+        if (k < nk) {
+          C xx = CONJ ? cconj(xv[u]) : xv[u];
+          C p = czero<C>();
+          cfma(p, v[u], xx);
+          prod[k] = p;
+        }
+      }
+    }
+    __syncthreads();
+    if (t < nr) {
+      C s = czero<C>();
+      for (int k = rp[t]; k < rp[t + 1]; ++k) s = cadd(s, prod[k]);
+      epi(r0 + t, CONJ ? cconj(s) : s, dacc);
+    }
+    __syncthreads();
+  }
+  if constexpr (Epi::K > 0) finish_reduction<KK, NT, Epi>(dacc, red, st);
+}
+
+// ---------------------------------------------------------------------------
+// K3'' SELL-32 SpMV (default when padding is small, e.g. the 7-point stencil):
+// the library copies the borrowed CSR once into slices of 32 consecutive rows
+// stored column-major (entry j of row 32s+l at off_s + 32j + l, padding
+// col = -1), so a warp reads 512 B of values + 128 B of columns per step,
+// fully coalesced, one row per lane, no shared memory and no barriers.  The
+// row sum runs in CSR column order (same order as the CSR kernels).
+// ---------------------------------------------------------------------------
+template <typename T, int NT, bool CONJ, class Epi>
+__global__ void __launch_bounds__(NT)
+spmv_sell_kernel(const int64_t* __restrict__ soff, const int32_t* __restrict__ swidth,
+                 const int32_t* __restrict__ scol, const typename CT<T>::c* __restrict__ sval,
+                 const typename CT<T>::c* __restrict__ x, int64_t nrows, Epi epi, Red red, State* st,
+                 const int* gate) {
+  using C = typename CT<T>::c;
+  constexpr int KK = Epi::K > 0 ? Epi::K : 1;
+  constexpr int U = 8;
+  if (*gate) return;
+  epi.load(st);
+  double2 dacc[KK];
+#pragma unroll
+  for (int k = 0; k < KK; ++k) dacc[k] = make_double2(0.0, 0.0);
+  const int64_t nwarps_rows = ((nrows + 31) / 32) * 32;
+  for (int64_t i = (int64_t)blockIdx.x * NT + threadIdx.x; i < nwarps_rows; i += (int64_t)gridDim.x * NT) {
+    const int64_t s = i >> 5;
+    const int lane = (int)(i & 31);
+    const int w = __ldg(swidth + s);
+    const int64_t base = __ldg(soff + s) + lane;
+    C acc = czero<C>();
+    for (int j0 = 0; j0 < w; j0 += U) {
+      int col[U];
+      C v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int j = j0 + u;
+        col[u] = j < w ? __ldcs(scol + base + 32 * (int64_t)j) : -1;
+        v[u] = j < w ? __ldcs(sval + base + 32 * (int64_t)j) : czero<C>();
+      }
+      C xv[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) xv[u] = col[u] >= 0 ? __ldg(x + col[u]) : czero<C>();
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (col[u] >= 0) {
+          C p = czero<C>();
+          cfma(p, v[u], CONJ ? cconj(xv[u]) : xv[u]);
+          acc = cadd(acc, p);
+        }
+      }
+    }
+    if (i < nrows) epi(i, CONJ ? cconj(acc) : acc, dacc);
+  }
+  if constexpr (Epi::K > 0) finish_reduction<KK, NT, Epi>(dacc, red, st);
+}
+
+// CSR -> SELL-32 scatter (one thread per row), run once at ccg_set_matvec_csr
+template <typename C>
+__global__ void csr_to_sell(const int32_t* __restrict__ rowptr, const int32_t* __restrict__ colind,
+                            const C* __restrict__ vals, const int64_t* __restrict__ soff,
+                            const int32_t* __restrict__ swidth, int64_t nrows, int32_t* scol, C* sval) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= ((nrows + 31) / 32) * 32) return;
+  const int64_t s = i >> 5;
+  const int lane = (int)(i & 31);
+  const int w = swidth[s];
+  const int64_t base = soff[s] + lane;
+  const int k0 = i < nrows ? rowptr[i] : 0, k1 = i < nrows ? rowptr[i + 1] : 0;
+  for (int j = 0; j < w; ++j) {
+    const int k = k0 + j;
+    C z; z.x = 0; z.y = 0;
+    scol[base + 32 * (int64_t)j] = k < k1 ? colind[k] : -1;
+    sval[base + 32 * (int64_t)j] = k < k1 ? vals[k] : z;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // K4 fused vector pass: one grid-stride sweep applying a method-phase
 // functor to every local element, with up to K fp64 partial sums.
 // ---------------------------------------------------------------------------
