@@ -35,7 +35,7 @@ thread_local std::string g_create_err;
 // ===========================================================================
 enum { NLOCAL = 12, NFULL = 3 };
 enum { OPK_NONE = 0, OPK_DENSE = 1, OPK_CSR = 2 };
-enum { GEMV_SPLIT = 0, GEMV_BULK = 1, GEMV_ROWS = 2 };
+enum { GEMV_SPLIT = 0, GEMV_BULK = 1, GEMV_ROWS = 2, GEMV_COLS = 3 };
 
 struct ccg_ctx {
   int dtype = 0;
@@ -65,7 +65,10 @@ struct ccg_ctx {
   int bulk_grid = 0;
   int gemv_mode = 0;      // GEMV_SPLIT (default) | GEMV_BULK | GEMV_ROWS (env CCG_GEMV)
   int split_W = 0, split_strips = 1, split_nrb = 1, nstage2_grid = 1, split_ur = 8;
-  void* npart = nullptr;  // [strips][nloc] partial row sums of the split GEMV
+  bool cols_ok = false;   // column-owner GEMV usable (vectorised layout, n % V == 0)
+  int cols_strips = 1, cols_S = 1, dual_S = 1;
+  bool qmr_dual = true;   // QMR: A·p and Aᴴ·q in one pass over A (env CCG_QMR_DUAL=0 disables)
+  void* npart = nullptr;  // [strips][nloc] partial row sums of the split / column-owner GEMV
   size_t npart_bytes = 0;
   // workspace
   State* st = nullptr;
@@ -293,6 +296,14 @@ struct Engine {
         gemv_h_stage2<T, NT, Epi><<<c->nstage2_grid, NT, 0, c->stream>>>(part, c->split_strips, c->nloc, 0,
                                                                           c->nloc, epi, make_red(c), c->st, gate);
       }
+    } else if (c->opk == OPK_DENSE && c->gemv_mode == GEMV_COLS && c->cols_ok) {
+      C* part = reinterpret_cast<C*>(c->npart);
+      gemv_cols<T, NT, true, false, false><<<dim3(c->cols_strips, c->cols_S), NT, 0, c->stream>>>(
+          reinterpret_cast<const C*>(c->A), c->lda, xfull, nullptr, c->nloc, c->n, part, nullptr, gate);
+      c->launches++;
+      CK(c, cudaGetLastError());
+      gemv_h_stage2<T, NT, Epi><<<c->nstage2_grid, NT, 0, c->stream>>>(part, c->cols_strips, c->nloc, 0, c->nloc,
+                                                                        epi, make_red(c), c->st, gate);
     } else if (c->opk == OPK_DENSE && c->gemv_mode == GEMV_BULK && c->bulk_ok) {
       constexpr size_t smem = bulk_smem_bytes<BR, BSTAGES>();
       auto kern = gemv_n_bulk<T, BR, BSTAGES, Epi>;
@@ -373,6 +384,43 @@ struct Engine {
     return pass(c, ep, gate);
   }
 
+  // p̃ = A·p (epilogue ea) and w = Aᴴ·q (epilogue eh) in ONE pass over A
+  // (gemv_cols<DO_N, DO_H>).  ea's scalar step runs
+  // before eh's epilogue (QMR: ε, β before w̃ = Aᴴq − conj(β)w).
+  template <class EpiA, class EpiH>
+  static int matvec_dual(ccg_ctx* c, const C* pfull, const C* qloc, EpiA ea, EpiH eh, const int* gate) {
+    const C* A = reinterpret_cast<const C*>(c->A);
+    C* np = reinterpret_cast<C*>(c->npart);
+    C* hp = reinterpret_cast<C*>(c->hpart);
+    tev_begin(c, 0);
+    gemv_cols<T, NT, true, true, true><<<dim3(c->cols_strips, c->dual_S), NT, 0, c->stream>>>(
+        A, c->lda, pfull, qloc, c->nloc, c->n, np, hp, gate);
+    c->launches++;
+    CK(c, cudaGetLastError());
+    gemv_h_stage2<T, NT, EpiA><<<c->nstage2_grid, NT, 0, c->stream>>>(np, c->cols_strips, c->nloc, 0, c->nloc, ea,
+                                                                      make_red(c), c->st, gate);
+    c->launches++;
+    tev_end(c);
+    CK(c, cudaGetLastError());
+    TRY(post<EpiA>(c, gate));
+    if (c->world == 1) {
+      gemv_h_stage2<T, NT, EpiH><<<c->stage2_grid, NT, 0, c->stream>>>(hp, c->dual_S, c->n, 0, c->n, eh,
+                                                                       make_red(c), c->st, gate);
+      c->launches++;
+      CK(c, cudaGetLastError());
+      return CCG_OK;
+    }
+    Store<T> stv{reinterpret_cast<C*>(c->wfull)};
+    gemv_h_stage2<T, NT, Store<T>><<<c->stage2_grid, NT, 0, c->stream>>>(hp, c->dual_S, c->n, 0, c->n, stv,
+                                                                         make_red(c), c->st, gate);
+    c->launches++;
+    CK(c, cudaGetLastError());
+    C* wl = L(c, NLOCAL - 1);
+    NK(c, c->comm->reduce_scatter(c->wfull, wl, (size_t)c->nloc * 2, ndt(), c->stream));
+    EpiPass<C, EpiH> ep{eh, wl};
+    return pass(c, ep, gate);
+  }
+
   // ==================== method schedules ====================
   // local vector slots (NLOCAL-1 is reserved for the multi-GPU Aᴴ result)
   enum { X = 0 };
@@ -426,8 +474,13 @@ struct Engine {
     const int* g = &c->st->done;
     TRY(pass(c, QmP<T>{L(c, 5), L(c, 6), Fs(c, 0), L(c, 7)}, g));
     TRY(allgather(c, 0));
-    TRY(matvec_a(c, F(c, 0), QmPt<T>{L(c, 8), L(c, 7)}, g));
-    TRY(matvec_h(c, L(c, 7), true, QmVW<T>{L(c, 3), L(c, 4), L(c, 8), L(c, 5), L(c, 6)}, g));
+    if (c->opk == OPK_DENSE && c->cols_ok && c->qmr_dual) {
+      TRY(matvec_dual(c, F(c, 0), L(c, 7), QmPt<T>{L(c, 8), L(c, 7)},
+                      QmVW<T>{L(c, 3), L(c, 4), L(c, 8), L(c, 5), L(c, 6)}, g));
+    } else {
+      TRY(matvec_a(c, F(c, 0), QmPt<T>{L(c, 8), L(c, 7)}, g));
+      TRY(matvec_h(c, L(c, 7), true, QmVW<T>{L(c, 3), L(c, 4), L(c, 8), L(c, 5), L(c, 6)}, g));
+    }
     return pass(c, QmDV<T>{L(c, 9), L(c, 10), L(c, X), L(c, 2), Fs(c, 0), L(c, 8), L(c, 3), L(c, 4), L(c, 5),
                            L(c, 6)},
                 g);
@@ -518,7 +571,42 @@ static int choose_launch(ccg_ctx* c) {
   c->bulk_grid = (int)std::max<int64_t>(1, std::min<int64_t>((c->nloc + E::BR - 1) / E::BR, c->sm_count));
   {
     const char* gm = getenv("CCG_GEMV");
-    c->gemv_mode = (gm && !strcmp(gm, "bulk")) ? GEMV_BULK : (gm && !strcmp(gm, "rows")) ? GEMV_ROWS : GEMV_SPLIT;
+    c->gemv_mode = (gm && !strcmp(gm, "bulk"))   ? GEMV_BULK
+                   : (gm && !strcmp(gm, "rows")) ? GEMV_ROWS
+                   : (gm && !strcmp(gm, "cols")) ? GEMV_COLS
+                                                 : GEMV_SPLIT;
+    const char* qd = getenv("CCG_QMR_DUAL");
+    c->qmr_dual = !(qd && !strcmp(qd, "0"));
+  }
+  // column-owner GEMV (A·x in GEMV_COLS mode; QMR dual product): strips of NT·V
+  // columns; A·x alone: whole waves of (strip, split) CTAs; dual: as for Aᴴ
+  c->cols_ok = c->opk == OPK_DENSE && c->vec_ok && (c->n % CT<T>::V) == 0;
+  if (c->cols_ok) {
+    const int64_t nvc = c->n / CT<T>::V;
+    c->cols_strips = (int)std::max<int64_t>(1, (nvc + NT - 1) / NT);
+    int occc = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occc, gemv_cols<T, E::NT, true, false, false>, NT, 0);
+    if (occc < 1) occc = 1;
+    const int64_t slots_c = (int64_t)c->sm_count * occc;
+    const char* wv = getenv("CCG_COLS_WAVES");
+    const int64_t waves = wv ? std::max(1, atoi(wv)) : 2;
+    int64_t Sn = std::max<int64_t>(1, (waves * slots_c) / c->cols_strips);
+    c->cols_S = (int)std::min<int64_t>(Sn, std::max<int64_t>(1, c->nloc / 8));
+    int occd = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occd, gemv_cols<T, E::NT, true, true, true>, NT, 0);
+    if (occd < 1) occd = 1;
+    int64_t Sd = ((int64_t)c->sm_count * occd) / c->cols_strips;
+    Sd = std::max<int64_t>(1, std::min<int64_t>(Sd, 128));
+    c->dual_S = (int)std::min<int64_t>(Sd, std::max<int64_t>(1, c->nloc / 16));
+    c->nstage2_grid =
+        (int)std::max<int64_t>(1, std::min<int64_t>((c->nloc + NT - 1) / NT, (int64_t)c->sm_count * 4));
+    size_t need = (size_t)c->cols_strips * c->nloc * sizeof(C);
+    if (need > c->npart_bytes) {
+      if (c->npart) cudaFree(c->npart);
+      c->npart = nullptr;
+      CK(c, cudaMalloc(&c->npart, need));
+      c->npart_bytes = need;
+    }
   }
   if (c->opk == OPK_DENSE && c->gemv_mode == GEMV_SPLIT) {
     // x strip of 16 KiB in shared memory; whole waves of CTAs (strips × row blocks)
@@ -589,7 +677,7 @@ static int choose_launch(ccg_ctx* c) {
     c->spmv_grid = (int)std::max<int64_t>(1, std::min<int64_t>(c->csr_nblocks, (int64_t)c->sm_count * occ3));
   }
   // workspace sized for the chosen grids
-  size_t need_hpart = (size_t)c->ah_S * (size_t)c->n * sizeof(C);
+  size_t need_hpart = (size_t)std::max(c->ah_S, c->cols_ok ? c->dual_S : 1) * (size_t)c->n * sizeof(C);
   if (c->opk == OPK_DENSE && need_hpart > c->hpart_bytes) {
     if (c->hpart) cudaFree(c->hpart);
     c->hpart = nullptr;
@@ -599,7 +687,8 @@ static int choose_launch(ccg_ctx* c) {
   int64_t maxgrid = std::max<int64_t>({(int64_t)c->gemv_grid, (int64_t)c->ah_strips * c->ah_S,
                                        (int64_t)c->stage2_grid, (int64_t)c->pass_grid, (int64_t)c->spmv_grid,
                                        (int64_t)c->split_strips * c->split_nrb, (int64_t)c->nstage2_grid,
-                                       (int64_t)c->bulk_grid, (int64_t)c->sell_grid});
+                                       (int64_t)c->bulk_grid, (int64_t)c->sell_grid,
+                                       (int64_t)c->cols_strips * std::max(c->cols_S, c->dual_S)});
   size_t need_part = (size_t)maxgrid * 4;
   if (need_part > c->part_cap) {
     if (c->part) cudaFree(c->part);

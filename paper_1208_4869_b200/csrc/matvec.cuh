@@ -385,6 +385,142 @@ gemv_h_stage1(const typename CT<T>::c* __restrict__ A, int64_t lda,
   }
 }
 
+// ---------------------------------------------------------------------------
+// K1c / K2D gemv_cols: the column-owner layout of K2 applied to A·x, and to
+// A·x and Aᴴ·x together.  CTA (c, s) owns the column strip
+// [c·NT·V, (c+1)·NT·V) — thread t the 16-byte chunk t — and the rows of split
+// s, walked UR = 8 rows at a time (8 independent 16-B loads in flight per
+// thread: the CTA reads 8 whole 4-KiB row segments at once, no A reuse).
+//   DO_N: row partials Σ_{j∈strip} A_ij xn_j, reduced over the CTA's threads
+//         (transposed warp reduction, 9 shuffle pairs per 8 rows, then the
+//         warps in fixed order through double-buffered shared memory) and
+//         stored to npart[c][i] — gemv_h_stage2 sums the strips in order;
+//   DO_H: column partials Σ_{i∈split} op(A_ij) xh_i, op = conj (Aᴴ) or
+//         identity (Aᵀ), stored to hpart[s][j] — gemv_h_stage2 sums the splits.
+// With both, A·p and Aᴴ·q of one QMR iteration (they are
+// independent) come out of ONE pass over A.  Needs the
+// vectorised layout (16-B aligned A, lda·sizeof(C) % 16 == 0, n % V == 0).
+// ---------------------------------------------------------------------------
+template <typename C>
+__device__ __forceinline__ void shfl_c(C& v, int o) {
+  v.x = __shfl_xor_sync(0xffffffffu, v.x, o);
+  v.y = __shfl_xor_sync(0xffffffffu, v.y, o);
+}
+
+// v[0..7]: per-lane partials of 8 rows.  After the call lane L holds, in v[0],
+// the warp sum of row (L >> 2) & 7 (fixed order: deterministic).
+template <typename C>
+__device__ __forceinline__ void warp_transpose_reduce8(C (&v)[8], int lane) {
+  const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    C send = b4 ? v[j] : v[j + 4];
+    const C keep = b4 ? v[j + 4] : v[j];
+    shfl_c(send, 16);
+    v[j] = cadd(keep, send);
+  }
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    C send = b3 ? v[j] : v[j + 2];
+    const C keep = b3 ? v[j + 2] : v[j];
+    shfl_c(send, 8);
+    v[j] = cadd(keep, send);
+  }
+  {
+    C send = b2 ? v[0] : v[1];
+    const C keep = b2 ? v[1] : v[0];
+    shfl_c(send, 4);
+    v[0] = cadd(keep, send);
+  }
+  C t = v[0];
+  shfl_c(t, 2);
+  v[0] = cadd(v[0], t);
+  t = v[0];
+  shfl_c(t, 1);
+  v[0] = cadd(v[0], t);
+}
+
+template <typename T, int NT, bool DO_N, bool DO_H, bool CONJ>
+__global__ void __launch_bounds__(NT)
+gemv_cols(const typename CT<T>::c* __restrict__ A, int64_t lda,
+          const typename CT<T>::c* __restrict__ xn, const typename CT<T>::c* __restrict__ xh,
+          int64_t nrows, int64_t n, typename CT<T>::c* __restrict__ npart,
+          typename CT<T>::c* __restrict__ hpart, const int* gate) {
+  using C = typename CT<T>::c;
+  using LV = typename CT<T>::v;
+  constexpr int V = CT<T>::V;
+  constexpr int UR = 8;
+  constexpr int CH = 512;  // rows of xh per shared-memory chunk
+  if (*gate) return;
+  __shared__ C xs[DO_H ? CH : 1];
+  __shared__ C red[2][NT / 32][UR];
+  const int S = gridDim.y, s = blockIdx.y;
+  const int64_t i0 = nrows * s / S, i1 = nrows * (s + 1) / S;
+  const int64_t jv = (int64_t)blockIdx.x * NT + threadIdx.x;  // 16-byte chunk index
+  const int64_t nv = n / V;
+  const bool active = jv < nv;
+  const int64_t jc = active ? jv : 0;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t ldv = lda / V;
+  C xr[V];
+#pragma unroll
+  for (int v = 0; v < V; ++v) xr[v] = czero<C>();
+  if (DO_N && active) unpack(*reinterpret_cast<const LV*>(xn + jv * V), xr);
+  C hacc[V];
+#pragma unroll
+  for (int v = 0; v < V; ++v) hacc[v] = czero<C>();
+  const LV* Ab = reinterpret_cast<const LV*>(A) + jc;
+  int buf = 0;
+  for (int64_t c0 = i0; c0 < i1; c0 += CH) {
+    const int cn = (int)min((int64_t)CH, i1 - c0);
+    if constexpr (DO_H) {
+      __syncthreads();
+      for (int t = threadIdx.x; t < cn; t += NT) xs[t] = xh[c0 + t];
+      __syncthreads();
+    }
+    for (int t = 0; t < cn; t += UR) {
+      const int nr = min(UR, cn - t);
+      LV a[UR];
+#pragma unroll
+      for (int u = 0; u < UR; ++u) a[u] = ld_stream(Ab + (c0 + t + min(u, nr - 1)) * ldv);
+      C rp[UR];
+#pragma unroll
+      for (int u = 0; u < UR; ++u) {
+        C ac[V];
+        unpack(a[u], ac);
+        rp[u] = czero<C>();
+        if (DO_N && active) {
+#pragma unroll
+          for (int v = 0; v < V; ++v) cfma(rp[u], ac[v], xr[v]);
+        }
+        if (DO_H && u < nr) {
+          const C xi = xs[t + u];
+#pragma unroll
+          for (int v = 0; v < V; ++v) {
+            if (CONJ) cfmac(hacc[v], ac[v], xi); else cfma(hacc[v], ac[v], xi);
+          }
+        }
+      }
+      if constexpr (DO_N) {
+        warp_transpose_reduce8(rp, lane);
+        if ((lane & 3) == 0) red[buf][warp][lane >> 2] = rp[0];
+        __syncthreads();
+        if (threadIdx.x < nr) {
+          C sum = red[buf][0][threadIdx.x];
+#pragma unroll
+          for (int w = 1; w < NT / 32; ++w) sum = cadd(sum, red[buf][w][threadIdx.x]);
+          npart[(int64_t)blockIdx.x * nrows + c0 + t + threadIdx.x] = sum;
+        }
+        buf ^= 1;
+      }
+    }
+  }
+  if (DO_H && active) {
+#pragma unroll
+    for (int v = 0; v < V; ++v) hpart[(int64_t)s * n + jv * V + v] = hacc[v];
+  }
+}
+
 // K2 stage 2: w_j = Σ_s part[s][off + j] in split order, then epilogue.
 template <typename T, int NT, class Epi>
 __global__ void __launch_bounds__(NT)

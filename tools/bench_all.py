@@ -26,7 +26,11 @@ from workloads.device import cfg4_rows_device  # noqa: E402
 
 V_PASSES = {"bicgstab": 18, "cgne": 10, "qmr": 26, "bicor": 24, "cors": 24}
 M_MATVEC = {"bicgstab": 2, "cgne": 2, "qmr": 2, "bicor": 2, "cors": 2}
+if os.environ.get("CCG_QMR_DUAL", "1") != "0":
+    M_MATVEC["qmr"] = 1                  # dual GEMV: A·p and Aᴴ·q in one pass
+KNOBS = {k: v for k, v in os.environ.items() if k.startswith("CCG_")}
 ALL = ("bicgstab", "cgne", "qmr", "bicor", "cors")
+SEL = set()
 
 
 def timed(h, method, y, x, tol, maxit, reps, stream):
@@ -51,6 +55,8 @@ def run_dense(cfg, A, y, methods, tol, maxit, reps, dtype):
     stream = torch.cuda.ExternalStream(ccg.ccg_get_stream(h))
     x = torch.empty_like(y)
     for m in methods:
+        if SEL and m not in SEL:
+            continue
         r, its, ms = timed(h, m, y, x, tol, maxit, reps, stream)
         b_iter = M_MATVEC[m] * n * n * s + V_PASSES[m] * n * s
         ips = its / (ms / 1e3)
@@ -58,7 +64,7 @@ def run_dense(cfg, A, y, methods, tol, maxit, reps, dtype):
                           "iterations": r["iterations"], "ms_per_solve": ms / reps,
                           "us_per_iteration": 1e3 * ms / its, "iterations_per_s": ips,
                           "effective_GBs": b_iter * ips / 1e9, "true_rel_res": r["true_rel_res"],
-                          "reps": reps}), flush=True)
+                          "reps": reps, "knobs": KNOBS}), flush=True)
     ccg.ccg_destroy(h)
 
 
@@ -68,6 +74,8 @@ def main():
     ap.add_argument("--reps", type=int, default=0)
     ap.add_argument("--methods", default="")
     a = ap.parse_args()
+    global SEL
+    SEL = set(a.methods.split(",")) if a.methods else set()
     dev = "cuda:0"
     for c in [int(v) for v in a.configs.split(",")]:
         cf = CONFIGS[c]

@@ -25,7 +25,7 @@ def run(dtype, n, reps, grid):
     h = ccg.ccg_create(dtype, n)
     esz = 8 if dtype == "c64" else 16
     for knobs in grid:
-        for k in ("CCG_GEMV", "CCG_SPLIT_KB", "CCG_SPLIT_UR", "CCG_SPLIT_WAVES"):
+        for k in ("CCG_GEMV", "CCG_SPLIT_KB", "CCG_SPLIT_UR", "CCG_SPLIT_WAVES", "CCG_COLS_WAVES"):
             os.environ.pop(k, None)
         os.environ.update({k: str(v) for k, v in knobs.items()})
         ccg.ccg_set_matvec_dense(h, A, 0, n)
@@ -50,6 +50,13 @@ def run(dtype, n, reps, grid):
 
 
 if __name__ == "__main__":
+    if "--modes" in sys.argv:
+        modes = [dict(CCG_GEMV=m) for m in ("split", "cols")] + [dict(CCG_GEMV="cols", CCG_COLS_WAVES=w)
+                                                                 for w in (1, 4, 8)]
+        run("c64", 32768, 10, modes)
+        run("c128", 16384, 10, modes)
+        run("c128", 4096, 50, modes)
+        sys.exit(0)
     grid = [dict(CCG_GEMV="split", CCG_SPLIT_KB=kb, CCG_SPLIT_UR=ur, CCG_SPLIT_WAVES=w)
             for kb, ur, w in itertools.product((8, 16, 24), (4, 8, 16), (1, 2, 4))]
     run("c64", 32768, 10, grid)
