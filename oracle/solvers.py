@@ -5,8 +5,9 @@ down (BiCGSTAB, CGNE, QMR: PIM90 set, §2.1, QMR "changed" per P:57 and
 Chaumet's corrected version P:101 §6; BiCOR / CORS: Carpentieri, Jing & Huang
 2011, §2.4).  The recurrences below follow SURVEY.md §8(c) O1-O5
 line by line, in that notation, with the readings Q1-Q16 listed in
-DESIGN.md §"Readings of the paper".  BiCG, CGS and COCR (§3.4) are
-included only as independent pins: BiCOR ≡ BiCG(shadow Aᴴr₀*), CORS ≡
+DESIGN.md §"Readings of the paper".  BiCG, CGS, CGNR and COCR (P:87
+§3.4) — the SURVEY §8(f) NEXT-3 rows — follow the standard published
+recurrences and double as pins of O4/O5: BiCOR ≡ BiCG(shadow Aᴴr₀*), CORS ≡
 CGS(shadow Aᴴr₀*), BiCOR(r₀* = conj r₀) ≡ COCR on complex-symmetric A.
 
 Common rules (SURVEY.md §8(c) "Common rules"):
@@ -398,7 +399,13 @@ def _cors(op, y, x, r, r0sq, tol2, maxit, ctx, hist, st, shadow=None):
 
 
 # ---------------------------------------------------------------------------
-# Pins only (not on the hot path): BiCG, CGS, COCR (§3.4).
+# The rest of the catalogue on the same kernels:
+# BiCG ("bigcg", §2.1), CGS (§2.1), CGNR ("cgmr" in P:57 §2.1, read
+# as PIM's CGNR — DESIGN.md R5), COCR (§3.4, Sogabe–Zhang).  The paper
+# writes none of them down; the recurrences are the standard published ones
+# (BiCG/CGS/CGNR: Templates / PIM; COCR: Sogabe–Zhang 2007), in the same
+# common rules as O1-O5.  They also serve as pins of O4/O5:
+# BiCOR ≡ BiCG(shadow Aᴴr₀*), CORS ≡ CGS(shadow Aᴴr₀*), BiCOR(conj r₀) ≡ COCR.
 # ---------------------------------------------------------------------------
 def _bicg(op, y, x, r, r0sq, tol2, maxit, ctx, hist, st, shadow=None):
     rt = r.copy() if shadow is None else np.array(shadow, dtype=y.dtype, copy=True)
@@ -406,22 +413,24 @@ def _bicg(op, y, x, r, r0sq, tol2, maxit, ctx, hist, st, shadow=None):
     rho_prev = None
     for k in range(1, maxit + 1):
         st["k"] = k
-        rho = ctx.c(ctx.dotc(rt, r))
+        rho = ctx.c(ctx.dotc(rt, r))                            # ρ = ⟨r̃, r⟩
+        ctx.check(rho)
         if rho == 0:
             raise _Breakdown("rho")
         if k == 1:
-            p, pt = r.copy(), rt.copy()
+            p, pt = r.copy(), rt.copy()                         # p = r, p̃ = r̃
         else:
-            beta = ctx.c(rho / rho_prev)
-            p = r + beta * p
-            pt = rt + ctx.c(beta.conjugate()) * pt
-        q = op.apply(p)
-        qt = op.apply_h(pt)
-        alpha = ctx.c(ctx.div(rho, ctx.dotc(pt, q), "sigma"))
-        st["x"] = x = x + alpha * p
-        r = r - alpha * q
-        rt = rt - ctx.c(alpha.conjugate()) * qt
+            beta = ctx.c(rho / rho_prev)                        # β = ρ/ρ_prev
+            p = r + beta * p                                    # p = r + βp
+            pt = rt + ctx.c(beta.conjugate()) * pt              # p̃ = r̃ + conj(β)p̃
+        q = op.apply(p)                                         # q = A p
+        qt = op.apply_h(pt)                                     # q̃ = Aᴴ p̃
+        alpha = ctx.c(ctx.div(rho, ctx.c(ctx.dotc(pt, q)), "sigma"))   # α = ρ/⟨p̃, q⟩
+        st["x"] = x = x + alpha * p                             # x += αp
+        r = r - alpha * q                                       # r −= αq
+        rt = rt - ctx.c(alpha.conjugate()) * qt                 # r̃ −= conj(α)q̃
         rr = ctx.r(ctx.norm_sq(r))
+        ctx.check(rr)
         hist.append(sqrt(rr))
         if _conv(rr, tol2, r0sq):
             return CONVERGED, k, False
@@ -435,23 +444,25 @@ def _cgs(op, y, x, r, r0sq, tol2, maxit, ctx, hist, st, shadow=None):
     rho_prev = None
     for k in range(1, maxit + 1):
         st["k"] = k
-        rho = ctx.c(ctx.dotc(rt, r))
+        rho = ctx.c(ctx.dotc(rt, r))                            # ρ = ⟨r̃, r⟩
+        ctx.check(rho)
         if rho == 0:
             raise _Breakdown("rho")
         if k == 1:
-            u = r.copy()
-            p = u.copy()
+            u = r.copy()                                        # u = r
+            p = u.copy()                                        # p = u
         else:
-            beta = ctx.c(rho / rho_prev)
-            u = r + beta * q
-            p = u + beta * (q + beta * p)
-        v = op.apply(p)
-        alpha = ctx.c(ctx.div(rho, ctx.dotc(rt, v), "sigma"))
-        q = u - alpha * v
+            beta = ctx.c(rho / rho_prev)                        # β = ρ/ρ_prev
+            u = r + beta * q                                    # u = r + βq
+            p = u + beta * (q + beta * p)                       # p = u + β(q + βp)
+        v = op.apply(p)                                         # v = A p
+        alpha = ctx.c(ctx.div(rho, ctx.c(ctx.dotc(rt, v)), "sigma"))   # α = ρ/⟨r̃, v⟩
+        q = u - alpha * v                                       # q = u − αv
         uq = u + q
-        st["x"] = x = x + alpha * uq
-        r = r - alpha * op.apply(uq)
+        st["x"] = x = x + alpha * uq                            # x += α(u + q)
+        r = r - alpha * op.apply(uq)                            # r −= α A(u + q)
         rr = ctx.r(ctx.norm_sq(r))
+        ctx.check(rr)
         hist.append(sqrt(rr))
         if _conv(rr, tol2, r0sq):
             return CONVERGED, k, False
@@ -460,35 +471,70 @@ def _cgs(op, y, x, r, r0sq, tol2, maxit, ctx, hist, st, shadow=None):
 
 
 def _cocr(op, y, x, r, r0sq, tol2, maxit, ctx, hist, st):
-    Ar = op.apply(r)
-    p, Ap = r.copy(), Ar.copy()
-    mu = ctx.c(ctx.dotu(r, Ar))
+    """COCR (§3.4): for complex-symmetric A (A = Aᵀ) the CR recurrence
+    with the unconjugated bilinear form [u, v] = Σ uᵢvᵢ; one A·x per iteration."""
+    Ar = op.apply(r)                                            # A r₀
+    p, Ap = r.copy(), Ar.copy()                                 # p = r, Ap = Ar
+    mu = ctx.c(ctx.dotu(r, Ar))                                 # μ = [r, Ar]
+    beta = None
     for k in range(1, maxit + 1):
         st["k"] = k
         if k > 1:
-            p = r + beta * p
-            Ap = Ar + beta * Ap
-        alpha = ctx.c(ctx.div(mu, ctx.dotu(Ap, Ap), "xi"))
-        st["x"] = x = x + alpha * p
-        r = r - alpha * Ap
+            p = r + beta * p                                    # p = r + βp
+            Ap = Ar + beta * Ap                                 # Ap = Ar + βAp
+        alpha = ctx.c(ctx.div(mu, ctx.c(ctx.dotu(Ap, Ap)), "xi"))   # α = μ/[Ap, Ap]
+        st["x"] = x = x + alpha * p                             # x += αp
+        r = r - alpha * Ap                                      # r −= αAp
         rr = ctx.r(ctx.norm_sq(r))
+        ctx.check(rr)
         hist.append(sqrt(rr))
         if _conv(rr, tol2, r0sq):
             return CONVERGED, k, False
-        Ar = op.apply(r)
-        mu_new = ctx.c(ctx.dotu(r, Ar))
-        beta = ctx.c(ctx.div(mu_new, mu, "rho"))
+        if k == maxit:              # no further iterate needs A r (as CGNE, DESIGN.md R2)
+            break
+        Ar = op.apply(r)                                        # A r
+        mu_new = ctx.c(ctx.dotu(r, Ar))                         # μ' = [r, Ar]
+        beta = ctx.c(ctx.div(mu_new, mu, "rho"))                # β = μ'/μ
         mu = mu_new
+    return MAXIT, maxit, False
+
+
+def _cgnr(op, y, x, r, r0sq, tol2, maxit, ctx, hist, st):
+    """CGNR (§2.1 "cgmr", read as PIM's CGNR — DESIGN.md R5): CG on the
+    normal equations AᴴA x = Aᴴy; stops on the residual y − A·x of the original
+    system like every other method (common rules)."""
+    z = op.apply_h(r)                                           # z = Aᴴ r
+    p = z.copy()                                                # p = z
+    gamma = ctx.r(ctx.norm_sq(z))                               # γ = ‖z‖²
+    for k in range(1, maxit + 1):
+        st["k"] = k
+        w = op.apply(p)                                         # w = A p
+        alpha = ctx.r(ctx.div(gamma, ctx.r(ctx.norm_sq(w)), "pi"))     # α = γ/‖w‖²
+        st["x"] = x = x + alpha * p                             # x += αp
+        r = r - alpha * w                                       # r −= αw
+        rr = ctx.r(ctx.norm_sq(r))
+        ctx.check(rr)
+        hist.append(sqrt(rr))
+        if _conv(rr, tol2, r0sq):
+            return CONVERGED, k, False
+        if k == maxit:              # no further iterate needs the next direction
+            break
+        z = op.apply_h(r)                                       # z = Aᴴ r
+        gamma_new = ctx.r(ctx.norm_sq(z))
+        beta = ctx.r(gamma_new / gamma)                         # β = γ'/γ
+        p = z + beta * p                                        # p = z + βp
+        gamma = gamma_new
     return MAXIT, maxit, False
 
 
 METHODS = {
     "bicgstab": _bicgstab, "cgne": _cgne, "qmr": _qmr, "bicor": _bicor,
     "cors": _cors,
-    # pins only
-    "bicg": _bicg, "cgs": _cgs, "cocr": _cocr,
+    # SURVEY §8(f) NEXT-3
+    "bicg": _bicg, "cgs": _cgs, "cocr": _cocr, "cgnr": _cgnr,
 }
 HOT_PATH = ("bicgstab", "cgne", "qmr", "bicor", "cors")
+NEXT3 = ("bicg", "cgs", "cocr", "cgnr")
 
 
 def solve(method, op, y, tol, maxit, x0=None, dots=None, **kw):

@@ -1,0 +1,172 @@
+"""Pins for the SURVEY §8(f) NEXT-3 oracle recurrences: BiCG, CGS, CGNR (P:57
+§2.1) and COCR (§3.4).  CPU only.
+
+Each is fixed by something other than itself:
+
+* exact Gaussian-rational arithmetic: finite termination with A·x == y
+  exactly at iteration n (generic A; complex-symmetric A for COCR);
+* textbook reductions checked by dense linear algebra over an explicit Krylov
+  basis: BiCG with shadow r₀ on Hermitian positive definite A is CG, whose
+  iterate minimises the A-norm error over K_k(A, y); CGNR's iterate minimises
+  ‖y − Ax‖ over K_k(AᴴA, Aᴴy); COCR on real symmetric A with a real right-hand
+  side is CR, whose iterate minimises ‖y − Ax‖ over K_k(A, y);
+* special cases (A = cI), the LU solution, scale invariance, work accounting,
+  the breakdown fixture.
+
+A dropped conjugation (e.g. conj(β) in BiCG's shadow update, or a conjugated
+product in COCR) breaks the Krylov-minimisation or termination pins.
+"""
+
+import numpy as np
+import pytest
+
+from oracle import solve, DenseOp
+from oracle.solvers import CONVERGED, MAXIT, BREAKDOWN, NEXT3
+from oracle.exact import to_exact
+from oracle.direct import lu_solve
+from workloads import dense_random, cfg1
+
+
+def _rand_int(n, seed, kind):
+    rng = np.random.default_rng(seed)
+    B = rng.integers(-4, 5, (n, n)) + 1j * rng.integers(-4, 5, (n, n))
+    if kind == "hpd":
+        A = B @ B.conj().T + np.eye(n)
+    elif kind == "csym":
+        A = B + B.T + 6 * np.eye(n)
+    else:
+        A = B + 6 * np.eye(n)
+    y = rng.integers(-3, 4, n) + 1j * rng.integers(-3, 4, n)
+    return A.astype(np.complex128), y.astype(np.complex128)
+
+
+def _krylov(M, v, k):
+    K = np.empty((len(v), k), dtype=np.complex128)
+    K[:, 0] = v
+    for j in range(1, k):
+        K[:, j] = M @ K[:, j - 1]
+    Q, _ = np.linalg.qr(K)
+    return Q
+
+
+@pytest.mark.parametrize("n", [3, 4, 5, 6])
+@pytest.mark.parametrize("method,kind", [("bicg", "gen"), ("bicg", "hpd"), ("cgs", "gen"), ("cgs", "hpd"),
+                                         ("cgnr", "gen"), ("cgnr", "hpd"), ("cocr", "csym")])
+def test_exact_finite_termination(method, kind, n):
+    A, y = _rand_int(n, seed=17 * n + len(kind), kind=kind)
+    Ae, ye = to_exact(A), to_exact(y)
+    op = DenseOp(Ae)
+    res = solve(method, op, ye, 0.0, n + 3)
+    assert res.status == CONVERGED, (res.status_name, res.breakdown)
+    assert res.iterations <= n
+    assert all(v == 0 for v in ye - op.apply(res.x)), "A·x must equal y exactly"
+    if kind != "hpd":
+        assert res.iterations == n
+
+
+def test_bicg_is_cg_on_hpd():
+    """BiCG, shadow r₀, Hermitian positive definite A = CG: x_k minimises
+    (x − x*)ᴴA(x − x*) over K_k(A, y)  ⇔  (QᴴAQ)c = Qᴴy, x_k = Qc."""
+    n = 40
+    rng = np.random.default_rng(3)
+    B = rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))
+    A = B @ B.conj().T / n + 0.5 * np.eye(n)
+    y = rng.standard_normal(n) + 1j * rng.standard_normal(n)
+    for k in range(1, 9):
+        res = solve("bicg", DenseOp(A), y, 0.0, k)
+        assert res.iterations == k
+        Q = _krylov(A, y, k)
+        xm = Q @ np.linalg.solve(Q.conj().T @ A @ Q, Q.conj().T @ y)
+        assert np.linalg.norm(res.x - xm) <= 1e-10 * np.linalg.norm(xm), k
+
+
+def test_cgnr_minimises_residual_over_normal_krylov_space():
+    n = 40
+    A = dense_random(n, seed=71, shift=1.5 - 0.5j)
+    y = dense_random(n, seed=72)[:, 0]
+    prev = np.inf
+    for k in range(1, 9):
+        res = solve("cgnr", DenseOp(A), y, 0.0, k)
+        assert res.iterations == k
+        Q = _krylov(A.conj().T @ A, A.conj().T @ y, k)
+        c, *_ = np.linalg.lstsq(A @ Q, y, rcond=None)
+        xm = Q @ c
+        assert np.linalg.norm(res.x - xm) <= 1e-9 * np.linalg.norm(xm), k
+        rn = np.linalg.norm(y - A @ res.x)
+        assert rn <= prev * (1 + 1e-12)
+        prev = rn
+
+
+@pytest.mark.parametrize("definite", [True, False])
+def test_cocr_is_cr_on_real_symmetric(definite):
+    """Real symmetric A (= Aᵀ = Aᴴ) and real y: [·,·] = ⟨·,·⟩ on the real
+    iterates, COCR = CR = residual minimisation over K_k(A, y)."""
+    n = 40
+    rng = np.random.default_rng(11)
+    B = rng.standard_normal((n, n))
+    A = ((B + B.T) / 2 + (10 * np.eye(n) if definite else 0.2 * np.eye(n))).astype(np.complex128)
+    y = rng.standard_normal(n).astype(np.complex128)
+    for k in range(1, 9):
+        res = solve("cocr", DenseOp(A), y, 0.0, k)
+        assert res.iterations == k
+        Q = _krylov(A, y, k)
+        c, *_ = np.linalg.lstsq(A @ Q, y, rcond=None)
+        xm = Q @ c
+        assert np.linalg.norm(res.x - xm) <= 1e-9 * np.linalg.norm(xm), k
+
+
+@pytest.mark.parametrize("method", NEXT3)
+def test_scaled_identity_one_iteration(method):
+    c = 3 - 4j
+    n = 10
+    rng = np.random.default_rng(0)
+    y = rng.standard_normal(n) + 1j * rng.standard_normal(n)
+    res = solve(method, DenseOp(c * np.eye(n, dtype=np.complex128)), y, 1e-12, 50)
+    assert res.status == CONVERGED and res.iterations == 1
+    np.testing.assert_allclose(res.x, y / c, rtol=1e-15, atol=1e-15)
+
+
+@pytest.mark.parametrize("n", [8, 16, 64])
+@pytest.mark.parametrize("method", NEXT3)
+def test_matches_lu(method, n):
+    A = dense_random(n, seed=n + 5, shift=3 - 1j)
+    if method == "cocr":
+        A = (A + A.T) / 2
+    rng = np.random.default_rng(n)
+    xs = rng.standard_normal(n) + 1j * rng.standard_normal(n)
+    y = A @ xs
+    res = solve(method, DenseOp(A), y, 1e-12, 10 * n)
+    assert res.status == CONVERGED
+    xl = lu_solve(A, y)
+    assert np.linalg.norm(res.x - xl) <= 1e-9 * np.linalg.norm(xl)
+    assert res.true_rel_res <= 10 * 1e-12 and res.rec_rel_res <= 1e-12
+
+
+@pytest.mark.parametrize("method", NEXT3)
+def test_scale_invariance(method):
+    A, y = cfg1(n=64, seed=3)
+    if method == "cocr":
+        A = (A + A.T) / 2
+    c = 3 - 4j
+    a = solve(method, DenseOp(A), y, 1e-10, 300)
+    b = solve(method, DenseOp(c * A), c * y, 1e-10, 300)
+    assert a.iterations == b.iterations
+    assert np.linalg.norm(a.x - b.x) <= 1e-8 * np.linalg.norm(a.x)
+
+
+def test_work_accounting():
+    A, y = cfg1(n=64, seed=4)
+    for m, want in {"bicg": (5, 5), "cgs": (10, 0), "cocr": (5, 0), "cgnr": (5, 5)}.items():
+        res = solve(m, DenseOp(A), y, 0.0, 5)
+        assert res.status == MAXIT and res.iterations == 5
+        assert (res.matvecs_a, res.matvecs_ah) == want, m
+
+
+def test_breakdown_fixture():
+    A = np.array([[0, 1], [-1, 0]], dtype=np.complex128)
+    y = np.array([1, 0], dtype=np.complex128)
+    for m, name in (("bicg", "sigma"), ("cgs", "sigma"), ("cocr", "rho")):
+        r = solve(m, DenseOp(A), y, 1e-10, 10)
+        assert r.status == BREAKDOWN and r.breakdown == name and r.iterations == 0, m
+    r = solve("cgnr", DenseOp(A), y, 1e-10, 10)      # A unitary: CGNR converges at once
+    assert r.status == CONVERGED and r.iterations == 1
