@@ -55,14 +55,22 @@ typedef enum { CCG_C64 = 0, CCG_C128 = 1 } ccg_dtype;
 /* Methods on the hot path (BASELINE.json north_star).  BiCGSTAB, CGNE, QMR:
  * PIM90 set (P:57 [§2.1]; QMR as corrected, P:101 [§6]).  BiCOR, CORS:
  * Carpentieri-Jing-Huang (P:69 [§2.4]).  Recurrences: SURVEY §8(c) O1-O5 /
- * DESIGN.md.  Operator needs: BiCGSTAB, CORS -> A·x only; CGNE, QMR, BiCOR ->
- * A·x and Aᴴ·x. */
+ * DESIGN.md.  The rest of the catalogue on the same kernels (SURVEY §8(f)
+ * NEXT-3): BiCG ("bigcg"), CGS, CGNR ("cgmr", read as CGNR) of the PIM90 set
+ * (P:57 [§2.1]) and COCR (P:87 [§3.4]; meant for complex-symmetric A = Aᵀ —
+ * the library does not check symmetry).  Recurrences: DESIGN.md §2.
+ * Operator needs: BiCGSTAB, CORS, CGS, COCR -> A·x only; CGNE, QMR, BiCOR,
+ * BiCG, CGNR -> A·x and Aᴴ·x. */
 typedef enum {
   CCG_BICGSTAB = 0,
   CCG_CGNE = 1,
   CCG_QMR = 2,
   CCG_BICOR = 3,
-  CCG_CORS = 4
+  CCG_CORS = 4,
+  CCG_BICG = 5,
+  CCG_CGS = 6,
+  CCG_COCR = 7,
+  CCG_CGNR = 8
 } ccg_method;
 
 /* The three products of the operator module: A·x (matvec),

@@ -92,8 +92,8 @@ struct ccg_ctx {
   // comm
   Comm* comm = nullptr;  // NcclComm or LoopbackComm (world > 1)
   // graphs per method
-  cudaGraphExec_t gexec[5] = {};
-  int64_t graph_launches_per_iter[5] = {};
+  cudaGraphExec_t gexec[M_COUNT] = {};
+  int64_t graph_launches_per_iter[M_COUNT] = {};
   // launch parameters
   int sm_count = 148;
   int gemv_grid = 0, ah_S = 1, ah_strips = 1, pass_grid = 0, stage2_grid = 0, spmv_grid = 0;
@@ -509,13 +509,77 @@ struct Engine {
     return pass(c, CoH<T>{L(c, 4), L(c, 5), Fs(c, 1), L(c, 8), L(c, 6), L(c, 7), L(c, X), Fs(c, 0)}, g);
   }
 
+  // ==================== SURVEY §8(f) NEXT-3 ====================
+  // A·p and Aᴴ·p̃ of one BiCG iteration are independent: dual GEMV when dense
+  template <class EpiA, class EpiH>
+  static int matvec_pair(ccg_ctx* c, int pfull_idx, const C* qloc, EpiA ea, EpiH eh, const int* gate) {
+    if (c->opk == OPK_DENSE && c->cols_ok && c->qmr_dual)
+      return matvec_dual(c, F(c, pfull_idx), qloc, ea, eh, gate);
+    TRY(matvec_a(c, F(c, pfull_idx), ea, gate));
+    return matvec_h(c, qloc, true, eh, gate);
+  }
+
+  // ---- BiCG: loc: 0 x, 1 y, 2 r, 3 rt, 4 pt, 5 q, 6 qt ; full: 0 p
+  static int bicg_setup(ccg_ctx* c, bool x0) { return init_residual(c, x0, L(c, 2), L(c, 3), nullptr, nullptr); }
+  static int bicg_iter(ccg_ctx* c) {
+    const int* g = &c->st->done;
+    TRY(pass(c, BgP<T>{L(c, 2), L(c, 3), Fs(c, 0), L(c, 4)}, g));
+    TRY(allgather(c, 0));
+    TRY(matvec_pair(c, 0, L(c, 4), BgQ<T>{L(c, 5), L(c, 4)}, Store<T>{L(c, 6)}, g));
+    return pass(c, BgX<T>{L(c, X), L(c, 2), L(c, 3), Fs(c, 0), L(c, 5), L(c, 6)}, g);
+  }
+
+  // ---- CGS: loc: 0 x, 1 y, 2 r, 3 rt, 4 u, 5 q, 6 v ; full: 0 p, 1 u+q
+  static int cgs_setup(ccg_ctx* c, bool x0) { return init_residual(c, x0, L(c, 2), L(c, 3), nullptr, nullptr); }
+  static int cgs_iter(ccg_ctx* c) {
+    const int* g = &c->st->done;
+    TRY(pass(c, CsP<T>{L(c, 2), L(c, 5), Fs(c, 0), L(c, 4)}, g));
+    TRY(allgather(c, 0));
+    TRY(matvec_a(c, F(c, 0), CsV<T>{L(c, 6), L(c, 3)}, g));
+    TRY(pass(c, CsQ<T>{L(c, 4), L(c, 6), L(c, 5), Fs(c, 1), L(c, X)}, g));
+    TRY(allgather(c, 1));
+    return matvec_a(c, F(c, 1), CsR<T>{L(c, 2), L(c, 3)}, g);
+  }
+
+  // ---- COCR: loc: 0 x, 1 y, 2 Ar, 3 p, 4 Ap ; full: 0 r
+  static int cocr_setup(ccg_ctx* c, bool x0) {
+    TRY(init_residual(c, x0, Fs(c, 0), nullptr, nullptr, nullptr));
+    TRY(allgather(c, 0));
+    return matvec_a(c, F(c, 0), CrAr0<T>{L(c, 2), Fs(c, 0)}, &c->st->done);
+  }
+  static int cocr_iter(ccg_ctx* c) {
+    const int* g = &c->st->done;
+    TRY(pass(c, CrP<T>{Fs(c, 0), L(c, 2), L(c, 3), L(c, 4)}, g));
+    TRY(pass(c, CrX<T>{L(c, X), Fs(c, 0), L(c, 3), L(c, 4)}, g));
+    TRY(allgather(c, 0));
+    return matvec_a(c, F(c, 0), CrAr<T>{L(c, 2), Fs(c, 0)}, g);
+  }
+
+  // ---- CGNR: loc: 0 x, 1 y, 2 r, 3 w, 4 z ; full: 0 p
+  static int cgnr_setup(ccg_ctx* c, bool x0) {
+    TRY(init_residual(c, x0, L(c, 2), nullptr, nullptr, nullptr));
+    return matvec_h(c, L(c, 2), true, CnZ0<T>{Fs(c, 0)}, &c->st->done);
+  }
+  static int cgnr_iter(ccg_ctx* c) {
+    const int* g = &c->st->done;
+    TRY(allgather(c, 0));
+    TRY(matvec_a(c, F(c, 0), CnW<T>{L(c, 3)}, g));
+    TRY(pass(c, CnX<T>{L(c, X), L(c, 2), Fs(c, 0), L(c, 3)}, g));
+    TRY(matvec_h(c, L(c, 2), true, CnZ<T>{L(c, 4)}, g));
+    return pass(c, CnP<T>{L(c, 4), Fs(c, 0)}, g);
+  }
+
   static int setup(ccg_ctx* c, int m, bool x0) {
     switch (m) {
       case M_BICGSTAB: return bicgstab_setup(c, x0);
       case M_CGNE: return cgne_setup(c, x0);
       case M_QMR: return qmr_setup(c, x0);
       case M_BICOR: return bicor_setup(c, x0);
-      default: return cors_setup(c, x0);
+      case M_CORS: return cors_setup(c, x0);
+      case M_BICG: return bicg_setup(c, x0);
+      case M_CGS: return cgs_setup(c, x0);
+      case M_COCR: return cocr_setup(c, x0);
+      default: return cgnr_setup(c, x0);
     }
   }
   static int iter(ccg_ctx* c, int m) {
@@ -524,7 +588,11 @@ struct Engine {
       case M_CGNE: return cgne_iter(c);
       case M_QMR: return qmr_iter(c);
       case M_BICOR: return bicor_iter(c);
-      default: return cors_iter(c);
+      case M_CORS: return cors_iter(c);
+      case M_BICG: return bicg_iter(c);
+      case M_CGS: return cgs_iter(c);
+      case M_COCR: return cocr_iter(c);
+      default: return cgnr_iter(c);
     }
   }
 
@@ -714,7 +782,7 @@ static void free_csr_copies(ccg_ctx* c) {
 }
 
 static void invalidate_graphs(ccg_ctx* c) {
-  for (int m = 0; m < 5; ++m) {
+  for (int m = 0; m < M_COUNT; ++m) {
     if (c->gexec[m]) cudaGraphExecDestroy(c->gexec[m]);
     c->gexec[m] = nullptr;
   }
@@ -1036,7 +1104,9 @@ static int stage_out(ccg_ctx* c, void* dst, const void* src, size_t bytes) {
   return CCG_OK;
 }
 
-static bool needs_ah(int m) { return m == CCG_CGNE || m == CCG_QMR || m == CCG_BICOR; }
+static bool needs_ah(int m) {
+  return m == CCG_CGNE || m == CCG_QMR || m == CCG_BICOR || m == CCG_BICG || m == CCG_CGNR;
+}
 
 int ccg_apply(ccg_handle c, ccg_op op, const void* x_local, void* y_local) {
   if (!c) return CCG_E_ARG;
@@ -1068,7 +1138,7 @@ int ccg_solve(ccg_handle c, ccg_method method, const void* x0_local, const void*
   auto t_start = std::chrono::steady_clock::now();
   if (!c) return CCG_E_ARG;
   if (!y_local || !x_local_out || !res) FAIL(c, CCG_E_ARG, "NULL y/x_out/res");
-  if ((int)method < 0 || (int)method > 4) FAIL(c, CCG_E_ARG, "bad method");
+  if ((int)method < 0 || (int)method >= M_COUNT) FAIL(c, CCG_E_ARG, "bad method");
   if (!(tol >= 0.0) || maxit < 1) FAIL(c, CCG_E_ARG, "tol must be >= 0 and maxit >= 1");
   if (c->opk == OPK_NONE) FAIL(c, CCG_E_STATE, "no operator set (call ccg_set_matvec_*)");
   if (needs_ah(method) && c->opk == OPK_CSR && (!(c->flags & CCG_FLAG_SYMMETRIC) || c->world > 1))

@@ -68,6 +68,12 @@ template <typename C> __device__ __forceinline__ void dotc_acc(double2& acc, C a
   acc.x = fma(ax, bx, acc.x); acc.x = fma(ay, by, acc.x);
   acc.y = fma(ax, by, acc.y); acc.y = fma(-ay, bx, acc.y);
 }
+// acc += a*b (unconjugated bilinear form [a, b], COCR)
+template <typename C> __device__ __forceinline__ void dotu_acc(double2& acc, C a, C b) {
+  double ax = a.x, ay = a.y, bx = b.x, by = b.y;
+  acc.x = fma(ax, bx, acc.x); acc.x = fma(-ay, by, acc.x);
+  acc.y = fma(ax, by, acc.y); acc.y = fma(ay, bx, acc.y);
+}
 template <typename C> __device__ __forceinline__ void nrm_acc(double2& acc, C a) {
   double ax = a.x, ay = a.y;
   acc.x = fma(ax, ax, acc.x); acc.x = fma(ay, ay, acc.x);
@@ -126,7 +132,8 @@ struct State {
 enum { ST_CONVERGED = 0, ST_MAXIT = 1, ST_BREAKDOWN = 2, ST_FALSE_CONV = 3, ST_NONFINITE = 4 };
 enum { BD_NONE = 0, BD_RHO = 1, BD_SIGMA = 2, BD_TT = 3, BD_OMEGA = 4, BD_PI = 5, BD_DELTA = 6,
        BD_EPSILON = 7, BD_BETA = 8, BD_XI = 9, BD_VNORM = 10, BD_WNORM = 11, BD_GAMMA = 12 };
-enum { M_BICGSTAB = 0, M_CGNE = 1, M_QMR = 2, M_BICOR = 3, M_CORS = 4 };
+enum { M_BICGSTAB = 0, M_CGNE = 1, M_QMR = 2, M_BICOR = 3, M_CORS = 4,
+       M_BICG = 5, M_CGS = 6, M_COCR = 7, M_CGNR = 8, M_COUNT = 9 };
 
 __device__ __forceinline__ void set_done(State* st, int status, int iters, int bd = BD_NONE) {
   st->done = 1; st->gate2 = 1; st->status = status; st->iterations = iters; st->breakdown = bd;

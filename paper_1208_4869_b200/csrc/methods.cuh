@@ -61,7 +61,9 @@ struct InitR {
     if (!isfinite(rr)) { set_done(st, ST_NONFINITE, 0); return; }
     if (rr == 0.0) { set_done(st, ST_CONVERGED, 0); return; }
     switch (st->method) {
-      case M_BICGSTAB: st->rho = make_double2(rr, 0.0); break;
+      case M_BICGSTAB:
+      case M_BICG:
+      case M_CGS: st->rho = make_double2(rr, 0.0); break;
       case M_CGNE: st->rho_r = rr; break;
       case M_QMR:
         st->rnrm = sqrt(rr); st->xnrm = sqrt(rr);
@@ -559,6 +561,299 @@ struct CoH {  // h = e − αq̂ ; ĥ = ê − αq ; x += α(e + h) ; r −= α(
     nrm_acc(acc[0], ri);
   }
   static __device__ void finish(State* st, const double2* s) { r_step(st, s[0].x); }
+};
+
+// ===========================================================================
+// BiCG, CGS, CGNR (§2.1), COCR (§3.4) on the
+// same matvec engine and fused passes (recurrences restated in DESIGN.md §2).
+// ===========================================================================
+// ρ' = ⟨r̃, r⟩ read at the end of an iteration (BiCG, CGS): after the
+// convergence test; zero → BREAKDOWN(rho) with k completed (the oracle raises
+// at the top of iteration k+1).
+__device__ __forceinline__ void next_rho(State* st, int k, double rr, double2 rho_new) {
+  bool stop;
+  conv_check_common(st, k, rr, stop);
+  if (stop) return;
+  if (!zfinite(rho_new)) { set_done(st, ST_NONFINITE, k); return; }
+  if (zzero(rho_new)) { set_done(st, ST_BREAKDOWN, k, BD_RHO); return; }
+  st->beta = zdiv(rho_new, st->rho);
+  st->rho = rho_new;
+  st->iter = k;
+}
+__device__ __forceinline__ void sigma_step(State* st, double2 sigma) {
+  const int k = st->iter + 1;
+  if (zzero(sigma)) { set_done(st, ST_BREAKDOWN, k - 1, BD_SIGMA); return; }
+  st->alpha = zdiv(st->rho, sigma);
+  if (!zfinite(st->alpha)) { set_done(st, ST_NONFINITE, k - 1); return; }
+}
+
+// ---- BiCG.  P → [A p → q, σ = ⟨p̃, q⟩ ; Aᴴ p̃ → q̃] → X
+template <typename T>
+struct BgP {  // p = r + βp ; p̃ = r̃ + conj(β)p̃   (k=1: copies)
+  static constexpr int K = 0;
+  using C = Cx<T>;
+  const C* r; const C* rt; C* p; C* pt;
+  C beta, cbeta; int first;
+  __device__ void load(const State* st) {
+    first = st->iter == 0; beta = fromd2<C>(st->beta); cbeta = fromd2<C>(zconj(st->beta));
+  }
+  __device__ void operator()(int64_t i, double2*) {
+    if (first) { p[i] = r[i]; pt[i] = rt[i]; return; }
+    p[i] = caxpy(r[i], beta, p[i]);
+    pt[i] = caxpy(rt[i], cbeta, pt[i]);
+  }
+  static __device__ void finish(State*, const double2*) {}
+};
+
+template <typename T>
+struct BgQ {  // q = A p ; σ = ⟨p̃, q⟩ ; α = ρ/σ   (counts the paired Aᴴp̃ too)
+  static constexpr int K = 1;
+  using C = Cx<T>;
+  C* q; const C* pt;
+  __device__ void load(const State*) {}
+  __device__ void operator()(int64_t i, C val, double2* acc) { q[i] = val; dotc_acc(acc[0], pt[i], val); }
+  static __device__ void finish(State* st, const double2* s) {
+    st->matvecs_a++;
+    st->matvecs_ah++;
+    sigma_step(st, s[0]);
+  }
+};
+
+template <typename T>
+struct BgX {  // x += αp ; r −= αq ; r̃ −= conj(α)q̃ ; ‖r‖², ⟨r̃, r⟩
+  static constexpr int K = 2;
+  using C = Cx<T>;
+  C* x; C* r; C* rt; const C* p; const C* q; const C* qt;
+  C alpha, calpha;
+  __device__ void load(const State* st) { alpha = fromd2<C>(st->alpha); calpha = fromd2<C>(zconj(st->alpha)); }
+  __device__ void operator()(int64_t i, double2* acc) {
+    x[i] = caxpy(x[i], alpha, p[i]);
+    const C ri = caxmy(r[i], alpha, q[i]);
+    const C rti = caxmy(rt[i], calpha, qt[i]);
+    r[i] = ri; rt[i] = rti;
+    nrm_acc(acc[0], ri);
+    dotc_acc(acc[1], rti, ri);
+  }
+  static __device__ void finish(State* st, const double2* s) { next_rho(st, st->iter + 1, s[0].x, s[1]); }
+};
+
+// ---- CGS.  P → [A p → v, σ = ⟨r̃, v⟩] → Q → [A(u+q) → r −= α·, ‖r‖², ⟨r̃, r⟩]
+template <typename T>
+struct CsP {  // u = r + βq ; p = u + β(q + βp)   (k=1: u = p = r)
+  static constexpr int K = 0;
+  using C = Cx<T>;
+  const C* r; const C* q; C* p; C* u;
+  C beta; int first;
+  __device__ void load(const State* st) { first = st->iter == 0; beta = fromd2<C>(st->beta); }
+  __device__ void operator()(int64_t i, double2*) {
+    if (first) { const C ri = r[i]; u[i] = ri; p[i] = ri; return; }
+    const C qi = q[i];
+    const C ui = caxpy(r[i], beta, qi);
+    u[i] = ui;
+    p[i] = caxpy(ui, beta, caxpy(qi, beta, p[i]));
+  }
+  static __device__ void finish(State*, const double2*) {}
+};
+
+template <typename T>
+struct CsV {  // v = A p ; σ = ⟨r̃, v⟩ ; α = ρ/σ
+  static constexpr int K = 1;
+  using C = Cx<T>;
+  C* v; const C* rt;
+  __device__ void load(const State*) {}
+  __device__ void operator()(int64_t i, C val, double2* acc) { v[i] = val; dotc_acc(acc[0], rt[i], val); }
+  static __device__ void finish(State* st, const double2* s) { st->matvecs_a++; sigma_step(st, s[0]); }
+};
+
+template <typename T>
+struct CsQ {  // q = u − αv ; u + q ; x += α(u + q)
+  static constexpr int K = 0;
+  using C = Cx<T>;
+  const C* u; const C* v; C* q; C* uq; C* x;
+  C alpha;
+  __device__ void load(const State* st) { alpha = fromd2<C>(st->alpha); }
+  __device__ void operator()(int64_t i, double2*) {
+    const C ui = u[i];
+    const C qi = caxmy(ui, alpha, v[i]);
+    q[i] = qi;
+    const C s = cadd(ui, qi);
+    uq[i] = s;
+    x[i] = caxpy(x[i], alpha, s);
+  }
+  static __device__ void finish(State*, const double2*) {}
+};
+
+template <typename T>
+struct CsR {  // r −= α A(u + q) ; ‖r‖², ⟨r̃, r⟩
+  static constexpr int K = 2;
+  using C = Cx<T>;
+  C* r; const C* rt;
+  C alpha;
+  __device__ void load(const State* st) { alpha = fromd2<C>(st->alpha); }
+  __device__ void operator()(int64_t i, C w, double2* acc) {
+    const C ri = caxmy(r[i], alpha, w);
+    r[i] = ri;
+    nrm_acc(acc[0], ri);
+    dotc_acc(acc[1], rt[i], ri);
+  }
+  static __device__ void finish(State* st, const double2* s) {
+    st->matvecs_a++;
+    next_rho(st, st->iter + 1, s[0].x, s[1]);
+  }
+};
+
+// ---- COCR (complex-symmetric A; unconjugated [u, v]).  Setup: [A r → Ar, μ].
+// Per iteration: P ([Ap, Ap] → α) → X (x, r, ‖r‖²) → [A r → Ar, μ' → β]
+template <typename T>
+struct CrAr0 {  // setup: Ar = A r₀ ; μ = [r₀, Ar₀]
+  static constexpr int K = 1;
+  using C = Cx<T>;
+  C* ar; const C* r;
+  __device__ void load(const State*) {}
+  __device__ void operator()(int64_t i, C val, double2* acc) { ar[i] = val; dotu_acc(acc[0], r[i], val); }
+  static __device__ void finish(State* st, const double2* s) { st->matvecs_a++; st->rho = s[0]; }
+};
+
+template <typename T>
+struct CrAr {  // Ar = A r ; μ' = [r, Ar] ; β = μ'/μ   (end of iteration k = iter)
+  static constexpr int K = 1;
+  using C = Cx<T>;
+  C* ar; const C* r;
+  __device__ void load(const State*) {}
+  __device__ void operator()(int64_t i, C val, double2* acc) { ar[i] = val; dotu_acc(acc[0], r[i], val); }
+  static __device__ void finish(State* st, const double2* s) {
+    st->matvecs_a++;
+    const int kc = st->iter - 1;   // the oracle raises inside iteration iter
+    if (zzero(st->rho)) { set_done(st, ST_BREAKDOWN, kc, BD_RHO); return; }
+    st->beta = zdiv(s[0], st->rho);
+    if (!zfinite(st->beta)) { set_done(st, ST_NONFINITE, kc); return; }
+    st->rho = s[0];
+  }
+};
+
+template <typename T>
+struct CrP {  // p = r + βp ; Ap = Ar + βAp (k=1: copies) ; [Ap, Ap] ; α = μ/[Ap, Ap]
+  static constexpr int K = 1;
+  using C = Cx<T>;
+  const C* r; const C* ar; C* p; C* ap;
+  C beta; int first;
+  __device__ void load(const State* st) { first = st->iter == 0; beta = fromd2<C>(st->beta); }
+  __device__ void operator()(int64_t i, double2* acc) {
+    C pi, api;
+    if (first) { pi = r[i]; api = ar[i]; }
+    else { pi = caxpy(r[i], beta, p[i]); api = caxpy(ar[i], beta, ap[i]); }
+    p[i] = pi; ap[i] = api;
+    dotu_acc(acc[0], api, api);
+  }
+  static __device__ void finish(State* st, const double2* s) {
+    const int k = st->iter + 1;
+    if (zzero(s[0])) { set_done(st, ST_BREAKDOWN, k - 1, BD_XI); return; }
+    st->alpha = zdiv(st->rho, s[0]);
+    if (!zfinite(st->alpha)) { set_done(st, ST_NONFINITE, k - 1); return; }
+  }
+};
+
+template <typename T>
+struct CrX {  // x += αp ; r −= αAp ; ‖r‖²
+  static constexpr int K = 1;
+  using C = Cx<T>;
+  C* x; C* r; const C* p; const C* ap;
+  C alpha;
+  __device__ void load(const State* st) { alpha = fromd2<C>(st->alpha); }
+  __device__ void operator()(int64_t i, double2* acc) {
+    x[i] = caxpy(x[i], alpha, p[i]);
+    const C ri = caxmy(r[i], alpha, ap[i]);
+    r[i] = ri;
+    nrm_acc(acc[0], ri);
+  }
+  static __device__ void finish(State* st, const double2* s) {
+    const int k = st->iter + 1;
+    bool stop;
+    conv_check_common(st, k, s[0].x, stop);
+    if (stop) return;
+    st->iter = k;
+  }
+};
+
+// ---- CGNR (CG on AᴴA x = Aᴴy).  Setup: [Aᴴ r → p = z, γ].  Per iteration:
+// [A p → w, ‖w‖² → α] → X (x, r, ‖r‖²) → [Aᴴ r → z, γ' → β] → P (p = z + βp)
+template <typename T>
+struct CnZ0 {  // setup: p = z = Aᴴ r₀ ; γ = ‖z‖²
+  static constexpr int K = 1;
+  using C = Cx<T>;
+  C* p;
+  __device__ void load(const State*) {}
+  __device__ void operator()(int64_t i, C w, double2* acc) { p[i] = w; nrm_acc(acc[0], w); }
+  static __device__ void finish(State* st, const double2* s) { st->matvecs_ah++; st->rho_r = s[0].x; }
+};
+
+template <typename T>
+struct CnW {  // w = A p ; α = γ/‖w‖²
+  static constexpr int K = 1;
+  using C = Cx<T>;
+  C* w;
+  __device__ void load(const State*) {}
+  __device__ void operator()(int64_t i, C val, double2* acc) { w[i] = val; nrm_acc(acc[0], val); }
+  static __device__ void finish(State* st, const double2* s) {
+    const int k = st->iter + 1;
+    st->matvecs_a++;
+    if (s[0].x == 0.0) { set_done(st, ST_BREAKDOWN, k - 1, BD_PI); return; }
+    st->alpha_r = st->rho_r / s[0].x;
+    if (!isfinite(st->alpha_r)) { set_done(st, ST_NONFINITE, k - 1); return; }
+  }
+};
+
+template <typename T>
+struct CnX {  // x += αp ; r −= αw ; ‖r‖²
+  static constexpr int K = 1;
+  using C = Cx<T>;
+  C* x; C* r; const C* p; const C* w;
+  T alpha;
+  __device__ void load(const State* st) { alpha = (T)st->alpha_r; }
+  __device__ void operator()(int64_t i, double2* acc) {
+    C xi = x[i], ri = r[i];
+    const C pi = p[i], wi = w[i];
+    xi.x += alpha * pi.x; xi.y += alpha * pi.y;
+    ri.x -= alpha * wi.x; ri.y -= alpha * wi.y;
+    x[i] = xi; r[i] = ri;
+    nrm_acc(acc[0], ri);
+  }
+  static __device__ void finish(State* st, const double2* s) {
+    const int k = st->iter + 1;
+    bool stop;
+    conv_check_common(st, k, s[0].x, stop);
+    if (stop) return;
+    st->iter = k;
+  }
+};
+
+template <typename T>
+struct CnZ {  // z = Aᴴ r ; γ' = ‖z‖² ; β = γ'/γ
+  static constexpr int K = 1;
+  using C = Cx<T>;
+  C* z;
+  __device__ void load(const State*) {}
+  __device__ void operator()(int64_t i, C w, double2* acc) { z[i] = w; nrm_acc(acc[0], w); }
+  static __device__ void finish(State* st, const double2* s) {
+    st->matvecs_ah++;
+    st->beta_r = s[0].x / st->rho_r;
+    st->rho_r = s[0].x;
+  }
+};
+
+template <typename T>
+struct CnP {  // p = z + βp
+  static constexpr int K = 0;
+  using C = Cx<T>;
+  const C* z; C* p;
+  T beta;
+  __device__ void load(const State* st) { beta = (T)st->beta_r; }
+  __device__ void operator()(int64_t i, double2*) {
+    const C zi = z[i], pi = p[i];
+    C v; v.x = zi.x + beta * pi.x; v.y = zi.y + beta * pi.y;
+    p[i] = v;
+  }
+  static __device__ void finish(State*, const double2*) {}
 };
 
 }  // namespace ccg

@@ -118,9 +118,12 @@ def test_sharded_dense_apply(G, dtype):
 
 
 @pytest.mark.parametrize("G", [2, 4])
-@pytest.mark.parametrize("method", ["bicgstab", "cgne", "qmr", "bicor", "cors"])
+@pytest.mark.parametrize("method", ["bicgstab", "cgne", "qmr", "bicor", "cors",
+                                    "bicg", "cgs", "cocr", "cgnr"])
 def test_sharded_cfg1_solve(G, method):
     A, y = cfg1()
+    if method == "cocr":
+        A = (A + A.T) / 2                      # COCR: complex-symmetric A
     g = DenseGroup(A, G)
     try:
         o = oracle.solve(method, DenseOp(A), y, 1e-10, 500)

@@ -86,3 +86,124 @@ def test_qmr_dual_c64_proxy(monkeypatch):
         ge = h.solve("qmr", y, 0.0, k)
     oe = oracle.solve("qmr", DenseOp(A), y, 0.0, k)
     assert relerr(ge["x"], oe.x) <= XTOL[np.complex64]
+
+
+# ---------------------------------------------------------------------------
+# NEXT-3: BiCG, CGS, CGNR (§2.1), COCR (§3.4) through ccg_solve
+# ---------------------------------------------------------------------------
+import paper_1208_4869_b200 as ccg                       # noqa: E402
+from oracle import CsrOp                                   # noqa: E402
+from oracle.solvers import NEXT3                           # noqa: E402
+from workloads import cfg1, helmholtz_csr, helmholtz_rhs   # noqa: E402
+from tests._gpu import Csr                                 # noqa: E402
+from tests.test_gpu_solve import _parity                   # noqa: E402
+
+
+def _csym(A):
+    return ((A + A.T) / 2).astype(A.dtype)
+
+
+@pytest.mark.parametrize("method", NEXT3)
+def test_next3_cfg1(method):
+    A, y = cfg1()
+    if method == "cocr":
+        A = _csym(A)              # COCR is defined for complex-symmetric A
+    with Dense(A) as h:
+        o, g = _parity(h, DenseOp(A), y, method, 1e-10, 500, np.complex128, tag="cfg1-next3")
+        assert (g["matvecs_a"], g["matvecs_ah"]) == (o.matvecs_a, o.matvecs_ah)
+        h.solve(method, y, 1e-10, 500)
+        hist = ccg.ccg_get_history(h.h)
+        np.testing.assert_allclose(hist, np.array(o.history, float) / o.history[0], rtol=1e-6, atol=1e-12)
+
+
+@pytest.mark.parametrize("method", NEXT3)
+def test_next3_cfg2(method):
+    """BASELINE config 2 (complex-symmetric DDA lattice, the natural COCR case)."""
+    A, y = cfg2()
+    with Dense(A) as h:
+        _parity(h, DenseOp(A), y, method, 1e-8, 2000, np.complex128, tag="cfg2-next3",
+                literal=method in ("bicg", "cocr"))
+
+
+@pytest.mark.parametrize("method", ["bicg", "cgs", "cgnr"])
+def test_next3_cfg3_proxy_c64(method):
+    n = 4096
+    A = gauss_shifted_rows(n, 0, n, seed=1)
+    y = cfg3_rhs(n)
+    with Dense(A) as h:
+        _parity(h, DenseOp(A), y, method, 1e-5, 500, np.complex64, tag="cfg3-proxy-next3", literal=False)
+
+
+@pytest.mark.parametrize("n", [1, 7, 257, 1000])
+@pytest.mark.parametrize("method", NEXT3)
+def test_next3_ragged(method, n):
+    A = dense_random(n, seed=n, dtype=np.complex128, shift=3 - 1j)
+    if method == "cocr":
+        A = _csym(A)
+    y = dense_random(n, seed=n + 1)[:, 0] * 3
+    with Dense(A) as h:
+        _parity(h, DenseOp(A), y, method, 1e-10, 600, np.complex128, tag=f"ragged{n}-next3")
+
+
+@pytest.mark.parametrize("method", NEXT3)
+def test_next3_degenerate(method):
+    c = 3 - 4j
+    n = 10
+    y = (np.arange(n) + 1j * np.arange(n)[::-1]).astype(np.complex128)
+    with Dense(c * np.eye(n, dtype=np.complex128)) as h:
+        g = h.solve(method, y, 1e-12, 50)
+    assert g["status"] == "CONVERGED" and g["iterations"] == 1
+    np.testing.assert_allclose(g["x"], y / c, rtol=1e-14, atol=1e-14)
+    A, yy = cfg1(n=32, seed=2)
+    if method == "cocr":
+        A = _csym(A)
+    with Dense(A) as h:
+        g = h.solve(method, np.zeros(32, np.complex128), 1e-10, 10)
+        assert g["status"] == "CONVERGED" and g["iterations"] == 0
+        g = h.solve(method, yy, 0.0, 3)
+        o = oracle.solve(method, DenseOp(A), yy, 0.0, 3)
+        assert g["status"] == "MAXIT" and g["iterations"] == 3
+        assert (g["matvecs_a"], g["matvecs_ah"]) == (o.matvecs_a, o.matvecs_ah)
+        yb = yy.copy()
+        yb[5] = np.nan
+        assert h.solve(method, yb, 1e-10, 10)["status"] == "NONFINITE"
+        xs = np.linalg.solve(A, yy)
+        o = oracle.solve(method, DenseOp(A), yy, 1e-12, 200, x0=0.5 * xs)
+        g = h.solve(method, yy, 1e-12, 200, x0=0.5 * xs)
+        assert abs(g["iterations"] - o.iterations) <= 2 and relerr(g["x"], o.x) <= 1e-9
+
+
+def test_next3_breakdown_fixture():
+    A = np.array([[0, 1], [-1, 0]], dtype=np.complex128)
+    y = np.array([1, 0], dtype=np.complex128)
+    with Dense(A) as h:
+        for m, name in (("bicg", "sigma"), ("cgs", "sigma"), ("cocr", "rho")):
+            g = h.solve(m, y, 1e-10, 10)
+            o = oracle.solve(m, DenseOp(A), y, 1e-10, 10)
+            assert g["status"] == "BREAKDOWN" and g["breakdown"] == name == o.breakdown, m
+            assert g["iterations"] == o.iterations == 0, m
+        g = h.solve("cgnr", y, 1e-10, 10)
+        assert g["status"] == "CONVERGED" and g["iterations"] == 1
+
+
+@pytest.mark.parametrize("method", ["cgs", "cocr"])
+def test_next3_csr_transpose_free(method):
+    """CGS and COCR need only A·x: they run on a CSR operator without the
+    symmetric flag (COCR on the complex-symmetric shifted Helmholtz matrix)."""
+    N = 16
+    rp, ci, v = helmholtz_csr(N, kh=10 / 128)
+    y = helmholtz_rhs(N)
+    with Csr(rp, ci, v, N ** 3) as h:
+        _parity(h, CsrOp(rp, ci, v), y, method, 1e-8, 3000, np.complex128, literal=False, tag="csr-next3")
+
+
+def test_next3_csr_capability():
+    rp, ci, v = helmholtz_csr(6)
+    with Csr(rp, ci, v, 216) as h:
+        for m in ("bicg", "cgnr"):
+            with pytest.raises(ccg.CcgError) as e:
+                h.solve(m, np.ones(216, np.complex128), 1e-8, 10)
+            assert e.value.code == -3
+    with Csr(rp, ci, v, 216, flags=ccg.FLAG_SYMMETRIC) as h:
+        g = h.solve("bicg", helmholtz_rhs(6), 1e-8, 500)
+        assert g["status"] == "CONVERGED"

@@ -24,12 +24,16 @@ from workloads import (cfg1, cfg2, gauss_shifted_rows, cfg3_rhs, cfg4_rhs, helmh
                        helmholtz_rhs, CONFIGS)
 from workloads.device import cfg4_rows_device  # noqa: E402
 
-V_PASSES = {"bicgstab": 18, "cgne": 10, "qmr": 26, "bicor": 24, "cors": 24}
-M_MATVEC = {"bicgstab": 2, "cgne": 2, "qmr": 2, "bicor": 2, "cors": 2}
+V_PASSES = {"bicgstab": 18, "cgne": 10, "qmr": 26, "bicor": 24, "cors": 24,
+            "bicg": 18, "cgs": 16, "cocr": 14, "cgnr": 11}                   # NEXT-3
+M_MATVEC = {"bicgstab": 2, "cgne": 2, "qmr": 2, "bicor": 2, "cors": 2,
+            "bicg": 2, "cgs": 2, "cocr": 1, "cgnr": 2}
 if os.environ.get("CCG_QMR_DUAL", "1") != "0":
     M_MATVEC["qmr"] = 1                  # dual GEMV: A·p and Aᴴ·q in one pass
+    M_MATVEC["bicg"] = 1
 KNOBS = {k: v for k, v in os.environ.items() if k.startswith("CCG_")}
-ALL = ("bicgstab", "cgne", "qmr", "bicor", "cors")
+ALL = ("bicgstab", "cgne", "qmr", "bicor", "cors", "bicg", "cgs", "cgnr")
+SYM = ALL + ("cocr",)                    # complex-symmetric configs (2, 4, 5) also run COCR
 SEL = set()
 
 
@@ -86,7 +90,7 @@ def main():
                       cf["maxit"], a.reps or 200, "c128")
         elif c == 2:
             A, y = cfg2()
-            run_dense(2, torch.from_numpy(A).to(dev), torch.from_numpy(y).to(dev), ALL, cf["tol"],
+            run_dense(2, torch.from_numpy(A).to(dev), torch.from_numpy(y).to(dev), SYM, cf["tol"],
                       cf["maxit"], a.reps or 50, "c128")
         elif c == 3:
             n = cf["n"]
@@ -105,7 +109,7 @@ def main():
                 cfg4_rows_device(r0, r0 + 4096, Ad[r0:r0 + 4096])
             torch.cuda.synchronize()
             print(json.dumps({"config": 4, "generate_s": time.time() - t0}), flush=True)
-            run_dense(4, Ad, torch.from_numpy(cfg4_rhs()).to(dev), ("bicgstab", "qmr", "bicor", "cgne"),
+            run_dense(4, Ad, torch.from_numpy(cfg4_rhs()).to(dev), ("bicgstab", "qmr", "bicor", "cgne", "cocr", "bicg"),
                       cf["tol"], cf["maxit"], a.reps or 1, "c128")
             del Ad
         elif c == 5:
@@ -118,10 +122,10 @@ def main():
             stream = torch.cuda.ExternalStream(ccg.ccg_get_stream(h))
             x = torch.empty_like(y)
             b_mat = len(v) * (16 + 4) + 4 * (n + 1)
-            for m in [m for m in ("bicgstab", "cors") if not a.methods or m in a.methods.split(",")]:
+            for m in [m for m in ("bicgstab", "cors", "cgs", "cocr") if not a.methods or m in a.methods.split(",")]:
                 r, its, ms = timed(h, m, y, x, cf["tol"], cf["maxit"], a.reps or 2, stream)
                 ips = its / (ms / 1e3)
-                b_iter = 2 * b_mat + V_PASSES[m] * n * 16
+                b_iter = (1 if m == "cocr" else 2) * b_mat + V_PASSES[m] * n * 16
                 print(json.dumps({"config": 5, "method": m, "n": n, "dtype": "c128", "status": r["status"],
                                   "iterations": r["iterations"], "ms_per_solve": ms / (a.reps or 2),
                                   "us_per_iteration": 1e3 * ms / its, "iterations_per_s": ips,
