@@ -66,7 +66,7 @@ struct ccg_ctx {
   int gemv_mode = 0;      // GEMV_SPLIT (default) | GEMV_BULK | GEMV_ROWS (env CCG_GEMV)
   int split_W = 0, split_strips = 1, split_nrb = 1, nstage2_grid = 1, split_ur = 8;
   bool cols_ok = false;   // column-owner GEMV usable (vectorised layout, n % V == 0)
-  int cols_strips = 1, cols_S = 1, dual_S = 1;
+  int cols_strips = 1, cols_S = 1, dual_S = 1, cols_rg = 1;
   bool qmr_dual = true;   // QMR: A·p and Aᴴ·q in one pass over A (env CCG_QMR_DUAL=0 disables)
   void* npart = nullptr;  // [strips][nloc] partial row sums of the split / column-owner GEMV
   size_t npart_bytes = 0;
@@ -298,8 +298,12 @@ struct Engine {
       }
     } else if (c->opk == OPK_DENSE && c->gemv_mode == GEMV_COLS && c->cols_ok) {
       C* part = reinterpret_cast<C*>(c->npart);
-      gemv_cols<T, NT, true, false, false><<<dim3(c->cols_strips, c->cols_S), NT, 0, c->stream>>>(
-          reinterpret_cast<const C*>(c->A), c->lda, xfull, nullptr, c->nloc, c->n, part, nullptr, gate);
+      if (c->cols_rg == 4)
+        gemv_cols<T, NT, true, false, false, 4><<<dim3(c->cols_strips, c->cols_S), NT, 0, c->stream>>>(
+            reinterpret_cast<const C*>(c->A), c->lda, xfull, nullptr, c->nloc, c->n, part, nullptr, gate);
+      else
+        gemv_cols<T, NT, true, false, false, 1><<<dim3(c->cols_strips, c->cols_S), NT, 0, c->stream>>>(
+            reinterpret_cast<const C*>(c->A), c->lda, xfull, nullptr, c->nloc, c->n, part, nullptr, gate);
       c->launches++;
       CK(c, cudaGetLastError());
       gemv_h_stage2<T, NT, Epi><<<c->nstage2_grid, NT, 0, c->stream>>>(part, c->cols_strips, c->nloc, 0, c->nloc,
@@ -620,6 +624,20 @@ struct Engine {
 // ===========================================================================
 // launch-parameter selection
 // ===========================================================================
+// Row splits S for a (strips × S) grid of column-owner CTAs: the smallest S ≥
+// ceil(slots/strips) whose grid fills its last wave to ≥ 90 % (wave
+// quantisation), at most 128 and at most max_rows_split (≥ 16 rows per split).
+static int64_t pick_splits(int64_t strips, int64_t slots, int64_t max_split) {
+  max_split = std::max<int64_t>(1, std::min<int64_t>(max_split, 128));
+  int64_t S0 = std::max<int64_t>(1, (slots + strips - 1) / strips);
+  if (S0 >= max_split) return max_split;
+  for (int64_t S = S0; S <= std::min<int64_t>(max_split, 4 * S0); ++S) {
+    const int64_t ctas = strips * S;
+    const int64_t waves = (ctas + slots - 1) / slots;
+    if (ctas >= (int64_t)(0.9 * waves * slots)) return S;
+  }
+  return S0;
+}
 template <typename T>
 static int choose_launch(ccg_ctx* c) {
   using E = Engine<T>;
@@ -652,8 +670,13 @@ static int choose_launch(ccg_ctx* c) {
   if (c->cols_ok) {
     const int64_t nvc = c->n / CT<T>::V;
     c->cols_strips = (int)std::max<int64_t>(1, (nvc + NT - 1) / NT);
+    const char* rg = getenv("CCG_COLS_RG");
+    c->cols_rg = (rg && atoi(rg) == 4) ? 4 : 1;
     int occc = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occc, gemv_cols<T, E::NT, true, false, false>, NT, 0);
+    if (c->cols_rg == 4)
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occc, gemv_cols<T, E::NT, true, false, false, 4>, NT, 0);
+    else
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occc, gemv_cols<T, E::NT, true, false, false, 1>, NT, 0);
     if (occc < 1) occc = 1;
     const int64_t slots_c = (int64_t)c->sm_count * occc;
     const char* wv = getenv("CCG_COLS_WAVES");
@@ -663,9 +686,7 @@ static int choose_launch(ccg_ctx* c) {
     int occd = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occd, gemv_cols<T, E::NT, true, true, true>, NT, 0);
     if (occd < 1) occd = 1;
-    int64_t Sd = ((int64_t)c->sm_count * occd) / c->cols_strips;
-    Sd = std::max<int64_t>(1, std::min<int64_t>(Sd, 128));
-    c->dual_S = (int)std::min<int64_t>(Sd, std::max<int64_t>(1, c->nloc / 16));
+    c->dual_S = (int)pick_splits(c->cols_strips, (int64_t)c->sm_count * occd, c->nloc / 16);
     c->nstage2_grid =
         (int)std::max<int64_t>(1, std::min<int64_t>((c->nloc + NT - 1) / NT, (int64_t)c->sm_count * 4));
     size_t need = (size_t)c->cols_strips * c->nloc * sizeof(C);

@@ -407,40 +407,34 @@ __device__ __forceinline__ void shfl_c(C& v, int o) {
   v.y = __shfl_xor_sync(0xffffffffu, v.y, o);
 }
 
-// v[0..7]: per-lane partials of 8 rows.  After the call lane L holds, in v[0],
-// the warp sum of row (L >> 2) & 7 (fixed order: deterministic).
-template <typename C>
-__device__ __forceinline__ void warp_transpose_reduce8(C (&v)[8], int lane) {
-  const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
+// v[0..N-1]: per-lane partials of N rows (N = 8 or 32).  Transposed warp
+// reduction: at each halving step lanes with the offset bit set keep the upper
+// half of their values and send the lower half (N−1 shuffle pairs in all), then
+// a plain butterfly over the remaining offsets.  Afterwards lane L holds, in
+// v[0], the warp sum of row L >> (5 − log2 N) (fixed order: deterministic).
+template <int N, typename C>
+__device__ __forceinline__ void warp_transpose_reduce(C (&v)[N], int lane) {
+  static_assert(N == 8 || N == 32, "N rows");
 #pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    C send = b4 ? v[j] : v[j + 4];
-    const C keep = b4 ? v[j + 4] : v[j];
-    shfl_c(send, 16);
-    v[j] = cadd(keep, send);
+  for (int m = N, o = 16; m > 1; m >>= 1, o >>= 1) {
+    const bool up = lane & o;
+#pragma unroll
+    for (int j = 0; j < m / 2; ++j) {
+      C send = up ? v[j] : v[j + m / 2];
+      const C keep = up ? v[j + m / 2] : v[j];
+      shfl_c(send, o);
+      v[j] = cadd(keep, send);
+    }
   }
 #pragma unroll
-  for (int j = 0; j < 2; ++j) {
-    C send = b3 ? v[j] : v[j + 2];
-    const C keep = b3 ? v[j + 2] : v[j];
-    shfl_c(send, 8);
-    v[j] = cadd(keep, send);
+  for (int o = 32 / N / 2; o >= 1; o >>= 1) {
+    C t = v[0];
+    shfl_c(t, o);
+    v[0] = cadd(v[0], t);
   }
-  {
-    C send = b2 ? v[0] : v[1];
-    const C keep = b2 ? v[1] : v[0];
-    shfl_c(send, 4);
-    v[0] = cadd(keep, send);
-  }
-  C t = v[0];
-  shfl_c(t, 2);
-  v[0] = cadd(v[0], t);
-  t = v[0];
-  shfl_c(t, 1);
-  v[0] = cadd(v[0], t);
 }
 
-template <typename T, int NT, bool DO_N, bool DO_H, bool CONJ>
+template <typename T, int NT, bool DO_N, bool DO_H, bool CONJ, int RG = 1>
 __global__ void __launch_bounds__(NT)
 gemv_cols(const typename CT<T>::c* __restrict__ A, int64_t lda,
           const typename CT<T>::c* __restrict__ xn, const typename CT<T>::c* __restrict__ xh,
@@ -449,11 +443,13 @@ gemv_cols(const typename CT<T>::c* __restrict__ A, int64_t lda,
   using C = typename CT<T>::c;
   using LV = typename CT<T>::v;
   constexpr int V = CT<T>::V;
-  constexpr int UR = 8;
-  constexpr int CH = 512;  // rows of xh per shared-memory chunk
+  constexpr int UR = 8;          // rows per group of loads in flight
+  constexpr int NR = UR * RG;    // rows per CTA reduction (RG groups)
+  constexpr int CH = 512;        // rows of xh per shared-memory chunk (multiple of NR)
+  static_assert(!(DO_H && RG != 1), "dual product: one group per reduction");
   if (*gate) return;
   __shared__ C xs[DO_H ? CH : 1];
-  __shared__ C red[2][NT / 32][UR];
+  __shared__ C red[2][NT / 32][NR];
   const int S = gridDim.y, s = blockIdx.y;
   const int64_t i0 = nrows * s / S, i1 = nrows * (s + 1) / S;
   const int64_t jv = (int64_t)blockIdx.x * NT + threadIdx.x;  // 16-byte chunk index
@@ -478,32 +474,37 @@ gemv_cols(const typename CT<T>::c* __restrict__ A, int64_t lda,
       for (int t = threadIdx.x; t < cn; t += NT) xs[t] = xh[c0 + t];
       __syncthreads();
     }
-    for (int t = 0; t < cn; t += UR) {
-      const int nr = min(UR, cn - t);
-      LV a[UR];
+    for (int t = 0; t < cn; t += NR) {
+      const int nr = min(NR, cn - t);
+      C rp[NR];
 #pragma unroll
-      for (int u = 0; u < UR; ++u) a[u] = ld_stream(Ab + (c0 + t + min(u, nr - 1)) * ldv);
-      C rp[UR];
+      for (int g = 0; g < RG; ++g) {
+        LV a[UR];
 #pragma unroll
-      for (int u = 0; u < UR; ++u) {
-        C ac[V];
-        unpack(a[u], ac);
-        rp[u] = czero<C>();
-        if (DO_N && active) {
+        for (int u = 0; u < UR; ++u) a[u] = ld_stream(Ab + (c0 + t + min(g * UR + u, nr - 1)) * ldv);
 #pragma unroll
-          for (int v = 0; v < V; ++v) cfma(rp[u], ac[v], xr[v]);
-        }
-        if (DO_H && u < nr) {
-          const C xi = xs[t + u];
+        for (int u = 0; u < UR; ++u) {
+          C ac[V];
+          unpack(a[u], ac);
+          C& r = rp[g * UR + u];
+          r = czero<C>();
+          if (DO_N && active) {
 #pragma unroll
-          for (int v = 0; v < V; ++v) {
-            if (CONJ) cfmac(hacc[v], ac[v], xi); else cfma(hacc[v], ac[v], xi);
+            for (int v = 0; v < V; ++v) cfma(r, ac[v], xr[v]);
+          }
+          if (DO_H && u < nr) {
+            const C xi = xs[t + u];
+#pragma unroll
+            for (int v = 0; v < V; ++v) {
+              if (CONJ) cfmac(hacc[v], ac[v], xi); else cfma(hacc[v], ac[v], xi);
+            }
           }
         }
       }
       if constexpr (DO_N) {
-        warp_transpose_reduce8(rp, lane);
-        if ((lane & 3) == 0) red[buf][warp][lane >> 2] = rp[0];
+        warp_transpose_reduce<NR>(rp, lane);
+        constexpr int SH = NR == 32 ? 0 : 2;
+        if ((lane & ((1 << SH) - 1)) == 0) red[buf][warp][lane >> SH] = rp[0];
         __syncthreads();
         if (threadIdx.x < nr) {
           C sum = red[buf][0][threadIdx.x];

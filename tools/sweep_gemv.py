@@ -25,7 +25,7 @@ def run(dtype, n, reps, grid):
     h = ccg.ccg_create(dtype, n)
     esz = 8 if dtype == "c64" else 16
     for knobs in grid:
-        for k in ("CCG_GEMV", "CCG_SPLIT_KB", "CCG_SPLIT_UR", "CCG_SPLIT_WAVES", "CCG_COLS_WAVES"):
+        for k in ("CCG_GEMV", "CCG_SPLIT_KB", "CCG_SPLIT_UR", "CCG_SPLIT_WAVES", "CCG_COLS_WAVES", "CCG_COLS_RG"):
             os.environ.pop(k, None)
         os.environ.update({k: str(v) for k, v in knobs.items()})
         ccg.ccg_set_matvec_dense(h, A, 0, n)
@@ -51,8 +51,8 @@ def run(dtype, n, reps, grid):
 
 if __name__ == "__main__":
     if "--modes" in sys.argv:
-        modes = [dict(CCG_GEMV=m) for m in ("split", "cols")] + [dict(CCG_GEMV="cols", CCG_COLS_WAVES=w)
-                                                                 for w in (1, 4, 8)]
+        modes = [dict(CCG_GEMV="split")] + [dict(CCG_GEMV="cols", CCG_COLS_RG=g, CCG_COLS_WAVES=w)
+                                            for g in (1, 4) for w in (1, 2, 4)]
         run("c64", 32768, 10, modes)
         run("c128", 16384, 10, modes)
         run("c128", 4096, 50, modes)
