@@ -171,6 +171,26 @@ int ccg_set_matvec_csr(ccg_handle h, const int32_t* rowptr, const int32_t* colin
                        const void* vals, int64_t row0, int64_t nloc, int64_t nnz_local,
                        uint32_t flags);
 
+/* Matrix-free 7-point stencil operator on an nx × ny × nz lattice (x fastest,
+ * global index i = ix + nx·(iy + ny·iz)), Dirichlet boundaries:
+ *   (A u)_i = d·u_i + ox·(u_{i−1} + u_{i+1}) + oy·(u_{i−nx} + u_{i+nx}) + oz·(u_{i−nx·ny} + u_{i+nx·ny}),
+ * terms whose neighbour lies outside the lattice omitted.  This is the paper's
+ * "own sparse matrix scheme" hook (P:95 [§5]: matvec / cmatvec written for a
+ * structured operator) for config 5's shifted Helmholtz operator (BJ:11:
+ * d = 6 − k²(1 + i/2), ox = oy = oz = −1): no matrix is
+ * stored, so one product moves 2·n complex values instead of CSR's 7n values
+ * + indices.
+ *   nx·ny·nz must equal the handle's n; with world > 1 rank r owns the planes
+ *   [r·nz/world, (r+1)·nz/world) (nz % world == 0, else CCG_E_DIM), i.e. the
+ *   same row range as every vector slice.
+ *   coeffs : HOST double[8] = {Re d, Im d, Re ox, Im ox, Re oy, Im oy, Re oz, Im oz}
+ *            (copied; finite, else CCG_E_ARG).
+ *   flags  : unused (A is complex symmetric by construction).
+ * Supports CCG_OP_A, CCG_OP_AT (= A) and CCG_OP_AH (conjugated coefficients),
+ * hence every method, on any world size. */
+int ccg_set_matvec_stencil7(ccg_handle h, int64_t nx, int64_t ny, int64_t nz, const double* coeffs,
+                            uint32_t flags);
+
 /* y_local = (op(A)·x)[row0 : row0+nloc] from x_local = x[row0 : row0+nloc].
  * x_local / y_local may be HOST or DEVICE pointers (detected); nloc elements.
  * Collective over ranks.  Blocks until y_local is written. */

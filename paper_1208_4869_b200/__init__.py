@@ -32,7 +32,7 @@ ERRORS = {0: "CCG_OK", -1: "CCG_E_ARG", -2: "CCG_E_DIM", -3: "CCG_E_CAPABILITY",
 
 # every symbol include/ccg.h declares (checked by tests/test_abi.py)
 EXPORTS = ("ccg_get_unique_id", "ccg_create", "ccg_create_loopback_group",
-           "ccg_set_matvec_dense", "ccg_set_matvec_csr",
+           "ccg_set_matvec_dense", "ccg_set_matvec_csr", "ccg_set_matvec_stencil7",
            "ccg_apply", "ccg_solve", "ccg_get_history", "ccg_set_timing", "ccg_get_timing",
            "ccg_last_launch_count", "ccg_get_stream", "ccg_last_error", "ccg_destroy",
            "ccg_version")
@@ -84,6 +84,7 @@ def load():
                                                      i64, ctypes.c_int]),
         "ccg_set_matvec_dense": (ctypes.c_int, [vp, vp, i64, i64, i64, u32]),
         "ccg_set_matvec_csr": (ctypes.c_int, [vp, vp, vp, vp, i64, i64, i64, u32]),
+        "ccg_set_matvec_stencil7": (ctypes.c_int, [vp, i64, i64, i64, ctypes.POINTER(dbl), u32]),
         "ccg_apply": (ctypes.c_int, [vp, ctypes.c_int, vp, vp]),
         "ccg_solve": (ctypes.c_int, [vp, ctypes.c_int, vp, vp, vp, dbl, i32,
                                      ctypes.POINTER(ccg_result)]),
@@ -185,6 +186,15 @@ def ccg_set_matvec_csr(h, rowptr, colind, vals, row0, nloc, nnz=None, flags=0):
     _check(h, load().ccg_set_matvec_csr(h, _ptr(rowptr), _ptr(colind), _ptr(vals), int(row0),
                                         int(nloc), int(nnz), int(flags)))
     _keepalive[h] = [rowptr, colind, vals]
+
+
+def ccg_set_matvec_stencil7(h, nx, ny, nz, d, ox, oy=None, oz=None, flags=0):
+    """Matrix-free 7-point stencil (d, ox, oy, oz complex scalars; oy, oz default to ox)."""
+    oy = ox if oy is None else oy
+    oz = ox if oz is None else oz
+    co = (ctypes.c_double * 8)(*[float(v) for z in (d, ox, oy, oz) for v in (complex(z).real, complex(z).imag)])
+    _check(h, load().ccg_set_matvec_stencil7(h, int(nx), int(ny), int(nz), co, int(flags)))
+    _keepalive[h] = []
 
 
 def ccg_apply(h, op, x, y):

@@ -34,7 +34,7 @@ thread_local std::string g_create_err;
 // context
 // ===========================================================================
 enum { NLOCAL = 12, NFULL = 3 };
-enum { OPK_NONE = 0, OPK_DENSE = 1, OPK_CSR = 2 };
+enum { OPK_NONE = 0, OPK_DENSE = 1, OPK_CSR = 2, OPK_STENCIL = 3 };
 enum { GEMV_SPLIT = 0, GEMV_BULK = 1, GEMV_ROWS = 2, GEMV_COLS = 3 };
 
 struct ccg_ctx {
@@ -60,6 +60,9 @@ struct ccg_ctx {
   int32_t* sell_col = nullptr;
   void* sell_val = nullptr;
   int sell_grid = 0;
+  // matrix-free 7-point stencil (ccg_set_matvec_stencil7)
+  int snx = 0, sny = 0, snz = 0, sz0 = 0, snzl = 0, szc = 4;
+  double2 scoef[4] = {};  // d, ox, oy, oz
   bool vec_ok = true;
   bool bulk_ok = false;   // TMA bulk-copy GEMV usable (alignment / n multiple of a 4 KiB tile)
   int bulk_grid = 0;
@@ -214,7 +217,7 @@ struct Engine {
   static int allgather(ccg_ctx* c, int fi) {
     if (c->world == 1) return CCG_OK;
     C* buf = F(c, fi);
-    if (c->opk == OPK_CSR) return halo_exchange(c, buf);
+    if (c->opk == OPK_CSR || c->opk == OPK_STENCIL) return halo_exchange(c, buf);
     NK(c, c->comm->allgather_inplace(buf, (size_t)c->nloc * 2, ndt(), c->stream));
     return CCG_OK;
   }
@@ -261,11 +264,27 @@ struct Engine {
           c->rowptr, c->colind, vals, x, c->nloc, epi, make_red(c), c->st, gate);
   }
 
+  // matrix-free stencil; conj => Aᴴ (= the stencil with conjugated
+  // coefficients, A being complex symmetric)
+  template <class Epi>
+  static void stencil(ccg_ctx* c, const C* xfull, bool conj, Epi epi, const int* gate) {
+    C k[4];
+    for (int i = 0; i < 4; ++i) {
+      k[i].x = (T)c->scoef[i].x;
+      k[i].y = (T)(conj ? -c->scoef[i].y : c->scoef[i].y);
+    }
+    dim3 g((c->snx + 31) / 32, (c->sny + 7) / 8, (c->snzl + c->szc - 1) / c->szc);
+    stencil7_kernel<T, Epi><<<g, 256, 0, c->stream>>>(xfull, c->snx, c->sny, c->snz, c->sz0, c->snzl, c->szc,
+                                                       k[0], k[1], k[2], k[3], epi, make_red(c), c->st, gate);
+  }
+
   // y_local = A · xfull (full-length buffer, own slice + gathered/halo parts)
   template <class Epi>
   static int matvec_a(ccg_ctx* c, const C* xfull, Epi epi, const int* gate) {
     tev_begin(c, 0);
-    if (c->opk == OPK_DENSE && c->gemv_mode == GEMV_SPLIT) {
+    if (c->opk == OPK_STENCIL) {
+      stencil(c, xfull, false, epi, gate);
+    } else if (c->opk == OPK_DENSE && c->gemv_mode == GEMV_SPLIT) {
       const C* A = reinterpret_cast<const C*>(c->A);
       C* part = reinterpret_cast<C*>(c->npart);
       dim3 g(c->split_strips, c->split_nrb);
@@ -338,6 +357,22 @@ struct Engine {
   // y_local = op(A) · x_local, op = Aᴴ (conj) or Aᵀ
   template <class Epi>
   static int matvec_h(ccg_ctx* c, const C* xloc, bool conj, Epi epi, const int* gate) {
+    if (c->opk == OPK_STENCIL) {
+      // complex-symmetric stencil: Aᵀ = A, Aᴴ = conj-coefficient stencil; the
+      // local input goes through full[2] for the halo planes
+      const C* xin = xloc;
+      if (c->world > 1) {
+        CK(c, cudaMemcpyAsync(Fs(c, 2), xloc, c->nloc * sizeof(C), cudaMemcpyDeviceToDevice, c->stream));
+        TRY(allgather(c, 2));
+        xin = F(c, 2);
+      }
+      tev_begin(c, 1);
+      stencil(c, xin, conj, epi, gate);
+      c->launches++;
+      tev_end(c);
+      CK(c, cudaGetLastError());
+      return post<Epi>(c, gate);
+    }
     if (c->opk == OPK_CSR) {
       // complex-symmetric CSR, single GPU: Aᴴx = conj(A conj x), Aᵀx = A x
       tev_begin(c, 1);
@@ -611,7 +646,7 @@ struct Engine {
   // ccg_apply
   static int apply(ccg_ctx* c, int op, const C* xin, C* yout) {
     const int* g = c->zero_gate;
-    if (op == CCG_OP_A || (op == CCG_OP_AT && c->opk == OPK_CSR)) {
+    if (op == CCG_OP_A || (op == CCG_OP_AT && (c->opk == OPK_CSR || c->opk == OPK_STENCIL))) {
       CK(c, cudaMemcpyAsync(Fs(c, 2), xin, c->nloc * sizeof(C), cudaMemcpyDeviceToDevice, c->stream));
       TRY(allgather(c, 2));
       return matvec_a(c, F(c, 2), Store<T>{yout}, g);
@@ -777,7 +812,10 @@ static int choose_launch(ccg_ctx* c) {
                                        (int64_t)c->stage2_grid, (int64_t)c->pass_grid, (int64_t)c->spmv_grid,
                                        (int64_t)c->split_strips * c->split_nrb, (int64_t)c->nstage2_grid,
                                        (int64_t)c->bulk_grid, (int64_t)c->sell_grid,
-                                       (int64_t)c->cols_strips * std::max(c->cols_S, c->dual_S)});
+                                       (int64_t)c->cols_strips * std::max(c->cols_S, c->dual_S),
+                                       c->opk == OPK_STENCIL ? (int64_t)((c->snx + 31) / 32) * ((c->sny + 7) / 8) *
+                                                                   ((c->snzl + c->szc - 1) / c->szc)
+                                                             : (int64_t)1});
   size_t need_part = (size_t)maxgrid * 4;
   if (need_part > c->part_cap) {
     if (c->part) cudaFree(c->part);
@@ -1104,6 +1142,33 @@ int ccg_set_matvec_csr(ccg_handle c, const int32_t* rowptr, const int32_t* colin
   c->halo = halo;
   c->flags = flags;
   c->vec_ok = true;
+  invalidate_graphs(c);
+  return c->dtype == CCG_C64 ? choose_launch<float>(c) : choose_launch<double>(c);
+}
+
+int ccg_set_matvec_stencil7(ccg_handle c, int64_t nx, int64_t ny, int64_t nz, const double* coeffs, uint32_t flags) {
+  if (!c) return CCG_E_ARG;
+  if (!coeffs) FAIL(c, CCG_E_ARG, "coeffs is NULL");
+  if (nx < 1 || ny < 1 || nz < 1 || nx > INT32_MAX || ny > INT32_MAX || nz > INT32_MAX)
+    FAIL(c, CCG_E_DIM, "bad lattice size");
+  if (nx * ny * nz != c->n) FAIL(c, CCG_E_DIM, "nx*ny*nz != n");
+  if (nz % c->world) FAIL(c, CCG_E_DIM, "nz must be divisible by world (z-slab sharding)");
+  for (int i = 0; i < 8; ++i)
+    if (!std::isfinite(coeffs[i])) FAIL(c, CCG_E_ARG, "non-finite stencil coefficient");
+  CK(c, cudaSetDevice(c->device));
+  free_csr_copies(c);
+  c->opk = OPK_STENCIL;
+  c->snx = (int)nx;
+  c->sny = (int)ny;
+  c->snz = (int)nz;
+  c->snzl = (int)(nz / c->world);
+  c->sz0 = c->rank * c->snzl;
+  for (int i = 0; i < 4; ++i) c->scoef[i] = make_double2(coeffs[2 * i], coeffs[2 * i + 1]);
+  c->halo = nx * ny;
+  c->flags = flags | CCG_FLAG_SYMMETRIC;
+  c->vec_ok = true;
+  const char* zc = getenv("CCG_STENCIL_ZC");
+  c->szc = zc ? std::max(1, atoi(zc)) : 4;
   invalidate_graphs(c);
   return c->dtype == CCG_C64 ? choose_launch<float>(c) : choose_launch<double>(c);
 }

@@ -183,8 +183,10 @@ __device__ __forceinline__ void block_sum(double2 (&v)[K], double2* sm) {
   }
 }
 
-__device__ __forceinline__ unsigned block_linear_id() { return blockIdx.x + gridDim.x * blockIdx.y; }
-__device__ __forceinline__ unsigned grid_blocks() { return gridDim.x * gridDim.y; }
+__device__ __forceinline__ unsigned block_linear_id() {
+  return blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+}
+__device__ __forceinline__ unsigned grid_blocks() { return gridDim.x * gridDim.y * gridDim.z; }
 
 template <int K, int NT, class Fin>
 __device__ __forceinline__ void finish_reduction(double2 (&v)[K], const Red& red, State* st) {

@@ -729,6 +729,69 @@ spmv_sell_kernel(const int64_t* __restrict__ soff, const int32_t* __restrict__ s
   if constexpr (Epi::K > 0) finish_reduction<KK, NT, Epi>(dacc, red, st);
 }
 
+// ---------------------------------------------------------------------------
+// K3s matrix-free 7-point stencil (the paper's "own
+// sparse matrix scheme" in matvec, P:95 [§5]): on an nx × ny × nz lattice
+// (x fastest) with Dirichlet boundaries,
+//   (A u)_p = d·u_p + ox·(u_{p±x̂}) + oy·(u_{p±ŷ}) + oz·(u_{p±ẑ}),
+// neighbours outside the lattice = 0 (config 5: d = 6 − k²(1 + i/2),
+// o = −1, BJ:11).  The rank owns planes [z0, z0 + nzl); x is a full-length
+// buffer at global indices whose halo planes z0 − 1 and z0 + nzl are filled.
+// No matrix is stored: per point one x read (L1/L2 serve the 6 neighbour
+// reads; the z neighbours rotate through registers as a thread marches zc
+// planes) and one y write, i.e. 2·n·s bytes instead of CSR's nnz·(s + 4).
+// Terms are summed in ascending column order, each product formed from zero
+// and then added — the same arithmetic as the CSR kernels on the equivalent
+// matrix, so the two operators give bitwise-identical products.
+// Block: 256 threads = 32 (x) × 8 (y); grid (⌈nx/32⌉, ⌈ny/8⌉, ⌈nzl/zc⌉).
+// ---------------------------------------------------------------------------
+template <typename C>
+__device__ __forceinline__ void st_term(C& acc, C coef, C v) {
+  C p = czero<C>();
+  cfma(p, coef, v);
+  acc = cadd(acc, p);
+}
+
+template <typename T, class Epi>
+__global__ void __launch_bounds__(256)
+stencil7_kernel(const typename CT<T>::c* __restrict__ x, int nx, int ny, int nz, int z0, int nzl, int zc,
+                typename CT<T>::c d, typename CT<T>::c ox, typename CT<T>::c oy, typename CT<T>::c oz,
+                Epi epi, Red red, State* st, const int* gate) {
+  using C = typename CT<T>::c;
+  constexpr int KK = Epi::K > 0 ? Epi::K : 1;
+  if (*gate) return;
+  epi.load(st);
+  double2 dacc[KK];
+#pragma unroll
+  for (int k = 0; k < KK; ++k) dacc[k] = make_double2(0.0, 0.0);
+  const int ix = blockIdx.x * 32 + (threadIdx.x & 31);
+  const int iy = blockIdx.y * 8 + (threadIdx.x >> 5);
+  const int zb = blockIdx.z * zc, ze = min(zb + zc, nzl);
+  const int64_t plane = (int64_t)nx * ny;
+  if (ix < nx && iy < ny && zb < ze) {
+    const int64_t col = ix + (int64_t)nx * iy;
+    int zg = z0 + zb;
+    C below = zg > 0 ? __ldg(x + col + plane * (zg - 1)) : czero<C>();
+    C cur = __ldg(x + col + plane * zg);
+    for (int zl = zb; zl < ze; ++zl, ++zg) {
+      const int64_t gi = col + plane * zg;
+      const C above = zg < nz - 1 ? __ldg(x + gi + plane) : czero<C>();
+      C acc = czero<C>();
+      if (zg > 0) st_term(acc, oz, below);
+      if (iy > 0) st_term(acc, oy, __ldg(x + gi - nx));
+      if (ix > 0) st_term(acc, ox, __ldg(x + gi - 1));
+      st_term(acc, d, cur);
+      if (ix < nx - 1) st_term(acc, ox, __ldg(x + gi + 1));
+      if (iy < ny - 1) st_term(acc, oy, __ldg(x + gi + nx));
+      if (zg < nz - 1) st_term(acc, oz, above);
+      epi(gi - plane * z0, acc, dacc);
+      below = cur;
+      cur = above;
+    }
+  }
+  if constexpr (Epi::K > 0) finish_reduction<KK, 256, Epi>(dacc, red, st);
+}
+
 // CSR -> SELL-32 scatter (one thread per row), run once at ccg_set_matvec_csr
 template <typename C>
 __global__ void csr_to_sell(const int32_t* __restrict__ rowptr, const int32_t* __restrict__ colind,

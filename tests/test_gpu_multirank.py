@@ -180,3 +180,46 @@ def test_sharded_csr_apply_and_solve(G):
         assert e.value.code == -3
     finally:
         g.close()
+
+
+class StencilGroup(DenseGroup):
+    def __init__(self, nx, ny, nz, G, coeffs):
+        self.n = nx * ny * nz
+        self.G = G
+        self.nloc = self.n // G
+        self.dtype = np.complex128
+        self.hs = ccg.ccg_create_loopback_group(G, "c128", self.n)
+        for r in range(G):
+            ccg.ccg_set_matvec_stencil7(self.hs[r], nx, ny, nz, *coeffs)
+
+
+@pytest.mark.parametrize("G", [2, 4])
+def test_sharded_stencil_apply_and_solve(G):
+    """z-slab sharded matrix-free stencil: halo planes through the loopback
+    communicator; all three products and Aᴴ / A-only methods vs the oracle."""
+    from workloads import lattice_csr, helmholtz_coeffs
+    nx, ny, nz = 20, 12, 16
+    co = (5.5 - 0.25j, -1.0 + 0.125j, -0.5, 0.75j)
+    op = CsrOp(*lattice_csr(nx, ny, nz, *co))
+    x = (np.random.default_rng(2).standard_normal(op.n) + 0.5j).astype(np.complex128)
+    g = StencilGroup(nx, ny, nz, G, co)
+    try:
+        for o in ("A", "AH", "AT"):
+            assert relerr(g.apply(x, o), reference_apply(op, x, o)) <= TOL[np.complex128], o
+    finally:
+        g.close()
+    N = 16
+    d, oo = helmholtz_coeffs()
+    op = CsrOp(*lattice_csr(N, N, N, d, oo))
+    y = helmholtz_rhs(N)
+    g = StencilGroup(N, N, N, G, (d, oo))
+    try:
+        for method in ("bicgstab", "cocr", "qmr"):
+            r = g.solve(method, y, 1e-8, 3000)
+            k0, kmin, kmax = iteration_envelope(method, op, y, 1e-8, 3000)
+            assert kmin - 2 <= r["iterations"] <= kmax + 2, (method, r["iterations"], kmin, kmax)
+            k = min(r["iterations"], k0)
+            xc, D = x_spread(method, op, y, k)
+            assert relerr(g.solve(method, y, 0.0, k)["x"], xc) <= max(1e-9, 2 * D), method
+    finally:
+        g.close()

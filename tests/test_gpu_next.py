@@ -96,7 +96,7 @@ from oracle import CsrOp                                   # noqa: E402
 from oracle.solvers import NEXT3                           # noqa: E402
 from workloads import cfg1, helmholtz_csr, helmholtz_rhs   # noqa: E402
 from tests._gpu import Csr                                 # noqa: E402
-from tests.test_gpu_solve import _parity                   # noqa: E402
+from tests.test_gpu_solve import _parity, _record          # noqa: E402
 
 
 def _csym(A):
@@ -207,3 +207,89 @@ def test_next3_csr_capability():
     with Csr(rp, ci, v, 216, flags=ccg.FLAG_SYMMETRIC) as h:
         g = h.solve("bicg", helmholtz_rhs(6), 1e-8, 500)
         assert g["status"] == "CONVERGED"
+
+
+# ---------------------------------------------------------------------------
+# NEXT-4: matrix-free 7-point stencil operator (ccg_set_matvec_stencil7)
+# ---------------------------------------------------------------------------
+from workloads import lattice_csr, helmholtz_coeffs          # noqa: E402
+from tests._gpu import to_dev, dt_name                         # noqa: E402
+import torch                                                   # noqa: E402
+
+
+class Stencil(Dense):
+    def __init__(self, nx, ny, nz, d, ox, oy=None, oz=None, dtype=np.complex128):
+        self.n = nx * ny * nz
+        self.dtype = dtype
+        self.h = ccg.ccg_create(dt_name(dtype), self.n)
+        ccg.ccg_set_matvec_stencil7(self.h, nx, ny, nz, d, ox, oy, oz)
+
+
+@pytest.mark.parametrize("dtype", [np.complex128, np.complex64])
+@pytest.mark.parametrize("dims", [(1, 1, 1), (2, 3, 4), (33, 9, 5), (64, 7, 3), (31, 17, 12), (128, 8, 9)])
+def test_stencil_apply_parity(dtype, dims):
+    nx, ny, nz = dims
+    d, ox, oy, oz = 5.5 - 0.25j, -1.0 + 0.125j, -0.5, 0.75j
+    op = CsrOp(*lattice_csr(nx, ny, nz, d, ox, oy, oz, dtype=dtype))
+    x = _x(nx * ny * nz, dtype, seed=nx)
+    with Stencil(nx, ny, nz, d, ox, oy, oz, dtype=dtype) as h:
+        for o in ("A", "AH", "AT"):
+            assert relerr(h.apply(x, o), reference_apply(op, x, o)) <= TOL[dtype], o
+
+
+def test_stencil_bitwise_equals_csr_kernel():
+    """Same arithmetic as the CSR kernels (ascending column order, product from
+    zero then added): the stencil and the CSR operator agree bitwise on every
+    product.  (Solves then differ only through the grid-dependent order of the
+    dot-product partials; they are checked against the oracle below.)"""
+    N = 24
+    d, o = helmholtz_coeffs()
+    rp, ci, v = lattice_csr(N, N, N, d, o)
+    with Csr(rp, ci, v, N ** 3) as hc, Stencil(N, N, N, d, o) as hs:
+        for seed in range(3):
+            x = _x(N ** 3, np.complex128, seed)
+            assert np.array_equal(hc.apply(x, "A"), hs.apply(x, "A"))
+
+
+@pytest.mark.parametrize("method", ["bicgstab", "cors", "cocr", "cgs", "qmr", "bicor", "cgne"])
+def test_stencil_solve_parity(method):
+    N = 16
+    d, o = helmholtz_coeffs()
+    rp, ci, v = lattice_csr(N, N, N, d, o)
+    y = helmholtz_rhs(N)
+    with Stencil(N, N, N, d, o) as h:
+        _parity(h, CsrOp(rp, ci, v), y, method, 1e-8, 4000, np.complex128, literal=False, tag="stencil")
+
+
+@pytest.mark.parametrize("method", ["bicgstab", "cors", "cocr"])
+def test_stencil_full_size_cfg5(method):
+    """Config 5 at full size on the matrix-free operator: the residual property
+    (recomputed by the oracle's own CSR product); the CSR path's iteration
+    count is recorded beside it (identical products, but this indefinite
+    problem is rounding-chaotic, so counts may differ)."""
+    rp, ci, v = helmholtz_csr(128)
+    y = helmholtz_rhs(128)
+    d, o = helmholtz_coeffs()
+    with Stencil(128, 128, 128, d, o) as h:
+        g = h.solve(method, y, 1e-8, 20000)
+    assert g["status"] == "CONVERGED"
+    tr = np.linalg.norm(y - CsrOp(rp, ci, v).apply(g["x"])) / np.linalg.norm(y)
+    assert tr <= 1e-7 and abs(tr - g["true_rel_res"]) <= 1e-3 * tr + 1e-15
+    with Csr(rp, ci, v, 128 ** 3) as hc:
+        gc = hc.solve(method, y, 1e-8, 20000)
+    assert gc["status"] == "CONVERGED"
+    _record(test="cfg5-full-stencil", method=method, k_stencil=g["iterations"], k_csr=gc["iterations"],
+            true_rel_res=tr)
+
+
+def test_stencil_bad_args():
+    h = ccg.ccg_create("c128", 60)
+    try:
+        with pytest.raises(ccg.CcgError) as e:
+            ccg.ccg_set_matvec_stencil7(h, 3, 4, 4, 6.0, -1.0)
+        assert e.value.code == -2
+        with pytest.raises(ccg.CcgError) as e:
+            ccg.ccg_set_matvec_stencil7(h, 3, 4, 5, float("nan"), -1.0)
+        assert e.value.code == -1
+    finally:
+        ccg.ccg_destroy(h)

@@ -59,3 +59,23 @@ def test_cfg1_deterministic():
     A2, y2 = cfg1()
     np.testing.assert_array_equal(A1, A2)
     np.testing.assert_array_equal(y1, y2)
+
+
+def test_lattice_csr_matches_helmholtz_and_closed_form():
+    """lattice_csr (the stencil operator written out) equals the config-5
+    generator bitwise on a cube, and on a non-cubic lattice its closed-form
+    eigenvectors ⊗ sin(π m i/(N+1)) give λ = d + 2 Σ o_a cos(π m_a/(N_a+1))."""
+    import numpy as np
+    from workloads import lattice_csr, helmholtz_csr, helmholtz_coeffs
+    from oracle import CsrOp
+    d, o = helmholtz_coeffs()
+    for a, b in zip(lattice_csr(9, 9, 9, d, o), helmholtz_csr(9)):
+        assert a.dtype == b.dtype and np.array_equal(a, b)
+    nx, ny, nz = 7, 5, 4
+    ox, oy, oz = -1.0 + 0.1j, -0.5, -2.0j
+    op = CsrOp(*lattice_csr(nx, ny, nz, 3 + 1j, ox, oy, oz))
+    m = (2, 3, 1)
+    vx, vy, vz = (np.sin(np.pi * mm * np.arange(1, N + 1) / (N + 1)) for mm, N in zip(m, (nx, ny, nz)))
+    v = np.einsum("k,j,i->kji", vz, vy, vx).ravel().astype(np.complex128)
+    lam = (3 + 1j) + 2 * sum(oo * np.cos(np.pi * mm / (N + 1)) for oo, mm, N in zip((ox, oy, oz), m, (nx, ny, nz)))
+    assert np.linalg.norm(op.apply(v) - lam * v) <= 1e-13 * np.linalg.norm(v) * abs(lam)

@@ -21,7 +21,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 import paper_1208_4869_b200 as ccg  # noqa: E402
 from workloads import (cfg1, cfg2, gauss_shifted_rows, cfg3_rhs, cfg4_rhs, helmholtz_csr,  # noqa: E402
-                       helmholtz_rhs, CONFIGS)
+                       helmholtz_rhs, helmholtz_coeffs, CONFIGS)
 from workloads.device import cfg4_rows_device  # noqa: E402
 
 V_PASSES = {"bicgstab": 18, "cgne": 10, "qmr": 26, "bicor": 24, "cors": 24,
@@ -116,22 +116,29 @@ def main():
             rp, ci, v = helmholtz_csr(128)
             y = torch.from_numpy(helmholtz_rhs(128)).to(dev)
             n = 128 ** 3
-            h = ccg.ccg_create("c128", n)
             rpd, cid, vd = (torch.from_numpy(t).to(dev) for t in (rp, ci, v))
-            ccg.ccg_set_matvec_csr(h, rpd, cid, vd, 0, n, len(v))
-            stream = torch.cuda.ExternalStream(ccg.ccg_get_stream(h))
-            x = torch.empty_like(y)
-            b_mat = len(v) * (16 + 4) + 4 * (n + 1)
-            for m in [m for m in ("bicgstab", "cors", "cgs", "cocr") if not a.methods or m in a.methods.split(",")]:
-                r, its, ms = timed(h, m, y, x, cf["tol"], cf["maxit"], a.reps or 2, stream)
-                ips = its / (ms / 1e3)
-                b_iter = (1 if m == "cocr" else 2) * b_mat + V_PASSES[m] * n * 16
-                print(json.dumps({"config": 5, "method": m, "n": n, "dtype": "c128", "status": r["status"],
-                                  "iterations": r["iterations"], "ms_per_solve": ms / (a.reps or 2),
-                                  "us_per_iteration": 1e3 * ms / its, "iterations_per_s": ips,
-                                  "effective_GBs": b_iter * ips / 1e9, "true_rel_res": r["true_rel_res"]}),
-                      flush=True)
-            ccg.ccg_destroy(h)
+            b_csr = len(v) * (16 + 4) + 4 * (n + 1)
+            for opname in ("csr", "stencil"):
+                h = ccg.ccg_create("c128", n)
+                if opname == "csr":
+                    ccg.ccg_set_matvec_csr(h, rpd, cid, vd, 0, n, len(v))
+                    b_mat = b_csr
+                else:
+                    d, o = helmholtz_coeffs()
+                    ccg.ccg_set_matvec_stencil7(h, 128, 128, 128, d, o)
+                    b_mat = 2 * n * 16          # x read + y write
+                stream = torch.cuda.ExternalStream(ccg.ccg_get_stream(h))
+                x = torch.empty_like(y)
+                for m in [m for m in ("bicgstab", "cors", "cgs", "cocr") if not a.methods or m in a.methods.split(",")]:
+                    r, its, ms = timed(h, m, y, x, cf["tol"], cf["maxit"], a.reps or 2, stream)
+                    ips = its / (ms / 1e3)
+                    b_iter = (1 if m == "cocr" else 2) * b_mat + V_PASSES[m] * n * 16
+                    print(json.dumps({"config": 5, "operator": opname, "method": m, "n": n, "dtype": "c128",
+                                      "status": r["status"], "iterations": r["iterations"],
+                                      "ms_per_solve": ms / (a.reps or 2), "us_per_iteration": 1e3 * ms / its,
+                                      "iterations_per_s": ips, "effective_GBs": b_iter * ips / 1e9,
+                                      "true_rel_res": r["true_rel_res"]}), flush=True)
+                ccg.ccg_destroy(h)
         torch.cuda.empty_cache()
 
 

@@ -17,6 +17,7 @@ __all__ = [
     "CONFIGS", "cfg1", "cfg2", "cfg3_rows", "cfg3_rhs", "cfg3", "gauss_shifted_rows",
     "dda_lattice_rows", "dda_lattice_rhs", "cfg2_like", "cfg4_rows", "cfg4_rhs",
     "helmholtz_csr", "helmholtz_rhs", "cfg5", "dense_random", "lattice_dims", "BLOCK",
+    "lattice_csr", "helmholtz_coeffs",
 ]
 
 # config index -> (dtype, n, methods, tol, maxit)  (BJ:7-11, maxit per Q8)
@@ -193,6 +194,35 @@ def helmholtz_csr(N=128, kh=10.0 / 128, z0=0, z1=None, dtype=np.complex128):
     colind = cols[valid].astype(np.int32)
     v = vals[valid]
     return rowptr.astype(np.int32), colind, v
+
+
+def lattice_csr(nx, ny, nz, d, ox, oy=None, oz=None, z0=0, z1=None, dtype=np.complex128):
+    """CSR of the constant-coefficient 7-point operator on an nx × ny × nz
+    lattice (x fastest, Dirichlet): diagonal d, x/y/z neighbours ox/oy/oz.
+    Rows of the z-slab [z0, z1), GLOBAL columns, sorted.  The stencil
+    operator's matrix (ccg_set_matvec_stencil7) written out for the oracle."""
+    oy = ox if oy is None else oy
+    oz = ox if oz is None else oz
+    z1 = nz if z1 is None else z1
+    P = nx * ny
+    j = np.arange(z0 * P, z1 * P, dtype=np.int64)
+    ix, iy, iz = j % nx, (j // nx) % ny, j // P
+    offs = (-P, -nx, -1, 0, 1, nx, P)
+    valid = np.stack([iz > 0, iy > 0, ix > 0, np.ones_like(ix, bool),
+                      ix < nx - 1, iy < ny - 1, iz < nz - 1], axis=1)
+    cols = j[:, None] + np.array(offs, dtype=np.int64)[None, :]
+    vals = np.empty(cols.shape, dtype=dtype)
+    for c, v in enumerate((oz, oy, ox, d, ox, oy, oz)):
+        vals[:, c] = dtype(v)
+    rowptr = np.zeros(len(j) + 1, dtype=np.int64)
+    np.cumsum(valid.sum(axis=1), out=rowptr[1:])
+    return rowptr.astype(np.int32), cols[valid].astype(np.int32), vals[valid]
+
+
+def helmholtz_coeffs(kh=10.0 / 128):
+    """(d, o) of config 5's operator (Q11): d = 6 − k²(1 + i/2), o = −1."""
+    k2 = kh * kh
+    return complex(6.0 - k2, -0.5 * k2), -1.0
 
 
 def helmholtz_rhs(N=128, z0=0, z1=None, dtype=np.complex128):
