@@ -13,11 +13,12 @@ What it computes (PAPER.md = "P:<line>", SPEC.md = "S:<line>"):
 * ``numerics``  - dotc / dotu / norm2, the F90 ``dot_product`` / ``sum(u*v)``
   intrinsics the paper substitutes for BLAS (§1).
 * ``operators`` - the user ``matvec`` / ``cmatvec`` of ``arraymodule`` (§5):
-  A·x, Aᴴ·x, Aᵀ·x for dense and CSR storage.
+  A·x, Aᴴ·x, Aᵀ·x for dense and CSR storage, and the lattice
+  (3-level Toeplitz, DDA-structured) operator via a library FFT.
 * ``solvers``   - BiCGSTAB, CGNE, QMR (PIM90 set, §2.1; §6) and
   BiCOR / CORS (§2.4), written step by step in the notation of
-  SURVEY.md §8(c) O1-O5, plus BiCG, CGS and COCR (§3.4) which are
-  used only as *equivalence pins* for BiCOR / CORS.
+  SURVEY.md §8(c) O1-O5, plus BiCG, CGS, CGNR and COCR (§3.4),
+  the SURVEY §8(f) NEXT-3 rows (also equivalence pins for BiCOR / CORS).
 * ``direct``    - dense LU with partial pivoting and the relative residual
   (S:466-508), the independent direct-solve check.
 
@@ -35,4 +36,4 @@ Parity pins: every function here is pinned by a ``-m "not gpu"`` test in
 
 from . import numerics, operators, solvers, direct, exact  # noqa: F401
 from .solvers import solve, Result, METHODS  # noqa: F401
-from .operators import DenseOp, CsrOp  # noqa: F401
+from .operators import DenseOp, CsrOp, ToeplitzOp  # noqa: F401

@@ -119,6 +119,61 @@ class CsrOp(_Counted):
         return D
 
 
+class ToeplitzOp(_Counted):
+    """3-level Toeplitz operator on an nx × ny × nz lattice (x fastest, unit
+    spacing): (A x)_i = d·x_i + Σ_{j≠i} K(r_i − r_j)·x_j — the discrete-dipole
+    structure of P:47 (§1) (BJ:8, BJ:10 configs are scalar instances).
+
+    The lattice sum is a linear convolution; this oracle evaluates it with a
+    library FFT (scipy.fft, a step of the definition) on the zero-padded
+    (2nz, 2ny, 2nx) box, in the working precision of ``kernel``.
+    ``kernel[dz+nz-1, dy+ny-1, dx+nx-1]`` = K(dx, dy, dz); the δ = 0 entry is
+    ignored.  Aᵀ convolves with K(−δ); Aᴴx = conj(Aᵀ conj(x)).  Pinned against
+    the dense definition (tests/test_oracle_numerics.py)."""
+
+    def __init__(self, kernel, dims, diag):
+        import scipy.fft as sf
+        super().__init__()
+        self._fft = sf
+        nx, ny, nz = dims
+        K = np.array(kernel).reshape(2 * nz - 1, 2 * ny - 1, 2 * nx - 1).copy()
+        K[nz - 1, ny - 1, nx - 1] = 0
+        self.dims = dims
+        self.n = nx * ny * nz
+        self.dtype = K.dtype
+        self.diag = self.dtype.type(diag)
+        self.Kh = self._embed_fft(K)
+        self.Kh_t = self._embed_fft(K[::-1, ::-1, ::-1])      # K(−δ)
+
+    def _embed_fft(self, K):
+        nx, ny, nz = self.dims
+        C = np.zeros((2 * nz, 2 * ny, 2 * nx), dtype=self.dtype)
+        # circulant index m ↔ displacement m (m < n) or m − 2n (m > n); m = n unused
+        idx = [np.r_[0:n, n + 1:2 * n] for n in (nz, ny, nx)]
+        src = [np.r_[n - 1:2 * n - 1, 0:n - 1] for n in (nz, ny, nx)]
+        C[np.ix_(*idx)] = K[np.ix_(*src)]
+        return self._fft.fftn(C)
+
+    def _conv(self, x, Kh):
+        nx, ny, nz = self.dims
+        X = np.zeros((2 * nz, 2 * ny, 2 * nx), dtype=self.dtype)
+        X[:nz, :ny, :nx] = np.asarray(x).reshape(nz, ny, nx)
+        return self._fft.ifftn(self._fft.fftn(X) * Kh)[:nz, :ny, :nx].ravel().astype(self.dtype)
+
+    def apply(self, x):
+        self.n_a += 1
+        return self.diag * x + self._conv(x, self.Kh)
+
+    def apply_t(self, x):
+        self.n_at += 1
+        return self.diag * x + self._conv(x, self.Kh_t)
+
+    def apply_h(self, x):
+        self.n_ah += 1
+        xc = np.conj(x)
+        return np.conj(self.diag * xc + self._conv(xc, self.Kh_t))
+
+
 def reference_apply(A, x, op="A"):
     """Per-matvec parity reference.
 

@@ -181,3 +181,46 @@ def test_exact_scalar():
     assert a / b * b == a
     assert (a * b).conjugate() == a.conjugate() * b.conjugate()
     assert GR(Fraction(1, 3), 0) * 3 == 1
+
+
+# ---------------- the lattice (3-level Toeplitz) operator ----------------
+def _dense_from_kernel(K, dims, diag):
+    """Brute force: A[i, j] = K(r_i − r_j), A[i, i] = diag, by explicit loops."""
+    nx, ny, nz = dims
+    n = nx * ny * nz
+    A = np.empty((n, n), dtype=np.complex128)
+    for i in range(n):
+        xi, yi, zi = i % nx, (i // nx) % ny, i // (nx * ny)
+        for j in range(n):
+            xj, yj, zj = j % nx, (j // nx) % ny, j // (nx * ny)
+            A[i, j] = diag if i == j else K[zi - zj + nz - 1, yi - yj + ny - 1, xi - xj + nx - 1]
+    return A
+
+
+def test_toeplitz_op_matches_dense_definition():
+    """Random non-symmetric kernel on a non-cubic lattice: A·x, Aᴴ·x, Aᵀ·x of
+    the FFT operator equal the brute-force dense matrix's products."""
+    from oracle import ToeplitzOp, DenseOp
+    dims = (5, 3, 4)
+    rng = np.random.default_rng(5)
+    K = rng.standard_normal((7, 5, 9)) + 1j * rng.standard_normal((7, 5, 9))
+    op = ToeplitzOp(K, dims, 2 - 1j)
+    A = _dense_from_kernel(K, dims, 2 - 1j)
+    x = rng.standard_normal(60) + 1j * rng.standard_normal(60)
+    for f, ref in ((op.apply, A @ x), (op.apply_t, A.T @ x), (op.apply_h, A.conj().T @ x)):
+        assert np.linalg.norm(f(x) - ref) <= 1e-14 * np.linalg.norm(ref)
+
+
+def test_dda_kernel_matches_lattice_rows_and_cfg2():
+    """dda_kernel holds exactly the off-diagonal entries of dda_lattice_rows;
+    the FFT operator reproduces config 2's dense product."""
+    from oracle import ToeplitzOp, DenseOp
+    from workloads import dda_kernel, dda_lattice_rows, cfg2
+    dims = (4, 3, 5)
+    K = dda_kernel(dims, 0.7)
+    A = dda_lattice_rows(dims, 0.7, 2.5 + 0.2j, 0, 60)
+    assert np.array_equal(_dense_from_kernel(K, dims, 2.5 + 0.2j), A)
+    A2, y2 = cfg2()
+    op = ToeplitzOp(dda_kernel((16, 16, 16), 1.0), (16, 16, 16), 3 + 0.5j)
+    assert np.linalg.norm(op.apply(y2) - A2 @ y2) <= 2e-15 * np.linalg.norm(A2 @ y2)
+    assert np.linalg.norm(op.apply_h(y2) - A2.conj().T @ y2) <= 2e-15 * np.linalg.norm(A2 @ y2)

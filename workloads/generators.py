@@ -17,7 +17,7 @@ __all__ = [
     "CONFIGS", "cfg1", "cfg2", "cfg3_rows", "cfg3_rhs", "cfg3", "gauss_shifted_rows",
     "dda_lattice_rows", "dda_lattice_rhs", "cfg2_like", "cfg4_rows", "cfg4_rhs",
     "helmholtz_csr", "helmholtz_rhs", "cfg5", "dense_random", "lattice_dims", "BLOCK",
-    "lattice_csr", "helmholtz_coeffs",
+    "lattice_csr", "helmholtz_coeffs", "dda_kernel",
 ]
 
 # config index -> (dtype, n, methods, tol, maxit)  (BJ:7-11, maxit per Q8)
@@ -141,6 +141,22 @@ def dda_lattice_rows(dims, k, diag, r0, r1, out=None):
         blk[rows - a, rows] = diag
         out[a - r0:b - r0] = blk
     return out
+
+
+def dda_kernel(dims, k, scale=0.1):
+    """K(δ) = scale·exp(i k|δ|)/|δ| for every lattice displacement δ (the
+    off-diagonal entries of dda_lattice_rows as a 3-level Toeplitz kernel),
+    shape (2nz−1, 2ny−1, 2nx−1), index [dz+nz−1, dy+ny−1, dx+nx−1]; δ = 0 → 0.
+    Same float64 operations as dda_lattice_rows, so the values agree bitwise."""
+    nx, ny, nz = dims
+    dz, dy, dx = np.meshgrid(np.arange(-(nz - 1), nz), np.arange(-(ny - 1), ny), np.arange(-(nx - 1), nx),
+                             indexing="ij")
+    dx, dy, dz = (a.astype(np.float64) for a in (dx, dy, dz))
+    d = np.sqrt(dx * dx + dy * dy + dz * dz)
+    with np.errstate(divide="ignore", invalid="ignore"):
+        K = scale * np.exp(1j * k * d) / d
+    K[nz - 1, ny - 1, nx - 1] = 0
+    return K.astype(np.complex128)
 
 
 def dda_lattice_rhs(dims, k):
