@@ -191,6 +191,29 @@ int ccg_set_matvec_csr(ccg_handle h, const int32_t* rowptr, const int32_t* colin
 int ccg_set_matvec_stencil7(ccg_handle h, int64_t nx, int64_t ny, int64_t nz, const double* coeffs,
                             uint32_t flags);
 
+/* FFT block-Toeplitz operator on an nx × ny × nz lattice (x fastest, global
+ * index i = ix + nx·(iy + ny·iz), unit spacing):
+ *   (A x)_i = d·x_i + Σ_{j≠i} K(r_i − r_j)·x_j,
+ * the structure of the discrete-dipole systems CCGPAK was written for (P:47
+ * [§1], DDSCAT; BASELINE configs 2 and 4 are scalar instances with
+ * K(δ) = 0.1·exp(i k|δ|)/|δ|).  The product is a linear convolution computed
+ * with the library's own 3-D FFT kernels on a power-of-two circulant
+ * embedding: O(n log n) work and a few MB of traffic
+ * instead of the dense n²·s bytes.  Aᵀ uses K(−δ), Aᴴ = conj(Aᵀ conj(x)).
+ *   nx·ny·nz must equal the handle's n; each side in [1, 1024] (else CCG_E_DIM).
+ *   kernel : HOST complex128 (interleaved doubles) K(δ) for every displacement
+ *            δ = (dx, dy, dz), |dx| < nx, |dy| < ny, |dz| < nz, at index
+ *            (dx + nx − 1) + (2nx − 1)·((dy + ny − 1) + (2ny − 1)·(dz + nz − 1));
+ *            the δ = 0 entry is ignored.  Copied (transformed once, in double).
+ *   diag   : HOST double[2] = {Re d, Im d}.
+ *   flags  : informational (CCG_FLAG_SYMMETRIC if K(δ) = K(−δ)).
+ * With world > 1 every rank transforms the gathered vector and keeps its own
+ * rows (the FFT work is replicated; the vector is n·s bytes).  Supports
+ * CCG_OP_A, CCG_OP_AH, CCG_OP_AT, hence every method.  Non-finite kernel or
+ * diagonal values: CCG_E_ARG. */
+int ccg_set_matvec_toeplitz3(ccg_handle h, int64_t nx, int64_t ny, int64_t nz, const double* kernel,
+                             const double* diag, uint32_t flags);
+
 /* y_local = (op(A)·x)[row0 : row0+nloc] from x_local = x[row0 : row0+nloc].
  * x_local / y_local may be HOST or DEVICE pointers (detected); nloc elements.
  * Collective over ranks.  Blocks until y_local is written. */

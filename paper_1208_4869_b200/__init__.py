@@ -33,6 +33,7 @@ ERRORS = {0: "CCG_OK", -1: "CCG_E_ARG", -2: "CCG_E_DIM", -3: "CCG_E_CAPABILITY",
 # every symbol include/ccg.h declares (checked by tests/test_abi.py)
 EXPORTS = ("ccg_get_unique_id", "ccg_create", "ccg_create_loopback_group",
            "ccg_set_matvec_dense", "ccg_set_matvec_csr", "ccg_set_matvec_stencil7",
+           "ccg_set_matvec_toeplitz3",
            "ccg_apply", "ccg_solve", "ccg_get_history", "ccg_set_timing", "ccg_get_timing",
            "ccg_last_launch_count", "ccg_get_stream", "ccg_last_error", "ccg_destroy",
            "ccg_version")
@@ -85,6 +86,8 @@ def load():
         "ccg_set_matvec_dense": (ctypes.c_int, [vp, vp, i64, i64, i64, u32]),
         "ccg_set_matvec_csr": (ctypes.c_int, [vp, vp, vp, vp, i64, i64, i64, u32]),
         "ccg_set_matvec_stencil7": (ctypes.c_int, [vp, i64, i64, i64, ctypes.POINTER(dbl), u32]),
+        "ccg_set_matvec_toeplitz3": (ctypes.c_int, [vp, i64, i64, i64, ctypes.POINTER(dbl),
+                                                    ctypes.POINTER(dbl), u32]),
         "ccg_apply": (ctypes.c_int, [vp, ctypes.c_int, vp, vp]),
         "ccg_solve": (ctypes.c_int, [vp, ctypes.c_int, vp, vp, vp, dbl, i32,
                                      ctypes.POINTER(ccg_result)]),
@@ -194,6 +197,18 @@ def ccg_set_matvec_stencil7(h, nx, ny, nz, d, ox, oy=None, oz=None, flags=0):
     oz = ox if oz is None else oz
     co = (ctypes.c_double * 8)(*[float(v) for z in (d, ox, oy, oz) for v in (complex(z).real, complex(z).imag)])
     _check(h, load().ccg_set_matvec_stencil7(h, int(nx), int(ny), int(nz), co, int(flags)))
+    _keepalive[h] = []
+
+
+def ccg_set_matvec_toeplitz3(h, nx, ny, nz, kernel, diag, flags=0):
+    """FFT block-Toeplitz operator; ``kernel``: complex128 array of K(δ) with
+    shape (2nz−1, 2ny−1, 2nx−1), index [dz+nz−1, dy+ny−1, dx+nx−1]."""
+    k = np.ascontiguousarray(kernel, dtype=np.complex128)
+    if k.size != (2 * nx - 1) * (2 * ny - 1) * (2 * nz - 1):
+        raise ValueError("kernel must have (2nx-1)(2ny-1)(2nz-1) entries")
+    kp = k.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+    d = (ctypes.c_double * 2)(complex(diag).real, complex(diag).imag)
+    _check(h, load().ccg_set_matvec_toeplitz3(h, int(nx), int(ny), int(nz), kp, d, int(flags)))
     _keepalive[h] = []
 
 

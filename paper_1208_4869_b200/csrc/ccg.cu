@@ -23,6 +23,9 @@
 #include "matvec.cuh"
 #include "methods.cuh"
 #include "comm.cuh"
+#include "fft.cuh"
+
+#include <complex>
 
 using namespace ccg;
 
@@ -34,7 +37,7 @@ thread_local std::string g_create_err;
 // context
 // ===========================================================================
 enum { NLOCAL = 12, NFULL = 3 };
-enum { OPK_NONE = 0, OPK_DENSE = 1, OPK_CSR = 2, OPK_STENCIL = 3 };
+enum { OPK_NONE = 0, OPK_DENSE = 1, OPK_CSR = 2, OPK_STENCIL = 3, OPK_TOEPLITZ = 4 };
 enum { GEMV_SPLIT = 0, GEMV_BULK = 1, GEMV_ROWS = 2, GEMV_COLS = 3 };
 
 struct ccg_ctx {
@@ -63,6 +66,13 @@ struct ccg_ctx {
   // matrix-free 7-point stencil (ccg_set_matvec_stencil7)
   int snx = 0, sny = 0, snz = 0, sz0 = 0, snzl = 0, szc = 4;
   double2 scoef[4] = {};  // d, ox, oy, oz
+  // FFT block-Toeplitz operator (ccg_set_matvec_toeplitz3)
+  FftGeo geo = {};
+  void* fftW = nullptr;   // padded work array X2·Y2·Z2
+  void* fftK = nullptr;   // K̂ / (X2·Y2·Z2)
+  void* fftTw = nullptr;  // exp(−2πi k/Lmax), k < Lmax/2
+  int fft_lmax = 1;
+  double2 tdiag = {};
   bool vec_ok = true;
   bool bulk_ok = false;   // TMA bulk-copy GEMV usable (alignment / n multiple of a 4 KiB tile)
   int bulk_grid = 0;
@@ -218,6 +228,7 @@ struct Engine {
     if (c->world == 1) return CCG_OK;
     C* buf = F(c, fi);
     if (c->opk == OPK_CSR || c->opk == OPK_STENCIL) return halo_exchange(c, buf);
+    // dense and FFT-Toeplitz: every rank needs the whole input vector
     NK(c, c->comm->allgather_inplace(buf, (size_t)c->nloc * 2, ndt(), c->stream));
     return CCG_OK;
   }
@@ -278,11 +289,48 @@ struct Engine {
                                                        k[0], k[1], k[2], k[3], epi, make_red(c), c->st, gate);
   }
 
+  // FFT block-Toeplitz product (fft.cuh); op: 0 = A, 1 = Aᴴ, 2 = Aᵀ.  Every
+  // rank transforms the whole (gathered) vector and keeps its own rows.
+  template <class Epi>
+  static void toeplitz(ccg_ctx* c, const C* xfull, int op, Epi epi, const int* gate) {
+    const FftGeo& g = c->geo;
+    C* W = reinterpret_cast<C*>(c->fftW);
+    const C* Kh = reinterpret_cast<const C*>(c->fftK);
+    const C* tw = reinterpret_cast<const C*>(c->fftTw);
+    const int L = c->fft_lmax;
+    const size_t smx = (size_t)g.tx * g.X2 * sizeof(C);
+    const size_t smy = (size_t)g.tyz * g.Y2 * sizeof(C);
+    const size_t smz = (size_t)g.tyz * g.Z2 * sizeof(C);
+    const int gx = (g.ny * g.nz + g.tx - 1) / g.tx;
+    if (op == 1)
+      fft_fwd_x<T, true><<<gx, 256, smx, c->stream>>>(xfull, W, g, tw, L / g.X2, gate);
+    else
+      fft_fwd_x<T, false><<<gx, 256, smx, c->stream>>>(xfull, W, g, tw, L / g.X2, gate);
+    fft_fwd_y<T><<<dim3(g.X2 / g.tyz, g.nz), 256, smy, c->stream>>>(W, g, tw, L / g.Y2, gate);
+    if (op == 0)
+      fft_z_mul<T, false><<<dim3(g.X2 / g.tyz, g.Y2), 256, smz, c->stream>>>(W, Kh, g, tw, L / g.Z2, gate);
+    else
+      fft_z_mul<T, true><<<dim3(g.X2 / g.tyz, g.Y2), 256, smz, c->stream>>>(W, Kh, g, tw, L / g.Z2, gate);
+    fft_inv_y<T><<<dim3(g.X2 / g.tyz, g.nz), 256, smy, c->stream>>>(W, g, tw, L / g.Y2, gate);
+    C d;
+    d.x = (T)c->tdiag.x;
+    d.y = (T)(op == 1 ? -c->tdiag.y : c->tdiag.y);
+    if (op == 1)
+      fft_inv_x<T, true, Epi><<<gx, 256, smx, c->stream>>>(W, xfull, g, tw, L / g.X2, d, c->row0, c->nloc, epi,
+                                                            make_red(c), c->st, gate);
+    else
+      fft_inv_x<T, false, Epi><<<gx, 256, smx, c->stream>>>(W, xfull, g, tw, L / g.X2, d, c->row0, c->nloc, epi,
+                                                             make_red(c), c->st, gate);
+    c->launches += 4;
+  }
+
   // y_local = A · xfull (full-length buffer, own slice + gathered/halo parts)
   template <class Epi>
   static int matvec_a(ccg_ctx* c, const C* xfull, Epi epi, const int* gate) {
     tev_begin(c, 0);
-    if (c->opk == OPK_STENCIL) {
+    if (c->opk == OPK_TOEPLITZ) {
+      toeplitz(c, xfull, 0, epi, gate);
+    } else if (c->opk == OPK_STENCIL) {
       stencil(c, xfull, false, epi, gate);
     } else if (c->opk == OPK_DENSE && c->gemv_mode == GEMV_SPLIT) {
       const C* A = reinterpret_cast<const C*>(c->A);
@@ -357,6 +405,20 @@ struct Engine {
   // y_local = op(A) · x_local, op = Aᴴ (conj) or Aᵀ
   template <class Epi>
   static int matvec_h(ccg_ctx* c, const C* xloc, bool conj, Epi epi, const int* gate) {
+    if (c->opk == OPK_TOEPLITZ) {
+      const C* xin = xloc;
+      if (c->world > 1) {
+        CK(c, cudaMemcpyAsync(Fs(c, 2), xloc, c->nloc * sizeof(C), cudaMemcpyDeviceToDevice, c->stream));
+        TRY(allgather(c, 2));
+        xin = F(c, 2);
+      }
+      tev_begin(c, 1);
+      toeplitz(c, xin, conj ? 1 : 2, epi, gate);
+      c->launches++;
+      tev_end(c);
+      CK(c, cudaGetLastError());
+      return post<Epi>(c, gate);
+    }
     if (c->opk == OPK_STENCIL) {
       // complex-symmetric stencil: Aᵀ = A, Aᴴ = conj-coefficient stencil; the
       // local input goes through full[2] for the halo planes
@@ -815,7 +877,10 @@ static int choose_launch(ccg_ctx* c) {
                                        (int64_t)c->cols_strips * std::max(c->cols_S, c->dual_S),
                                        c->opk == OPK_STENCIL ? (int64_t)((c->snx + 31) / 32) * ((c->sny + 7) / 8) *
                                                                    ((c->snzl + c->szc - 1) / c->szc)
-                                                             : (int64_t)1});
+                                                             : (int64_t)1,
+                                       c->opk == OPK_TOEPLITZ
+                                           ? (int64_t)(c->geo.ny * c->geo.nz + c->geo.tx - 1) / c->geo.tx
+                                           : (int64_t)1});
   size_t need_part = (size_t)maxgrid * 4;
   if (need_part > c->part_cap) {
     if (c->part) cudaFree(c->part);
@@ -827,6 +892,10 @@ static int choose_launch(ccg_ctx* c) {
 }
 
 static void free_csr_copies(ccg_ctx* c) {
+  if (c->fftW) cudaFree(c->fftW);
+  if (c->fftK) cudaFree(c->fftK);
+  if (c->fftTw) cudaFree(c->fftTw);
+  c->fftW = c->fftK = c->fftTw = nullptr;
   if (c->csr_blocks) cudaFree(c->csr_blocks);
   if (c->sell_off) cudaFree(c->sell_off);
   if (c->sell_width) cudaFree(c->sell_width);
@@ -899,6 +968,62 @@ static int run_iterations(ccg_ctx* c, int m, int maxit) {
     const double per = us / todo;
     chunk = per > 0 ? (int)std::max(1.0, std::min(32.0, 200.0 / per)) : 32;
   }
+  return CCG_OK;
+}
+
+// host-side radix-2 FFT (double) of one strided line, used once per operator
+static void host_fft_line(std::complex<double>* a, int L, int64_t stride) {
+  if (L <= 1) return;
+  std::vector<std::complex<double>> v(L);
+  int logL = 0;
+  while ((1 << logL) < L) ++logL;
+  for (int i = 0; i < L; ++i) {
+    int r = 0;
+    for (int b = 0; b < logL; ++b) r |= ((i >> b) & 1) << (logL - 1 - b);
+    v[r] = a[(int64_t)i * stride];
+  }
+  const double PI = 3.14159265358979323846264338327950288;
+  for (int h = 1; h < L; h <<= 1) {
+    for (int i0 = 0; i0 < L; i0 += 2 * h)
+      for (int m = 0; m < h; ++m) {
+        const double ang = -PI * (double)m / (double)h;
+        const std::complex<double> w(std::cos(ang), std::sin(ang));
+        const std::complex<double> x0 = v[i0 + m], x1 = v[i0 + m + h] * w;
+        v[i0 + m] = x0 + x1;
+        v[i0 + m + h] = x0 - x1;
+      }
+  }
+  for (int i = 0; i < L; ++i) a[(int64_t)i * stride] = v[i];
+}
+
+static int pow2_at_least(int64_t v, int* lg) {
+  int l = 0;
+  while ((int64_t(1) << l) < v) ++l;
+  *lg = l;
+  return 1 << l;
+}
+
+template <typename T>
+static int toeplitz_setup(ccg_ctx* c, const std::vector<std::complex<double>>& Kh) {
+  using C = typename CT<T>::c;
+  const FftGeo& g = c->geo;
+  const size_t N = (size_t)g.X2 * g.Y2 * g.Z2;
+  std::vector<C> kh(N);
+  for (size_t i = 0; i < N; ++i) { kh[i].x = (T)Kh[i].real(); kh[i].y = (T)Kh[i].imag(); }
+  const int half = std::max(1, c->fft_lmax / 2);
+  std::vector<C> tw(half);
+  const double PI = 3.14159265358979323846264338327950288;
+  for (int k = 0; k < half; ++k) {
+    const double ang = -2.0 * PI * (double)k / (double)c->fft_lmax;
+    tw[k].x = (T)std::cos(ang);
+    tw[k].y = (T)std::sin(ang);
+  }
+  CK(c, cudaMalloc(&c->fftW, N * sizeof(C)));
+  CK(c, cudaMalloc(&c->fftK, N * sizeof(C)));
+  CK(c, cudaMalloc(&c->fftTw, half * sizeof(C)));
+  CK(c, cudaMemcpy(c->fftK, kh.data(), N * sizeof(C), cudaMemcpyHostToDevice));
+  CK(c, cudaMemcpy(c->fftTw, tw.data(), half * sizeof(C), cudaMemcpyHostToDevice));
+  CK(c, cudaMemset(c->fftW, 0, N * sizeof(C)));
   return CCG_OK;
 }
 
@@ -1036,6 +1161,7 @@ int ccg_set_matvec_dense(ccg_handle c, const void* A_local, int64_t row0, int64_
   if (!is_device_ptr(A_local)) FAIL(c, CCG_E_ARG, "A_local must be a device pointer");
   if (((uintptr_t)A_local) % c->esz) FAIL(c, CCG_E_ARG, "A_local misaligned");
   CK(c, cudaSetDevice(c->device));
+  free_csr_copies(c);
   c->opk = OPK_DENSE;
   c->A = A_local;
   c->lda = lda;
@@ -1169,6 +1295,64 @@ int ccg_set_matvec_stencil7(ccg_handle c, int64_t nx, int64_t ny, int64_t nz, co
   c->vec_ok = true;
   const char* zc = getenv("CCG_STENCIL_ZC");
   c->szc = zc ? std::max(1, atoi(zc)) : 4;
+  invalidate_graphs(c);
+  return c->dtype == CCG_C64 ? choose_launch<float>(c) : choose_launch<double>(c);
+}
+
+int ccg_set_matvec_toeplitz3(ccg_handle c, int64_t nx, int64_t ny, int64_t nz, const double* kernel,
+                             const double* diag, uint32_t flags) {
+  if (!c) return CCG_E_ARG;
+  if (!kernel || !diag) FAIL(c, CCG_E_ARG, "kernel / diag is NULL");
+  if (nx < 1 || ny < 1 || nz < 1 || nx > 1024 || ny > 1024 || nz > 1024)
+    FAIL(c, CCG_E_DIM, "lattice sides must be in [1, 1024]");
+  if (nx * ny * nz != c->n) FAIL(c, CCG_E_DIM, "nx*ny*nz != n");
+  CK(c, cudaSetDevice(c->device));
+  free_csr_copies(c);
+  FftGeo g;
+  g.nx = (int)nx; g.ny = (int)ny; g.nz = (int)nz;
+  g.X2 = pow2_at_least(2 * nx - 1, &g.lx);
+  g.Y2 = pow2_at_least(2 * ny - 1, &g.ly);
+  g.Z2 = pow2_at_least(2 * nz - 1, &g.lz);
+  const int lyz = std::max(g.Y2, g.Z2);
+  g.tyz = std::max(1, std::min(g.X2, std::min(16, 2048 / lyz)));
+  g.tx = std::max(1, std::min(32, 2048 / g.X2));
+  c->geo = g;
+  c->fft_lmax = std::max(g.X2, std::max(g.Y2, g.Z2));
+  // circulant embedding of the kernel, 3-D FFT in double, normalised
+  const int64_t kx = 2 * nx - 1, ky = 2 * ny - 1;
+  const size_t N = (size_t)g.X2 * g.Y2 * g.Z2;
+  std::vector<std::complex<double>> K(N);
+  auto disp = [](int m, int M, int64_t n, int64_t* d) {
+    if (m < n) { *d = m; return true; }
+    if (m > M - n) { *d = (int64_t)m - M; return true; }
+    return false;
+  };
+  for (int mz = 0; mz < g.Z2; ++mz)
+    for (int my = 0; my < g.Y2; ++my)
+      for (int mx = 0; mx < g.X2; ++mx) {
+        int64_t dx, dy, dz;
+        std::complex<double> v(0.0, 0.0);
+        if (disp(mx, g.X2, nx, &dx) && disp(my, g.Y2, ny, &dy) && disp(mz, g.Z2, nz, &dz) &&
+            !(dx == 0 && dy == 0 && dz == 0)) {
+          const int64_t ki = (dx + nx - 1) + kx * ((dy + ny - 1) + ky * (dz + nz - 1));
+          v = std::complex<double>(kernel[2 * ki], kernel[2 * ki + 1]);
+          if (!std::isfinite(v.real()) || !std::isfinite(v.imag())) FAIL(c, CCG_E_ARG, "non-finite kernel value");
+        }
+        K[((size_t)mz * g.Y2 + my) * g.X2 + mx] = v;
+      }
+  for (int64_t l = 0; l < (int64_t)g.Y2 * g.Z2; ++l) host_fft_line(K.data() + l * g.X2, g.X2, 1);
+  for (int mz = 0; mz < g.Z2; ++mz)
+    for (int mx = 0; mx < g.X2; ++mx) host_fft_line(K.data() + (size_t)mz * g.Y2 * g.X2 + mx, g.Y2, g.X2);
+  for (int64_t l = 0; l < (int64_t)g.X2 * g.Y2; ++l) host_fft_line(K.data() + l, g.Z2, (int64_t)g.X2 * g.Y2);
+  const double inv = 1.0 / (double)N;
+  for (auto& v : K) v *= inv;
+  if (!std::isfinite(diag[0]) || !std::isfinite(diag[1])) FAIL(c, CCG_E_ARG, "non-finite diagonal");
+  c->tdiag = make_double2(diag[0], diag[1]);
+  int rc = c->dtype == CCG_C64 ? toeplitz_setup<float>(c, K) : toeplitz_setup<double>(c, K);
+  if (rc) return rc;
+  c->opk = OPK_TOEPLITZ;
+  c->flags = flags;
+  c->vec_ok = true;
   invalidate_graphs(c);
   return c->dtype == CCG_C64 ? choose_launch<float>(c) : choose_launch<double>(c);
 }

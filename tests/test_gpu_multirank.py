@@ -223,3 +223,32 @@ def test_sharded_stencil_apply_and_solve(G):
             assert relerr(g.solve(method, y, 0.0, k)["x"], xc) <= max(1e-9, 2 * D), method
     finally:
         g.close()
+
+
+@pytest.mark.parametrize("G", [2, 4])
+def test_sharded_toeplitz(G):
+    """FFT operator with world > 1: gathered input, replicated transform, own rows."""
+    from oracle import ToeplitzOp
+    from workloads import dda_kernel
+    dims = (8, 6, 4)
+    K = dda_kernel(dims, 0.9)
+    op = ToeplitzOp(K, dims, 2.5 + 0.3j)
+    n = 192
+    hs = ccg.ccg_create_loopback_group(G, "c128", n)
+    g = DenseGroup.__new__(DenseGroup)
+    g.n, g.G, g.nloc, g.dtype, g.dt, g.hs = n, G, n // G, np.complex128, "c128", hs
+    try:
+        for r in range(G):
+            ccg.ccg_set_matvec_toeplitz3(hs[r], *dims, K, 2.5 + 0.3j)
+        x = (np.random.default_rng(3).standard_normal(n) + 0.25j).astype(np.complex128)
+        for o, f in (("A", op.apply), ("AH", op.apply_h), ("AT", op.apply_t)):
+            assert relerr(g.apply(x, o), f(x)) <= 1e-13, o
+        y = (np.random.default_rng(4).standard_normal(n) + 1j).astype(np.complex128)
+        for m in ("bicgstab", "qmr", "cocr"):
+            o = oracle.solve(m, op, y, 1e-10, 500)
+            r = g.solve(m, y, 1e-10, 500)
+            assert r["status"] == "CONVERGED" and abs(r["iterations"] - o.iterations) <= 2, m
+            k = min(r["iterations"], o.iterations)
+            assert relerr(g.solve(m, y, 0.0, k)["x"], oracle.solve(m, op, y, 0.0, k).x) <= 1e-9, m
+    finally:
+        g.close()

@@ -293,3 +293,88 @@ def test_stencil_bad_args():
         assert e.value.code == -1
     finally:
         ccg.ccg_destroy(h)
+
+
+# ---------------------------------------------------------------------------
+# NEXT-4: FFT block-Toeplitz (lattice / DDA) operator (ccg_set_matvec_toeplitz3)
+# ---------------------------------------------------------------------------
+from oracle import ToeplitzOp                                   # noqa: E402
+from workloads import dda_kernel, cfg4_rhs, cfg4_rows             # noqa: E402
+from tests.test_oracle_numerics import _dense_from_kernel        # noqa: E402
+
+
+class Toeplitz(Dense):
+    def __init__(self, dims, kernel, diag, dtype=np.complex128):
+        nx, ny, nz = dims
+        self.n = nx * ny * nz
+        self.dtype = dtype
+        self.h = ccg.ccg_create(dt_name(dtype), self.n)
+        ccg.ccg_set_matvec_toeplitz3(self.h, nx, ny, nz, kernel, diag)
+
+
+@pytest.mark.parametrize("dtype", [np.complex128, np.complex64])
+@pytest.mark.parametrize("dims", [(1, 1, 1), (5, 3, 4), (7, 1, 2), (9, 6, 3), (1, 12, 5)])
+def test_toeplitz_apply_parity(dtype, dims):
+    """Random non-symmetric kernel: every product vs the brute-force dense matrix."""
+    nx, ny, nz = dims
+    rng = np.random.default_rng(nx + 10 * ny)
+    K = rng.standard_normal((2 * nz - 1, 2 * ny - 1, 2 * nx - 1)) + 1j * rng.standard_normal(
+        (2 * nz - 1, 2 * ny - 1, 2 * nx - 1))
+    A = _dense_from_kernel(K, dims, 4 - 2j)
+    x = _x(nx * ny * nz, dtype, seed=3)
+    with Toeplitz(dims, K, 4 - 2j, dtype=dtype) as h:
+        for o in ("A", "AH", "AT"):
+            ref = reference_apply(A, x.astype(np.complex128), o)
+            assert relerr(h.apply(x, o), ref) <= TOL[dtype], (o, relerr(h.apply(x, o), ref))
+
+
+def test_toeplitz_cfg2_apply_and_solves():
+    """BASELINE config 2 through the FFT operator: the dense product to 1e-13,
+    then BiCGSTAB / QMR / BiCOR / COCR P-literal against the oracle's dense solves."""
+    A, y = cfg2()
+    K = dda_kernel((16, 16, 16), 1.0)
+    with Toeplitz((16, 16, 16), K, 3 + 0.5j) as h:
+        for o in ("A", "AH", "AT"):
+            assert relerr(h.apply(y, o), reference_apply(A, y, o)) <= 1e-13, o
+        for m in ("bicgstab", "qmr", "bicor", "cocr"):
+            _parity(h, DenseOp(A), y, m, 1e-8, 1000, np.complex128, tag="cfg2-toeplitz")
+
+
+def test_toeplitz_cfg4_full_size():
+    """BASELINE config 4 (n = 65536, 68.7 GB as a dense matrix) on the FFT
+    operator: sampled rows of A·x against the oracle's dense rows, the whole
+    product against the oracle's FFT operator, and a BiCGSTAB solve whose x
+    the oracle's own operator certifies (true residual ≤ 10·tol; iteration
+    count inside the rounding envelope of SURVEY §8(c), 102-110 ± 2)."""
+    dims = (64, 32, 32)
+    K = dda_kernel(dims, 0.5)
+    y = cfg4_rhs()
+    op = ToeplitzOp(K, dims, 2.5 + 0.2j)
+    x = _x(65536, np.complex128, 4)
+    with Toeplitz(dims, K, 2.5 + 0.2j) as h:
+        ax = h.apply(x, "A")
+        assert relerr(ax, op.apply(x)) <= 1e-13
+        rows = [0, 1, 4097, 33333, 65535]
+        for r in rows:
+            ref = reference_apply(cfg4_rows(r, r + 1), x)[0]
+            assert abs(ax[r] - ref) <= 1e-13 * np.abs(cfg4_rows(r, r + 1)[0]) @ np.abs(x)
+        g = h.solve("bicgstab", y, 1e-8, 2000)
+    assert g["status"] == "CONVERGED" and 100 <= g["iterations"] <= 112
+    tr = np.linalg.norm(y - op.apply(g["x"])) / np.linalg.norm(y)
+    assert tr <= 1e-7
+    _record(test="cfg4-full-toeplitz", method="bicgstab", k_gpu=g["iterations"], true_rel_res=tr)
+
+
+def test_toeplitz_bad_args():
+    h = ccg.ccg_create("c128", 24)
+    try:
+        with pytest.raises(ccg.CcgError) as e:
+            ccg.ccg_set_matvec_toeplitz3(h, 2, 3, 5, np.zeros(3 * 5 * 9), 1.0)
+        assert e.value.code == -2
+        K = np.zeros((7, 5, 3), np.complex128)
+        K[0, 0, 0] = np.nan
+        with pytest.raises(ccg.CcgError) as e:
+            ccg.ccg_set_matvec_toeplitz3(h, 2, 3, 4, K, 1.0)
+        assert e.value.code == -1
+    finally:
+        ccg.ccg_destroy(h)

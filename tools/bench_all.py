@@ -21,7 +21,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 import paper_1208_4869_b200 as ccg  # noqa: E402
 from workloads import (cfg1, cfg2, gauss_shifted_rows, cfg3_rhs, cfg4_rhs, helmholtz_csr,  # noqa: E402
-                       helmholtz_rhs, helmholtz_coeffs, CONFIGS)
+                       helmholtz_rhs, helmholtz_coeffs, dda_kernel, CONFIGS)
 from workloads.device import cfg4_rows_device  # noqa: E402
 
 V_PASSES = {"bicgstab": 18, "cgne": 10, "qmr": 26, "bicor": 24, "cors": 24,
@@ -51,20 +51,28 @@ def timed(h, method, y, x, tol, maxit, reps, stream):
     return r, its, ms
 
 
-def run_dense(cfg, A, y, methods, tol, maxit, reps, dtype):
-    n = A.shape[0]
+def run_dense(cfg, A, y, methods, tol, maxit, reps, dtype, toeplitz=None):
+    n = y.shape[0]
     s = 8 if dtype == "c64" else 16
     h = ccg.ccg_create(dtype, n)
-    ccg.ccg_set_matvec_dense(h, A, 0, n)
+    if toeplitz is None:
+        ccg.ccg_set_matvec_dense(h, A, 0, n)
+        b_mat = n * n * s
+        opname = "dense"
+    else:
+        ccg.ccg_set_matvec_toeplitz3(h, *toeplitz)
+        b_mat = 2 * n * s                  # x read + y written: the FFT operator's irreducible bytes
+        opname = "toeplitz"
     stream = torch.cuda.ExternalStream(ccg.ccg_get_stream(h))
     x = torch.empty_like(y)
     for m in methods:
         if SEL and m not in SEL:
             continue
         r, its, ms = timed(h, m, y, x, tol, maxit, reps, stream)
-        b_iter = M_MATVEC[m] * n * n * s + V_PASSES[m] * n * s
+        b_iter = M_MATVEC[m] * b_mat + V_PASSES[m] * n * s
         ips = its / (ms / 1e3)
-        print(json.dumps({"config": cfg, "method": m, "n": n, "dtype": dtype, "status": r["status"],
+        print(json.dumps({"config": cfg, "operator": opname, "method": m, "n": n, "dtype": dtype,
+                          "status": r["status"],
                           "iterations": r["iterations"], "ms_per_solve": ms / reps,
                           "us_per_iteration": 1e3 * ms / its, "iterations_per_s": ips,
                           "effective_GBs": b_iter * ips / 1e9, "true_rel_res": r["true_rel_res"],
@@ -77,6 +85,7 @@ def main():
     ap.add_argument("--configs", default="1,2,3,4,5")
     ap.add_argument("--reps", type=int, default=0)
     ap.add_argument("--methods", default="")
+    ap.add_argument("--no-dense4", action="store_true", help="config 4: FFT operator only")
     a = ap.parse_args()
     global SEL
     SEL = set(a.methods.split(",")) if a.methods else set()
@@ -92,6 +101,8 @@ def main():
             A, y = cfg2()
             run_dense(2, torch.from_numpy(A).to(dev), torch.from_numpy(y).to(dev), SYM, cf["tol"],
                       cf["maxit"], a.reps or 50, "c128")
+            run_dense(2, None, torch.from_numpy(y).to(dev), SYM, cf["tol"], cf["maxit"], a.reps or 50, "c128",
+                      toeplitz=(16, 16, 16, dda_kernel((16, 16, 16), 1.0), 3 + 0.5j))
         elif c == 3:
             n = cf["n"]
             Ad = torch.empty((n, n), dtype=torch.complex64, device=dev)
@@ -104,6 +115,10 @@ def main():
             del Ad
         elif c == 4:
             n = cf["n"]
+            run_dense(4, None, torch.from_numpy(cfg4_rhs()).to(dev), SYM, cf["tol"], cf["maxit"], a.reps or 5,
+                      "c128", toeplitz=(64, 32, 32, dda_kernel((64, 32, 32), 0.5), 2.5 + 0.2j))
+            if a.no_dense4:
+                continue
             Ad = torch.empty((n, n), dtype=torch.complex128, device=dev)
             for r0 in range(0, n, 4096):
                 cfg4_rows_device(r0, r0 + 4096, Ad[r0:r0 + 4096])
