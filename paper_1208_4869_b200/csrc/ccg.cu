@@ -24,6 +24,7 @@
 #include "methods.cuh"
 #include "comm.cuh"
 #include "fft.cuh"
+#include "cluster.cuh"
 
 #include <complex>
 
@@ -73,6 +74,10 @@ struct ccg_ctx {
   void* fftTw = nullptr;  // exp(−2πi k/Lmax), k < Lmax/2
   int fft_lmax = 1;
   double2 tdiag = {};
+  // whole-loop cluster kernel for small dense systems (cluster.cuh)
+  bool cluster_ok = false;
+  int cluster_size = 0;   // 0 = not yet chosen
+  int cl_method = 0, cl_has_x0 = 0;
   bool vec_ok = true;
   bool bulk_ok = false;   // TMA bulk-copy GEMV usable (alignment / n multiple of a 4 KiB tile)
   int bulk_grid = 0;
@@ -608,6 +613,106 @@ struct Engine {
     TRY(allgather(c, 1));
     TRY(matvec_a(c, F(c, 1), CoQ<T>{L(c, 8), L(c, 2)}, g));
     return pass(c, CoH<T>{L(c, 4), L(c, 5), Fs(c, 1), L(c, 8), L(c, 6), L(c, 7), L(c, X), Fs(c, 0)}, g);
+  }
+
+  // ==================== whole solve loop in one cluster (cluster.cuh) ====================
+  template <class M>
+  static int launch_cluster(ccg_ctx* c, const M& m) {
+    auto kern = cluster_solve<T, M>;
+    C* y = L(c, 1);
+    ClCommon<T> cm{InitR<T>{y, nullptr, nullptr, nullptr, nullptr}, Copy<T>{L(c, X), Fs(c, 2)},
+                   Copy<T>{L(c, X), Fs(c, 2)}, TrueRes<T>{y}, F(c, 2), c->cl_has_x0};
+    switch (c->cl_method) {   // r₀ copies, as init_residual() of each method
+      case M_BICGSTAB: case M_BICG: case M_CGS: cm.ir.d0 = L(c, 2); cm.ir.d1 = L(c, 3); break;
+      case M_CGNE: case M_CGNR: cm.ir.d0 = L(c, 2); break;
+      case M_QMR: cm.ir.d0 = L(c, 2); cm.ir.d1 = L(c, 3); cm.ir.d2 = L(c, 4); break;
+      case M_BICOR: case M_CORS: cm.ir.d0 = Fs(c, 0); cm.ir.d1 = L(c, 2); break;
+      default: cm.ir.d0 = Fs(c, 0); break;   // COCR
+    }
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    cfg.blockDim = dim3(CL_NT);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = c->stream;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    if (c->cluster_size == 0) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      c->cluster_size = 8;
+      for (int cs : {16, 8, 4}) {
+        cfg.gridDim = dim3(cs);
+        at[0].val.clusterDim.x = cs;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        int ncl = 0;
+        if (cudaOccupancyMaxActiveClusters(&ncl, kern, &cfg) == cudaSuccess && ncl >= 1) {
+          c->cluster_size = cs;
+          break;
+        }
+        cudaGetLastError();
+      }
+      const char* cs = getenv("CCG_CLUSTER_SIZE");
+      if (cs) c->cluster_size = std::max(1, std::min(CL_MAX, atoi(cs)));
+    } else {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    }
+    cfg.gridDim = dim3(c->cluster_size);
+    at[0].val.clusterDim.x = c->cluster_size;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    CK(c, cudaLaunchKernelEx(&cfg, kern, m, cm, c->st, reinterpret_cast<const C*>(c->A), c->lda, c->n));
+    c->launches++;
+    return CCG_OK;
+  }
+
+  static int cluster_run(ccg_ctx* c, int m) {
+    switch (m) {
+      case M_BICGSTAB:
+        return launch_cluster(c, ClBicgstab<T>{BsP<T>{L(c, 2), Fs(c, 0), L(c, 4)}, BsV<T>{L(c, 4), L(c, 3)},
+                                               BsS<T>{L(c, 2), L(c, 4), Fs(c, 1)}, BsT<T>{L(c, 5), Fs(c, 1)},
+                                               BsX<T>{L(c, X), L(c, 2), Fs(c, 0), Fs(c, 1), L(c, 5), L(c, 3)},
+                                               F(c, 0), F(c, 1)});
+      case M_CGNE:
+        return launch_cluster(c, ClCgne<T>{CgQ<T>{L(c, 2), L(c, X), Fs(c, 0)}, CgP<T>{Fs(c, 0)}, CgP0<T>{Fs(c, 0)},
+                                           F(c, 0), L(c, 2)});
+      case M_QMR:
+        return launch_cluster(
+            c, ClQmr<T>{QmP<T>{L(c, 5), L(c, 6), Fs(c, 0), L(c, 7)}, QmPt<T>{L(c, 8), L(c, 7)},
+                        QmVW<T>{L(c, 3), L(c, 4), L(c, 8), L(c, 5), L(c, 6)},
+                        QmDV<T>{L(c, 9), L(c, 10), L(c, X), L(c, 2), Fs(c, 0), L(c, 8), L(c, 3), L(c, 4), L(c, 5),
+                                L(c, 6)},
+                        QmV<T>{L(c, 3), L(c, 4), L(c, 5), L(c, 6)}, F(c, 0), L(c, 7)});
+      case M_BICOR:
+        return launch_cluster(c, ClBicor<T>{RhoEpi<T>{L(c, 3), L(c, 2)},
+                                            BcP<T>{Fs(c, 0), L(c, 2), L(c, 3), L(c, 4), L(c, 5), L(c, 6)},
+                                            BcQs<T>{L(c, 7), L(c, 6)},
+                                            BcX<T>{L(c, X), Fs(c, 0), L(c, 2), L(c, 4), L(c, 6), L(c, 7)}, F(c, 0),
+                                            L(c, 5)});
+      case M_CORS:
+        return launch_cluster(
+            c, ClCors<T>{RhoEpi<T>{L(c, 3), L(c, 2)}, CoP<T>{Fs(c, 0), L(c, 3), L(c, 6), L(c, 7), L(c, 4), L(c, 5), Fs(c, 1)},
+                         CoQ<T>{L(c, 8), L(c, 2)},
+                         CoH<T>{L(c, 4), L(c, 5), Fs(c, 1), L(c, 8), L(c, 6), L(c, 7), L(c, X), Fs(c, 0)}, F(c, 0),
+                         F(c, 1)});
+      case M_BICG:
+        return launch_cluster(c, ClBicg<T>{BgP<T>{L(c, 2), L(c, 3), Fs(c, 0), L(c, 4)}, BgQ<T>{L(c, 5), L(c, 4)},
+                                           Store<T>{L(c, 6)},
+                                           BgX<T>{L(c, X), L(c, 2), L(c, 3), Fs(c, 0), L(c, 5), L(c, 6)}, F(c, 0),
+                                           L(c, 4)});
+      case M_CGS:
+        return launch_cluster(c, ClCgs<T>{CsP<T>{L(c, 2), L(c, 5), Fs(c, 0), L(c, 4)}, CsV<T>{L(c, 6), L(c, 3)},
+                                          CsQ<T>{L(c, 4), L(c, 6), L(c, 5), Fs(c, 1), L(c, X)},
+                                          CsR<T>{L(c, 2), L(c, 3)}, F(c, 0), F(c, 1)});
+      case M_COCR:
+        return launch_cluster(c, ClCocr<T>{CrP<T>{Fs(c, 0), L(c, 2), L(c, 3), L(c, 4)},
+                                           CrX<T>{L(c, X), Fs(c, 0), L(c, 3), L(c, 4)}, CrAr<T>{L(c, 2), Fs(c, 0)},
+                                           CrAr0<T>{L(c, 2), Fs(c, 0)}, F(c, 0)});
+      default:
+        return launch_cluster(c, ClCgnr<T>{CnW<T>{L(c, 3)}, CnX<T>{L(c, X), L(c, 2), Fs(c, 0), L(c, 3)},
+                                           CnZ<T>{L(c, 4)}, CnP<T>{L(c, 4), Fs(c, 0)}, CnZ0<T>{Fs(c, 0)}, F(c, 0),
+                                           L(c, 2)});
+    }
   }
 
   // ==================== SURVEY §8(f) NEXT-3 ====================
@@ -1167,6 +1272,14 @@ int ccg_set_matvec_dense(ccg_handle c, const void* A_local, int64_t row0, int64_
   c->lda = lda;
   c->flags = flags;
   c->vec_ok = (c->esz == 16) || (((uintptr_t)A_local % 16) == 0 && (lda % 2) == 0);
+  {
+    // small L2-resident systems: the whole loop in one cluster (cluster.cuh)
+    const char* ce = getenv("CCG_CLUSTER");
+    const char* cb = getenv("CCG_CLUSTER_MAXBYTES");
+    const double maxb = cb ? atof(cb) : 4.0 * 1024 * 1024;
+    c->cluster_ok = c->world == 1 && !(ce && !strcmp(ce, "0")) &&
+                    (double)c->n * (double)c->n * (double)c->esz <= maxb;
+  }
   invalidate_graphs(c);
   return c->dtype == CCG_C64 ? choose_launch<float>(c) : choose_launch<double>(c);
 }
@@ -1443,12 +1556,22 @@ int ccg_solve(ccg_handle c, ccg_method method, const void* x0_local, const void*
     CK(c, cudaMemsetAsync(c->loc[0], 0, bytes, c->stream));
   }
   const bool has_x0 = x0_local != nullptr;
-  int rc = c->dtype == CCG_C64 ? Engine<float>::setup(c, method, has_x0) : Engine<double>::setup(c, method, has_x0);
-  if (rc) return rc;
-  rc = c->dtype == CCG_C64 ? run_iterations<float>(c, method, maxit) : run_iterations<double>(c, method, maxit);
-  if (rc) return rc;
-  rc = c->dtype == CCG_C64 ? Engine<float>::true_residual(c) : Engine<double>::true_residual(c);
-  if (rc) return rc;
+  int rc;
+  if (c->opk == OPK_DENSE && c->cluster_ok && c->world == 1 && !c->timing) {
+    // small dense system: setup, every iteration and the true residual in ONE
+    // cluster launch (cluster.cuh); maxit and the stopping rule live in the State
+    c->cl_method = method;
+    c->cl_has_x0 = has_x0 ? 1 : 0;
+    rc = c->dtype == CCG_C64 ? Engine<float>::cluster_run(c, method) : Engine<double>::cluster_run(c, method);
+    if (rc) return rc;
+  } else {
+    rc = c->dtype == CCG_C64 ? Engine<float>::setup(c, method, has_x0) : Engine<double>::setup(c, method, has_x0);
+    if (rc) return rc;
+    rc = c->dtype == CCG_C64 ? run_iterations<float>(c, method, maxit) : run_iterations<double>(c, method, maxit);
+    if (rc) return rc;
+    rc = c->dtype == CCG_C64 ? Engine<float>::true_residual(c) : Engine<double>::true_residual(c);
+    if (rc) return rc;
+  }
   CK(c, cudaMemcpyAsync(c->st_host, c->st, sizeof(State), cudaMemcpyDeviceToHost, c->stream));
   TRY(stage_out(c, x_local_out, c->loc[0], bytes));
   CK(c, cudaStreamSynchronize(c->stream));

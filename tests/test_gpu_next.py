@@ -378,3 +378,38 @@ def test_toeplitz_bad_args():
         assert e.value.code == -1
     finally:
         ccg.ccg_destroy(h)
+
+
+# ---------------------------------------------------------------------------
+# Whole solve loop in one thread-block cluster (cluster.cuh; small dense n)
+# ---------------------------------------------------------------------------
+ALL9 = ("bicgstab", "cgne", "qmr", "bicor", "cors") + NEXT3
+
+
+@pytest.mark.parametrize("cluster", ["0", "1"])
+@pytest.mark.parametrize("method", ALL9)
+def test_cluster_loop_cfg1(monkeypatch, cluster, method):
+    """Config 1 with the single-cluster loop (default at this size) and with the
+    multi-kernel graph loop: both P-literal against the oracle, same matvec
+    counts and residual history."""
+    monkeypatch.setenv("CCG_CLUSTER", cluster)
+    A, y = cfg1()
+    if method == "cocr":
+        A = _csym(A)
+    with Dense(A) as h:
+        o, g = _parity(h, DenseOp(A), y, method, 1e-10, 500, np.complex128, tag=f"cfg1-cluster{cluster}")
+        assert (g["matvecs_a"], g["matvecs_ah"]) == (o.matvecs_a, o.matvecs_ah)
+        h.solve(method, y, 1e-10, 500)
+        np.testing.assert_allclose(ccg.ccg_get_history(h.h), np.array(o.history, float) / o.history[0],
+                                   rtol=1e-6, atol=1e-12)
+
+
+@pytest.mark.parametrize("n", [1, 5, 33, 200, 511])
+@pytest.mark.parametrize("method", ["bicgstab", "qmr", "cgne", "bicg"])
+def test_cluster_loop_ragged_c64(monkeypatch, n, method):
+    """Row ranges that do not divide the cluster (n < cluster size included), c64."""
+    monkeypatch.setenv("CCG_CLUSTER", "1")
+    A = dense_random(n, seed=n, dtype=np.complex64, shift=3 - 1j)
+    y = (dense_random(n, seed=n + 1)[:, 0] * 3).astype(np.complex64)
+    with Dense(A) as h:
+        _parity(h, DenseOp(A), y, method, 1e-5, 300, np.complex64, tag=f"cluster-c64-{n}", literal=False)
