@@ -313,10 +313,11 @@ def run_ccg(args):
     ach_a = bytes_a / (ms_a / n_a * 1e-3) / 1e9 if n_a else None
     ach_ah = bytes_ah / (ms_ah / n_ah * 1e-3) / 1e9 if n_ah else None
     traffic = ncu_traffic()
-    roof = {"bound": "hbm", "kernel": "gemv_n_kernel<float,8,256> (A·x)",
+    roof = {"bound": "hbm", "kernel": "gemv_n_split<float,256,8> (A·x, + strip-sum stage 2)",
             "achieved": ach_a, "peak": peak, "unit": "GB/s",
             "frac": (ach_a / peak) if ach_a else None,
             "frac_of_8TBs": (ach_a / 8000.0) if ach_a else None,
+            "frac_of_7p7TBs_nominal": (ach_a / 7700.0) if ach_a else None,
             "traffic": traffic.get("dram_bytes_per_launch") if traffic else None,
             "algorithmic_bytes_per_launch": bytes_a, "avg_launch_ms": (ms_a / n_a) if n_a else None,
             "launches_timed": n_a, "peak_source": peak_src,

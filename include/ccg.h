@@ -236,8 +236,11 @@ int ccg_get_history(ccg_handle h, double* rel_res, int32_t cap, int32_t* len);
 
 /* Device time of the matvec kernels of the last ccg_solve / ccg_apply when
  * timing is enabled (CUDA events on the handle's stream around every matvec
- * launch; disables graph capture while on).  ms_a/ms_ah: summed milliseconds of
- * the A·x and Aᴴ·x kernels, n_a/n_ah: launch counts.  Any pointer may be NULL. */
+ * launch; disables graph capture and the single-cluster loop while on).
+ * ms_a/ms_ah: summed milliseconds of the A·x and Aᴴ·x kernels (the QMR/BiCG
+ * dual product counts as A·x); n_a/n_ah: products actually executed (launches
+ * gated off after convergence are not counted, their few µs stay in the sum).
+ * Any pointer may be NULL. */
 int ccg_set_timing(ccg_handle h, int enable);
 int ccg_get_timing(ccg_handle h, double* ms_a, int32_t* n_a, double* ms_ah, int32_t* n_ah);
 

@@ -1589,6 +1589,13 @@ int ccg_solve(ccg_handle c, ccg_method method, const void* x0_local, const void*
   res->true_rel_res = r0 > 0 ? sqrt(s.true_rr) / r0 : 0.0;
   if (!std::isfinite(s.true_rr)) res->status = CCG_NONFINITE;
   if (res->status == CCG_CONVERGED && res->true_rel_res > 10.0 * tol) res->status = CCG_FALSE_CONVERGENCE;
+  if (c->timing) {
+    // average over EXECUTED products: launches gated off after convergence
+    // (e.g. CGNE's Aᴴr in the converged iteration) return at once and would
+    // otherwise deflate the per-launch time (their few µs stay in the sum)
+    c->n_a = std::min(c->n_a, res->matvecs_a + 1);   // + the true-residual product
+    c->n_ah = std::min(c->n_ah, res->matvecs_ah);
+  }
   c->hist_len = std::min(c->hist_cap, res->iterations + 1);
   res->wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count();
   return CCG_OK;
