@@ -90,7 +90,8 @@ typedef enum {
   CCG_E_STATE = -4,      /* ccg_apply/ccg_solve before any ccg_set_matvec_* */
   CCG_E_CUDA = -5,       /* CUDA runtime error (text in ccg_last_error) */
   CCG_E_NCCL = -6,       /* NCCL error or NCCL unavailable with world > 1 */
-  CCG_E_OOM = -7         /* device allocation failed */
+  CCG_E_OOM = -7,        /* device allocation failed */
+  CCG_E_USER = -8        /* a user matvec callback returned non-zero */
 } ccg_err;
 
 /* Solve outcome (mirrors SPEC SolverOutcome). */
@@ -213,6 +214,30 @@ int ccg_set_matvec_stencil7(ccg_handle h, int64_t nx, int64_t ny, int64_t nz, co
  * diagonal values: CCG_E_ARG. */
 int ccg_set_matvec_toeplitz3(ccg_handle h, int64_t nx, int64_t ny, int64_t nz, const double* kernel,
                              const double* diag, uint32_t flags);
+
+/* User operator: the paper's own contract, P:95 [§5] "User can implement
+ * his/her own sparse matrix scheme in matvec and cmatvec" (the product
+ * is "separated from the conjugate gradient iterations itself").  The library
+ * calls fn for every product and runs the iteration (fused vector passes,
+ * reductions, scalar steps) around it.
+ *   fn(user, op, x, y, n, row0, nloc, stream) must ENQUEUE on `stream` (a
+ *   cudaStream_t) y[0:nloc] = (op(A)·x)[row0 : row0+nloc] and return 0, where
+ *   op is CCG_OP_A / CCG_OP_AH / CCG_OP_AT, x a DEVICE pointer to the FULL
+ *   length-n input (gathered over ranks when world > 1) and y a DEVICE pointer
+ *   to nloc outputs, both in the handle's precision, valid only until the
+ *   product's work completes on the stream.  A non-zero return aborts the
+ *   call with CCG_E_USER.
+ *   caps  : CCG_CB_A (required) | CCG_CB_AH | CCG_CB_AT — the products fn
+ *           provides (methods needing Aᴴ without CCG_CB_AH: CCG_E_CAPABILITY);
+ *           | CCG_CB_GRAPH_SAFE if fn only enqueues capturable asynchronous work
+ *           (then the iteration runs as a replayed CUDA graph and fn is called
+ *           once per method, at capture; otherwise fn is called every product).
+ *   user  : opaque, passed back.  fn, user and whatever they reference are
+ *           borrowed until ccg_destroy or the next set_matvec. */
+enum { CCG_CB_A = 1, CCG_CB_AH = 2, CCG_CB_AT = 4, CCG_CB_GRAPH_SAFE = 8 };
+typedef int (*ccg_matvec_fn)(void* user, int op, const void* x, void* y, int64_t n, int64_t row0,
+                             int64_t nloc, void* stream);
+int ccg_set_matvec_callback(ccg_handle h, ccg_matvec_fn fn, void* user, uint32_t caps, uint32_t flags);
 
 /* y_local = (op(A)·x)[row0 : row0+nloc] from x_local = x[row0 : row0+nloc].
  * x_local / y_local may be HOST or DEVICE pointers (detected); nloc elements.

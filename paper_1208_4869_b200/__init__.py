@@ -28,12 +28,15 @@ STATUS = {0: "CONVERGED", 1: "MAXIT", 2: "BREAKDOWN", 3: "FALSE_CONVERGENCE", 4:
 BREAKDOWN = {0: None, 1: "rho", 2: "sigma", 3: "tt", 4: "omega", 5: "pi", 6: "delta",
              7: "epsilon", 8: "beta", 9: "xi", 10: "vnorm", 11: "wnorm", 12: "gamma"}
 ERRORS = {0: "CCG_OK", -1: "CCG_E_ARG", -2: "CCG_E_DIM", -3: "CCG_E_CAPABILITY",
-          -4: "CCG_E_STATE", -5: "CCG_E_CUDA", -6: "CCG_E_NCCL", -7: "CCG_E_OOM"}
+          -4: "CCG_E_STATE", -5: "CCG_E_CUDA", -6: "CCG_E_NCCL", -7: "CCG_E_OOM", -8: "CCG_E_USER"}
+CB_A, CB_AH, CB_AT, CB_GRAPH_SAFE = 1, 2, 4, 8
+MATVEC_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
+                             ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p)
 
 # every symbol include/ccg.h declares (checked by tests/test_abi.py)
 EXPORTS = ("ccg_get_unique_id", "ccg_create", "ccg_create_loopback_group",
            "ccg_set_matvec_dense", "ccg_set_matvec_csr", "ccg_set_matvec_stencil7",
-           "ccg_set_matvec_toeplitz3",
+           "ccg_set_matvec_toeplitz3", "ccg_set_matvec_callback",
            "ccg_apply", "ccg_solve", "ccg_get_history", "ccg_set_timing", "ccg_get_timing",
            "ccg_last_launch_count", "ccg_get_stream", "ccg_last_error", "ccg_destroy",
            "ccg_version")
@@ -88,6 +91,7 @@ def load():
         "ccg_set_matvec_stencil7": (ctypes.c_int, [vp, i64, i64, i64, ctypes.POINTER(dbl), u32]),
         "ccg_set_matvec_toeplitz3": (ctypes.c_int, [vp, i64, i64, i64, ctypes.POINTER(dbl),
                                                     ctypes.POINTER(dbl), u32]),
+        "ccg_set_matvec_callback": (ctypes.c_int, [vp, MATVEC_FN, vp, u32, u32]),
         "ccg_apply": (ctypes.c_int, [vp, ctypes.c_int, vp, vp]),
         "ccg_solve": (ctypes.c_int, [vp, ctypes.c_int, vp, vp, vp, dbl, i32,
                                      ctypes.POINTER(ccg_result)]),
@@ -210,6 +214,29 @@ def ccg_set_matvec_toeplitz3(h, nx, ny, nz, kernel, diag, flags=0):
     d = (ctypes.c_double * 2)(complex(diag).real, complex(diag).imag)
     _check(h, load().ccg_set_matvec_toeplitz3(h, int(nx), int(ny), int(nz), kp, d, int(flags)))
     _keepalive[h] = []
+
+
+def ccg_set_matvec_callback(h, fn, caps=CB_A, flags=0):
+    """User operator: ``fn(op, x_ptr, y_ptr, n, row0, nloc, stream_ptr) -> int``
+    must enqueue y[0:nloc] = (op(A)·x)[row0:row0+nloc] on the stream (device
+    pointers; op 0 = A, 1 = Aᴴ, 2 = Aᵀ) and return 0."""
+    def tramp(user, op, x, y, n, row0, nloc, stream):
+        try:
+            return int(fn(op, x, y, n, row0, nloc, stream) or 0)
+        except Exception:  # pragma: no cover - reported as CCG_E_USER
+            import traceback
+            traceback.print_exc()
+            return 1
+    cfn = MATVEC_FN(tramp)
+    _check(h, load().ccg_set_matvec_callback(h, cfn, None, int(caps), int(flags)))
+    _keepalive[h] = [cfn, fn]
+
+
+def ccg_set_matvec_callback_ptr(h, fn_addr, user_addr=None, caps=CB_A, flags=0):
+    """Same, with a native function pointer (address) and an opaque user pointer."""
+    cfn = ctypes.cast(ctypes.c_void_p(int(fn_addr)), MATVEC_FN)
+    _check(h, load().ccg_set_matvec_callback(h, cfn, user_addr, int(caps), int(flags)))
+    _keepalive[h] = [cfn]
 
 
 def ccg_apply(h, op, x, y):

@@ -38,7 +38,7 @@ thread_local std::string g_create_err;
 // context
 // ===========================================================================
 enum { NLOCAL = 12, NFULL = 3 };
-enum { OPK_NONE = 0, OPK_DENSE = 1, OPK_CSR = 2, OPK_STENCIL = 3, OPK_TOEPLITZ = 4 };
+enum { OPK_NONE = 0, OPK_DENSE = 1, OPK_CSR = 2, OPK_STENCIL = 3, OPK_TOEPLITZ = 4, OPK_CALLBACK = 5 };
 enum { GEMV_SPLIT = 0, GEMV_BULK = 1, GEMV_ROWS = 2, GEMV_COLS = 3 };
 
 struct ccg_ctx {
@@ -74,6 +74,11 @@ struct ccg_ctx {
   void* fftTw = nullptr;  // exp(−2πi k/Lmax), k < Lmax/2
   int fft_lmax = 1;
   double2 tdiag = {};
+  // user matvec callback (ccg_set_matvec_callback)
+  ccg_matvec_fn cb_fn = nullptr;
+  void* cb_user = nullptr;
+  uint32_t cb_caps = 0;
+  void* cb_out = nullptr;   // nloc output rows of the user's product
   // whole-loop cluster kernel for small dense systems (cluster.cuh)
   bool cluster_ok = false;
   int cluster_size = 0;   // 0 = not yet chosen
@@ -329,9 +334,24 @@ struct Engine {
     c->launches += 4;
   }
 
+  // the user's product (ccg_set_matvec_callback) into cb_out, then the
+  // method's epilogue as one fused pass over it
+  template <class Epi>
+  static int user_product(ccg_ctx* c, int op, const C* xfull, Epi epi, const int* gate) {
+    C* out = reinterpret_cast<C*>(c->cb_out);
+    tev_begin(c, op == CCG_OP_A ? 0 : 1);
+    const int rc = c->cb_fn(c->cb_user, op, xfull, out, c->n, c->row0, c->nloc, c->stream);
+    tev_end(c);
+    if (rc != 0) FAIL(c, CCG_E_USER, "user matvec callback returned " + std::to_string(rc));
+    CK(c, cudaGetLastError());
+    EpiPass<C, Epi> ep{epi, out};
+    return pass(c, ep, gate);
+  }
+
   // y_local = A · xfull (full-length buffer, own slice + gathered/halo parts)
   template <class Epi>
   static int matvec_a(ccg_ctx* c, const C* xfull, Epi epi, const int* gate) {
+    if (c->opk == OPK_CALLBACK) return user_product(c, CCG_OP_A, xfull, epi, gate);
     tev_begin(c, 0);
     if (c->opk == OPK_TOEPLITZ) {
       toeplitz(c, xfull, 0, epi, gate);
@@ -410,6 +430,15 @@ struct Engine {
   // y_local = op(A) · x_local, op = Aᴴ (conj) or Aᵀ
   template <class Epi>
   static int matvec_h(ccg_ctx* c, const C* xloc, bool conj, Epi epi, const int* gate) {
+    if (c->opk == OPK_CALLBACK) {
+      const C* xin = xloc;
+      if (c->world > 1) {
+        CK(c, cudaMemcpyAsync(Fs(c, 2), xloc, c->nloc * sizeof(C), cudaMemcpyDeviceToDevice, c->stream));
+        TRY(allgather(c, 2));
+        xin = F(c, 2);
+      }
+      return user_product(c, conj ? CCG_OP_AH : CCG_OP_AT, xin, epi, gate);
+    }
     if (c->opk == OPK_TOEPLITZ) {
       const C* xin = xloc;
       if (c->world > 1) {
@@ -997,6 +1026,8 @@ static int choose_launch(ccg_ctx* c) {
 }
 
 static void free_csr_copies(ccg_ctx* c) {
+  if (c->cb_out) cudaFree(c->cb_out);
+  c->cb_out = nullptr;
   if (c->fftW) cudaFree(c->fftW);
   if (c->fftK) cudaFree(c->fftK);
   if (c->fftTw) cudaFree(c->fftTw);
@@ -1036,7 +1067,8 @@ static int run_iterations(ccg_ctx* c, int m, int maxit) {
   };
   TRY(read_done());
   if (done) return CCG_OK;
-  if (c->timing || (c->comm && !c->comm->graph_safe)) {
+  const bool eager_cb = c->opk == OPK_CALLBACK && !(c->cb_caps & CCG_CB_GRAPH_SAFE);
+  if (c->timing || eager_cb || (c->comm && !c->comm->graph_safe)) {
     for (int k = 0; k < maxit && !done; ++k) {
       TRY(E::iter(c, m));
       TRY(read_done());
@@ -1470,6 +1502,23 @@ int ccg_set_matvec_toeplitz3(ccg_handle c, int64_t nx, int64_t ny, int64_t nz, c
   return c->dtype == CCG_C64 ? choose_launch<float>(c) : choose_launch<double>(c);
 }
 
+int ccg_set_matvec_callback(ccg_handle c, ccg_matvec_fn fn, void* user, uint32_t caps, uint32_t flags) {
+  if (!c) return CCG_E_ARG;
+  if (!fn) FAIL(c, CCG_E_ARG, "fn is NULL");
+  if (!(caps & CCG_CB_A)) FAIL(c, CCG_E_ARG, "caps must include CCG_CB_A");
+  CK(c, cudaSetDevice(c->device));
+  free_csr_copies(c);
+  CK(c, cudaMalloc(&c->cb_out, (size_t)std::max<int64_t>(c->nloc, 1) * c->esz));
+  c->opk = OPK_CALLBACK;
+  c->cb_fn = fn;
+  c->cb_user = user;
+  c->cb_caps = caps;
+  c->flags = flags;
+  c->vec_ok = true;
+  invalidate_graphs(c);
+  return c->dtype == CCG_C64 ? choose_launch<float>(c) : choose_launch<double>(c);
+}
+
 static int stage_in(ccg_ctx* c, void* dst, const void* src, size_t bytes) {
   if (is_device_ptr(src)) {
     CK(c, cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, c->stream));
@@ -1498,6 +1547,8 @@ int ccg_apply(ccg_handle c, ccg_op op, const void* x_local, void* y_local) {
   if (c->opk == OPK_NONE) FAIL(c, CCG_E_STATE, "no operator set (call ccg_set_matvec_*)");
   if (c->opk == OPK_CSR && op != CCG_OP_A && (!(c->flags & CCG_FLAG_SYMMETRIC) || c->world > 1))
     FAIL(c, CCG_E_CAPABILITY, "CSR Aᴴ/Aᵀ needs CCG_FLAG_SYMMETRIC and world == 1");
+  if (c->opk == OPK_CALLBACK && !(c->cb_caps & (op == CCG_OP_A ? CCG_CB_A : op == CCG_OP_AH ? CCG_CB_AH : CCG_CB_AT)))
+    FAIL(c, CCG_E_CAPABILITY, "the user callback does not provide this product");
   CK(c, cudaSetDevice(c->device));
   c->launches = 0;
   c->ms_a = c->ms_ah = 0;
@@ -1526,6 +1577,8 @@ int ccg_solve(ccg_handle c, ccg_method method, const void* x0_local, const void*
   if (c->opk == OPK_NONE) FAIL(c, CCG_E_STATE, "no operator set (call ccg_set_matvec_*)");
   if (needs_ah(method) && c->opk == OPK_CSR && (!(c->flags & CCG_FLAG_SYMMETRIC) || c->world > 1))
     FAIL(c, CCG_E_CAPABILITY, "method needs Aᴴ; CSR provides it only with CCG_FLAG_SYMMETRIC and world == 1");
+  if (c->opk == OPK_CALLBACK && (!(c->cb_caps & CCG_CB_A) || (needs_ah(method) && !(c->cb_caps & CCG_CB_AH))))
+    FAIL(c, CCG_E_CAPABILITY, "the user callback does not provide the products this method needs");
   CK(c, cudaSetDevice(c->device));
   c->launches = 0;
   c->ms_a = c->ms_ah = 0;
