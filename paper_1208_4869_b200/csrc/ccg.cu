@@ -263,7 +263,16 @@ struct Engine {
   // -------------------- kernels --------------------
   template <class Op>
   static int pass(ccg_ctx* c, Op op, const int* gate) {
-    pass_kernel<NT, Op><<<c->pass_grid, NT, 0, c->stream>>>(op, c->nloc, make_red(c), c->st, gate);
+    // whole waves at this functor's own occupancy (register use differs
+    // between phases: 32-48 registers => 5-8 CTAs per SM)
+    static int occ = 0;
+    if (occ == 0) {
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pass_kernel<NT, Op>, NT, 0);
+      occ = std::max(1, std::min(occ, 8));
+    }
+    const int grid = (int)std::max<int64_t>(
+        1, std::min<int64_t>((c->nloc + NT - 1) / NT, (int64_t)c->sm_count * occ));
+    pass_kernel<NT, Op><<<grid, NT, 0, c->stream>>>(op, c->nloc, make_red(c), c->st, gate);
     c->launches++;
     CK(c, cudaGetLastError());
     return post<Op>(c, gate);

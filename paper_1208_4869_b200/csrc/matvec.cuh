@@ -682,6 +682,34 @@ spmv_stream_kernel(const int32_t* __restrict__ rowptr, const int32_t* __restrict
 // fully coalesced, one row per lane, no shared memory and no barriers.  The
 // row sum runs in CSR column order (same order as the CSR kernels).
 // ---------------------------------------------------------------------------
+// one SELL row of exactly W stored entries: all W column indices, then all W
+// values and x gathers are issued before any arithmetic (padding: col = −1,
+// gather clamped to index 0 and its product skipped), then the products are
+// added in CSR column order, each formed from zero
+template <int W, bool CONJ, typename C>
+__device__ __forceinline__ C sell_row(const int32_t* __restrict__ scol, const C* __restrict__ sval,
+                                      const C* __restrict__ x, int64_t base) {
+  int col[W];
+#pragma unroll
+  for (int u = 0; u < W; ++u) col[u] = __ldcs(scol + base + 32 * (int64_t)u);
+  C v[W], xv[W];
+#pragma unroll
+  for (int u = 0; u < W; ++u) {
+    v[u] = __ldcs(sval + base + 32 * (int64_t)u);
+    xv[u] = __ldg(x + max(col[u], 0));
+  }
+  C acc = czero<C>();
+#pragma unroll
+  for (int u = 0; u < W; ++u) {
+    C p = czero<C>();
+    cfma(p, v[u], CONJ ? cconj(xv[u]) : xv[u]);
+    const C a2 = cadd(acc, p);
+    acc.x = col[u] >= 0 ? a2.x : acc.x;   // select, not a branch: the loads stay batched
+    acc.y = col[u] >= 0 ? a2.y : acc.y;
+  }
+  return acc;
+}
+
 template <typename T, int NT, bool CONJ, class Epi>
 __global__ void __launch_bounds__(NT)
 spmv_sell_kernel(const int64_t* __restrict__ soff, const int32_t* __restrict__ swidth,
@@ -697,36 +725,102 @@ spmv_sell_kernel(const int64_t* __restrict__ soff, const int32_t* __restrict__ s
 #pragma unroll
   for (int k = 0; k < KK; ++k) dacc[k] = make_double2(0.0, 0.0);
   const int64_t nwarps_rows = ((nrows + 31) / 32) * 32;
-  for (int64_t i = (int64_t)blockIdx.x * NT + threadIdx.x; i < nwarps_rows; i += (int64_t)gridDim.x * NT) {
+  const int64_t stride = (int64_t)gridDim.x * NT;
+  int64_t i = (int64_t)blockIdx.x * NT + threadIdx.x;
+  // two rows per step (i, i + stride) when their slices share the common
+  // stencil width 7: twice the loads in flight per thread
+  for (; i + stride < nwarps_rows; i += 2 * stride) {
+    const int64_t s1 = i >> 5, s2 = (i + stride) >> 5;
+    const int lane = (int)(i & 31);
+    const int w1 = __ldg(swidth + s1), w2 = __ldg(swidth + s2);
+    if (w1 != 7 || w2 != 7) break;      // warp-uniform; the generic loop below finishes
+    const int64_t b1 = __ldg(soff + s1) + lane, b2 = __ldg(soff + s2) + lane;
+    int c1[7], c2[7];
+#pragma unroll
+    for (int u = 0; u < 7; ++u) { c1[u] = __ldcs(scol + b1 + 32 * u); c2[u] = __ldcs(scol + b2 + 32 * u); }
+    C v1[7], v2[7], x1[7], x2[7];
+#pragma unroll
+    for (int u = 0; u < 7; ++u) {
+      v1[u] = __ldcs(sval + b1 + 32 * u); x1[u] = __ldg(x + max(c1[u], 0));
+      v2[u] = __ldcs(sval + b2 + 32 * u); x2[u] = __ldg(x + max(c2[u], 0));
+    }
+    C a1 = czero<C>(), a2 = czero<C>();
+#pragma unroll
+    for (int u = 0; u < 7; ++u) {
+      C p = czero<C>(), q = czero<C>();
+      cfma(p, v1[u], CONJ ? cconj(x1[u]) : x1[u]);
+      cfma(q, v2[u], CONJ ? cconj(x2[u]) : x2[u]);
+      const C t1 = cadd(a1, p), t2 = cadd(a2, q);
+      a1.x = c1[u] >= 0 ? t1.x : a1.x; a1.y = c1[u] >= 0 ? t1.y : a1.y;
+      a2.x = c2[u] >= 0 ? t2.x : a2.x; a2.y = c2[u] >= 0 ? t2.y : a2.y;
+    }
+    if (i < nrows) epi(i, CONJ ? cconj(a1) : a1, dacc);
+    if (i + stride < nrows) epi(i + stride, CONJ ? cconj(a2) : a2, dacc);
+  }
+  for (; i < nwarps_rows; i += stride) {
     const int64_t s = i >> 5;
     const int lane = (int)(i & 31);
     const int w = __ldg(swidth + s);
     const int64_t base = __ldg(soff + s) + lane;
-    C acc = czero<C>();
-    for (int j0 = 0; j0 < w; j0 += U) {
-      int col[U];
-      C v[U];
+    C acc;
+    switch (w) {   // warp-uniform: the whole slice shares its width
+      case 0: acc = czero<C>(); break;
+      case 1: acc = sell_row<1, CONJ>(scol, sval, x, base); break;
+      case 2: acc = sell_row<2, CONJ>(scol, sval, x, base); break;
+      case 3: acc = sell_row<3, CONJ>(scol, sval, x, base); break;
+      case 4: acc = sell_row<4, CONJ>(scol, sval, x, base); break;
+      case 5: acc = sell_row<5, CONJ>(scol, sval, x, base); break;
+      case 6: acc = sell_row<6, CONJ>(scol, sval, x, base); break;
+      case 7: acc = sell_row<7, CONJ>(scol, sval, x, base); break;
+      case 8: acc = sell_row<8, CONJ>(scol, sval, x, base); break;
+      default: {
+        acc = czero<C>();
+        for (int j0 = 0; j0 < w; j0 += U) {
+          int col[U];
+          C v[U];
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int j = j0 + u;
-        col[u] = j < w ? __ldcs(scol + base + 32 * (int64_t)j) : -1;
-        v[u] = j < w ? __ldcs(sval + base + 32 * (int64_t)j) : czero<C>();
-      }
-      C xv[U];
+          for (int u = 0; u < U; ++u) {
+            const int j = j0 + u;
+            col[u] = j < w ? __ldcs(scol + base + 32 * (int64_t)j) : -1;
+            v[u] = j < w ? __ldcs(sval + base + 32 * (int64_t)j) : czero<C>();
+          }
+          C xv[U];
 #pragma unroll
-      for (int u = 0; u < U; ++u) xv[u] = col[u] >= 0 ? __ldg(x + col[u]) : czero<C>();
+          for (int u = 0; u < U; ++u) xv[u] = col[u] >= 0 ? __ldg(x + col[u]) : czero<C>();
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        if (col[u] >= 0) {
-          C p = czero<C>();
-          cfma(p, v[u], CONJ ? cconj(xv[u]) : xv[u]);
-          acc = cadd(acc, p);
+          for (int u = 0; u < U; ++u) {
+            if (col[u] >= 0) {
+              C p = czero<C>();
+              cfma(p, v[u], CONJ ? cconj(xv[u]) : xv[u]);
+              acc = cadd(acc, p);
+            }
+          }
         }
       }
     }
     if (i < nrows) epi(i, CONJ ? cconj(acc) : acc, dacc);
   }
   if constexpr (Epi::K > 0) finish_reduction<KK, NT, Epi>(dacc, red, st);
+}
+
+// CSR -> SELL-32 scatter (one thread per row), run once at ccg_set_matvec_csr
+template <typename C>
+__global__ void csr_to_sell(const int32_t* __restrict__ rowptr, const int32_t* __restrict__ colind,
+                            const C* __restrict__ vals, const int64_t* __restrict__ soff,
+                            const int32_t* __restrict__ swidth, int64_t nrows, int32_t* scol, C* sval) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= ((nrows + 31) / 32) * 32) return;
+  const int64_t s = i >> 5;
+  const int lane = (int)(i & 31);
+  const int w = swidth[s];
+  const int64_t base = soff[s] + lane;
+  const int k0 = i < nrows ? rowptr[i] : 0, k1 = i < nrows ? rowptr[i + 1] : 0;
+  for (int j = 0; j < w; ++j) {
+    const int k = k0 + j;
+    C z; z.x = 0; z.y = 0;
+    scol[base + 32 * (int64_t)j] = k < k1 ? colind[k] : -1;
+    sval[base + 32 * (int64_t)j] = k < k1 ? vals[k] : z;
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -790,26 +884,6 @@ stencil7_kernel(const typename CT<T>::c* __restrict__ x, int nx, int ny, int nz,
     }
   }
   if constexpr (Epi::K > 0) finish_reduction<KK, 256, Epi>(dacc, red, st);
-}
-
-// CSR -> SELL-32 scatter (one thread per row), run once at ccg_set_matvec_csr
-template <typename C>
-__global__ void csr_to_sell(const int32_t* __restrict__ rowptr, const int32_t* __restrict__ colind,
-                            const C* __restrict__ vals, const int64_t* __restrict__ soff,
-                            const int32_t* __restrict__ swidth, int64_t nrows, int32_t* scol, C* sval) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= ((nrows + 31) / 32) * 32) return;
-  const int64_t s = i >> 5;
-  const int lane = (int)(i & 31);
-  const int w = swidth[s];
-  const int64_t base = soff[s] + lane;
-  const int k0 = i < nrows ? rowptr[i] : 0, k1 = i < nrows ? rowptr[i + 1] : 0;
-  for (int j = 0; j < w; ++j) {
-    const int k = k0 + j;
-    C z; z.x = 0; z.y = 0;
-    scol[base + 32 * (int64_t)j] = k < k1 ? colind[k] : -1;
-    sval[base + 32 * (int64_t)j] = k < k1 ? vals[k] : z;
-  }
 }
 
 // ---------------------------------------------------------------------------

@@ -1,0 +1,6 @@
+set -x
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gpu_next.py tests/test_gpu_apply.py -m gpu -q -x -p no:cacheprovider -k "csr or stencil" > gpurun_out/pytest_sell.log 2>&1; echo pytest=$?; tail -2 gpurun_out/pytest_sell.log
+timeout 600 python tools/bench_all.py --configs 5 > gpurun_out/bench5.log 2>&1; echo b=$?; cut -c1-200 gpurun_out/bench5.log
+CMD="python tools/bench_all.py --configs 5 --reps 1 --methods bicgstab"
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:"pass_kernel" -s 300 -c 3 -o gpurun_out/prof5p $CMD > gpurun_out/ncu5p.log 2>&1; echo ncu=$?
