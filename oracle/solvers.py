@@ -527,14 +527,72 @@ def _cgnr(op, y, x, r, r0sq, tol2, maxit, ctx, hist, st):
     return MAXIT, maxit, False
 
 
+def _tfqmr(op, y, x, r, r0sq, tol2, maxit, ctx, hist, st, shadow=None):
+    """TFQMR (§2.1: "QMR and TFQMR algorithms are in this version
+    changed"; Freund's transpose-free QMR, Saad Alg. 7.8 restated in pairs of
+    half-steps m = 2k−2, 2k−1).  TFQMR carries no residual vector: the stopping
+    test is Freund's bound ‖r_m‖ ≤ τ_m·√(m+1) ≤ tol·‖r₀‖ (R9); an exit
+    after the first half of pair k reports iteration k with half_step (R10);
+    shadow r₀* = r₀ (R11)."""
+    st["k"] = 1                     # the setup product and α belong to iteration 1
+    rs = r.copy() if shadow is None else np.asarray(shadow, dtype=y.dtype)
+    w = r.copy()                                                # w₀ = r₀
+    u = r.copy()                                                # u₀ = r₀
+    v = op.apply(u)                                             # v₀ = A u₀
+    d = _zero_like(y)                                           # d₀ = 0
+    tau = ctx.r(sqrt(r0sq))                                     # τ₀ = ‖r₀‖
+    theta = ctx.r(0)
+    eta = ctx.c(0)
+    rho = ctx.c(ctx.dotc(rs, r))                                # ρ₀ = ⟨r₀*, r₀⟩
+    ctx.check(rho)
+    if rho == 0:
+        raise _Breakdown("rho")
+    alpha = ctx.c(ctx.div(rho, ctx.c(ctx.dotc(rs, v)), "sigma"))    # α = ρ/⟨r₀*, v⟩
+    au_even = v                                                 # A u₀ = v₀ (u₀ = p₀ = r₀)
+    u2 = au = None
+    bound2 = r0sq
+    for k in range(1, maxit + 1):
+        st["k"] = k
+        for half in (0, 1):
+            if half == 0:
+                u2 = u - alpha * v                              # u_{m+1} = u_m − α v_m
+                au, um = au_even, u                             # A u_m, kept from the last product (m even)
+            else:
+                au, um = op.apply(u2), u2                       # A u_m        (m odd)
+            w = w - alpha * au                                  # w_{m+1} = w_m − α A u_m
+            d = um + ctx.c(theta * theta * eta / alpha) * d     # d_{m+1} = u_m + (θ_m² η_m/α) d_m
+            theta = ctx.r(sqrt(ctx.norm_sq(w)) / tau)           # θ_{m+1} = ‖w_{m+1}‖/τ_m
+            cc = ctx.r(1 / sqrt(1 + theta * theta))             # c_{m+1} = 1/√(1+θ²)
+            tau = ctx.r(tau * theta * cc)                       # τ_{m+1} = τ_m θ c
+            eta = ctx.c(cc * cc * alpha)                        # η_{m+1} = c² α
+            ctx.check(theta, tau, eta)
+            st["x"] = x = x + eta * d                           # x_{m+1} = x_m + η d
+            bound2 = ctx.r(tau * tau * (2 * k + half))          # (τ_{m+1}·√(m+2))²
+            if _conv(bound2, tol2, r0sq):
+                hist.append(sqrt(bound2))
+                return CONVERGED, k, half == 0
+        hist.append(sqrt(bound2))
+        rho_new = ctx.c(ctx.dotc(rs, w))                        # ρ_{m+1} = ⟨r₀*, w_{m+1}⟩
+        ctx.check(rho_new)
+        if rho_new == 0:
+            raise _Breakdown("rho")
+        beta = ctx.c(rho_new / rho)                             # β = ρ_{m+1}/ρ_{m−1}
+        rho = rho_new
+        u = w + beta * u2                                       # u_{m+1} = w + β u_m
+        au_even = op.apply(u)                                   # A u_{m+1}
+        v = au_even + beta * (au + beta * v)                    # v = A u + β(A u_m + β v)
+        alpha = ctx.c(ctx.div(rho, ctx.c(ctx.dotc(rs, v)), "sigma"))
+    return MAXIT, maxit, False
+
+
 METHODS = {
     "bicgstab": _bicgstab, "cgne": _cgne, "qmr": _qmr, "bicor": _bicor,
     "cors": _cors,
     # SURVEY §8(f) NEXT-3
-    "bicg": _bicg, "cgs": _cgs, "cocr": _cocr, "cgnr": _cgnr,
+    "bicg": _bicg, "cgs": _cgs, "cocr": _cocr, "cgnr": _cgnr, "tfqmr": _tfqmr,
 }
 HOT_PATH = ("bicgstab", "cgne", "qmr", "bicor", "cors")
-NEXT3 = ("bicg", "cgs", "cocr", "cgnr")
+NEXT3 = ("bicg", "cgs", "cocr", "cgnr", "tfqmr")
 
 
 def solve(method, op, y, tol, maxit, x0=None, dots=None, **kw):

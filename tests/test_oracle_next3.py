@@ -156,7 +156,7 @@ def test_scale_invariance(method):
 
 def test_work_accounting():
     A, y = cfg1(n=64, seed=4)
-    for m, want in {"bicg": (5, 5), "cgs": (10, 0), "cocr": (5, 0), "cgnr": (5, 5)}.items():
+    for m, want in {"bicg": (5, 5), "cgs": (10, 0), "cocr": (5, 0), "cgnr": (5, 5), "tfqmr": (11, 0)}.items():
         res = solve(m, DenseOp(A), y, 0.0, 5)
         assert res.status == MAXIT and res.iterations == 5
         assert (res.matvecs_a, res.matvecs_ah) == want, m
@@ -165,8 +165,45 @@ def test_work_accounting():
 def test_breakdown_fixture():
     A = np.array([[0, 1], [-1, 0]], dtype=np.complex128)
     y = np.array([1, 0], dtype=np.complex128)
-    for m, name in (("bicg", "sigma"), ("cgs", "sigma"), ("cocr", "rho")):
+    for m, name in (("bicg", "sigma"), ("cgs", "sigma"), ("cocr", "rho"), ("tfqmr", "sigma")):
         r = solve(m, DenseOp(A), y, 1e-10, 10)
         assert r.status == BREAKDOWN and r.breakdown == name and r.iterations == 0, m
     r = solve("cgnr", DenseOp(A), y, 1e-10, 10)      # A unitary: CGNR converges at once
     assert r.status == CONVERGED and r.iterations == 1
+
+
+# ---------------- TFQMR (§2.1) ----------------
+def test_tfqmr_residual_bound_invariant():
+    """Freund's bound ‖r_m‖ ≤ τ_m·√(m+1) (the quantity the stopping test uses)
+    holds for the true residual after every pair and every half-step exit."""
+    n = 60
+    A = dense_random(n, seed=81, shift=1.5 + 0.5j)
+    y = dense_random(n, seed=82)[:, 0]
+    for k in range(1, 16):
+        res = solve("tfqmr", DenseOp(A), y, 0.0, k)
+        assert res.iterations == k
+        bound = float(res.history[-1])
+        true = np.linalg.norm(y - A @ res.x)
+        assert true <= bound * (1 + 1e-9), (k, true, bound)
+    # half-step exits too: a tolerance hit at the first half of a pair
+    for tol in (1e-2, 1e-4, 1e-6, 1e-8):
+        res = solve("tfqmr", DenseOp(A), y, tol, 200)
+        assert res.status == CONVERGED
+        assert np.linalg.norm(y - A @ res.x) <= float(res.history[-1]) * (1 + 1e-9)
+        assert res.true_rel_res <= tol
+
+
+@pytest.mark.parametrize("n", [4, 6])
+def test_tfqmr_mpmath_termination(n):
+    """100-digit arithmetic: the CGS polynomial it smooths terminates at
+    iteration n, so does TFQMR (quasi-residual ~1e-95), with A·x = y."""
+    mpmath = pytest.importorskip("mpmath")
+    A, y = _rand_int(n, seed=300 + n, kind="gen")
+    with mpmath.workdps(100):
+        Am = np.array([[mpmath.mpc(complex(v)) for v in row] for row in A], dtype=object)
+        ym = np.array([mpmath.mpc(complex(v)) for v in y], dtype=object)
+        res = solve("tfqmr", DenseOp(Am), ym, 1e-90, n + 2)
+        assert res.status == CONVERGED and res.iterations <= n
+        r = ym - Am.dot(res.x)
+        rel = mpmath.sqrt(sum(abs(v) ** 2 for v in r)) / mpmath.sqrt(sum(abs(v) ** 2 for v in ym))
+        assert rel < mpmath.mpf("1e-85")
