@@ -59,8 +59,9 @@ typedef enum { CCG_C64 = 0, CCG_C128 = 1 } ccg_dtype;
  * NEXT-3): BiCG ("bigcg"), CGS, CGNR ("cgmr", read as CGNR) of the PIM90 set
  * (P:57 [§2.1]) and COCR (P:87 [§3.4]; meant for complex-symmetric A = Aᵀ —
  * the library does not check symmetry).  Recurrences: DESIGN.md §2.
- * Operator needs: BiCGSTAB, CORS, CGS, COCR -> A·x only; CGNE, QMR, BiCOR,
- * BiCG, CGNR -> A·x and Aᴴ·x. */
+ * TFQMR (P:57 [§2.1], "QMR and TFQMR ... changed") is the transpose-free QMR
+ * smoothing of CGS.  Operator needs: BiCGSTAB, CORS, CGS, COCR, TFQMR -> A·x
+ * only; CGNE, QMR, BiCOR, BiCG, CGNR -> A·x and Aᴴ·x. */
 typedef enum {
   CCG_BICGSTAB = 0,
   CCG_CGNE = 1,
@@ -70,7 +71,8 @@ typedef enum {
   CCG_BICG = 5,
   CCG_CGS = 6,
   CCG_COCR = 7,
-  CCG_CGNR = 8
+  CCG_CGNR = 8,
+  CCG_TFQMR = 9   /* P:57 [§2.1]; stops on Freund's bound τ_m·√(m+1) ≤ tol·‖r₀‖ (R9) */
 } ccg_method;
 
 /* The three products of the operator module: A·x (matvec),

@@ -572,6 +572,8 @@ def _tfqmr(op, y, x, r, r0sq, tol2, maxit, ctx, hist, st, shadow=None):
                 hist.append(sqrt(bound2))
                 return CONVERGED, k, half == 0
         hist.append(sqrt(bound2))
+        if k == maxit:              # no further iterate needs the next products (R2)
+            break
         rho_new = ctx.c(ctx.dotc(rs, w))                        # ρ_{m+1} = ⟨r₀*, w_{m+1}⟩
         ctx.check(rho_new)
         if rho_new == 0:

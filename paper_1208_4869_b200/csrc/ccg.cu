@@ -665,6 +665,7 @@ struct Engine {
       case M_CGNE: case M_CGNR: cm.ir.d0 = L(c, 2); break;
       case M_QMR: cm.ir.d0 = L(c, 2); cm.ir.d1 = L(c, 3); cm.ir.d2 = L(c, 4); break;
       case M_BICOR: case M_CORS: cm.ir.d0 = Fs(c, 0); cm.ir.d1 = L(c, 2); break;
+      case M_TFQMR: cm.ir.d0 = L(c, 2); cm.ir.d1 = L(c, 3); cm.ir.d2 = Fs(c, 0); break;
       default: cm.ir.d0 = Fs(c, 0); break;   // COCR
     }
     cudaLaunchConfig_t cfg = {};
@@ -746,6 +747,12 @@ struct Engine {
         return launch_cluster(c, ClCocr<T>{CrP<T>{Fs(c, 0), L(c, 2), L(c, 3), L(c, 4)},
                                            CrX<T>{L(c, X), Fs(c, 0), L(c, 3), L(c, 4)}, CrAr<T>{L(c, 2), Fs(c, 0)},
                                            CrAr0<T>{L(c, 2), Fs(c, 0)}, F(c, 0)});
+      case M_TFQMR:
+        return launch_cluster(c, ClTfqmr<T>{TfE<T>{Fs(c, 0), L(c, 4), L(c, 6), Fs(c, 1), L(c, 3), L(c, 5)},
+                                            TfO<T>{L(c, 7), L(c, X), L(c, 3), L(c, 5), Fs(c, 1), L(c, 2)},
+                                            TfU<T>{L(c, X), L(c, 5), L(c, 3), Fs(c, 1), Fs(c, 0)},
+                                            TfV<T>{L(c, 6), L(c, 7), L(c, 4), L(c, 2)},
+                                            TfV0<T>{L(c, 4), L(c, 6), L(c, 2)}, F(c, 0), F(c, 1)});
       default:
         return launch_cluster(c, ClCgnr<T>{CnW<T>{L(c, 3)}, CnX<T>{L(c, X), L(c, 2), Fs(c, 0), L(c, 3)},
                                            CnZ<T>{L(c, 4)}, CnP<T>{L(c, 4), Fs(c, 0)}, CnZ0<T>{Fs(c, 0)}, F(c, 0),
@@ -813,6 +820,23 @@ struct Engine {
     return pass(c, CnP<T>{L(c, 4), Fs(c, 0)}, g);
   }
 
+  // ---- TFQMR: loc: 0 x, 1 y, 2 r0*, 3 w, 4 v, 5 d, 6 A·u (even), 7 A·u2 ; full: 0 u, 1 u2
+  static int tfqmr_setup(ccg_ctx* c, bool x0) {
+    TRY(init_residual(c, x0, L(c, 2), L(c, 3), Fs(c, 0), nullptr));
+    TRY(allgather(c, 0));
+    return matvec_a(c, F(c, 0), TfV0<T>{L(c, 4), L(c, 6), L(c, 2)}, &c->st->done);
+  }
+  static int tfqmr_iter(ccg_ctx* c) {
+    const int* g = &c->st->done;
+    const int* g2 = &c->st->gate2;
+    TRY(pass(c, TfE<T>{Fs(c, 0), L(c, 4), L(c, 6), Fs(c, 1), L(c, 3), L(c, 5)}, g));
+    TRY(allgather(c, 1));
+    TRY(matvec_a(c, F(c, 1), TfO<T>{L(c, 7), L(c, X), L(c, 3), L(c, 5), Fs(c, 1), L(c, 2)}, g2));
+    TRY(pass(c, TfU<T>{L(c, X), L(c, 5), L(c, 3), Fs(c, 1), Fs(c, 0)}, g));
+    TRY(allgather(c, 0));
+    return matvec_a(c, F(c, 0), TfV<T>{L(c, 6), L(c, 7), L(c, 4), L(c, 2)}, g);
+  }
+
   static int setup(ccg_ctx* c, int m, bool x0) {
     switch (m) {
       case M_BICGSTAB: return bicgstab_setup(c, x0);
@@ -823,6 +847,7 @@ struct Engine {
       case M_BICG: return bicg_setup(c, x0);
       case M_CGS: return cgs_setup(c, x0);
       case M_COCR: return cocr_setup(c, x0);
+      case M_TFQMR: return tfqmr_setup(c, x0);
       default: return cgnr_setup(c, x0);
     }
   }
@@ -836,6 +861,7 @@ struct Engine {
       case M_BICG: return bicg_iter(c);
       case M_CGS: return cgs_iter(c);
       case M_COCR: return cocr_iter(c);
+      case M_TFQMR: return tfqmr_iter(c);
       default: return cgnr_iter(c);
     }
   }

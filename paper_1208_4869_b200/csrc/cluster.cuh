@@ -298,6 +298,19 @@ struct ClCommon {
   int has_x0;
 };
 
+template <typename T>
+struct ClTfqmr {
+  TfE<T> e; TfO<T> o; TfU<T> u; TfV<T> v; TfV0<T> v0;
+  const typename CT<T>::c *uf, *u2f;
+  __device__ void setup(ClusterCtx<T>& cx) { cx.gemv(v0, uf); }
+  __device__ void iter(ClusterCtx<T>& cx) {
+    CL_PH(cx.pass(e));
+    if (!cx.st->gate2) cx.gemv(o, u2f);
+    CL_PH(cx.pass(u));
+    CL_PH(cx.gemv(v, uf));
+  }
+};
+
 template <typename T, class M>
 __global__ void __launch_bounds__(CL_NT, 1)
 cluster_solve(M m, ClCommon<T> cm, State* gst, const typename CT<T>::c* __restrict__ A, int64_t lda, int64_t n) {

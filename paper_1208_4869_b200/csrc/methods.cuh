@@ -64,6 +64,10 @@ struct InitR {
       case M_BICGSTAB:
       case M_BICG:
       case M_CGS: st->rho = make_double2(rr, 0.0); break;
+      case M_TFQMR:
+        st->rho = make_double2(rr, 0.0);
+        st->tau = sqrt(rr); st->theta = 0.0; st->eta = make_double2(0.0, 0.0);
+        break;
       case M_CGNE: st->rho_r = rr; break;
       case M_QMR:
         st->rnrm = sqrt(rr); st->xnrm = sqrt(rr);
@@ -854,6 +858,140 @@ struct CnP {  // p = z + βp
     p[i] = v;
   }
   static __device__ void finish(State*, const double2*) {}
+};
+
+// ---- TFQMR (§2.1; Saad Alg. 7.8 in pairs of half-steps, readings R9-R11).
+// Setup: [A u₀ → v = A u₀, σ → α].  Pair k: E (pass, first half-step) →
+// [A u₂ → O: second half-step, ρ', β] (skipped after an E exit) → U (pass:
+// pending x update; u = w + βu₂) → [A u → v = Au + β(Au₂ + βv), σ → α]
+__device__ __forceinline__ bool tf_step(State* st, double ww, int bound_mult) {
+  // θ, c, τ, η from ‖w_{m+1}‖²; returns true on convergence (τ²·(m+2) ≤ tol²‖r₀‖²)
+  const double theta = sqrt(ww) / st->tau;
+  const double c = 1.0 / sqrt(1.0 + theta * theta);
+  const double tau = st->tau * theta * c;
+  const double2 eta = zscal(st->alpha, c * c);
+  const int k = st->iter + 1;
+  if (!isfinite(theta) || !isfinite(tau) || !zfinite(eta)) { set_done(st, ST_NONFINITE, k - 1); return false; }
+  st->theta = theta; st->tau = tau; st->eta = eta;
+  const double bound2 = tau * tau * (double)bound_mult;
+  if (bound2 <= st->tol2r0) { push_hist(st, k, bound2); return true; }
+  st->ss = bound2;
+  return false;
+}
+
+template <typename T>
+struct TfV0 {  // setup: v = A u₀ (= A u_even) ; σ = ⟨r₀*, v⟩ ; α = ρ/σ
+  static constexpr int K = 1;
+  using C = Cx<T>;
+  C* v; C* aue; const C* rs;
+  __device__ void load(const State*) {}
+  __device__ void operator()(int64_t i, C val, double2* acc) { v[i] = val; aue[i] = val; dotc_acc(acc[0], rs[i], val); }
+  static __device__ void finish(State* st, const double2* s) { st->matvecs_a++; sigma_step(st, s[0]); }
+};
+
+template <typename T>
+struct TfE {  // u₂ = u − αv ; w −= α·A u ; d = u + (θ²η/α)d ; ‖w‖² → θ, c, τ, η
+  static constexpr int K = 1;
+  using C = Cx<T>;
+  const C* u; const C* v; const C* aue; C* u2; C* w; C* d;
+  C alpha, coef; int first;
+  __device__ void load(const State* st) {
+    first = st->iter == 0;
+    alpha = fromd2<C>(st->alpha);
+    coef = fromd2<C>(zdiv(zscal(st->eta, st->theta * st->theta), st->alpha));
+  }
+  __device__ void operator()(int64_t i, double2* acc) {
+    const C ui = u[i];
+    u2[i] = caxmy(ui, alpha, v[i]);
+    const C wi = caxmy(w[i], alpha, aue[i]);
+    w[i] = wi;
+    d[i] = first ? ui : caxpy(ui, coef, d[i]);
+    nrm_acc(acc[0], wi);
+  }
+  static __device__ void finish(State* st, const double2* s) {
+    if (tf_step(st, s[0].x, 2 * (st->iter + 1))) { st->half = 1; st->gate2 = 1; }
+  }
+};
+
+template <typename T>
+struct TfO {  // A u₂ ; x += η d (E's update) ; w −= α A u₂ ; d = u₂ + (θ²η/α)d ; ‖w‖², ⟨r₀*, w⟩
+  static constexpr int K = 2;
+  using C = Cx<T>;
+  C* au; C* x; C* w; C* d; const C* u2; const C* rs;
+  C alpha, eta, coef;
+  __device__ void load(const State* st) {
+    alpha = fromd2<C>(st->alpha);
+    eta = fromd2<C>(st->eta);
+    coef = fromd2<C>(zdiv(zscal(st->eta, st->theta * st->theta), st->alpha));
+  }
+  __device__ void operator()(int64_t i, C val, double2* acc) {
+    au[i] = val;
+    const C di = d[i];
+    x[i] = caxpy(x[i], eta, di);
+    const C wi = caxmy(w[i], alpha, val);
+    w[i] = wi;
+    d[i] = caxpy(u2[i], coef, di);
+    nrm_acc(acc[0], wi);
+    dotc_acc(acc[1], rs[i], wi);
+  }
+  static __device__ void finish(State* st, const double2* s) {
+    const int k = st->iter + 1;
+    st->matvecs_a++;
+    if (tf_step(st, s[0].x, 2 * k + 1)) { st->fin = 1; return; }
+    if (st->done) return;
+    if (k >= st->maxit) return;                       // R2: no products for an iterate nobody uses
+    const double2 rho_new = s[1];
+    if (!zfinite(rho_new)) { set_done(st, ST_NONFINITE, k - 1); return; }
+    if (zzero(rho_new)) { set_done(st, ST_BREAKDOWN, k - 1, BD_RHO); return; }
+    st->beta = zdiv(rho_new, st->rho);
+    st->rho = rho_new;
+  }
+};
+
+template <typename T>
+struct TfU {  // x += η d (the pending update) ; u = w + β u₂ ; end of pair k
+  static constexpr int K = 1;
+  using C = Cx<T>;
+  C* x; const C* d; const C* w; const C* u2; C* u;
+  C eta, beta; int stop;
+  __device__ void load(const State* st) {
+    eta = fromd2<C>(st->eta); beta = fromd2<C>(st->beta);
+    stop = st->half || st->fin || st->iter + 1 >= st->maxit;
+  }
+  __device__ void operator()(int64_t i, double2*) {
+    x[i] = caxpy(x[i], eta, d[i]);
+    if (!stop) u[i] = caxpy(w[i], beta, u2[i]);
+  }
+  static __device__ void finish(State* st, const double2*) {
+    const int k = st->iter + 1;
+    if (st->half || st->fin) { set_done(st, ST_CONVERGED, k); return; }
+    push_hist(st, k, st->ss);
+    st->iter = k;
+    if (k >= st->maxit) set_done(st, ST_MAXIT, k);
+  }
+};
+
+template <typename T>
+struct TfV {  // A u (kept) ; v = A u + β(A u₂ + βv) ; σ = ⟨r₀*, v⟩ ; α = ρ/σ
+  static constexpr int K = 1;
+  using C = Cx<T>;
+  C* aue; const C* au; C* v; const C* rs;
+  C beta;
+  __device__ void load(const State* st) { beta = fromd2<C>(st->beta); }
+  __device__ void operator()(int64_t i, C val, double2* acc) {
+    aue[i] = val;
+    const C vi = caxpy(val, beta, caxpy(au[i], beta, v[i]));
+    v[i] = vi;
+    dotc_acc(acc[0], rs[i], vi);
+  }
+  static __device__ void finish(State* st, const double2* s) {
+    st->matvecs_a++;
+    const double2 sigma = s[0];
+    const int kc = st->iter - 1;            // the oracle raises inside pair `iter`
+    if (zzero(sigma)) { set_done(st, ST_BREAKDOWN, kc, BD_SIGMA); return; }
+    st->alpha = zdiv(st->rho, sigma);
+    if (!zfinite(st->alpha)) { set_done(st, ST_NONFINITE, kc); return; }
+  }
 };
 
 }  // namespace ccg

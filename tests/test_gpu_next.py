@@ -125,7 +125,7 @@ def test_next3_cfg2(method):
                 literal=method in ("bicg", "cocr"))
 
 
-@pytest.mark.parametrize("method", ["bicg", "cgs", "cgnr"])
+@pytest.mark.parametrize("method", ["bicg", "cgs", "cgnr", "tfqmr"])
 def test_next3_cfg3_proxy_c64(method):
     n = 4096
     A = gauss_shifted_rows(n, 0, n, seed=1)
@@ -177,7 +177,7 @@ def test_next3_breakdown_fixture():
     A = np.array([[0, 1], [-1, 0]], dtype=np.complex128)
     y = np.array([1, 0], dtype=np.complex128)
     with Dense(A) as h:
-        for m, name in (("bicg", "sigma"), ("cgs", "sigma"), ("cocr", "rho")):
+        for m, name in (("bicg", "sigma"), ("cgs", "sigma"), ("cocr", "rho"), ("tfqmr", "sigma")):
             g = h.solve(m, y, 1e-10, 10)
             o = oracle.solve(m, DenseOp(A), y, 1e-10, 10)
             assert g["status"] == "BREAKDOWN" and g["breakdown"] == name == o.breakdown, m
@@ -186,7 +186,7 @@ def test_next3_breakdown_fixture():
         assert g["status"] == "CONVERGED" and g["iterations"] == 1
 
 
-@pytest.mark.parametrize("method", ["cgs", "cocr"])
+@pytest.mark.parametrize("method", ["cgs", "cocr", "tfqmr"])
 def test_next3_csr_transpose_free(method):
     """CGS and COCR need only A·x: they run on a CSR operator without the
     symmetric flag (COCR on the complex-symmetric shifted Helmholtz matrix)."""
