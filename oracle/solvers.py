@@ -587,14 +587,87 @@ def _tfqmr(op, y, x, r, r0sq, tol2, maxit, ctx, hist, st, shadow=None):
     return MAXIT, maxit, False
 
 
+def _gmres(op, y, x, r, r0sq, tol2, maxit, ctx, hist, st, restart=30):
+    """Restarted GMRES(m) ("rgmres", §2.1): Arnoldi
+    with classical Gram–Schmidt applied twice (CGS2, R13), complex
+    Givens rotations, back substitution at the end of a cycle; the stopping
+    test is the Givens residual |g_{j+1}| ≤ tol·‖r₀‖ (the recurrence residual,
+    R15); a restart recomputes r = y − A·x explicitly (one product, R14);
+    ``iterations`` counts Arnoldi steps (one A·x each)."""
+    m = int(restart)
+    k = 0
+    rr = r0sq
+    while True:
+        beta = ctx.r(sqrt(rr))
+        V = [r / beta]                                          # v₁ = r/β
+        R = []                                                  # rotated columns of H
+        cs, sn = [], []
+        g = [ctx.c(beta)]                                       # g = β e₁
+        for j in range(m):
+            k += 1
+            st["k"] = k
+            w = op.apply(V[j])                                  # w = A v_j
+            h = [ctx.c(ctx.dotc(V[i], w)) for i in range(j + 1)]      # h = Vᴴw
+            for i in range(j + 1):
+                w = w - h[i] * V[i]                             # w −= V h
+            h2 = [ctx.c(ctx.dotc(V[i], w)) for i in range(j + 1)]     # second pass (CGS2)
+            for i in range(j + 1):
+                w = w - h2[i] * V[i]
+            h = [ctx.c(a + b) for a, b in zip(h, h2)]
+            hn = ctx.r(sqrt(ctx.norm_sq(w)))                    # h_{j+1,j} = ‖w‖
+            ctx.check(hn, *h)
+            for i in range(j):                                  # previous rotations
+                a, b = h[i], h[i + 1]
+                h[i] = ctx.c(cs[i] * a + sn[i] * b)
+                h[i + 1] = ctx.c(-sn[i].conjugate() * a + cs[i] * b)
+            a = h[j]                                            # new rotation zeroing h_{j+1,j}
+            if a == 0:
+                c, s_ = ctx.r(0), ctx.c(1)
+            else:
+                aa = abs(a)
+                nu = ctx.r(sqrt(aa * aa + hn * hn))
+                c, s_ = ctx.r(aa / nu), ctx.c((a / aa) * (hn / nu))
+            cs.append(c)
+            sn.append(s_)
+            h[j] = ctx.c(c * a + s_ * hn)
+            g.append(ctx.c(-s_.conjugate() * g[j]))             # g_{j+1} = −conj(s) g_j
+            g[j] = ctx.c(c * g[j])                              # g_j = c g_j
+            R.append(h)
+            res = abs(g[j + 1])
+            hist.append(res)
+            conv = _conv(res * res, tol2, r0sq)
+            if conv or k == maxit or j == m - 1:
+                yv = [None] * (j + 1)                           # back substitution R y = g
+                for i in range(j, -1, -1):
+                    t = g[i]
+                    for l in range(i + 1, j + 1):
+                        t = t - R[l][i] * yv[l]
+                    yv[i] = ctx.c(ctx.div(t, R[i][i], "gamma"))
+                for i in range(j + 1):
+                    x = x + yv[i] * V[i]                        # x += V y
+                st["x"] = x
+                if conv:
+                    return CONVERGED, k, False
+                if k == maxit:
+                    return MAXIT, k, False
+                break
+            V.append(w / hn)                                    # v_{j+1} = w/h_{j+1,j}
+        r = y - op.apply(x)                                     # restart: explicit residual
+        rr = ctx.r(ctx.norm_sq(r))
+        ctx.check(rr)
+        if _conv(rr, tol2, r0sq):
+            return CONVERGED, k, False
+
+
 METHODS = {
     "bicgstab": _bicgstab, "cgne": _cgne, "qmr": _qmr, "bicor": _bicor,
     "cors": _cors,
     # SURVEY §8(f) NEXT-3
     "bicg": _bicg, "cgs": _cgs, "cocr": _cocr, "cgnr": _cgnr, "tfqmr": _tfqmr,
+    "gmres": _gmres,
 }
 HOT_PATH = ("bicgstab", "cgne", "qmr", "bicor", "cors")
-NEXT3 = ("bicg", "cgs", "cocr", "cgnr", "tfqmr")
+NEXT3 = ("bicg", "cgs", "cocr", "cgnr", "tfqmr", "gmres")
 
 
 def solve(method, op, y, tol, maxit, x0=None, dots=None, **kw):

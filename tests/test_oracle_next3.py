@@ -156,7 +156,8 @@ def test_scale_invariance(method):
 
 def test_work_accounting():
     A, y = cfg1(n=64, seed=4)
-    for m, want in {"bicg": (5, 5), "cgs": (10, 0), "cocr": (5, 0), "cgnr": (5, 5), "tfqmr": (10, 0)}.items():
+    for m, want in {"bicg": (5, 5), "cgs": (10, 0), "cocr": (5, 0), "cgnr": (5, 5), "tfqmr": (10, 0),
+                          "gmres": (5, 0)}.items():
         res = solve(m, DenseOp(A), y, 0.0, 5)
         assert res.status == MAXIT and res.iterations == 5
         assert (res.matvecs_a, res.matvecs_ah) == want, m
@@ -207,3 +208,72 @@ def test_tfqmr_mpmath_termination(n):
         r = ym - Am.dot(res.x)
         rel = mpmath.sqrt(sum(abs(v) ** 2 for v in r)) / mpmath.sqrt(sum(abs(v) ** 2 for v in ym))
         assert rel < mpmath.mpf("1e-85")
+
+
+# ---------------- GMRES(m) (§2.1 "rgmres") ----------------
+def _ls_krylov(A, r0, k):
+    Q = _krylov(A, r0, k)
+    c, *_ = np.linalg.lstsq(A @ Q, r0, rcond=None)
+    return Q @ c
+
+
+def test_gmres_is_krylov_least_squares_and_history_is_true_residual():
+    """x_k = x₀ + argmin over K_k(A, r₀) of ‖y − A x‖ (dense least squares on a
+    QR'd Krylov basis), and the Givens residual recorded in the history equals
+    the true residual of x_k."""
+    n = 50
+    A = dense_random(n, seed=91, shift=1.0 + 1.0j)
+    y = dense_random(n, seed=92)[:, 0]
+    prev = np.inf
+    for k in range(1, 12):
+        res = solve("gmres", DenseOp(A), y, 0.0, k)
+        assert res.iterations == k
+        xm = _ls_krylov(A, y, k)
+        assert np.linalg.norm(res.x - xm) <= 1e-9 * np.linalg.norm(xm), k
+        true = np.linalg.norm(y - A @ res.x)
+        assert abs(float(res.history[-1]) - true) <= 1e-10 * np.linalg.norm(y), k
+        assert true <= prev * (1 + 1e-12)
+        prev = true
+
+
+def test_gmres_restart_restarts_from_the_current_iterate():
+    """GMRES(4): after a restart at x₄ the next iterates are x₄ + argmin over
+    K_j(A, y − A x₄); the restart costs one extra product."""
+    n = 40
+    A = dense_random(n, seed=93, shift=2.0 - 0.5j)
+    y = dense_random(n, seed=94)[:, 0]
+    x4 = solve("gmres", DenseOp(A), y, 0.0, 4, restart=4).x
+    r4 = y - A @ x4
+    for j in range(1, 4):
+        res = solve("gmres", DenseOp(A), y, 0.0, 4 + j, restart=4)
+        assert res.iterations == 4 + j and res.matvecs_a == 4 + j + 1
+        xm = x4 + _ls_krylov(A, r4, j)
+        assert np.linalg.norm(res.x - xm) <= 1e-9 * np.linalg.norm(xm), j
+
+
+@pytest.mark.parametrize("n", [4, 6])
+def test_gmres_mpmath_termination(n):
+    mpmath = pytest.importorskip("mpmath")
+    A, y = _rand_int(n, seed=400 + n, kind="gen")
+    with mpmath.workdps(100):
+        Am = np.array([[mpmath.mpc(complex(v)) for v in row] for row in A], dtype=object)
+        ym = np.array([mpmath.mpc(complex(v)) for v in y], dtype=object)
+        res = solve("gmres", DenseOp(Am), ym, 1e-90, n + 2)
+        assert res.status == CONVERGED and res.iterations == n
+        r = ym - Am.dot(res.x)
+        rel = mpmath.sqrt(sum(abs(v) ** 2 for v in r)) / mpmath.sqrt(sum(abs(v) ** 2 for v in ym))
+        assert rel < mpmath.mpf("1e-85")
+
+
+def test_gmres_cgs2_keeps_the_givens_residual_true():
+    """Ill-conditioned A (eigenvalues over 8 decades): with the second
+    Gram–Schmidt pass (R13) the Givens residual stays the true residual to
+    ~2e-13 over 60 steps; one pass drifts to ~1.4e-12 (loss of orthogonality)."""
+    n = 120
+    rng = np.random.default_rng(5)
+    Q, _ = np.linalg.qr(rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n)))
+    A = (Q * (np.logspace(0, 8, n) * np.exp(1j * rng.uniform(0, 0.3, n)))) @ Q.conj().T
+    y = rng.standard_normal(n) + 1j * rng.standard_normal(n)
+    res = solve("gmres", DenseOp(A), y, 0.0, 60, restart=60)
+    gap = abs(float(res.history[-1]) - np.linalg.norm(y - A @ res.x)) / np.linalg.norm(y)
+    assert gap <= 6e-13
