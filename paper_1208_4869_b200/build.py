@@ -9,7 +9,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libccg.so")
 SOURCES = ["ccg.cu"]
-DEPS = ["ccg.cu", "common.cuh", "matvec.cuh", "methods.cuh", "bulk.cuh", "comm.cuh", "fft.cuh", "cluster.cuh"]
+DEPS = ["ccg.cu", "common.cuh", "matvec.cuh", "methods.cuh", "bulk.cuh", "comm.cuh", "fft.cuh", "cluster.cuh", "gmres.cuh"]
 
 
 def nccl_include():

@@ -25,6 +25,7 @@
 #include "comm.cuh"
 #include "fft.cuh"
 #include "cluster.cuh"
+#include "gmres.cuh"
 
 #include <complex>
 
@@ -79,6 +80,16 @@ struct ccg_ctx {
   void* cb_user = nullptr;
   uint32_t cb_caps = 0;
   void* cb_out = nullptr;   // nloc output rows of the user's product
+  // GMRES(m) workspace (gmres.cuh)
+  int gm_m = 30;
+  GmDev* gm_dev = nullptr;
+  void* gm_V = nullptr;     // (m+1) × nloc basis
+  size_t gm_V_bytes = 0;
+  double2* gm_part = nullptr;
+  unsigned* gm_ticket = nullptr;
+  double2* gm_rank = nullptr;
+  double2* gm_all = nullptr;
+  int gm_grid = 1;
   // whole-loop cluster kernel for small dense systems (cluster.cuh)
   bool cluster_ok = false;
   int cluster_size = 0;   // 0 = not yet chosen
@@ -837,6 +848,56 @@ struct Engine {
     return matvec_a(c, F(c, 0), TfV<T>{L(c, 6), L(c, 7), L(c, 4), L(c, 2)}, g);
   }
 
+  // ---- GMRES(m): loc: 0 x, 1 y, 2 w ; basis V (gm_V) ; full: 0 v_j, 2 x (restart)
+  static C* Vb(ccg_ctx* c) { return reinterpret_cast<C*>(c->gm_V); }
+  template <int MODE>
+  static int gm_pass_launch(ccg_ctx* c, C* w, const double2* coef, double2* dst, const int* gate) {
+    const bool fuse = c->world == 1;
+    gm_pass<T, MODE><<<c->gm_grid, GM_NT, 0, c->stream>>>(Vb(c), c->nloc, w, coef, fuse ? dst : c->gm_rank, c->nloc,
+                                                           c->gm_dev, c->gm_part, c->gm_ticket, fuse ? 1 : 0, gate);
+    c->launches++;
+    CK(c, cudaGetLastError());
+    if (!fuse) {
+      NK(c, c->comm->allgather(c->gm_rank, c->gm_all, (size_t)(GM_MAX + 1) * 2, CT_F64, c->stream));
+      gm_ranksum<<<1, 128, 0, c->stream>>>(c->gm_all, c->world, MODE == 2 ? 1 : GM_MAX + 1, GM_MAX + 1, dst, gate);
+      c->launches++;
+    }
+    return CCG_OK;
+  }
+  static int gmres_setup(ccg_ctx* c, bool x0) {
+    TRY(init_residual(c, x0, Vb(c), nullptr, nullptr, nullptr));
+    gm_normalize<T><<<c->pass_grid, NT, 0, c->stream>>>(Vb(c), c->nloc, Vb(c), Fs(c, 0), c->nloc, c->gm_dev, 1,
+                                                         &c->st->done);
+    c->launches++;
+    CK(c, cudaGetLastError());
+    return CCG_OK;
+  }
+  static int gmres_iter(ccg_ctx* c) {
+    const int* g = &c->st->done;
+    GmDev* gm = c->gm_dev;
+    C* w = L(c, 2);
+    TRY(allgather(c, 0));
+    TRY(matvec_a(c, F(c, 0), Store<T>{w}, g));
+    TRY(gm_pass_launch<0>(c, w, nullptr, gm->hcol, g));
+    TRY(gm_pass_launch<1>(c, w, gm->hcol, gm->h2, g));
+    TRY(gm_pass_launch<2>(c, w, gm->h2, &gm->ww2, g));
+    gm_step<<<1, 1, 0, c->stream>>>(c->st, gm, g);
+    gm_normalize<T><<<c->pass_grid, NT, 0, c->stream>>>(Vb(c), c->nloc, w, Fs(c, 0), c->nloc, gm, 0, &gm->endflag);
+    gm_trisolve<<<1, 1, 0, c->stream>>>(c->st, gm, &gm->noend);
+    gm_xupdate<T><<<c->pass_grid, NT, 0, c->stream>>>(L(c, X), Vb(c), c->nloc, c->nloc, gm, &gm->noxupd);
+    c->launches += 4;
+    CK(c, cudaGetLastError());
+    TRY(pass(c, Copy<T>{L(c, X), Fs(c, 2)}, &gm->norestart));
+    TRY(allgather(c, 2));
+    TRY(matvec_a(c, F(c, 2), GmR<T>{L(c, 1), Vb(c)}, &gm->norestart));
+    gm_normalize<T><<<c->pass_grid, NT, 0, c->stream>>>(Vb(c), c->nloc, Vb(c), Fs(c, 0), c->nloc, gm, 1,
+                                                         &gm->norestart);
+    gm_reset<<<1, 1, 0, c->stream>>>(gm);
+    c->launches += 2;
+    CK(c, cudaGetLastError());
+    return CCG_OK;
+  }
+
   static int setup(ccg_ctx* c, int m, bool x0) {
     switch (m) {
       case M_BICGSTAB: return bicgstab_setup(c, x0);
@@ -848,6 +909,7 @@ struct Engine {
       case M_CGS: return cgs_setup(c, x0);
       case M_COCR: return cocr_setup(c, x0);
       case M_TFQMR: return tfqmr_setup(c, x0);
+      case M_GMRES: return gmres_setup(c, x0);
       default: return cgnr_setup(c, x0);
     }
   }
@@ -862,6 +924,7 @@ struct Engine {
       case M_CGS: return cgs_iter(c);
       case M_COCR: return cocr_iter(c);
       case M_TFQMR: return tfqmr_iter(c);
+      case M_GMRES: return gmres_iter(c);
       default: return cgnr_iter(c);
     }
   }
@@ -1554,6 +1617,39 @@ int ccg_set_matvec_callback(ccg_handle c, ccg_matvec_fn fn, void* user, uint32_t
   return c->dtype == CCG_C64 ? choose_launch<float>(c) : choose_launch<double>(c);
 }
 
+int ccg_set_gmres_restart(ccg_handle c, int32_t m) {
+  if (!c) return CCG_E_ARG;
+  if (m < 1 || m > GM_MAX) FAIL(c, CCG_E_ARG, "GMRES restart length must be in [1, 64]");
+  if (m != c->gm_m) invalidate_graphs(c);
+  c->gm_m = m;
+  return CCG_OK;
+}
+
+// GMRES workspace: basis (m+1) × nloc, Hessenberg data, per-CTA multi-dot slots
+static int gmres_workspace(ccg_ctx* c) {
+  const size_t need = (size_t)(c->gm_m + 1) * (size_t)c->nloc * c->esz;
+  if (need > c->gm_V_bytes) {
+    if (c->gm_V) cudaFree(c->gm_V);
+    c->gm_V = nullptr;
+    c->gm_V_bytes = 0;
+    CK(c, cudaMalloc(&c->gm_V, need));
+    c->gm_V_bytes = need;
+    invalidate_graphs(c);
+  }
+  if (!c->gm_dev) {
+    CK(c, cudaMalloc(&c->gm_dev, sizeof(GmDev)));
+    CK(c, cudaMemset(c->gm_dev, 0, sizeof(GmDev)));
+    c->gm_grid = (int)std::max<int64_t>(1, std::min<int64_t>((c->nloc + GM_NT - 1) / GM_NT, (int64_t)c->sm_count * 4));
+    CK(c, cudaMalloc(&c->gm_part, (size_t)c->gm_grid * (GM_MAX + 1) * sizeof(double2)));
+    CK(c, cudaMalloc(&c->gm_ticket, sizeof(unsigned)));
+    CK(c, cudaMemset(c->gm_ticket, 0, sizeof(unsigned)));
+    CK(c, cudaMalloc(&c->gm_rank, (size_t)(GM_MAX + 1) * sizeof(double2)));
+    CK(c, cudaMalloc(&c->gm_all, (size_t)c->world * (GM_MAX + 1) * sizeof(double2)));
+  }
+  CK(c, cudaMemcpyAsync(&c->gm_dev->m, &c->gm_m, sizeof(int), cudaMemcpyHostToDevice, c->stream));
+  return CCG_OK;
+}
+
 static int stage_in(ccg_ctx* c, void* dst, const void* src, size_t bytes) {
   if (is_device_ptr(src)) {
     CK(c, cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, c->stream));
@@ -1634,6 +1730,10 @@ int ccg_solve(ccg_handle c, ccg_method method, const void* x0_local, const void*
   s0.tol2 = tol * tol;
   s0.hist = c->hist;
   s0.hist_cap = c->hist_cap;
+  if (method == CCG_GMRES) {
+    TRY(gmres_workspace(c));
+    s0.gm = c->gm_dev;
+  }
   *c->st_host = s0;
   CK(c, cudaMemcpyAsync(c->st, c->st_host, sizeof(State), cudaMemcpyHostToDevice, c->stream));
   // inputs: x -> loc[0], y -> loc[1]
@@ -1645,7 +1745,7 @@ int ccg_solve(ccg_handle c, ccg_method method, const void* x0_local, const void*
   }
   const bool has_x0 = x0_local != nullptr;
   int rc;
-  if (c->opk == OPK_DENSE && c->cluster_ok && c->world == 1 && !c->timing) {
+  if (c->opk == OPK_DENSE && c->cluster_ok && c->world == 1 && !c->timing && method != CCG_GMRES) {
     // small dense system: setup, every iteration and the true residual in ONE
     // cluster launch (cluster.cuh); maxit and the stopping rule live in the State
     c->cl_method = method;
@@ -1735,6 +1835,12 @@ int ccg_destroy(ccg_handle c) {
   free_csr_copies(c);
   if (c->part) cudaFree(c->part);
   if (c->hist) cudaFree(c->hist);
+  if (c->gm_V) cudaFree(c->gm_V);
+  if (c->gm_dev) cudaFree(c->gm_dev);
+  if (c->gm_part) cudaFree(c->gm_part);
+  if (c->gm_ticket) cudaFree(c->gm_ticket);
+  if (c->gm_rank) cudaFree(c->gm_rank);
+  if (c->gm_all) cudaFree(c->gm_all);
   if (c->st) cudaFree(c->st);
   if (c->st_host) cudaFreeHost(c->st_host);
   if (c->ticket) cudaFree(c->ticket);

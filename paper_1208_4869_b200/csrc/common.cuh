@@ -100,6 +100,32 @@ __device__ __forceinline__ bool zfinite(double2 a) { return isfinite(a.x) && isf
 __device__ __forceinline__ bool zzero(double2 a) { return a.x == 0.0 && a.y == 0.0; }
 
 // ---------------------------------------------------------------------------
+// GMRES(m) device workspace (gmres.cuh): Hessenberg/Givens data and the
+// per-step flags that gate the cycle-end and restart kernels of the graph
+// ---------------------------------------------------------------------------
+constexpr int GM_MAX = 64;     // longest restart cycle
+constexpr int GM_NT = 256;     // threads per CTA = rows per tile
+
+struct GmDev {
+  double2 hcol[GM_MAX + 1];               // pass-1 dots, then the rotated column
+  double2 h2[GM_MAX + 1];                 // pass-2 dots
+  double2 R[GM_MAX * (GM_MAX + 1)];       // rotated columns: R[j·(GM_MAX+1) + i]
+  double2 g[GM_MAX + 1];
+  double cs[GM_MAX];
+  double2 sn[GM_MAX];
+  double2 y[GM_MAX];
+  double2 ww2;                            // ‖w‖² after the second pass (.x)
+  double hn;                              // h_{j+1,j}
+  int m, j, k;                            // restart length, inner index, Arnoldi steps
+  int pend;                               // status to set after the x update (-1: restart)
+  int endflag;                            // 1: cycle ended (skip the normalisation)
+  int noend;                              // 0: run the cycle-end kernels
+  int noxupd;                             // 0: run the x update
+  int norestart;                          // 0: run the restart kernels
+};
+
+
+// ---------------------------------------------------------------------------
 // Device-resident solver state.  Written only by single-thread "finish"
 // steps; read by every kernel of the next phase (stream order).
 // ---------------------------------------------------------------------------
@@ -127,6 +153,7 @@ struct State {
   double rnrm, xnrm, rnrm_next, xnrm_next, gamma_prev, gamma, theta, theta_prev, c2;
   double rho_r, pi_r, alpha_r, beta_r;  // CGNE (real scalars)
   double tau;      // TFQMR τ_m
+  void* gm;        // GmDev* (GMRES)
   int fin;         // TFQMR: converged at the second half-step, x update pending
   double ss;
 };
@@ -135,7 +162,7 @@ enum { ST_CONVERGED = 0, ST_MAXIT = 1, ST_BREAKDOWN = 2, ST_FALSE_CONV = 3, ST_N
 enum { BD_NONE = 0, BD_RHO = 1, BD_SIGMA = 2, BD_TT = 3, BD_OMEGA = 4, BD_PI = 5, BD_DELTA = 6,
        BD_EPSILON = 7, BD_BETA = 8, BD_XI = 9, BD_VNORM = 10, BD_WNORM = 11, BD_GAMMA = 12 };
 enum { M_BICGSTAB = 0, M_CGNE = 1, M_QMR = 2, M_BICOR = 3, M_CORS = 4,
-       M_BICG = 5, M_CGS = 6, M_COCR = 7, M_CGNR = 8, M_TFQMR = 9, M_COUNT = 10 };
+       M_BICG = 5, M_CGS = 6, M_COCR = 7, M_CGNR = 8, M_TFQMR = 9, M_GMRES = 10, M_COUNT = 11 };
 
 __device__ __forceinline__ void set_done(State* st, int status, int iters, int bd = BD_NONE) {
   st->done = 1; st->gate2 = 1; st->status = status; st->iterations = iters; st->breakdown = bd;

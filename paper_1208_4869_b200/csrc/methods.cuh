@@ -64,6 +64,13 @@ struct InitR {
       case M_BICGSTAB:
       case M_BICG:
       case M_CGS: st->rho = make_double2(rr, 0.0); break;
+      case M_GMRES: {
+        GmDev* gm = reinterpret_cast<GmDev*>(st->gm);
+        gm->g[0] = make_double2(sqrt(rr), 0.0);
+        gm->j = 0; gm->k = 0; gm->pend = -1;
+        gm->endflag = 0; gm->noend = 1; gm->noxupd = 1; gm->norestart = 1;
+        break;
+      }
       case M_TFQMR:
         st->rho = make_double2(rr, 0.0);
         st->tau = sqrt(rr); st->theta = 0.0; st->eta = make_double2(0.0, 0.0);

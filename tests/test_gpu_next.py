@@ -186,7 +186,7 @@ def test_next3_breakdown_fixture():
         assert g["status"] == "CONVERGED" and g["iterations"] == 1
 
 
-@pytest.mark.parametrize("method", ["cgs", "cocr", "tfqmr"])
+@pytest.mark.parametrize("method", ["cgs", "cocr", "tfqmr", "gmres"])
 def test_next3_csr_transpose_free(method):
     """CGS and COCR need only A·x: they run on a CSR operator without the
     symmetric flag (COCR on the complex-symmetric shifted Helmholtz matrix)."""
@@ -512,3 +512,35 @@ def test_callback_python_eager():
     finally:
         ccg.ccg_destroy(h)
         inner.close()
+
+
+
+@pytest.mark.parametrize("restart", [1, 5, 17, 64])
+def test_gmres_restart_lengths(restart):
+    """GMRES(m) for several restart lengths (cycle ends, restarts with the
+    explicit residual) against the oracle with the same m: P-literal."""
+    n = 300
+    A = dense_random(n, seed=31, dtype=np.complex128, shift=2.0 - 1.0j)
+    y = dense_random(n, seed=32)[:, 0] * 2
+    with Dense(A) as h:
+        ccg.ccg_set_gmres_restart(h.h, restart)
+        o = oracle.solve("gmres", DenseOp(A), y, 1e-10, 400, restart=restart)
+        g = h.solve("gmres", y, 1e-10, 400)
+        assert g["status"] == o.status_name == "CONVERGED"
+        assert abs(g["iterations"] - o.iterations) <= 2
+        assert (g["matvecs_a"], g["matvecs_ah"]) == (o.matvecs_a, o.matvecs_ah) or g["iterations"] != o.iterations
+        k = min(g["iterations"], o.iterations)
+        ge = h.solve("gmres", y, 0.0, k)
+        oe = oracle.solve("gmres", DenseOp(A), y, 0.0, k, restart=restart)
+        assert relerr(ge["x"], oe.x) <= 1e-9
+        with pytest.raises(ccg.CcgError) as e:
+            ccg.ccg_set_gmres_restart(h.h, 65)
+        assert e.value.code == -1
+
+
+def test_gmres_c64_cfg3_proxy():
+    n = 4096
+    A = gauss_shifted_rows(n, 0, n, seed=1)
+    y = cfg3_rhs(n)
+    with Dense(A) as h:
+        _parity(h, DenseOp(A), y, "gmres", 1e-5, 500, np.complex64, tag="cfg3-proxy-gmres", literal=False)
