@@ -659,15 +659,103 @@ def _gmres(op, y, x, r, r0sq, tol2, maxit, ctx, hist, st, restart=30):
             return CONVERGED, k, False
 
 
+def _small_solve(Z, z, ctx, name):
+    """Gaussian elimination with partial pivoting on a small ℓ×ℓ system (any
+    scalar type: working precision, exact rationals, mpmath)."""
+    n = len(z)
+    M = [list(row) + [zi] for row, zi in zip(Z, z)]
+    for c in range(n):
+        p = max(range(c, n), key=lambda i: M[i][c].real * M[i][c].real + M[i][c].imag * M[i][c].imag)
+        if M[p][c] == 0:
+            raise _Breakdown(name)
+        M[c], M[p] = M[p], M[c]
+        for i in range(c + 1, n):
+            f = M[i][c] / M[c][c]
+            for j in range(c, n + 1):
+                M[i][j] = M[i][j] - f * M[c][j]
+    g = [None] * n
+    for i in range(n - 1, -1, -1):
+        t = M[i][n]
+        for j in range(i + 1, n):
+            t = t - M[i][j] * g[j]
+        g[i] = ctx.c(t / M[i][i])
+    return g
+
+
+def _bicgstabl(op, y, x, r, r0sq, tol2, maxit, ctx, hist, st, ell=2, shadow=None, trace=None):
+    """BiCGstab(ℓ) (P:79 §3.1, the "vanilla" algorithm of Sleijpen–Fokkema;
+    SURVEY §8(f) NEXT-3): per cycle ℓ BiCG steps (two A·x each) build r̂₀..r̂_ℓ,
+    û₀..û_ℓ with r̂_{j+1} = A r̂_j; the minimal-residual part then minimises
+    ‖r̂₀ − Σ_{j=1..ℓ} γ_j r̂_j‖ through the normal equations Z γ = z,
+    Z_ij = ⟨r̂_i, r̂_j⟩, z_i = ⟨r̂_i, r̂₀⟩ (R16-R18).  ``iterations``
+    counts BiCG steps; r̂₀ is the current residual after every step, so the
+    stopping test runs after every step and after the MR part.  ℓ = 1 is
+    BiCGSTAB (pinned)."""
+    L = int(ell)
+    rt = r.copy() if shadow is None else np.asarray(shadow, dtype=y.dtype)
+    R = [r.copy()] + [None] * L
+    U = [_zero_like(y)] + [None] * L
+    rho0, alpha, omega = ctx.c(1), ctx.c(0), ctx.c(1)
+    k = 0
+    while True:
+        rho0 = ctx.c(-omega * rho0)                                 # ρ₀ = −ω ρ₀
+        for j in range(L):                                          # BiCG part
+            k += 1
+            st["k"] = k
+            rho1 = ctx.c(ctx.dotc(rt, R[j]))                        # ρ₁ = ⟨r̃, r̂_j⟩
+            ctx.check(rho1)
+            beta = ctx.c(alpha * ctx.div(rho1, rho0, "rho"))        # β = α ρ₁/ρ₀
+            rho0 = rho1
+            for i in range(j + 1):
+                U[i] = R[i] - beta * U[i]                           # û_i = r̂_i − β û_i
+            U[j + 1] = op.apply(U[j])                               # û_{j+1} = A û_j
+            gam = ctx.c(ctx.dotc(rt, U[j + 1]))                     # γ = ⟨r̃, û_{j+1}⟩
+            alpha = ctx.c(ctx.div(rho0, gam, "sigma"))              # α = ρ₀/γ
+            for i in range(j + 1):
+                R[i] = R[i] - alpha * U[i + 1]                      # r̂_i −= α û_{i+1}
+            st["x"] = x = x + alpha * U[0]                          # x += α û₀
+            rr = ctx.r(ctx.norm_sq(R[0]))                           # r̂₀ is the residual of x
+            ctx.check(rr)
+            hist.append(sqrt(rr))
+            if _conv(rr, tol2, r0sq):
+                return CONVERGED, k, False
+            if k == maxit and j < L - 1:                            # mid-cycle: no MR part
+                return MAXIT, k, False
+            R[j + 1] = op.apply(R[j])                               # r̂_{j+1} = A r̂_j
+        # MR part: Z γ = z
+        Z = [[ctx.c(ctx.dotc(R[i], R[jj])) for jj in range(1, L + 1)] for i in range(1, L + 1)]
+        zv = [ctx.c(ctx.dotc(R[i], R[0])) for i in range(1, L + 1)]
+        g = _small_solve(Z, zv, ctx, "omega")
+        omega = g[L - 1]                                            # ω = γ_ℓ
+        for jj in range(1, L + 1):
+            x = x + g[jj - 1] * R[jj - 1]                           # x += Σ γ_j r̂_{j−1}
+        st["x"] = x
+        for jj in range(1, L + 1):
+            R[0] = R[0] - g[jj - 1] * R[jj]                         # r̂₀ −= Σ γ_j r̂_j
+        for jj in range(1, L + 1):
+            U[0] = U[0] - g[jj - 1] * U[jj]                         # û₀ −= Σ γ_j û_j
+        if trace is not None:                                       # pins only
+            trace(R, U)
+        rr = ctx.r(ctx.norm_sq(R[0]))
+        ctx.check(rr)
+        hist[-1] = sqrt(rr)                                         # the residual of iteration k
+        if _conv(rr, tol2, r0sq):
+            return CONVERGED, k, False
+        if k >= maxit:
+            return MAXIT, k, False
+        if omega == 0:
+            raise _Breakdown("omega")
+
+
 METHODS = {
     "bicgstab": _bicgstab, "cgne": _cgne, "qmr": _qmr, "bicor": _bicor,
     "cors": _cors,
     # SURVEY §8(f) NEXT-3
     "bicg": _bicg, "cgs": _cgs, "cocr": _cocr, "cgnr": _cgnr, "tfqmr": _tfqmr,
-    "gmres": _gmres,
+    "gmres": _gmres, "bicgstabl": _bicgstabl,
 }
 HOT_PATH = ("bicgstab", "cgne", "qmr", "bicor", "cors")
-NEXT3 = ("bicg", "cgs", "cocr", "cgnr", "tfqmr", "gmres")
+NEXT3 = ("bicg", "cgs", "cocr", "cgnr", "tfqmr", "gmres", "bicgstabl")
 
 
 def solve(method, op, y, tol, maxit, x0=None, dots=None, **kw):

@@ -157,7 +157,7 @@ def test_scale_invariance(method):
 def test_work_accounting():
     A, y = cfg1(n=64, seed=4)
     for m, want in {"bicg": (5, 5), "cgs": (10, 0), "cocr": (5, 0), "cgnr": (5, 5), "tfqmr": (10, 0),
-                          "gmres": (5, 0)}.items():
+                          "gmres": (5, 0), "bicgstabl": (9, 0)}.items():
         res = solve(m, DenseOp(A), y, 0.0, 5)
         assert res.status == MAXIT and res.iterations == 5
         assert (res.matvecs_a, res.matvecs_ah) == want, m
@@ -166,7 +166,8 @@ def test_work_accounting():
 def test_breakdown_fixture():
     A = np.array([[0, 1], [-1, 0]], dtype=np.complex128)
     y = np.array([1, 0], dtype=np.complex128)
-    for m, name in (("bicg", "sigma"), ("cgs", "sigma"), ("cocr", "rho"), ("tfqmr", "sigma")):
+    for m, name in (("bicg", "sigma"), ("cgs", "sigma"), ("cocr", "rho"), ("tfqmr", "sigma"),
+                    ("bicgstabl", "sigma")):
         r = solve(m, DenseOp(A), y, 1e-10, 10)
         assert r.status == BREAKDOWN and r.breakdown == name and r.iterations == 0, m
     r = solve("cgnr", DenseOp(A), y, 1e-10, 10)      # A unitary: CGNR converges at once
@@ -277,3 +278,52 @@ def test_gmres_cgs2_keeps_the_givens_residual_true():
     res = solve("gmres", DenseOp(A), y, 0.0, 60, restart=60)
     gap = abs(float(res.history[-1]) - np.linalg.norm(y - A @ res.x)) / np.linalg.norm(y)
     assert gap <= 6e-13
+
+
+# ---------------- BiCGstab(ℓ) (§3.1) ----------------
+def test_bicgstabl_one_is_bicgstab():
+    """ℓ = 1: the minimal-residual part is BiCGSTAB's ω step — same iterates
+    and the same number of products at every k."""
+    A = dense_random(40, seed=101, shift=1.5 - 1j)
+    y = dense_random(40, seed=102)[:, 0]
+    for k in range(1, 11):
+        a = solve("bicgstabl", DenseOp(A), y, 0.0, k, ell=1)
+        b = solve("bicgstab", DenseOp(A), y, 0.0, k)
+        assert a.matvecs_a == b.matvecs_a == 2 * k
+        assert np.linalg.norm(a.x - b.x) <= 1e-13 * np.linalg.norm(b.x), k
+    a = solve("bicgstabl", DenseOp(A), y, 1e-10, 200, ell=1)
+    b = solve("bicgstab", DenseOp(A), y, 1e-10, 200)
+    assert (a.iterations, a.matvecs_a) == (b.iterations, b.matvecs_a)     # incl. the half-step exit
+
+
+@pytest.mark.parametrize("n", [3, 4, 5, 6])
+@pytest.mark.parametrize("ell", [1, 2, 3])
+def test_bicgstabl_exact_finite_termination(ell, n):
+    A, y = _rand_int(n, seed=23 * n + ell, kind="gen")
+    Ae, ye = to_exact(A), to_exact(y)
+    op = DenseOp(Ae)
+    res = solve("bicgstabl", op, ye, 0.0, n + 3 * ell, ell=ell)
+    assert res.status == CONVERGED, (res.status_name, res.breakdown)
+    assert res.iterations <= n
+    assert all(v == 0 for v in ye - op.apply(res.x)), "A·x must equal y exactly"
+
+
+def test_bicgstabl_mr_part_minimises_over_the_cycle_space():
+    """After every cycle the MR update leaves r̂₀ orthogonal to r̂₁..r̂_ℓ (the
+    normal equations of the minimal-residual polynomial), the invariants
+    r̂_j = A r̂_{j−1}, û_j = A û_{j−1} hold, and r̂₀ is the residual y − A x."""
+    A = dense_random(50, seed=105, shift=2 + 1j)
+    y = dense_random(50, seed=106)[:, 0]
+    for ell in (2, 3, 4):
+        cycles = []
+        res = solve("bicgstabl", DenseOp(A), y, 0.0, 4 * ell, ell=ell,
+                    trace=lambda R, U: cycles.append(([v.copy() for v in R], [v.copy() for v in U])))
+        assert len(cycles) == 4
+        for R, U in cycles:
+            nr = np.linalg.norm(R[0])
+            for j in range(1, ell + 1):
+                assert abs(np.vdot(R[j], R[0])) <= 1e-10 * np.linalg.norm(R[j]) * nr, (ell, j)
+                if j < ell:
+                    assert np.linalg.norm(R[j + 1] - A @ R[j]) <= 1e-10 * np.linalg.norm(R[j + 1])
+                    assert np.linalg.norm(U[j + 1] - A @ U[j]) <= 1e-10 * np.linalg.norm(U[j + 1])
+        assert np.linalg.norm(cycles[-1][0][0] - (y - A @ res.x)) <= 1e-10 * np.linalg.norm(y)
