@@ -73,8 +73,10 @@ typedef enum {
   CCG_COCR = 7,
   CCG_CGNR = 8,
   CCG_TFQMR = 9,  /* P:57 [§2.1]; stops on Freund's bound τ_m·√(m+1) ≤ tol·‖r₀‖ (R9) */
-  CCG_GMRES = 10  /* restarted GMRES(m), P:57 [§2.1] "rgmres"; m from ccg_set_gmres_restart (default 30);
+  CCG_GMRES = 10, /* restarted GMRES(m), P:57 [§2.1] "rgmres"; m from ccg_set_gmres_restart (default 30);
                      iterations = Arnoldi steps, + one A·x per restart (R12-R15) */
+  CCG_BICGSTABL = 11 /* BiCGstab(ℓ), P:79 [§3.1] (vanilla); ℓ from ccg_set_bicgstab_ell (default 2);
+                        iterations = BiCG steps, two A·x each (R16-R18) */
 } ccg_method;
 
 /* The three products of the operator module: A·x (matvec),
@@ -251,6 +253,9 @@ int ccg_apply(ccg_handle h, ccg_op op, const void* x_local, void* y_local);
 /* Restart length m of CCG_GMRES (1 ≤ m ≤ 64, else CCG_E_ARG; default 30).  The
  * basis (m+1 vectors of nloc elements) is allocated by the next GMRES solve. */
 int ccg_set_gmres_restart(ccg_handle h, int32_t m);
+
+/* ℓ of CCG_BICGSTABL (1 ≤ ℓ ≤ 4, else CCG_E_ARG; default 2; ℓ = 1 is BiCGSTAB). */
+int ccg_set_bicgstab_ell(ccg_handle h, int32_t ell);
 
 /* Solve A x = y with `method` (stopping rule ‖r_k‖ ≤ tol·‖r_0‖
  * on the recurrence residual, r_0 = y − A·x0; true residual recomputed at exit).

@@ -21,7 +21,7 @@ LIB_PATH = os.path.join(_HERE, "libccg.so")
 
 C64, C128 = 0, 1
 METHODS = {"bicgstab": 0, "cgne": 1, "qmr": 2, "bicor": 3, "cors": 4,
-           "bicg": 5, "cgs": 6, "cocr": 7, "cgnr": 8, "tfqmr": 9, "gmres": 10}
+           "bicg": 5, "cgs": 6, "cocr": 7, "cgnr": 8, "tfqmr": 9, "gmres": 10, "bicgstabl": 11}
 OPS = {"A": 0, "AH": 1, "AT": 2}
 FLAG_SYMMETRIC = 1
 STATUS = {0: "CONVERGED", 1: "MAXIT", 2: "BREAKDOWN", 3: "FALSE_CONVERGENCE", 4: "NONFINITE"}
@@ -37,6 +37,7 @@ MATVEC_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_int, ctypes
 EXPORTS = ("ccg_get_unique_id", "ccg_create", "ccg_create_loopback_group",
            "ccg_set_matvec_dense", "ccg_set_matvec_csr", "ccg_set_matvec_stencil7",
            "ccg_set_matvec_toeplitz3", "ccg_set_matvec_callback", "ccg_set_gmres_restart",
+           "ccg_set_bicgstab_ell",
            "ccg_apply", "ccg_solve", "ccg_get_history", "ccg_set_timing", "ccg_get_timing",
            "ccg_last_launch_count", "ccg_get_stream", "ccg_last_error", "ccg_destroy",
            "ccg_version")
@@ -93,6 +94,7 @@ def load():
                                                     ctypes.POINTER(dbl), u32]),
         "ccg_set_matvec_callback": (ctypes.c_int, [vp, MATVEC_FN, vp, u32, u32]),
         "ccg_set_gmres_restart": (ctypes.c_int, [vp, i32]),
+        "ccg_set_bicgstab_ell": (ctypes.c_int, [vp, i32]),
         "ccg_apply": (ctypes.c_int, [vp, ctypes.c_int, vp, vp]),
         "ccg_solve": (ctypes.c_int, [vp, ctypes.c_int, vp, vp, vp, dbl, i32,
                                      ctypes.POINTER(ccg_result)]),
@@ -242,6 +244,10 @@ def ccg_set_matvec_callback_ptr(h, fn_addr, user_addr=None, caps=CB_A, flags=0):
 
 def ccg_set_gmres_restart(h, m):
     _check(h, load().ccg_set_gmres_restart(h, int(m)))
+
+
+def ccg_set_bicgstab_ell(h, ell):
+    _check(h, load().ccg_set_bicgstab_ell(h, int(ell)))
 
 
 def ccg_apply(h, op, x, y):

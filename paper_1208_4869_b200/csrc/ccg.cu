@@ -90,6 +90,10 @@ struct ccg_ctx {
   double2* gm_rank = nullptr;
   double2* gm_all = nullptr;
   int gm_grid = 1;
+  // BiCGstab(ℓ) workspace: r̂₀..r̂_ℓ, û₀..û_ℓ as full-length buffers
+  int bl_l = 2, bl_built = 0;
+  void* bl_buf = nullptr;
+  size_t bl_bytes = 0;
   // whole-loop cluster kernel for small dense systems (cluster.cuh)
   bool cluster_ok = false;
   int cluster_size = 0;   // 0 = not yet chosen
@@ -898,6 +902,66 @@ struct Engine {
     return CCG_OK;
   }
 
+  // ---- BiCGstab(ℓ): loc: 0 x, 1 y, 3 r̃ ; bl_buf: r̂₀..r̂_ℓ then û₀..û_ℓ (full length each)
+  static C* BLR(ccg_ctx* c, int a) { return reinterpret_cast<C*>(c->bl_buf) + (size_t)a * c->n; }
+  static C* BLU(ccg_ctx* c, int a) { return BLR(c, c->bl_l + 1 + a); }
+  static C* BRs(ccg_ctx* c, int a) { return BLR(c, a) + c->row0; }
+  static C* BUs(ccg_ctx* c, int a) { return BLU(c, a) + c->row0; }
+  static int allgather_buf(ccg_ctx* c, C* buf) {
+    if (c->world == 1) return CCG_OK;
+    if (c->opk == OPK_CSR || c->opk == OPK_STENCIL) return halo_exchange(c, buf);
+    NK(c, c->comm->allgather_inplace(buf, (size_t)c->nloc * 2, ndt(), c->stream));
+    return CCG_OK;
+  }
+  static int bicgstabl_setup(ccg_ctx* c, bool x0) {
+    TRY(init_residual(c, x0, BRs(c, 0), L(c, 3), nullptr, nullptr));
+    CK(c, cudaMemsetAsync(BUs(c, 0), 0, (size_t)c->nloc * sizeof(C), c->stream));
+    return CCG_OK;
+  }
+  template <int LL>
+  static int bicgstabl_mr(ccg_ctx* c, const int* g) {
+    BlGram<T, LL> G{};
+    BlM<T, LL> M{};
+    for (int a = 0; a <= LL; ++a) {
+      G.r[a] = BRs(c, a);
+      M.r[a] = BRs(c, a);
+      M.u[a] = BUs(c, a);
+    }
+    M.x = L(c, X);
+    M.rt = L(c, 3);
+    TRY(pass(c, G, g));
+    return pass(c, M, g);
+  }
+  static int bicgstabl_iter(ccg_ctx* c) {
+    const int* g = &c->st->done;
+    const int ell = c->bl_l;
+    for (int j = 0; j < ell; ++j) {
+      BlP<T> P{};
+      for (int a = 0; a <= j; ++a) { P.u[a] = BUs(c, a); P.r[a] = BRs(c, a); }
+      P.J = j;
+      TRY(pass(c, P, g));
+      TRY(allgather_buf(c, BLU(c, j)));
+      TRY(matvec_a(c, BLU(c, j), BlU<T>{BUs(c, j + 1), L(c, 3)}, g));
+      BlX<T> Xp{};
+      for (int a = 0; a <= j; ++a) Xp.r[a] = BRs(c, a);
+      for (int a = 0; a <= j + 1; ++a) Xp.u[a] = BUs(c, a);
+      Xp.x = L(c, X);
+      Xp.J = j;
+      TRY(pass(c, Xp, g));
+      TRY(allgather_buf(c, BLR(c, j)));
+      if (j < ell - 1)
+        TRY(matvec_a(c, BLR(c, j), BlR<T>{BRs(c, j + 1), L(c, 3)}, g));
+      else
+        TRY(matvec_a(c, BLR(c, j), BlRL<T>{BRs(c, j + 1)}, g));
+    }
+    switch (ell) {
+      case 1: return bicgstabl_mr<1>(c, g);
+      case 2: return bicgstabl_mr<2>(c, g);
+      case 3: return bicgstabl_mr<3>(c, g);
+      default: return bicgstabl_mr<4>(c, g);
+    }
+  }
+
   static int setup(ccg_ctx* c, int m, bool x0) {
     switch (m) {
       case M_BICGSTAB: return bicgstab_setup(c, x0);
@@ -910,6 +974,7 @@ struct Engine {
       case M_COCR: return cocr_setup(c, x0);
       case M_TFQMR: return tfqmr_setup(c, x0);
       case M_GMRES: return gmres_setup(c, x0);
+      case M_BICGSTABL: return bicgstabl_setup(c, x0);
       default: return cgnr_setup(c, x0);
     }
   }
@@ -925,6 +990,7 @@ struct Engine {
       case M_COCR: return cocr_iter(c);
       case M_TFQMR: return tfqmr_iter(c);
       case M_GMRES: return gmres_iter(c);
+      case M_BICGSTABL: return bicgstabl_iter(c);
       default: return cgnr_iter(c);
     }
   }
@@ -1113,7 +1179,7 @@ static int choose_launch(ccg_ctx* c) {
                                        c->opk == OPK_TOEPLITZ
                                            ? (int64_t)(c->geo.ny * c->geo.nz + c->geo.tx - 1) / c->geo.tx
                                            : (int64_t)1});
-  size_t need_part = (size_t)maxgrid * 4;
+  size_t need_part = (size_t)maxgrid * 16;   // up to 16 partial sums per CTA (BiCGstab(ℓ) Gram pass)
   if (need_part > c->part_cap) {
     if (c->part) cudaFree(c->part);
     c->part = nullptr;
@@ -1328,8 +1394,8 @@ static int create_impl(ccg_handle* h, ccg_dtype dt, int64_t n, int world, int ra
   CKC(cudaMallocHost(&c->st_host, sizeof(State)));
   CKC(cudaMalloc(&c->ticket, sizeof(unsigned)));
   CKC(cudaMemset(c->ticket, 0, sizeof(unsigned)));
-  CKC(cudaMalloc(&c->rank_sum, 8 * sizeof(double2)));
-  CKC(cudaMalloc(&c->all_sums, (size_t)8 * world * sizeof(double2)));
+  CKC(cudaMalloc(&c->rank_sum, 16 * sizeof(double2)));
+  CKC(cudaMalloc(&c->all_sums, (size_t)16 * world * sizeof(double2)));
   CKC(cudaMalloc(&c->zero_gate, sizeof(int)));
   CKC(cudaMemset(c->zero_gate, 0, sizeof(int)));
   for (int i = 0; i < NLOCAL; ++i) {
@@ -1625,11 +1691,38 @@ int ccg_set_gmres_restart(ccg_handle c, int32_t m) {
   return CCG_OK;
 }
 
+int ccg_set_bicgstab_ell(ccg_handle c, int32_t ell) {
+  if (!c) return CCG_E_ARG;
+  if (ell < 1 || ell > BL_MAX) FAIL(c, CCG_E_ARG, "BiCGstab(l): l must be in [1, 4]");
+  if (ell != c->bl_l) invalidate_graphs(c);
+  c->bl_l = ell;
+  return CCG_OK;
+}
+
+static int bicgstabl_workspace(ccg_ctx* c) {
+  const size_t need = (size_t)2 * (c->bl_l + 1) * (size_t)c->n * c->esz;
+  if (need > c->bl_bytes) {
+    if (c->bl_buf) cudaFree(c->bl_buf);
+    c->bl_buf = nullptr;
+    c->bl_bytes = 0;
+    CK(c, cudaMalloc(&c->bl_buf, need));
+    CK(c, cudaMemset(c->bl_buf, 0, need));
+    c->bl_bytes = need;
+  }
+  invalidate_graphs(c);   // buffer layout depends on ℓ
+  if (!c->gm_dev) {
+    CK(c, cudaMalloc(&c->gm_dev, sizeof(GmDev)));
+    CK(c, cudaMemset(c->gm_dev, 0, sizeof(GmDev)));
+  }
+  return CCG_OK;
+}
+
 // GMRES workspace: basis (m+1) × nloc, Hessenberg data, per-CTA multi-dot slots
 static int gmres_workspace(ccg_ctx* c) {
   const size_t need = (size_t)(c->gm_m + 1) * (size_t)c->nloc * c->esz;
   if (need > c->gm_V_bytes) {
     if (c->gm_V) cudaFree(c->gm_V);
+  if (c->bl_buf) cudaFree(c->bl_buf);
     c->gm_V = nullptr;
     c->gm_V_bytes = 0;
     CK(c, cudaMalloc(&c->gm_V, need));
@@ -1734,6 +1827,11 @@ int ccg_solve(ccg_handle c, ccg_method method, const void* x0_local, const void*
     TRY(gmres_workspace(c));
     s0.gm = c->gm_dev;
   }
+  if (method == CCG_BICGSTABL) {
+    if (c->bl_l != c->bl_built) { TRY(bicgstabl_workspace(c)); c->bl_built = c->bl_l; }
+    s0.gm = c->gm_dev;
+    s0.bl_l = c->bl_l;
+  }
   *c->st_host = s0;
   CK(c, cudaMemcpyAsync(c->st, c->st_host, sizeof(State), cudaMemcpyHostToDevice, c->stream));
   // inputs: x -> loc[0], y -> loc[1]
@@ -1745,7 +1843,8 @@ int ccg_solve(ccg_handle c, ccg_method method, const void* x0_local, const void*
   }
   const bool has_x0 = x0_local != nullptr;
   int rc;
-  if (c->opk == OPK_DENSE && c->cluster_ok && c->world == 1 && !c->timing && method != CCG_GMRES) {
+  if (c->opk == OPK_DENSE && c->cluster_ok && c->world == 1 && !c->timing && method != CCG_GMRES &&
+      method != CCG_BICGSTABL) {
     // small dense system: setup, every iteration and the true residual in ONE
     // cluster launch (cluster.cuh); maxit and the stopping rule live in the State
     c->cl_method = method;
@@ -1836,6 +1935,7 @@ int ccg_destroy(ccg_handle c) {
   if (c->part) cudaFree(c->part);
   if (c->hist) cudaFree(c->hist);
   if (c->gm_V) cudaFree(c->gm_V);
+  if (c->bl_buf) cudaFree(c->bl_buf);
   if (c->gm_dev) cudaFree(c->gm_dev);
   if (c->gm_part) cudaFree(c->gm_part);
   if (c->gm_ticket) cudaFree(c->gm_ticket);

@@ -153,7 +153,8 @@ struct State {
   double rnrm, xnrm, rnrm_next, xnrm_next, gamma_prev, gamma, theta, theta_prev, c2;
   double rho_r, pi_r, alpha_r, beta_r;  // CGNE (real scalars)
   double tau;      // TFQMR τ_m
-  void* gm;        // GmDev* (GMRES)
+  void* gm;        // GmDev* (GMRES; BiCGstab(ℓ) scratch)
+  int bl_l;        // BiCGstab(ℓ): ℓ
   int fin;         // TFQMR: converged at the second half-step, x update pending
   double ss;
 };
@@ -162,7 +163,8 @@ enum { ST_CONVERGED = 0, ST_MAXIT = 1, ST_BREAKDOWN = 2, ST_FALSE_CONV = 3, ST_N
 enum { BD_NONE = 0, BD_RHO = 1, BD_SIGMA = 2, BD_TT = 3, BD_OMEGA = 4, BD_PI = 5, BD_DELTA = 6,
        BD_EPSILON = 7, BD_BETA = 8, BD_XI = 9, BD_VNORM = 10, BD_WNORM = 11, BD_GAMMA = 12 };
 enum { M_BICGSTAB = 0, M_CGNE = 1, M_QMR = 2, M_BICOR = 3, M_CORS = 4,
-       M_BICG = 5, M_CGS = 6, M_COCR = 7, M_CGNR = 8, M_TFQMR = 9, M_GMRES = 10, M_COUNT = 11 };
+       M_BICG = 5, M_CGS = 6, M_COCR = 7, M_CGNR = 8, M_TFQMR = 9, M_GMRES = 10,
+       M_BICGSTABL = 11, M_COUNT = 12 };
 
 __device__ __forceinline__ void set_done(State* st, int status, int iters, int bd = BD_NONE) {
   st->done = 1; st->gate2 = 1; st->status = status; st->iterations = iters; st->breakdown = bd;

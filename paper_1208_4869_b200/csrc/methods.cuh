@@ -71,6 +71,14 @@ struct InitR {
         gm->endflag = 0; gm->noend = 1; gm->noxupd = 1; gm->norestart = 1;
         break;
       }
+      case M_BICGSTABL:
+        // ρ₀ = −ω·1 = −1 at the first cycle start; step 1: ρ₁ = ⟨r̃, r₀⟩ = ‖r₀‖²,
+        // β = α·(ρ₁/ρ₀) with α = 0, ρ₀ ← ρ₁
+        st->alpha = make_double2(0.0, 0.0);
+        st->omega = make_double2(1.0, 0.0);
+        st->beta = zmul(st->alpha, zdiv(make_double2(rr, 0.0), make_double2(-1.0, 0.0)));
+        st->rho = make_double2(rr, 0.0);
+        break;
       case M_TFQMR:
         st->rho = make_double2(rr, 0.0);
         st->tau = sqrt(rr); st->theta = 0.0; st->eta = make_double2(0.0, 0.0);
@@ -998,6 +1006,190 @@ struct TfV {  // A u (kept) ; v = A u + β(A u₂ + βv) ; σ = ⟨r₀*, v⟩ ;
     if (zzero(sigma)) { set_done(st, ST_BREAKDOWN, kc, BD_SIGMA); return; }
     st->alpha = zdiv(st->rho, sigma);
     if (!zfinite(st->alpha)) { set_done(st, ST_NONFINITE, kc); return; }
+  }
+};
+
+// ---- BiCGstab(ℓ) (§3.1; vanilla Sleijpen–Fokkema, readings R16-R18).
+// Per BiCG step j: P_j (û_i = r̂_i − βû_i, i ≤ j) → [A û_j → û_{j+1}, γ → α] →
+// X_j (r̂_i −= αû_{i+1}, x += αû₀, ‖r̂₀‖²) → [A r̂_j → r̂_{j+1}, ρ₁ → β].
+// MR part: Gram pass (Z, z, and the ℓ×ℓ solve in its scalar step) → M (x, r̂₀,
+// û₀ updates, ‖r̂₀‖², ⟨r̃, r̂₀⟩ → the next cycle's ρ₀, ρ₁, β).
+constexpr int BL_MAX = 4;
+
+template <typename T>
+struct BlP {
+  static constexpr int K = 0;
+  using C = Cx<T>;
+  C* u[BL_MAX + 1]; const C* r[BL_MAX + 1]; int J;
+  C beta;
+  __device__ void load(const State* st) { beta = fromd2<C>(st->beta); }
+  __device__ void operator()(int64_t i, double2*) {
+    for (int a = 0; a <= J; ++a) u[a][i] = caxmy(r[a][i], beta, u[a][i]);
+  }
+  static __device__ void finish(State*, const double2*) {}
+};
+
+template <typename T>
+struct BlU {  // û_{j+1} = A û_j ; γ = ⟨r̃, û_{j+1}⟩ ; α = ρ₀/γ
+  static constexpr int K = 1;
+  using C = Cx<T>;
+  C* un; const C* rt;
+  __device__ void load(const State*) {}
+  __device__ void operator()(int64_t i, C val, double2* acc) { un[i] = val; dotc_acc(acc[0], rt[i], val); }
+  static __device__ void finish(State* st, const double2* s) { st->matvecs_a++; sigma_step(st, s[0]); }
+};
+
+template <typename T>
+struct BlX {  // r̂_i −= α û_{i+1} (i ≤ j) ; x += α û₀ ; ‖r̂₀‖² ; stopping test
+  static constexpr int K = 1;
+  using C = Cx<T>;
+  C* r[BL_MAX + 1]; const C* u[BL_MAX + 1]; C* x; int J;
+  C alpha;
+  __device__ void load(const State* st) { alpha = fromd2<C>(st->alpha); }
+  __device__ void operator()(int64_t i, double2* acc) {
+    for (int a = 0; a <= J; ++a) r[a][i] = caxmy(r[a][i], alpha, u[a + 1][i]);
+    x[i] = caxpy(x[i], alpha, u[0][i]);
+    nrm_acc(acc[0], r[0][i]);
+  }
+  static __device__ void finish(State* st, const double2* s) {
+    const int k = st->iter + 1;
+    const double rr = s[0].x;
+    if (!isfinite(rr)) { set_done(st, ST_NONFINITE, k - 1); return; }
+    push_hist(st, k, rr);
+    st->iter = k;
+    if (rr <= st->tol2r0) { set_done(st, ST_CONVERGED, k); return; }
+    if (k >= st->maxit && (k % st->bl_l) != 0) set_done(st, ST_MAXIT, k);   // mid-cycle
+  }
+};
+
+// ρ₁ → β for the next step (also the start of a cycle, after M)
+__device__ __forceinline__ void bl_next_beta(State* st, double2 rho1) {
+  const int k = st->iter;
+  if (!zfinite(rho1)) { set_done(st, ST_NONFINITE, k); return; }
+  if (zzero(st->rho)) { set_done(st, ST_BREAKDOWN, k, BD_RHO); return; }
+  st->beta = zmul(st->alpha, zdiv(rho1, st->rho));
+  st->rho = rho1;
+}
+
+template <typename T>
+struct BlR {  // r̂_{j+1} = A r̂_j ; ρ₁ = ⟨r̃, r̂_{j+1}⟩ ; β = α ρ₁/ρ₀ (not the last step of a cycle)
+  static constexpr int K = 1;
+  using C = Cx<T>;
+  C* rn; const C* rt;
+  __device__ void load(const State*) {}
+  __device__ void operator()(int64_t i, C val, double2* acc) { rn[i] = val; dotc_acc(acc[0], rt[i], val); }
+  static __device__ void finish(State* st, const double2* s) { st->matvecs_a++; bl_next_beta(st, s[0]); }
+};
+
+template <typename T>
+struct BlRL {  // r̂_ℓ = A r̂_{ℓ−1} (last step of a cycle: only the product)
+  static constexpr int K = 1;
+  using C = Cx<T>;
+  C* rn;
+  __device__ void load(const State*) {}
+  __device__ void operator()(int64_t i, C val, double2*) { rn[i] = val; }
+  static __device__ void finish(State* st, const double2*) { st->matvecs_a++; }
+};
+
+// MR part, Gram pass: Z_ij = ⟨r̂_i, r̂_j⟩ (1 ≤ i ≤ j ≤ L), z_i = ⟨r̂_i, r̂₀⟩; the
+// scalar step solves Z γ = z (partial pivoting by |·|², as the oracle) into the
+// scratch gm->y and sets ω = γ_L.  Z lives in gm->R, z in gm->g.
+template <typename T, int L>
+struct BlGram {
+  static constexpr int K = L * (L + 1) / 2 + L;
+  using C = Cx<T>;
+  const C* r[BL_MAX + 1];
+  __device__ void load(const State*) {}
+  __device__ void operator()(int64_t i, double2* acc) {
+    C v[L + 1];
+#pragma unroll
+    for (int a = 0; a <= L; ++a) v[a] = r[a][i];
+    int p = 0;
+#pragma unroll
+    for (int a = 1; a <= L; ++a)
+#pragma unroll
+      for (int b = a; b <= L; ++b) dotc_acc(acc[p++], v[a], v[b]);
+#pragma unroll
+    for (int a = 1; a <= L; ++a) dotc_acc(acc[p++], v[a], v[0]);
+  }
+  static __device__ void finish(State* st, const double2* s) {
+    GmDev* gm = reinterpret_cast<GmDev*>(st->gm);
+    double2 M[L][L + 1];
+    int p = 0;
+    for (int a = 0; a < L; ++a)
+      for (int b = a; b < L; ++b) { M[a][b] = s[p]; M[b][a] = zconj(s[p]); ++p; }
+    for (int a = 0; a < L; ++a) M[a][L] = s[p++];
+    for (int c = 0; c < L; ++c) {
+      int piv = c;
+      double best = M[c][c].x * M[c][c].x + M[c][c].y * M[c][c].y;
+      for (int i = c + 1; i < L; ++i) {
+        const double m2 = M[i][c].x * M[i][c].x + M[i][c].y * M[i][c].y;
+        if (m2 > best) { best = m2; piv = i; }
+      }
+      if (zzero(M[piv][c])) { set_done(st, ST_BREAKDOWN, st->iter - 1, BD_OMEGA); return; }
+      if (piv != c)
+        for (int j = 0; j <= L; ++j) { const double2 t = M[c][j]; M[c][j] = M[piv][j]; M[piv][j] = t; }
+      for (int i = c + 1; i < L; ++i) {
+        const double2 f = zdiv(M[i][c], M[c][c]);
+        for (int j = c; j <= L; ++j) {
+          const double2 q = zmul(f, M[c][j]);
+          M[i][j] = make_double2(M[i][j].x - q.x, M[i][j].y - q.y);
+        }
+      }
+    }
+    for (int i = L - 1; i >= 0; --i) {
+      double2 t = M[i][L];
+      for (int j = i + 1; j < L; ++j) {
+        const double2 q = zmul(M[i][j], gm->y[j]);
+        t = make_double2(t.x - q.x, t.y - q.y);
+      }
+      gm->y[i] = zdiv(t, M[i][i]);
+      if (!zfinite(gm->y[i])) { set_done(st, ST_NONFINITE, st->iter - 1); return; }
+    }
+    st->omega = gm->y[L - 1];
+  }
+};
+
+template <typename T, int L>
+struct BlM {  // x += Σ γ_j r̂_{j−1} ; r̂₀ −= Σ γ_j r̂_j ; û₀ −= Σ γ_j û_j ; ‖r̂₀‖², ⟨r̃, r̂₀⟩
+  static constexpr int K = 2;
+  using C = Cx<T>;
+  C* r[BL_MAX + 1]; C* u[BL_MAX + 1]; C* x; const C* rt;
+  C g[L];
+  __device__ void load(const State* st) {
+    const GmDev* gm = reinterpret_cast<const GmDev*>(st->gm);
+#pragma unroll
+    for (int a = 0; a < L; ++a) g[a] = fromd2<C>(gm->y[a]);
+  }
+  __device__ void operator()(int64_t i, double2* acc) {
+    C rv[L + 1];
+#pragma unroll
+    for (int a = 0; a <= L; ++a) rv[a] = r[a][i];
+    C xv = x[i];
+#pragma unroll
+    for (int a = 1; a <= L; ++a) xv = caxpy(xv, g[a - 1], rv[a - 1]);
+    x[i] = xv;
+    C r0 = rv[0];
+#pragma unroll
+    for (int a = 1; a <= L; ++a) r0 = caxmy(r0, g[a - 1], rv[a]);
+    r[0][i] = r0;
+    C u0 = u[0][i];
+#pragma unroll
+    for (int a = 1; a <= L; ++a) u0 = caxmy(u0, g[a - 1], u[a][i]);
+    u[0][i] = u0;
+    nrm_acc(acc[0], r0);
+    dotc_acc(acc[1], rt[i], r0);
+  }
+  static __device__ void finish(State* st, const double2* s) {
+    const int k = st->iter;
+    const double rr = s[0].x;
+    if (!isfinite(rr)) { set_done(st, ST_NONFINITE, k - 1); return; }
+    push_hist(st, k, rr);
+    if (rr <= st->tol2r0) { set_done(st, ST_CONVERGED, k); return; }
+    if (k >= st->maxit) { set_done(st, ST_MAXIT, k); return; }
+    if (zzero(st->omega)) { set_done(st, ST_BREAKDOWN, k - 1, BD_OMEGA); return; }
+    st->rho = zmul(make_double2(-st->omega.x, -st->omega.y), st->rho);   // ρ₀ = −ω ρ₀
+    bl_next_beta(st, s[1]);
   }
 };
 

@@ -119,7 +119,7 @@ def test_sharded_dense_apply(G, dtype):
 
 @pytest.mark.parametrize("G", [2, 4])
 @pytest.mark.parametrize("method", ["bicgstab", "cgne", "qmr", "bicor", "cors",
-                                    "bicg", "cgs", "cocr", "cgnr", "tfqmr", "gmres"])
+                                    "bicg", "cgs", "cocr", "cgnr", "tfqmr", "gmres", "bicgstabl"])
 def test_sharded_cfg1_solve(G, method):
     A, y = cfg1()
     if method == "cocr":

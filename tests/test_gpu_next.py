@@ -177,7 +177,8 @@ def test_next3_breakdown_fixture():
     A = np.array([[0, 1], [-1, 0]], dtype=np.complex128)
     y = np.array([1, 0], dtype=np.complex128)
     with Dense(A) as h:
-        for m, name in (("bicg", "sigma"), ("cgs", "sigma"), ("cocr", "rho"), ("tfqmr", "sigma")):
+        for m, name in (("bicg", "sigma"), ("cgs", "sigma"), ("cocr", "rho"), ("tfqmr", "sigma"),
+                        ("bicgstabl", "sigma")):
             g = h.solve(m, y, 1e-10, 10)
             o = oracle.solve(m, DenseOp(A), y, 1e-10, 10)
             assert g["status"] == "BREAKDOWN" and g["breakdown"] == name == o.breakdown, m
@@ -544,3 +545,33 @@ def test_gmres_c64_cfg3_proxy():
     y = cfg3_rhs(n)
     with Dense(A) as h:
         _parity(h, DenseOp(A), y, "gmres", 1e-5, 500, np.complex64, tag="cfg3-proxy-gmres", literal=False)
+
+
+
+@pytest.mark.parametrize("ell", [1, 2, 3, 4])
+def test_bicgstabl_ells(ell):
+    """BiCGstab(ℓ) for every supported ℓ against the oracle with the same ℓ
+    (P-literal, matvec counts, residual history); ℓ = 1 reproduces the GPU
+    BiCGSTAB iteration count."""
+    n = 400
+    A = dense_random(n, seed=41, dtype=np.complex128, shift=1.5 - 1.0j)
+    y = dense_random(n, seed=42)[:, 0] * 2
+    with Dense(A) as h:
+        ccg.ccg_set_bicgstab_ell(h.h, ell)
+        o = oracle.solve("bicgstabl", DenseOp(A), y, 1e-10, 400, ell=ell)
+        g = h.solve("bicgstabl", y, 1e-10, 400)
+        assert g["status"] == o.status_name == "CONVERGED"
+        assert abs(g["iterations"] - o.iterations) <= 2
+        if g["iterations"] == o.iterations:
+            assert (g["matvecs_a"], g["matvecs_ah"]) == (o.matvecs_a, o.matvecs_ah)
+            np.testing.assert_allclose(ccg.ccg_get_history(h.h), np.array(o.history, float) / o.history[0],
+                                       rtol=1e-6, atol=1e-12)
+        k = min(g["iterations"], o.iterations)
+        ge = h.solve("bicgstabl", y, 0.0, k)
+        oe = oracle.solve("bicgstabl", DenseOp(A), y, 0.0, k, ell=ell)
+        assert relerr(ge["x"], oe.x) <= 1e-9
+        if ell == 1:
+            assert g["iterations"] == h.solve("bicgstab", y, 1e-10, 400)["iterations"]
+        with pytest.raises(ccg.CcgError) as e:
+            ccg.ccg_set_bicgstab_ell(h.h, 5)
+        assert e.value.code == -1
