@@ -41,6 +41,8 @@ def parse():
     p.add_argument("--impl", default="ccg", choices=["ccg", "reference"])
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--sharded-vectors", action="store_true",
+                   help="N>1: row-sharded vectors (C1 allgather + scalar allgathers) instead of replicated vectors")
     return p.parse_args()
 
 
@@ -228,7 +230,10 @@ def run_ccg(args):
     yloc = torch.from_numpy(yfull[row0:row0 + nloc].copy()).to(dev)
     xloc = torch.empty_like(yloc)
 
-    h = ccg.ccg_create("c64", N, world=world, rank=rank, nccl_id=nccl_id, device=local_rank)
+    # N > 1: replicated vectors (SURVEY §8(f) NEXT-2 ii) — one collective per
+    # product and none per reduction phase
+    opts = ccg.OPT_REPLICATED if (world > 1 and not args.sharded_vectors) else 0
+    h = ccg.ccg_create("c64", N, world=world, rank=rank, nccl_id=nccl_id, device=local_rank, options=opts)
     ccg.ccg_set_matvec_dense(h, Ad, row0, nloc)
     stream = torch.cuda.ExternalStream(ccg.ccg_get_stream(h), device=dev)
 
@@ -337,7 +342,8 @@ def run_ccg(args):
                 "dtype": "c64", "data": "synthetic",
                 "config": {"workload": WORKLOAD, "n": N, "methods": list(METHODS), "tol": TOL,
                            "maxit": MAXIT, "iterations_per_step": its_total // args.steps,
-                           "parallelism": f"row-shard{world}",
+                           "parallelism": f"row-shard{world}" + (
+                               "+replicated-vectors" if world > 1 and not args.sharded_vectors else ""),
                            "l2": "A is 8.6 GB >> 126 MB L2: no flush needed"},
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": launches_total, "clocks": clocks}

@@ -145,6 +145,20 @@ int ccg_get_unique_id(uint8_t id[128]);
 int ccg_create(ccg_handle* h, ccg_dtype dt, int64_t n, int world, int rank,
                const uint8_t* nccl_id, int device, void* cuda_stream);
 
+/* ccg_create with options.  CCG_OPT_REPLICATED (world > 1; SURVEY §8(f)
+ * NEXT-2 ii): every rank keeps the WHOLE Krylov vectors (n elements; vector
+ * passes and dot products run redundantly and identically on every rank), the
+ * operator stays row-sharded.  A product then costs one collective — the
+ * allgather of its output rows (A·x), or of each rank's full-length partial,
+ * summed in rank order (dense Aᴴ·x) — and no reduction phase needs any
+ * collective: BiCGSTAB does 2 collectives per iteration instead of 2 input
+ * allgathers + 4 scalar allgathers.  The API is unchanged: vector arguments
+ * are still this rank's nloc-row slices.  Costs n·s per vector pass per rank
+ * (negligible against a dense row block). */
+enum { CCG_OPT_REPLICATED = 1 };
+int ccg_create_ex(ccg_handle* h, ccg_dtype dt, int64_t n, int world, int rank,
+                  const uint8_t* nccl_id, int device, void* cuda_stream, uint32_t options);
+
 /* Validation hook for the sharded path on ONE GPU: creates `world` (≥ 2)
  * handles hs[0..world-1] for ranks 0..world-1 of an n×n system on `device`,
  * wired to an in-process loopback communicator instead of NCCL (every
@@ -155,6 +169,9 @@ int ccg_create(ccg_handle* h, ccg_dtype dt, int64_t n, int world, int rank,
  * (same kernels, same row ownership); each is released with ccg_destroy.
  * On error no handle is left allocated. */
 int ccg_create_loopback_group(ccg_handle* hs, int world, ccg_dtype dt, int64_t n, int device);
+/* Same with ccg_create_ex options (e.g. CCG_OPT_REPLICATED). */
+int ccg_create_loopback_group_ex(ccg_handle* hs, int world, ccg_dtype dt, int64_t n, int device,
+                                 uint32_t options);
 
 /* Dense operator (matvec + cmatvec of a row-major matrix; P:95 [§5]).
  *   A_local : DEVICE pointer to this rank's rows, row-major, nloc × n with

@@ -34,7 +34,8 @@ MATVEC_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_int, ctypes
                              ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p)
 
 # every symbol include/ccg.h declares (checked by tests/test_abi.py)
-EXPORTS = ("ccg_get_unique_id", "ccg_create", "ccg_create_loopback_group",
+EXPORTS = ("ccg_get_unique_id", "ccg_create", "ccg_create_ex", "ccg_create_loopback_group",
+           "ccg_create_loopback_group_ex",
            "ccg_set_matvec_dense", "ccg_set_matvec_csr", "ccg_set_matvec_stencil7",
            "ccg_set_matvec_toeplitz3", "ccg_set_matvec_callback", "ccg_set_gmres_restart",
            "ccg_set_bicgstab_ell",
@@ -87,6 +88,10 @@ def load():
                                       ctypes.c_int, ctypes.c_char_p, ctypes.c_int, vp]),
         "ccg_create_loopback_group": (ctypes.c_int, [ctypes.POINTER(vp), ctypes.c_int, ctypes.c_int,
                                                      i64, ctypes.c_int]),
+        "ccg_create_ex": (ctypes.c_int, [ctypes.POINTER(vp), ctypes.c_int, i64, ctypes.c_int,
+                                         ctypes.c_int, ctypes.c_char_p, ctypes.c_int, vp, u32]),
+        "ccg_create_loopback_group_ex": (ctypes.c_int, [ctypes.POINTER(vp), ctypes.c_int, ctypes.c_int,
+                                                        i64, ctypes.c_int, u32]),
         "ccg_set_matvec_dense": (ctypes.c_int, [vp, vp, i64, i64, i64, u32]),
         "ccg_set_matvec_csr": (ctypes.c_int, [vp, vp, vp, vp, i64, i64, i64, u32]),
         "ccg_set_matvec_stencil7": (ctypes.c_int, [vp, i64, i64, i64, ctypes.POINTER(dbl), u32]),
@@ -165,20 +170,28 @@ def ccg_get_unique_id():
     return buf.raw
 
 
-def ccg_create(dtype, n, world=1, rank=0, nccl_id=None, device=0, stream=None):
+OPT_REPLICATED = 1
+
+
+def ccg_create(dtype, n, world=1, rank=0, nccl_id=None, device=0, stream=None, options=0):
     h = ctypes.c_void_p()
     sp = None if stream is None else ctypes.c_void_p(getattr(stream, "cuda_stream", stream))
-    rc = load().ccg_create(ctypes.byref(h), _dtype_code(dtype), int(n), int(world), int(rank),
-                           nccl_id, int(device), sp)
+    if options:
+        rc = load().ccg_create_ex(ctypes.byref(h), _dtype_code(dtype), int(n), int(world), int(rank),
+                                  nccl_id, int(device), sp, int(options))
+    else:
+        rc = load().ccg_create(ctypes.byref(h), _dtype_code(dtype), int(n), int(world), int(rank),
+                               nccl_id, int(device), sp)
     _check(None, rc)
     _keepalive[h.value] = []
     return h.value
 
 
-def ccg_create_loopback_group(world, dtype, n, device=0):
+def ccg_create_loopback_group(world, dtype, n, device=0, options=0):
     """`world` handles sharing an in-process loopback communicator (one GPU)."""
     hs = (ctypes.c_void_p * world)()
-    _check(None, load().ccg_create_loopback_group(hs, int(world), _dtype_code(dtype), int(n), int(device)))
+    _check(None, load().ccg_create_loopback_group_ex(hs, int(world), _dtype_code(dtype), int(n), int(device),
+                                                     int(options)))
     out = [hs[r] for r in range(world)]
     for h in out:
         _keepalive[h] = []

@@ -44,7 +44,11 @@ enum { GEMV_SPLIT = 0, GEMV_BULK = 1, GEMV_ROWS = 2, GEMV_COLS = 3 };
 
 struct ccg_ctx {
   int dtype = 0;
-  int64_t n = 0, nloc = 0, row0 = 0;
+  int64_t n = 0, nloc = 0, row0 = 0;   // vector slice of this rank (whole vector when rep)
+  int64_t mnloc = 0, mrow0 = 0;         // operator rows of this rank (= nloc, row0 unless rep)
+  bool rep = false;                     // replicated-vector mode (SURVEY §8(f) NEXT-2 ii)
+  void* rep_tmp = nullptr;              // n: product rows gathered from every rank
+  void* rep_parts = nullptr;            // world × n: Aᴴ partials of every rank
   int world = 1, rank = 0, device = 0;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
@@ -191,7 +195,7 @@ static Red make_red(ccg_ctx* c) {
   r.part = c->part;
   r.ticket = c->ticket;
   r.rank_sum = c->rank_sum;
-  r.fuse = c->world == 1 ? 1 : 0;
+  r.fuse = (c->world == 1 || c->rep) ? 1 : 0;   // replicated vectors: reductions are local
   return r;
 }
 
@@ -250,7 +254,7 @@ struct Engine {
 
   // -------------------- collectives --------------------
   static int allgather(ccg_ctx* c, int fi) {
-    if (c->world == 1) return CCG_OK;
+    if (c->world == 1 || c->rep) return CCG_OK;   // replicated vectors are whole on every rank
     C* buf = F(c, fi);
     if (c->opk == OPK_CSR || c->opk == OPK_STENCIL) return halo_exchange(c, buf);
     // dense and FFT-Toeplitz: every rank needs the whole input vector
@@ -266,7 +270,7 @@ struct Engine {
   static int post(ccg_ctx* c, const int* gate) {
     constexpr int K = Fin::K;
     if constexpr (K > 0) {
-      if (c->world > 1) {
+      if (c->world > 1 && !c->rep) {
         NK(c, c->comm->allgather(c->rank_sum, c->all_sums, (size_t)K * 2, CT_F64, c->stream));
         scalar_kernel<K, Fin><<<1, 1, 0, c->stream>>>(c->all_sums, c->world, c->st, gate);
         c->launches++;
@@ -299,14 +303,14 @@ struct Engine {
     const C* vals = reinterpret_cast<const C*>(c->vals);
     if (c->sell_col)
       spmv_sell_kernel<T, NT, CONJ, Epi><<<c->sell_grid, NT, 0, c->stream>>>(
-          c->sell_off, c->sell_width, c->sell_col, reinterpret_cast<const C*>(c->sell_val), x, c->nloc, epi,
+          c->sell_off, c->sell_width, c->sell_col, reinterpret_cast<const C*>(c->sell_val), x, c->mnloc, epi,
           make_red(c), c->st, gate);
     else if (c->csr_blocks)
       spmv_stream_kernel<T, NT, SNNZ, CONJ, Epi><<<c->spmv_grid, NT, 0, c->stream>>>(
           c->rowptr, c->colind, vals, x, c->csr_blocks, c->csr_nblocks, epi, make_red(c), c->st, gate);
     else
       spmv_csr_kernel<T, LPR, NT, CONJ, Epi><<<c->spmv_grid, NT, 0, c->stream>>>(
-          c->rowptr, c->colind, vals, x, c->nloc, epi, make_red(c), c->st, gate);
+          c->rowptr, c->colind, vals, x, c->mnloc, epi, make_red(c), c->st, gate);
   }
 
   // matrix-free stencil; conj => Aᴴ (= the stencil with conjugated
@@ -362,13 +366,25 @@ struct Engine {
   // method's epilogue as one fused pass over it
   template <class Epi>
   static int user_product(ccg_ctx* c, int op, const C* xfull, Epi epi, const int* gate) {
-    C* out = reinterpret_cast<C*>(c->cb_out);
+    C* out = c->rep ? reinterpret_cast<C*>(c->rep_tmp) : reinterpret_cast<C*>(c->cb_out);
     tev_begin(c, op == CCG_OP_A ? 0 : 1);
-    const int rc = c->cb_fn(c->cb_user, op, xfull, out, c->n, c->row0, c->nloc, c->stream);
+    const int rc = c->cb_fn(c->cb_user, op, xfull, c->rep ? out + c->mrow0 : out, c->n, c->mrow0, c->mnloc,
+                            c->stream);
     tev_end(c);
     if (rc != 0) FAIL(c, CCG_E_USER, "user matvec callback returned " + std::to_string(rc));
     CK(c, cudaGetLastError());
+    if (c->rep) NK(c, c->comm->allgather_inplace(out, (size_t)c->mnloc * 2, ndt(), c->stream));
     EpiPass<C, Epi> ep{epi, out};
+    return pass(c, ep, gate);
+  }
+
+  // replicated vectors: this rank's product rows (Store into rep_tmp at mrow0),
+  // allgathered, then the method epilogue as one pass over the whole vector
+  template <class Epi>
+  static int rep_finish_rows(ccg_ctx* c, Epi epi, const int* gate) {
+    C* tmp = reinterpret_cast<C*>(c->rep_tmp);
+    NK(c, c->comm->allgather_inplace(tmp, (size_t)c->mnloc * 2, ndt(), c->stream));
+    EpiPass<C, Epi> ep{epi, tmp};
     return pass(c, ep, gate);
   }
 
@@ -376,6 +392,16 @@ struct Engine {
   template <class Epi>
   static int matvec_a(ccg_ctx* c, const C* xfull, Epi epi, const int* gate) {
     if (c->opk == OPK_CALLBACK) return user_product(c, CCG_OP_A, xfull, epi, gate);
+    if (c->rep && c->opk != OPK_TOEPLITZ) {
+      TRY(matvec_rows(c, xfull, Store<T>{reinterpret_cast<C*>(c->rep_tmp) + c->mrow0}, gate));
+      return rep_finish_rows(c, epi, gate);
+    }
+    return matvec_rows(c, xfull, epi, gate);
+  }
+
+  // this rank's rows of A·x (all operators), epilogue per row
+  template <class Epi>
+  static int matvec_rows(ccg_ctx* c, const C* xfull, Epi epi, const int* gate) {
     tev_begin(c, 0);
     if (c->opk == OPK_TOEPLITZ) {
       toeplitz(c, xfull, 0, epi, gate);
@@ -389,40 +415,40 @@ struct Engine {
       if (c->split_strips == 1) {
         if (c->vec_ok)
           gemv_n_split<T, NT, SUR, true, true, Epi><<<g, NT, smem, c->stream>>>(
-              A, c->lda, xfull, c->n, c->nloc, c->split_W, part, epi, make_red(c), c->st, gate);
+              A, c->lda, xfull, c->n, c->mnloc, c->split_W, part, epi, make_red(c), c->st, gate);
         else
           gemv_n_split<T, NT, SUR, false, true, Epi><<<g, NT, smem, c->stream>>>(
-              A, c->lda, xfull, c->n, c->nloc, c->split_W, part, epi, make_red(c), c->st, gate);
+              A, c->lda, xfull, c->n, c->mnloc, c->split_W, part, epi, make_red(c), c->st, gate);
       } else {
         Store<T> none{nullptr};
         if (c->vec_ok && c->split_ur == 16)
           gemv_n_split<T, NT, 16, true, false, Store<T>><<<g, NT, smem, c->stream>>>(
-              A, c->lda, xfull, c->n, c->nloc, c->split_W, part, none, make_red(c), c->st, gate);
+              A, c->lda, xfull, c->n, c->mnloc, c->split_W, part, none, make_red(c), c->st, gate);
         else if (c->vec_ok && c->split_ur == 4)
           gemv_n_split<T, NT, 4, true, false, Store<T>><<<g, NT, smem, c->stream>>>(
-              A, c->lda, xfull, c->n, c->nloc, c->split_W, part, none, make_red(c), c->st, gate);
+              A, c->lda, xfull, c->n, c->mnloc, c->split_W, part, none, make_red(c), c->st, gate);
         else if (c->vec_ok)
           gemv_n_split<T, NT, SUR, true, false, Store<T>><<<g, NT, smem, c->stream>>>(
-              A, c->lda, xfull, c->n, c->nloc, c->split_W, part, none, make_red(c), c->st, gate);
+              A, c->lda, xfull, c->n, c->mnloc, c->split_W, part, none, make_red(c), c->st, gate);
         else
           gemv_n_split<T, NT, SUR, false, false, Store<T>><<<g, NT, smem, c->stream>>>(
-              A, c->lda, xfull, c->n, c->nloc, c->split_W, part, none, make_red(c), c->st, gate);
+              A, c->lda, xfull, c->n, c->mnloc, c->split_W, part, none, make_red(c), c->st, gate);
         c->launches++;
         CK(c, cudaGetLastError());
-        gemv_h_stage2<T, NT, Epi><<<c->nstage2_grid, NT, 0, c->stream>>>(part, c->split_strips, c->nloc, 0,
-                                                                          c->nloc, epi, make_red(c), c->st, gate);
+        gemv_h_stage2<T, NT, Epi><<<c->nstage2_grid, NT, 0, c->stream>>>(part, c->split_strips, c->mnloc, 0,
+                                                                          c->mnloc, epi, make_red(c), c->st, gate);
       }
     } else if (c->opk == OPK_DENSE && c->gemv_mode == GEMV_COLS && c->cols_ok) {
       C* part = reinterpret_cast<C*>(c->npart);
       if (c->cols_rg == 4)
         gemv_cols<T, NT, true, false, false, 4><<<dim3(c->cols_strips, c->cols_S), NT, 0, c->stream>>>(
-            reinterpret_cast<const C*>(c->A), c->lda, xfull, nullptr, c->nloc, c->n, part, nullptr, gate);
+            reinterpret_cast<const C*>(c->A), c->lda, xfull, nullptr, c->mnloc, c->n, part, nullptr, gate);
       else
         gemv_cols<T, NT, true, false, false, 1><<<dim3(c->cols_strips, c->cols_S), NT, 0, c->stream>>>(
-            reinterpret_cast<const C*>(c->A), c->lda, xfull, nullptr, c->nloc, c->n, part, nullptr, gate);
+            reinterpret_cast<const C*>(c->A), c->lda, xfull, nullptr, c->mnloc, c->n, part, nullptr, gate);
       c->launches++;
       CK(c, cudaGetLastError());
-      gemv_h_stage2<T, NT, Epi><<<c->nstage2_grid, NT, 0, c->stream>>>(part, c->cols_strips, c->nloc, 0, c->nloc,
+      gemv_h_stage2<T, NT, Epi><<<c->nstage2_grid, NT, 0, c->stream>>>(part, c->cols_strips, c->mnloc, 0, c->mnloc,
                                                                         epi, make_red(c), c->st, gate);
     } else if (c->opk == OPK_DENSE && c->gemv_mode == GEMV_BULK && c->bulk_ok) {
       constexpr size_t smem = bulk_smem_bytes<BR, BSTAGES>();
@@ -433,15 +459,15 @@ struct Engine {
         attr_set = true;
       }
       kern<<<c->bulk_grid, BULK_NT, smem, c->stream>>>(reinterpret_cast<const C*>(c->A), c->lda, xfull, c->n,
-                                                       c->nloc, epi, make_red(c), c->st, gate);
+                                                       c->mnloc, epi, make_red(c), c->st, gate);
     } else if (c->opk == OPK_DENSE) {
       const C* A = reinterpret_cast<const C*>(c->A);
       if (c->vec_ok)
         gemv_n_kernel<T, R, NT, true, Epi><<<c->gemv_grid, NT, 0, c->stream>>>(
-            A, c->lda, xfull, c->n, c->nloc, epi, make_red(c), c->st, gate);
+            A, c->lda, xfull, c->n, c->mnloc, epi, make_red(c), c->st, gate);
       else
         gemv_n_kernel<T, R, NT, false, Epi><<<c->gemv_grid, NT, 0, c->stream>>>(
-            A, c->lda, xfull, c->n, c->nloc, epi, make_red(c), c->st, gate);
+            A, c->lda, xfull, c->n, c->mnloc, epi, make_red(c), c->st, gate);
     } else {
       spmv<false>(c, xfull, epi, gate);
     }
@@ -451,12 +477,16 @@ struct Engine {
     return post<Epi>(c, gate);
   }
 
-  // y_local = op(A) · x_local, op = Aᴴ (conj) or Aᵀ
+  // y_local = op(A) · x_local, op = Aᴴ (conj) or Aᵀ.  With replicated vectors
+  // x_local is the whole vector: complex-symmetric operators compute their own
+  // rows, the dense product this rank's full-length partial, summed over ranks
+  // in rank order inside the epilogue pass.
   template <class Epi>
   static int matvec_h(ccg_ctx* c, const C* xloc, bool conj, Epi epi, const int* gate) {
+    const bool gathered_in = c->world > 1 && !c->rep;   // the input needs gathering first
     if (c->opk == OPK_CALLBACK) {
       const C* xin = xloc;
-      if (c->world > 1) {
+      if (gathered_in) {
         CK(c, cudaMemcpyAsync(Fs(c, 2), xloc, c->nloc * sizeof(C), cudaMemcpyDeviceToDevice, c->stream));
         TRY(allgather(c, 2));
         xin = F(c, 2);
@@ -465,7 +495,7 @@ struct Engine {
     }
     if (c->opk == OPK_TOEPLITZ) {
       const C* xin = xloc;
-      if (c->world > 1) {
+      if (gathered_in) {
         CK(c, cudaMemcpyAsync(Fs(c, 2), xloc, c->nloc * sizeof(C), cudaMemcpyDeviceToDevice, c->stream));
         TRY(allgather(c, 2));
         xin = F(c, 2);
@@ -477,48 +507,44 @@ struct Engine {
       CK(c, cudaGetLastError());
       return post<Epi>(c, gate);
     }
-    if (c->opk == OPK_STENCIL) {
-      // complex-symmetric stencil: Aᵀ = A, Aᴴ = conj-coefficient stencil; the
-      // local input goes through full[2] for the halo planes
+    if (c->opk == OPK_STENCIL || c->opk == OPK_CSR) {
+      // complex-symmetric operator: Aᵀ = A, Aᴴx = conj(A conj x) (the stencil
+      // conjugates its coefficients); its own rows from the whole input
       const C* xin = xloc;
-      if (c->world > 1) {
+      if (gathered_in) {
         CK(c, cudaMemcpyAsync(Fs(c, 2), xloc, c->nloc * sizeof(C), cudaMemcpyDeviceToDevice, c->stream));
         TRY(allgather(c, 2));
         xin = F(c, 2);
       }
+      auto launch = [&](auto e) {
+        if (c->opk == OPK_STENCIL) stencil(c, xin, conj, e, gate);
+        else if (conj) spmv<true>(c, xin, e, gate);
+        else spmv<false>(c, xin, e, gate);
+      };
       tev_begin(c, 1);
-      stencil(c, xin, conj, epi, gate);
+      if (c->rep) launch(Store<T>{reinterpret_cast<C*>(c->rep_tmp) + c->mrow0});
+      else launch(epi);
       c->launches++;
       tev_end(c);
       CK(c, cudaGetLastError());
-      return post<Epi>(c, gate);
-    }
-    if (c->opk == OPK_CSR) {
-      // complex-symmetric CSR, single GPU: Aᴴx = conj(A conj x), Aᵀx = A x
-      tev_begin(c, 1);
-      if (conj)
-        spmv<true>(c, xloc, epi, gate);
-      else
-        spmv<false>(c, xloc, epi, gate);
-      c->launches++;
-      tev_end(c);
-      CK(c, cudaGetLastError());
+      if (c->rep) return rep_finish_rows(c, epi, gate);
       return post<Epi>(c, gate);
     }
     const C* A = reinterpret_cast<const C*>(c->A);
     C* part = reinterpret_cast<C*>(c->hpart);
+    const C* xr = c->rep ? xloc + c->mrow0 : xloc;   // the x entries of this rank's rows
     dim3 g1(c->ah_strips, c->ah_S);
     tev_begin(c, 1);
     if (c->vec_ok) {
       if (conj)
-        gemv_h_stage1<T, true, NT, UR, true><<<g1, NT, 0, c->stream>>>(A, c->lda, xloc, c->nloc, c->n, part, gate);
+        gemv_h_stage1<T, true, NT, UR, true><<<g1, NT, 0, c->stream>>>(A, c->lda, xr, c->mnloc, c->n, part, gate);
       else
-        gemv_h_stage1<T, false, NT, UR, true><<<g1, NT, 0, c->stream>>>(A, c->lda, xloc, c->nloc, c->n, part, gate);
+        gemv_h_stage1<T, false, NT, UR, true><<<g1, NT, 0, c->stream>>>(A, c->lda, xr, c->mnloc, c->n, part, gate);
     } else {
       if (conj)
-        gemv_h_stage1<T, true, NT, UR, false><<<g1, NT, 0, c->stream>>>(A, c->lda, xloc, c->nloc, c->n, part, gate);
+        gemv_h_stage1<T, true, NT, UR, false><<<g1, NT, 0, c->stream>>>(A, c->lda, xr, c->mnloc, c->n, part, gate);
       else
-        gemv_h_stage1<T, false, NT, UR, false><<<g1, NT, 0, c->stream>>>(A, c->lda, xloc, c->nloc, c->n, part, gate);
+        gemv_h_stage1<T, false, NT, UR, false><<<g1, NT, 0, c->stream>>>(A, c->lda, xr, c->mnloc, c->n, part, gate);
     }
     c->launches++;
     CK(c, cudaGetLastError());
@@ -530,14 +556,22 @@ struct Engine {
       CK(c, cudaGetLastError());
       return CCG_OK;
     }
-    // multi GPU: full-length partial of this rank -> reduce-scatter -> epilogue pass
-    Store<T> stv{reinterpret_cast<C*>(c->wfull)};
+    // multi GPU: full-length partial of this rank
+    C* wf = c->rep ? reinterpret_cast<C*>(c->rep_tmp) : reinterpret_cast<C*>(c->wfull);
+    Store<T> stv{wf};
     gemv_h_stage2<T, NT, Store<T>><<<c->stage2_grid, NT, 0, c->stream>>>(part, c->ah_S, c->n, 0, c->n, stv,
                                                                          make_red(c), c->st, gate);
     c->launches++;
     tev_end(c);
     CK(c, cudaGetLastError());
-    C* wl = L(c, NLOCAL - 1);
+    if (c->rep) {
+      // every rank's partial, summed in rank order inside the epilogue pass
+      C* parts = reinterpret_cast<C*>(c->rep_parts);
+      NK(c, c->comm->allgather(wf, parts, (size_t)c->n * 2, ndt(), c->stream));
+      EpiPassSum<C, Epi> ep{epi, parts, c->world, c->n};
+      return pass(c, ep, gate);
+    }
+    C* wl = L(c, NLOCAL - 1);   // row-sharded: reduce-scatter -> epilogue pass
     NK(c, c->comm->reduce_scatter(c->wfull, wl, (size_t)c->nloc * 2, ndt(), c->stream));
     EpiPass<C, Epi> ep{epi, wl};
     return pass(c, ep, gate);
@@ -633,7 +667,7 @@ struct Engine {
     const int* g = &c->st->done;
     TRY(pass(c, QmP<T>{L(c, 5), L(c, 6), Fs(c, 0), L(c, 7)}, g));
     TRY(allgather(c, 0));
-    if (c->opk == OPK_DENSE && c->cols_ok && c->qmr_dual) {
+    if (c->opk == OPK_DENSE && c->cols_ok && c->qmr_dual && !c->rep) {
       TRY(matvec_dual(c, F(c, 0), L(c, 7), QmPt<T>{L(c, 8), L(c, 7)},
                       QmVW<T>{L(c, 3), L(c, 4), L(c, 8), L(c, 5), L(c, 6)}, g));
     } else {
@@ -779,7 +813,7 @@ struct Engine {
   // A·p and Aᴴ·p̃ of one BiCG iteration are independent: dual GEMV when dense
   template <class EpiA, class EpiH>
   static int matvec_pair(ccg_ctx* c, int pfull_idx, const C* qloc, EpiA ea, EpiH eh, const int* gate) {
-    if (c->opk == OPK_DENSE && c->cols_ok && c->qmr_dual)
+    if (c->opk == OPK_DENSE && c->cols_ok && c->qmr_dual && !c->rep)
       return matvec_dual(c, F(c, pfull_idx), qloc, ea, eh, gate);
     TRY(matvec_a(c, F(c, pfull_idx), ea, gate));
     return matvec_h(c, qloc, true, eh, gate);
@@ -856,7 +890,7 @@ struct Engine {
   static C* Vb(ccg_ctx* c) { return reinterpret_cast<C*>(c->gm_V); }
   template <int MODE>
   static int gm_pass_launch(ccg_ctx* c, C* w, const double2* coef, double2* dst, const int* gate) {
-    const bool fuse = c->world == 1;
+    const bool fuse = c->world == 1 || c->rep;
     gm_pass<T, MODE><<<c->gm_grid, GM_NT, 0, c->stream>>>(Vb(c), c->nloc, w, coef, fuse ? dst : c->gm_rank, c->nloc,
                                                            c->gm_dev, c->gm_part, c->gm_ticket, fuse ? 1 : 0, gate);
     c->launches++;
@@ -908,7 +942,7 @@ struct Engine {
   static C* BRs(ccg_ctx* c, int a) { return BLR(c, a) + c->row0; }
   static C* BUs(ccg_ctx* c, int a) { return BLU(c, a) + c->row0; }
   static int allgather_buf(ccg_ctx* c, C* buf) {
-    if (c->world == 1) return CCG_OK;
+    if (c->world == 1 || c->rep) return CCG_OK;
     if (c->opk == OPK_CSR || c->opk == OPK_STENCIL) return halo_exchange(c, buf);
     NK(c, c->comm->allgather_inplace(buf, (size_t)c->nloc * 2, ndt(), c->stream));
     return CCG_OK;
@@ -1044,12 +1078,12 @@ static int choose_launch(ccg_ctx* c) {
   else
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gemv_n_kernel<T, E::R, E::NT, false, Store<T>>, NT, 0);
   if (occ < 1) occ = 1;
-  const int64_t groups = (c->nloc + E::R - 1) / E::R;
+  const int64_t groups = (c->mnloc + E::R - 1) / E::R;
   c->gemv_grid = (int)std::max<int64_t>(1, std::min<int64_t>(groups, (int64_t)c->sm_count * occ));
   c->bulk_ok = c->opk == OPK_DENSE && getenv("CCG_NO_BULK") == nullptr &&
                ((c->n * (int64_t)sizeof(C)) % BULK_TILE == 0) && ((c->lda * (int64_t)sizeof(C)) % 16 == 0) &&
                (((uintptr_t)c->A) % 16 == 0);
-  c->bulk_grid = (int)std::max<int64_t>(1, std::min<int64_t>((c->nloc + E::BR - 1) / E::BR, c->sm_count));
+  c->bulk_grid = (int)std::max<int64_t>(1, std::min<int64_t>((c->mnloc + E::BR - 1) / E::BR, c->sm_count));
   {
     const char* gm = getenv("CCG_GEMV");
     c->gemv_mode = (gm && !strcmp(gm, "bulk"))   ? GEMV_BULK
@@ -1077,14 +1111,14 @@ static int choose_launch(ccg_ctx* c) {
     const char* wv = getenv("CCG_COLS_WAVES");
     const int64_t waves = wv ? std::max(1, atoi(wv)) : 2;
     int64_t Sn = std::max<int64_t>(1, (waves * slots_c) / c->cols_strips);
-    c->cols_S = (int)std::min<int64_t>(Sn, std::max<int64_t>(1, c->nloc / 8));
+    c->cols_S = (int)std::min<int64_t>(Sn, std::max<int64_t>(1, c->mnloc / 8));
     int occd = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occd, gemv_cols<T, E::NT, true, true, true>, NT, 0);
     if (occd < 1) occd = 1;
-    c->dual_S = (int)pick_splits(c->cols_strips, (int64_t)c->sm_count * occd, c->nloc / 16);
+    c->dual_S = (int)pick_splits(c->cols_strips, (int64_t)c->sm_count * occd, c->mnloc / 16);
     c->nstage2_grid =
-        (int)std::max<int64_t>(1, std::min<int64_t>((c->nloc + NT - 1) / NT, (int64_t)c->sm_count * 4));
-    size_t need = (size_t)c->cols_strips * c->nloc * sizeof(C);
+        (int)std::max<int64_t>(1, std::min<int64_t>((c->mnloc + NT - 1) / NT, (int64_t)c->sm_count * 4));
+    size_t need = (size_t)c->cols_strips * c->mnloc * sizeof(C);
     if (need > c->npart_bytes) {
       if (c->npart) cudaFree(c->npart);
       c->npart = nullptr;
@@ -1116,13 +1150,13 @@ static int choose_launch(ccg_ctx* c) {
     int64_t nrb = 1;
     for (int k = max_waves; k >= 1; --k) {
       nrb = std::max<int64_t>(1, (k * slots) / c->split_strips);
-      if (c->nloc / nrb >= 64 || k == 1) break;
+      if (c->mnloc / nrb >= 64 || k == 1) break;
     }
-    nrb = std::min<int64_t>(nrb, std::max<int64_t>(1, c->nloc / 8));
+    nrb = std::min<int64_t>(nrb, std::max<int64_t>(1, c->mnloc / 8));
     c->split_nrb = (int)nrb;
     c->nstage2_grid =
-        (int)std::max<int64_t>(1, std::min<int64_t>((c->nloc + NT - 1) / NT, (int64_t)c->sm_count * 4));
-    size_t need = c->split_strips > 1 ? (size_t)c->split_strips * c->nloc * sizeof(C) : 0;
+        (int)std::max<int64_t>(1, std::min<int64_t>((c->mnloc + NT - 1) / NT, (int64_t)c->sm_count * 4));
+    size_t need = c->split_strips > 1 ? (size_t)c->split_strips * c->mnloc * sizeof(C) : 0;
     if (need > c->npart_bytes) {
       if (c->npart) cudaFree(c->npart);
       c->npart = nullptr;
@@ -1140,17 +1174,17 @@ static int choose_launch(ccg_ctx* c) {
   const int64_t slots = (int64_t)c->sm_count * occ1;
   int64_t S = slots / c->ah_strips;
   S = std::max<int64_t>(1, std::min<int64_t>(S, 128));
-  S = std::min<int64_t>(S, std::max<int64_t>(1, c->nloc / 16));
+  S = std::min<int64_t>(S, std::max<int64_t>(1, c->mnloc / 16));
   c->ah_S = (int)S;
   c->stage2_grid = (int)std::max<int64_t>(1, std::min<int64_t>((c->n + NT - 1) / NT, (int64_t)c->sm_count * 4));
   c->pass_grid = (int)std::max<int64_t>(1, std::min<int64_t>((c->nloc + NT - 1) / NT, (int64_t)c->sm_count * 8));
   c->spmv_grid = (int)std::max<int64_t>(
-      1, std::min<int64_t>((c->nloc + NT / E::LPR - 1) / (NT / E::LPR), (int64_t)c->sm_count * 8));
+      1, std::min<int64_t>((c->mnloc + NT / E::LPR - 1) / (NT / E::LPR), (int64_t)c->sm_count * 8));
   if (c->sell_col) {
     int occ4 = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ4, spmv_sell_kernel<T, E::NT, false, Store<T>>, NT, 0);
     if (occ4 < 1) occ4 = 1;
-    const int64_t thr = ((c->nloc + 31) / 32) * 32;
+    const int64_t thr = ((c->mnloc + 31) / 32) * 32;
     c->sell_grid = (int)std::max<int64_t>(1, std::min<int64_t>((thr + NT - 1) / NT, (int64_t)c->sm_count * occ4));
   }
   if (c->csr_blocks) {
@@ -1343,7 +1377,7 @@ int ccg_get_unique_id(uint8_t id[128]) {
 }
 
 static int create_impl(ccg_handle* h, ccg_dtype dt, int64_t n, int world, int rank, const uint8_t* nccl_id,
-                       int device, void* cuda_stream, LoopbackGroup* lg) {
+                       int device, void* cuda_stream, LoopbackGroup* lg, uint32_t options = 0) {
   if (!h) { g_create_err = "h is NULL"; return CCG_E_ARG; }
   *h = nullptr;
   if (dt != CCG_C64 && dt != CCG_C128) { g_create_err = "bad dtype"; return CCG_E_ARG; }
@@ -1364,8 +1398,11 @@ static int create_impl(ccg_handle* h, ccg_dtype dt, int64_t n, int world, int ra
   c->n = n;
   c->world = world;
   c->rank = rank;
-  c->nloc = n / world;
-  c->row0 = (int64_t)rank * c->nloc;
+  c->mnloc = n / world;
+  c->mrow0 = (int64_t)rank * c->mnloc;
+  c->rep = world > 1 && (options & CCG_OPT_REPLICATED);
+  c->nloc = c->rep ? n : c->mnloc;      // vectors: whole (replicated) or this rank's slice
+  c->row0 = c->rep ? 0 : c->mrow0;
   c->device = device;
   auto bail = [&](int code) {
     g_create_err = c->err;
@@ -1406,6 +1443,10 @@ static int create_impl(ccg_handle* h, ccg_dtype dt, int64_t n, int world, int ra
     CKC(cudaMalloc(&c->full[i], (size_t)n * c->esz));
     CKC(cudaMemset(c->full[i], 0, (size_t)n * c->esz));
   }
+  if (c->rep) {
+    CKC(cudaMalloc(&c->rep_tmp, (size_t)n * c->esz));
+    CKC(cudaMalloc(&c->rep_parts, (size_t)n * world * c->esz));
+  }
   if (world > 1) {
     CKC(cudaMalloc(&c->wfull, (size_t)n * c->esz));
     if (lg) {
@@ -1431,14 +1472,24 @@ int ccg_create(ccg_handle* h, ccg_dtype dt, int64_t n, int world, int rank, cons
   return create_impl(h, dt, n, world, rank, nccl_id, device, cuda_stream, nullptr);
 }
 
+int ccg_create_ex(ccg_handle* h, ccg_dtype dt, int64_t n, int world, int rank, const uint8_t* nccl_id, int device,
+                  void* cuda_stream, uint32_t options) {
+  return create_impl(h, dt, n, world, rank, nccl_id, device, cuda_stream, nullptr, options);
+}
+
+int ccg_create_loopback_group_ex(ccg_handle* hs, int world, ccg_dtype dt, int64_t n, int device, uint32_t options);
 int ccg_create_loopback_group(ccg_handle* hs, int world, ccg_dtype dt, int64_t n, int device) {
+  return ccg_create_loopback_group_ex(hs, world, dt, n, device, 0);
+}
+
+int ccg_create_loopback_group_ex(ccg_handle* hs, int world, ccg_dtype dt, int64_t n, int device, uint32_t options) {
   if (!hs || world < 2) { g_create_err = "hs is NULL or world < 2"; return CCG_E_ARG; }
   LoopbackGroup* lg = new LoopbackGroup(world);
   lg->refs = 1;  // held until every handle exists
   int rc = CCG_OK;
   int made = 0;
   for (int r = 0; r < world; ++r) {
-    rc = create_impl(&hs[r], dt, n, world, r, nullptr, device, nullptr, lg);
+    rc = create_impl(&hs[r], dt, n, world, r, nullptr, device, nullptr, lg, options);
     if (rc) break;
     made++;
   }
@@ -1457,7 +1508,7 @@ int ccg_create_loopback_group(ccg_handle* hs, int world, ccg_dtype dt, int64_t n
 int ccg_set_matvec_dense(ccg_handle c, const void* A_local, int64_t row0, int64_t nloc, int64_t lda, uint32_t flags) {
   if (!c) return CCG_E_ARG;
   if (!A_local) FAIL(c, CCG_E_ARG, "A_local is NULL");
-  if (row0 != c->row0 || nloc != c->nloc) FAIL(c, CCG_E_DIM, "row0/nloc differ from the handle's row range");
+  if (row0 != c->mrow0 || nloc != c->mnloc) FAIL(c, CCG_E_DIM, "row0/nloc differ from the handle's row range");
   if (lda < c->n) FAIL(c, CCG_E_DIM, "lda < n");
   if (!is_device_ptr(A_local)) FAIL(c, CCG_E_ARG, "A_local must be a device pointer");
   if (((uintptr_t)A_local) % c->esz) FAIL(c, CCG_E_ARG, "A_local misaligned");
@@ -1484,7 +1535,7 @@ int ccg_set_matvec_csr(ccg_handle c, const int32_t* rowptr, const int32_t* colin
                        int64_t nloc, int64_t nnz_local, uint32_t flags) {
   if (!c) return CCG_E_ARG;
   if (!rowptr || !colind || !vals) FAIL(c, CCG_E_ARG, "NULL CSR pointer");
-  if (row0 != c->row0 || nloc != c->nloc) FAIL(c, CCG_E_DIM, "row0/nloc differ from the handle's row range");
+  if (row0 != c->mrow0 || nloc != c->mnloc) FAIL(c, CCG_E_DIM, "row0/nloc differ from the handle's row range");
   if (nnz_local < 0 || nnz_local > INT32_MAX) FAIL(c, CCG_E_DIM, "nnz out of range");
   if (!is_device_ptr(rowptr) || !is_device_ptr(colind) || !is_device_ptr(vals))
     FAIL(c, CCG_E_ARG, "CSR arrays must be device pointers");
@@ -1504,8 +1555,9 @@ int ccg_set_matvec_csr(ccg_handle c, const int32_t* rowptr, const int32_t* colin
       if (j >= row0 + nloc) halo = std::max<int64_t>(halo, j - (row0 + nloc) + 1);
     }
   }
-  if (c->world > 1 && halo > nloc) FAIL(c, CCG_E_ARG, "CSR columns reach beyond the neighbour ranks (halo > nloc)");
-  if (c->world > 1) {
+  if (c->world > 1 && !c->rep && halo > nloc)
+    FAIL(c, CCG_E_ARG, "CSR columns reach beyond the neighbour ranks (halo > nloc)");
+  if (c->world > 1 && !c->rep) {
     // all ranks use the same (maximum) halo width so that sends match receives
     int64_t* dh = nullptr;
     CK(c, cudaMalloc(&dh, sizeof(int64_t) * c->world));
@@ -1672,7 +1724,7 @@ int ccg_set_matvec_callback(ccg_handle c, ccg_matvec_fn fn, void* user, uint32_t
   if (!(caps & CCG_CB_A)) FAIL(c, CCG_E_ARG, "caps must include CCG_CB_A");
   CK(c, cudaSetDevice(c->device));
   free_csr_copies(c);
-  CK(c, cudaMalloc(&c->cb_out, (size_t)std::max<int64_t>(c->nloc, 1) * c->esz));
+  CK(c, cudaMalloc(&c->cb_out, (size_t)std::max<int64_t>(c->mnloc, 1) * c->esz));
   c->opk = OPK_CALLBACK;
   c->cb_fn = fn;
   c->cb_user = user;
@@ -1760,6 +1812,23 @@ static int stage_out(ccg_ctx* c, void* dst, const void* src, size_t bytes) {
   return CCG_OK;
 }
 
+// user vector slices (this rank's mnloc rows) <-> library vectors; with
+// replicated vectors the slice sits at mrow0 and is allgathered in place
+static int vec_in(ccg_ctx* c, void* dst, const void* src) {
+  const size_t bytes = (size_t)c->mnloc * c->esz;
+  char* d = static_cast<char*>(dst) + (c->rep ? (size_t)c->mrow0 * c->esz : 0);
+  TRY(stage_in(c, d, src, bytes));
+  if (c->rep) {
+    const int r = c->comm->allgather_inplace(dst, (size_t)c->mnloc * 2, c->esz == 8 ? CT_F32 : CT_F64, c->stream);
+    if (r) FAIL(c, r, c->comm->err);
+  }
+  return CCG_OK;
+}
+static int vec_out(ccg_ctx* c, void* dst, const void* src) {
+  const char* s = static_cast<const char*>(src) + (c->rep ? (size_t)c->mrow0 * c->esz : 0);
+  return stage_out(c, dst, s, (size_t)c->mnloc * c->esz);
+}
+
 static bool needs_ah(int m) {
   return m == CCG_CGNE || m == CCG_QMR || m == CCG_BICOR || m == CCG_BICG || m == CCG_CGNR;
 }
@@ -1769,23 +1838,22 @@ int ccg_apply(ccg_handle c, ccg_op op, const void* x_local, void* y_local) {
   if (!x_local || !y_local) FAIL(c, CCG_E_ARG, "NULL vector");
   if (op != CCG_OP_A && op != CCG_OP_AH && op != CCG_OP_AT) FAIL(c, CCG_E_ARG, "bad op");
   if (c->opk == OPK_NONE) FAIL(c, CCG_E_STATE, "no operator set (call ccg_set_matvec_*)");
-  if (c->opk == OPK_CSR && op != CCG_OP_A && (!(c->flags & CCG_FLAG_SYMMETRIC) || c->world > 1))
-    FAIL(c, CCG_E_CAPABILITY, "CSR Aᴴ/Aᵀ needs CCG_FLAG_SYMMETRIC and world == 1");
+  if (c->opk == OPK_CSR && op != CCG_OP_A && (!(c->flags & CCG_FLAG_SYMMETRIC) || (c->world > 1 && !c->rep)))
+    FAIL(c, CCG_E_CAPABILITY, "CSR Aᴴ/Aᵀ needs CCG_FLAG_SYMMETRIC and world == 1 (or replicated vectors)");
   if (c->opk == OPK_CALLBACK && !(c->cb_caps & (op == CCG_OP_A ? CCG_CB_A : op == CCG_OP_AH ? CCG_CB_AH : CCG_CB_AT)))
     FAIL(c, CCG_E_CAPABILITY, "the user callback does not provide this product");
   CK(c, cudaSetDevice(c->device));
   c->launches = 0;
   c->ms_a = c->ms_ah = 0;
   c->n_a = c->n_ah = 0;
-  const size_t bytes = (size_t)c->nloc * c->esz;
   void* xin = c->loc[3];
   void* yout = c->loc[4];
-  TRY(stage_in(c, xin, x_local, bytes));
+  TRY(vec_in(c, xin, x_local));
   int rc = c->dtype == CCG_C64
                ? Engine<float>::apply(c, op, (const float2*)xin, (float2*)yout)
                : Engine<double>::apply(c, op, (const double2*)xin, (double2*)yout);
   if (rc) return rc;
-  TRY(stage_out(c, y_local, yout, bytes));
+  TRY(vec_out(c, y_local, yout));
   CK(c, cudaStreamSynchronize(c->stream));
   tev_collect(c);
   return CCG_OK;
@@ -1799,7 +1867,7 @@ int ccg_solve(ccg_handle c, ccg_method method, const void* x0_local, const void*
   if ((int)method < 0 || (int)method >= M_COUNT) FAIL(c, CCG_E_ARG, "bad method");
   if (!(tol >= 0.0) || maxit < 1) FAIL(c, CCG_E_ARG, "tol must be >= 0 and maxit >= 1");
   if (c->opk == OPK_NONE) FAIL(c, CCG_E_STATE, "no operator set (call ccg_set_matvec_*)");
-  if (needs_ah(method) && c->opk == OPK_CSR && (!(c->flags & CCG_FLAG_SYMMETRIC) || c->world > 1))
+  if (needs_ah(method) && c->opk == OPK_CSR && (!(c->flags & CCG_FLAG_SYMMETRIC) || (c->world > 1 && !c->rep)))
     FAIL(c, CCG_E_CAPABILITY, "method needs Aᴴ; CSR provides it only with CCG_FLAG_SYMMETRIC and world == 1");
   if (c->opk == OPK_CALLBACK && (!(c->cb_caps & CCG_CB_A) || (needs_ah(method) && !(c->cb_caps & CCG_CB_AH))))
     FAIL(c, CCG_E_CAPABILITY, "the user callback does not provide the products this method needs");
@@ -1807,7 +1875,7 @@ int ccg_solve(ccg_handle c, ccg_method method, const void* x0_local, const void*
   c->launches = 0;
   c->ms_a = c->ms_ah = 0;
   c->n_a = c->n_ah = 0;
-  const size_t bytes = (size_t)c->nloc * c->esz;
+  const size_t bytes = (size_t)c->nloc * c->esz;   // library vectors (whole when replicated)
   // history buffer
   if (maxit + 1 > c->hist_cap) {
     if (c->hist) cudaFree(c->hist);
@@ -1835,9 +1903,9 @@ int ccg_solve(ccg_handle c, ccg_method method, const void* x0_local, const void*
   *c->st_host = s0;
   CK(c, cudaMemcpyAsync(c->st, c->st_host, sizeof(State), cudaMemcpyHostToDevice, c->stream));
   // inputs: x -> loc[0], y -> loc[1]
-  TRY(stage_in(c, c->loc[1], y_local, bytes));
+  TRY(vec_in(c, c->loc[1], y_local));
   if (x0_local) {
-    TRY(stage_in(c, c->loc[0], x0_local, bytes));
+    TRY(vec_in(c, c->loc[0], x0_local));
   } else {
     CK(c, cudaMemsetAsync(c->loc[0], 0, bytes, c->stream));
   }
@@ -1860,7 +1928,7 @@ int ccg_solve(ccg_handle c, ccg_method method, const void* x0_local, const void*
     if (rc) return rc;
   }
   CK(c, cudaMemcpyAsync(c->st_host, c->st, sizeof(State), cudaMemcpyDeviceToHost, c->stream));
-  TRY(stage_out(c, x_local_out, c->loc[0], bytes));
+  TRY(vec_out(c, x_local_out, c->loc[0]));
   CK(c, cudaStreamSynchronize(c->stream));
   tev_collect(c);
   const State& s = *c->st_host;
@@ -1929,6 +1997,8 @@ int ccg_destroy(ccg_handle c) {
   for (int i = 0; i < NLOCAL; ++i) if (c->loc[i]) cudaFree(c->loc[i]);
   for (int i = 0; i < NFULL; ++i) if (c->full[i]) cudaFree(c->full[i]);
   if (c->wfull) cudaFree(c->wfull);
+  if (c->rep_tmp) cudaFree(c->rep_tmp);
+  if (c->rep_parts) cudaFree(c->rep_parts);
   if (c->hpart) cudaFree(c->hpart);
   if (c->npart) cudaFree(c->npart);
   free_csr_copies(c);

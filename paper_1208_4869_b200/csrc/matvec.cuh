@@ -915,6 +915,26 @@ struct EpiPass {
   static __device__ void finish(State* st, const double2* s) { Epi::finish(st, s); }
 };
 
+// replicated vectors: the epilogue over Σ_ranks parts[r][i] (rank order, fp64)
+template <typename C, class Epi>
+struct EpiPassSum {
+  static constexpr int K = Epi::K;
+  Epi epi;
+  const C* parts;
+  int world;
+  int64_t n;
+  __device__ void load(const State* st) { epi.load(st); }
+  __device__ void operator()(int64_t i, double2* acc) {
+    double2 s = make_double2(0.0, 0.0);
+    for (int r = 0; r < world; ++r) {
+      const C p = parts[(int64_t)r * n + i];
+      s.x += (double)p.x; s.y += (double)p.y;
+    }
+    epi(i, fromd2<C>(s), acc);
+  }
+  static __device__ void finish(State* st, const double2* s) { Epi::finish(st, s); }
+};
+
 // multi-GPU scalar step: sum the world×K allgathered rank sums in rank order
 template <int K, class Fin>
 __global__ void scalar_kernel(const double2* all, int world, State* st, const int* gate) {

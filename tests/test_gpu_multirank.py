@@ -43,13 +43,13 @@ def _threads(G, fn):
 
 
 class DenseGroup:
-    def __init__(self, A, G):
+    def __init__(self, A, G, options=0):
         self.n = A.shape[0]
         self.G = G
         self.nloc = self.n // G
         self.dtype = A.dtype.type
         self.dt = "c64" if self.dtype == np.complex64 else "c128"
-        self.hs = ccg.ccg_create_loopback_group(G, self.dt, self.n)
+        self.hs = ccg.ccg_create_loopback_group(G, self.dt, self.n, options=options)
         self.parts = [to_dev(A[r * self.nloc:(r + 1) * self.nloc]) for r in range(G)]
         for r in range(G):
             ccg.ccg_set_matvec_dense(self.hs[r], self.parts[r], r * self.nloc, self.nloc, lda=self.n)
@@ -85,12 +85,12 @@ class DenseGroup:
 
 
 class CsrGroup(DenseGroup):
-    def __init__(self, N, G, flags=0):
+    def __init__(self, N, G, flags=0, options=0):
         self.n = N ** 3
         self.G = G
         self.nloc = self.n // G
         self.dtype = np.complex128
-        self.hs = ccg.ccg_create_loopback_group(G, "c128", self.n)
+        self.hs = ccg.ccg_create_loopback_group(G, "c128", self.n, options=options)
         zs = N // G
         self.keep = []
         parts = [helmholtz_csr(N, kh=10 / 128, z0=r * zs, z1=(r + 1) * zs) for r in range(G)]
@@ -183,12 +183,12 @@ def test_sharded_csr_apply_and_solve(G):
 
 
 class StencilGroup(DenseGroup):
-    def __init__(self, nx, ny, nz, G, coeffs):
+    def __init__(self, nx, ny, nz, G, coeffs, options=0):
         self.n = nx * ny * nz
         self.G = G
         self.nloc = self.n // G
         self.dtype = np.complex128
-        self.hs = ccg.ccg_create_loopback_group(G, "c128", self.n)
+        self.hs = ccg.ccg_create_loopback_group(G, "c128", self.n, options=options)
         for r in range(G):
             ccg.ccg_set_matvec_stencil7(self.hs[r], nx, ny, nz, *coeffs)
 
@@ -250,5 +250,95 @@ def test_sharded_toeplitz(G):
             assert r["status"] == "CONVERGED" and abs(r["iterations"] - o.iterations) <= 2, m
             k = min(r["iterations"], o.iterations)
             assert relerr(g.solve(m, y, 0.0, k)["x"], oracle.solve(m, op, y, 0.0, k).x) <= 1e-9, m
+    finally:
+        g.close()
+
+
+
+# ---------------------------------------------------------------------------
+# Replicated-vector mode (CCG_OPT_REPLICATED; SURVEY §8(f) NEXT-2 ii): whole
+# vectors on every rank, row-sharded operator, one collective per product
+# ---------------------------------------------------------------------------
+ALL12 = ["bicgstab", "cgne", "qmr", "bicor", "cors", "bicg", "cgs", "cocr", "cgnr", "tfqmr", "gmres", "bicgstabl"]
+
+
+@pytest.mark.parametrize("G", [2, 4])
+@pytest.mark.parametrize("dtype", [np.complex128, np.complex64])
+def test_replicated_dense_apply(G, dtype):
+    n = 2048
+    A = dense_random(n, seed=G + 7, dtype=dtype, shift=1.5)
+    x = (np.random.default_rng(3).standard_normal(n) + 1j).astype(dtype)
+    g = DenseGroup(A, G, options=ccg.OPT_REPLICATED)
+    try:
+        for op in ("A", "AH", "AT"):
+            assert relerr(g.apply(x, op), reference_apply(A, x, op)) <= TOL[dtype], op
+    finally:
+        g.close()
+
+
+@pytest.mark.parametrize("G", [2, 4])
+@pytest.mark.parametrize("method", ALL12)
+def test_replicated_cfg1_solve(G, method):
+    """Every method on config 1 with replicated vectors: P-literal against the
+    oracle, every rank returns the same result (checked by DenseGroup.solve)."""
+    A, y = cfg1()
+    if method == "cocr":
+        A = (A + A.T) / 2
+    g = DenseGroup(A, G, options=ccg.OPT_REPLICATED)
+    try:
+        o = oracle.solve(method, DenseOp(A), y, 1e-10, 500)
+        r = g.solve(method, y, 1e-10, 500)
+        assert r["status"] == "CONVERGED" and abs(r["iterations"] - o.iterations) <= 2, (r, o.iterations)
+        if r["iterations"] == o.iterations:
+            assert (r["matvecs_a"], r["matvecs_ah"]) == (o.matvecs_a, o.matvecs_ah)
+        k = min(r["iterations"], o.iterations)
+        assert relerr(g.solve(method, y, 0.0, k)["x"], oracle.solve(method, DenseOp(A), y, 0.0, k).x) <= 1e-9
+    finally:
+        g.close()
+
+
+@pytest.mark.parametrize("G", [2, 4])
+def test_replicated_csr_stencil_toeplitz(G):
+    """The sparse, matrix-free and lattice operators with replicated vectors
+    (no halo exchange: each rank's rows read the whole vector), incl. the Aᴴ
+    methods on the complex-symmetric CSR operator, which the row-sharded mode
+    cannot run."""
+    from workloads import lattice_csr, helmholtz_coeffs, dda_kernel
+    from oracle import ToeplitzOp
+    N = 16
+    d, oo = helmholtz_coeffs()
+    op = CsrOp(*lattice_csr(N, N, N, d, oo))
+    y = helmholtz_rhs(N)
+    x = (np.random.default_rng(5).standard_normal(op.n) + 0.5j).astype(np.complex128)
+    for grp in (CsrGroup(N, G, flags=ccg.FLAG_SYMMETRIC, options=ccg.OPT_REPLICATED),
+                StencilGroup(N, N, N, G, (d, oo), options=ccg.OPT_REPLICATED)):
+        try:
+            for o in ("A", "AH", "AT"):
+                assert relerr(grp.apply(x, o), reference_apply(op, x, o)) <= 1e-13, o
+            for method in ("bicgstab", "qmr", "cocr"):
+                r = grp.solve(method, y, 1e-8, 3000)
+                k0, kmin, kmax = iteration_envelope(method, op, y, 1e-8, 3000)
+                assert kmin - 2 <= r["iterations"] <= kmax + 2, (method, r["iterations"], kmin, kmax)
+                k = min(r["iterations"], k0)
+                xc, D = x_spread(method, op, y, k)
+                assert relerr(grp.solve(method, y, 0.0, k)["x"], xc) <= max(1e-9, 2 * D), method
+        finally:
+            grp.close()
+    dims = (8, 6, 4)
+    K = dda_kernel(dims, 0.9)
+    top = ToeplitzOp(K, dims, 2.5 + 0.3j)
+    hs = ccg.ccg_create_loopback_group(G, "c128", 192, options=ccg.OPT_REPLICATED)
+    g = DenseGroup.__new__(DenseGroup)
+    g.n, g.G, g.nloc, g.dtype, g.dt, g.hs = 192, G, 192 // G, np.complex128, "c128", hs
+    try:
+        for r in range(G):
+            ccg.ccg_set_matvec_toeplitz3(hs[r], *dims, K, 2.5 + 0.3j)
+        xt = x[:192]
+        for o, f in (("A", top.apply), ("AH", top.apply_h), ("AT", top.apply_t)):
+            assert relerr(g.apply(xt, o), f(xt)) <= 1e-13, o
+        yt = y[:192] + 1.0
+        ot = oracle.solve("bicgstab", top, yt, 1e-10, 500)
+        rt = g.solve("bicgstab", yt, 1e-10, 500)
+        assert rt["status"] == "CONVERGED" and abs(rt["iterations"] - ot.iterations) <= 2
     finally:
         g.close()
