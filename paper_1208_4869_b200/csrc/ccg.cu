@@ -148,8 +148,15 @@ struct ccg_ctx {
   int n_a = 0, n_ah = 0;
   int64_t launches = 0;
   bool capturing = false;
+  bool pdl = true;        // programmatic dependent launch (env CCG_PDL=0 disables)
   std::string err;
 };
+
+// kernel launch, with the programmatic-dependent-launch attribute unless
+// disabled (CCG_PDL=0): every launched kernel begins with pdl_gate()/pdl_wait()
+template <typename... KArgs, typename... Args>
+static void launch_k(ccg_ctx* c, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                     Args&&... args);
 
 #define FAIL(c, code, msg)       \
   do {                           \
@@ -180,6 +187,26 @@ struct ccg_ctx {
     int rc_ = (expr);        \
     if (rc_ != CCG_OK) return rc_; \
   } while (0)
+
+template <typename... KArgs, typename... Args>
+static void launch_k(ccg_ctx* c, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                     Args&&... args) {
+  if (!c->pdl) {
+    kern<<<grid, block, smem, s>>>(std::forward<Args>(args)...);
+    return;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 static bool is_device_ptr(const void* p) {
   cudaPointerAttributes a;
@@ -272,7 +299,7 @@ struct Engine {
     if constexpr (K > 0) {
       if (c->world > 1 && !c->rep) {
         NK(c, c->comm->allgather(c->rank_sum, c->all_sums, (size_t)K * 2, CT_F64, c->stream));
-        scalar_kernel<K, Fin><<<1, 1, 0, c->stream>>>(c->all_sums, c->world, c->st, gate);
+        launch_k(c, scalar_kernel<K, Fin>, 1, 1, 0, c->stream, c->all_sums, c->world, c->st, gate);
         c->launches++;
       }
     }
@@ -291,7 +318,7 @@ struct Engine {
     }
     const int grid = (int)std::max<int64_t>(
         1, std::min<int64_t>((c->nloc + NT - 1) / NT, (int64_t)c->sm_count * occ));
-    pass_kernel<NT, Op><<<grid, NT, 0, c->stream>>>(op, c->nloc, make_red(c), c->st, gate);
+    launch_k(c, pass_kernel<NT, Op>, grid, NT, 0, c->stream, op, c->nloc, make_red(c), c->st, gate);
     c->launches++;
     CK(c, cudaGetLastError());
     return post<Op>(c, gate);
@@ -302,14 +329,14 @@ struct Engine {
   static void spmv(ccg_ctx* c, const C* x, Epi epi, const int* gate) {
     const C* vals = reinterpret_cast<const C*>(c->vals);
     if (c->sell_col)
-      spmv_sell_kernel<T, NT, CONJ, Epi><<<c->sell_grid, NT, 0, c->stream>>>(
+      launch_k(c, spmv_sell_kernel<T, NT, CONJ, Epi>, c->sell_grid, NT, 0, c->stream, 
           c->sell_off, c->sell_width, c->sell_col, reinterpret_cast<const C*>(c->sell_val), x, c->mnloc, epi,
           make_red(c), c->st, gate);
     else if (c->csr_blocks)
-      spmv_stream_kernel<T, NT, SNNZ, CONJ, Epi><<<c->spmv_grid, NT, 0, c->stream>>>(
+      launch_k(c, spmv_stream_kernel<T, NT, SNNZ, CONJ, Epi>, c->spmv_grid, NT, 0, c->stream, 
           c->rowptr, c->colind, vals, x, c->csr_blocks, c->csr_nblocks, epi, make_red(c), c->st, gate);
     else
-      spmv_csr_kernel<T, LPR, NT, CONJ, Epi><<<c->spmv_grid, NT, 0, c->stream>>>(
+      launch_k(c, spmv_csr_kernel<T, LPR, NT, CONJ, Epi>, c->spmv_grid, NT, 0, c->stream, 
           c->rowptr, c->colind, vals, x, c->mnloc, epi, make_red(c), c->st, gate);
   }
 
@@ -323,7 +350,7 @@ struct Engine {
       k[i].y = (T)(conj ? -c->scoef[i].y : c->scoef[i].y);
     }
     dim3 g((c->snx + 31) / 32, (c->sny + 7) / 8, (c->snzl + c->szc - 1) / c->szc);
-    stencil7_kernel<T, Epi><<<g, 256, 0, c->stream>>>(xfull, c->snx, c->sny, c->snz, c->sz0, c->snzl, c->szc,
+    launch_k(c, stencil7_kernel<T, Epi>, g, 256, 0, c->stream, xfull, c->snx, c->sny, c->snz, c->sz0, c->snzl, c->szc,
                                                        k[0], k[1], k[2], k[3], epi, make_red(c), c->st, gate);
   }
 
@@ -341,23 +368,23 @@ struct Engine {
     const size_t smz = (size_t)g.tyz * g.Z2 * sizeof(C);
     const int gx = (g.ny * g.nz + g.tx - 1) / g.tx;
     if (op == 1)
-      fft_fwd_x<T, true><<<gx, 256, smx, c->stream>>>(xfull, W, g, tw, L / g.X2, gate);
+      launch_k(c, fft_fwd_x<T, true>, gx, 256, smx, c->stream, xfull, W, g, tw, L / g.X2, gate);
     else
-      fft_fwd_x<T, false><<<gx, 256, smx, c->stream>>>(xfull, W, g, tw, L / g.X2, gate);
-    fft_fwd_y<T><<<dim3(g.X2 / g.tyz, g.nz), 256, smy, c->stream>>>(W, g, tw, L / g.Y2, gate);
+      launch_k(c, fft_fwd_x<T, false>, gx, 256, smx, c->stream, xfull, W, g, tw, L / g.X2, gate);
+    launch_k(c, fft_fwd_y<T>, dim3(g.X2 / g.tyz, g.nz), 256, smy, c->stream, W, g, tw, L / g.Y2, gate);
     if (op == 0)
-      fft_z_mul<T, false><<<dim3(g.X2 / g.tyz, g.Y2), 256, smz, c->stream>>>(W, Kh, g, tw, L / g.Z2, gate);
+      launch_k(c, fft_z_mul<T, false>, dim3(g.X2 / g.tyz, g.Y2), 256, smz, c->stream, W, Kh, g, tw, L / g.Z2, gate);
     else
-      fft_z_mul<T, true><<<dim3(g.X2 / g.tyz, g.Y2), 256, smz, c->stream>>>(W, Kh, g, tw, L / g.Z2, gate);
-    fft_inv_y<T><<<dim3(g.X2 / g.tyz, g.nz), 256, smy, c->stream>>>(W, g, tw, L / g.Y2, gate);
+      launch_k(c, fft_z_mul<T, true>, dim3(g.X2 / g.tyz, g.Y2), 256, smz, c->stream, W, Kh, g, tw, L / g.Z2, gate);
+    launch_k(c, fft_inv_y<T>, dim3(g.X2 / g.tyz, g.nz), 256, smy, c->stream, W, g, tw, L / g.Y2, gate);
     C d;
     d.x = (T)c->tdiag.x;
     d.y = (T)(op == 1 ? -c->tdiag.y : c->tdiag.y);
     if (op == 1)
-      fft_inv_x<T, true, Epi><<<gx, 256, smx, c->stream>>>(W, xfull, g, tw, L / g.X2, d, c->row0, c->nloc, epi,
+      launch_k(c, fft_inv_x<T, true, Epi>, gx, 256, smx, c->stream, W, xfull, g, tw, L / g.X2, d, c->row0, c->nloc, epi,
                                                             make_red(c), c->st, gate);
     else
-      fft_inv_x<T, false, Epi><<<gx, 256, smx, c->stream>>>(W, xfull, g, tw, L / g.X2, d, c->row0, c->nloc, epi,
+      launch_k(c, fft_inv_x<T, false, Epi>, gx, 256, smx, c->stream, W, xfull, g, tw, L / g.X2, d, c->row0, c->nloc, epi,
                                                              make_red(c), c->st, gate);
     c->launches += 4;
   }
@@ -414,41 +441,41 @@ struct Engine {
       const size_t smem = (size_t)c->split_W * sizeof(C);
       if (c->split_strips == 1) {
         if (c->vec_ok)
-          gemv_n_split<T, NT, SUR, true, true, Epi><<<g, NT, smem, c->stream>>>(
+          launch_k(c, gemv_n_split<T, NT, SUR, true, true, Epi>, g, NT, smem, c->stream, 
               A, c->lda, xfull, c->n, c->mnloc, c->split_W, part, epi, make_red(c), c->st, gate);
         else
-          gemv_n_split<T, NT, SUR, false, true, Epi><<<g, NT, smem, c->stream>>>(
+          launch_k(c, gemv_n_split<T, NT, SUR, false, true, Epi>, g, NT, smem, c->stream, 
               A, c->lda, xfull, c->n, c->mnloc, c->split_W, part, epi, make_red(c), c->st, gate);
       } else {
         Store<T> none{nullptr};
         if (c->vec_ok && c->split_ur == 16)
-          gemv_n_split<T, NT, 16, true, false, Store<T>><<<g, NT, smem, c->stream>>>(
+          launch_k(c, gemv_n_split<T, NT, 16, true, false, Store<T>>, g, NT, smem, c->stream, 
               A, c->lda, xfull, c->n, c->mnloc, c->split_W, part, none, make_red(c), c->st, gate);
         else if (c->vec_ok && c->split_ur == 4)
-          gemv_n_split<T, NT, 4, true, false, Store<T>><<<g, NT, smem, c->stream>>>(
+          launch_k(c, gemv_n_split<T, NT, 4, true, false, Store<T>>, g, NT, smem, c->stream, 
               A, c->lda, xfull, c->n, c->mnloc, c->split_W, part, none, make_red(c), c->st, gate);
         else if (c->vec_ok)
-          gemv_n_split<T, NT, SUR, true, false, Store<T>><<<g, NT, smem, c->stream>>>(
+          launch_k(c, gemv_n_split<T, NT, SUR, true, false, Store<T>>, g, NT, smem, c->stream, 
               A, c->lda, xfull, c->n, c->mnloc, c->split_W, part, none, make_red(c), c->st, gate);
         else
-          gemv_n_split<T, NT, SUR, false, false, Store<T>><<<g, NT, smem, c->stream>>>(
+          launch_k(c, gemv_n_split<T, NT, SUR, false, false, Store<T>>, g, NT, smem, c->stream, 
               A, c->lda, xfull, c->n, c->mnloc, c->split_W, part, none, make_red(c), c->st, gate);
         c->launches++;
         CK(c, cudaGetLastError());
-        gemv_h_stage2<T, NT, Epi><<<c->nstage2_grid, NT, 0, c->stream>>>(part, c->split_strips, c->mnloc, 0,
+        launch_k(c, gemv_h_stage2<T, NT, Epi>, c->nstage2_grid, NT, 0, c->stream, part, c->split_strips, c->mnloc, 0,
                                                                           c->mnloc, epi, make_red(c), c->st, gate);
       }
     } else if (c->opk == OPK_DENSE && c->gemv_mode == GEMV_COLS && c->cols_ok) {
       C* part = reinterpret_cast<C*>(c->npart);
       if (c->cols_rg == 4)
-        gemv_cols<T, NT, true, false, false, 4><<<dim3(c->cols_strips, c->cols_S), NT, 0, c->stream>>>(
+        launch_k(c, gemv_cols<T, NT, true, false, false, 4>, dim3(c->cols_strips, c->cols_S), NT, 0, c->stream, 
             reinterpret_cast<const C*>(c->A), c->lda, xfull, nullptr, c->mnloc, c->n, part, nullptr, gate);
       else
-        gemv_cols<T, NT, true, false, false, 1><<<dim3(c->cols_strips, c->cols_S), NT, 0, c->stream>>>(
+        launch_k(c, gemv_cols<T, NT, true, false, false, 1>, dim3(c->cols_strips, c->cols_S), NT, 0, c->stream, 
             reinterpret_cast<const C*>(c->A), c->lda, xfull, nullptr, c->mnloc, c->n, part, nullptr, gate);
       c->launches++;
       CK(c, cudaGetLastError());
-      gemv_h_stage2<T, NT, Epi><<<c->nstage2_grid, NT, 0, c->stream>>>(part, c->cols_strips, c->mnloc, 0, c->mnloc,
+      launch_k(c, gemv_h_stage2<T, NT, Epi>, c->nstage2_grid, NT, 0, c->stream, part, c->cols_strips, c->mnloc, 0, c->mnloc,
                                                                         epi, make_red(c), c->st, gate);
     } else if (c->opk == OPK_DENSE && c->gemv_mode == GEMV_BULK && c->bulk_ok) {
       constexpr size_t smem = bulk_smem_bytes<BR, BSTAGES>();
@@ -458,15 +485,15 @@ struct Engine {
         CK(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr_set = true;
       }
-      kern<<<c->bulk_grid, BULK_NT, smem, c->stream>>>(reinterpret_cast<const C*>(c->A), c->lda, xfull, c->n,
+      launch_k(c, kern, c->bulk_grid, BULK_NT, smem, c->stream, reinterpret_cast<const C*>(c->A), c->lda, xfull, c->n,
                                                        c->mnloc, epi, make_red(c), c->st, gate);
     } else if (c->opk == OPK_DENSE) {
       const C* A = reinterpret_cast<const C*>(c->A);
       if (c->vec_ok)
-        gemv_n_kernel<T, R, NT, true, Epi><<<c->gemv_grid, NT, 0, c->stream>>>(
+        launch_k(c, gemv_n_kernel<T, R, NT, true, Epi>, c->gemv_grid, NT, 0, c->stream, 
             A, c->lda, xfull, c->n, c->mnloc, epi, make_red(c), c->st, gate);
       else
-        gemv_n_kernel<T, R, NT, false, Epi><<<c->gemv_grid, NT, 0, c->stream>>>(
+        launch_k(c, gemv_n_kernel<T, R, NT, false, Epi>, c->gemv_grid, NT, 0, c->stream, 
             A, c->lda, xfull, c->n, c->mnloc, epi, make_red(c), c->st, gate);
     } else {
       spmv<false>(c, xfull, epi, gate);
@@ -537,19 +564,19 @@ struct Engine {
     tev_begin(c, 1);
     if (c->vec_ok) {
       if (conj)
-        gemv_h_stage1<T, true, NT, UR, true><<<g1, NT, 0, c->stream>>>(A, c->lda, xr, c->mnloc, c->n, part, gate);
+        launch_k(c, gemv_h_stage1<T, true, NT, UR, true>, g1, NT, 0, c->stream, A, c->lda, xr, c->mnloc, c->n, part, gate);
       else
-        gemv_h_stage1<T, false, NT, UR, true><<<g1, NT, 0, c->stream>>>(A, c->lda, xr, c->mnloc, c->n, part, gate);
+        launch_k(c, gemv_h_stage1<T, false, NT, UR, true>, g1, NT, 0, c->stream, A, c->lda, xr, c->mnloc, c->n, part, gate);
     } else {
       if (conj)
-        gemv_h_stage1<T, true, NT, UR, false><<<g1, NT, 0, c->stream>>>(A, c->lda, xr, c->mnloc, c->n, part, gate);
+        launch_k(c, gemv_h_stage1<T, true, NT, UR, false>, g1, NT, 0, c->stream, A, c->lda, xr, c->mnloc, c->n, part, gate);
       else
-        gemv_h_stage1<T, false, NT, UR, false><<<g1, NT, 0, c->stream>>>(A, c->lda, xr, c->mnloc, c->n, part, gate);
+        launch_k(c, gemv_h_stage1<T, false, NT, UR, false>, g1, NT, 0, c->stream, A, c->lda, xr, c->mnloc, c->n, part, gate);
     }
     c->launches++;
     CK(c, cudaGetLastError());
     if (c->world == 1) {
-      gemv_h_stage2<T, NT, Epi><<<c->stage2_grid, NT, 0, c->stream>>>(part, c->ah_S, c->n, 0, c->n, epi,
+      launch_k(c, gemv_h_stage2<T, NT, Epi>, c->stage2_grid, NT, 0, c->stream, part, c->ah_S, c->n, 0, c->n, epi,
                                                                        make_red(c), c->st, gate);
       c->launches++;
       tev_end(c);
@@ -559,7 +586,7 @@ struct Engine {
     // multi GPU: full-length partial of this rank
     C* wf = c->rep ? reinterpret_cast<C*>(c->rep_tmp) : reinterpret_cast<C*>(c->wfull);
     Store<T> stv{wf};
-    gemv_h_stage2<T, NT, Store<T>><<<c->stage2_grid, NT, 0, c->stream>>>(part, c->ah_S, c->n, 0, c->n, stv,
+    launch_k(c, gemv_h_stage2<T, NT, Store<T>>, c->stage2_grid, NT, 0, c->stream, part, c->ah_S, c->n, 0, c->n, stv,
                                                                          make_red(c), c->st, gate);
     c->launches++;
     tev_end(c);
@@ -586,25 +613,25 @@ struct Engine {
     C* np = reinterpret_cast<C*>(c->npart);
     C* hp = reinterpret_cast<C*>(c->hpart);
     tev_begin(c, 0);
-    gemv_cols<T, NT, true, true, true><<<dim3(c->cols_strips, c->dual_S), NT, 0, c->stream>>>(
+    launch_k(c, gemv_cols<T, NT, true, true, true>, dim3(c->cols_strips, c->dual_S), NT, 0, c->stream, 
         A, c->lda, pfull, qloc, c->nloc, c->n, np, hp, gate);
     c->launches++;
     CK(c, cudaGetLastError());
-    gemv_h_stage2<T, NT, EpiA><<<c->nstage2_grid, NT, 0, c->stream>>>(np, c->cols_strips, c->nloc, 0, c->nloc, ea,
+    launch_k(c, gemv_h_stage2<T, NT, EpiA>, c->nstage2_grid, NT, 0, c->stream, np, c->cols_strips, c->nloc, 0, c->nloc, ea,
                                                                       make_red(c), c->st, gate);
     c->launches++;
     tev_end(c);
     CK(c, cudaGetLastError());
     TRY(post<EpiA>(c, gate));
     if (c->world == 1) {
-      gemv_h_stage2<T, NT, EpiH><<<c->stage2_grid, NT, 0, c->stream>>>(hp, c->dual_S, c->n, 0, c->n, eh,
+      launch_k(c, gemv_h_stage2<T, NT, EpiH>, c->stage2_grid, NT, 0, c->stream, hp, c->dual_S, c->n, 0, c->n, eh,
                                                                        make_red(c), c->st, gate);
       c->launches++;
       CK(c, cudaGetLastError());
       return CCG_OK;
     }
     Store<T> stv{reinterpret_cast<C*>(c->wfull)};
-    gemv_h_stage2<T, NT, Store<T>><<<c->stage2_grid, NT, 0, c->stream>>>(hp, c->dual_S, c->n, 0, c->n, stv,
+    launch_k(c, gemv_h_stage2<T, NT, Store<T>>, c->stage2_grid, NT, 0, c->stream, hp, c->dual_S, c->n, 0, c->n, stv,
                                                                          make_red(c), c->st, gate);
     c->launches++;
     CK(c, cudaGetLastError());
@@ -891,20 +918,20 @@ struct Engine {
   template <int MODE>
   static int gm_pass_launch(ccg_ctx* c, C* w, const double2* coef, double2* dst, const int* gate) {
     const bool fuse = c->world == 1 || c->rep;
-    gm_pass<T, MODE><<<c->gm_grid, GM_NT, 0, c->stream>>>(Vb(c), c->nloc, w, coef, fuse ? dst : c->gm_rank, c->nloc,
+    launch_k(c, gm_pass<T, MODE>, c->gm_grid, GM_NT, 0, c->stream, Vb(c), c->nloc, w, coef, fuse ? dst : c->gm_rank, c->nloc,
                                                            c->gm_dev, c->gm_part, c->gm_ticket, fuse ? 1 : 0, gate);
     c->launches++;
     CK(c, cudaGetLastError());
     if (!fuse) {
       NK(c, c->comm->allgather(c->gm_rank, c->gm_all, (size_t)(GM_MAX + 1) * 2, CT_F64, c->stream));
-      gm_ranksum<<<1, 128, 0, c->stream>>>(c->gm_all, c->world, MODE == 2 ? 1 : GM_MAX + 1, GM_MAX + 1, dst, gate);
+      launch_k(c, gm_ranksum, 1, 128, 0, c->stream, c->gm_all, c->world, MODE == 2 ? 1 : GM_MAX + 1, GM_MAX + 1, dst, gate);
       c->launches++;
     }
     return CCG_OK;
   }
   static int gmres_setup(ccg_ctx* c, bool x0) {
     TRY(init_residual(c, x0, Vb(c), nullptr, nullptr, nullptr));
-    gm_normalize<T><<<c->pass_grid, NT, 0, c->stream>>>(Vb(c), c->nloc, Vb(c), Fs(c, 0), c->nloc, c->gm_dev, 1,
+    launch_k(c, gm_normalize<T>, c->pass_grid, NT, 0, c->stream, Vb(c), c->nloc, Vb(c), Fs(c, 0), c->nloc, c->gm_dev, 1,
                                                          &c->st->done);
     c->launches++;
     CK(c, cudaGetLastError());
@@ -919,18 +946,18 @@ struct Engine {
     TRY(gm_pass_launch<0>(c, w, nullptr, gm->hcol, g));
     TRY(gm_pass_launch<1>(c, w, gm->hcol, gm->h2, g));
     TRY(gm_pass_launch<2>(c, w, gm->h2, &gm->ww2, g));
-    gm_step<<<1, 1, 0, c->stream>>>(c->st, gm, g);
-    gm_normalize<T><<<c->pass_grid, NT, 0, c->stream>>>(Vb(c), c->nloc, w, Fs(c, 0), c->nloc, gm, 0, &gm->endflag);
-    gm_trisolve<<<1, 1, 0, c->stream>>>(c->st, gm, &gm->noend);
-    gm_xupdate<T><<<c->pass_grid, NT, 0, c->stream>>>(L(c, X), Vb(c), c->nloc, c->nloc, gm, &gm->noxupd);
+    launch_k(c, gm_step, 1, 1, 0, c->stream, c->st, gm, g);
+    launch_k(c, gm_normalize<T>, c->pass_grid, NT, 0, c->stream, Vb(c), c->nloc, w, Fs(c, 0), c->nloc, gm, 0, &gm->endflag);
+    launch_k(c, gm_trisolve, 1, 1, 0, c->stream, c->st, gm, &gm->noend);
+    launch_k(c, gm_xupdate<T>, c->pass_grid, NT, 0, c->stream, L(c, X), Vb(c), c->nloc, c->nloc, gm, &gm->noxupd);
     c->launches += 4;
     CK(c, cudaGetLastError());
     TRY(pass(c, Copy<T>{L(c, X), Fs(c, 2)}, &gm->norestart));
     TRY(allgather(c, 2));
     TRY(matvec_a(c, F(c, 2), GmR<T>{L(c, 1), Vb(c)}, &gm->norestart));
-    gm_normalize<T><<<c->pass_grid, NT, 0, c->stream>>>(Vb(c), c->nloc, Vb(c), Fs(c, 0), c->nloc, gm, 1,
+    launch_k(c, gm_normalize<T>, c->pass_grid, NT, 0, c->stream, Vb(c), c->nloc, Vb(c), Fs(c, 0), c->nloc, gm, 1,
                                                          &gm->norestart);
-    gm_reset<<<1, 1, 0, c->stream>>>(gm);
+    launch_k(c, gm_reset, 1, 1, 0, c->stream, gm);
     c->launches += 2;
     CK(c, cudaGetLastError());
     return CCG_OK;
@@ -1404,6 +1431,10 @@ static int create_impl(ccg_handle* h, ccg_dtype dt, int64_t n, int world, int ra
   c->nloc = c->rep ? n : c->mnloc;      // vectors: whole (replicated) or this rank's slice
   c->row0 = c->rep ? 0 : c->mrow0;
   c->device = device;
+  {
+    const char* pe = getenv("CCG_PDL");
+    c->pdl = !(pe && !strcmp(pe, "0"));
+  }
   auto bail = [&](int code) {
     g_create_err = c->err;
     ccg_destroy(c);

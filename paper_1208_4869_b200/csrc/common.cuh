@@ -10,6 +10,23 @@
 namespace ccg {
 
 // ---------------------------------------------------------------------------
+// Programmatic dependent launch (sm_90+): every kernel of the path starts by
+// waiting until its predecessor has completed and its writes are visible
+// (pdl_gate / pdl_wait).  No kernel triggers early: griddepcontrol.wait only
+// guarantees the writes made BEFORE the primary's trigger, and every kernel
+// writes the State its successor gates on in its very last step, so the
+// implicit trigger at exit is the only safe one; what PDL still buys is the
+// successor's launch processing overlapping the predecessor's execution.
+// A kernel launched without the PDL attribute passes the wait as a no-op.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ int pdl_gate(const int* gate) {
+  pdl_wait();
+  return *gate;
+}
+
+// ---------------------------------------------------------------------------
 // complex types: cplx<float> = interleaved c64, cplx<double> = c128
 // ---------------------------------------------------------------------------
 template <typename T> struct CT;

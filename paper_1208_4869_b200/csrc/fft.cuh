@@ -97,7 +97,7 @@ __global__ void __launch_bounds__(256)
 fft_fwd_x(const typename CT<T>::c* __restrict__ x, typename CT<T>::c* __restrict__ W, FftGeo g,
           const typename CT<T>::c* __restrict__ tw, int twstride, const int* gate) {
   using C = typename CT<T>::c;
-  if (*gate) return;
+  if (pdl_gate(gate)) return;
   extern __shared__ __align__(16) unsigned char fft_sm[];
   C* buf = reinterpret_cast<C*>(fft_sm);
   const int TX = g.tx, L = g.X2;
@@ -130,7 +130,7 @@ __global__ void __launch_bounds__(256)
 fft_fwd_y(typename CT<T>::c* __restrict__ W, FftGeo g, const typename CT<T>::c* __restrict__ tw, int twstride,
           const int* gate) {
   using C = typename CT<T>::c;
-  if (*gate) return;
+  if (pdl_gate(gate)) return;
   extern __shared__ __align__(16) unsigned char fft_sm[];
   C* buf = reinterpret_cast<C*>(fft_sm);
   const int TX = g.tyz, L = g.Y2;
@@ -154,7 +154,7 @@ __global__ void __launch_bounds__(256)
 fft_z_mul(typename CT<T>::c* __restrict__ W, const typename CT<T>::c* __restrict__ Kh, FftGeo g,
           const typename CT<T>::c* __restrict__ tw, int twstride, const int* gate) {
   using C = typename CT<T>::c;
-  if (*gate) return;
+  if (pdl_gate(gate)) return;
   extern __shared__ __align__(16) unsigned char fft_sm[];
   C* buf = reinterpret_cast<C*>(fft_sm);
   const int TX = g.tyz, L = g.Z2;
@@ -190,7 +190,7 @@ __global__ void __launch_bounds__(256)
 fft_inv_y(typename CT<T>::c* __restrict__ W, FftGeo g, const typename CT<T>::c* __restrict__ tw, int twstride,
           const int* gate) {
   using C = typename CT<T>::c;
-  if (*gate) return;
+  if (pdl_gate(gate)) return;
   extern __shared__ __align__(16) unsigned char fft_sm[];
   C* buf = reinterpret_cast<C*>(fft_sm);
   const int TX = g.tyz, L = g.Y2;
@@ -216,7 +216,7 @@ fft_inv_x(const typename CT<T>::c* __restrict__ W, const typename CT<T>::c* __re
           Epi epi, Red red, State* st, const int* gate) {
   using C = typename CT<T>::c;
   constexpr int KK = Epi::K > 0 ? Epi::K : 1;
-  if (*gate) return;
+  if (pdl_gate(gate)) return;
   epi.load(st);
   extern __shared__ __align__(16) unsigned char fft_sm[];
   C* buf = reinterpret_cast<C*>(fft_sm);

@@ -28,7 +28,7 @@ gm_pass(const typename CT<T>::c* __restrict__ V, int64_t ldv, typename CT<T>::c*
   using C = typename CT<T>::c;
   constexpr int NW = GM_NT / 32;
   constexpr int NA = (GM_MAX + 1 + NW - 1) / NW;   // accumulators per lane (vectors per warp)
-  if (*gate) return;
+  if (pdl_gate(gate)) return;
   __shared__ C wt[GM_NT];
   __shared__ C cf[GM_MAX + 1];
   __shared__ double2 nsm[NW];
@@ -108,7 +108,7 @@ gm_pass(const typename CT<T>::c* __restrict__ V, int64_t ldv, typename CT<T>::c*
 
 // world > 1: sum the allgathered rank sums in rank order
 __global__ void gm_ranksum(const double2* all, int world, int count, int stride, double2* out, const int* gate) {
-  if (*gate) return;
+  if (pdl_gate(gate)) return;
   for (int i = threadIdx.x; i < count; i += blockDim.x) {
     double2 s = make_double2(0.0, 0.0);
     for (int r = 0; r < world; ++r) { s.x += all[r * stride + i].x; s.y += all[r * stride + i].y; }
@@ -118,7 +118,7 @@ __global__ void gm_ranksum(const double2* all, int world, int count, int stride,
 
 // Arnoldi / Givens step (one thread)
 __global__ void gm_step(State* st, GmDev* gm, const int* gate) {
-  if (*gate) return;
+  if (pdl_gate(gate)) return;
   const int j = gm->j;
   const int k = ++gm->k;
   st->matvecs_a++;
@@ -175,7 +175,7 @@ __global__ void gm_normalize(typename CT<T>::c* V, int64_t ldv, const typename C
                              typename CT<T>::c* full_slice, int64_t nrows, const GmDev* gm,
                              int use_beta, const int* gate) {
   using C = typename CT<T>::c;
-  if (*gate) return;
+  if (pdl_gate(gate)) return;
   const int jj = use_beta ? 0 : gm->j;
   const T d = (T)(use_beta ? gm->g[0].x : gm->hn);
   C* vj = V + (int64_t)jj * ldv;
@@ -188,7 +188,7 @@ __global__ void gm_normalize(typename CT<T>::c* V, int64_t ldv, const typename C
 
 // back substitution R y = g (one thread); decides done / restart
 __global__ void gm_trisolve(State* st, GmDev* gm, const int* gate) {
-  if (*gate) return;
+  if (pdl_gate(gate)) return;
   const int J = gm->j + 1;
   for (int i = J - 1; i >= 0; --i) {
     double2 t = gm->g[i];
@@ -211,7 +211,7 @@ template <typename T>
 __global__ void gm_xupdate(typename CT<T>::c* __restrict__ x, const typename CT<T>::c* __restrict__ V, int64_t ldv,
                            int64_t nrows, const GmDev* gm, const int* gate) {
   using C = typename CT<T>::c;
-  if (*gate) return;
+  if (pdl_gate(gate)) return;
   const int J = gm->j + 1;
   __shared__ C ys[GM_MAX];
   for (int i = threadIdx.x; i < J; i += blockDim.x) ys[i] = fromd2<C>(gm->y[i]);
@@ -225,6 +225,7 @@ __global__ void gm_xupdate(typename CT<T>::c* __restrict__ x, const typename CT<
 
 // end of every replayed step: re-arm the flags
 __global__ void gm_reset(GmDev* gm) {
+  pdl_wait();
   gm->endflag = 0;
   gm->noend = 1;
   gm->noxupd = 1;

@@ -44,7 +44,7 @@ gemv_n_kernel(const typename CT<T>::c* __restrict__ A, int64_t lda,
   constexpr int V = VEC ? CT<T>::V : 1;
   using LV = typename std::conditional<VEC, typename CT<T>::v, C>::type;
   constexpr int KK = Epi::K > 0 ? Epi::K : 1;
-  if (*gate) return;
+  if (pdl_gate(gate)) return;
   epi.load(st);
   __shared__ C sm[NT / 32][R];
   double2 dacc[KK];
@@ -140,7 +140,7 @@ gemv_n_bulk(const typename CT<T>::c* __restrict__ A, int64_t lda,
   constexpr int V = CT<T>::V;
   constexpr int KK = Epi::K > 0 ? Epi::K : 1;
   constexpr int TC = BULK_TILE / (int)sizeof(C);   // complex per row segment
-  if (*gate) return;
+  if (pdl_gate(gate)) return;
   epi.load(st);
   extern __shared__ __align__(128) unsigned char smem_raw[];
   unsigned char* tiles = smem_raw;                                  // [STAGES][R+1][4096]
@@ -256,7 +256,7 @@ gemv_n_split(const typename CT<T>::c* __restrict__ A, int64_t lda,
   constexpr int V = VEC ? CT<T>::V : 1;
   using LV = typename std::conditional<VEC, typename CT<T>::v, C>::type;
   constexpr int KK = Epi::K > 0 ? Epi::K : 1;
-  if (*gate) return;
+  if (pdl_gate(gate)) return;
   if constexpr (FUSED) epi.load(st);
   extern __shared__ __align__(16) unsigned char xs_raw[];
   C* xs = reinterpret_cast<C*>(xs_raw);
@@ -325,7 +325,7 @@ gemv_h_stage1(const typename CT<T>::c* __restrict__ A, int64_t lda,
   constexpr int V = VEC ? CT<T>::V : 1;
   using LV = typename std::conditional<VEC, typename CT<T>::v, C>::type;
   constexpr int CH = 512;  // rows of x per smem chunk
-  if (*gate) return;
+  if (pdl_gate(gate)) return;
   __shared__ C xs[CH];
   const int S = gridDim.y, s = blockIdx.y;
   const int64_t i0 = nrows * s / S, i1 = nrows * (s + 1) / S;
@@ -447,7 +447,7 @@ gemv_cols(const typename CT<T>::c* __restrict__ A, int64_t lda,
   constexpr int NR = UR * RG;    // rows per CTA reduction (RG groups)
   constexpr int CH = 512;        // rows of xh per shared-memory chunk (multiple of NR)
   static_assert(!(DO_H && RG != 1), "dual product: one group per reduction");
-  if (*gate) return;
+  if (pdl_gate(gate)) return;
   __shared__ C xs[DO_H ? CH : 1];
   __shared__ C red[2][NT / 32][NR];
   const int S = gridDim.y, s = blockIdx.y;
@@ -529,7 +529,7 @@ gemv_h_stage2(const typename CT<T>::c* __restrict__ part, int S, int64_t n, int6
               int64_t nout, Epi epi, Red red, State* st, const int* gate) {
   using C = typename CT<T>::c;
   constexpr int KK = Epi::K > 0 ? Epi::K : 1;
-  if (*gate) return;
+  if (pdl_gate(gate)) return;
   epi.load(st);
   double2 dacc[KK];
 #pragma unroll
@@ -558,7 +558,7 @@ spmv_csr_kernel(const int32_t* __restrict__ rowptr, const int32_t* __restrict__ 
                 int64_t nrows, Epi epi, Red red, State* st, const int* gate) {
   using C = typename CT<T>::c;
   constexpr int KK = Epi::K > 0 ? Epi::K : 1;
-  if (*gate) return;
+  if (pdl_gate(gate)) return;
   epi.load(st);
   double2 dacc[KK];
 #pragma unroll
@@ -602,7 +602,7 @@ spmv_stream_kernel(const int32_t* __restrict__ rowptr, const int32_t* __restrict
   using C = typename CT<T>::c;
   constexpr int KK = Epi::K > 0 ? Epi::K : 1;
   constexpr int U = 8;
-  if (*gate) return;
+  if (pdl_gate(gate)) return;
   epi.load(st);
   __shared__ C prod[NNZ_MAX];
   __shared__ int32_t rp[NT + 1];
@@ -719,7 +719,7 @@ spmv_sell_kernel(const int64_t* __restrict__ soff, const int32_t* __restrict__ s
   using C = typename CT<T>::c;
   constexpr int KK = Epi::K > 0 ? Epi::K : 1;
   constexpr int U = 8;
-  if (*gate) return;
+  if (pdl_gate(gate)) return;
   epi.load(st);
   double2 dacc[KK];
 #pragma unroll
@@ -853,7 +853,7 @@ stencil7_kernel(const typename CT<T>::c* __restrict__ x, int nx, int ny, int nz,
                 Epi epi, Red red, State* st, const int* gate) {
   using C = typename CT<T>::c;
   constexpr int KK = Epi::K > 0 ? Epi::K : 1;
-  if (*gate) return;
+  if (pdl_gate(gate)) return;
   epi.load(st);
   double2 dacc[KK];
 #pragma unroll
@@ -894,7 +894,7 @@ template <int NT, class Op>
 __global__ void __launch_bounds__(NT)
 pass_kernel(Op op, int64_t n, Red red, State* st, const int* gate) {
   constexpr int KK = Op::K > 0 ? Op::K : 1;
-  if (*gate) return;
+  if (pdl_gate(gate)) return;
   op.load(st);
   double2 dacc[KK];
 #pragma unroll
@@ -938,7 +938,7 @@ struct EpiPassSum {
 // multi-GPU scalar step: sum the world×K allgathered rank sums in rank order
 template <int K, class Fin>
 __global__ void scalar_kernel(const double2* all, int world, State* st, const int* gate) {
-  if (*gate) return;
+  if (pdl_gate(gate)) return;
   double2 s[K];
   for (int k = 0; k < K; ++k) s[k] = make_double2(0.0, 0.0);
   for (int r = 0; r < world; ++r)
