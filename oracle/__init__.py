@@ -35,5 +35,5 @@ Parity pins: every function here is pinned by a ``-m "not gpu"`` test in
 """
 
 from . import numerics, operators, solvers, direct, exact  # noqa: F401
-from .solvers import solve, Result, METHODS  # noqa: F401
-from .operators import DenseOp, CsrOp, ToeplitzOp  # noqa: F401
+from .solvers import solve, solve_jacobi, Result, METHODS  # noqa: F401
+from .operators import DenseOp, CsrOp, ToeplitzOp, JacobiRightOp  # noqa: F401

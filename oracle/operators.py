@@ -174,6 +174,31 @@ class ToeplitzOp(_Counted):
         return np.conj(self.diag * xc + self._conv(xc, self.Kh_t))
 
 
+class JacobiRightOp(_Counted):
+    """Right Jacobi preconditioning: the operator
+    B = A·D⁻¹ with D = diag(d) — B·v = A(D⁻¹v), Bᴴ·v = D⁻ᴴ(Aᴴv), Bᵀ·v = D⁻¹(Aᵀv).
+    A solve of B u = y gives x = D⁻¹u; the residual y − B u = y − A x is the
+    original system's, so the common stopping rule is unchanged."""
+
+    def __init__(self, op, d):
+        super().__init__()
+        self.op = op
+        self.dinv = 1.0 / np.asarray(d)
+        self.n = op.n
+
+    def apply(self, x):
+        self.n_a += 1
+        return self.op.apply(self.dinv * x)
+
+    def apply_h(self, x):
+        self.n_ah += 1
+        return np.conj(self.dinv) * self.op.apply_h(x)
+
+    def apply_t(self, x):
+        self.n_at += 1
+        return self.dinv * self.op.apply_t(x)
+
+
 def reference_apply(A, x, op="A"):
     """Per-matvec parity reference.
 

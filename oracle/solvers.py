@@ -766,3 +766,15 @@ def solve(method, op, y, tol, maxit, x0=None, dots=None, **kw):
     if method not in METHODS:
         raise ValueError(f"unknown method {method!r}")
     return _run(METHODS[method], op, y, tol, maxit, x0, dots=dots, **kw)
+
+
+def solve_jacobi(method, op, d, y, tol, maxit, x0=None, **kw):
+    """Right-Jacobi-preconditioned solve: run ``method``
+    on B u = y with B = A·diag(d)⁻¹ (u₀ = D x₀), return x = D⁻¹u in the Result
+    (true residual recomputed by the wrapper, i.e. y − A x)."""
+    from .operators import JacobiRightOp
+    B = JacobiRightOp(op, d)
+    u0 = None if x0 is None else np.asarray(d) * np.asarray(x0)
+    res = solve(method, B, y, tol, maxit, x0=u0, **kw)
+    res.x = (B.dinv * res.x).astype(res.x.dtype)
+    return res

@@ -327,3 +327,34 @@ def test_bicgstabl_mr_part_minimises_over_the_cycle_space():
                     assert np.linalg.norm(R[j + 1] - A @ R[j]) <= 1e-10 * np.linalg.norm(R[j + 1])
                     assert np.linalg.norm(U[j + 1] - A @ U[j]) <= 1e-10 * np.linalg.norm(U[j + 1])
         assert np.linalg.norm(cycles[-1][0][0] - (y - A @ res.x)) <= 1e-10 * np.linalg.norm(y)
+
+
+# ---------------- right Jacobi preconditioning (NEXT-4) ----------------
+def test_jacobi_constant_diagonal_is_a_rescaling():
+    """d = c·1: B = A/c, u = c·x — the same iterates (scale invariance)."""
+    from oracle import solve_jacobi
+    A, y = cfg1(n=64, seed=8)
+    for m in ("bicgstab", "qmr", "gmres"):
+        a = solve(m, DenseOp(A), y, 1e-10, 300)
+        b = solve_jacobi(m, DenseOp(A), np.full(64, 3 - 4j), y, 1e-10, 300)
+        assert a.iterations == b.iterations
+        assert np.linalg.norm(a.x - b.x) <= 1e-9 * np.linalg.norm(a.x), m
+
+
+def test_jacobi_diagonal_matrix_one_iteration_and_badly_scaled_speedup():
+    from oracle import solve_jacobi
+    rng = np.random.default_rng(12)
+    n = 80
+    d = np.logspace(0, 4, n) * np.exp(1j * rng.uniform(0, 2 * np.pi, n))
+    y = rng.standard_normal(n) + 1j * rng.standard_normal(n)
+    r = solve_jacobi("bicgstab", DenseOp(np.diag(d)), d, y, 1e-12, 10)
+    assert r.status == CONVERGED and r.iterations == 1
+    np.testing.assert_allclose(r.x, y / d, rtol=1e-13)
+    A = np.diag(d) + 0.3 * (rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))) / np.sqrt(n)
+    plain = solve("bicgstab", DenseOp(A), y, 1e-10, 2000)
+    pre = solve_jacobi("bicgstab", DenseOp(A), d, y, 1e-10, 2000)
+    assert pre.status == CONVERGED and pre.iterations <= 20               # unpreconditioned: > 2000 (MAXIT)
+    assert plain.status != CONVERGED or plain.iterations >= 10 * pre.iterations
+    xl = lu_solve(A, y)
+    assert np.linalg.norm(pre.x - xl) <= 1e-8 * np.linalg.norm(xl)
+    assert np.linalg.norm(y - A @ pre.x) / np.linalg.norm(y) <= 1e-9
