@@ -271,6 +271,16 @@ int ccg_apply(ccg_handle h, ccg_op op, const void* x_local, void* y_local);
  * basis (m+1 vectors of nloc elements) is allocated by the next GMRES solve. */
 int ccg_set_gmres_restart(ccg_handle h, int32_t m);
 
+/* Right Jacobi preconditioning of the following ccg_solve calls (SURVEY §8(f)
+ * NEXT-4): the method runs on B u = y with B = A·D⁻¹, D = diag(d), and returns
+ * x = D⁻¹u.  The residual y − B u is the original y − A x, so tolerances and
+ * the true residual keep their meaning; products by ccg_apply are unaffected.
+ *   diag_local : HOST or DEVICE pointer to this rank's nloc diagonal entries d
+ *                (the handle's precision; finite and nonzero, else CCG_E_ARG);
+ *                copied.  NULL disables preconditioning.  Collective (world > 1).
+ *   flags      : reserved, 0. */
+int ccg_set_jacobi(ccg_handle h, const void* diag_local, uint32_t flags);
+
 /* ℓ of CCG_BICGSTABL (1 ≤ ℓ ≤ 4, else CCG_E_ARG; default 2; ℓ = 1 is BiCGSTAB). */
 int ccg_set_bicgstab_ell(ccg_handle h, int32_t ell);
 

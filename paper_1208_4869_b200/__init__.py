@@ -38,7 +38,7 @@ EXPORTS = ("ccg_get_unique_id", "ccg_create", "ccg_create_ex", "ccg_create_loopb
            "ccg_create_loopback_group_ex",
            "ccg_set_matvec_dense", "ccg_set_matvec_csr", "ccg_set_matvec_stencil7",
            "ccg_set_matvec_toeplitz3", "ccg_set_matvec_callback", "ccg_set_gmres_restart",
-           "ccg_set_bicgstab_ell",
+           "ccg_set_bicgstab_ell", "ccg_set_jacobi",
            "ccg_apply", "ccg_solve", "ccg_get_history", "ccg_set_timing", "ccg_get_timing",
            "ccg_last_launch_count", "ccg_get_stream", "ccg_last_error", "ccg_destroy",
            "ccg_version")
@@ -100,6 +100,7 @@ def load():
         "ccg_set_matvec_callback": (ctypes.c_int, [vp, MATVEC_FN, vp, u32, u32]),
         "ccg_set_gmres_restart": (ctypes.c_int, [vp, i32]),
         "ccg_set_bicgstab_ell": (ctypes.c_int, [vp, i32]),
+        "ccg_set_jacobi": (ctypes.c_int, [vp, vp, u32]),
         "ccg_apply": (ctypes.c_int, [vp, ctypes.c_int, vp, vp]),
         "ccg_solve": (ctypes.c_int, [vp, ctypes.c_int, vp, vp, vp, dbl, i32,
                                      ctypes.POINTER(ccg_result)]),
@@ -257,6 +258,12 @@ def ccg_set_matvec_callback_ptr(h, fn_addr, user_addr=None, caps=CB_A, flags=0):
 
 def ccg_set_gmres_restart(h, m):
     _check(h, load().ccg_set_gmres_restart(h, int(m)))
+
+
+def ccg_set_jacobi(h, diag_local, flags=0):
+    """Right Jacobi preconditioning of later solves (diag_local: this rank's
+    diagonal entries, host or device; None disables)."""
+    _check(h, load().ccg_set_jacobi(h, None if diag_local is None else _ptr(diag_local, "diag"), int(flags)))
 
 
 def ccg_set_bicgstab_ell(h, ell):

@@ -98,6 +98,11 @@ struct ccg_ctx {
   int bl_l = 2, bl_built = 0;
   void* bl_buf = nullptr;
   size_t bl_bytes = 0;
+  // right Jacobi preconditioning (ccg_set_jacobi): d and 1/d over all n rows
+  void* jac_d = nullptr;
+  void* jac_dinv = nullptr;
+  void* jac_tmp = nullptr;   // n: D⁻¹·(product input)
+  bool jac_active = false;   // inside ccg_solve
   // whole-loop cluster kernel for small dense systems (cluster.cuh)
   bool cluster_ok = false;
   int cluster_size = 0;   // 0 = not yet chosen
@@ -168,7 +173,7 @@ static void launch_k(ccg_ctx* c, void (*kern)(KArgs...), dim3 grid, dim3 block, 
   do {                                                                                     \
     cudaError_t e_ = (call);                                                               \
     if (e_ != cudaSuccess) {                                                               \
-      (c)->err = std::string(#call) + ": " + cudaGetErrorString(e_);                       \
+      (c)->err = std::string(#call) + " (line " + std::to_string(__LINE__) + "): " + cudaGetErrorString(e_); \
       return CCG_E_CUDA;                                                                   \
     }                                                                                      \
   } while (0)
@@ -205,7 +210,11 @@ static void launch_k(ccg_ctx* c, void (*kern)(KArgs...), dim3 grid, dim3 block, 
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+  if (e != cudaSuccess) {
+    fprintf(stderr, "libccg: launch failed (%s): grid %u,%u,%u block %u smem %zu\n", cudaGetErrorString(e), grid.x,
+            grid.y, grid.z, block.x, smem);
+  }
 }
 
 static bool is_device_ptr(const void* p) {
@@ -324,6 +333,17 @@ struct Engine {
     return post<Op>(c, gate);
   }
 
+  // a K = 0 elementwise pass over `count` elements (the whole vector)
+  template <class Op>
+  static int pass_count(ccg_ctx* c, Op op, int64_t count, const int* gate) {
+    static_assert(Op::K == 0, "pass_count: no reduction");
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((count + NT - 1) / NT, (int64_t)c->sm_count * 8));
+    launch_k(c, pass_kernel<NT, Op>, grid, NT, 0, c->stream, op, count, make_red(c), c->st, gate);
+    c->launches++;
+    CK(c, cudaGetLastError());
+    return CCG_OK;
+  }
+
   // CSR SpMV: CSR-stream blocks (default) or LPR lanes per row (CCG_SPMV=lanes)
   template <bool CONJ, class Epi>
   static void spmv(ccg_ctx* c, const C* x, Epi epi, const int* gate) {
@@ -418,6 +438,11 @@ struct Engine {
   // y_local = A · xfull (full-length buffer, own slice + gathered/halo parts)
   template <class Epi>
   static int matvec_a(ccg_ctx* c, const C* xfull, Epi epi, const int* gate) {
+    if (c->jac_active) {   // B·v = A(D⁻¹v): scale the (whole) input first
+      C* tmp = reinterpret_cast<C*>(c->jac_tmp);
+      TRY(pass_count(c, JacScale<T>{xfull, reinterpret_cast<const C*>(c->jac_dinv), tmp}, c->n, gate));
+      xfull = tmp;
+    }
     if (c->opk == OPK_CALLBACK) return user_product(c, CCG_OP_A, xfull, epi, gate);
     if (c->rep && c->opk != OPK_TOEPLITZ) {
       TRY(matvec_rows(c, xfull, Store<T>{reinterpret_cast<C*>(c->rep_tmp) + c->mrow0}, gate));
@@ -510,6 +535,14 @@ struct Engine {
   // in rank order inside the epilogue pass.
   template <class Epi>
   static int matvec_h(ccg_ctx* c, const C* xloc, bool conj, Epi epi, const int* gate) {
+    if (c->jac_active) {   // Bᴴv = conj(D⁻¹)(Aᴴv), Bᵀv = D⁻¹(Aᵀv): scale inside the epilogue
+      JacEpi<T, Epi> je{epi, reinterpret_cast<const C*>(c->jac_dinv) + c->row0, conj ? 1 : 0};
+      return matvec_h_impl(c, xloc, conj, je, gate);
+    }
+    return matvec_h_impl(c, xloc, conj, epi, gate);
+  }
+  template <class Epi>
+  static int matvec_h_impl(ccg_ctx* c, const C* xloc, bool conj, Epi epi, const int* gate) {
     const bool gathered_in = c->world > 1 && !c->rep;   // the input needs gathering first
     if (c->opk == OPK_CALLBACK) {
       const C* xin = xloc;
@@ -694,7 +727,7 @@ struct Engine {
     const int* g = &c->st->done;
     TRY(pass(c, QmP<T>{L(c, 5), L(c, 6), Fs(c, 0), L(c, 7)}, g));
     TRY(allgather(c, 0));
-    if (c->opk == OPK_DENSE && c->cols_ok && c->qmr_dual && !c->rep) {
+    if (c->opk == OPK_DENSE && c->cols_ok && c->qmr_dual && !c->rep && !c->jac_active) {
       TRY(matvec_dual(c, F(c, 0), L(c, 7), QmPt<T>{L(c, 8), L(c, 7)},
                       QmVW<T>{L(c, 3), L(c, 4), L(c, 8), L(c, 5), L(c, 6)}, g));
     } else {
@@ -840,7 +873,7 @@ struct Engine {
   // A·p and Aᴴ·p̃ of one BiCG iteration are independent: dual GEMV when dense
   template <class EpiA, class EpiH>
   static int matvec_pair(ccg_ctx* c, int pfull_idx, const C* qloc, EpiA ea, EpiH eh, const int* gate) {
-    if (c->opk == OPK_DENSE && c->cols_ok && c->qmr_dual && !c->rep)
+    if (c->opk == OPK_DENSE && c->cols_ok && c->qmr_dual && !c->rep && !c->jac_active)
       return matvec_dual(c, F(c, pfull_idx), qloc, ea, eh, gate);
     TRY(matvec_a(c, F(c, pfull_idx), ea, gate));
     return matvec_h(c, qloc, true, eh, gate);
@@ -1062,6 +1095,16 @@ struct Engine {
     TRY(pass(c, Copy<T>{L(c, X), Fs(c, 2)}, g));
     TRY(allgather(c, 2));
     return matvec_a(c, F(c, 2), TrueRes<T>{L(c, 1)}, g);
+  }
+
+  // right Jacobi around a solve: u₀ = D·x₀ before, x = D⁻¹·u after
+  static int jac_in(ccg_ctx* c) {
+    return pass_count(c, JacScale<T>{L(c, X), reinterpret_cast<const C*>(c->jac_d) + c->row0, L(c, X)}, c->nloc,
+                      c->zero_gate);
+  }
+  static int jac_out(ccg_ctx* c) {
+    return pass_count(c, JacScale<T>{L(c, X), reinterpret_cast<const C*>(c->jac_dinv) + c->row0, L(c, X)}, c->nloc,
+                      c->zero_gate);
   }
 
   // ccg_apply
@@ -1774,6 +1817,57 @@ int ccg_set_gmres_restart(ccg_handle c, int32_t m) {
   return CCG_OK;
 }
 
+int ccg_set_jacobi(ccg_handle c, const void* diag_local, uint32_t flags) {
+  if (!c) return CCG_E_ARG;
+  (void)flags;
+  CK(c, cudaSetDevice(c->device));
+  invalidate_graphs(c);
+  if (!diag_local) {
+    if (c->jac_d) cudaFree(c->jac_d);
+    if (c->jac_dinv) cudaFree(c->jac_dinv);
+    if (c->jac_tmp) cudaFree(c->jac_tmp);
+    c->jac_d = c->jac_dinv = c->jac_tmp = nullptr;
+    return CCG_OK;
+  }
+  // host copy of this rank's diagonal, validated, inverted in double; the whole
+  // d and 1/d are allgathered so every rank can scale whole product inputs
+  const size_t es = c->esz;
+  std::vector<unsigned char> hd((size_t)c->mnloc * es);
+  if (is_device_ptr(diag_local)) CK(c, cudaMemcpy(hd.data(), diag_local, hd.size(), cudaMemcpyDeviceToHost));
+  else memcpy(hd.data(), diag_local, hd.size());
+  std::vector<unsigned char> hinv(hd.size());
+  for (int64_t i = 0; i < c->mnloc; ++i) {
+    double re, im;
+    if (es == 8) { re = reinterpret_cast<float*>(hd.data())[2 * i]; im = reinterpret_cast<float*>(hd.data())[2 * i + 1]; }
+    else { re = reinterpret_cast<double*>(hd.data())[2 * i]; im = reinterpret_cast<double*>(hd.data())[2 * i + 1]; }
+    if (!(std::isfinite(re) && std::isfinite(im)) || (re == 0.0 && im == 0.0))
+      FAIL(c, CCG_E_ARG, "Jacobi: diagonal entries must be finite and nonzero");
+    const std::complex<double> inv = 1.0 / std::complex<double>(re, im);
+    if (es == 8) {
+      reinterpret_cast<float*>(hinv.data())[2 * i] = (float)inv.real();
+      reinterpret_cast<float*>(hinv.data())[2 * i + 1] = (float)inv.imag();
+    } else {
+      reinterpret_cast<double*>(hinv.data())[2 * i] = inv.real();
+      reinterpret_cast<double*>(hinv.data())[2 * i + 1] = inv.imag();
+    }
+  }
+  const size_t full = (size_t)c->n * es;
+  if (!c->jac_d) CK(c, cudaMalloc(&c->jac_d, full));
+  if (!c->jac_dinv) CK(c, cudaMalloc(&c->jac_dinv, full));
+  if (!c->jac_tmp) CK(c, cudaMalloc(&c->jac_tmp, full));
+  CK(c, cudaMemcpy(static_cast<char*>(c->jac_d) + (size_t)c->mrow0 * es, hd.data(), hd.size(), cudaMemcpyHostToDevice));
+  CK(c, cudaMemcpy(static_cast<char*>(c->jac_dinv) + (size_t)c->mrow0 * es, hinv.data(), hinv.size(),
+                   cudaMemcpyHostToDevice));
+  if (c->world > 1) {
+    const CommType t = es == 8 ? CT_F32 : CT_F64;
+    int r = c->comm->allgather_inplace(c->jac_d, (size_t)c->mnloc * 2, t, c->stream);
+    if (!r) r = c->comm->allgather_inplace(c->jac_dinv, (size_t)c->mnloc * 2, t, c->stream);
+    if (r) FAIL(c, r, c->comm->err);
+    CK(c, cudaStreamSynchronize(c->stream));
+  }
+  return CCG_OK;
+}
+
 int ccg_set_bicgstab_ell(ccg_handle c, int32_t ell) {
   if (!c) return CCG_E_ARG;
   if (ell < 1 || ell > BL_MAX) FAIL(c, CCG_E_ARG, "BiCGstab(l): l must be in [1, 4]");
@@ -1805,16 +1899,17 @@ static int gmres_workspace(ccg_ctx* c) {
   const size_t need = (size_t)(c->gm_m + 1) * (size_t)c->nloc * c->esz;
   if (need > c->gm_V_bytes) {
     if (c->gm_V) cudaFree(c->gm_V);
-  if (c->bl_buf) cudaFree(c->bl_buf);
     c->gm_V = nullptr;
     c->gm_V_bytes = 0;
     CK(c, cudaMalloc(&c->gm_V, need));
     c->gm_V_bytes = need;
     invalidate_graphs(c);
   }
-  if (!c->gm_dev) {
+  if (!c->gm_dev) {   // (BiCGstab(ℓ) may have allocated the scratch already)
     CK(c, cudaMalloc(&c->gm_dev, sizeof(GmDev)));
     CK(c, cudaMemset(c->gm_dev, 0, sizeof(GmDev)));
+  }
+  if (!c->gm_part) {
     c->gm_grid = (int)std::max<int64_t>(1, std::min<int64_t>((c->nloc + GM_NT - 1) / GM_NT, (int64_t)c->sm_count * 4));
     CK(c, cudaMalloc(&c->gm_part, (size_t)c->gm_grid * (GM_MAX + 1) * sizeof(double2)));
     CK(c, cudaMalloc(&c->gm_ticket, sizeof(unsigned)));
@@ -1942,8 +2037,15 @@ int ccg_solve(ccg_handle c, ccg_method method, const void* x0_local, const void*
   }
   const bool has_x0 = x0_local != nullptr;
   int rc;
+  if (c->jac_dinv) {
+    c->jac_active = true;
+    if (has_x0) {
+      rc = c->dtype == CCG_C64 ? Engine<float>::jac_in(c) : Engine<double>::jac_in(c);
+      if (rc) { c->jac_active = false; return rc; }
+    }
+  }
   if (c->opk == OPK_DENSE && c->cluster_ok && c->world == 1 && !c->timing && method != CCG_GMRES &&
-      method != CCG_BICGSTABL) {
+      method != CCG_BICGSTABL && !c->jac_dinv) {
     // small dense system: setup, every iteration and the true residual in ONE
     // cluster launch (cluster.cuh); maxit and the stopping rule live in the State
     c->cl_method = method;
@@ -1956,6 +2058,11 @@ int ccg_solve(ccg_handle c, ccg_method method, const void* x0_local, const void*
     rc = c->dtype == CCG_C64 ? run_iterations<float>(c, method, maxit) : run_iterations<double>(c, method, maxit);
     if (rc) return rc;
     rc = c->dtype == CCG_C64 ? Engine<float>::true_residual(c) : Engine<double>::true_residual(c);
+    if (rc) { c->jac_active = false; return rc; }
+  }
+  if (c->jac_active) {
+    c->jac_active = false;
+    rc = c->dtype == CCG_C64 ? Engine<float>::jac_out(c) : Engine<double>::jac_out(c);
     if (rc) return rc;
   }
   CK(c, cudaMemcpyAsync(c->st_host, c->st, sizeof(State), cudaMemcpyDeviceToHost, c->stream));
@@ -2037,6 +2144,9 @@ int ccg_destroy(ccg_handle c) {
   if (c->hist) cudaFree(c->hist);
   if (c->gm_V) cudaFree(c->gm_V);
   if (c->bl_buf) cudaFree(c->bl_buf);
+  if (c->jac_d) cudaFree(c->jac_d);
+  if (c->jac_dinv) cudaFree(c->jac_dinv);
+  if (c->jac_tmp) cudaFree(c->jac_tmp);
   if (c->gm_dev) cudaFree(c->gm_dev);
   if (c->gm_part) cudaFree(c->gm_part);
   if (c->gm_ticket) cudaFree(c->gm_ticket);

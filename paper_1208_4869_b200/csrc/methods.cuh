@@ -1193,4 +1193,31 @@ struct BlM {  // x += Î£ Î³_j rÌ‚_{jâˆ’1} ; rÌ‚â‚€ âˆ’= Î£ Î³_j rÌ‚_j ; Ã»â‚€ âˆ
   }
 };
 
+// ---- right Jacobi preconditioning (SURVEY Â§8(f) NEXT-4): B = AÂ·Dâ»Â¹
+template <typename T>
+struct JacScale {  // out = s âŠ™ x  (product input Dâ»Â¹x; xâ‚€ â†’ D xâ‚€; exit x = Dâ»Â¹u)
+  static constexpr int K = 0;
+  using C = Cx<T>;
+  const C* x; const C* s; C* out;
+  __device__ void load(const State*) {}
+  __device__ void operator()(int64_t i, double2*) { out[i] = cmul(s[i], x[i]); }
+  static __device__ void finish(State*, const double2*) {}
+};
+
+template <typename T, class Epi>
+struct JacEpi {  // Bá´´v = conj(Dâ»Â¹)(Aá´´v), Báµ€v = Dâ»Â¹(Aáµ€v): scale the product, then the method epilogue
+  static constexpr int K = Epi::K;
+  using C = Cx<T>;
+  Epi epi;
+  const C* dinv;   // at the output's index origin
+  int conj;
+  __device__ void load(const State* st) { epi.load(st); }
+  __device__ void operator()(int64_t i, C val, double2* acc) {
+    C s = dinv[i];
+    if (conj) s.y = -s.y;
+    epi(i, cmul(s, val), acc);
+  }
+  static __device__ void finish(State* st, const double2* sm) { Epi::finish(st, sm); }
+};
+
 }  // namespace ccg

@@ -342,3 +342,27 @@ def test_replicated_csr_stencil_toeplitz(G):
         assert rt["status"] == "CONVERGED" and abs(rt["iterations"] - ot.iterations) <= 2
     finally:
         g.close()
+
+
+@pytest.mark.parametrize("options", [0, 1])
+@pytest.mark.parametrize("G", [2, 4])
+def test_sharded_jacobi(G, options):
+    """Right Jacobi with the row-sharded and the replicated-vector layouts."""
+    rng = np.random.default_rng(12)
+    n = 256
+    d = np.logspace(0, 4, n) * np.exp(1j * rng.uniform(0, 2 * np.pi, n))
+    A = (np.diag(d) + 0.3 * (rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))) / np.sqrt(n))
+    A = A.astype(np.complex128)
+    y = (rng.standard_normal(n) + 1j * rng.standard_normal(n)).astype(np.complex128)
+    g = DenseGroup(A, G, options=options)
+    try:
+        _threads(G, lambda r: ccg.ccg_set_jacobi(g.hs[r], to_dev(d[r * g.nloc:(r + 1) * g.nloc].copy())))
+        for method in ("bicgstab", "qmr", "gmres"):
+            o = oracle.solve_jacobi(method, DenseOp(A), d, y, 1e-10, 500)
+            r = g.solve(method, y, 1e-10, 500)
+            assert r["status"] == "CONVERGED" and abs(r["iterations"] - o.iterations) <= 2, method
+            k = min(r["iterations"], o.iterations)
+            assert relerr(g.solve(method, y, 0.0, k)["x"],
+                          oracle.solve_jacobi(method, DenseOp(A), d, y, 0.0, k).x) <= 1e-9, method
+    finally:
+        g.close()

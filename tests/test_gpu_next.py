@@ -575,3 +575,78 @@ def test_bicgstabl_ells(ell):
         with pytest.raises(ccg.CcgError) as e:
             ccg.ccg_set_bicgstab_ell(h.h, 5)
         assert e.value.code == -1
+
+
+# ---------------------------------------------------------------------------
+# Right Jacobi preconditioning (ccg_set_jacobi; NEXT-4)
+# ---------------------------------------------------------------------------
+def _badly_scaled(n, seed=12):
+    rng = np.random.default_rng(seed)
+    d = np.logspace(0, 4, n) * np.exp(1j * rng.uniform(0, 2 * np.pi, n))
+    A = np.diag(d) + 0.3 * (rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))) / np.sqrt(n)
+    y = rng.standard_normal(n) + 1j * rng.standard_normal(n)
+    return A.astype(np.complex128), d.astype(np.complex128), y.astype(np.complex128)
+
+
+@pytest.mark.parametrize("method", ["bicgstab", "qmr", "cgne", "bicor", "gmres", "bicgstabl", "tfqmr", "cgnr"])
+def test_jacobi_badly_scaled(method):
+    """A diagonal spanning four decades: unpreconditioned the methods stall,
+    with right Jacobi they converge in a handful of iterations — GPU against the
+    oracle's preconditioned solve (P-literal), x = D⁻¹u returned."""
+    n = 300
+    A, d, y = _badly_scaled(n)
+    o = oracle.solve_jacobi(method, DenseOp(A), d, y, 1e-10, 3000)
+    with Dense(A) as h:
+        ccg.ccg_set_jacobi(h.h, to_dev(d))
+        g = h.solve(method, y, 1e-10, 3000)
+        assert g["status"] == o.status_name == "CONVERGED", (g["status"], o.status_name)
+        assert abs(g["iterations"] - o.iterations) <= 2 and g["iterations"] <= 60
+        assert g["true_rel_res"] <= 1e-9
+        k = min(g["iterations"], o.iterations)
+        ge = h.solve(method, y, 0.0, k)
+        oe = oracle.solve_jacobi(method, DenseOp(A), d, y, 0.0, k)
+        assert relerr(ge["x"], oe.x) <= 1e-9
+        xs = np.linalg.solve(A, y)
+        gx = h.solve(method, y, 1e-10, 3000, x0=0.5 * xs)
+        ox = oracle.solve_jacobi(method, DenseOp(A), d, y, 1e-10, 3000, x0=0.5 * xs)
+        assert abs(gx["iterations"] - ox.iterations) <= 2 and relerr(gx["x"], xs) <= 1e-8
+        ccg.ccg_set_jacobi(h.h, None)                 # disabled again: the plain method
+        gp = h.solve(method, y, 1e-10, 200)
+        assert gp["iterations"] > 2 * g["iterations"] or gp["status"] != "CONVERGED"
+
+
+def test_jacobi_constant_diagonal_cfg1():
+    A, y = cfg1()
+    with Dense(A) as h:
+        g0 = h.solve("bicgstab", y, 1e-10, 500)
+        ccg.ccg_set_jacobi(h.h, np.full(256, 3 - 4j))
+        g1 = h.solve("bicgstab", y, 1e-10, 500)
+    assert g0["iterations"] == g1["iterations"]
+    assert relerr(g1["x"], g0["x"]) <= 1e-9
+    h2 = ccg.ccg_create("c128", 4)
+    try:
+        with pytest.raises(ccg.CcgError) as e:
+            ccg.ccg_set_jacobi(h2, np.array([1, 2, 0, 4], np.complex128))
+        assert e.value.code == -1
+    finally:
+        ccg.ccg_destroy(h2)
+
+
+def test_workspaces_coexist_on_one_handle():
+    """GMRES, BiCGstab(ℓ) and Jacobi workspaces allocated in any order on one
+    handle stay valid (each method repeated after the others allocated)."""
+    n = 300
+    A, d, y = _badly_scaled(n, seed=21)
+    with Dense(A) as h:
+        ccg.ccg_set_jacobi(h.h, to_dev(d))
+        ref = {m: oracle.solve_jacobi(m, DenseOp(A), d, y, 1e-10, 500) for m in ("bicgstabl", "gmres", "bicgstab")}
+        for m in ("bicgstabl", "gmres", "bicgstabl", "bicgstab", "gmres"):
+            g = h.solve(m, y, 1e-10, 500)
+            assert g["status"] == "CONVERGED" and abs(g["iterations"] - ref[m].iterations) <= 2, m
+            assert relerr(g["x"], ref[m].x) <= 1e-8, m
+        ccg.ccg_set_gmres_restart(h.h, 7)
+        ccg.ccg_set_bicgstab_ell(h.h, 3)
+        for m, kw in (("gmres", {"restart": 7}), ("bicgstabl", {"ell": 3})):
+            o = oracle.solve_jacobi(m, DenseOp(A), d, y, 1e-10, 500, **kw)
+            g = h.solve(m, y, 1e-10, 500)
+            assert abs(g["iterations"] - o.iterations) <= 2 and relerr(g["x"], o.x) <= 1e-8, m
