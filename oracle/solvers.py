@@ -747,15 +747,82 @@ def _bicgstabl(op, y, x, r, r0sq, tol2, maxit, ctx, hist, st, ell=2, shadow=None
             raise _Breakdown("omega")
 
 
+def _pbicgstab(op, y, x, r, r0sq, tol2, maxit, ctx, hist, st, shadow=None):
+    """Pipelined BiCGSTAB (SURVEY §8(f) NEXT-2 iii; Cools–Vanroose's
+    communication-hiding form): the same iterates as O1 in exact arithmetic
+    (pinned), with the auxiliary recurrences s = A p, z = A s, w = A r,
+    t = A w, v = A z so that each iteration needs TWO reduction phases, each
+    independent of the product that follows it ({⟨q,y⟩, ⟨y,y⟩, ‖q‖²} ∥ v = A z;
+    {⟨r̃,r⟩, ⟨r̃,w⟩, ⟨r̃,s⟩, ⟨r̃,z⟩, ‖r‖²} ∥ t = A w).  Half-step exit on ‖q‖ (q is
+    O1's s) as Q4."""
+    rt = r.copy() if shadow is None else np.asarray(shadow, dtype=y.dtype)
+    st["k"] = 1                         # the setup products and α₀ belong to iteration 1
+    w = op.apply(r)                                             # w₀ = A r₀
+    t = op.apply(w)                                             # t₀ = A w₀
+    rho = ctx.c(ctx.dotc(rt, r))                                # ρ₀ = ⟨r̃, r₀⟩
+    ctx.check(rho)
+    if rho == 0:
+        raise _Breakdown("rho")
+    alpha = ctx.c(ctx.div(rho, ctx.c(ctx.dotc(rt, w)), "sigma"))   # α₀ = ρ₀/⟨r̃, w₀⟩
+    beta = omega = ctx.c(0)
+    p = s = z = v = None
+    for k in range(1, maxit + 1):
+        st["k"] = k
+        if k == 1:
+            p, s, z = r.copy(), w.copy(), t.copy()
+        else:
+            p = r + beta * (p - omega * s)                      # p = r + β(p − ωs)
+            s = w + beta * (s - omega * z)                      # s = w + β(s − ωz)
+            z = t + beta * (z - omega * v)                      # z = t + β(z − ωv)
+        q = r - alpha * s                                       # q = r − αs
+        yv = w - alpha * z                                      # y = w − αz
+        qq = ctx.r(ctx.norm_sq(q))
+        ctx.check(qq)
+        if _conv(qq, tol2, r0sq):                               # half-step exit (Q4)
+            st["x"] = x = x + alpha * p
+            hist.append(sqrt(qq))
+            return CONVERGED, k, True
+        qy = ctx.c(ctx.dotc(yv, q))                             # ⟨y, q⟩
+        yy = ctx.r(ctx.norm_sq(yv))                             # ⟨y, y⟩
+        v = op.apply(z)                                         # v = A z
+        omega = ctx.c(ctx.div(qy, yy, "tt"))                    # ω = ⟨y,q⟩/⟨y,y⟩
+        if omega == 0:
+            raise _Breakdown("omega")
+        st["x"] = x = x + alpha * p + omega * q                 # x += αp + ωq
+        r = q - omega * yv                                      # r = q − ωy
+        w = yv - omega * (t - alpha * v)                        # w = y − ω(t − αv)
+        rr = ctx.r(ctx.norm_sq(r))
+        ctx.check(rr)
+        hist.append(sqrt(rr))
+        if _conv(rr, tol2, r0sq):
+            return CONVERGED, k, False
+        if k == maxit:              # no further iterate needs the next products (R2)
+            break
+        rho_new = ctx.c(ctx.dotc(rt, r))                        # ⟨r̃, r⟩
+        rw = ctx.c(ctx.dotc(rt, w))                             # ⟨r̃, w⟩
+        rs_ = ctx.c(ctx.dotc(rt, s))                            # ⟨r̃, s⟩
+        rz = ctx.c(ctx.dotc(rt, z))                             # ⟨r̃, z⟩
+        t = op.apply(w)                                         # t = A w
+        ctx.check(rho_new)
+        if rho_new == 0:
+            raise _Breakdown("rho")
+        beta = ctx.c((alpha / omega) * (rho_new / rho))         # β = (α/ω) ρ'/ρ
+        rho = rho_new
+        alpha = ctx.c(ctx.div(rho, ctx.c(rw + beta * rs_ - beta * omega * rz), "sigma"))
+    return MAXIT, maxit, False
+
+
 METHODS = {
     "bicgstab": _bicgstab, "cgne": _cgne, "qmr": _qmr, "bicor": _bicor,
     "cors": _cors,
     # SURVEY §8(f) NEXT-3
     "bicg": _bicg, "cgs": _cgs, "cocr": _cocr, "cgnr": _cgnr, "tfqmr": _tfqmr,
     "gmres": _gmres, "bicgstabl": _bicgstabl,
+    "pbicgstab": _pbicgstab,    # NEXT-2 (iii)
 }
 HOT_PATH = ("bicgstab", "cgne", "qmr", "bicor", "cors")
 NEXT3 = ("bicg", "cgs", "cocr", "cgnr", "tfqmr", "gmres", "bicgstabl")
+NEXT2 = ("pbicgstab",)
 
 
 def solve(method, op, y, tol, maxit, x0=None, dots=None, **kw):
