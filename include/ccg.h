@@ -75,8 +75,11 @@ typedef enum {
   CCG_TFQMR = 9,  /* P:57 [§2.1]; stops on Freund's bound τ_m·√(m+1) ≤ tol·‖r₀‖ (R9) */
   CCG_GMRES = 10, /* restarted GMRES(m), P:57 [§2.1] "rgmres"; m from ccg_set_gmres_restart (default 30);
                      iterations = Arnoldi steps, + one A·x per restart (R12-R15) */
-  CCG_BICGSTABL = 11 /* BiCGstab(ℓ), P:79 [§3.1] (vanilla); ℓ from ccg_set_bicgstab_ell (default 2);
+  CCG_BICGSTABL = 11, /* BiCGstab(ℓ), P:79 [§3.1] (vanilla); ℓ from ccg_set_bicgstab_ell (default 2);
                         iterations = BiCG steps, two A·x each (R16-R18) */
+  CCG_PBICGSTAB = 12 /* pipelined BiCGSTAB (SURVEY §8(f) NEXT-2 iii): BiCGSTAB's iterates in exact
+                        arithmetic with two reduction phases per iteration, each independent of the
+                        product that follows it (2 A·x per iteration + 2 at setup, the last skipped) */
 } ccg_method;
 
 /* The three products of the operator module: A·x (matvec),

@@ -21,7 +21,8 @@ LIB_PATH = os.path.join(_HERE, "libccg.so")
 
 C64, C128 = 0, 1
 METHODS = {"bicgstab": 0, "cgne": 1, "qmr": 2, "bicor": 3, "cors": 4,
-           "bicg": 5, "cgs": 6, "cocr": 7, "cgnr": 8, "tfqmr": 9, "gmres": 10, "bicgstabl": 11}
+           "bicg": 5, "cgs": 6, "cocr": 7, "cgnr": 8, "tfqmr": 9, "gmres": 10, "bicgstabl": 11,
+           "pbicgstab": 12}
 OPS = {"A": 0, "AH": 1, "AT": 2}
 FLAG_SYMMETRIC = 1
 STATUS = {0: "CONVERGED", 1: "MAXIT", 2: "BREAKDOWN", 3: "FALSE_CONVERGENCE", 4: "NONFINITE"}

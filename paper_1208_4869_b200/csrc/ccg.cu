@@ -1056,6 +1056,28 @@ struct Engine {
     }
   }
 
+  // ---- p-BiCGSTAB: loc: 0 x, 1 y, 2 r, 3 r̃, 4 p, 5 s, 6 q, 7 y, 8 v, 9 t ; full: 0 z (r₀ at setup), 1 w
+  static int pbicgstab_setup(ccg_ctx* c, bool x0) {
+    const int* g = &c->st->done;
+    TRY(init_residual(c, x0, L(c, 2), L(c, 3), Fs(c, 0), nullptr));
+    TRY(allgather(c, 0));
+    TRY(matvec_a(c, F(c, 0), PbW0<T>{Fs(c, 1), L(c, 3)}, g));
+    TRY(allgather(c, 1));
+    return matvec_a(c, F(c, 1), PbStore<T>{L(c, 9)}, g);
+  }
+  static int pbicgstab_iter(ccg_ctx* c) {
+    const int* g = &c->st->done;
+    const int* g2 = &c->st->gate2;
+    TRY(pass(c, PbP1<T>{L(c, 2), Fs(c, 1), L(c, 9), L(c, 8), L(c, 4), L(c, 5), Fs(c, 0), L(c, 6), L(c, 7)}, g));
+    TRY(allgather(c, 0));
+    TRY(matvec_a(c, F(c, 0), PbStore<T>{L(c, 8)}, g2));
+    TRY(pass(c, PbP2<T>{L(c, X), L(c, 2), Fs(c, 1), L(c, 4), L(c, 6), L(c, 7), L(c, 9), L(c, 8), L(c, 5), Fs(c, 0),
+                        L(c, 3)},
+             g));
+    TRY(allgather(c, 1));
+    return matvec_a(c, F(c, 1), PbT<T>{L(c, 9)}, g);
+  }
+
   static int setup(ccg_ctx* c, int m, bool x0) {
     switch (m) {
       case M_BICGSTAB: return bicgstab_setup(c, x0);
@@ -1069,6 +1091,7 @@ struct Engine {
       case M_TFQMR: return tfqmr_setup(c, x0);
       case M_GMRES: return gmres_setup(c, x0);
       case M_BICGSTABL: return bicgstabl_setup(c, x0);
+      case M_PBICGSTAB: return pbicgstab_setup(c, x0);
       default: return cgnr_setup(c, x0);
     }
   }
@@ -1085,6 +1108,7 @@ struct Engine {
       case M_TFQMR: return tfqmr_iter(c);
       case M_GMRES: return gmres_iter(c);
       case M_BICGSTABL: return bicgstabl_iter(c);
+      case M_PBICGSTAB: return pbicgstab_iter(c);
       default: return cgnr_iter(c);
     }
   }
@@ -2045,7 +2069,7 @@ int ccg_solve(ccg_handle c, ccg_method method, const void* x0_local, const void*
     }
   }
   if (c->opk == OPK_DENSE && c->cluster_ok && c->world == 1 && !c->timing && method != CCG_GMRES &&
-      method != CCG_BICGSTABL && !c->jac_dinv) {
+      method != CCG_BICGSTABL && method != CCG_PBICGSTAB && !c->jac_dinv) {
     // small dense system: setup, every iteration and the true residual in ONE
     // cluster launch (cluster.cuh); maxit and the stopping rule live in the State
     c->cl_method = method;

@@ -172,6 +172,7 @@ struct State {
   double tau;      // TFQMR τ_m
   void* gm;        // GmDev* (GMRES; BiCGstab(ℓ) scratch)
   int bl_l;        // BiCGstab(ℓ): ℓ
+  double2 pb_rho, pb_rw, pb_rs, pb_rz;   // p-BiCGSTAB: ⟨r̃,r⟩, ⟨r̃,w⟩, ⟨r̃,s⟩, ⟨r̃,z⟩ of the last phase
   int fin;         // TFQMR: converged at the second half-step, x update pending
   double ss;
 };
@@ -181,7 +182,7 @@ enum { BD_NONE = 0, BD_RHO = 1, BD_SIGMA = 2, BD_TT = 3, BD_OMEGA = 4, BD_PI = 5
        BD_EPSILON = 7, BD_BETA = 8, BD_XI = 9, BD_VNORM = 10, BD_WNORM = 11, BD_GAMMA = 12 };
 enum { M_BICGSTAB = 0, M_CGNE = 1, M_QMR = 2, M_BICOR = 3, M_CORS = 4,
        M_BICG = 5, M_CGS = 6, M_COCR = 7, M_CGNR = 8, M_TFQMR = 9, M_GMRES = 10,
-       M_BICGSTABL = 11, M_COUNT = 12 };
+       M_BICGSTABL = 11, M_PBICGSTAB = 12, M_COUNT = 13 };
 
 __device__ __forceinline__ void set_done(State* st, int status, int iters, int bd = BD_NONE) {
   st->done = 1; st->gate2 = 1; st->status = status; st->iterations = iters; st->breakdown = bd;

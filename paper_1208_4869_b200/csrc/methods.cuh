@@ -63,6 +63,7 @@ struct InitR {
     switch (st->method) {
       case M_BICGSTAB:
       case M_BICG:
+      case M_PBICGSTAB:
       case M_CGS: st->rho = make_double2(rr, 0.0); break;
       case M_GMRES: {
         GmDev* gm = reinterpret_cast<GmDev*>(st->gm);
@@ -1190,6 +1191,128 @@ struct BlM {  // x += Î£ Î³_j rÌ‚_{jâˆ’1} ; rÌ‚â‚€ âˆ’= Î£ Î³_j rÌ‚_j ; Ã»â‚€ âˆ
     if (zzero(st->omega)) { set_done(st, ST_BREAKDOWN, k - 1, BD_OMEGA); return; }
     st->rho = zmul(make_double2(-st->omega.x, -st->omega.y), st->rho);   // Ïâ‚€ = âˆ’Ï‰ Ïâ‚€
     bl_next_beta(st, s[1]);
+  }
+};
+
+// ---- pipelined BiCGSTAB (SURVEY Â§8(f) NEXT-2 iii; oracle _pbicgstab).
+// Setup: [A r â†’ w, Ïƒ â†’ Î±] [A w â†’ t].  Per iteration: P1 (p, s, z, q, y;
+// â€–qâ€–Â², âŸ¨y,qâŸ©, â€–yâ€–Â² â†’ half-step test, Ï‰) â†’ [A z â†’ v] â†’ P2 (x, r, w; â€–râ€–Â²,
+// âŸ¨rÌƒ,râŸ©, âŸ¨rÌƒ,wâŸ©, âŸ¨rÌƒ,sâŸ©, âŸ¨rÌƒ,zâŸ©) â†’ [A w â†’ t; then Î², Î±].
+template <typename T>
+struct PbW0 {  // setup: wâ‚€ = A râ‚€ ; Î±â‚€ = Ïâ‚€/âŸ¨rÌƒ, wâ‚€âŸ©
+  static constexpr int K = 1;
+  using C = Cx<T>;
+  C* w; const C* rt;
+  __device__ void load(const State*) {}
+  __device__ void operator()(int64_t i, C val, double2* acc) { w[i] = val; dotc_acc(acc[0], rt[i], val); }
+  static __device__ void finish(State* st, const double2* s) { st->matvecs_a++; sigma_step(st, s[0]); }
+};
+
+template <typename T>
+struct PbStore {  // a product stored (v = A z, tâ‚€ = A wâ‚€); counts it
+  static constexpr int K = 1;
+  using C = Cx<T>;
+  C* out;
+  __device__ void load(const State*) {}
+  __device__ void operator()(int64_t i, C val, double2*) { out[i] = val; }
+  static __device__ void finish(State* st, const double2*) { st->matvecs_a++; }
+};
+
+template <typename T>
+struct PbP1 {  // p, s, z updates ; q = r âˆ’ Î±s ; y = w âˆ’ Î±z ; â€–qâ€–Â², âŸ¨y,qâŸ©, â€–yâ€–Â²
+  static constexpr int K = 3;
+  using C = Cx<T>;
+  const C* r; const C* w; const C* t; const C* v; C* p; C* s; C* z; C* q; C* y;
+  C alpha, beta, omega; int first;
+  __device__ void load(const State* st) {
+    first = st->iter == 0;
+    alpha = fromd2<C>(st->alpha); beta = fromd2<C>(st->beta); omega = fromd2<C>(st->omega);
+  }
+  __device__ void operator()(int64_t i, double2* acc) {
+    C pi, si, zi;
+    if (first) { pi = r[i]; si = w[i]; zi = t[i]; }
+    else {
+      pi = caxpy(r[i], beta, caxmy(p[i], omega, s[i]));
+      si = caxpy(w[i], beta, caxmy(s[i], omega, z[i]));
+      zi = caxpy(t[i], beta, caxmy(z[i], omega, v[i]));
+    }
+    p[i] = pi; s[i] = si; z[i] = zi;
+    const C qi = caxmy(r[i], alpha, si), yi = caxmy(w[i], alpha, zi);
+    q[i] = qi; y[i] = yi;
+    nrm_acc(acc[0], qi);
+    dotc_acc(acc[1], yi, qi);
+    nrm_acc(acc[2], yi);
+  }
+  static __device__ void finish(State* st, const double2* sm) {
+    const int k = st->iter + 1;
+    const double qq = sm[0].x;
+    if (!isfinite(qq)) { set_done(st, ST_NONFINITE, k - 1); return; }
+    st->ss = qq;
+    if (qq <= st->tol2r0) { st->half = 1; st->gate2 = 1; return; }
+    const double yy = sm[2].x;
+    if (yy == 0.0) { set_done(st, ST_BREAKDOWN, k - 1, BD_TT); return; }
+    st->omega = make_double2(sm[1].x / yy, sm[1].y / yy);
+    if (!zfinite(st->omega)) { set_done(st, ST_NONFINITE, k - 1); return; }
+    if (zzero(st->omega)) { set_done(st, ST_BREAKDOWN, k - 1, BD_OMEGA); return; }
+  }
+};
+
+template <typename T>
+struct PbP2 {  // x += Î±p + Ï‰q ; r = q âˆ’ Ï‰y ; w = y âˆ’ Ï‰(t âˆ’ Î±v) ; â€–râ€–Â², âŸ¨rÌƒ,râŸ©, âŸ¨rÌƒ,wâŸ©, âŸ¨rÌƒ,sâŸ©, âŸ¨rÌƒ,zâŸ©
+  static constexpr int K = 5;            // (half-step: x += Î±p only)
+  using C = Cx<T>;
+  C* x; C* r; C* w; const C* p; const C* q; const C* y; const C* t; const C* v; const C* s; const C* z;
+  const C* rt;
+  C alpha, omega; int half;
+  __device__ void load(const State* st) {
+    alpha = fromd2<C>(st->alpha); omega = fromd2<C>(st->omega); half = st->half;
+  }
+  __device__ void operator()(int64_t i, double2* acc) {
+    if (half) { x[i] = caxpy(x[i], alpha, p[i]); return; }
+    const C qi = q[i], yi = y[i];
+    x[i] = caxpy(caxpy(x[i], alpha, p[i]), omega, qi);
+    const C ri = caxmy(qi, omega, yi);
+    const C wi = caxmy(yi, omega, caxmy(t[i], alpha, v[i]));
+    r[i] = ri; w[i] = wi;
+    const C rti = rt[i];
+    nrm_acc(acc[0], ri);
+    dotc_acc(acc[1], rti, ri);
+    dotc_acc(acc[2], rti, wi);
+    dotc_acc(acc[3], rti, s[i]);
+    dotc_acc(acc[4], rti, z[i]);
+  }
+  static __device__ void finish(State* st, const double2* sm) {
+    const int k = st->iter + 1;
+    if (st->half) { push_hist(st, k, st->ss); set_done(st, ST_CONVERGED, k); return; }
+    bool stop;
+    conv_check_common(st, k, sm[0].x, stop);
+    if (stop) return;
+    st->pb_rho = sm[1]; st->pb_rw = sm[2]; st->pb_rs = sm[3]; st->pb_rz = sm[4];
+    st->iter = k;
+  }
+};
+
+template <typename T>
+struct PbT {  // t = A w ; then Î² = (Î±/Ï‰)(Ï'/Ï), Î± = Ï'/(âŸ¨rÌƒ,wâŸ© + Î²âŸ¨rÌƒ,sâŸ© âˆ’ Î²Ï‰âŸ¨rÌƒ,zâŸ©)
+  static constexpr int K = 1;
+  using C = Cx<T>;
+  C* t;
+  __device__ void load(const State*) {}
+  __device__ void operator()(int64_t i, C val, double2*) { t[i] = val; }
+  static __device__ void finish(State* st, const double2*) {
+    st->matvecs_a++;
+    const int kc = st->iter - 1;         // the oracle raises inside iteration `iter`
+    const double2 rho_new = st->pb_rho;
+    if (!zfinite(rho_new)) { set_done(st, ST_NONFINITE, kc); return; }
+    if (zzero(rho_new)) { set_done(st, ST_BREAKDOWN, kc, BD_RHO); return; }
+    const double2 beta = zmul(zdiv(st->alpha, st->omega), zdiv(rho_new, st->rho));
+    st->beta = beta;
+    st->rho = rho_new;
+    const double2 bs = zmul(beta, st->pb_rs), bwz = zmul(zmul(beta, st->omega), st->pb_rz);
+    const double2 den = make_double2(st->pb_rw.x + bs.x - bwz.x, st->pb_rw.y + bs.y - bwz.y);
+    if (zzero(den)) { set_done(st, ST_BREAKDOWN, kc, BD_SIGMA); return; }
+    st->alpha = zdiv(rho_new, den);
+    if (!zfinite(st->alpha)) { set_done(st, ST_NONFINITE, kc); return; }
   }
 };
 

@@ -119,7 +119,7 @@ def test_sharded_dense_apply(G, dtype):
 
 @pytest.mark.parametrize("G", [2, 4])
 @pytest.mark.parametrize("method", ["bicgstab", "cgne", "qmr", "bicor", "cors",
-                                    "bicg", "cgs", "cocr", "cgnr", "tfqmr", "gmres", "bicgstabl"])
+                                    "bicg", "cgs", "cocr", "cgnr", "tfqmr", "gmres", "bicgstabl", "pbicgstab"])
 def test_sharded_cfg1_solve(G, method):
     A, y = cfg1()
     if method == "cocr":
@@ -259,7 +259,8 @@ def test_sharded_toeplitz(G):
 # Replicated-vector mode (CCG_OPT_REPLICATED; SURVEY §8(f) NEXT-2 ii): whole
 # vectors on every rank, row-sharded operator, one collective per product
 # ---------------------------------------------------------------------------
-ALL12 = ["bicgstab", "cgne", "qmr", "bicor", "cors", "bicg", "cgs", "cocr", "cgnr", "tfqmr", "gmres", "bicgstabl"]
+ALL12 = ["bicgstab", "cgne", "qmr", "bicor", "cors", "bicg", "cgs", "cocr", "cgnr", "tfqmr", "gmres", "bicgstabl",
+         "pbicgstab"]
 
 
 @pytest.mark.parametrize("G", [2, 4])

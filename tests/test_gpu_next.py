@@ -93,7 +93,8 @@ def test_qmr_dual_c64_proxy(monkeypatch):
 # ---------------------------------------------------------------------------
 import paper_1208_4869_b200 as ccg                       # noqa: E402
 from oracle import CsrOp                                   # noqa: E402
-from oracle.solvers import NEXT3                           # noqa: E402
+from oracle.solvers import NEXT3 as _N3, NEXT2              # noqa: E402
+NEXT3 = _N3 + NEXT2          # the generic per-method GPU checks cover NEXT-2 (iii) too
 from workloads import cfg1, helmholtz_csr, helmholtz_rhs   # noqa: E402
 from tests._gpu import Csr                                 # noqa: E402
 from tests.test_gpu_solve import _parity, _record          # noqa: E402
@@ -125,7 +126,7 @@ def test_next3_cfg2(method):
                 literal=method in ("bicg", "cocr"))
 
 
-@pytest.mark.parametrize("method", ["bicg", "cgs", "cgnr", "tfqmr"])
+@pytest.mark.parametrize("method", ["bicg", "cgs", "cgnr", "tfqmr", "pbicgstab"])
 def test_next3_cfg3_proxy_c64(method):
     n = 4096
     A = gauss_shifted_rows(n, 0, n, seed=1)
@@ -178,7 +179,7 @@ def test_next3_breakdown_fixture():
     y = np.array([1, 0], dtype=np.complex128)
     with Dense(A) as h:
         for m, name in (("bicg", "sigma"), ("cgs", "sigma"), ("cocr", "rho"), ("tfqmr", "sigma"),
-                        ("bicgstabl", "sigma")):
+                        ("bicgstabl", "sigma"), ("pbicgstab", "sigma")):
             g = h.solve(m, y, 1e-10, 10)
             o = oracle.solve(m, DenseOp(A), y, 1e-10, 10)
             assert g["status"] == "BREAKDOWN" and g["breakdown"] == name == o.breakdown, m
@@ -187,7 +188,7 @@ def test_next3_breakdown_fixture():
         assert g["status"] == "CONVERGED" and g["iterations"] == 1
 
 
-@pytest.mark.parametrize("method", ["cgs", "cocr", "tfqmr", "gmres"])
+@pytest.mark.parametrize("method", ["cgs", "cocr", "tfqmr", "gmres", "pbicgstab"])
 def test_next3_csr_transpose_free(method):
     """CGS and COCR need only A·x: they run on a CSR operator without the
     symmetric flag (COCR on the complex-symmetric shifted Helmholtz matrix)."""

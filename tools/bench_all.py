@@ -25,14 +25,14 @@ from workloads import (cfg1, cfg2, gauss_shifted_rows, cfg3_rhs, cfg4_rhs, helmh
 from workloads.device import cfg4_rows_device  # noqa: E402
 
 V_PASSES = {"bicgstab": 18, "cgne": 10, "qmr": 26, "bicor": 24, "cors": 24,
-            "bicg": 18, "cgs": 16, "cocr": 14, "cgnr": 11, "tfqmr": 28, "gmres": 0, "bicgstabl": 16}      # NEXT-3
+            "bicg": 18, "cgs": 16, "cocr": 14, "cgnr": 11, "tfqmr": 28, "gmres": 0, "bicgstabl": 16, "pbicgstab": 26}      # NEXT-3
 M_MATVEC = {"bicgstab": 2, "cgne": 2, "qmr": 2, "bicor": 2, "cors": 2,
-            "bicg": 2, "cgs": 2, "cocr": 1, "cgnr": 2, "tfqmr": 2, "gmres": 1, "bicgstabl": 2}
+            "bicg": 2, "cgs": 2, "cocr": 1, "cgnr": 2, "tfqmr": 2, "gmres": 1, "bicgstabl": 2, "pbicgstab": 2}
 if os.environ.get("CCG_QMR_DUAL", "1") != "0":
     M_MATVEC["qmr"] = 1                  # dual GEMV: A·p and Aᴴ·q in one pass
     M_MATVEC["bicg"] = 1
 KNOBS = {k: v for k, v in os.environ.items() if k.startswith("CCG_")}
-ALL = ("bicgstab", "cgne", "qmr", "bicor", "cors", "bicg", "cgs", "cgnr", "tfqmr", "gmres", "bicgstabl")
+ALL = ("bicgstab", "cgne", "qmr", "bicor", "cors", "bicg", "cgs", "cgnr", "tfqmr", "gmres", "bicgstabl", "pbicgstab")
 SYM = ALL + ("cocr",)                    # complex-symmetric configs (2, 4, 5) also run COCR
 SEL = set()
 
@@ -124,7 +124,7 @@ def main():
                 cfg4_rows_device(r0, r0 + 4096, Ad[r0:r0 + 4096])
             torch.cuda.synchronize()
             print(json.dumps({"config": 4, "generate_s": time.time() - t0}), flush=True)
-            run_dense(4, Ad, torch.from_numpy(cfg4_rhs()).to(dev), ("bicgstab", "qmr", "bicor", "cgne", "cocr", "bicg", "tfqmr", "gmres", "bicgstabl"),
+            run_dense(4, Ad, torch.from_numpy(cfg4_rhs()).to(dev), ("bicgstab", "qmr", "bicor", "cgne", "cocr", "bicg", "tfqmr", "gmres", "bicgstabl", "pbicgstab"),
                       cf["tol"], cf["maxit"], a.reps or 1, "c128")
             del Ad
         elif c == 5:
@@ -144,7 +144,7 @@ def main():
                     b_mat = 2 * n * 16          # x read + y write
                 stream = torch.cuda.ExternalStream(ccg.ccg_get_stream(h))
                 x = torch.empty_like(y)
-                for m in [m for m in ("bicgstab", "cors", "cgs", "cocr", "tfqmr", "gmres", "bicgstabl") if not a.methods or m in a.methods.split(",")]:
+                for m in [m for m in ("bicgstab", "cors", "cgs", "cocr", "tfqmr", "gmres", "bicgstabl", "pbicgstab") if not a.methods or m in a.methods.split(",")]:
                     r, its, ms = timed(h, m, y, x, cf["tol"], cf["maxit"], a.reps or 2, stream)
                     ips = its / (ms / 1e3)
                     b_iter = (1 if m == "cocr" else 2) * b_mat + V_PASSES[m] * n * 16
