@@ -1180,10 +1180,15 @@ static int choose_launch(ccg_ctx* c) {
   c->bulk_grid = (int)std::max<int64_t>(1, std::min<int64_t>((c->mnloc + E::BR - 1) / E::BR, c->sm_count));
   {
     const char* gm = getenv("CCG_GEMV");
-    c->gemv_mode = (gm && !strcmp(gm, "bulk"))   ? GEMV_BULK
-                   : (gm && !strcmp(gm, "rows")) ? GEMV_ROWS
-                   : (gm && !strcmp(gm, "cols")) ? GEMV_COLS
-                                                 : GEMV_SPLIT;
+    c->gemv_mode = (gm && !strcmp(gm, "bulk"))    ? GEMV_BULK
+                   : (gm && !strcmp(gm, "rows"))  ? GEMV_ROWS
+                   : (gm && !strcmp(gm, "cols"))  ? GEMV_COLS
+                   : (gm && !strcmp(gm, "split")) ? GEMV_SPLIT
+                   // default: the column-owner A·x below 1 GiB of rows (measured
+                   // 5.55 vs 5.18 TB/s at config 2's 268 MB, gemv_modes.jsonl),
+                   // the split kernel above (7.19 vs 6.99 TB/s at config 3)
+                   : ((double)c->mnloc * (double)c->n * (double)sizeof(C) < 1073741824.0) ? GEMV_COLS
+                                                                                           : GEMV_SPLIT;
     const char* qd = getenv("CCG_QMR_DUAL");
     c->qmr_dual = !(qd && !strcmp(qd, "0"));
   }

@@ -50,6 +50,12 @@ def run(dtype, n, reps, grid):
 
 
 if __name__ == "__main__":
+    if "--medium" in sys.argv:
+        modes = ([dict(CCG_GEMV=m) for m in ("split", "cols", "bulk", "rows")] +
+                 [dict(CCG_GEMV="split", CCG_SPLIT_KB=kb, CCG_SPLIT_UR=ur, CCG_SPLIT_WAVES=w)
+                  for kb in (4, 8, 16, 32) for ur in (4, 8) for w in (1, 2, 4)])
+        run("c128", 4096, 100, modes)
+        sys.exit(0)
     if "--modes" in sys.argv:
         modes = [dict(CCG_GEMV="split")] + [dict(CCG_GEMV="cols", CCG_COLS_RG=g, CCG_COLS_WAVES=w)
                                             for g in (1, 4) for w in (1, 2, 4)]
