@@ -387,16 +387,19 @@ struct Engine {
     const size_t smy = (size_t)g.tyz * g.Y2 * sizeof(C);
     const size_t smz = (size_t)g.tyz * g.Z2 * sizeof(C);
     const int gx = (g.ny * g.nz + g.tx - 1) / g.tx;
+    // threads per CTA: one per butterfly of its lines (a multiple of 32, ≤ 256)
+    auto bt = [](int lines, int len) { return std::max(32, std::min(256, ((lines * len / 2 + 31) / 32) * 32)); };
+    const int btx = bt(g.tx, g.X2), bty = bt(g.tyz, g.Y2), btz = bt(g.tyz, g.Z2);
     if (op == 1)
-      launch_k(c, fft_fwd_x<T, true>, gx, 256, smx, c->stream, xfull, W, g, tw, L / g.X2, gate);
+      launch_k(c, fft_fwd_x<T, true>, gx, btx, smx, c->stream, xfull, W, g, tw, L / g.X2, gate);
     else
-      launch_k(c, fft_fwd_x<T, false>, gx, 256, smx, c->stream, xfull, W, g, tw, L / g.X2, gate);
-    launch_k(c, fft_fwd_y<T>, dim3(g.X2 / g.tyz, g.nz), 256, smy, c->stream, W, g, tw, L / g.Y2, gate);
+      launch_k(c, fft_fwd_x<T, false>, gx, btx, smx, c->stream, xfull, W, g, tw, L / g.X2, gate);
+    launch_k(c, fft_fwd_y<T>, dim3(g.X2 / g.tyz, g.nz), bty, smy, c->stream, W, g, tw, L / g.Y2, gate);
     if (op == 0)
-      launch_k(c, fft_z_mul<T, false>, dim3(g.X2 / g.tyz, g.Y2), 256, smz, c->stream, W, Kh, g, tw, L / g.Z2, gate);
+      launch_k(c, fft_z_mul<T, false>, dim3(g.X2 / g.tyz, g.Y2), btz, smz, c->stream, W, Kh, g, tw, L / g.Z2, gate);
     else
-      launch_k(c, fft_z_mul<T, true>, dim3(g.X2 / g.tyz, g.Y2), 256, smz, c->stream, W, Kh, g, tw, L / g.Z2, gate);
-    launch_k(c, fft_inv_y<T>, dim3(g.X2 / g.tyz, g.nz), 256, smy, c->stream, W, g, tw, L / g.Y2, gate);
+      launch_k(c, fft_z_mul<T, true>, dim3(g.X2 / g.tyz, g.Y2), btz, smz, c->stream, W, Kh, g, tw, L / g.Z2, gate);
+    launch_k(c, fft_inv_y<T>, dim3(g.X2 / g.tyz, g.nz), bty, smy, c->stream, W, g, tw, L / g.Y2, gate);
     C d;
     d.x = (T)c->tdiag.x;
     d.y = (T)(op == 1 ? -c->tdiag.y : c->tdiag.y);
@@ -1778,8 +1781,13 @@ int ccg_set_matvec_toeplitz3(ccg_handle c, int64_t nx, int64_t ny, int64_t nz, c
   g.Y2 = pow2_at_least(2 * ny - 1, &g.ly);
   g.Z2 = pow2_at_least(2 * nz - 1, &g.lz);
   const int lyz = std::max(g.Y2, g.Z2);
+  // lines per CTA: at most 2048 points in shared memory, and few enough that
+  // every pass launches ≥ 2 CTAs per SM (the y pass has the fewest lines)
+  const int want = 2 * c->sm_count;
   g.tyz = std::max(1, std::min(g.X2, std::min(16, 2048 / lyz)));
+  while (g.tyz > 1 && (g.X2 / g.tyz) * std::min(g.nz, g.Y2) < want) g.tyz >>= 1;
   g.tx = std::max(1, std::min(32, 2048 / g.X2));
+  while (g.tx > 1 && (g.ny * g.nz + g.tx - 1) / g.tx < want) --g.tx;
   c->geo = g;
   c->fft_lmax = std::max(g.X2, std::max(g.Y2, g.Z2));
   // circulant embedding of the kernel, 3-D FFT in double, normalised
