@@ -7,7 +7,8 @@
 // embedded in a circulant of size X2 × Y2 × Z2 (each ≥ 2n − 1, a power of
 // two) it becomes  y = IFFT( FFT(K_pad) ⊙ FFT(x_pad) )  restricted to the box.
 //
-// Five kernels per product (all line FFTs in shared memory, radix-2):
+// Five kernels per product (all line FFTs in shared memory, radix-2 stages
+// fused in pairs):
 //   fwd_x   : the ny·nz nonzero x-lines of x_pad (zero padding not read)
 //   fwd_y   : the X2·nz nonzero y-lines
 //   z_mul   : every (kx, ky) z-line: forward FFT, ⊙ K̂ (the mirrored entry
@@ -45,15 +46,41 @@ __device__ __forceinline__ C twiddle(const C* __restrict__ tw, int m, int stride
   return w;
 }
 
-// In-place radix-2 decimation-in-time FFT of TX lines of length L = 2^logL
-// held in shared memory as buf[l·TX + t]; input in bit-reversed order,
-// output natural.  Called by all threads of the CTA.
+// In-place decimation-in-time FFT of TX lines of length L = 2^logL held in
+// shared memory as buf[l·TX + t]; input in bit-reversed order, output
+// natural.  Radix-2 stages are fused in pairs (each thread takes a quad of
+// points through stages s and s+1 in registers: the same operations in the
+// same order as two radix-2 stages, half the barriers and shared-memory
+// traffic); an odd last stage runs alone.  Called by all threads of the CTA.
 template <typename C>
 __device__ void fft_dit(C* buf, int logL, int TX, bool inv, const C* __restrict__ tw, int twstride) {
   const int L = 1 << logL;
-  const int nb = TX * (L >> 1);
-  for (int s = 0; s < logL; ++s) {
+  int s = 0;
+  for (; s + 1 < logL; s += 2) {
     const int h = 1 << s;
+    const int nq = TX * (L >> 2);
+    __syncthreads();
+    for (int b = threadIdx.x; b < nq; b += blockDim.x) {
+      const int t = b % TX, q = b / TX;
+      const int m = q & (h - 1);
+      const int i0 = ((q >> s) << (s + 2)) + m;
+      const C w1 = twiddle(tw, m << (logL - s - 1), twstride, inv);
+      const C w2 = twiddle(tw, m << (logL - s - 2), twstride, inv);
+      const C w3 = twiddle(tw, (m + h) << (logL - s - 2), twstride, inv);
+      const C x0 = buf[i0 * TX + t], x1 = buf[(i0 + h) * TX + t];
+      const C x2 = buf[(i0 + 2 * h) * TX + t], x3 = buf[(i0 + 3 * h) * TX + t];
+      const C p1 = cmul(x1, w1), p3 = cmul(x3, w1);
+      const C a0 = cadd(x0, p1), a1 = csub(x0, p1), a2 = cadd(x2, p3), a3 = csub(x2, p3);
+      const C q2 = cmul(a2, w2), q3 = cmul(a3, w3);
+      buf[i0 * TX + t] = cadd(a0, q2);
+      buf[(i0 + 2 * h) * TX + t] = csub(a0, q2);
+      buf[(i0 + h) * TX + t] = cadd(a1, q3);
+      buf[(i0 + 3 * h) * TX + t] = csub(a1, q3);
+    }
+  }
+  if (s < logL) {                       // odd last stage
+    const int h = 1 << s;
+    const int nb = TX * (L >> 1);
     __syncthreads();
     for (int b = threadIdx.x; b < nb; b += blockDim.x) {
       const int t = b % TX, q = b / TX;
@@ -69,19 +96,40 @@ __device__ void fft_dit(C* buf, int logL, int TX, bool inv, const C* __restrict_
   __syncthreads();
 }
 
-// In-place radix-2 decimation-in-frequency FFT: natural input, bit-reversed output.
+// In-place decimation-in-frequency FFT: natural input, bit-reversed output;
+// stages s = logL−1 … 0 fused in pairs (s, s−1) the same way.
 template <typename C>
 __device__ void fft_dif(C* buf, int logL, int TX, bool inv, const C* __restrict__ tw, int twstride) {
   const int L = 1 << logL;
-  const int nb = TX * (L >> 1);
-  for (int s = logL - 1; s >= 0; --s) {
-    const int h = 1 << s;
+  int s = logL - 1;
+  for (; s >= 1; s -= 2) {
+    const int H = 1 << s, hh = H >> 1;
+    const int nq = TX * (L >> 2);
+    __syncthreads();
+    for (int b = threadIdx.x; b < nq; b += blockDim.x) {
+      const int t = b % TX, q = b / TX;
+      const int m = q & (hh - 1);
+      const int i0 = ((q >> (s - 1)) << (s + 1)) + m;
+      const C wa = twiddle(tw, m << (logL - s - 1), twstride, inv);
+      const C wb = twiddle(tw, (m + hh) << (logL - s - 1), twstride, inv);
+      const C wc = twiddle(tw, m << (logL - s), twstride, inv);
+      const C x0 = buf[i0 * TX + t], x1 = buf[(i0 + hh) * TX + t];
+      const C x2 = buf[(i0 + H) * TX + t], x3 = buf[(i0 + H + hh) * TX + t];
+      const C a0 = cadd(x0, x2), a2 = cmul(csub(x0, x2), wa);
+      const C a1 = cadd(x1, x3), a3 = cmul(csub(x1, x3), wb);
+      buf[i0 * TX + t] = cadd(a0, a1);
+      buf[(i0 + hh) * TX + t] = cmul(csub(a0, a1), wc);
+      buf[(i0 + H) * TX + t] = cadd(a2, a3);
+      buf[(i0 + H + hh) * TX + t] = cmul(csub(a2, a3), wc);
+    }
+  }
+  if (s == 0) {                         // odd last stage
+    const int nb = TX * (L >> 1);
     __syncthreads();
     for (int b = threadIdx.x; b < nb; b += blockDim.x) {
       const int t = b % TX, q = b / TX;
-      const int m = q & (h - 1);
-      const int i0 = ((q >> s) << (s + 1)) + m, i1 = i0 + h;
-      const C w = twiddle(tw, m << (logL - s - 1), twstride, inv);
+      const int i0 = q << 1, i1 = i0 + 1;
+      const C w = twiddle(tw, 0, twstride, inv);
       const C a = buf[i0 * TX + t];
       const C bb = buf[i1 * TX + t];
       buf[i0 * TX + t] = cadd(a, bb);
