@@ -44,7 +44,7 @@ def build(force=False, verbose=False):
         return LIB
     cmd = [nvcc(), "-O3", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
            "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
-           "--expt-relaxed-constexpr", "-Xptxas", "-v" if verbose else "-O3",
+           "--expt-relaxed-constexpr", "--split-compile", "0", "-Xptxas", "-v" if verbose else "-O3",
            "-I", os.path.join(ROOT, "include"), "-I", nccl_include(),
            "-o", LIB + ".tmp"] + [os.path.join(CSRC, s) for s in SOURCES] + [
            "-ldl", "-Xlinker", "-rpath=" + nccl_libdir()]

@@ -68,7 +68,8 @@ struct ccg_ctx {
   int32_t* sell_width = nullptr;
   int32_t* sell_col = nullptr;
   void* sell_val = nullptr;
-  int sell_grid = 0;
+  int sell_grid[2] = {0, 0};
+  int sell_one = 0, sell_waves = 1;   // SELL load schedule / grid waves (CCG_SELL_ONE, CCG_SELL_WAVES)
   // matrix-free 7-point stencil (ccg_set_matvec_stencil7)
   int snx = 0, sny = 0, snz = 0, sz0 = 0, snzl = 0, szc = 4;
   double2 scoef[4] = {};  // d, ox, oy, oz
@@ -348,10 +349,12 @@ struct Engine {
   template <bool CONJ, class Epi>
   static void spmv(ccg_ctx* c, const C* x, Epi epi, const int* gate) {
     const C* vals = reinterpret_cast<const C*>(c->vals);
-    if (c->sell_col)
-      launch_k(c, spmv_sell_kernel<T, NT, CONJ, Epi>, c->sell_grid, NT, 0, c->stream, 
+    if (c->sell_col) {
+      auto k = c->sell_one ? spmv_sell_kernel<T, NT, CONJ, true, Epi> : spmv_sell_kernel<T, NT, CONJ, false, Epi>;
+      launch_k(c, k, c->sell_grid[c->sell_one], NT, 0, c->stream,
           c->sell_off, c->sell_width, c->sell_col, reinterpret_cast<const C*>(c->sell_val), x, c->mnloc, epi,
           make_red(c), c->st, gate);
+    }
     else if (c->csr_blocks)
       launch_k(c, spmv_stream_kernel<T, NT, SNNZ, CONJ, Epi>, c->spmv_grid, NT, 0, c->stream, 
           c->rowptr, c->colind, vals, x, c->csr_blocks, c->csr_nblocks, epi, make_red(c), c->st, gate);
@@ -1283,11 +1286,21 @@ static int choose_launch(ccg_ctx* c) {
   c->spmv_grid = (int)std::max<int64_t>(
       1, std::min<int64_t>((c->mnloc + NT / E::LPR - 1) / (NT / E::LPR), (int64_t)c->sm_count * 8));
   if (c->sell_col) {
-    int occ4 = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ4, spmv_sell_kernel<T, E::NT, false, Store<T>>, NT, 0);
-    if (occ4 < 1) occ4 = 1;
+    // measured (tools/sweep_sell.py, interleaved medians, profiles/r01/
+    // sweep_sell.jsonl): one row per step at ≥ 3 CTAs/SM wins for both dtypes
+    // (config 5 COCR c128 172.6 → 135.6 µs/it, c64 87.7 → 84.3)
+    c->sell_one = 1;
+    const char* sm = getenv("CCG_SELL_ONE");
+    if (sm) c->sell_one = atoi(sm) != 0;
+    const char* sw = getenv("CCG_SELL_WAVES");
+    if (sw) c->sell_waves = std::max(1, std::min(64, atoi(sw)));
+    int occ4[2] = {0, 0};
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ4[0], spmv_sell_kernel<T, E::NT, false, false, Store<T>>, NT, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ4[1], spmv_sell_kernel<T, E::NT, false, true, Store<T>>, NT, 0);
     const int64_t thr = ((c->mnloc + 31) / 32) * 32;
-    c->sell_grid = (int)std::max<int64_t>(1, std::min<int64_t>((thr + NT - 1) / NT, (int64_t)c->sm_count * occ4));
+    for (int m = 0; m < 2; ++m)
+      c->sell_grid[m] = (int)std::max<int64_t>(
+          1, std::min<int64_t>((thr + NT - 1) / NT, (int64_t)c->sm_count * std::max(1, occ4[m]) * c->sell_waves));
   }
   if (c->csr_blocks) {
     int occ3 = 0;
@@ -1307,7 +1320,7 @@ static int choose_launch(ccg_ctx* c) {
   int64_t maxgrid = std::max<int64_t>({(int64_t)c->gemv_grid, (int64_t)c->ah_strips * c->ah_S,
                                        (int64_t)c->stage2_grid, (int64_t)c->pass_grid, (int64_t)c->spmv_grid,
                                        (int64_t)c->split_strips * c->split_nrb, (int64_t)c->nstage2_grid,
-                                       (int64_t)c->bulk_grid, (int64_t)c->sell_grid,
+                                       (int64_t)c->bulk_grid, (int64_t)std::max(c->sell_grid[0], c->sell_grid[1]),
                                        (int64_t)c->cols_strips * std::max(c->cols_S, c->dual_S),
                                        c->opk == OPK_STENCIL ? (int64_t)((c->snx + 31) / 32) * ((c->sny + 7) / 8) *
                                                                    ((c->snzl + c->szc - 1) / c->szc)

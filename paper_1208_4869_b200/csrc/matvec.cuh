@@ -710,8 +710,14 @@ __device__ __forceinline__ C sell_row(const int32_t* __restrict__ scol, const C*
   return acc;
 }
 
-template <typename T, int NT, bool CONJ, class Epi>
-__global__ void __launch_bounds__(NT)
+// Load schedule, chosen per dtype by measurement (tools/sweep_sell.py):
+// ONE = false — two rows per step for width-7 slices, ptxas' default register
+// budget (it interleaves the loads with the FMAs: ~2-3 loads in flight);
+// ONE = true — one row per step with "≥ 3 CTAs/SM" in the launch bounds, under
+// which ptxas issues all 14 loads of a row before its arithmetic (78-94
+// registers): c128 SpMV 64.6 → 57.9 µs at config 5 (cold ncu), the default.
+template <typename T, int NT, bool CONJ, bool ONE, class Epi>
+__global__ void __launch_bounds__(NT, ONE ? 3 : 0)
 spmv_sell_kernel(const int64_t* __restrict__ soff, const int32_t* __restrict__ swidth,
                  const int32_t* __restrict__ scol, const typename CT<T>::c* __restrict__ sval,
                  const typename CT<T>::c* __restrict__ x, int64_t nrows, Epi epi, Red red, State* st,
@@ -729,7 +735,7 @@ spmv_sell_kernel(const int64_t* __restrict__ soff, const int32_t* __restrict__ s
   int64_t i = (int64_t)blockIdx.x * NT + threadIdx.x;
   // two rows per step (i, i + stride) when their slices share the common
   // stencil width 7: twice the loads in flight per thread
-  for (; i + stride < nwarps_rows; i += 2 * stride) {
+  for (; !ONE && i + stride < nwarps_rows; i += 2 * stride) {
     const int64_t s1 = i >> 5, s2 = (i + stride) >> 5;
     const int lane = (int)(i & 31);
     const int w1 = __ldg(swidth + s1), w2 = __ldg(swidth + s2);

@@ -153,7 +153,7 @@ struct BsV {  // v = A p ; œÉ = ‚ü®rÃÉ, v‚ü© ; Œ± = œÅ/œÉ
   using C = Cx<T>;
   C* v; const C* rt;
   __device__ void load(const State*) {}
-  __device__ void operator()(int64_t i, C val, double2* acc) { v[i] = val; dotc_acc(acc[0], rt[i], val); }
+  __device__ void operator()(int64_t i, C val, double2* acc) { const C b = rt[i]; v[i] = val; dotc_acc(acc[0], b, val); }
   static __device__ void finish(State* st, const double2* s) {
     const int k = st->iter + 1;
     st->matvecs_a++;
@@ -192,8 +192,9 @@ struct BsT {  // t = A s ; ‚ü®t,s‚ü©, ‚ü®t,t‚ü© ; œâ
   C* t; const C* s;
   __device__ void load(const State*) {}
   __device__ void operator()(int64_t i, C val, double2* acc) {
+    const C si = s[i];
     t[i] = val;
-    dotc_acc(acc[0], val, s[i]);
+    dotc_acc(acc[0], val, si);
     nrm_acc(acc[1], val);
   }
   static __device__ void finish(State* st, const double2* sm) {
@@ -218,12 +219,14 @@ struct BsX {  // x += Œ±p + œâs ; r = s ‚àí œât ; ‚Äñr‚Äñ¬≤, ‚ü®rÃÉ, r‚ü©   (hal
   }
   __device__ void operator()(int64_t i, double2* acc) {
     if (half) { x[i] = caxpy(x[i], alpha, p[i]); return; }
-    const C si = s[i];
-    x[i] = caxpy(caxpy(x[i], alpha, p[i]), omega, si);
-    const C ri = caxmy(si, omega, t[i]);
+    // every load issued before the first store (the pointers are not
+    // restrict-qualified, so a store would otherwise order the loads after it)
+    const C xi = x[i], pi = p[i], si = s[i], ti = t[i], rti = rt[i];
+    x[i] = caxpy(caxpy(xi, alpha, pi), omega, si);
+    const C ri = caxmy(si, omega, ti);
     r[i] = ri;
     nrm_acc(acc[0], ri);
-    dotc_acc(acc[1], rt[i], ri);
+    dotc_acc(acc[1], rti, ri);
   }
   static __device__ void finish(State* st, const double2* sm) {
     const int k = st->iter + 1;
@@ -352,9 +355,10 @@ struct QmP {  // p = v ‚àí (ŒæŒ¥/Œµ)p ; q = w ‚àí conj(œÅŒ¥/Œµ)q   (k=1: p = v, 
     first = st->iter == 0; cp = fromd2<C>(st->cp); cq = fromd2<C>(st->cq);
   }
   __device__ void operator()(int64_t i, double2*) {
-    if (first) { p[i] = v[i]; q[i] = w[i]; return; }
-    p[i] = caxmy(v[i], cp, p[i]);
-    q[i] = caxmy(w[i], cq, q[i]);
+    if (first) { const C vi = v[i], wi = w[i]; p[i] = vi; q[i] = wi; return; }
+    const C vi = v[i], pi = p[i], wi = w[i], qi = q[i];
+    p[i] = caxmy(vi, cp, pi);
+    q[i] = caxmy(wi, cq, qi);
   }
   static __device__ void finish(State*, const double2*) {}
 };
@@ -365,7 +369,7 @@ struct QmPt {  // pÃÉ = A p ; Œµ = ‚ü®q, pÃÉ‚ü© ; Œ≤ = Œµ/Œ¥
   using C = Cx<T>;
   C* pt; const C* q;
   __device__ void load(const State*) {}
-  __device__ void operator()(int64_t i, C val, double2* acc) { pt[i] = val; dotc_acc(acc[0], q[i], val); }
+  __device__ void operator()(int64_t i, C val, double2* acc) { const C b = q[i]; pt[i] = val; dotc_acc(acc[0], b, val); }
   static __device__ void finish(State* st, const double2* s) {
     const int k = st->iter + 1;
     st->matvecs_a++;
@@ -423,18 +427,20 @@ struct QmDV {  // d, s ; x += d ; r ‚àí= s ; ‚Äñr‚Äñ¬≤ ; v = ·πΩ/œÅ' ; w = wÃÉ/Œ
     first = st->iter == 0;
   }
   __device__ void operator()(int64_t i, double2* acc) {
-    C di = cmul(eta, p[i]), si = cmul(eta, pt[i]);
+    const C pi = p[i], pti = pt[i], xi = x[i], rold = r[i], vti = vt[i], wti = wt[i];
+    C dd = czero<C>(), ss = czero<C>();
+    if (!first) { dd = d[i]; ss = sv[i]; }
+    C di = cmul(eta, pi), si = cmul(eta, pti);
     if (!first) {
-      const C dd = d[i], ss = sv[i];
       di.x += c2 * dd.x; di.y += c2 * dd.y;
       si.x += c2 * ss.x; si.y += c2 * ss.y;
     }
     d[i] = di; sv[i] = si;
-    x[i] = cadd(x[i], di);
-    const C ri = csub(r[i], si);
+    x[i] = cadd(xi, di);
+    const C ri = csub(rold, si);
     r[i] = ri;
     nrm_acc(acc[0], ri);
-    const C vi = cdivr(vt[i], rn), wi = cdivr(wt[i], xn);
+    const C vi = cdivr(vti, rn), wi = cdivr(wti, xn);
     v[i] = vi; w[i] = wi;
     dotc_acc(acc[1], wi, vi);
   }
@@ -482,7 +488,7 @@ struct RhoEpi {  // rÃÇ = A r ; œÅ = ‚ü®shadow, rÃÇ‚ü©   (BiCOR and CORS)
   using C = Cx<T>;
   C* rh; const C* sh;
   __device__ void load(const State*) {}
-  __device__ void operator()(int64_t i, C val, double2* acc) { rh[i] = val; dotc_acc(acc[0], sh[i], val); }
+  __device__ void operator()(int64_t i, C val, double2* acc) { const C b = sh[i]; rh[i] = val; dotc_acc(acc[0], b, val); }
   static __device__ void finish(State* st, const double2* s) { rho_step(st, s[0], true); }
 };
 
@@ -496,10 +502,12 @@ struct BcP {  // p = r + Œ≤p ; p* = r* + conj(Œ≤)p* ; q = rÃÇ + Œ≤q   (k=1: copi
     first = st->iter == 0; beta = fromd2<C>(st->beta); cbeta = fromd2<C>(zconj(st->beta));
   }
   __device__ void operator()(int64_t i, double2*) {
-    if (first) { p[i] = r[i]; ps[i] = rs[i]; q[i] = rh[i]; return; }
-    p[i] = caxpy(r[i], beta, p[i]);
-    ps[i] = caxpy(rs[i], cbeta, ps[i]);
-    q[i] = caxpy(rh[i], beta, q[i]);
+    const C ri = r[i], rsi = rs[i], rhi = rh[i];
+    if (first) { p[i] = ri; ps[i] = rsi; q[i] = rhi; return; }
+    const C pi = p[i], psi = ps[i], qi = q[i];
+    p[i] = caxpy(ri, beta, pi);
+    ps[i] = caxpy(rsi, cbeta, psi);
+    q[i] = caxpy(rhi, beta, qi);
   }
   static __device__ void finish(State*, const double2*) {}
 };
@@ -522,10 +530,11 @@ struct BcX {  // x += Œ±p ; r ‚àí= Œ±q ; r* ‚àí= conj(Œ±)q* ; ‚Äñr‚Äñ¬≤
   C alpha, calpha;
   __device__ void load(const State* st) { alpha = fromd2<C>(st->alpha); calpha = fromd2<C>(zconj(st->alpha)); }
   __device__ void operator()(int64_t i, double2* acc) {
-    x[i] = caxpy(x[i], alpha, p[i]);
-    const C ri = caxmy(r[i], alpha, q[i]);
+    const C xi = x[i], pi = p[i], rold = r[i], qi = q[i], rsi = rs[i], qsi = qs[i];
+    x[i] = caxpy(xi, alpha, pi);
+    const C ri = caxmy(rold, alpha, qi);
     r[i] = ri;
-    rs[i] = caxmy(rs[i], calpha, qs[i]);
+    rs[i] = caxmy(rsi, calpha, qsi);
     nrm_acc(acc[0], ri);
   }
   static __device__ void finish(State* st, const double2* s) { r_step(st, s[0].x); }
@@ -543,12 +552,12 @@ struct CoP {  // e = r + Œ≤h ; √™ = rÃÇ + Œ≤ƒ• ; qÃÇ = √™ + Œ≤(ƒ• + Œ≤qÃÇ)   (k=
   C beta; int first;
   __device__ void load(const State* st) { first = st->iter == 0; beta = fromd2<C>(st->beta); }
   __device__ void operator()(int64_t i, double2*) {
-    if (first) { const C v = rh[i]; e[i] = r[i]; eh[i] = v; qh[i] = v; return; }
-    const C hhi = hh[i];
-    e[i] = caxpy(r[i], beta, h[i]);
-    const C ehi = caxpy(rh[i], beta, hhi);
+    if (first) { const C v = rh[i], ri = r[i]; e[i] = ri; eh[i] = v; qh[i] = v; return; }
+    const C hhi = hh[i], ri = r[i], hi = h[i], rhi = rh[i], qhi = qh[i];
+    e[i] = caxpy(ri, beta, hi);
+    const C ehi = caxpy(rhi, beta, hhi);
     eh[i] = ehi;
-    qh[i] = caxpy(ehi, beta, caxpy(hhi, beta, qh[i]));
+    qh[i] = caxpy(ehi, beta, caxpy(hhi, beta, qhi));
   }
   static __device__ void finish(State*, const double2*) {}
 };
@@ -559,7 +568,7 @@ struct CoQ {  // q = A qÃÇ ; Œæ = ‚ü®r‚ÇÄ*, q‚ü© ; Œ± = œÅ/Œæ
   using C = Cx<T>;
   C* q; const C* r0s;
   __device__ void load(const State*) {}
-  __device__ void operator()(int64_t i, C val, double2* acc) { q[i] = val; dotc_acc(acc[0], r0s[i], val); }
+  __device__ void operator()(int64_t i, C val, double2* acc) { const C b = r0s[i]; q[i] = val; dotc_acc(acc[0], b, val); }
   static __device__ void finish(State* st, const double2* s) { st->matvecs_a++; xi_step(st, s[0]); }
 };
 
@@ -571,12 +580,12 @@ struct CoH {  // h = e ‚àí Œ±qÃÇ ; ƒ• = √™ ‚àí Œ±q ; x += Œ±(e + h) ; r ‚àí= Œ±(
   C alpha;
   __device__ void load(const State* st) { alpha = fromd2<C>(st->alpha); }
   __device__ void operator()(int64_t i, double2* acc) {
-    const C ei = e[i], ehi = eh[i];
-    const C hi = caxmy(ei, alpha, qh[i]);
-    const C hhi = caxmy(ehi, alpha, q[i]);
+    const C ei = e[i], ehi = eh[i], qhi = qh[i], qi = q[i], xi = x[i], rold = r[i];
+    const C hi = caxmy(ei, alpha, qhi);
+    const C hhi = caxmy(ehi, alpha, qi);
     h[i] = hi; hh[i] = hhi;
-    x[i] = caxpy(x[i], alpha, cadd(ei, hi));
-    const C ri = caxmy(r[i], alpha, cadd(ehi, hhi));
+    x[i] = caxpy(xi, alpha, cadd(ei, hi));
+    const C ri = caxmy(rold, alpha, cadd(ehi, hhi));
     r[i] = ri;
     nrm_acc(acc[0], ri);
   }
@@ -618,9 +627,11 @@ struct BgP {  // p = r + Œ≤p ; pÃÉ = rÃÉ + conj(Œ≤)pÃÉ   (k=1: copies)
     first = st->iter == 0; beta = fromd2<C>(st->beta); cbeta = fromd2<C>(zconj(st->beta));
   }
   __device__ void operator()(int64_t i, double2*) {
-    if (first) { p[i] = r[i]; pt[i] = rt[i]; return; }
-    p[i] = caxpy(r[i], beta, p[i]);
-    pt[i] = caxpy(rt[i], cbeta, pt[i]);
+    const C ri = r[i], rti = rt[i];
+    if (first) { p[i] = ri; pt[i] = rti; return; }
+    const C pi = p[i], pti = pt[i];
+    p[i] = caxpy(ri, beta, pi);
+    pt[i] = caxpy(rti, cbeta, pti);
   }
   static __device__ void finish(State*, const double2*) {}
 };
@@ -631,7 +642,7 @@ struct BgQ {  // q = A p ; œÉ = ‚ü®pÃÉ, q‚ü© ; Œ± = œÅ/œÉ   (counts the paired A
   using C = Cx<T>;
   C* q; const C* pt;
   __device__ void load(const State*) {}
-  __device__ void operator()(int64_t i, C val, double2* acc) { q[i] = val; dotc_acc(acc[0], pt[i], val); }
+  __device__ void operator()(int64_t i, C val, double2* acc) { const C b = pt[i]; q[i] = val; dotc_acc(acc[0], b, val); }
   static __device__ void finish(State* st, const double2* s) {
     st->matvecs_a++;
     st->matvecs_ah++;
@@ -647,9 +658,10 @@ struct BgX {  // x += Œ±p ; r ‚àí= Œ±q ; rÃÉ ‚àí= conj(Œ±)qÃÉ ; ‚Äñr‚Äñ¬≤, ‚ü®rÃ
   C alpha, calpha;
   __device__ void load(const State* st) { alpha = fromd2<C>(st->alpha); calpha = fromd2<C>(zconj(st->alpha)); }
   __device__ void operator()(int64_t i, double2* acc) {
-    x[i] = caxpy(x[i], alpha, p[i]);
-    const C ri = caxmy(r[i], alpha, q[i]);
-    const C rti = caxmy(rt[i], calpha, qt[i]);
+    const C xi = x[i], pi = p[i], rold = r[i], qi = q[i], rtold = rt[i], qti = qt[i];
+    x[i] = caxpy(xi, alpha, pi);
+    const C ri = caxmy(rold, alpha, qi);
+    const C rti = caxmy(rtold, calpha, qti);
     r[i] = ri; rt[i] = rti;
     nrm_acc(acc[0], ri);
     dotc_acc(acc[1], rti, ri);
@@ -667,10 +679,10 @@ struct CsP {  // u = r + Œ≤q ; p = u + Œ≤(q + Œ≤p)   (k=1: u = p = r)
   __device__ void load(const State* st) { first = st->iter == 0; beta = fromd2<C>(st->beta); }
   __device__ void operator()(int64_t i, double2*) {
     if (first) { const C ri = r[i]; u[i] = ri; p[i] = ri; return; }
-    const C qi = q[i];
-    const C ui = caxpy(r[i], beta, qi);
+    const C qi = q[i], ri = r[i], pi = p[i];
+    const C ui = caxpy(ri, beta, qi);
     u[i] = ui;
-    p[i] = caxpy(ui, beta, caxpy(qi, beta, p[i]));
+    p[i] = caxpy(ui, beta, caxpy(qi, beta, pi));
   }
   static __device__ void finish(State*, const double2*) {}
 };
@@ -681,7 +693,7 @@ struct CsV {  // v = A p ; œÉ = ‚ü®rÃÉ, v‚ü© ; Œ± = œÅ/œÉ
   using C = Cx<T>;
   C* v; const C* rt;
   __device__ void load(const State*) {}
-  __device__ void operator()(int64_t i, C val, double2* acc) { v[i] = val; dotc_acc(acc[0], rt[i], val); }
+  __device__ void operator()(int64_t i, C val, double2* acc) { const C b = rt[i]; v[i] = val; dotc_acc(acc[0], b, val); }
   static __device__ void finish(State* st, const double2* s) { st->matvecs_a++; sigma_step(st, s[0]); }
 };
 
@@ -693,12 +705,12 @@ struct CsQ {  // q = u ‚àí Œ±v ; u + q ; x += Œ±(u + q)
   C alpha;
   __device__ void load(const State* st) { alpha = fromd2<C>(st->alpha); }
   __device__ void operator()(int64_t i, double2*) {
-    const C ui = u[i];
-    const C qi = caxmy(ui, alpha, v[i]);
+    const C ui = u[i], vi = v[i], xi = x[i];
+    const C qi = caxmy(ui, alpha, vi);
     q[i] = qi;
     const C s = cadd(ui, qi);
     uq[i] = s;
-    x[i] = caxpy(x[i], alpha, s);
+    x[i] = caxpy(xi, alpha, s);
   }
   static __device__ void finish(State*, const double2*) {}
 };
@@ -711,10 +723,11 @@ struct CsR {  // r ‚àí= Œ± A(u + q) ; ‚Äñr‚Äñ¬≤, ‚ü®rÃÉ, r‚ü©
   C alpha;
   __device__ void load(const State* st) { alpha = fromd2<C>(st->alpha); }
   __device__ void operator()(int64_t i, C w, double2* acc) {
-    const C ri = caxmy(r[i], alpha, w);
+    const C rold = r[i], rti = rt[i];
+    const C ri = caxmy(rold, alpha, w);
     r[i] = ri;
     nrm_acc(acc[0], ri);
-    dotc_acc(acc[1], rt[i], ri);
+    dotc_acc(acc[1], rti, ri);
   }
   static __device__ void finish(State* st, const double2* s) {
     st->matvecs_a++;
@@ -730,7 +743,7 @@ struct CrAr0 {  // setup: Ar = A r‚ÇÄ ; Œº = [r‚ÇÄ, Ar‚ÇÄ]
   using C = Cx<T>;
   C* ar; const C* r;
   __device__ void load(const State*) {}
-  __device__ void operator()(int64_t i, C val, double2* acc) { ar[i] = val; dotu_acc(acc[0], r[i], val); }
+  __device__ void operator()(int64_t i, C val, double2* acc) { const C b = r[i]; ar[i] = val; dotu_acc(acc[0], b, val); }
   static __device__ void finish(State* st, const double2* s) { st->matvecs_a++; st->rho = s[0]; }
 };
 
@@ -740,7 +753,7 @@ struct CrAr {  // Ar = A r ; Œº' = [r, Ar] ; Œ≤ = Œº'/Œº   (end of iteration k =
   using C = Cx<T>;
   C* ar; const C* r;
   __device__ void load(const State*) {}
-  __device__ void operator()(int64_t i, C val, double2* acc) { ar[i] = val; dotu_acc(acc[0], r[i], val); }
+  __device__ void operator()(int64_t i, C val, double2* acc) { const C b = r[i]; ar[i] = val; dotu_acc(acc[0], b, val); }
   static __device__ void finish(State* st, const double2* s) {
     st->matvecs_a++;
     const int kc = st->iter - 1;   // the oracle raises inside iteration iter
@@ -781,8 +794,9 @@ struct CrX {  // x += Œ±p ; r ‚àí= Œ±Ap ; ‚Äñr‚Äñ¬≤
   C alpha;
   __device__ void load(const State* st) { alpha = fromd2<C>(st->alpha); }
   __device__ void operator()(int64_t i, double2* acc) {
-    x[i] = caxpy(x[i], alpha, p[i]);
-    const C ri = caxmy(r[i], alpha, ap[i]);
+    const C xi = x[i], pi = p[i], rold = r[i], api = ap[i];
+    x[i] = caxpy(xi, alpha, pi);
+    const C ri = caxmy(rold, alpha, api);
     r[i] = ri;
     nrm_acc(acc[0], ri);
   }
@@ -901,7 +915,7 @@ struct TfV0 {  // setup: v = A u‚ÇÄ (= A u_even) ; œÉ = ‚ü®r‚ÇÄ*, v‚ü© ; Œ± = œÅ
   using C = Cx<T>;
   C* v; C* aue; const C* rs;
   __device__ void load(const State*) {}
-  __device__ void operator()(int64_t i, C val, double2* acc) { v[i] = val; aue[i] = val; dotc_acc(acc[0], rs[i], val); }
+  __device__ void operator()(int64_t i, C val, double2* acc) { const C b = rs[i]; v[i] = val; aue[i] = val; dotc_acc(acc[0], b, val); }
   static __device__ void finish(State* st, const double2* s) { st->matvecs_a++; sigma_step(st, s[0]); }
 };
 
@@ -917,11 +931,12 @@ struct TfE {  // u‚ÇÇ = u ‚àí Œ±v ; w ‚àí= Œ±¬∑A u ; d = u + (Œ∏¬≤Œ∑/Œ±)d ; ‚Äñw
     coef = fromd2<C>(zdiv(zscal(st->eta, st->theta * st->theta), st->alpha));
   }
   __device__ void operator()(int64_t i, double2* acc) {
-    const C ui = u[i];
-    u2[i] = caxmy(ui, alpha, v[i]);
-    const C wi = caxmy(w[i], alpha, aue[i]);
+    const C ui = u[i], vi = v[i], wold = w[i], auei = aue[i];
+    const C dold = first ? ui : d[i];
+    u2[i] = caxmy(ui, alpha, vi);
+    const C wi = caxmy(wold, alpha, auei);
     w[i] = wi;
-    d[i] = first ? ui : caxpy(ui, coef, d[i]);
+    d[i] = first ? ui : caxpy(ui, coef, dold);
     nrm_acc(acc[0], wi);
   }
   static __device__ void finish(State* st, const double2* s) {
@@ -941,14 +956,14 @@ struct TfO {  // A u‚ÇÇ ; x += Œ∑ d (E's update) ; w ‚àí= Œ± A u‚ÇÇ ; d = u‚ÇÇ +
     coef = fromd2<C>(zdiv(zscal(st->eta, st->theta * st->theta), st->alpha));
   }
   __device__ void operator()(int64_t i, C val, double2* acc) {
+    const C di = d[i], xi = x[i], wold = w[i], u2i = u2[i], rsi = rs[i];
     au[i] = val;
-    const C di = d[i];
-    x[i] = caxpy(x[i], eta, di);
-    const C wi = caxmy(w[i], alpha, val);
+    x[i] = caxpy(xi, eta, di);
+    const C wi = caxmy(wold, alpha, val);
     w[i] = wi;
-    d[i] = caxpy(u2[i], coef, di);
+    d[i] = caxpy(u2i, coef, di);
     nrm_acc(acc[0], wi);
-    dotc_acc(acc[1], rs[i], wi);
+    dotc_acc(acc[1], rsi, wi);
   }
   static __device__ void finish(State* st, const double2* s) {
     const int k = st->iter + 1;
@@ -975,8 +990,11 @@ struct TfU {  // x += Œ∑ d (the pending update) ; u = w + Œ≤ u‚ÇÇ ; end of pair 
     stop = st->half || st->fin || st->iter + 1 >= st->maxit;
   }
   __device__ void operator()(int64_t i, double2*) {
-    x[i] = caxpy(x[i], eta, d[i]);
-    if (!stop) u[i] = caxpy(w[i], beta, u2[i]);
+    const C xi = x[i], di = d[i];
+    C wi = czero<C>(), u2i = czero<C>();
+    if (!stop) { wi = w[i]; u2i = u2[i]; }
+    x[i] = caxpy(xi, eta, di);
+    if (!stop) u[i] = caxpy(wi, beta, u2i);
   }
   static __device__ void finish(State* st, const double2*) {
     const int k = st->iter + 1;
@@ -995,10 +1013,11 @@ struct TfV {  // A u (kept) ; v = A u + Œ≤(A u‚ÇÇ + Œ≤v) ; œÉ = ‚ü®r‚ÇÄ*, v‚ü© ;
   C beta;
   __device__ void load(const State* st) { beta = fromd2<C>(st->beta); }
   __device__ void operator()(int64_t i, C val, double2* acc) {
+    const C aui = au[i], vold = v[i], rsi = rs[i];
     aue[i] = val;
-    const C vi = caxpy(val, beta, caxpy(au[i], beta, v[i]));
+    const C vi = caxpy(val, beta, caxpy(aui, beta, vold));
     v[i] = vi;
-    dotc_acc(acc[0], rs[i], vi);
+    dotc_acc(acc[0], rsi, vi);
   }
   static __device__ void finish(State* st, const double2* s) {
     st->matvecs_a++;
@@ -1036,7 +1055,7 @@ struct BlU {  // √ª_{j+1} = A √ª_j ; Œ≥ = ‚ü®rÃÉ, √ª_{j+1}‚ü© ; Œ± = œÅ‚ÇÄ/Œ≥
   using C = Cx<T>;
   C* un; const C* rt;
   __device__ void load(const State*) {}
-  __device__ void operator()(int64_t i, C val, double2* acc) { un[i] = val; dotc_acc(acc[0], rt[i], val); }
+  __device__ void operator()(int64_t i, C val, double2* acc) { const C b = rt[i]; un[i] = val; dotc_acc(acc[0], b, val); }
   static __device__ void finish(State* st, const double2* s) { st->matvecs_a++; sigma_step(st, s[0]); }
 };
 
@@ -1078,7 +1097,7 @@ struct BlR {  // rÃÇ_{j+1} = A rÃÇ_j ; œÅ‚ÇÅ = ‚ü®rÃÉ, rÃÇ_{j+1}‚ü© ; Œ≤ = Œ± œÅ
   using C = Cx<T>;
   C* rn; const C* rt;
   __device__ void load(const State*) {}
-  __device__ void operator()(int64_t i, C val, double2* acc) { rn[i] = val; dotc_acc(acc[0], rt[i], val); }
+  __device__ void operator()(int64_t i, C val, double2* acc) { const C b = rt[i]; rn[i] = val; dotc_acc(acc[0], b, val); }
   static __device__ void finish(State* st, const double2* s) { st->matvecs_a++; bl_next_beta(st, s[0]); }
 };
 
@@ -1204,7 +1223,7 @@ struct PbW0 {  // setup: w‚ÇÄ = A r‚ÇÄ ; Œ±‚ÇÄ = œÅ‚ÇÄ/‚ü®rÃÉ, w‚ÇÄ‚ü©
   using C = Cx<T>;
   C* w; const C* rt;
   __device__ void load(const State*) {}
-  __device__ void operator()(int64_t i, C val, double2* acc) { w[i] = val; dotc_acc(acc[0], rt[i], val); }
+  __device__ void operator()(int64_t i, C val, double2* acc) { const C b = rt[i]; w[i] = val; dotc_acc(acc[0], b, val); }
   static __device__ void finish(State* st, const double2* s) { st->matvecs_a++; sigma_step(st, s[0]); }
 };
 
@@ -1236,8 +1255,9 @@ struct PbP1 {  // p, s, z updates ; q = r ‚àí Œ±s ; y = w ‚àí Œ±z ; ‚Äñq‚Äñ¬≤, ‚
       si = caxpy(w[i], beta, caxmy(s[i], omega, z[i]));
       zi = caxpy(t[i], beta, caxmy(z[i], omega, v[i]));
     }
+    const C ri = r[i], wi = w[i];
     p[i] = pi; s[i] = si; z[i] = zi;
-    const C qi = caxmy(r[i], alpha, si), yi = caxmy(w[i], alpha, zi);
+    const C qi = caxmy(ri, alpha, si), yi = caxmy(wi, alpha, zi);
     q[i] = qi; y[i] = yi;
     nrm_acc(acc[0], qi);
     dotc_acc(acc[1], yi, qi);
@@ -1269,17 +1289,17 @@ struct PbP2 {  // x += Œ±p + œâq ; r = q ‚àí œây ; w = y ‚àí œâ(t ‚àí Œ±v) ; ‚Äñ
   }
   __device__ void operator()(int64_t i, double2* acc) {
     if (half) { x[i] = caxpy(x[i], alpha, p[i]); return; }
-    const C qi = q[i], yi = y[i];
-    x[i] = caxpy(caxpy(x[i], alpha, p[i]), omega, qi);
+    const C qi = q[i], yi = y[i], xi = x[i], pi = p[i], ti = t[i], vi = v[i];
+    const C rti = rt[i], si = s[i], zi = z[i];
+    x[i] = caxpy(caxpy(xi, alpha, pi), omega, qi);
     const C ri = caxmy(qi, omega, yi);
-    const C wi = caxmy(yi, omega, caxmy(t[i], alpha, v[i]));
+    const C wi = caxmy(yi, omega, caxmy(ti, alpha, vi));
     r[i] = ri; w[i] = wi;
-    const C rti = rt[i];
     nrm_acc(acc[0], ri);
     dotc_acc(acc[1], rti, ri);
     dotc_acc(acc[2], rti, wi);
-    dotc_acc(acc[3], rti, s[i]);
-    dotc_acc(acc[4], rti, z[i]);
+    dotc_acc(acc[3], rti, si);
+    dotc_acc(acc[4], rti, zi);
   }
   static __device__ void finish(State* st, const double2* sm) {
     const int k = st->iter + 1;

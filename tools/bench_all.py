@@ -86,6 +86,7 @@ def main():
     ap.add_argument("--reps", type=int, default=0)
     ap.add_argument("--methods", default="")
     ap.add_argument("--no-dense4", action="store_true", help="config 4: FFT operator only")
+    ap.add_argument("--ops", default="csr,stencil", help="config 5 operators")
     a = ap.parse_args()
     global SEL
     SEL = set(a.methods.split(",")) if a.methods else set()
@@ -133,7 +134,7 @@ def main():
             n = 128 ** 3
             rpd, cid, vd = (torch.from_numpy(t).to(dev) for t in (rp, ci, v))
             b_csr = len(v) * (16 + 4) + 4 * (n + 1)
-            for opname in ("csr", "stencil"):
+            for opname in [o for o in ("csr", "stencil") if o in a.ops.split(",")]:
                 h = ccg.ccg_create("c128", n)
                 if opname == "csr":
                     ccg.ccg_set_matvec_csr(h, rpd, cid, vd, 0, n, len(v))
