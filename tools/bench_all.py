@@ -87,6 +87,7 @@ def main():
     ap.add_argument("--methods", default="")
     ap.add_argument("--no-dense4", action="store_true", help="config 4: FFT operator only")
     ap.add_argument("--ops", default="csr,stencil", help="config 5 operators")
+    ap.add_argument("--ops2", default="dense,toeplitz", help="config 2 operators")
     a = ap.parse_args()
     global SEL
     SEL = set(a.methods.split(",")) if a.methods else set()
@@ -100,10 +101,12 @@ def main():
                       cf["maxit"], a.reps or 200, "c128")
         elif c == 2:
             A, y = cfg2()
-            run_dense(2, torch.from_numpy(A).to(dev), torch.from_numpy(y).to(dev), SYM, cf["tol"],
-                      cf["maxit"], a.reps or 50, "c128")
-            run_dense(2, None, torch.from_numpy(y).to(dev), SYM, cf["tol"], cf["maxit"], a.reps or 50, "c128",
-                      toeplitz=(16, 16, 16, dda_kernel((16, 16, 16), 1.0), 3 + 0.5j))
+            if "dense" in a.ops2.split(","):
+                run_dense(2, torch.from_numpy(A).to(dev), torch.from_numpy(y).to(dev), SYM, cf["tol"],
+                          cf["maxit"], a.reps or 50, "c128")
+            if "toeplitz" in a.ops2.split(","):
+                run_dense(2, None, torch.from_numpy(y).to(dev), SYM, cf["tol"], cf["maxit"], a.reps or 50, "c128",
+                          toeplitz=(16, 16, 16, dda_kernel((16, 16, 16), 1.0), 3 + 0.5j))
         elif c == 3:
             n = cf["n"]
             Ad = torch.empty((n, n), dtype=torch.complex64, device=dev)
