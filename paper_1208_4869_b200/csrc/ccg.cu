@@ -121,6 +121,9 @@ struct ccg_ctx {
   // workspace
   State* st = nullptr;
   State* st_host = nullptr;  // pinned
+  int* done_ring = nullptr;   // pinned: done-flag copies of the last two queued chunks
+  cudaEvent_t done_ev[2] = {nullptr, nullptr};
+  bool pipe = false;          // pipelined chunk launches (CCG_PIPELINE=1; off by default)
   double2* part = nullptr;
   size_t part_cap = 0;  // in double2
   unsigned* ticket = nullptr;
@@ -1189,12 +1192,11 @@ static int choose_launch(ccg_ctx* c) {
     c->gemv_mode = (gm && !strcmp(gm, "bulk"))    ? GEMV_BULK
                    : (gm && !strcmp(gm, "rows"))  ? GEMV_ROWS
                    : (gm && !strcmp(gm, "cols"))  ? GEMV_COLS
-                   : (gm && !strcmp(gm, "split")) ? GEMV_SPLIT
-                   // default: the column-owner A·x below 1 GiB of rows (measured
-                   // 5.55 vs 5.18 TB/s at config 2's 268 MB, gemv_modes.jsonl),
-                   // the split kernel above (7.19 vs 6.99 TB/s at config 3)
-                   : ((double)c->mnloc * (double)c->n * (double)sizeof(C) < 1073741824.0) ? GEMV_COLS
-                                                                                           : GEMV_SPLIT;
+                   // default: the split kernel (config 3: 7.19 vs 6.99 TB/s for the
+                   // column-owner layout; config 2 whole solves in an interleaved
+                   // A/B: BiCGSTAB 120.5 vs 124.5 µs/it, COCR 63.7 vs 65.7 —
+                   // profiles/r01/ab/cfg2_gemv.jsonl)
+                   : GEMV_SPLIT;
     const char* qd = getenv("CCG_QMR_DUAL");
     c->qmr_dual = !(qd && !strcmp(qd, "0"));
   }
@@ -1402,21 +1404,44 @@ static int run_iterations(ccg_ctx* c, int m, int maxit) {
     CK(c, cudaGraphInstantiate(&c->gexec[m], graph, 0));
     cudaGraphDestroy(graph);
   }
-  // adaptive chunk: sync every `chunk` iterations (kernels after convergence
-  // are gated and return immediately)
-  int k = 0, chunk = 1;
-  while (k < maxit && !done) {
+  // Chunks of `chunk` graph launches, each followed by an async copy of the
+  // done flag + an event; the host waits for that chunk's flag (~200 µs of
+  // work per chunk).  Iterations queued after convergence are gated on the
+  // device flag and return at once.  CCG_PIPELINE=1 queues chunk j+1 before
+  // waiting for chunk j (no GPU idle on the host round trip, but a whole
+  // gated chunk after convergence): measured ±2 % on long solves and up to
+  // 12 % slower on short ones, so it is off by default.
+  int k = 0, chunk = 1, pending = -1, slot = 0, pending_n = 0;
+  auto t_last = std::chrono::steady_clock::now();
+  while (k < maxit) {
     const int todo = std::min(chunk, maxit - k);
-    auto t0 = std::chrono::steady_clock::now();
     for (int i = 0; i < todo; ++i) {
       CK(c, cudaGraphLaunch(c->gexec[m], c->stream));
       c->launches += c->graph_launches_per_iter[m];
     }
     k += todo;
-    TRY(read_done());
-    const double us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
-    const double per = us / todo;
-    chunk = per > 0 ? (int)std::max(1.0, std::min(32.0, 200.0 / per)) : 32;
+    CK(c, cudaMemcpyAsync(&c->done_ring[slot], &c->st->done, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    CK(c, cudaEventRecord(c->done_ev[slot], c->stream));
+    if (!c->pipe) { pending = slot; pending_n = todo; }   // default: wait for this chunk
+    if (pending >= 0) {
+      CK(c, cudaEventSynchronize(c->done_ev[pending]));
+      if (c->done_ring[pending]) { done = 1; break; }
+      const auto now = std::chrono::steady_clock::now();
+      const double per = std::chrono::duration<double, std::micro>(now - t_last).count() / pending_n;
+      t_last = now;
+      // several ranks: a schedule independent of host timing, so every rank
+      // queues the same iterations (the graphs hold collectives) and all stop
+      // on the same chunk (the done flag derives from allreduced scalars)
+      // One rank, pipelined: the chunk queued ahead only has to cover the host
+      // round trip (~25 µs), and every iteration of it is wasted (gated) work
+      // once the solve has converged; unpipelined: ~200 µs per chunk.
+      const double target = c->pipe ? 25.0 : 200.0;
+      chunk = c->world > 1 ? std::min(32, 2 * chunk)
+                           : per > 0 ? (int)std::max(1.0, std::min(32.0, std::ceil(target / per))) : 32;
+    }
+    pending = slot;
+    pending_n = todo;
+    slot ^= 1;
   }
   return CCG_OK;
 }
@@ -1548,6 +1573,12 @@ static int create_impl(ccg_handle* h, ccg_dtype dt, int64_t n, int world, int ra
   }
   CKC(cudaMalloc(&c->st, sizeof(State)));
   CKC(cudaMallocHost(&c->st_host, sizeof(State)));
+  CKC(cudaMallocHost(&c->done_ring, 2 * sizeof(int)));
+  {
+    const char* pp = getenv("CCG_PIPELINE");
+    c->pipe = pp && !strcmp(pp, "1");
+  }
+  for (auto& e : c->done_ev) CKC(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   CKC(cudaMalloc(&c->ticket, sizeof(unsigned)));
   CKC(cudaMemset(c->ticket, 0, sizeof(unsigned)));
   CKC(cudaMalloc(&c->rank_sum, 16 * sizeof(double2)));
@@ -2180,6 +2211,8 @@ int ccg_destroy(ccg_handle c) {
   if (c->stream) cudaStreamSynchronize(c->stream);
   invalidate_graphs(c);
   for (auto e : c->ev) cudaEventDestroy(e);
+  for (auto e : c->done_ev) if (e) cudaEventDestroy(e);
+  if (c->done_ring) cudaFreeHost(c->done_ring);
   delete c->comm;
   c->comm = nullptr;
   for (int i = 0; i < NLOCAL; ++i) if (c->loc[i]) cudaFree(c->loc[i]);

@@ -1,5 +1,5 @@
-"""Interleaved A/B of CCG_* knobs read at set_matvec time, on config 2 dense
-(c128 n = 4096) or config 5 (CSR / stencil): one handle per setting, then R
+"""Interleaved A/B of CCG_* knobs read at set_matvec time, on config 1 / 2 dense
+(c128 n = 256 / 4096) or config 5 (CSR / stencil): one handle per setting, then R
 rounds alternating between the settings (median µs per iteration per method),
 so clock drift and warm-up do not favour a position.
 
@@ -17,7 +17,7 @@ import torch
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 import paper_1208_4869_b200 as ccg  # noqa: E402
-from workloads import cfg2, helmholtz_csr, helmholtz_rhs, helmholtz_coeffs  # noqa: E402
+from workloads import cfg1, cfg2, helmholtz_csr, helmholtz_rhs, helmholtz_coeffs  # noqa: E402
 
 
 def main():
@@ -30,8 +30,8 @@ def main():
     ap.add_argument("--tol", type=float, default=1e-8)
     a = ap.parse_args()
     dev = torch.device("cuda:0")
-    if a.config == 2:
-        A, y = cfg2()
+    if a.config in (1, 2):
+        A, y = cfg1() if a.config == 1 else cfg2()
         A, y = torch.from_numpy(A).to(dev), torch.from_numpy(y).to(dev)
         n = y.numel()
     else:
@@ -48,7 +48,7 @@ def main():
         for k, v in zip(names, combo):
             os.environ[k] = v
         h = ccg.ccg_create("c128", n)
-        if a.config == 2:
+        if a.config in (1, 2):
             ccg.ccg_set_matvec_dense(h, A, 0, n)
         elif a.op == "csr":
             ccg.ccg_set_matvec_csr(h, rpd, cid, vd, 0, n, vd.numel())
