@@ -17,7 +17,7 @@ import torch
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 import paper_1208_4869_b200 as ccg  # noqa: E402
-from workloads import cfg1, cfg2, helmholtz_csr, helmholtz_rhs, helmholtz_coeffs  # noqa: E402
+from workloads import cfg1, cfg2, cfg4_rhs, dda_kernel, helmholtz_csr, helmholtz_rhs, helmholtz_coeffs  # noqa: E402
 
 
 def main():
@@ -30,7 +30,11 @@ def main():
     ap.add_argument("--tol", type=float, default=1e-8)
     a = ap.parse_args()
     dev = torch.device("cuda:0")
-    if a.config in (1, 2):
+    if a.config == 4:                    # the FFT lattice operator (64 × 32 × 32)
+        y = torch.from_numpy(cfg4_rhs()).to(dev)
+        n = y.numel()
+        kern = dda_kernel((64, 32, 32), 0.5)
+    elif a.config in (1, 2):
         A, y = cfg1() if a.config == 1 else cfg2()
         A, y = torch.from_numpy(A).to(dev), torch.from_numpy(y).to(dev)
         n = y.numel()
@@ -48,7 +52,9 @@ def main():
         for k, v in zip(names, combo):
             os.environ[k] = v
         h = ccg.ccg_create("c128", n)
-        if a.config in (1, 2):
+        if a.config == 4:
+            ccg.ccg_set_matvec_toeplitz3(h, 64, 32, 32, kern, 2.5 + 0.2j)
+        elif a.config in (1, 2):
             ccg.ccg_set_matvec_dense(h, A, 0, n)
         elif a.op == "csr":
             ccg.ccg_set_matvec_csr(h, rpd, cid, vd, 0, n, vd.numel())
