@@ -651,3 +651,46 @@ def test_workspaces_coexist_on_one_handle():
             o = oracle.solve_jacobi(m, DenseOp(A), d, y, 1e-10, 500, **kw)
             g = h.solve(m, y, 1e-10, 500)
             assert abs(g["iterations"] - o.iterations) <= 2 and relerr(g["x"], o.x) <= 1e-8, m
+
+
+# ---------------------------------------------------------------------------
+# Schedule knobs that must not change results: the SELL load schedule
+# (CCG_SELL_ONE: one row per step vs two) and the pipelined chunk launches
+# (CCG_PIPELINE=1) reorder only when loads issue / when the host waits, so
+# products and whole solves are bitwise identical to the defaults.
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("dtype", [np.complex128, np.complex64])
+def test_sell_schedules_bitwise(monkeypatch, dtype):
+    N = 20                                        # 8000 rows: ragged last slice, boundary widths < 7
+    rp, ci, v = helmholtz_csr(N, kh=10 / 128)
+    v = v.astype(dtype)
+    x = _x(N ** 3, dtype, seed=5)
+    ys, sols = [], []
+    for one in ("0", "1"):
+        monkeypatch.setenv("CCG_SELL_ONE", one)
+        with Csr(rp, ci, v, N ** 3, flags=ccg.FLAG_SYMMETRIC) as h:
+            ys.append((h.apply(x, "A"), h.apply(x, "AH")))
+            sols.append(h.solve("bicgstab", helmholtz_rhs(N).astype(dtype), 1e-6, 3000))
+    assert np.array_equal(ys[0][0], ys[1][0]) and np.array_equal(ys[0][1], ys[1][1])
+    assert sols[0]["iterations"] == sols[1]["iterations"] and np.array_equal(sols[0]["x"], sols[1]["x"])
+    assert relerr(ys[1][0], reference_apply_csr(rp, ci, v, x)) <= TOL[dtype]
+
+
+def reference_apply_csr(rp, ci, v, x):
+    return CsrOp(rp, ci, v.astype(np.complex128)).apply(x.astype(np.complex128))
+
+
+@pytest.mark.parametrize("method", ["bicgstab", "cocr", "gmres"])
+def test_pipelined_chunks_bitwise(monkeypatch, method):
+    N = 16
+    rp, ci, v = helmholtz_csr(N, kh=10 / 128)
+    y = helmholtz_rhs(N)
+    out = []
+    for pipe in ("0", "1"):
+        monkeypatch.setenv("CCG_PIPELINE", pipe)
+        with Csr(rp, ci, v, N ** 3) as h:
+            out.append(h.solve(method, y, 1e-8, 3000))
+    a, b = out
+    assert a["status"] == b["status"] == "CONVERGED"
+    assert a["iterations"] == b["iterations"] and np.array_equal(a["x"], b["x"])
+    assert a["true_rel_res"] == b["true_rel_res"]
