@@ -783,7 +783,7 @@ struct Engine {
       case M_CGNE: case M_CGNR: cm.ir.d0 = L(c, 2); break;
       case M_QMR: cm.ir.d0 = L(c, 2); cm.ir.d1 = L(c, 3); cm.ir.d2 = L(c, 4); break;
       case M_BICOR: case M_CORS: cm.ir.d0 = Fs(c, 0); cm.ir.d1 = L(c, 2); break;
-      case M_TFQMR: cm.ir.d0 = L(c, 2); cm.ir.d1 = L(c, 3); cm.ir.d2 = Fs(c, 0); break;
+      case M_TFQMR: case M_PBICGSTAB: cm.ir.d0 = L(c, 2); cm.ir.d1 = L(c, 3); cm.ir.d2 = Fs(c, 0); break;
       default: cm.ir.d0 = Fs(c, 0); break;   // COCR
     }
     cudaLaunchConfig_t cfg = {};
@@ -871,6 +871,14 @@ struct Engine {
                                             TfU<T>{L(c, X), L(c, 5), L(c, 3), Fs(c, 1), Fs(c, 0)},
                                             TfV<T>{L(c, 6), L(c, 7), L(c, 4), L(c, 2)},
                                             TfV0<T>{L(c, 4), L(c, 6), L(c, 2)}, F(c, 0), F(c, 1)});
+      case M_PBICGSTAB:
+        return launch_cluster(
+            c, ClPbicgstab<T>{PbW0<T>{Fs(c, 1), L(c, 3)}, PbStore<T>{L(c, 9)},
+                              PbP1<T>{L(c, 2), Fs(c, 1), L(c, 9), L(c, 8), L(c, 4), L(c, 5), Fs(c, 0), L(c, 6), L(c, 7)},
+                              PbStore<T>{L(c, 8)},
+                              PbP2<T>{L(c, X), L(c, 2), Fs(c, 1), L(c, 4), L(c, 6), L(c, 7), L(c, 9), L(c, 8), L(c, 5),
+                                      Fs(c, 0), L(c, 3)},
+                              PbT<T>{L(c, 9)}, F(c, 0), F(c, 1)});
       default:
         return launch_cluster(c, ClCgnr<T>{CnW<T>{L(c, 3)}, CnX<T>{L(c, X), L(c, 2), Fs(c, 0), L(c, 3)},
                                            CnZ<T>{L(c, 4)}, CnP<T>{L(c, 4), Fs(c, 0)}, CnZ0<T>{Fs(c, 0)}, F(c, 0),
@@ -2126,7 +2134,7 @@ int ccg_solve(ccg_handle c, ccg_method method, const void* x0_local, const void*
     }
   }
   if (c->opk == OPK_DENSE && c->cluster_ok && c->world == 1 && !c->timing && method != CCG_GMRES &&
-      method != CCG_BICGSTABL && method != CCG_PBICGSTAB && !c->jac_dinv) {
+      method != CCG_BICGSTABL && !c->jac_dinv) {
     // small dense system: setup, every iteration and the true residual in ONE
     // cluster launch (cluster.cuh); maxit and the stopping rule live in the State
     c->cl_method = method;

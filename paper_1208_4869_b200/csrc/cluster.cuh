@@ -45,7 +45,7 @@ __device__ __forceinline__ double2 dsmem_ld(const double2* local_addr, unsigned 
 }
 
 constexpr int CL_NT = 512;
-constexpr int CL_KMAX = 4;
+constexpr int CL_KMAX = 5;   // p-BiCGSTAB's second pass has 5 partial sums
 constexpr int CL_MAX = 16;
 
 template <typename T>
@@ -308,6 +308,23 @@ struct ClTfqmr {
     if (!cx.st->gate2) cx.gemv(o, u2f);
     CL_PH(cx.pass(u));
     CL_PH(cx.gemv(v, uf));
+  }
+};
+
+// p-BiCGSTAB (NEXT-2 iii): same phases and buffers as the graph schedule
+template <typename T>
+struct ClPbicgstab {
+  PbW0<T> w0; PbStore<T> t0; PbP1<T> p1; PbStore<T> v; PbP2<T> p2; PbT<T> t;
+  const typename CT<T>::c *zf, *wf;
+  __device__ void setup(ClusterCtx<T>& cx) {
+    CL_PH(cx.gemv(w0, zf));
+    CL_PH(cx.gemv(t0, wf));
+  }
+  __device__ void iter(ClusterCtx<T>& cx) {
+    CL_PH(cx.pass(p1));
+    if (!cx.st->gate2) cx.gemv(v, zf);
+    CL_PH(cx.pass(p2));
+    CL_PH(cx.gemv(t, wf));
   }
 };
 
