@@ -1999,7 +1999,21 @@ static int gmres_workspace(ccg_ctx* c) {
     CK(c, cudaMemset(c->gm_dev, 0, sizeof(GmDev)));
   }
   if (!c->gm_part) {
-    c->gm_grid = (int)std::max<int64_t>(1, std::min<int64_t>((c->nloc + GM_NT - 1) / GM_NT, (int64_t)c->sm_count * 4));
+    // one full wave of the multi-dot passes: CTAs per SM = their occupancy
+    // (76-78 registers → 3 at c128; the former fixed 4 per SM left a
+    // quarter of the CTAs for a second wave).  CCG_GM_CPS overrides (A/B).
+    int o0 = 0, o1 = 0;
+    if (c->dtype == CCG_C64) {
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o0, gm_pass<float, 0>, GM_NT, 0);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, gm_pass<float, 1>, GM_NT, 0);
+    } else {
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o0, gm_pass<double, 0>, GM_NT, 0);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, gm_pass<double, 1>, GM_NT, 0);
+    }
+    int cps = std::max(1, std::min(o0, o1));
+    const char* gc = getenv("CCG_GM_CPS");
+    if (gc) cps = std::max(1, std::min(32, atoi(gc)));
+    c->gm_grid = (int)std::max<int64_t>(1, std::min<int64_t>((c->nloc + GM_NT - 1) / GM_NT, (int64_t)c->sm_count * cps));
     CK(c, cudaMalloc(&c->gm_part, (size_t)c->gm_grid * (GM_MAX + 1) * sizeof(double2)));
     CK(c, cudaMalloc(&c->gm_ticket, sizeof(unsigned)));
     CK(c, cudaMemset(c->gm_ticket, 0, sizeof(unsigned)));
