@@ -95,6 +95,7 @@ struct ccg_ctx {
   double2* gm_rank = nullptr;
   double2* gm_all = nullptr;
   int gm_grid = 1;
+  int gm_fast = 1;   // unrolled multi-dot loads (CCG_GM_FAST=0 disables)
   // BiCGstab(ℓ) workspace: r̂₀..r̂_ℓ, û₀..û_ℓ as full-length buffers
   int bl_l = 2, bl_built = 0;
   void* bl_buf = nullptr;
@@ -968,8 +969,9 @@ struct Engine {
   template <int MODE>
   static int gm_pass_launch(ccg_ctx* c, C* w, const double2* coef, double2* dst, const int* gate) {
     const bool fuse = c->world == 1 || c->rep;
-    launch_k(c, gm_pass<T, MODE>, c->gm_grid, GM_NT, 0, c->stream, Vb(c), c->nloc, w, coef, fuse ? dst : c->gm_rank, c->nloc,
-                                                           c->gm_dev, c->gm_part, c->gm_ticket, fuse ? 1 : 0, gate);
+    auto kern = c->gm_fast ? gm_pass<T, MODE, true> : gm_pass<T, MODE, false>;
+    launch_k(c, kern, c->gm_grid, GM_NT, 0, c->stream, Vb(c), c->nloc, w, coef, fuse ? dst : c->gm_rank, c->nloc,
+             c->gm_dev, c->gm_part, c->gm_ticket, fuse ? 1 : 0, gate);
     c->launches++;
     CK(c, cudaGetLastError());
     if (!fuse) {
@@ -2009,6 +2011,17 @@ static int gmres_workspace(ccg_ctx* c) {
     } else {
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o0, gm_pass<double, 0>, GM_NT, 0);
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, gm_pass<double, 1>, GM_NT, 0);
+    }
+    const char* gf = getenv("CCG_GM_FAST");
+    c->gm_fast = !(gf && !strcmp(gf, "0"));
+    if (c->gm_fast) {
+      if (c->dtype == CCG_C64) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o0, gm_pass<float, 0, true>, GM_NT, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, gm_pass<float, 1, true>, GM_NT, 0);
+      } else {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o0, gm_pass<double, 0, true>, GM_NT, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, gm_pass<double, 1, true>, GM_NT, 0);
+      }
     }
     int cps = std::max(1, std::min(o0, o1));
     const char* gc = getenv("CCG_GM_CPS");

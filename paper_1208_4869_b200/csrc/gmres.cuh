@@ -20,7 +20,12 @@
 namespace ccg {
 
 // MODE 0: out = Vᴴw ; MODE 1: w −= V·coef, out = Vᴴw ; MODE 2: w −= V·coef, out[0] = ‖w‖²
-template <typename T, int MODE>
+// FAST (default): the update's loads go in groups of 4 and a full tile's
+// multi-dot loads are unrolled (issued before their FMAs).  Same operations
+// in the same order; the compiler's FMA contraction of the unrolled code can
+// differ at the last bit (config 5: identical iteration counts, true residual
+// equal to 1e-17 relative).
+template <typename T, int MODE, bool FAST = false>
 __global__ void __launch_bounds__(GM_NT)
 gm_pass(const typename CT<T>::c* __restrict__ V, int64_t ldv, typename CT<T>::c* __restrict__ w,
         const double2* __restrict__ coef, double2* out, int64_t nrows, const GmDev* gm, double2* part,
@@ -47,7 +52,17 @@ gm_pass(const typename CT<T>::c* __restrict__ V, int64_t ldv, typename CT<T>::c*
     if (r < nrows) {
       wv = w[r];
       if (MODE > 0) {
-        for (int i = 0; i < J; ++i) wv = caxmy(wv, cf[i], V[(int64_t)i * ldv + r]);
+        int i = 0;
+        if constexpr (FAST) {
+          for (; i + 4 <= J; i += 4) {
+            C vv[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) vv[u] = V[(int64_t)(i + u) * ldv + r];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) wv = caxmy(wv, cf[i + u], vv[u]);
+          }
+        }
+        for (; i < J; ++i) wv = caxmy(wv, cf[i], V[(int64_t)i * ldv + r]);
         w[r] = wv;
       }
     }
@@ -63,7 +78,15 @@ gm_pass(const typename CT<T>::c* __restrict__ V, int64_t ldv, typename CT<T>::c*
         const int i = warp + a * NW;
         if (i < J) {
           const C* vi = V + (int64_t)i * ldv + base;
-          for (int rr = lane; rr < nr; rr += 32) dotc_acc(acc[a], vi[rr], wt[rr]);
+          if (FAST && nr == GM_NT) {
+            C vv[GM_NT / 32];
+#pragma unroll
+            for (int k = 0; k < GM_NT / 32; ++k) vv[k] = vi[lane + 32 * k];
+#pragma unroll
+            for (int k = 0; k < GM_NT / 32; ++k) dotc_acc(acc[a], vv[k], wt[lane + 32 * k]);
+          } else {
+            for (int rr = lane; rr < nr; rr += 32) dotc_acc(acc[a], vi[rr], wt[rr]);
+          }
         }
       }
     }
