@@ -96,6 +96,7 @@ struct ccg_ctx {
   double2* gm_all = nullptr;
   int gm_grid = 1;
   int gm_fast = 1;   // unrolled multi-dot loads (CCG_GM_FAST=0 disables)
+  int gm_vgrid = 1;  // one wave of gm_normalize / gm_xupdate
   // BiCGstab(ℓ) workspace: r̂₀..r̂_ℓ, û₀..û_ℓ as full-length buffers
   int bl_l = 2, bl_built = 0;
   void* bl_buf = nullptr;
@@ -983,7 +984,7 @@ struct Engine {
   }
   static int gmres_setup(ccg_ctx* c, bool x0) {
     TRY(init_residual(c, x0, Vb(c), nullptr, nullptr, nullptr));
-    launch_k(c, gm_normalize<T>, c->pass_grid, NT, 0, c->stream, Vb(c), c->nloc, Vb(c), Fs(c, 0), c->nloc, c->gm_dev, 1,
+    launch_k(c, gm_normalize<T>, c->gm_vgrid, NT, 0, c->stream, Vb(c), c->nloc, Vb(c), Fs(c, 0), c->nloc, c->gm_dev, 1,
                                                          &c->st->done);
     c->launches++;
     CK(c, cudaGetLastError());
@@ -999,15 +1000,15 @@ struct Engine {
     TRY(gm_pass_launch<1>(c, w, gm->hcol, gm->h2, g));
     TRY(gm_pass_launch<2>(c, w, gm->h2, &gm->ww2, g));
     launch_k(c, gm_step, 1, 1, 0, c->stream, c->st, gm, g);
-    launch_k(c, gm_normalize<T>, c->pass_grid, NT, 0, c->stream, Vb(c), c->nloc, w, Fs(c, 0), c->nloc, gm, 0, &gm->endflag);
+    launch_k(c, gm_normalize<T>, c->gm_vgrid, NT, 0, c->stream, Vb(c), c->nloc, w, Fs(c, 0), c->nloc, gm, 0, &gm->endflag);
     launch_k(c, gm_trisolve, 1, 1, 0, c->stream, c->st, gm, &gm->noend);
-    launch_k(c, gm_xupdate<T>, c->pass_grid, NT, 0, c->stream, L(c, X), Vb(c), c->nloc, c->nloc, gm, &gm->noxupd);
+    launch_k(c, gm_xupdate<T>, c->gm_vgrid, NT, 0, c->stream, L(c, X), Vb(c), c->nloc, c->nloc, gm, &gm->noxupd);
     c->launches += 4;
     CK(c, cudaGetLastError());
     TRY(pass(c, Copy<T>{L(c, X), Fs(c, 2)}, &gm->norestart));
     TRY(allgather(c, 2));
     TRY(matvec_a(c, F(c, 2), GmR<T>{L(c, 1), Vb(c)}, &gm->norestart));
-    launch_k(c, gm_normalize<T>, c->pass_grid, NT, 0, c->stream, Vb(c), c->nloc, Vb(c), Fs(c, 0), c->nloc, gm, 1,
+    launch_k(c, gm_normalize<T>, c->gm_vgrid, NT, 0, c->stream, Vb(c), c->nloc, Vb(c), Fs(c, 0), c->nloc, gm, 1,
                                                          &gm->norestart);
     launch_k(c, gm_reset, 1, 1, 0, c->stream, gm);
     c->launches += 2;
@@ -2027,6 +2028,16 @@ static int gmres_workspace(ccg_ctx* c) {
     const char* gc = getenv("CCG_GM_CPS");
     if (gc) cps = std::max(1, std::min(32, atoi(gc)));
     c->gm_grid = (int)std::max<int64_t>(1, std::min<int64_t>((c->nloc + GM_NT - 1) / GM_NT, (int64_t)c->sm_count * cps));
+    int on = 0, ox = 0;
+    if (c->dtype == CCG_C64) {
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&on, gm_normalize<float>, 256, 0);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ox, gm_xupdate<float>, 256, 0);
+    } else {
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&on, gm_normalize<double>, 256, 0);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ox, gm_xupdate<double>, 256, 0);
+    }
+    c->gm_vgrid = (int)std::max<int64_t>(
+        1, std::min<int64_t>((c->nloc + 255) / 256, (int64_t)c->sm_count * std::max(1, std::min(on, ox))));
     CK(c, cudaMalloc(&c->gm_part, (size_t)c->gm_grid * (GM_MAX + 1) * sizeof(double2)));
     CK(c, cudaMalloc(&c->gm_ticket, sizeof(unsigned)));
     CK(c, cudaMemset(c->gm_ticket, 0, sizeof(unsigned)));
