@@ -158,7 +158,13 @@ int ccg_create(ccg_handle* h, ccg_dtype dt, int64_t n, int world, int rank,
  * allgathers + 4 scalar allgathers.  The API is unchanged: vector arguments
  * are still this rank's nloc-row slices.  Costs n·s per vector pass per rank
  * (negligible against a dense row block). */
-enum { CCG_OPT_REPLICATED = 1 };
+/* CCG_OPT_FORCE_COMM: take the sharded code path (NCCL collectives, the fixed
+ * chunk schedule, graph-captured collectives) even with world == 1, where a
+ * one-rank NCCL communicator is created (nccl_id may then be NULL).  Every
+ * collective is then an identity, so results equal the world == 1 path up to
+ * summation order; it exists to run the NCCL data plane on one GPU.  Combine
+ * with CCG_OPT_REPLICATED for the replicated-vector mode. */
+enum { CCG_OPT_REPLICATED = 1, CCG_OPT_FORCE_COMM = 2 };
 int ccg_create_ex(ccg_handle* h, ccg_dtype dt, int64_t n, int world, int rank,
                   const uint8_t* nccl_id, int device, void* cuda_stream, uint32_t options);
 
@@ -316,6 +322,20 @@ int ccg_get_timing(ccg_handle h, double* ms_a, int32_t* n_a, double* ms_ah, int3
  * (graph-launched kernels included; early-exit kernels after convergence
  * are counted because they are launched). */
 int64_t ccg_last_launch_count(ccg_handle h);
+
+/* Execution statistics of the last ccg_solve on this handle (diagnostics; the
+ * evidence that the sharded data plane ran).  key:
+ *   CCG_STAT_COMM_KIND          0 = no communicator, 1 = NCCL, 2 = loopback
+ *   CCG_STAT_GRAPH_REPLAYS      iteration-graph launches (cudaGraphLaunch)
+ *   CCG_STAT_GRAPH_COLLECTIVES  collective calls executed inside graph replays
+ *                               (calls captured per iteration × replays)
+ *   CCG_STAT_EAGER_COLLECTIVES  collective calls issued outside graphs (setup,
+ *                               true residual, eager loops)
+ *   CCG_STAT_WORLD, CCG_STAT_REPLICATED  the handle's world size / vector mode
+ * Returns CCG_E_ARG for an unknown key or NULL value. */
+enum { CCG_STAT_COMM_KIND = 0, CCG_STAT_GRAPH_REPLAYS = 1, CCG_STAT_GRAPH_COLLECTIVES = 2,
+       CCG_STAT_EAGER_COLLECTIVES = 3, CCG_STAT_WORLD = 4, CCG_STAT_REPLICATED = 5 };
+int ccg_get_stat(ccg_handle h, int32_t key, int64_t* value);
 
 /* cudaStream_t of the handle (for callers that order their own work). */
 void* ccg_get_stream(ccg_handle h);

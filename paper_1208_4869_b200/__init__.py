@@ -41,7 +41,7 @@ EXPORTS = ("ccg_get_unique_id", "ccg_create", "ccg_create_ex", "ccg_create_loopb
            "ccg_set_matvec_toeplitz3", "ccg_set_matvec_callback", "ccg_set_gmres_restart",
            "ccg_set_bicgstab_ell", "ccg_set_jacobi",
            "ccg_apply", "ccg_solve", "ccg_get_history", "ccg_set_timing", "ccg_get_timing",
-           "ccg_last_launch_count", "ccg_get_stream", "ccg_last_error", "ccg_destroy",
+           "ccg_last_launch_count", "ccg_get_stat", "ccg_get_stream", "ccg_last_error", "ccg_destroy",
            "ccg_version")
 
 
@@ -110,6 +110,7 @@ def load():
         "ccg_get_timing": (ctypes.c_int, [vp, ctypes.POINTER(dbl), ctypes.POINTER(i32),
                                           ctypes.POINTER(dbl), ctypes.POINTER(i32)]),
         "ccg_last_launch_count": (i64, [vp]),
+        "ccg_get_stat": (ctypes.c_int, [vp, i32, ctypes.POINTER(i64)]),
         "ccg_get_stream": (vp, [vp]),
         "ccg_last_error": (ctypes.c_char_p, [vp]),
         "ccg_destroy": (ctypes.c_int, [vp]),
@@ -173,6 +174,7 @@ def ccg_get_unique_id():
 
 
 OPT_REPLICATED = 1
+OPT_FORCE_COMM = 2
 
 
 def ccg_create(dtype, n, world=1, rank=0, nccl_id=None, device=0, stream=None, options=0):
@@ -310,6 +312,21 @@ def ccg_get_timing(h):
 
 def ccg_last_launch_count(h):
     return int(load().ccg_last_launch_count(h))
+
+
+STATS = {"comm_kind": 0, "graph_replays": 1, "graph_collectives": 2, "eager_collectives": 3,
+         "world": 4, "replicated": 5}
+
+
+def ccg_get_stat(h, key):
+    """Execution statistics of the last solve (include/ccg.h CCG_STAT_*)."""
+    v = ctypes.c_int64()
+    _check(h, load().ccg_get_stat(h, STATS[key], ctypes.byref(v)))
+    return int(v.value)
+
+
+def ccg_get_stats(h):
+    return {k: ccg_get_stat(h, k) for k in STATS}
 
 
 def ccg_get_stream(h):

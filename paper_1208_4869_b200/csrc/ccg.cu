@@ -1,1168 +1,16 @@
-// ccg.cu — libccg.so: C-ABI (include/ccg.h), matvec engine dispatch, the
-// per-method iteration schedules, CUDA-graph iteration loop and the NCCL
-// row-sharded multi-GPU path.
+// ccg.cu — libccg.so: the C-ABI (include/ccg.h), launch-parameter selection,
+// the CUDA-graph iteration loop and handle / operator / communicator setup.
+// The per-method schedules are in methods_*.cu (Engine<T>, engine.cuh).
 //
 // Paper mapping (PAPER.md = P:<line>):  matvec / cmatvec separated from the
 // iteration (P:17, P:95 [§5]) -> ccg_set_matvec_* + the kernels of
 // matvec.cuh; cgmodule's epsilon_err / maxit -> ccg_solve(tol, maxit);
 // ddprecision.f90 single/double switch -> ccg_dtype.
-#include <cuda_runtime.h>
-#include <dlfcn.h>
-#include <stdint.h>
-#include <stdio.h>
-#include <string.h>
-
-#include <algorithm>
-#include <chrono>
-#include <cmath>
-#include <string>
-#include <vector>
-
-#include "../../include/ccg.h"
-#include "common.cuh"
-#include "matvec.cuh"
-#include "methods.cuh"
-#include "comm.cuh"
-#include "fft.cuh"
-#include "cluster.cuh"
-#include "gmres.cuh"
-
-#include <complex>
-
-using namespace ccg;
+#include "engine.cuh"
 
 namespace {
-thread_local std::string g_create_err;
+thread_local std::string g_create_err;   // ccg_last_error(NULL): why the last create failed
 }  // namespace
-
-// ===========================================================================
-// context
-// ===========================================================================
-enum { NLOCAL = 12, NFULL = 3 };
-enum { OPK_NONE = 0, OPK_DENSE = 1, OPK_CSR = 2, OPK_STENCIL = 3, OPK_TOEPLITZ = 4, OPK_CALLBACK = 5 };
-enum { GEMV_SPLIT = 0, GEMV_BULK = 1, GEMV_ROWS = 2, GEMV_COLS = 3 };
-
-struct ccg_ctx {
-  int dtype = 0;
-  int64_t n = 0, nloc = 0, row0 = 0;   // vector slice of this rank (whole vector when rep)
-  int64_t mnloc = 0, mrow0 = 0;         // operator rows of this rank (= nloc, row0 unless rep)
-  bool rep = false;                     // replicated-vector mode (SURVEY §8(f) NEXT-2 ii)
-  void* rep_tmp = nullptr;              // n: product rows gathered from every rank
-  void* rep_parts = nullptr;            // world × n: Aᴴ partials of every rank
-  int world = 1, rank = 0, device = 0;
-  cudaStream_t stream = nullptr;
-  bool own_stream = false;
-  size_t esz = 8;  // bytes per complex
-  // operator
-  int opk = OPK_NONE;
-  const void* A = nullptr;
-  int64_t lda = 0;
-  uint32_t flags = 0;
-  const int32_t* rowptr = nullptr;
-  const int32_t* colind = nullptr;
-  const void* vals = nullptr;
-  int64_t nnz = 0, halo = 0;
-  int32_t* csr_blocks = nullptr;  // CSR-stream row-block boundaries (device)
-  int csr_nblocks = 0;
-  int64_t* sell_off = nullptr;    // SELL-32 copy of the CSR operator (owned)
-  int32_t* sell_width = nullptr;
-  int32_t* sell_col = nullptr;
-  void* sell_val = nullptr;
-  int sell_grid[2] = {0, 0};
-  int sell_one = 0, sell_waves = 1;   // SELL load schedule / grid waves (CCG_SELL_ONE, CCG_SELL_WAVES)
-  // matrix-free 7-point stencil (ccg_set_matvec_stencil7)
-  int snx = 0, sny = 0, snz = 0, sz0 = 0, snzl = 0, szc = 4;
-  double2 scoef[4] = {};  // d, ox, oy, oz
-  // FFT block-Toeplitz operator (ccg_set_matvec_toeplitz3)
-  FftGeo geo = {};
-  void* fftW = nullptr;   // padded work array X2·Y2·Z2
-  void* fftK = nullptr;   // K̂ / (X2·Y2·Z2)
-  void* fftTw = nullptr;  // exp(−2πi k/Lmax), k < Lmax/2
-  int fft_lmax = 1;
-  double2 tdiag = {};
-  // user matvec callback (ccg_set_matvec_callback)
-  ccg_matvec_fn cb_fn = nullptr;
-  void* cb_user = nullptr;
-  uint32_t cb_caps = 0;
-  void* cb_out = nullptr;   // nloc output rows of the user's product
-  // GMRES(m) workspace (gmres.cuh)
-  int gm_m = 30;
-  GmDev* gm_dev = nullptr;
-  void* gm_V = nullptr;     // (m+1) × nloc basis
-  size_t gm_V_bytes = 0;
-  double2* gm_part = nullptr;
-  unsigned* gm_ticket = nullptr;
-  double2* gm_rank = nullptr;
-  double2* gm_all = nullptr;
-  int gm_grid = 1;
-  int gm_fast = 1;   // unrolled multi-dot loads (CCG_GM_FAST=0 disables)
-  int gm_vgrid = 1;  // one wave of gm_normalize / gm_xupdate
-  // BiCGstab(ℓ) workspace: r̂₀..r̂_ℓ, û₀..û_ℓ as full-length buffers
-  int bl_l = 2, bl_built = 0;
-  void* bl_buf = nullptr;
-  size_t bl_bytes = 0;
-  // right Jacobi preconditioning (ccg_set_jacobi): d and 1/d over all n rows
-  void* jac_d = nullptr;
-  void* jac_dinv = nullptr;
-  void* jac_tmp = nullptr;   // n: D⁻¹·(product input)
-  bool jac_active = false;   // inside ccg_solve
-  // whole-loop cluster kernel for small dense systems (cluster.cuh)
-  bool cluster_ok = false;
-  int cluster_size = 0;   // 0 = not yet chosen
-  int cl_method = 0, cl_has_x0 = 0;
-  bool vec_ok = true;
-  bool bulk_ok = false;   // TMA bulk-copy GEMV usable (alignment / n multiple of a 4 KiB tile)
-  int bulk_grid = 0;
-  int gemv_mode = 0;      // GEMV_SPLIT (default) | GEMV_BULK | GEMV_ROWS (env CCG_GEMV)
-  int split_W = 0, split_strips = 1, split_nrb = 1, nstage2_grid = 1, split_ur = 8;
-  bool cols_ok = false;   // column-owner GEMV usable (vectorised layout, n % V == 0)
-  int cols_strips = 1, cols_S = 1, dual_S = 1, cols_rg = 1;
-  bool qmr_dual = true;   // QMR: A·p and Aᴴ·q in one pass over A (env CCG_QMR_DUAL=0 disables)
-  void* npart = nullptr;  // [strips][nloc] partial row sums of the split / column-owner GEMV
-  size_t npart_bytes = 0;
-  // workspace
-  State* st = nullptr;
-  State* st_host = nullptr;  // pinned
-  int* done_ring = nullptr;   // pinned: done-flag copies of the last two queued chunks
-  cudaEvent_t done_ev[2] = {nullptr, nullptr};
-  bool pipe = false;          // pipelined chunk launches (CCG_PIPELINE=1; off by default)
-  double2* part = nullptr;
-  size_t part_cap = 0;  // in double2
-  unsigned* ticket = nullptr;
-  double2* rank_sum = nullptr;
-  double2* all_sums = nullptr;
-  int* zero_gate = nullptr;
-  void* loc[NLOCAL] = {};
-  void* full[NFULL] = {};
-  void* hpart = nullptr;
-  size_t hpart_bytes = 0;
-  void* wfull = nullptr;
-  double* hist = nullptr;
-  int hist_cap = 0;
-  int hist_len = 0;
-  void* stage_in = nullptr;  // pinned staging (host pointer I/O)
-  size_t stage_bytes = 0;
-  // comm
-  Comm* comm = nullptr;  // NcclComm or LoopbackComm (world > 1)
-  // graphs per method
-  cudaGraphExec_t gexec[M_COUNT] = {};
-  int64_t graph_launches_per_iter[M_COUNT] = {};
-  // launch parameters
-  int sm_count = 148;
-  int gemv_grid = 0, ah_S = 1, ah_strips = 1, pass_grid = 0, stage2_grid = 0, spmv_grid = 0;
-  // timing
-  bool timing = false;
-  std::vector<cudaEvent_t> ev;
-  size_t ev_used = 0;
-  std::vector<int> ev_kind;
-  double ms_a = 0, ms_ah = 0;
-  int n_a = 0, n_ah = 0;
-  int64_t launches = 0;
-  bool capturing = false;
-  bool pdl = true;        // programmatic dependent launch (env CCG_PDL=0 disables)
-  std::string err;
-};
-
-// kernel launch, with the programmatic-dependent-launch attribute unless
-// disabled (CCG_PDL=0): every launched kernel begins with pdl_gate()/pdl_wait()
-template <typename... KArgs, typename... Args>
-static void launch_k(ccg_ctx* c, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
-                     Args&&... args);
-
-#define FAIL(c, code, msg)       \
-  do {                           \
-    (c)->err = (msg);            \
-    return (code);               \
-  } while (0)
-
-#define CK(c, call)                                                                        \
-  do {                                                                                     \
-    cudaError_t e_ = (call);                                                               \
-    if (e_ != cudaSuccess) {                                                               \
-      (c)->err = std::string(#call) + " (line " + std::to_string(__LINE__) + "): " + cudaGetErrorString(e_); \
-      return CCG_E_CUDA;                                                                   \
-    }                                                                                      \
-  } while (0)
-
-#define NK(c, call)                 \
-  do {                              \
-    int r_ = (call);                \
-    if (r_ != 0) {                  \
-      (c)->err = (c)->comm->err;    \
-      return r_;                    \
-    }                               \
-  } while (0)
-
-#define TRY(expr)            \
-  do {                       \
-    int rc_ = (expr);        \
-    if (rc_ != CCG_OK) return rc_; \
-  } while (0)
-
-template <typename... KArgs, typename... Args>
-static void launch_k(ccg_ctx* c, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
-                     Args&&... args) {
-  if (!c->pdl) {
-    kern<<<grid, block, smem, s>>>(std::forward<Args>(args)...);
-    return;
-  }
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = grid;
-  cfg.blockDim = block;
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = s;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = 1;
-  const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
-  if (e != cudaSuccess) {
-    fprintf(stderr, "libccg: launch failed (%s): grid %u,%u,%u block %u smem %zu\n", cudaGetErrorString(e), grid.x,
-            grid.y, grid.z, block.x, smem);
-  }
-}
-
-static bool is_device_ptr(const void* p) {
-  cudaPointerAttributes a;
-  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
-    cudaGetLastError();
-    return false;
-  }
-  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
-}
-
-static Red make_red(ccg_ctx* c) {
-  Red r;
-  r.part = c->part;
-  r.ticket = c->ticket;
-  r.rank_sum = c->rank_sum;
-  r.fuse = (c->world == 1 || c->rep) ? 1 : 0;   // replicated vectors: reductions are local
-  return r;
-}
-
-// ---------------------------------------------------------------------------
-// timing events around matvec launches (kind 0 = A, 1 = AH)
-// ---------------------------------------------------------------------------
-static void tev_begin(ccg_ctx* c, int kind) {
-  if (!c->timing) return;
-  if (c->ev_used + 2 > c->ev.size()) {
-    for (int i = 0; i < 256; ++i) {
-      cudaEvent_t e;
-      cudaEventCreate(&e);
-      c->ev.push_back(e);
-    }
-  }
-  cudaEventRecord(c->ev[c->ev_used], c->stream);
-  c->ev_kind.push_back(kind);
-}
-static void tev_end(ccg_ctx* c) {
-  if (!c->timing) return;
-  cudaEventRecord(c->ev[c->ev_used + 1], c->stream);
-  c->ev_used += 2;
-}
-static void tev_collect(ccg_ctx* c) {
-  if (!c->timing) return;
-  cudaStreamSynchronize(c->stream);
-  for (size_t p = 0; p < c->ev_kind.size(); ++p) {
-    float ms = 0.f;
-    cudaEventElapsedTime(&ms, c->ev[2 * p], c->ev[2 * p + 1]);
-    if (c->ev_kind[p] == 0) { c->ms_a += ms; c->n_a++; } else { c->ms_ah += ms; c->n_ah++; }
-  }
-  c->ev_used = 0;
-  c->ev_kind.clear();
-}
-
-// ===========================================================================
-// Engine<T>: launches
-// ===========================================================================
-template <typename T>
-struct Engine {
-  using C = typename CT<T>::c;
-  static constexpr int NT = 256;
-  static constexpr int R = 8;
-  static constexpr int UR = 8;
-  static constexpr int LPR = 8;
-  static constexpr int BR = 8;        // rows per group, bulk GEMV
-  static constexpr int BSTAGES = 5;   // pipeline depth, bulk GEMV (5 x 36 KiB smem)
-  static constexpr int SUR = 8;       // 16-byte loads in flight per lane, split GEMV
-  static constexpr int SNNZ = 2048;   // nonzeros per CSR-stream block
-
-  static C* L(ccg_ctx* c, int i) { return reinterpret_cast<C*>(c->loc[i]); }
-  static C* F(ccg_ctx* c, int i) { return reinterpret_cast<C*>(c->full[i]); }
-  static C* Fs(ccg_ctx* c, int i) { return reinterpret_cast<C*>(c->full[i]) + c->row0; }  // own slice
-
-  static CommType ndt() { return sizeof(T) == 4 ? CT_F32 : CT_F64; }
-
-  // -------------------- collectives --------------------
-  static int allgather(ccg_ctx* c, int fi) {
-    if (c->world == 1 || c->rep) return CCG_OK;   // replicated vectors are whole on every rank
-    C* buf = F(c, fi);
-    if (c->opk == OPK_CSR || c->opk == OPK_STENCIL) return halo_exchange(c, buf);
-    // dense and FFT-Toeplitz: every rank needs the whole input vector
-    NK(c, c->comm->allgather_inplace(buf, (size_t)c->nloc * 2, ndt(), c->stream));
-    return CCG_OK;
-  }
-  static int halo_exchange(ccg_ctx* c, C* buf) {
-    NK(c, c->comm->halo(buf, c->row0, c->nloc, c->halo, sizeof(C), ndt(), c->stream));
-    return CCG_OK;
-  }
-  // scalar phase for world > 1: allgather this rank's K sums, sum in rank order
-  template <class Fin>
-  static int post(ccg_ctx* c, const int* gate) {
-    constexpr int K = Fin::K;
-    if constexpr (K > 0) {
-      if (c->world > 1 && !c->rep) {
-        NK(c, c->comm->allgather(c->rank_sum, c->all_sums, (size_t)K * 2, CT_F64, c->stream));
-        launch_k(c, scalar_kernel<K, Fin>, 1, 1, 0, c->stream, c->all_sums, c->world, c->st, gate);
-        c->launches++;
-      }
-    }
-    return CCG_OK;
-  }
-
-  // -------------------- kernels --------------------
-  template <class Op>
-  static int pass(ccg_ctx* c, Op op, const int* gate) {
-    // whole waves at this functor's own occupancy (register use differs
-    // between phases: 32-48 registers => 5-8 CTAs per SM)
-    static int occ = 0;
-    if (occ == 0) {
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, pass_kernel<NT, Op>, NT, 0);
-      occ = std::max(1, std::min(occ, 8));
-    }
-    const int grid = (int)std::max<int64_t>(
-        1, std::min<int64_t>((c->nloc + NT - 1) / NT, (int64_t)c->sm_count * occ));
-    launch_k(c, pass_kernel<NT, Op>, grid, NT, 0, c->stream, op, c->nloc, make_red(c), c->st, gate);
-    c->launches++;
-    CK(c, cudaGetLastError());
-    return post<Op>(c, gate);
-  }
-
-  // a K = 0 elementwise pass over `count` elements (the whole vector)
-  template <class Op>
-  static int pass_count(ccg_ctx* c, Op op, int64_t count, const int* gate) {
-    static_assert(Op::K == 0, "pass_count: no reduction");
-    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((count + NT - 1) / NT, (int64_t)c->sm_count * 8));
-    launch_k(c, pass_kernel<NT, Op>, grid, NT, 0, c->stream, op, count, make_red(c), c->st, gate);
-    c->launches++;
-    CK(c, cudaGetLastError());
-    return CCG_OK;
-  }
-
-  // CSR SpMV: CSR-stream blocks (default) or LPR lanes per row (CCG_SPMV=lanes)
-  template <bool CONJ, class Epi>
-  static void spmv(ccg_ctx* c, const C* x, Epi epi, const int* gate) {
-    const C* vals = reinterpret_cast<const C*>(c->vals);
-    if (c->sell_col) {
-      auto k = c->sell_one ? spmv_sell_kernel<T, NT, CONJ, true, Epi> : spmv_sell_kernel<T, NT, CONJ, false, Epi>;
-      launch_k(c, k, c->sell_grid[c->sell_one], NT, 0, c->stream,
-          c->sell_off, c->sell_width, c->sell_col, reinterpret_cast<const C*>(c->sell_val), x, c->mnloc, epi,
-          make_red(c), c->st, gate);
-    }
-    else if (c->csr_blocks)
-      launch_k(c, spmv_stream_kernel<T, NT, SNNZ, CONJ, Epi>, c->spmv_grid, NT, 0, c->stream, 
-          c->rowptr, c->colind, vals, x, c->csr_blocks, c->csr_nblocks, epi, make_red(c), c->st, gate);
-    else
-      launch_k(c, spmv_csr_kernel<T, LPR, NT, CONJ, Epi>, c->spmv_grid, NT, 0, c->stream, 
-          c->rowptr, c->colind, vals, x, c->mnloc, epi, make_red(c), c->st, gate);
-  }
-
-  // matrix-free stencil; conj => Aᴴ (= the stencil with conjugated
-  // coefficients, A being complex symmetric)
-  template <class Epi>
-  static void stencil(ccg_ctx* c, const C* xfull, bool conj, Epi epi, const int* gate) {
-    C k[4];
-    for (int i = 0; i < 4; ++i) {
-      k[i].x = (T)c->scoef[i].x;
-      k[i].y = (T)(conj ? -c->scoef[i].y : c->scoef[i].y);
-    }
-    dim3 g((c->snx + 31) / 32, (c->sny + 7) / 8, (c->snzl + c->szc - 1) / c->szc);
-    launch_k(c, stencil7_kernel<T, Epi>, g, 256, 0, c->stream, xfull, c->snx, c->sny, c->snz, c->sz0, c->snzl, c->szc,
-                                                       k[0], k[1], k[2], k[3], epi, make_red(c), c->st, gate);
-  }
-
-  // FFT block-Toeplitz product (fft.cuh); op: 0 = A, 1 = Aᴴ, 2 = Aᵀ.  Every
-  // rank transforms the whole (gathered) vector and keeps its own rows.
-  template <class Epi>
-  static void toeplitz(ccg_ctx* c, const C* xfull, int op, Epi epi, const int* gate) {
-    const FftGeo& g = c->geo;
-    C* W = reinterpret_cast<C*>(c->fftW);
-    const C* Kh = reinterpret_cast<const C*>(c->fftK);
-    const C* tw = reinterpret_cast<const C*>(c->fftTw);
-    const int L = c->fft_lmax;
-    const size_t smx = (size_t)g.tx * g.X2 * sizeof(C);
-    const size_t smy = (size_t)g.tyz * g.Y2 * sizeof(C);
-    const size_t smz = (size_t)g.tyz * g.Z2 * sizeof(C);
-    const int gx = (g.ny * g.nz + g.tx - 1) / g.tx;
-    // threads per CTA: one per butterfly of its lines (a multiple of 32, ≤ 256)
-    auto bt = [](int lines, int len) { return std::max(32, std::min(256, ((lines * len / 2 + 31) / 32) * 32)); };
-    const int btx = bt(g.tx, g.X2), bty = bt(g.tyz, g.Y2), btz = bt(g.tyz, g.Z2);
-    if (op == 1)
-      launch_k(c, fft_fwd_x<T, true>, gx, btx, smx, c->stream, xfull, W, g, tw, L / g.X2, gate);
-    else
-      launch_k(c, fft_fwd_x<T, false>, gx, btx, smx, c->stream, xfull, W, g, tw, L / g.X2, gate);
-    launch_k(c, fft_fwd_y<T>, dim3(g.X2 / g.tyz, g.nz), bty, smy, c->stream, W, g, tw, L / g.Y2, gate);
-    if (op == 0)
-      launch_k(c, fft_z_mul<T, false>, dim3(g.X2 / g.tyz, g.Y2), btz, smz, c->stream, W, Kh, g, tw, L / g.Z2, gate);
-    else
-      launch_k(c, fft_z_mul<T, true>, dim3(g.X2 / g.tyz, g.Y2), btz, smz, c->stream, W, Kh, g, tw, L / g.Z2, gate);
-    launch_k(c, fft_inv_y<T>, dim3(g.X2 / g.tyz, g.nz), bty, smy, c->stream, W, g, tw, L / g.Y2, gate);
-    C d;
-    d.x = (T)c->tdiag.x;
-    d.y = (T)(op == 1 ? -c->tdiag.y : c->tdiag.y);
-    if (op == 1)
-      launch_k(c, fft_inv_x<T, true, Epi>, gx, 256, smx, c->stream, W, xfull, g, tw, L / g.X2, d, c->row0, c->nloc, epi,
-                                                            make_red(c), c->st, gate);
-    else
-      launch_k(c, fft_inv_x<T, false, Epi>, gx, 256, smx, c->stream, W, xfull, g, tw, L / g.X2, d, c->row0, c->nloc, epi,
-                                                             make_red(c), c->st, gate);
-    c->launches += 4;
-  }
-
-  // the user's product (ccg_set_matvec_callback) into cb_out, then the
-  // method's epilogue as one fused pass over it
-  template <class Epi>
-  static int user_product(ccg_ctx* c, int op, const C* xfull, Epi epi, const int* gate) {
-    C* out = c->rep ? reinterpret_cast<C*>(c->rep_tmp) : reinterpret_cast<C*>(c->cb_out);
-    tev_begin(c, op == CCG_OP_A ? 0 : 1);
-    const int rc = c->cb_fn(c->cb_user, op, xfull, c->rep ? out + c->mrow0 : out, c->n, c->mrow0, c->mnloc,
-                            c->stream);
-    tev_end(c);
-    if (rc != 0) FAIL(c, CCG_E_USER, "user matvec callback returned " + std::to_string(rc));
-    CK(c, cudaGetLastError());
-    if (c->rep) NK(c, c->comm->allgather_inplace(out, (size_t)c->mnloc * 2, ndt(), c->stream));
-    EpiPass<C, Epi> ep{epi, out};
-    return pass(c, ep, gate);
-  }
-
-  // replicated vectors: this rank's product rows (Store into rep_tmp at mrow0),
-  // allgathered, then the method epilogue as one pass over the whole vector
-  template <class Epi>
-  static int rep_finish_rows(ccg_ctx* c, Epi epi, const int* gate) {
-    C* tmp = reinterpret_cast<C*>(c->rep_tmp);
-    NK(c, c->comm->allgather_inplace(tmp, (size_t)c->mnloc * 2, ndt(), c->stream));
-    EpiPass<C, Epi> ep{epi, tmp};
-    return pass(c, ep, gate);
-  }
-
-  // y_local = A · xfull (full-length buffer, own slice + gathered/halo parts)
-  template <class Epi>
-  static int matvec_a(ccg_ctx* c, const C* xfull, Epi epi, const int* gate) {
-    if (c->jac_active) {   // B·v = A(D⁻¹v): scale the (whole) input first
-      C* tmp = reinterpret_cast<C*>(c->jac_tmp);
-      TRY(pass_count(c, JacScale<T>{xfull, reinterpret_cast<const C*>(c->jac_dinv), tmp}, c->n, gate));
-      xfull = tmp;
-    }
-    if (c->opk == OPK_CALLBACK) return user_product(c, CCG_OP_A, xfull, epi, gate);
-    if (c->rep && c->opk != OPK_TOEPLITZ) {
-      TRY(matvec_rows(c, xfull, Store<T>{reinterpret_cast<C*>(c->rep_tmp) + c->mrow0}, gate));
-      return rep_finish_rows(c, epi, gate);
-    }
-    return matvec_rows(c, xfull, epi, gate);
-  }
-
-  // this rank's rows of A·x (all operators), epilogue per row
-  template <class Epi>
-  static int matvec_rows(ccg_ctx* c, const C* xfull, Epi epi, const int* gate) {
-    tev_begin(c, 0);
-    if (c->opk == OPK_TOEPLITZ) {
-      toeplitz(c, xfull, 0, epi, gate);
-    } else if (c->opk == OPK_STENCIL) {
-      stencil(c, xfull, false, epi, gate);
-    } else if (c->opk == OPK_DENSE && c->gemv_mode == GEMV_SPLIT) {
-      const C* A = reinterpret_cast<const C*>(c->A);
-      C* part = reinterpret_cast<C*>(c->npart);
-      dim3 g(c->split_strips, c->split_nrb);
-      const size_t smem = (size_t)c->split_W * sizeof(C);
-      if (c->split_strips == 1) {
-        if (c->vec_ok)
-          launch_k(c, gemv_n_split<T, NT, SUR, true, true, Epi>, g, NT, smem, c->stream, 
-              A, c->lda, xfull, c->n, c->mnloc, c->split_W, part, epi, make_red(c), c->st, gate);
-        else
-          launch_k(c, gemv_n_split<T, NT, SUR, false, true, Epi>, g, NT, smem, c->stream, 
-              A, c->lda, xfull, c->n, c->mnloc, c->split_W, part, epi, make_red(c), c->st, gate);
-      } else {
-        Store<T> none{nullptr};
-        if (c->vec_ok && c->split_ur == 16)
-          launch_k(c, gemv_n_split<T, NT, 16, true, false, Store<T>>, g, NT, smem, c->stream, 
-              A, c->lda, xfull, c->n, c->mnloc, c->split_W, part, none, make_red(c), c->st, gate);
-        else if (c->vec_ok && c->split_ur == 4)
-          launch_k(c, gemv_n_split<T, NT, 4, true, false, Store<T>>, g, NT, smem, c->stream, 
-              A, c->lda, xfull, c->n, c->mnloc, c->split_W, part, none, make_red(c), c->st, gate);
-        else if (c->vec_ok)
-          launch_k(c, gemv_n_split<T, NT, SUR, true, false, Store<T>>, g, NT, smem, c->stream, 
-              A, c->lda, xfull, c->n, c->mnloc, c->split_W, part, none, make_red(c), c->st, gate);
-        else
-          launch_k(c, gemv_n_split<T, NT, SUR, false, false, Store<T>>, g, NT, smem, c->stream, 
-              A, c->lda, xfull, c->n, c->mnloc, c->split_W, part, none, make_red(c), c->st, gate);
-        c->launches++;
-        CK(c, cudaGetLastError());
-        launch_k(c, gemv_h_stage2<T, NT, Epi>, c->nstage2_grid, NT, 0, c->stream, part, c->split_strips, c->mnloc, 0,
-                                                                          c->mnloc, epi, make_red(c), c->st, gate);
-      }
-    } else if (c->opk == OPK_DENSE && c->gemv_mode == GEMV_COLS && c->cols_ok) {
-      C* part = reinterpret_cast<C*>(c->npart);
-      if (c->cols_rg == 4)
-        launch_k(c, gemv_cols<T, NT, true, false, false, 4>, dim3(c->cols_strips, c->cols_S), NT, 0, c->stream, 
-            reinterpret_cast<const C*>(c->A), c->lda, xfull, nullptr, c->mnloc, c->n, part, nullptr, gate);
-      else
-        launch_k(c, gemv_cols<T, NT, true, false, false, 1>, dim3(c->cols_strips, c->cols_S), NT, 0, c->stream, 
-            reinterpret_cast<const C*>(c->A), c->lda, xfull, nullptr, c->mnloc, c->n, part, nullptr, gate);
-      c->launches++;
-      CK(c, cudaGetLastError());
-      launch_k(c, gemv_h_stage2<T, NT, Epi>, c->nstage2_grid, NT, 0, c->stream, part, c->cols_strips, c->mnloc, 0, c->mnloc,
-                                                                        epi, make_red(c), c->st, gate);
-    } else if (c->opk == OPK_DENSE && c->gemv_mode == GEMV_BULK && c->bulk_ok) {
-      constexpr size_t smem = bulk_smem_bytes<BR, BSTAGES>();
-      auto kern = gemv_n_bulk<T, BR, BSTAGES, Epi>;
-      static bool attr_set = false;  // per instantiation
-      if (!attr_set) {
-        CK(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr_set = true;
-      }
-      launch_k(c, kern, c->bulk_grid, BULK_NT, smem, c->stream, reinterpret_cast<const C*>(c->A), c->lda, xfull, c->n,
-                                                       c->mnloc, epi, make_red(c), c->st, gate);
-    } else if (c->opk == OPK_DENSE) {
-      const C* A = reinterpret_cast<const C*>(c->A);
-      if (c->vec_ok)
-        launch_k(c, gemv_n_kernel<T, R, NT, true, Epi>, c->gemv_grid, NT, 0, c->stream, 
-            A, c->lda, xfull, c->n, c->mnloc, epi, make_red(c), c->st, gate);
-      else
-        launch_k(c, gemv_n_kernel<T, R, NT, false, Epi>, c->gemv_grid, NT, 0, c->stream, 
-            A, c->lda, xfull, c->n, c->mnloc, epi, make_red(c), c->st, gate);
-    } else {
-      spmv<false>(c, xfull, epi, gate);
-    }
-    c->launches++;
-    tev_end(c);
-    CK(c, cudaGetLastError());
-    return post<Epi>(c, gate);
-  }
-
-  // y_local = op(A) · x_local, op = Aᴴ (conj) or Aᵀ.  With replicated vectors
-  // x_local is the whole vector: complex-symmetric operators compute their own
-  // rows, the dense product this rank's full-length partial, summed over ranks
-  // in rank order inside the epilogue pass.
-  template <class Epi>
-  static int matvec_h(ccg_ctx* c, const C* xloc, bool conj, Epi epi, const int* gate) {
-    if (c->jac_active) {   // Bᴴv = conj(D⁻¹)(Aᴴv), Bᵀv = D⁻¹(Aᵀv): scale inside the epilogue
-      JacEpi<T, Epi> je{epi, reinterpret_cast<const C*>(c->jac_dinv) + c->row0, conj ? 1 : 0};
-      return matvec_h_impl(c, xloc, conj, je, gate);
-    }
-    return matvec_h_impl(c, xloc, conj, epi, gate);
-  }
-  template <class Epi>
-  static int matvec_h_impl(ccg_ctx* c, const C* xloc, bool conj, Epi epi, const int* gate) {
-    const bool gathered_in = c->world > 1 && !c->rep;   // the input needs gathering first
-    if (c->opk == OPK_CALLBACK) {
-      const C* xin = xloc;
-      if (gathered_in) {
-        CK(c, cudaMemcpyAsync(Fs(c, 2), xloc, c->nloc * sizeof(C), cudaMemcpyDeviceToDevice, c->stream));
-        TRY(allgather(c, 2));
-        xin = F(c, 2);
-      }
-      return user_product(c, conj ? CCG_OP_AH : CCG_OP_AT, xin, epi, gate);
-    }
-    if (c->opk == OPK_TOEPLITZ) {
-      const C* xin = xloc;
-      if (gathered_in) {
-        CK(c, cudaMemcpyAsync(Fs(c, 2), xloc, c->nloc * sizeof(C), cudaMemcpyDeviceToDevice, c->stream));
-        TRY(allgather(c, 2));
-        xin = F(c, 2);
-      }
-      tev_begin(c, 1);
-      toeplitz(c, xin, conj ? 1 : 2, epi, gate);
-      c->launches++;
-      tev_end(c);
-      CK(c, cudaGetLastError());
-      return post<Epi>(c, gate);
-    }
-    if (c->opk == OPK_STENCIL || c->opk == OPK_CSR) {
-      // complex-symmetric operator: Aᵀ = A, Aᴴx = conj(A conj x) (the stencil
-      // conjugates its coefficients); its own rows from the whole input
-      const C* xin = xloc;
-      if (gathered_in) {
-        CK(c, cudaMemcpyAsync(Fs(c, 2), xloc, c->nloc * sizeof(C), cudaMemcpyDeviceToDevice, c->stream));
-        TRY(allgather(c, 2));
-        xin = F(c, 2);
-      }
-      auto launch = [&](auto e) {
-        if (c->opk == OPK_STENCIL) stencil(c, xin, conj, e, gate);
-        else if (conj) spmv<true>(c, xin, e, gate);
-        else spmv<false>(c, xin, e, gate);
-      };
-      tev_begin(c, 1);
-      if (c->rep) launch(Store<T>{reinterpret_cast<C*>(c->rep_tmp) + c->mrow0});
-      else launch(epi);
-      c->launches++;
-      tev_end(c);
-      CK(c, cudaGetLastError());
-      if (c->rep) return rep_finish_rows(c, epi, gate);
-      return post<Epi>(c, gate);
-    }
-    const C* A = reinterpret_cast<const C*>(c->A);
-    C* part = reinterpret_cast<C*>(c->hpart);
-    const C* xr = c->rep ? xloc + c->mrow0 : xloc;   // the x entries of this rank's rows
-    dim3 g1(c->ah_strips, c->ah_S);
-    tev_begin(c, 1);
-    if (c->vec_ok) {
-      if (conj)
-        launch_k(c, gemv_h_stage1<T, true, NT, UR, true>, g1, NT, 0, c->stream, A, c->lda, xr, c->mnloc, c->n, part, gate);
-      else
-        launch_k(c, gemv_h_stage1<T, false, NT, UR, true>, g1, NT, 0, c->stream, A, c->lda, xr, c->mnloc, c->n, part, gate);
-    } else {
-      if (conj)
-        launch_k(c, gemv_h_stage1<T, true, NT, UR, false>, g1, NT, 0, c->stream, A, c->lda, xr, c->mnloc, c->n, part, gate);
-      else
-        launch_k(c, gemv_h_stage1<T, false, NT, UR, false>, g1, NT, 0, c->stream, A, c->lda, xr, c->mnloc, c->n, part, gate);
-    }
-    c->launches++;
-    CK(c, cudaGetLastError());
-    if (c->world == 1) {
-      launch_k(c, gemv_h_stage2<T, NT, Epi>, c->stage2_grid, NT, 0, c->stream, part, c->ah_S, c->n, 0, c->n, epi,
-                                                                       make_red(c), c->st, gate);
-      c->launches++;
-      tev_end(c);
-      CK(c, cudaGetLastError());
-      return CCG_OK;
-    }
-    // multi GPU: full-length partial of this rank
-    C* wf = c->rep ? reinterpret_cast<C*>(c->rep_tmp) : reinterpret_cast<C*>(c->wfull);
-    Store<T> stv{wf};
-    launch_k(c, gemv_h_stage2<T, NT, Store<T>>, c->stage2_grid, NT, 0, c->stream, part, c->ah_S, c->n, 0, c->n, stv,
-                                                                         make_red(c), c->st, gate);
-    c->launches++;
-    tev_end(c);
-    CK(c, cudaGetLastError());
-    if (c->rep) {
-      // every rank's partial, summed in rank order inside the epilogue pass
-      C* parts = reinterpret_cast<C*>(c->rep_parts);
-      NK(c, c->comm->allgather(wf, parts, (size_t)c->n * 2, ndt(), c->stream));
-      EpiPassSum<C, Epi> ep{epi, parts, c->world, c->n};
-      return pass(c, ep, gate);
-    }
-    C* wl = L(c, NLOCAL - 1);   // row-sharded: reduce-scatter -> epilogue pass
-    NK(c, c->comm->reduce_scatter(c->wfull, wl, (size_t)c->nloc * 2, ndt(), c->stream));
-    EpiPass<C, Epi> ep{epi, wl};
-    return pass(c, ep, gate);
-  }
-
-  // p̃ = A·p (epilogue ea) and w = Aᴴ·q (epilogue eh) in ONE pass over A
-  // (gemv_cols<DO_N, DO_H>).  ea's scalar step runs
-  // before eh's epilogue (QMR: ε, β before w̃ = Aᴴq − conj(β)w).
-  template <class EpiA, class EpiH>
-  static int matvec_dual(ccg_ctx* c, const C* pfull, const C* qloc, EpiA ea, EpiH eh, const int* gate) {
-    const C* A = reinterpret_cast<const C*>(c->A);
-    C* np = reinterpret_cast<C*>(c->npart);
-    C* hp = reinterpret_cast<C*>(c->hpart);
-    tev_begin(c, 0);
-    launch_k(c, gemv_cols<T, NT, true, true, true>, dim3(c->cols_strips, c->dual_S), NT, 0, c->stream, 
-        A, c->lda, pfull, qloc, c->nloc, c->n, np, hp, gate);
-    c->launches++;
-    CK(c, cudaGetLastError());
-    launch_k(c, gemv_h_stage2<T, NT, EpiA>, c->nstage2_grid, NT, 0, c->stream, np, c->cols_strips, c->nloc, 0, c->nloc, ea,
-                                                                      make_red(c), c->st, gate);
-    c->launches++;
-    tev_end(c);
-    CK(c, cudaGetLastError());
-    TRY(post<EpiA>(c, gate));
-    if (c->world == 1) {
-      launch_k(c, gemv_h_stage2<T, NT, EpiH>, c->stage2_grid, NT, 0, c->stream, hp, c->dual_S, c->n, 0, c->n, eh,
-                                                                       make_red(c), c->st, gate);
-      c->launches++;
-      CK(c, cudaGetLastError());
-      return CCG_OK;
-    }
-    Store<T> stv{reinterpret_cast<C*>(c->wfull)};
-    launch_k(c, gemv_h_stage2<T, NT, Store<T>>, c->stage2_grid, NT, 0, c->stream, hp, c->dual_S, c->n, 0, c->n, stv,
-                                                                         make_red(c), c->st, gate);
-    c->launches++;
-    CK(c, cudaGetLastError());
-    C* wl = L(c, NLOCAL - 1);
-    NK(c, c->comm->reduce_scatter(c->wfull, wl, (size_t)c->nloc * 2, ndt(), c->stream));
-    EpiPass<C, EpiH> ep{eh, wl};
-    return pass(c, ep, gate);
-  }
-
-  // ==================== method schedules ====================
-  // local vector slots (NLOCAL-1 is reserved for the multi-GPU Aᴴ result)
-  enum { X = 0 };
-
-  static int init_residual(ccg_ctx* c, bool has_x0, C* d0, C* d1, C* d2, C* d3) {
-    const int* g = c->zero_gate;
-    C* y = L(c, 1);  // y is staged in loc[1] by solve()
-    InitR<T> ir{y, d0, d1, d2, d3};
-    if (has_x0) {
-      // x0 already copied into loc[X]; gather it into full[2]
-      Copy<T> cp{L(c, X), Fs(c, 2)};
-      TRY(pass(c, cp, g));
-      TRY(allgather(c, 2));
-      return matvec_a(c, F(c, 2), ir, g);
-    }
-    return pass(c, ir, g);
-  }
-
-  // ---- BiCGSTAB: loc: 0 x, 1 y, 2 r, 3 rt, 4 v, 5 t ; full: 0 p, 1 s
-  static int bicgstab_setup(ccg_ctx* c, bool x0) { return init_residual(c, x0, L(c, 2), L(c, 3), nullptr, nullptr); }
-  static int bicgstab_iter(ccg_ctx* c) {
-    const int* g = &c->st->done;
-    const int* g2 = &c->st->gate2;
-    TRY(pass(c, BsP<T>{L(c, 2), Fs(c, 0), L(c, 4)}, g));
-    TRY(allgather(c, 0));
-    TRY(matvec_a(c, F(c, 0), BsV<T>{L(c, 4), L(c, 3)}, g));
-    TRY(pass(c, BsS<T>{L(c, 2), L(c, 4), Fs(c, 1)}, g));
-    TRY(allgather(c, 1));
-    TRY(matvec_a(c, F(c, 1), BsT<T>{L(c, 5), Fs(c, 1)}, g2));
-    return pass(c, BsX<T>{L(c, X), L(c, 2), Fs(c, 0), Fs(c, 1), L(c, 5), L(c, 3)}, g);
-  }
-
-  // ---- CGNE: loc: 0 x, 1 y, 2 r ; full: 0 p
-  static int cgne_setup(ccg_ctx* c, bool x0) {
-    TRY(init_residual(c, x0, L(c, 2), nullptr, nullptr, nullptr));
-    return matvec_h(c, L(c, 2), true, CgP0<T>{Fs(c, 0)}, &c->st->done);
-  }
-  static int cgne_iter(ccg_ctx* c) {
-    const int* g = &c->st->done;
-    TRY(allgather(c, 0));
-    TRY(matvec_a(c, F(c, 0), CgQ<T>{L(c, 2), L(c, X), Fs(c, 0)}, g));
-    return matvec_h(c, L(c, 2), true, CgP<T>{Fs(c, 0)}, g);
-  }
-
-  // ---- QMR: loc: 0 x, 1 y, 2 r, 3 vt, 4 wt, 5 v, 6 w, 7 q, 8 pt, 9 d, 10 s ; full: 0 p
-  static int qmr_setup(ccg_ctx* c, bool x0) {
-    TRY(init_residual(c, x0, L(c, 2), L(c, 3), L(c, 4), nullptr));
-    return pass(c, QmV<T>{L(c, 3), L(c, 4), L(c, 5), L(c, 6)}, &c->st->done);
-  }
-  static int qmr_iter(ccg_ctx* c) {
-    const int* g = &c->st->done;
-    TRY(pass(c, QmP<T>{L(c, 5), L(c, 6), Fs(c, 0), L(c, 7)}, g));
-    TRY(allgather(c, 0));
-    if (c->opk == OPK_DENSE && c->cols_ok && c->qmr_dual && !c->rep && !c->jac_active) {
-      TRY(matvec_dual(c, F(c, 0), L(c, 7), QmPt<T>{L(c, 8), L(c, 7)},
-                      QmVW<T>{L(c, 3), L(c, 4), L(c, 8), L(c, 5), L(c, 6)}, g));
-    } else {
-      TRY(matvec_a(c, F(c, 0), QmPt<T>{L(c, 8), L(c, 7)}, g));
-      TRY(matvec_h(c, L(c, 7), true, QmVW<T>{L(c, 3), L(c, 4), L(c, 8), L(c, 5), L(c, 6)}, g));
-    }
-    return pass(c, QmDV<T>{L(c, 9), L(c, 10), L(c, X), L(c, 2), Fs(c, 0), L(c, 8), L(c, 3), L(c, 4), L(c, 5),
-                           L(c, 6)},
-                g);
-  }
-
-  // ---- BiCOR: loc: 0 x, 1 y, 2 rs, 3 rh, 4 p, 5 ps, 6 q, 7 qs ; full: 0 r
-  static int bicor_setup(ccg_ctx* c, bool x0) { return init_residual(c, x0, Fs(c, 0), L(c, 2), nullptr, nullptr); }
-  static int bicor_iter(ccg_ctx* c) {
-    const int* g = &c->st->done;
-    TRY(allgather(c, 0));
-    TRY(matvec_a(c, F(c, 0), RhoEpi<T>{L(c, 3), L(c, 2)}, g));
-    TRY(pass(c, BcP<T>{Fs(c, 0), L(c, 2), L(c, 3), L(c, 4), L(c, 5), L(c, 6)}, g));
-    TRY(matvec_h(c, L(c, 5), true, BcQs<T>{L(c, 7), L(c, 6)}, g));
-    return pass(c, BcX<T>{L(c, X), Fs(c, 0), L(c, 2), L(c, 4), L(c, 6), L(c, 7)}, g);
-  }
-
-  // ---- CORS: loc: 0 x, 1 y, 2 r0s, 3 rh, 4 e, 5 eh, 6 h, 7 hh, 8 q ; full: 0 r, 1 qh
-  static int cors_setup(ccg_ctx* c, bool x0) { return init_residual(c, x0, Fs(c, 0), L(c, 2), nullptr, nullptr); }
-  static int cors_iter(ccg_ctx* c) {
-    const int* g = &c->st->done;
-    TRY(allgather(c, 0));
-    TRY(matvec_a(c, F(c, 0), RhoEpi<T>{L(c, 3), L(c, 2)}, g));
-    TRY(pass(c, CoP<T>{Fs(c, 0), L(c, 3), L(c, 6), L(c, 7), L(c, 4), L(c, 5), Fs(c, 1)}, g));
-    TRY(allgather(c, 1));
-    TRY(matvec_a(c, F(c, 1), CoQ<T>{L(c, 8), L(c, 2)}, g));
-    return pass(c, CoH<T>{L(c, 4), L(c, 5), Fs(c, 1), L(c, 8), L(c, 6), L(c, 7), L(c, X), Fs(c, 0)}, g);
-  }
-
-  // ==================== whole solve loop in one cluster (cluster.cuh) ====================
-  template <class M>
-  static int launch_cluster(ccg_ctx* c, const M& m) {
-    auto kern = cluster_solve<T, M>;
-    C* y = L(c, 1);
-    ClCommon<T> cm{InitR<T>{y, nullptr, nullptr, nullptr, nullptr}, Copy<T>{L(c, X), Fs(c, 2)},
-                   Copy<T>{L(c, X), Fs(c, 2)}, TrueRes<T>{y}, F(c, 2), c->cl_has_x0};
-    switch (c->cl_method) {   // r₀ copies, as init_residual() of each method
-      case M_BICGSTAB: case M_BICG: case M_CGS: cm.ir.d0 = L(c, 2); cm.ir.d1 = L(c, 3); break;
-      case M_CGNE: case M_CGNR: cm.ir.d0 = L(c, 2); break;
-      case M_QMR: cm.ir.d0 = L(c, 2); cm.ir.d1 = L(c, 3); cm.ir.d2 = L(c, 4); break;
-      case M_BICOR: case M_CORS: cm.ir.d0 = Fs(c, 0); cm.ir.d1 = L(c, 2); break;
-      case M_TFQMR: case M_PBICGSTAB: cm.ir.d0 = L(c, 2); cm.ir.d1 = L(c, 3); cm.ir.d2 = Fs(c, 0); break;
-      default: cm.ir.d0 = Fs(c, 0); break;   // COCR
-    }
-    cudaLaunchConfig_t cfg = {};
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    cfg.blockDim = dim3(CL_NT);
-    cfg.dynamicSmemBytes = 0;
-    cfg.stream = c->stream;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    if (c->cluster_size == 0) {
-      cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-      c->cluster_size = 8;
-      for (int cs : {16, 8, 4}) {
-        cfg.gridDim = dim3(cs);
-        at[0].val.clusterDim.x = cs;
-        at[0].val.clusterDim.y = 1;
-        at[0].val.clusterDim.z = 1;
-        int ncl = 0;
-        if (cudaOccupancyMaxActiveClusters(&ncl, kern, &cfg) == cudaSuccess && ncl >= 1) {
-          c->cluster_size = cs;
-          break;
-        }
-        cudaGetLastError();
-      }
-      const char* cs = getenv("CCG_CLUSTER_SIZE");
-      if (cs) c->cluster_size = std::max(1, std::min(CL_MAX, atoi(cs)));
-    } else {
-      cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    }
-    cfg.gridDim = dim3(c->cluster_size);
-    at[0].val.clusterDim.x = c->cluster_size;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    CK(c, cudaLaunchKernelEx(&cfg, kern, m, cm, c->st, reinterpret_cast<const C*>(c->A), c->lda, c->n));
-    c->launches++;
-    return CCG_OK;
-  }
-
-  static int cluster_run(ccg_ctx* c, int m) {
-    switch (m) {
-      case M_BICGSTAB:
-        return launch_cluster(c, ClBicgstab<T>{BsP<T>{L(c, 2), Fs(c, 0), L(c, 4)}, BsV<T>{L(c, 4), L(c, 3)},
-                                               BsS<T>{L(c, 2), L(c, 4), Fs(c, 1)}, BsT<T>{L(c, 5), Fs(c, 1)},
-                                               BsX<T>{L(c, X), L(c, 2), Fs(c, 0), Fs(c, 1), L(c, 5), L(c, 3)},
-                                               F(c, 0), F(c, 1)});
-      case M_CGNE:
-        return launch_cluster(c, ClCgne<T>{CgQ<T>{L(c, 2), L(c, X), Fs(c, 0)}, CgP<T>{Fs(c, 0)}, CgP0<T>{Fs(c, 0)},
-                                           F(c, 0), L(c, 2)});
-      case M_QMR:
-        return launch_cluster(
-            c, ClQmr<T>{QmP<T>{L(c, 5), L(c, 6), Fs(c, 0), L(c, 7)}, QmPt<T>{L(c, 8), L(c, 7)},
-                        QmVW<T>{L(c, 3), L(c, 4), L(c, 8), L(c, 5), L(c, 6)},
-                        QmDV<T>{L(c, 9), L(c, 10), L(c, X), L(c, 2), Fs(c, 0), L(c, 8), L(c, 3), L(c, 4), L(c, 5),
-                                L(c, 6)},
-                        QmV<T>{L(c, 3), L(c, 4), L(c, 5), L(c, 6)}, F(c, 0), L(c, 7)});
-      case M_BICOR:
-        return launch_cluster(c, ClBicor<T>{RhoEpi<T>{L(c, 3), L(c, 2)},
-                                            BcP<T>{Fs(c, 0), L(c, 2), L(c, 3), L(c, 4), L(c, 5), L(c, 6)},
-                                            BcQs<T>{L(c, 7), L(c, 6)},
-                                            BcX<T>{L(c, X), Fs(c, 0), L(c, 2), L(c, 4), L(c, 6), L(c, 7)}, F(c, 0),
-                                            L(c, 5)});
-      case M_CORS:
-        return launch_cluster(
-            c, ClCors<T>{RhoEpi<T>{L(c, 3), L(c, 2)}, CoP<T>{Fs(c, 0), L(c, 3), L(c, 6), L(c, 7), L(c, 4), L(c, 5), Fs(c, 1)},
-                         CoQ<T>{L(c, 8), L(c, 2)},
-                         CoH<T>{L(c, 4), L(c, 5), Fs(c, 1), L(c, 8), L(c, 6), L(c, 7), L(c, X), Fs(c, 0)}, F(c, 0),
-                         F(c, 1)});
-      case M_BICG:
-        return launch_cluster(c, ClBicg<T>{BgP<T>{L(c, 2), L(c, 3), Fs(c, 0), L(c, 4)}, BgQ<T>{L(c, 5), L(c, 4)},
-                                           Store<T>{L(c, 6)},
-                                           BgX<T>{L(c, X), L(c, 2), L(c, 3), Fs(c, 0), L(c, 5), L(c, 6)}, F(c, 0),
-                                           L(c, 4)});
-      case M_CGS:
-        return launch_cluster(c, ClCgs<T>{CsP<T>{L(c, 2), L(c, 5), Fs(c, 0), L(c, 4)}, CsV<T>{L(c, 6), L(c, 3)},
-                                          CsQ<T>{L(c, 4), L(c, 6), L(c, 5), Fs(c, 1), L(c, X)},
-                                          CsR<T>{L(c, 2), L(c, 3)}, F(c, 0), F(c, 1)});
-      case M_COCR:
-        return launch_cluster(c, ClCocr<T>{CrP<T>{Fs(c, 0), L(c, 2), L(c, 3), L(c, 4)},
-                                           CrX<T>{L(c, X), Fs(c, 0), L(c, 3), L(c, 4)}, CrAr<T>{L(c, 2), Fs(c, 0)},
-                                           CrAr0<T>{L(c, 2), Fs(c, 0)}, F(c, 0)});
-      case M_TFQMR:
-        return launch_cluster(c, ClTfqmr<T>{TfE<T>{Fs(c, 0), L(c, 4), L(c, 6), Fs(c, 1), L(c, 3), L(c, 5)},
-                                            TfO<T>{L(c, 7), L(c, X), L(c, 3), L(c, 5), Fs(c, 1), L(c, 2)},
-                                            TfU<T>{L(c, X), L(c, 5), L(c, 3), Fs(c, 1), Fs(c, 0)},
-                                            TfV<T>{L(c, 6), L(c, 7), L(c, 4), L(c, 2)},
-                                            TfV0<T>{L(c, 4), L(c, 6), L(c, 2)}, F(c, 0), F(c, 1)});
-      case M_PBICGSTAB:
-        return launch_cluster(
-            c, ClPbicgstab<T>{PbW0<T>{Fs(c, 1), L(c, 3)}, PbStore<T>{L(c, 9)},
-                              PbP1<T>{L(c, 2), Fs(c, 1), L(c, 9), L(c, 8), L(c, 4), L(c, 5), Fs(c, 0), L(c, 6), L(c, 7)},
-                              PbStore<T>{L(c, 8)},
-                              PbP2<T>{L(c, X), L(c, 2), Fs(c, 1), L(c, 4), L(c, 6), L(c, 7), L(c, 9), L(c, 8), L(c, 5),
-                                      Fs(c, 0), L(c, 3)},
-                              PbT<T>{L(c, 9)}, F(c, 0), F(c, 1)});
-      default:
-        return launch_cluster(c, ClCgnr<T>{CnW<T>{L(c, 3)}, CnX<T>{L(c, X), L(c, 2), Fs(c, 0), L(c, 3)},
-                                           CnZ<T>{L(c, 4)}, CnP<T>{L(c, 4), Fs(c, 0)}, CnZ0<T>{Fs(c, 0)}, F(c, 0),
-                                           L(c, 2)});
-    }
-  }
-
-  // ==================== SURVEY §8(f) NEXT-3 ====================
-  // A·p and Aᴴ·p̃ of one BiCG iteration are independent: dual GEMV when dense
-  template <class EpiA, class EpiH>
-  static int matvec_pair(ccg_ctx* c, int pfull_idx, const C* qloc, EpiA ea, EpiH eh, const int* gate) {
-    if (c->opk == OPK_DENSE && c->cols_ok && c->qmr_dual && !c->rep && !c->jac_active)
-      return matvec_dual(c, F(c, pfull_idx), qloc, ea, eh, gate);
-    TRY(matvec_a(c, F(c, pfull_idx), ea, gate));
-    return matvec_h(c, qloc, true, eh, gate);
-  }
-
-  // ---- BiCG: loc: 0 x, 1 y, 2 r, 3 rt, 4 pt, 5 q, 6 qt ; full: 0 p
-  static int bicg_setup(ccg_ctx* c, bool x0) { return init_residual(c, x0, L(c, 2), L(c, 3), nullptr, nullptr); }
-  static int bicg_iter(ccg_ctx* c) {
-    const int* g = &c->st->done;
-    TRY(pass(c, BgP<T>{L(c, 2), L(c, 3), Fs(c, 0), L(c, 4)}, g));
-    TRY(allgather(c, 0));
-    TRY(matvec_pair(c, 0, L(c, 4), BgQ<T>{L(c, 5), L(c, 4)}, Store<T>{L(c, 6)}, g));
-    return pass(c, BgX<T>{L(c, X), L(c, 2), L(c, 3), Fs(c, 0), L(c, 5), L(c, 6)}, g);
-  }
-
-  // ---- CGS: loc: 0 x, 1 y, 2 r, 3 rt, 4 u, 5 q, 6 v ; full: 0 p, 1 u+q
-  static int cgs_setup(ccg_ctx* c, bool x0) { return init_residual(c, x0, L(c, 2), L(c, 3), nullptr, nullptr); }
-  static int cgs_iter(ccg_ctx* c) {
-    const int* g = &c->st->done;
-    TRY(pass(c, CsP<T>{L(c, 2), L(c, 5), Fs(c, 0), L(c, 4)}, g));
-    TRY(allgather(c, 0));
-    TRY(matvec_a(c, F(c, 0), CsV<T>{L(c, 6), L(c, 3)}, g));
-    TRY(pass(c, CsQ<T>{L(c, 4), L(c, 6), L(c, 5), Fs(c, 1), L(c, X)}, g));
-    TRY(allgather(c, 1));
-    return matvec_a(c, F(c, 1), CsR<T>{L(c, 2), L(c, 3)}, g);
-  }
-
-  // ---- COCR: loc: 0 x, 1 y, 2 Ar, 3 p, 4 Ap ; full: 0 r
-  static int cocr_setup(ccg_ctx* c, bool x0) {
-    TRY(init_residual(c, x0, Fs(c, 0), nullptr, nullptr, nullptr));
-    TRY(allgather(c, 0));
-    return matvec_a(c, F(c, 0), CrAr0<T>{L(c, 2), Fs(c, 0)}, &c->st->done);
-  }
-  static int cocr_iter(ccg_ctx* c) {
-    const int* g = &c->st->done;
-    TRY(pass(c, CrP<T>{Fs(c, 0), L(c, 2), L(c, 3), L(c, 4)}, g));
-    TRY(pass(c, CrX<T>{L(c, X), Fs(c, 0), L(c, 3), L(c, 4)}, g));
-    TRY(allgather(c, 0));
-    return matvec_a(c, F(c, 0), CrAr<T>{L(c, 2), Fs(c, 0)}, g);
-  }
-
-  // ---- CGNR: loc: 0 x, 1 y, 2 r, 3 w, 4 z ; full: 0 p
-  static int cgnr_setup(ccg_ctx* c, bool x0) {
-    TRY(init_residual(c, x0, L(c, 2), nullptr, nullptr, nullptr));
-    return matvec_h(c, L(c, 2), true, CnZ0<T>{Fs(c, 0)}, &c->st->done);
-  }
-  static int cgnr_iter(ccg_ctx* c) {
-    const int* g = &c->st->done;
-    TRY(allgather(c, 0));
-    TRY(matvec_a(c, F(c, 0), CnW<T>{L(c, 3)}, g));
-    TRY(pass(c, CnX<T>{L(c, X), L(c, 2), Fs(c, 0), L(c, 3)}, g));
-    TRY(matvec_h(c, L(c, 2), true, CnZ<T>{L(c, 4)}, g));
-    return pass(c, CnP<T>{L(c, 4), Fs(c, 0)}, g);
-  }
-
-  // ---- TFQMR: loc: 0 x, 1 y, 2 r0*, 3 w, 4 v, 5 d, 6 A·u (even), 7 A·u2 ; full: 0 u, 1 u2
-  static int tfqmr_setup(ccg_ctx* c, bool x0) {
-    TRY(init_residual(c, x0, L(c, 2), L(c, 3), Fs(c, 0), nullptr));
-    TRY(allgather(c, 0));
-    return matvec_a(c, F(c, 0), TfV0<T>{L(c, 4), L(c, 6), L(c, 2)}, &c->st->done);
-  }
-  static int tfqmr_iter(ccg_ctx* c) {
-    const int* g = &c->st->done;
-    const int* g2 = &c->st->gate2;
-    TRY(pass(c, TfE<T>{Fs(c, 0), L(c, 4), L(c, 6), Fs(c, 1), L(c, 3), L(c, 5)}, g));
-    TRY(allgather(c, 1));
-    TRY(matvec_a(c, F(c, 1), TfO<T>{L(c, 7), L(c, X), L(c, 3), L(c, 5), Fs(c, 1), L(c, 2)}, g2));
-    TRY(pass(c, TfU<T>{L(c, X), L(c, 5), L(c, 3), Fs(c, 1), Fs(c, 0)}, g));
-    TRY(allgather(c, 0));
-    return matvec_a(c, F(c, 0), TfV<T>{L(c, 6), L(c, 7), L(c, 4), L(c, 2)}, g);
-  }
-
-  // ---- GMRES(m): loc: 0 x, 1 y, 2 w ; basis V (gm_V) ; full: 0 v_j, 2 x (restart)
-  static C* Vb(ccg_ctx* c) { return reinterpret_cast<C*>(c->gm_V); }
-  template <int MODE>
-  static int gm_pass_launch(ccg_ctx* c, C* w, const double2* coef, double2* dst, const int* gate) {
-    const bool fuse = c->world == 1 || c->rep;
-    auto kern = c->gm_fast ? gm_pass<T, MODE, true> : gm_pass<T, MODE, false>;
-    launch_k(c, kern, c->gm_grid, GM_NT, 0, c->stream, Vb(c), c->nloc, w, coef, fuse ? dst : c->gm_rank, c->nloc,
-             c->gm_dev, c->gm_part, c->gm_ticket, fuse ? 1 : 0, gate);
-    c->launches++;
-    CK(c, cudaGetLastError());
-    if (!fuse) {
-      NK(c, c->comm->allgather(c->gm_rank, c->gm_all, (size_t)(GM_MAX + 1) * 2, CT_F64, c->stream));
-      launch_k(c, gm_ranksum, 1, 128, 0, c->stream, c->gm_all, c->world, MODE == 2 ? 1 : GM_MAX + 1, GM_MAX + 1, dst, gate);
-      c->launches++;
-    }
-    return CCG_OK;
-  }
-  static int gmres_setup(ccg_ctx* c, bool x0) {
-    TRY(init_residual(c, x0, Vb(c), nullptr, nullptr, nullptr));
-    launch_k(c, gm_normalize<T>, c->gm_vgrid, NT, 0, c->stream, Vb(c), c->nloc, Vb(c), Fs(c, 0), c->nloc, c->gm_dev, 1,
-                                                         &c->st->done);
-    c->launches++;
-    CK(c, cudaGetLastError());
-    return CCG_OK;
-  }
-  static int gmres_iter(ccg_ctx* c) {
-    const int* g = &c->st->done;
-    GmDev* gm = c->gm_dev;
-    C* w = L(c, 2);
-    TRY(allgather(c, 0));
-    TRY(matvec_a(c, F(c, 0), Store<T>{w}, g));
-    TRY(gm_pass_launch<0>(c, w, nullptr, gm->hcol, g));
-    TRY(gm_pass_launch<1>(c, w, gm->hcol, gm->h2, g));
-    TRY(gm_pass_launch<2>(c, w, gm->h2, &gm->ww2, g));
-    launch_k(c, gm_step, 1, 1, 0, c->stream, c->st, gm, g);
-    launch_k(c, gm_normalize<T>, c->gm_vgrid, NT, 0, c->stream, Vb(c), c->nloc, w, Fs(c, 0), c->nloc, gm, 0, &gm->endflag);
-    launch_k(c, gm_trisolve, 1, 1, 0, c->stream, c->st, gm, &gm->noend);
-    launch_k(c, gm_xupdate<T>, c->gm_vgrid, NT, 0, c->stream, L(c, X), Vb(c), c->nloc, c->nloc, gm, &gm->noxupd);
-    c->launches += 4;
-    CK(c, cudaGetLastError());
-    TRY(pass(c, Copy<T>{L(c, X), Fs(c, 2)}, &gm->norestart));
-    TRY(allgather(c, 2));
-    TRY(matvec_a(c, F(c, 2), GmR<T>{L(c, 1), Vb(c)}, &gm->norestart));
-    launch_k(c, gm_normalize<T>, c->gm_vgrid, NT, 0, c->stream, Vb(c), c->nloc, Vb(c), Fs(c, 0), c->nloc, gm, 1,
-                                                         &gm->norestart);
-    launch_k(c, gm_reset, 1, 1, 0, c->stream, gm);
-    c->launches += 2;
-    CK(c, cudaGetLastError());
-    return CCG_OK;
-  }
-
-  // ---- BiCGstab(ℓ): loc: 0 x, 1 y, 3 r̃ ; bl_buf: r̂₀..r̂_ℓ then û₀..û_ℓ (full length each)
-  static C* BLR(ccg_ctx* c, int a) { return reinterpret_cast<C*>(c->bl_buf) + (size_t)a * c->n; }
-  static C* BLU(ccg_ctx* c, int a) { return BLR(c, c->bl_l + 1 + a); }
-  static C* BRs(ccg_ctx* c, int a) { return BLR(c, a) + c->row0; }
-  static C* BUs(ccg_ctx* c, int a) { return BLU(c, a) + c->row0; }
-  static int allgather_buf(ccg_ctx* c, C* buf) {
-    if (c->world == 1 || c->rep) return CCG_OK;
-    if (c->opk == OPK_CSR || c->opk == OPK_STENCIL) return halo_exchange(c, buf);
-    NK(c, c->comm->allgather_inplace(buf, (size_t)c->nloc * 2, ndt(), c->stream));
-    return CCG_OK;
-  }
-  static int bicgstabl_setup(ccg_ctx* c, bool x0) {
-    TRY(init_residual(c, x0, BRs(c, 0), L(c, 3), nullptr, nullptr));
-    CK(c, cudaMemsetAsync(BUs(c, 0), 0, (size_t)c->nloc * sizeof(C), c->stream));
-    return CCG_OK;
-  }
-  template <int LL>
-  static int bicgstabl_mr(ccg_ctx* c, const int* g) {
-    BlGram<T, LL> G{};
-    BlM<T, LL> M{};
-    for (int a = 0; a <= LL; ++a) {
-      G.r[a] = BRs(c, a);
-      M.r[a] = BRs(c, a);
-      M.u[a] = BUs(c, a);
-    }
-    M.x = L(c, X);
-    M.rt = L(c, 3);
-    TRY(pass(c, G, g));
-    return pass(c, M, g);
-  }
-  static int bicgstabl_iter(ccg_ctx* c) {
-    const int* g = &c->st->done;
-    const int ell = c->bl_l;
-    for (int j = 0; j < ell; ++j) {
-      BlP<T> P{};
-      for (int a = 0; a <= j; ++a) { P.u[a] = BUs(c, a); P.r[a] = BRs(c, a); }
-      P.J = j;
-      TRY(pass(c, P, g));
-      TRY(allgather_buf(c, BLU(c, j)));
-      TRY(matvec_a(c, BLU(c, j), BlU<T>{BUs(c, j + 1), L(c, 3)}, g));
-      BlX<T> Xp{};
-      for (int a = 0; a <= j; ++a) Xp.r[a] = BRs(c, a);
-      for (int a = 0; a <= j + 1; ++a) Xp.u[a] = BUs(c, a);
-      Xp.x = L(c, X);
-      Xp.J = j;
-      TRY(pass(c, Xp, g));
-      TRY(allgather_buf(c, BLR(c, j)));
-      if (j < ell - 1)
-        TRY(matvec_a(c, BLR(c, j), BlR<T>{BRs(c, j + 1), L(c, 3)}, g));
-      else
-        TRY(matvec_a(c, BLR(c, j), BlRL<T>{BRs(c, j + 1)}, g));
-    }
-    switch (ell) {
-      case 1: return bicgstabl_mr<1>(c, g);
-      case 2: return bicgstabl_mr<2>(c, g);
-      case 3: return bicgstabl_mr<3>(c, g);
-      default: return bicgstabl_mr<4>(c, g);
-    }
-  }
-
-  // ---- p-BiCGSTAB: loc: 0 x, 1 y, 2 r, 3 r̃, 4 p, 5 s, 6 q, 7 y, 8 v, 9 t ; full: 0 z (r₀ at setup), 1 w
-  static int pbicgstab_setup(ccg_ctx* c, bool x0) {
-    const int* g = &c->st->done;
-    TRY(init_residual(c, x0, L(c, 2), L(c, 3), Fs(c, 0), nullptr));
-    TRY(allgather(c, 0));
-    TRY(matvec_a(c, F(c, 0), PbW0<T>{Fs(c, 1), L(c, 3)}, g));
-    TRY(allgather(c, 1));
-    return matvec_a(c, F(c, 1), PbStore<T>{L(c, 9)}, g);
-  }
-  static int pbicgstab_iter(ccg_ctx* c) {
-    const int* g = &c->st->done;
-    const int* g2 = &c->st->gate2;
-    TRY(pass(c, PbP1<T>{L(c, 2), Fs(c, 1), L(c, 9), L(c, 8), L(c, 4), L(c, 5), Fs(c, 0), L(c, 6), L(c, 7)}, g));
-    TRY(allgather(c, 0));
-    TRY(matvec_a(c, F(c, 0), PbStore<T>{L(c, 8)}, g2));
-    TRY(pass(c, PbP2<T>{L(c, X), L(c, 2), Fs(c, 1), L(c, 4), L(c, 6), L(c, 7), L(c, 9), L(c, 8), L(c, 5), Fs(c, 0),
-                        L(c, 3)},
-             g));
-    TRY(allgather(c, 1));
-    return matvec_a(c, F(c, 1), PbT<T>{L(c, 9)}, g);
-  }
-
-  static int setup(ccg_ctx* c, int m, bool x0) {
-    switch (m) {
-      case M_BICGSTAB: return bicgstab_setup(c, x0);
-      case M_CGNE: return cgne_setup(c, x0);
-      case M_QMR: return qmr_setup(c, x0);
-      case M_BICOR: return bicor_setup(c, x0);
-      case M_CORS: return cors_setup(c, x0);
-      case M_BICG: return bicg_setup(c, x0);
-      case M_CGS: return cgs_setup(c, x0);
-      case M_COCR: return cocr_setup(c, x0);
-      case M_TFQMR: return tfqmr_setup(c, x0);
-      case M_GMRES: return gmres_setup(c, x0);
-      case M_BICGSTABL: return bicgstabl_setup(c, x0);
-      case M_PBICGSTAB: return pbicgstab_setup(c, x0);
-      default: return cgnr_setup(c, x0);
-    }
-  }
-  static int iter(ccg_ctx* c, int m) {
-    switch (m) {
-      case M_BICGSTAB: return bicgstab_iter(c);
-      case M_CGNE: return cgne_iter(c);
-      case M_QMR: return qmr_iter(c);
-      case M_BICOR: return bicor_iter(c);
-      case M_CORS: return cors_iter(c);
-      case M_BICG: return bicg_iter(c);
-      case M_CGS: return cgs_iter(c);
-      case M_COCR: return cocr_iter(c);
-      case M_TFQMR: return tfqmr_iter(c);
-      case M_GMRES: return gmres_iter(c);
-      case M_BICGSTABL: return bicgstabl_iter(c);
-      case M_PBICGSTAB: return pbicgstab_iter(c);
-      default: return cgnr_iter(c);
-    }
-  }
-
-  // true residual ‖y − A x‖²
-  static int true_residual(ccg_ctx* c) {
-    const int* g = c->zero_gate;
-    TRY(pass(c, Copy<T>{L(c, X), Fs(c, 2)}, g));
-    TRY(allgather(c, 2));
-    return matvec_a(c, F(c, 2), TrueRes<T>{L(c, 1)}, g);
-  }
-
-  // right Jacobi around a solve: u₀ = D·x₀ before, x = D⁻¹·u after
-  static int jac_in(ccg_ctx* c) {
-    return pass_count(c, JacScale<T>{L(c, X), reinterpret_cast<const C*>(c->jac_d) + c->row0, L(c, X)}, c->nloc,
-                      c->zero_gate);
-  }
-  static int jac_out(ccg_ctx* c) {
-    return pass_count(c, JacScale<T>{L(c, X), reinterpret_cast<const C*>(c->jac_dinv) + c->row0, L(c, X)}, c->nloc,
-                      c->zero_gate);
-  }
-
-  // ccg_apply
-  static int apply(ccg_ctx* c, int op, const C* xin, C* yout) {
-    const int* g = c->zero_gate;
-    if (op == CCG_OP_A || (op == CCG_OP_AT && (c->opk == OPK_CSR || c->opk == OPK_STENCIL))) {
-      CK(c, cudaMemcpyAsync(Fs(c, 2), xin, c->nloc * sizeof(C), cudaMemcpyDeviceToDevice, c->stream));
-      TRY(allgather(c, 2));
-      return matvec_a(c, F(c, 2), Store<T>{yout}, g);
-    }
-    CK(c, cudaMemcpyAsync(L(c, 2), xin, c->nloc * sizeof(C), cudaMemcpyDeviceToDevice, c->stream));
-    return matvec_h(c, L(c, 2), op == CCG_OP_AH, Store<T>{yout}, g);
-  }
-};
 
 // ===========================================================================
 // launch-parameter selection
@@ -1405,9 +253,12 @@ static int run_iterations(ccg_ctx* c, int m, int maxit) {
   if (!c->gexec[m]) {
     cudaGraph_t graph;
     int64_t l0 = c->launches;
+    const int64_t calls0 = c->comm ? c->comm->calls : 0;
     CK(c, cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
     int rc = E::iter(c, m);
     cudaError_t e2 = cudaStreamEndCapture(c->stream, &graph);
+    c->coll_per_iter[m] = (c->comm ? c->comm->calls : 0) - calls0;
+    c->stat_capture_calls += c->coll_per_iter[m];
     if (rc) return rc;
     if (e2 != cudaSuccess) FAIL(c, CCG_E_CUDA, std::string("graph capture: ") + cudaGetErrorString(e2));
     c->graph_launches_per_iter[m] = c->launches - l0;
@@ -1429,6 +280,8 @@ static int run_iterations(ccg_ctx* c, int m, int maxit) {
     for (int i = 0; i < todo; ++i) {
       CK(c, cudaGraphLaunch(c->gexec[m], c->stream));
       c->launches += c->graph_launches_per_iter[m];
+      c->stat_replays++;
+      c->stat_graph_coll += c->coll_per_iter[m];
     }
     k += todo;
     CK(c, cudaMemcpyAsync(&c->done_ring[slot], &c->st->done, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
@@ -1447,7 +300,7 @@ static int run_iterations(ccg_ctx* c, int m, int maxit) {
       // round trip (~25 µs), and every iteration of it is wasted (gated) work
       // once the solve has converged; unpipelined: ~200 µs per chunk.
       const double target = c->pipe ? 25.0 : 200.0;
-      chunk = c->world > 1 ? std::min(32, 2 * chunk)
+      chunk = c->dist ? std::min(32, 2 * chunk)
                            : per > 0 ? (int)std::max(1.0, std::min(32.0, std::ceil(target / per))) : 32;
     }
     pending = slot;
@@ -1507,9 +360,10 @@ static int toeplitz_setup(ccg_ctx* c, const std::vector<std::complex<double>>& K
   CK(c, cudaMalloc(&c->fftW, N * sizeof(C)));
   CK(c, cudaMalloc(&c->fftK, N * sizeof(C)));
   CK(c, cudaMalloc(&c->fftTw, half * sizeof(C)));
-  CK(c, cudaMemcpy(c->fftK, kh.data(), N * sizeof(C), cudaMemcpyHostToDevice));
-  CK(c, cudaMemcpy(c->fftTw, tw.data(), half * sizeof(C), cudaMemcpyHostToDevice));
-  CK(c, cudaMemset(c->fftW, 0, N * sizeof(C)));
+  TRY(h2d(c, c->fftK, kh.data(), N * sizeof(C)));
+  TRY(h2d(c, c->fftTw, tw.data(), half * sizeof(C)));
+  CK(c, cudaMemsetAsync(c->fftW, 0, N * sizeof(C), c->stream));
+  CK(c, cudaStreamSynchronize(c->stream));
   return CCG_OK;
 }
 
@@ -1551,7 +405,8 @@ static int create_impl(ccg_handle* h, ccg_dtype dt, int64_t n, int world, int ra
   c->rank = rank;
   c->mnloc = n / world;
   c->mrow0 = (int64_t)rank * c->mnloc;
-  c->rep = world > 1 && (options & CCG_OPT_REPLICATED);
+  c->dist = world > 1 || (options & CCG_OPT_FORCE_COMM);
+  c->rep = c->dist && (options & CCG_OPT_REPLICATED);
   c->nloc = c->rep ? n : c->mnloc;      // vectors: whole (replicated) or this rank's slice
   c->row0 = c->rep ? 0 : c->mrow0;
   c->device = device;
@@ -1608,7 +463,7 @@ static int create_impl(ccg_handle* h, ccg_dtype dt, int64_t n, int world, int ra
     CKC(cudaMalloc(&c->rep_tmp, (size_t)n * c->esz));
     CKC(cudaMalloc(&c->rep_parts, (size_t)n * world * c->esz));
   }
-  if (world > 1) {
+  if (c->dist) {
     CKC(cudaMalloc(&c->wfull, (size_t)n * c->esz));
     if (lg) {
       {
@@ -1619,6 +474,11 @@ static int create_impl(ccg_handle* h, ccg_dtype dt, int64_t n, int world, int ra
     } else {
       NcclComm* nc = new NcclComm();
       c->comm = nc;
+      uint8_t own_id[128];
+      if (!nccl_id) {   // world == 1 with CCG_OPT_FORCE_COMM: a one-rank communicator
+        if (ccg_get_unique_id(own_id) != CCG_OK) { c->err = g_create_err; return bail(CCG_E_NCCL); }
+        nccl_id = own_id;
+      }
       int rc = nc->init(world, rank, nccl_id);
       if (rc) { c->err = nc->err; return bail(CCG_E_NCCL); }
     }
@@ -1685,7 +545,7 @@ int ccg_set_matvec_dense(ccg_handle c, const void* A_local, int64_t row0, int64_
     const char* ce = getenv("CCG_CLUSTER");
     const char* cb = getenv("CCG_CLUSTER_MAXBYTES");
     const double maxb = cb ? atof(cb) : 4.0 * 1024 * 1024;
-    c->cluster_ok = c->world == 1 && !(ce && !strcmp(ce, "0")) &&
+    c->cluster_ok = !c->dist && !(ce && !strcmp(ce, "0")) &&
                     (double)c->n * (double)c->n * (double)c->esz <= maxb;
   }
   invalidate_graphs(c);
@@ -1701,36 +561,53 @@ int ccg_set_matvec_csr(ccg_handle c, const int32_t* rowptr, const int32_t* colin
   if (!is_device_ptr(rowptr) || !is_device_ptr(colind) || !is_device_ptr(vals))
     FAIL(c, CCG_E_ARG, "CSR arrays must be device pointers");
   CK(c, cudaSetDevice(c->device));
-  // validate structure and compute the halo width on the host (one-time copy)
+  // validate structure and compute the halo width on the host (one-time copy).
+  // A local failure is recorded, not returned: with several ranks every rank
+  // first enters the halo-width allgather, so an input error on one rank is an
+  // error on all of them instead of a hang in the collective.
+  int lcode = CCG_OK;
+  std::string lmsg;
+  auto lfail = [&](int code, const char* m) {
+    if (lcode == CCG_OK) { lcode = code; lmsg = m; }
+  };
   std::vector<int32_t> rp(nloc + 1), ci(nnz_local);
+  int64_t halo = 0;
   CK(c, cudaMemcpy(rp.data(), rowptr, (nloc + 1) * sizeof(int32_t), cudaMemcpyDeviceToHost));
   if (nnz_local) CK(c, cudaMemcpy(ci.data(), colind, nnz_local * sizeof(int32_t), cudaMemcpyDeviceToHost));
-  if (rp[0] != 0 || rp[nloc] != nnz_local) FAIL(c, CCG_E_DIM, "rowptr[0] != 0 or rowptr[nloc] != nnz");
-  int64_t halo = 0;
-  for (int64_t i = 0; i < nloc; ++i) {
-    if (rp[i + 1] < rp[i]) FAIL(c, CCG_E_ARG, "rowptr not nondecreasing");
+  if (rp[0] != 0 || rp[nloc] != nnz_local) lfail(CCG_E_DIM, "rowptr[0] != 0 or rowptr[nloc] != nnz");
+  for (int64_t i = 0; i < nloc && lcode == CCG_OK; ++i) {
+    if (rp[i + 1] < rp[i]) { lfail(CCG_E_ARG, "rowptr not nondecreasing"); break; }
     for (int32_t k = rp[i]; k < rp[i + 1]; ++k) {
       const int64_t j = ci[k];
-      if (j < 0 || j >= c->n) FAIL(c, CCG_E_ARG, "column index out of range");
+      if (j < 0 || j >= c->n) { lfail(CCG_E_ARG, "column index out of range"); break; }
       if (j < row0) halo = std::max<int64_t>(halo, row0 - j);
       if (j >= row0 + nloc) halo = std::max<int64_t>(halo, j - (row0 + nloc) + 1);
     }
   }
-  if (c->world > 1 && !c->rep && halo > nloc)
-    FAIL(c, CCG_E_ARG, "CSR columns reach beyond the neighbour ranks (halo > nloc)");
-  if (c->world > 1 && !c->rep) {
-    // all ranks use the same (maximum) halo width so that sends match receives
+  if (lcode == CCG_OK && c->dist && !c->rep && halo > nloc)
+    lfail(CCG_E_ARG, "CSR columns reach beyond the neighbour ranks (halo > nloc)");
+  if (c->dist && !c->rep) {
+    // all ranks use the same (maximum) halo width so that sends match receives,
+    // and share their validation status
+    const int64_t mine[2] = {halo, (int64_t)lcode};
     int64_t* dh = nullptr;
-    CK(c, cudaMalloc(&dh, sizeof(int64_t) * c->world));
-    CK(c, cudaMemcpy(dh + c->rank, &halo, sizeof(int64_t), cudaMemcpyHostToDevice));
-    int r = c->comm->allgather(dh + c->rank, dh, 1, CT_I64, c->stream);
+    CK(c, cudaMalloc(&dh, sizeof(int64_t) * 2 * c->world));
+    CK(c, cudaMemcpyAsync(dh + 2 * c->rank, mine, sizeof(mine), cudaMemcpyHostToDevice, c->stream));
+    int r = c->comm->allgather(dh + 2 * c->rank, dh, 2, CT_I64, c->stream);
     if (r) { cudaFree(dh); FAIL(c, r, c->comm->err); }
-    std::vector<int64_t> hs(c->world);
+    std::vector<int64_t> hs(2 * c->world);
+    CK(c, cudaMemcpyAsync(hs.data(), dh, sizeof(int64_t) * 2 * c->world, cudaMemcpyDeviceToHost, c->stream));
     CK(c, cudaStreamSynchronize(c->stream));
-    CK(c, cudaMemcpy(hs.data(), dh, sizeof(int64_t) * c->world, cudaMemcpyDeviceToHost));
     cudaFree(dh);
-    for (auto v : hs) halo = std::max(halo, v);
+    if (lcode != CCG_OK) FAIL(c, lcode, lmsg);
+    for (int p = 0; p < c->world; ++p) {
+      if (hs[2 * p + 1] != CCG_OK)
+        FAIL(c, (int)hs[2 * p + 1], "ccg_set_matvec_csr failed on rank " + std::to_string(p));
+      halo = std::max(halo, hs[2 * p]);
+    }
     if (halo > nloc) FAIL(c, CCG_E_ARG, "halo > nloc on some rank");
+  } else if (lcode != CCG_OK) {
+    FAIL(c, lcode, lmsg);
   }
   // CSR-stream row blocks: ≤ 256 rows and ≤ 2048 nonzeros each (long rows alone)
   free_csr_copies(c);
@@ -1754,8 +631,8 @@ int ccg_set_matvec_csr(ccg_handle c, const int32_t* rowptr, const int32_t* colin
       CK(c, cudaMalloc(&c->sell_width, nsl * sizeof(int32_t)));
       CK(c, cudaMalloc(&c->sell_col, std::max<int64_t>(tot, 1) * sizeof(int32_t)));
       CK(c, cudaMalloc(&c->sell_val, std::max<int64_t>(tot, 1) * c->esz));
-      CK(c, cudaMemcpy(c->sell_off, off.data(), nsl * sizeof(int64_t), cudaMemcpyHostToDevice));
-      CK(c, cudaMemcpy(c->sell_width, wid.data(), nsl * sizeof(int32_t), cudaMemcpyHostToDevice));
+      TRY(h2d(c, c->sell_off, off.data(), nsl * sizeof(int64_t)));
+      TRY(h2d(c, c->sell_width, wid.data(), nsl * sizeof(int32_t)));
       const int64_t thr = nsl * 32;
       const int g = (int)((thr + 255) / 256);
       if (c->esz == 8)
@@ -1780,7 +657,7 @@ int ccg_set_matvec_csr(ccg_handle c, const int32_t* rowptr, const int32_t* colin
     }
     c->csr_nblocks = (int)bl.size() - 1;
     CK(c, cudaMalloc(&c->csr_blocks, bl.size() * sizeof(int32_t)));
-    CK(c, cudaMemcpy(c->csr_blocks, bl.data(), bl.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+    TRY(h2d(c, c->csr_blocks, bl.data(), bl.size() * sizeof(int32_t)));
   }
   c->opk = OPK_CSR;
   c->rowptr = rowptr;
@@ -1928,12 +805,14 @@ int ccg_set_jacobi(ccg_handle c, const void* diag_local, uint32_t flags) {
   if (is_device_ptr(diag_local)) CK(c, cudaMemcpy(hd.data(), diag_local, hd.size(), cudaMemcpyDeviceToHost));
   else memcpy(hd.data(), diag_local, hd.size());
   std::vector<unsigned char> hinv(hd.size());
+  // a bad entry is recorded, not returned, so that with several ranks every
+  // rank still enters the allgathers below (no hang); the status is agreed
+  int lcode = CCG_OK;
   for (int64_t i = 0; i < c->mnloc; ++i) {
     double re, im;
     if (es == 8) { re = reinterpret_cast<float*>(hd.data())[2 * i]; im = reinterpret_cast<float*>(hd.data())[2 * i + 1]; }
     else { re = reinterpret_cast<double*>(hd.data())[2 * i]; im = reinterpret_cast<double*>(hd.data())[2 * i + 1]; }
-    if (!(std::isfinite(re) && std::isfinite(im)) || (re == 0.0 && im == 0.0))
-      FAIL(c, CCG_E_ARG, "Jacobi: diagonal entries must be finite and nonzero");
+    if (!(std::isfinite(re) && std::isfinite(im)) || (re == 0.0 && im == 0.0)) { lcode = CCG_E_ARG; break; }
     const std::complex<double> inv = 1.0 / std::complex<double>(re, im);
     if (es == 8) {
       reinterpret_cast<float*>(hinv.data())[2 * i] = (float)inv.real();
@@ -1943,14 +822,29 @@ int ccg_set_jacobi(ccg_handle c, const void* diag_local, uint32_t flags) {
       reinterpret_cast<double*>(hinv.data())[2 * i + 1] = inv.imag();
     }
   }
+  if (c->dist) {
+    int64_t* dcode = nullptr;
+    const int64_t mine = lcode;
+    std::vector<int64_t> all(c->world);
+    CK(c, cudaMalloc(&dcode, sizeof(int64_t) * c->world));
+    CK(c, cudaMemcpyAsync(dcode + c->rank, &mine, sizeof(int64_t), cudaMemcpyHostToDevice, c->stream));
+    int r = c->comm->allgather(dcode + c->rank, dcode, 1, CT_I64, c->stream);
+    if (!r) {
+      cudaMemcpyAsync(all.data(), dcode, sizeof(int64_t) * c->world, cudaMemcpyDeviceToHost, c->stream);
+      cudaStreamSynchronize(c->stream);
+    }
+    cudaFree(dcode);
+    if (r) FAIL(c, r, c->comm->err);
+    for (auto v : all) if (v != CCG_OK) lcode = (int)v;
+  }
+  if (lcode != CCG_OK) FAIL(c, lcode, "Jacobi: diagonal entries must be finite and nonzero (on every rank)");
   const size_t full = (size_t)c->n * es;
   if (!c->jac_d) CK(c, cudaMalloc(&c->jac_d, full));
   if (!c->jac_dinv) CK(c, cudaMalloc(&c->jac_dinv, full));
   if (!c->jac_tmp) CK(c, cudaMalloc(&c->jac_tmp, full));
-  CK(c, cudaMemcpy(static_cast<char*>(c->jac_d) + (size_t)c->mrow0 * es, hd.data(), hd.size(), cudaMemcpyHostToDevice));
-  CK(c, cudaMemcpy(static_cast<char*>(c->jac_dinv) + (size_t)c->mrow0 * es, hinv.data(), hinv.size(),
-                   cudaMemcpyHostToDevice));
-  if (c->world > 1) {
+  TRY(h2d(c, static_cast<char*>(c->jac_d) + (size_t)c->mrow0 * es, hd.data(), hd.size()));
+  TRY(h2d(c, static_cast<char*>(c->jac_dinv) + (size_t)c->mrow0 * es, hinv.data(), hinv.size()));
+  if (c->dist) {
     const CommType t = es == 8 ? CT_F32 : CT_F64;
     int r = c->comm->allgather_inplace(c->jac_d, (size_t)c->mnloc * 2, t, c->stream);
     if (!r) r = c->comm->allgather_inplace(c->jac_dinv, (size_t)c->mnloc * 2, t, c->stream);
@@ -2091,7 +985,7 @@ int ccg_apply(ccg_handle c, ccg_op op, const void* x_local, void* y_local) {
   if (!x_local || !y_local) FAIL(c, CCG_E_ARG, "NULL vector");
   if (op != CCG_OP_A && op != CCG_OP_AH && op != CCG_OP_AT) FAIL(c, CCG_E_ARG, "bad op");
   if (c->opk == OPK_NONE) FAIL(c, CCG_E_STATE, "no operator set (call ccg_set_matvec_*)");
-  if (c->opk == OPK_CSR && op != CCG_OP_A && (!(c->flags & CCG_FLAG_SYMMETRIC) || (c->world > 1 && !c->rep)))
+  if (c->opk == OPK_CSR && op != CCG_OP_A && (!(c->flags & CCG_FLAG_SYMMETRIC) || (c->dist && !c->rep)))
     FAIL(c, CCG_E_CAPABILITY, "CSR Aᴴ/Aᵀ needs CCG_FLAG_SYMMETRIC and world == 1 (or replicated vectors)");
   if (c->opk == OPK_CALLBACK && !(c->cb_caps & (op == CCG_OP_A ? CCG_CB_A : op == CCG_OP_AH ? CCG_CB_AH : CCG_CB_AT)))
     FAIL(c, CCG_E_CAPABILITY, "the user callback does not provide this product");
@@ -2120,7 +1014,7 @@ int ccg_solve(ccg_handle c, ccg_method method, const void* x0_local, const void*
   if ((int)method < 0 || (int)method >= M_COUNT) FAIL(c, CCG_E_ARG, "bad method");
   if (!(tol >= 0.0) || maxit < 1) FAIL(c, CCG_E_ARG, "tol must be >= 0 and maxit >= 1");
   if (c->opk == OPK_NONE) FAIL(c, CCG_E_STATE, "no operator set (call ccg_set_matvec_*)");
-  if (needs_ah(method) && c->opk == OPK_CSR && (!(c->flags & CCG_FLAG_SYMMETRIC) || (c->world > 1 && !c->rep)))
+  if (needs_ah(method) && c->opk == OPK_CSR && (!(c->flags & CCG_FLAG_SYMMETRIC) || (c->dist && !c->rep)))
     FAIL(c, CCG_E_CAPABILITY, "method needs Aᴴ; CSR provides it only with CCG_FLAG_SYMMETRIC and world == 1");
   if (c->opk == OPK_CALLBACK && (!(c->cb_caps & CCG_CB_A) || (needs_ah(method) && !(c->cb_caps & CCG_CB_AH))))
     FAIL(c, CCG_E_CAPABILITY, "the user callback does not provide the products this method needs");
@@ -2128,6 +1022,8 @@ int ccg_solve(ccg_handle c, ccg_method method, const void* x0_local, const void*
   c->launches = 0;
   c->ms_a = c->ms_ah = 0;
   c->n_a = c->n_ah = 0;
+  c->stat_replays = c->stat_graph_coll = c->stat_capture_calls = 0;
+  const int64_t calls_start = c->comm ? c->comm->calls : 0;
   const size_t bytes = (size_t)c->nloc * c->esz;   // library vectors (whole when replicated)
   // history buffer
   if (maxit + 1 > c->hist_cap) {
@@ -2171,15 +1067,17 @@ int ccg_solve(ccg_handle c, ccg_method method, const void* x0_local, const void*
       if (rc) { c->jac_active = false; return rc; }
     }
   }
-  if (c->opk == OPK_DENSE && c->cluster_ok && c->world == 1 && !c->timing && method != CCG_GMRES &&
+  if (c->opk == OPK_DENSE && c->cluster_ok && !c->dist && !c->timing && method != CCG_GMRES &&
       method != CCG_BICGSTABL && !c->jac_dinv) {
     // small dense system: setup, every iteration and the true residual in ONE
     // cluster launch (cluster.cuh); maxit and the stopping rule live in the State
     c->cl_method = method;
     c->cl_has_x0 = has_x0 ? 1 : 0;
     rc = c->dtype == CCG_C64 ? Engine<float>::cluster_run(c, method) : Engine<double>::cluster_run(c, method);
-    if (rc) return rc;
-  } else {
+    if (rc && rc != CCG_FALLBACK) return rc;
+  }
+  if (!(c->opk == OPK_DENSE && c->cluster_ok && !c->dist && !c->timing && method != CCG_GMRES &&
+        method != CCG_BICGSTABL && !c->jac_dinv)) {
     rc = c->dtype == CCG_C64 ? Engine<float>::setup(c, method, has_x0) : Engine<double>::setup(c, method, has_x0);
     if (rc) return rc;
     rc = c->dtype == CCG_C64 ? run_iterations<float>(c, method, maxit) : run_iterations<double>(c, method, maxit);
@@ -2217,6 +1115,7 @@ int ccg_solve(ccg_handle c, ccg_method method, const void* x0_local, const void*
     c->n_ah = std::min(c->n_ah, res->matvecs_ah);
   }
   c->hist_len = std::min(c->hist_cap, res->iterations + 1);
+  c->stat_eager_coll = (c->comm ? c->comm->calls : 0) - calls_start - c->stat_capture_calls;
   res->wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count();
   return CCG_OK;
 }
@@ -2246,6 +1145,20 @@ int ccg_get_timing(ccg_handle c, double* ms_a, int32_t* n_a, double* ms_ah, int3
 }
 
 int64_t ccg_last_launch_count(ccg_handle c) { return c ? c->launches : -1; }
+
+int ccg_get_stat(ccg_handle c, int32_t key, int64_t* value) {
+  if (!c || !value) return CCG_E_ARG;
+  switch (key) {
+    case CCG_STAT_COMM_KIND: *value = c->comm ? c->comm->kind : 0; break;
+    case CCG_STAT_GRAPH_REPLAYS: *value = c->stat_replays; break;
+    case CCG_STAT_GRAPH_COLLECTIVES: *value = c->stat_graph_coll; break;
+    case CCG_STAT_EAGER_COLLECTIVES: *value = c->stat_eager_coll; break;
+    case CCG_STAT_WORLD: *value = c->world; break;
+    case CCG_STAT_REPLICATED: *value = c->rep ? 1 : 0; break;
+    default: FAIL(c, CCG_E_ARG, "unknown stat key");
+  }
+  return CCG_OK;
+}
 
 void* ccg_get_stream(ccg_handle c) { return c ? (void*)c->stream : nullptr; }
 

@@ -80,6 +80,8 @@ struct Comm {
   int world = 1, rank = 0;
   std::string err;
   bool graph_safe = true;  // may be captured in a CUDA graph
+  int kind = 0;            // 1 = NCCL, 2 = loopback (ccg_get_stat CCG_STAT_COMM_KIND)
+  int64_t calls = 0;       // collective calls issued (host side; a captured call counts once)
   virtual ~Comm() {}
   // buf holds world chunks of `count` elements; chunk `rank` is filled
   virtual int allgather_inplace(void* buf, size_t count, CommType t, cudaStream_t s) = 0;
@@ -103,6 +105,7 @@ struct NcclComm : Comm {
   }
   int init(int w, int r, const uint8_t* id) {
     world = w; rank = r;
+    kind = 1;
     if (!nccl_load()) { err = g_nccl.err; return -6; }
     ncclUniqueId u;
     memcpy(u.internal, id, 128);
@@ -113,19 +116,23 @@ struct NcclComm : Comm {
     if (comm && g_nccl.loaded) g_nccl.CommDestroy(comm);
   }
   int allgather_inplace(void* buf, size_t count, CommType t, cudaStream_t s) override {
+    ++calls;
     char* b = static_cast<char*>(buf);
     ncclResult_t e = g_nccl.AllGather(b + rank * count * ct_size(t), b, count, nt(t), comm, s);
     return e == ncclSuccess ? 0 : fail(e, "ncclAllGather");
   }
   int allgather(const void* send, void* recv, size_t count, CommType t, cudaStream_t s) override {
+    ++calls;
     ncclResult_t e = g_nccl.AllGather(send, recv, count, nt(t), comm, s);
     return e == ncclSuccess ? 0 : fail(e, "ncclAllGather");
   }
   int reduce_scatter(const void* send, void* recv, size_t count, CommType t, cudaStream_t s) override {
+    ++calls;
     ncclResult_t e = g_nccl.ReduceScatter(send, recv, count, nt(t), ncclSum, comm, s);
     return e == ncclSuccess ? 0 : fail(e, "ncclReduceScatter");
   }
   int halo(void* buf, int64_t row0, int64_t nloc, int64_t h, size_t esz, CommType t, cudaStream_t s) override {
+    ++calls;
     if (h == 0) return 0;
     char* b = static_cast<char*>(buf);
     const size_t cnt = (size_t)h * esz / ct_size(t);
@@ -189,6 +196,7 @@ struct LoopbackComm : Comm {
     world = grp->world;
     rank = r;
     graph_safe = false;
+    kind = 2;
   }
   ~LoopbackComm() override {
     if (dptrs) cudaFree(dptrs);
@@ -216,6 +224,7 @@ struct LoopbackComm : Comm {
     return rc;
   }
   int allgather_inplace(void* buf, size_t count, CommType t, cudaStream_t s) override {
+    ++calls;
     const size_t bytes = count * ct_size(t);
     int rc = publish(buf, s);
     for (int p = 0; p < world && !rc; ++p)
@@ -226,6 +235,7 @@ struct LoopbackComm : Comm {
     return rc ? rc : rc2;
   }
   int allgather(const void* send, void* recv, size_t count, CommType t, cudaStream_t s) override {
+    ++calls;
     const size_t bytes = count * ct_size(t);
     int rc = publish(send, s);
     for (int p = 0; p < world && !rc; ++p)
@@ -235,6 +245,7 @@ struct LoopbackComm : Comm {
     return rc ? rc : rc2;
   }
   int reduce_scatter(const void* send, void* recv, size_t count, CommType t, cudaStream_t s) override {
+    ++calls;
     int rc = publish(send, s);
     if (!rc && !dptrs) rc = cu(cudaMalloc(&dptrs, sizeof(void*) * world), "loopback alloc");
     if (!rc) rc = cu(cudaMemcpyAsync(dptrs, g->ptr.data(), sizeof(void*) * world, cudaMemcpyHostToDevice, s),
@@ -253,6 +264,7 @@ struct LoopbackComm : Comm {
     return rc ? rc : rc2;
   }
   int halo(void* buf, int64_t row0, int64_t nloc, int64_t h, size_t esz, CommType, cudaStream_t s) override {
+    ++calls;
     int rc = publish(buf, s);
     char* b = static_cast<char*>(buf);
     if (!rc && h > 0 && rank > 0)

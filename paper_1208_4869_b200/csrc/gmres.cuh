@@ -130,7 +130,7 @@ gm_pass(const typename CT<T>::c* __restrict__ V, int64_t ldv, typename CT<T>::c*
 }
 
 // world > 1: sum the allgathered rank sums in rank order
-__global__ void gm_ranksum(const double2* all, int world, int count, int stride, double2* out, const int* gate) {
+static __global__ void gm_ranksum(const double2* all, int world, int count, int stride, double2* out, const int* gate) {
   if (pdl_gate(gate)) return;
   for (int i = threadIdx.x; i < count; i += blockDim.x) {
     double2 s = make_double2(0.0, 0.0);
@@ -140,7 +140,7 @@ __global__ void gm_ranksum(const double2* all, int world, int count, int stride,
 }
 
 // Arnoldi / Givens step (one thread)
-__global__ void gm_step(State* st, GmDev* gm, const int* gate) {
+static __global__ void gm_step(State* st, GmDev* gm, const int* gate) {
   if (pdl_gate(gate)) return;
   const int j = gm->j;
   const int k = ++gm->k;
@@ -210,7 +210,7 @@ __global__ void gm_normalize(typename CT<T>::c* V, int64_t ldv, const typename C
 }
 
 // back substitution R y = g (one thread); decides done / restart
-__global__ void gm_trisolve(State* st, GmDev* gm, const int* gate) {
+static __global__ void gm_trisolve(State* st, GmDev* gm, const int* gate) {
   if (pdl_gate(gate)) return;
   const int J = gm->j + 1;
   for (int i = J - 1; i >= 0; --i) {
@@ -247,7 +247,7 @@ __global__ void gm_xupdate(typename CT<T>::c* __restrict__ x, const typename CT<
 }
 
 // end of every replayed step: re-arm the flags
-__global__ void gm_reset(GmDev* gm) {
+static __global__ void gm_reset(GmDev* gm) {
   pdl_wait();
   gm->endflag = 0;
   gm->noend = 1;

@@ -54,6 +54,7 @@ class Dense:
         x0d = None if x0 is None else to_dev(x0.astype(self.dtype))
         r = ccg.ccg_solve(self.h, method, x0d, yd, x, tol, maxit)
         r["x"] = x.cpu().numpy()
+        r["hist"] = ccg.ccg_get_history(self.h)
         return r
 
     def close(self):
@@ -73,3 +74,27 @@ class Csr(Dense):
         self.rp, self.ci, self.v = to_dev(rowptr), to_dev(colind), to_dev(vals)
         self.h = ccg.ccg_create(dt_name(self.dtype), n)
         ccg.ccg_set_matvec_csr(self.h, self.rp, self.ci, self.v, 0, n, len(vals), flags=flags)
+
+
+def envelope_parity(method, op, y, tol, maxit, dtype, g, solve_at_k, rec=None, **kw):
+    """SURVEY §8(c) P-envelope, all four criteria (oracle/envelope.py):
+    (1) k_GPU ∈ [k_min − 2, k_max + 2]; (2) x at equal k within max(bar, 2·D)
+    with D the pairwise spread; (3) true residual ≤ 10·tol; (4) the GPU
+    residual history (g["hist"]) agrees with the clean oracle history to H
+    over the envelope's agreement window.  `g` is the GPU result of the
+    tolerance-driven solve; `solve_at_k(k)` returns the GPU x after exactly k
+    iterations."""
+    from oracle.envelope import envelope, x_spread
+    env = envelope(method, op, y, tol, maxit, **kw)
+    rec = {} if rec is None else rec
+    rec.update(envelope_k=[env.k_min, env.k_max], envelope_window=env.window)
+    assert env.check_k(g["iterations"]), rec
+    k = min(g["iterations"], env.k_clean)
+    xc, D = x_spread(method, op, y, k, **kw)
+    err = relerr(solve_at_k(k), xc)
+    herr = env.history_error(g["hist"])
+    rec.update(envelope_D=D, x_err_equal_k=err, hist_err=herr)
+    assert err <= max(XTOL[np.dtype(dtype).type], 2 * D), rec
+    assert g["true_rel_res"] <= 10 * tol, rec
+    assert herr <= env.H, rec
+    return rec

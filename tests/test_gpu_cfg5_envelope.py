@@ -1,0 +1,103 @@
+"""BASELINE config 5 at FULL size (sparse c128 shifted Helmholtz, 128³ CSR,
+n = 2,097,152; BJ:11 — the paper's "own sparse matrix scheme" operator,
+PAPER.md:95 §5) against the oracle's rounding envelope (SURVEY §8(c)
+P-envelope).
+
+The envelope was computed once by `tools/make_cfg5_envelope.py`, which calls
+only oracle/ (the clean run and 8 noise seeds take ~1 h of CPU), and stored in
+`tests/golden/cfg5_envelope.json`.  Every operator and launch knob the
+library has for this problem must land inside it:
+
+  (1) iteration count in [k_min − 2, k_max + 2];
+  (4) residual history equal to the clean oracle history to H = 1e-8 over the
+      envelope's agreement window;
+  (3) true residual ≤ 10·tol, recomputed here by the oracle's own CSR product;
+  (2) x after exactly k iterations within max(1e-9, 2·D(k)) of the clean
+      oracle iterate, for the k at which the golden file records D(k) (the
+      oracle's clean iterate is recomputed here: ≤ 40 iterations).
+"""
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+from oracle import CsrOp
+from workloads import helmholtz_csr, helmholtz_rhs, helmholtz_coeffs
+from tests._gpu import Csr, relerr
+from tests.test_gpu_next import Stencil
+from tests.test_gpu_solve import _record
+
+pytestmark = pytest.mark.gpu
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden", "cfg5_envelope.json")
+N = 128
+
+VARIANTS = [
+    ("csr", {}),                              # library SELL-32 copy, one row per step (default)
+    ("csr", {"CCG_SELL_ONE": "0"}),           # SELL-32, two rows per step
+    ("csr", {"CCG_SPMV": "stream"}),          # CSR-stream blocks
+    ("csr", {"CCG_SPMV": "lanes"}),           # 8 lanes per row
+    ("stencil", {"CCG_STENCIL_ZC": "4"}),     # matrix-free operator (NEXT-4), z-chunks
+    ("stencil", {"CCG_STENCIL_ZC": "8"}),
+    ("stencil", {"CCG_STENCIL_ZC": "16"}),
+]
+
+
+@pytest.fixture(scope="module")
+def problem():
+    rp, ci, v = helmholtz_csr(N)
+    return rp, ci, v, helmholtz_rhs(N), CsrOp(rp, ci, v), json.load(open(GOLD))
+
+
+_XC = {}
+
+
+def _oracle_x(op, y, method, k):
+    if (method, k) not in _XC:
+        _XC[(method, k)] = oracle.solve(method, op, y, 0.0, k).x
+    return _XC[(method, k)]
+
+
+def _handle(kind, rp, ci, v):
+    if kind == "csr":
+        return Csr(rp, ci, v, N ** 3)
+    d, o = helmholtz_coeffs()
+    return Stencil(N, N, N, d, o)
+
+
+@pytest.mark.parametrize("method", ["bicgstab", "cors"])
+@pytest.mark.parametrize("kind,env", VARIANTS, ids=[f"{k}-{'-'.join(f'{a}={b}' for a, b in e.items()) or 'default'}"
+                                                     for k, e in VARIANTS])
+def test_cfg5_full_size_envelope(problem, method, kind, env, monkeypatch):
+    rp, ci, v, y, op, gold = problem
+    e = gold["methods"][method]
+    for key, val in env.items():
+        monkeypatch.setenv(key, val)
+    with _handle(kind, rp, ci, v) as h:
+        g = h.solve(method, y, gold["tol"], gold["maxit"])
+        xk = {int(k): h.solve(method, y, 0.0, int(k))["x"] for k in e["D"]}
+    rec = dict(test="cfg5-full-envelope", op=kind, env=env, method=method, k_gpu=g["iterations"],
+               envelope_k=[e["k_min"], e["k_max"]], window=e["window"])
+    assert g["status"] == "CONVERGED", rec
+    # (1) iteration count
+    assert e["k_min"] - 2 <= g["iterations"] <= e["k_max"] + 2, rec
+    # (4) history over the agreement window
+    hc = np.asarray(e["hist_clean"])
+    K = min(e["window"], len(g["hist"]) - 1)
+    herr = float(np.max(np.abs(g["hist"][:K + 1] - hc[:K + 1]) / hc[:K + 1])) if K >= 0 else 0.0
+    rec["hist_err"] = herr
+    assert herr <= gold["H"], rec
+    # (3) true residual by the oracle's CSR product
+    tr = np.linalg.norm(y - op.apply(g["x"])) / np.linalg.norm(y)
+    rec["true_rel_res"] = tr
+    assert tr <= 10 * gold["tol"], rec
+    assert abs(tr - g["true_rel_res"]) <= 1e-3 * tr + 1e-15, rec
+    # (2) x at equal k
+    for k, D in e["D"].items():
+        err = relerr(xk[int(k)], _oracle_x(op, y, method, int(k)))
+        rec[f"x_err_k{k}"] = err
+        assert err <= max(1e-9, 2 * D), rec
+    _record(**rec)

@@ -18,9 +18,8 @@ import paper_1208_4869_b200 as ccg
 import oracle
 from oracle import DenseOp, CsrOp
 from oracle.operators import reference_apply
-from oracle.envelope import iteration_envelope, x_spread
 from workloads import cfg1, cfg2, dense_random, helmholtz_csr, helmholtz_rhs
-from tests._gpu import to_dev, relerr, XTOL, TOL, Dense
+from tests._gpu import to_dev, relerr, XTOL, TOL, Dense, envelope_parity
 
 pytestmark = pytest.mark.gpu
 
@@ -71,10 +70,12 @@ class DenseGroup:
             x = yd.clone()
             res = ccg.ccg_solve(self.hs[r], method, None, yd, x, tol, maxit)
             res["x"] = x.cpu().numpy()
+            res["hist"] = ccg.ccg_get_history(self.hs[r])
             return res
         rs = _threads(self.G, f)
         for k in ("status", "iterations", "matvecs_a", "matvecs_ah", "true_rel_res", "rec_rel_res"):
             assert all(r[k] == rs[0][k] for r in rs), (k, [r[k] for r in rs])   # every rank agrees
+        assert all(np.array_equal(r["hist"], rs[0]["hist"]) for r in rs)
         out = dict(rs[0])
         out["x"] = np.concatenate([r["x"] for r in rs])
         return out
@@ -168,11 +169,8 @@ def test_sharded_csr_apply_and_solve(G):
         for method in ("bicgstab", "cors"):
             r = g.solve(method, y, 1e-8, 2000)
             assert r["status"] == "CONVERGED" and r["true_rel_res"] <= 1e-7
-            k0, kmin, kmax = iteration_envelope(method, op, y, 1e-8, 2000)
-            assert kmin - 2 <= r["iterations"] <= kmax + 2, (method, r["iterations"], kmin, kmax)
-            k = min(r["iterations"], k0)
-            xc, D = x_spread(method, op, y, k)
-            assert relerr(g.solve(method, y, 0.0, k)["x"], xc) <= max(1e-9, 2 * D)
+            envelope_parity(method, op, y, 1e-8, 2000, np.complex128, r,
+                            lambda k: g.solve(method, y, 0.0, k)["x"], dict(method=method, G=G))
         # CSR Aᴴ is single-GPU only
         xd = to_dev(x[:g.nloc].astype(np.complex128))
         with pytest.raises(ccg.CcgError) as e:
@@ -216,11 +214,8 @@ def test_sharded_stencil_apply_and_solve(G):
     try:
         for method in ("bicgstab", "cocr", "qmr"):
             r = g.solve(method, y, 1e-8, 3000)
-            k0, kmin, kmax = iteration_envelope(method, op, y, 1e-8, 3000)
-            assert kmin - 2 <= r["iterations"] <= kmax + 2, (method, r["iterations"], kmin, kmax)
-            k = min(r["iterations"], k0)
-            xc, D = x_spread(method, op, y, k)
-            assert relerr(g.solve(method, y, 0.0, k)["x"], xc) <= max(1e-9, 2 * D), method
+            envelope_parity(method, op, y, 1e-8, 3000, np.complex128, r,
+                            lambda k: g.solve(method, y, 0.0, k)["x"], dict(method=method, G=G))
     finally:
         g.close()
 
@@ -318,11 +313,8 @@ def test_replicated_csr_stencil_toeplitz(G):
                 assert relerr(grp.apply(x, o), reference_apply(op, x, o)) <= 1e-13, o
             for method in ("bicgstab", "qmr", "cocr"):
                 r = grp.solve(method, y, 1e-8, 3000)
-                k0, kmin, kmax = iteration_envelope(method, op, y, 1e-8, 3000)
-                assert kmin - 2 <= r["iterations"] <= kmax + 2, (method, r["iterations"], kmin, kmax)
-                k = min(r["iterations"], k0)
-                xc, D = x_spread(method, op, y, k)
-                assert relerr(grp.solve(method, y, 0.0, k)["x"], xc) <= max(1e-9, 2 * D), method
+                envelope_parity(method, op, y, 1e-8, 3000, np.complex128, r,
+                                lambda k: grp.solve(method, y, 0.0, k)["x"], dict(method=method, G=G))
         finally:
             grp.close()
     dims = (8, 6, 4)

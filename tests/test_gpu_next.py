@@ -477,6 +477,7 @@ def test_callback_graph_safe_native(tridiag_lib, method):
                 xo = torch.empty_like(yv)
                 r = ccg.ccg_solve(h, m, None, yv, xo, tol, maxit)
                 r["x"] = xo.cpu().numpy()
+                r["hist"] = ccg.ccg_get_history(h)
                 return r
         yv = _x(n, np.complex128, 6)
         o, g = _parity(H(), DenseOp(A), yv, method, 1e-10, 2000, np.complex128, tag="callback")
@@ -510,6 +511,7 @@ def test_callback_python_eager():
                 xo = torch.empty_like(yv)
                 r = ccg.ccg_solve(h, m, None, yv, xo, tol, maxit)
                 r["x"] = xo.cpu().numpy()
+                r["hist"] = ccg.ccg_get_history(h)
                 return r
         for m in ("bicgstab", "cgne"):
             _parity(H(), DenseOp(A), y, m, 1e-10, 500, np.complex128, tag="callback-py")

@@ -17,7 +17,7 @@ __all__ = [
     "CONFIGS", "cfg1", "cfg2", "cfg3_rows", "cfg3_rhs", "cfg3", "gauss_shifted_rows",
     "dda_lattice_rows", "dda_lattice_rhs", "cfg2_like", "cfg4_rows", "cfg4_rhs",
     "helmholtz_csr", "helmholtz_rhs", "cfg5", "dense_random", "lattice_dims", "BLOCK",
-    "lattice_csr", "helmholtz_coeffs", "dda_kernel",
+    "lattice_csr", "helmholtz_coeffs", "dda_kernel", "graded_svd",
 ]
 
 # config index -> (dtype, n, methods, tol, maxit)  (BJ:7-11, maxit per Q8)
@@ -266,3 +266,18 @@ def dense_random(n, seed=0, dtype=np.complex128, shift=0.0, scale=None):
     A = scale * (rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n)))
     A[np.diag_indices(n)] += shift
     return A.astype(dtype)
+
+
+def graded_svd(n=8, decades=5, seed=5, dtype=np.complex128):
+    """SPEC.md:281 (finalize) fixture: a seeded n×n system with singular values
+    logspace(0, −decades, n) between two random unitary factors (QR of
+    complex Gaussian matrices from default_rng(seed), drawn in the order U, V,
+    then y).  Near stagnation at tight tolerances the CGS recurrence residual
+    drifts below the attainable true residual (the FALSE_CONVERGENCE case)."""
+    rng = np.random.default_rng(seed)
+    U, _ = np.linalg.qr(rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n)))
+    V, _ = np.linalg.qr(rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n)))
+    s = np.logspace(0, -float(decades), n)
+    A = (U * s) @ V.conj().T
+    y = rng.standard_normal(n) + 1j * rng.standard_normal(n)
+    return A.astype(dtype), y.astype(dtype)
