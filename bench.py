@@ -43,6 +43,8 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--sharded-vectors", action="store_true",
                    help="N>1: row-sharded vectors (C1 allgather + scalar allgathers) instead of replicated vectors")
+    p.add_argument("--force-comm", action="store_true",
+                   help="N=1: run the sharded code path through a one-rank NCCL communicator (CCG_OPT_FORCE_COMM)")
     return p.parse_args()
 
 
@@ -156,6 +158,15 @@ def oracle_sample(A, y, budget_s=20.0):
                       ", ".join(runs) + "); NumPy BLAS GEMV, Aᴴx as conj(conj(x)ᵀA)"}
 
 
+def bench_config(world, args):
+    """The config dict both arms print (identical by construction)."""
+    rep = world > 1 and not args.sharded_vectors
+    return {"workload": WORKLOAD, "n": N, "methods": list(METHODS), "tol": TOL, "maxit": MAXIT,
+            "parallelism": f"row-shard{world}" + ("+replicated-vectors" if rep else ""),
+            "vector_mode": "replicated" if rep else "sharded",
+            "l2": "A is 8.6 GB >> 126 MB L2: no flush needed"}
+
+
 def gen_rows(r0, r1, out):
     from workloads import gauss_shifted_rows
     return gauss_shifted_rows(N, r0, r1, seed=1, out=out)
@@ -170,20 +181,22 @@ def run_reference(args):
     A = np.empty((N, N), dtype=np.complex64)
     gen_rows(0, N, A)
     y = cfg3_rhs(N)
-    vals = []
+    vals, secs = [], []
     cb = None
     for _ in range(min(args.warmup, 1)):           # warm BLAS / page in A
         oracle_sample(A, y, budget_s=60.0)
     for _ in range(args.steps):
+        t0 = time.perf_counter()
         cb = oracle_sample(A, y, budget_s=60.0)
+        secs.append(time.perf_counter() - t0)
         vals.append(cb["value"])
     v = float(np.median(vals))
     cb["value"] = v
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "iterations/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": None, "higher_is_better": True, "scaling": "strong",
+            "ms_per_step": 1e3 * float(np.median(secs)), "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "c64", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "n": N, "methods": list(METHODS), "tol": TOL},
+            "config": bench_config(world, args),
             "cpu_baseline": cb,
             "e2e": {"value": v, "unit": "iterations/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
@@ -200,6 +213,10 @@ def run_ccg(args):
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
+    uses_nccl = world > 1 or args.force_comm
+    if uses_nccl:   # NCCL init lines (nRanks, transport) on stderr for the record
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
@@ -232,7 +249,8 @@ def run_ccg(args):
 
     # N > 1: replicated vectors (SURVEY §8(f) NEXT-2 ii) — one collective per
     # product and none per reduction phase
-    opts = ccg.OPT_REPLICATED if (world > 1 and not args.sharded_vectors) else 0
+    opts = (ccg.OPT_REPLICATED if (world > 1 and not args.sharded_vectors) else 0) | \
+        (ccg.OPT_FORCE_COMM if args.force_comm else 0)
     h = ccg.ccg_create("c64", N, world=world, rank=rank, nccl_id=nccl_id, device=local_rank, options=opts)
     ccg.ccg_set_matvec_dense(h, Ad, row0, nloc)
     stream = torch.cuda.ExternalStream(ccg.ccg_get_stream(h), device=dev)
@@ -256,8 +274,8 @@ def run_ccg(args):
     for _ in range(args.warmup):
         step()
 
-    # ---- timed region (device events on the library stream + kernel events)
-    ccg.ccg_set_timing(h, 1)
+    # ---- timed region: the production path (graph replay, no per-kernel
+    # events); device events on the library stream, max over ranks
     sampler = ClockSampler(local_rank)
     sampler.start()
     time.sleep(0.3)
@@ -266,26 +284,38 @@ def run_ccg(args):
     ev1 = torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
     its_total, launches_total = 0, 0
-    ms_a = ms_ah = 0.0
-    n_a = n_ah = 0
+    mv_a = mv_ah = 0
     for _ in range(args.steps):
         for m in METHODS:
             r = ccg.ccg_solve(h, m, None, yloc, xloc, TOL, MAXIT)
             assert r["status"] == "CONVERGED", r
             its_total += r["iterations"]
+            mv_a += r["matvecs_a"] + 1          # + the true-residual product
+            mv_ah += r["matvecs_ah"]
             launches_total += ccg.ccg_last_launch_count(h)
-            t = ccg.ccg_get_timing(h)
-            ms_a += t["ms_a"]; n_a += t["n_a"]; ms_ah += t["ms_ah"]; n_ah += t["n_ah"]
     ev1.record(stream)
     barrier()
     clocks = sampler.stop()
-    ccg.ccg_set_timing(h, 0)
+    stats = ccg.ccg_get_stats(h)
     ms = ev0.elapsed_time(ev1)
     if dist:
         t = torch.tensor([ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     value = its_total / (ms / 1e3)
+
+    # ---- kernel timing pass (separate, not the headline): CUDA events around
+    # every product launch on the library stream (library timing mode)
+    ccg.ccg_set_timing(h, 1)
+    ms_a = ms_ah = 0.0
+    n_a = n_ah = 0
+    for _ in range(max(1, min(args.steps, 3))):
+        for m in METHODS:
+            r = ccg.ccg_solve(h, m, None, yloc, xloc, TOL, MAXIT)
+            assert r["status"] == "CONVERGED", r
+            t = ccg.ccg_get_timing(h)
+            ms_a += t["ms_a"]; n_a += t["n_a"]; ms_ah += t["ms_ah"]; n_ah += t["n_ah"]
+    ccg.ccg_set_timing(h, 0)
 
     # ---- e2e: host (pinned) buffers through the C-ABI, copies inside the call
     e2e = None
@@ -298,6 +328,7 @@ def run_ccg(args):
         for _ in range(args.steps):
             for m in METHODS:
                 r = ccg.ccg_solve(h, m, None, yh, xh, TOL, MAXIT)
+                assert r["status"] == "CONVERGED", r
                 its_e += r["iterations"]
         barrier()
         dt = time.perf_counter() - t0
@@ -329,7 +360,14 @@ def run_ccg(args):
             "ah": {"kernel": "gemv_h_stage1+stage2 (Aᴴ·x)", "achieved": ach_ah,
                    "frac": (ach_ah / peak) if ach_ah else None,
                    "avg_launch_ms": (ms_ah / n_ah) if n_ah else None, "launches_timed": n_ah},
-            "matvec_share_of_step": ((ms_a + ms_ah) / ms) if ms else None}
+            "timing_pass": "separate pass with per-launch CUDA events (library timing mode); "
+                           "the headline value is the graph-replay path without them"}
+    # whole-step effective bandwidth: the products' algorithmic bytes over the
+    # (production-path) step time — vector passes not counted
+    step_bytes = mv_a * bytes_a + mv_ah * bytes_ah
+    roof["step_effective_gbs"] = step_bytes / (ms * 1e-3) / 1e9
+    roof["step_effective_frac"] = roof["step_effective_gbs"] / peak
+    roof["matvec_share_of_step"] = ((ms_a / n_a * mv_a + ms_ah / n_ah * mv_ah) / ms) if (n_a and n_ah) else None
 
     cpu = None
     if keep_host:
@@ -340,11 +378,12 @@ def run_ccg(args):
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
                 "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
                 "dtype": "c64", "data": "synthetic",
-                "config": {"workload": WORKLOAD, "n": N, "methods": list(METHODS), "tol": TOL,
-                           "maxit": MAXIT, "iterations_per_step": its_total // args.steps,
-                           "parallelism": f"row-shard{world}" + (
-                               "+replicated-vectors" if world > 1 and not args.sharded_vectors else ""),
-                           "l2": "A is 8.6 GB >> 126 MB L2: no flush needed"},
+                "config": bench_config(world, args),
+                "iterations_per_step": its_total // args.steps,
+                "comm": {"kind": {0: "none", 1: "nccl", 2: "loopback"}[stats["comm_kind"]],
+                         "graph_replays": stats["graph_replays"],
+                         "collectives_in_graphs_last_solve": stats["graph_collectives"],
+                         "force_comm": bool(args.force_comm)},
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": launches_total, "clocks": clocks}
         print(json.dumps(line), flush=True)

@@ -164,7 +164,16 @@ int ccg_create(ccg_handle* h, ccg_dtype dt, int64_t n, int world, int rank,
  * collective is then an identity, so results equal the world == 1 path up to
  * summation order; it exists to run the NCCL data plane on one GPU.  Combine
  * with CCG_OPT_REPLICATED for the replicated-vector mode. */
-enum { CCG_OPT_REPLICATED = 1, CCG_OPT_FORCE_COMM = 2 };
+/* CCG_OPT_P2P (with CCG_OPT_REPLICATED; world <= 8, one NVLink/NVSwitch
+ * domain; SURVEY §8(f) NEXT-2 i): the gather that ends every replicated-mode
+ * product (rows of A·x, dense Aᴴ partials) is fused into the product kernel's
+ * epilogue — each output element is stored directly into every rank's
+ * buffer through an NCCL symmetric-memory window (ncclCommWindowRegister,
+ * ncclGetPeerPointer), followed by a release flag per rank and an acquire
+ * wait; no NCCL collective remains on the product path.  Double-buffered by
+ * a device-side exchange epoch.  CCG_E_CAPABILITY if NCCL has no windows.
+ * (The user-callback operator keeps the NCCL allgather.) */
+enum { CCG_OPT_REPLICATED = 1, CCG_OPT_FORCE_COMM = 2, CCG_OPT_P2P = 4 };
 int ccg_create_ex(ccg_handle* h, ccg_dtype dt, int64_t n, int world, int rank,
                   const uint8_t* nccl_id, int device, void* cuda_stream, uint32_t options);
 
@@ -334,7 +343,8 @@ int64_t ccg_last_launch_count(ccg_handle h);
  *   CCG_STAT_WORLD, CCG_STAT_REPLICATED  the handle's world size / vector mode
  * Returns CCG_E_ARG for an unknown key or NULL value. */
 enum { CCG_STAT_COMM_KIND = 0, CCG_STAT_GRAPH_REPLAYS = 1, CCG_STAT_GRAPH_COLLECTIVES = 2,
-       CCG_STAT_EAGER_COLLECTIVES = 3, CCG_STAT_WORLD = 4, CCG_STAT_REPLICATED = 5 };
+       CCG_STAT_EAGER_COLLECTIVES = 3, CCG_STAT_WORLD = 4, CCG_STAT_REPLICATED = 5,
+       CCG_STAT_P2P_EXCHANGES = 6 /* P2P mirror exchanges issued (host side, since create) */ };
 int ccg_get_stat(ccg_handle h, int32_t key, int64_t* value);
 
 /* cudaStream_t of the handle (for callers that order their own work). */

@@ -175,6 +175,7 @@ def ccg_get_unique_id():
 
 OPT_REPLICATED = 1
 OPT_FORCE_COMM = 2
+OPT_P2P = 4
 
 
 def ccg_create(dtype, n, world=1, rank=0, nccl_id=None, device=0, stream=None, options=0):
@@ -315,7 +316,7 @@ def ccg_last_launch_count(h):
 
 
 STATS = {"comm_kind": 0, "graph_replays": 1, "graph_collectives": 2, "eager_collectives": 3,
-         "world": 4, "replicated": 5}
+         "world": 4, "replicated": 5, "p2p_exchanges": 6}
 
 
 def ccg_get_stat(h, key):

@@ -8,9 +8,26 @@
 // ddprecision.f90 single/double switch -> ccg_dtype.
 #include "engine.cuh"
 
+#include <nccl_device.h>   // ncclGetPeerPointer (header-only device API, NCCL 2.28)
+
 namespace {
 thread_local std::string g_create_err;   // ccg_last_error(NULL): why the last create failed
 }  // namespace
+
+// every rank's base address of an NCCL symmetric-memory window
+static __global__ void p2p_resolve(ncclWindow_t w, int world, char** out) {
+  const int p = threadIdx.x;
+  if (p < world) out[p] = static_cast<char*>(ncclGetPeerPointer(w, 0, p));
+}
+
+// P2P mirror region: [parity 0 | parity 1] × [rep_tmp n | rep_parts world·n],
+// then P2P_MAX flags (CCG_OPT_P2P, p2p.cuh)
+static size_t mirror_layout(ccg_ctx* c) {
+  const size_t half = ((size_t)c->n * (1 + c->world) * c->esz + 255) & ~(size_t)255;
+  c->mirror_half = half;
+  c->mirror_flags = 2 * half;
+  return (2 * half + P2P_MAX * sizeof(uint64_t) + 4095) & ~(size_t)4095;   // NCCL_WIN_REQUIRED_ALIGNMENT
+}
 
 // ===========================================================================
 // launch-parameter selection
@@ -463,6 +480,11 @@ static int create_impl(ccg_handle* h, ccg_dtype dt, int64_t n, int world, int ra
     CKC(cudaMalloc(&c->rep_tmp, (size_t)n * c->esz));
     CKC(cudaMalloc(&c->rep_parts, (size_t)n * world * c->esz));
   }
+  if ((options & CCG_OPT_P2P) && !(c->rep && world <= P2P_MAX)) {
+    c->err = "CCG_OPT_P2P needs CCG_OPT_REPLICATED, a communicator (world > 1 or CCG_OPT_FORCE_COMM) and world <= 8";
+    return bail(CCG_E_ARG);
+  }
+  c->p2p = (options & CCG_OPT_P2P) != 0;
   if (c->dist) {
     CKC(cudaMalloc(&c->wfull, (size_t)n * c->esz));
     if (lg) {
@@ -481,6 +503,31 @@ static int create_impl(ccg_handle* h, ccg_dtype dt, int64_t n, int world, int ra
       }
       int rc = nc->init(world, rank, nccl_id);
       if (rc) { c->err = nc->err; return bail(CCG_E_NCCL); }
+      if (c->p2p) {   // symmetric-memory window + every rank's address of it
+        c->mirror_bytes = mirror_layout(c);
+        rc = nc->window_alloc(c->mirror_bytes, &c->mirror, &c->win);
+        if (rc) { c->err = nc->err; return bail(rc == -3 ? CCG_E_CAPABILITY : CCG_E_NCCL); }
+        char** dptr = nullptr;
+        CKC(cudaMalloc(&dptr, sizeof(char*) * P2P_MAX));
+        p2p_resolve<<<1, 32, 0, c->stream>>>(c->win, world, dptr);
+        cudaError_t e1 = cudaGetLastError();
+        if (e1 == cudaSuccess)
+          e1 = cudaMemcpyAsync(c->peer_base, dptr, sizeof(char*) * world, cudaMemcpyDeviceToHost, c->stream);
+        if (e1 == cudaSuccess) e1 = cudaStreamSynchronize(c->stream);
+        cudaFree(dptr);
+        CKC(e1);
+      }
+    }
+    if (c->p2p) {
+      if (lg) {   // loopback: the peers' regions are filled in by the group
+        c->mirror_bytes = mirror_layout(c);
+        CKC(cudaMalloc(&c->mirror, c->mirror_bytes));
+        c->peer_base[rank] = static_cast<char*>(c->mirror);
+      }
+      CKC(cudaMemsetAsync(c->mirror, 0, c->mirror_bytes, c->stream));
+      CKC(cudaMalloc(&c->p2p_ctr, 2 * sizeof(uint64_t)));
+      CKC(cudaMemsetAsync(c->p2p_ctr, 0, 2 * sizeof(uint64_t), c->stream));
+      CKC(cudaStreamSynchronize(c->stream));
     }
   }
 #undef CKC
@@ -516,6 +563,9 @@ int ccg_create_loopback_group_ex(ccg_handle* hs, int world, ccg_dtype dt, int64_
   }
   if (rc) {
     for (int r = 0; r < made; ++r) ccg_destroy(hs[r]);
+  } else if (options & CCG_OPT_P2P) {   // every rank sees every rank's mirror region
+    for (int r = 0; r < world; ++r)
+      for (int p = 0; p < world; ++p) hs[r]->peer_base[p] = static_cast<char*>(hs[p]->mirror);
   }
   bool last = false;
   {
@@ -1155,6 +1205,7 @@ int ccg_get_stat(ccg_handle c, int32_t key, int64_t* value) {
     case CCG_STAT_EAGER_COLLECTIVES: *value = c->stat_eager_coll; break;
     case CCG_STAT_WORLD: *value = c->world; break;
     case CCG_STAT_REPLICATED: *value = c->rep ? 1 : 0; break;
+    case CCG_STAT_P2P_EXCHANGES: *value = c->p2p_calls; break;
     default: FAIL(c, CCG_E_ARG, "unknown stat key");
   }
   return CCG_OK;
@@ -1172,6 +1223,13 @@ int ccg_destroy(ccg_handle c) {
   for (auto e : c->ev) cudaEventDestroy(e);
   for (auto e : c->done_ev) if (e) cudaEventDestroy(e);
   if (c->done_ring) cudaFreeHost(c->done_ring);
+  if (c->mirror) {
+    NcclComm* nc = c->win ? dynamic_cast<NcclComm*>(c->comm) : nullptr;
+    if (nc) nc->window_free(c->mirror, c->win);
+    else cudaFree(c->mirror);
+    c->mirror = nullptr;
+  }
+  if (c->p2p_ctr) cudaFree(c->p2p_ctr);
   delete c->comm;
   c->comm = nullptr;
   for (int i = 0; i < NLOCAL; ++i) if (c->loc[i]) cudaFree(c->loc[i]);

@@ -43,6 +43,11 @@ struct NcclApi {
   ncclResult_t (*GroupStart)() = nullptr;
   ncclResult_t (*GroupEnd)() = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  // symmetric memory (NCCL ≥ 2.27; optional: only the P2P mirror mode needs them)
+  ncclResult_t (*MemAlloc)(void**, size_t) = nullptr;
+  ncclResult_t (*MemFree)(void*) = nullptr;
+  ncclResult_t (*WindowRegister)(ncclComm_t, void*, size_t, ncclWindow_t*, int) = nullptr;
+  ncclResult_t (*WindowDeregister)(ncclComm_t, ncclWindow_t) = nullptr;
 };
 inline NcclApi g_nccl;
 
@@ -68,6 +73,11 @@ inline bool nccl_load() {
   CCG_LOADSYM(GroupEnd, "ncclGroupEnd");
   CCG_LOADSYM(GetErrorString, "ncclGetErrorString");
 #undef CCG_LOADSYM
+  g_nccl.MemAlloc = reinterpret_cast<decltype(g_nccl.MemAlloc)>(dlsym(h, "ncclMemAlloc"));
+  g_nccl.MemFree = reinterpret_cast<decltype(g_nccl.MemFree)>(dlsym(h, "ncclMemFree"));
+  g_nccl.WindowRegister = reinterpret_cast<decltype(g_nccl.WindowRegister)>(dlsym(h, "ncclCommWindowRegister"));
+  g_nccl.WindowDeregister =
+      reinterpret_cast<decltype(g_nccl.WindowDeregister)>(dlsym(h, "ncclCommWindowDeregister"));
   g_nccl.loaded = true;
   return true;
 }
@@ -93,6 +103,10 @@ struct Comm {
   // global positions (their halo), and receive theirs.
   virtual int halo(void* buf, int64_t row0, int64_t nloc, int64_t h, size_t esz, CommType t,
                    cudaStream_t s) = 0;
+  // P2P mirror exchange (p2p.cuh): a point where every rank's preceding work
+  // is complete.  NCCL: nothing (the device flags order it); loopback: a host
+  // barrier, so that no kernel ever waits on another rank's kernel.
+  virtual int sync_point(cudaStream_t) { return 0; }
 };
 
 // ---------------------------------------------------------------------------
@@ -114,6 +128,19 @@ struct NcclComm : Comm {
   }
   ~NcclComm() override {
     if (comm && g_nccl.loaded) g_nccl.CommDestroy(comm);
+  }
+  // symmetric-memory window of `bytes` (collective over the ranks)
+  int window_alloc(size_t bytes, void** ptr, ncclWindow_t* win) {
+    if (!g_nccl.MemAlloc || !g_nccl.WindowRegister) { err = "NCCL has no symmetric-memory windows"; return -3; }
+    ncclResult_t e = g_nccl.MemAlloc(ptr, bytes);
+    if (e != ncclSuccess) return fail(e, "ncclMemAlloc");
+    e = g_nccl.WindowRegister(comm, *ptr, bytes, win, NCCL_WIN_COLL_SYMMETRIC);
+    if (e != ncclSuccess) { g_nccl.MemFree(*ptr); *ptr = nullptr; return fail(e, "ncclCommWindowRegister"); }
+    return 0;
+  }
+  void window_free(void* ptr, ncclWindow_t win) {
+    if (win && g_nccl.WindowDeregister) g_nccl.WindowDeregister(comm, win);
+    if (ptr && g_nccl.MemFree) g_nccl.MemFree(ptr);
   }
   int allgather_inplace(void* buf, size_t count, CommType t, cudaStream_t s) override {
     ++calls;
@@ -263,6 +290,7 @@ struct LoopbackComm : Comm {
     int rc2 = done(s);
     return rc ? rc : rc2;
   }
+  int sync_point(cudaStream_t s) override { return done(s); }
   int halo(void* buf, int64_t row0, int64_t nloc, int64_t h, size_t esz, CommType, cudaStream_t s) override {
     ++calls;
     int rc = publish(buf, s);

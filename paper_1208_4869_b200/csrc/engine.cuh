@@ -29,6 +29,7 @@
 #include "fft.cuh"
 #include "cluster.cuh"
 #include "gmres.cuh"
+#include "p2p.cuh"
 
 #include <complex>
 #include <unordered_map>
@@ -50,6 +51,16 @@ struct ccg_ctx {
   bool rep = false;                     // replicated-vector mode (SURVEY §8(f) NEXT-2 ii)
   void* rep_tmp = nullptr;              // n: product rows gathered from every rank
   void* rep_parts = nullptr;            // world × n: Aᴴ partials of every rank
+  // P2P mirror exchange (CCG_OPT_P2P, p2p.cuh): rep_tmp / rep_parts live in a
+  // double-buffered mirror region [parity][rep_tmp n | rep_parts world·n] +
+  // flags, which every rank's product epilogue writes directly
+  bool p2p = false;
+  void* mirror = nullptr;               // this rank's region (owned)
+  size_t mirror_bytes = 0, mirror_half = 0;   // bytes; offset of parity 1
+  size_t mirror_flags = 0;              // offset of the flag array (P2P_MAX uint64)
+  char* peer_base[P2P_MAX] = {};        // every rank's region (this process's addresses)
+  ncclWindow_t win = nullptr;           // NCCL symmetric-memory window (NCCL mode)
+  uint64_t* p2p_ctr = nullptr;          // device: send / receive epochs
   int world = 1, rank = 0, device = 0;
   bool dist = false;                    // sharded code path with a communicator (world > 1, or
                                         // CCG_OPT_FORCE_COMM: a one-rank NCCL communicator)
@@ -165,6 +176,7 @@ struct ccg_ctx {
   // a call captured in the iteration graph counts once per replay)
   int64_t coll_per_iter[M_COUNT] = {};
   int64_t stat_replays = 0, stat_graph_coll = 0, stat_eager_coll = 0, stat_capture_calls = 0;
+  int64_t p2p_calls = 0;   // P2P mirror exchanges issued (host side; a captured one counts once)
   bool capturing = false;
   bool pdl = true;        // programmatic dependent launch (env CCG_PDL=0 disables)
   std::unordered_map<const void*, int> occ_cache;   // per-kernel occupancy / attribute flags (this device)
@@ -461,10 +473,55 @@ struct Engine {
   // allgathered, then the method epilogue as one pass over the whole vector
   template <class Epi>
   static int rep_finish_rows(ccg_ctx* c, Epi epi, const int* gate) {
+    if (c->p2p) {   // rows already mirrored into every rank by the product epilogue
+      TRY(p2p_exchange(c, gate));
+      EpiPassMirror<T, Epi> ep{epi, mirror_view(c, 0)};
+      return pass(c, ep, gate);
+    }
     C* tmp = reinterpret_cast<C*>(c->rep_tmp);
     NK(c, c->comm->allgather_inplace(tmp, (size_t)c->mnloc * 2, ndt(), c->stream));
     EpiPass<C, Epi> ep{epi, tmp};
     return pass(c, ep, gate);
+  }
+
+  // -------------------- P2P mirror exchange (p2p.cuh) --------------------
+  // the product epilogue: element i of this rank's output -> element off + i of
+  // every rank's mirror buffer `which` (0 = rep_tmp, 1 = rep_parts)
+  static MirrorStore<T> mirror_store(ccg_ctx* c, int which, int64_t off) {
+    MirrorStore<T> m{};
+    const size_t base = which == 0 ? 0 : (size_t)c->n * sizeof(C);
+    for (int par = 0; par < 2; ++par)
+      for (int p = 0; p < c->world; ++p)
+        m.dst[par][p] = reinterpret_cast<C*>(c->peer_base[p] + par * c->mirror_half + base) + off;
+    m.ctr = c->p2p_ctr;
+    m.world = c->world;
+    return m;
+  }
+  static MirrorView<T> mirror_view(ccg_ctx* c, int which) {
+    MirrorView<T> v{};
+    const size_t base = which == 0 ? 0 : (size_t)c->n * sizeof(C);
+    for (int par = 0; par < 2; ++par)
+      v.buf[par] = reinterpret_cast<const C*>(static_cast<char*>(c->mirror) + par * c->mirror_half + base);
+    v.ctr = c->p2p_ctr;
+    return v;
+  }
+  // after the mirrored product: publish this rank's epoch, (loopback: host
+  // barrier), wait for every rank's
+  static int p2p_exchange(ccg_ctx* c, const int* gate) {
+    P2pCtl ctl{};
+    for (int p = 0; p < c->world; ++p)
+      ctl.flags[p] = reinterpret_cast<uint64_t*>(c->peer_base[p] + c->mirror_flags);
+    ctl.ctr = c->p2p_ctr;
+    ctl.world = c->world;
+    ctl.rank = c->rank;
+    launch_k(c, p2p_signal, 1, 1, 0, c->stream, ctl, gate);
+    CK(c, cudaGetLastError());
+    NK(c, c->comm->sync_point(c->stream));
+    launch_k(c, p2p_wait, 1, 1, 0, c->stream, ctl, gate);
+    c->launches += 2;
+    c->p2p_calls++;
+    CK(c, cudaGetLastError());
+    return CCG_OK;
   }
 
   // y_local = A · xfull (full-length buffer, own slice + gathered/halo parts)
@@ -477,7 +534,8 @@ struct Engine {
     }
     if (c->opk == OPK_CALLBACK) return user_product(c, CCG_OP_A, xfull, epi, gate);
     if (c->rep && c->opk != OPK_TOEPLITZ) {
-      TRY(matvec_rows(c, xfull, Store<T>{reinterpret_cast<C*>(c->rep_tmp) + c->mrow0}, gate));
+      if (c->p2p) TRY(matvec_rows(c, xfull, mirror_store(c, 0, c->mrow0), gate));
+      else TRY(matvec_rows(c, xfull, Store<T>{reinterpret_cast<C*>(c->rep_tmp) + c->mrow0}, gate));
       return rep_finish_rows(c, epi, gate);
     }
     return matvec_rows(c, xfull, epi, gate);
@@ -614,7 +672,8 @@ struct Engine {
         else spmv<false>(c, xin, e, gate);
       };
       tev_begin(c, 1);
-      if (c->rep) launch(Store<T>{reinterpret_cast<C*>(c->rep_tmp) + c->mrow0});
+      if (c->rep && c->p2p) launch(mirror_store(c, 0, c->mrow0));
+      else if (c->rep) launch(Store<T>{reinterpret_cast<C*>(c->rep_tmp) + c->mrow0});
       else launch(epi);
       c->launches++;
       tev_end(c);
@@ -649,6 +708,16 @@ struct Engine {
       return CCG_OK;
     }
     // multi GPU: full-length partial of this rank
+    if (c->rep && c->p2p) {   // straight into slot `rank` of every rank's partial array
+      launch_k(c, gemv_h_stage2<T, NT, MirrorStore<T>>, c->stage2_grid, NT, 0, c->stream, part, c->ah_S, c->n, 0, c->n,
+               mirror_store(c, 1, (int64_t)c->rank * c->n), make_red(c), c->st, gate);
+      c->launches++;
+      tev_end(c);
+      CK(c, cudaGetLastError());
+      TRY(p2p_exchange(c, gate));
+      EpiPassMirrorSum<T, Epi> ep{epi, mirror_view(c, 1), c->world, c->n};
+      return pass(c, ep, gate);
+    }
     C* wf = c->rep ? reinterpret_cast<C*>(c->rep_tmp) : reinterpret_cast<C*>(c->wfull);
     Store<T> stv{wf};
     launch_k(c, gemv_h_stage2<T, NT, Store<T>>, c->stage2_grid, NT, 0, c->stream, part, c->ah_S, c->n, 0, c->n, stv,

@@ -685,7 +685,7 @@ spmv_stream_kernel(const int32_t* __restrict__ rowptr, const int32_t* __restrict
 // one SELL row of exactly W stored entries: all W column indices, then all W
 // values and x gathers are issued before any arithmetic (padding: col = −1,
 // gather clamped to index 0 and its product skipped), then the products are
-// added in CSR column order, each formed from zero
+// accumulated by FMA in CSR column order
 template <int W, bool CONJ, typename C>
 __device__ __forceinline__ C sell_row(const int32_t* __restrict__ scol, const C* __restrict__ sval,
                                       const C* __restrict__ x, int64_t base) {
@@ -701,9 +701,8 @@ __device__ __forceinline__ C sell_row(const int32_t* __restrict__ scol, const C*
   C acc = czero<C>();
 #pragma unroll
   for (int u = 0; u < W; ++u) {
-    C p = czero<C>();
-    cfma(p, v[u], CONJ ? cconj(xv[u]) : xv[u]);
-    const C a2 = cadd(acc, p);
+    C a2 = acc;
+    cfma(a2, v[u], CONJ ? cconj(xv[u]) : xv[u]);   // acc += v·x as 4 FMAs
     acc.x = col[u] >= 0 ? a2.x : acc.x;   // select, not a branch: the loads stay batched
     acc.y = col[u] >= 0 ? a2.y : acc.y;
   }
@@ -753,10 +752,9 @@ spmv_sell_kernel(const int64_t* __restrict__ soff, const int32_t* __restrict__ s
     C a1 = czero<C>(), a2 = czero<C>();
 #pragma unroll
     for (int u = 0; u < 7; ++u) {
-      C p = czero<C>(), q = czero<C>();
-      cfma(p, v1[u], CONJ ? cconj(x1[u]) : x1[u]);
-      cfma(q, v2[u], CONJ ? cconj(x2[u]) : x2[u]);
-      const C t1 = cadd(a1, p), t2 = cadd(a2, q);
+      C t1 = a1, t2 = a2;
+      cfma(t1, v1[u], CONJ ? cconj(x1[u]) : x1[u]);
+      cfma(t2, v2[u], CONJ ? cconj(x2[u]) : x2[u]);
       a1.x = c1[u] >= 0 ? t1.x : a1.x; a1.y = c1[u] >= 0 ? t1.y : a1.y;
       a2.x = c2[u] >= 0 ? t2.x : a2.x; a2.y = c2[u] >= 0 ? t2.y : a2.y;
     }
@@ -840,16 +838,20 @@ __global__ void csr_to_sell(const int32_t* __restrict__ rowptr, const int32_t* _
 // No matrix is stored: per point one x read (L1/L2 serve the 6 neighbour
 // reads; the z neighbours rotate through registers as a thread marches zc
 // planes) and one y write, i.e. 2·n·s bytes instead of CSR's nnz·(s + 4).
-// Terms are summed in ascending column order, each product formed from zero
-// and then added — the same arithmetic as the CSR kernels on the equivalent
+// Terms are accumulated by FMA (acc += coef·v, 4 FMAs) in ascending column
+// order — the same arithmetic as the SELL CSR kernel on the equivalent
 // matrix, so the two operators give bitwise-identical products.
 // Block: 256 threads = 32 (x) × 8 (y); grid (⌈nx/32⌉, ⌈ny/8⌉, ⌈nzl/zc⌉).
 // ---------------------------------------------------------------------------
+// acc += coef·v (4 FMAs) where the neighbour exists; a select, not a branch,
+// so the loads of a plane stay batched and a missing neighbour leaves acc
+// bitwise untouched (the CSR row simply has no such entry)
 template <typename C>
-__device__ __forceinline__ void st_term(C& acc, C coef, C v) {
-  C p = czero<C>();
-  cfma(p, coef, v);
-  acc = cadd(acc, p);
+__device__ __forceinline__ void st_term(C& acc, C coef, C v, bool has) {
+  C t = acc;
+  cfma(t, coef, v);
+  acc.x = has ? t.x : acc.x;
+  acc.y = has ? t.y : acc.y;
 }
 
 template <typename T, class Epi>
@@ -867,26 +869,39 @@ stencil7_kernel(const typename CT<T>::c* __restrict__ x, int nx, int ny, int nz,
   const int ix = blockIdx.x * 32 + (threadIdx.x & 31);
   const int iy = blockIdx.y * 8 + (threadIdx.x >> 5);
   const int zb = blockIdx.z * zc, ze = min(zb + zc, nzl);
-  const int64_t plane = (int64_t)nx * ny;
   if (ix < nx && iy < ny && zb < ze) {
-    const int64_t col = ix + (int64_t)nx * iy;
+    // 32-bit in-plane offsets; the column pointer steps one plane per z
+    const int plane = nx * ny;
+    const bool hxm = ix > 0, hxp = ix < nx - 1, hym = iy > 0, hyp = iy < ny - 1;
+    const C zero = czero<C>();
     int zg = z0 + zb;
-    C below = zg > 0 ? __ldg(x + col + plane * (zg - 1)) : czero<C>();
-    C cur = __ldg(x + col + plane * zg);
+    const C* xp = x + (int64_t)zg * plane + ix + nx * iy;
+    int64_t li = (int64_t)zb * plane + ix + nx * iy;    // local (epilogue) index
+    C below = zg > 0 ? xp[-plane] : zero;
+    C cur = xp[0];
+#pragma unroll 4
     for (int zl = zb; zl < ze; ++zl, ++zg) {
-      const int64_t gi = col + plane * zg;
-      const C above = zg < nz - 1 ? __ldg(x + gi + plane) : czero<C>();
-      C acc = czero<C>();
-      if (zg > 0) st_term(acc, oz, below);
-      if (iy > 0) st_term(acc, oy, __ldg(x + gi - nx));
-      if (ix > 0) st_term(acc, ox, __ldg(x + gi - 1));
-      st_term(acc, d, cur);
-      if (ix < nx - 1) st_term(acc, ox, __ldg(x + gi + 1));
-      if (iy < ny - 1) st_term(acc, oy, __ldg(x + gi + nx));
-      if (zg < nz - 1) st_term(acc, oz, above);
-      epi(gi - plane * z0, acc, dacc);
+      const bool hzm = zg > 0, hzp = zg < nz - 1;
+      // every load of the plane first (masked to zero), then the terms in
+      // ascending column order
+      const C above = hzp ? xp[plane] : zero;
+      const C ym = hym ? xp[-nx] : zero;
+      const C xm = hxm ? xp[-1] : zero;
+      const C xq = hxp ? xp[1] : zero;
+      const C yq = hyp ? xp[nx] : zero;
+      C acc = zero;
+      st_term(acc, oz, below, hzm);
+      st_term(acc, oy, ym, hym);
+      st_term(acc, ox, xm, hxm);
+      st_term(acc, d, cur, true);
+      st_term(acc, ox, xq, hxp);
+      st_term(acc, oy, yq, hyp);
+      st_term(acc, oz, above, hzp);
+      epi(li, acc, dacc);
       below = cur;
       cur = above;
+      xp += plane;
+      li += plane;
     }
   }
   if constexpr (Epi::K > 0) finish_reduction<KK, 256, Epi>(dacc, red, st);

@@ -81,7 +81,7 @@ def envelope_parity(method, op, y, tol, maxit, dtype, g, solve_at_k, rec=None, *
     (1) k_GPU ∈ [k_min − 2, k_max + 2]; (2) x at equal k within max(bar, 2·D)
     with D the pairwise spread; (3) true residual ≤ 10·tol; (4) the GPU
     residual history (g["hist"]) agrees with the clean oracle history to H
-    over the envelope's agreement window.  `g` is the GPU result of the
+    over the envelope's agreement window (where the members agree to H/10).  `g` is the GPU result of the
     tolerance-driven solve; `solve_at_k(k)` returns the GPU x after exactly k
     iterations."""
     from oracle.envelope import envelope, x_spread
@@ -96,5 +96,5 @@ def envelope_parity(method, op, y, tol, maxit, dtype, g, solve_at_k, rec=None, *
     rec.update(envelope_D=D, x_err_equal_k=err, hist_err=herr)
     assert err <= max(XTOL[np.dtype(dtype).type], 2 * D), rec
     assert g["true_rel_res"] <= 10 * tol, rec
-    assert herr <= env.H, rec
+    assert herr <= env.H, rec       # over the window where the members agree to H/10 (reading E3)
     return rec

@@ -10,7 +10,8 @@ library has for this problem must land inside it:
 
   (1) iteration count in [k_min − 2, k_max + 2];
   (4) residual history equal to the clean oracle history to H = 1e-8 over the
-      envelope's agreement window;
+      envelope's agreement window (the members agree to H/10 there;
+      oracle/envelope.py, reading E3);
   (3) true residual ≤ 10·tol, recomputed here by the oracle's own CSR product;
   (2) x after exactly k iterations within max(1e-9, 2·D(k)) of the clean
       oracle iterate, for the k at which the golden file records D(k) (the
@@ -25,6 +26,7 @@ import pytest
 
 import oracle
 from oracle import CsrOp
+from oracle.envelope import window_from_spread, history_error, WINDOW_FACTOR
 from workloads import helmholtz_csr, helmholtz_rhs, helmholtz_coeffs
 from tests._gpu import Csr, relerr
 from tests.test_gpu_next import Stencil
@@ -79,25 +81,25 @@ def test_cfg5_full_size_envelope(problem, method, kind, env, monkeypatch):
     with _handle(kind, rp, ci, v) as h:
         g = h.solve(method, y, gold["tol"], gold["maxit"])
         xk = {int(k): h.solve(method, y, 0.0, int(k))["x"] for k in e["D"]}
-    rec = dict(test="cfg5-full-envelope", op=kind, env=env, method=method, k_gpu=g["iterations"],
-               envelope_k=[e["k_min"], e["k_max"]], window=e["window"])
-    assert g["status"] == "CONVERGED", rec
-    # (1) iteration count
-    assert e["k_min"] - 2 <= g["iterations"] <= e["k_max"] + 2, rec
-    # (4) history over the agreement window
-    hc = np.asarray(e["hist_clean"])
-    K = min(e["window"], len(g["hist"]) - 1)
-    herr = float(np.max(np.abs(g["hist"][:K + 1] - hc[:K + 1]) / hc[:K + 1])) if K >= 0 else 0.0
-    rec["hist_err"] = herr
-    assert herr <= gold["H"], rec
+    rec = dict(test="cfg5-full-envelope", op=kind, env=env, method=method, status=g["status"],
+               k_gpu=g["iterations"], envelope_k=[e["k_min"], e["k_max"]], seeds=e.get("seeds", 8))
+    # (4) history over the agreement window (members agree to H/10, reading E3)
+    win = window_from_spread(e["hist_spread"], gold["H"] * WINDOW_FACTOR)
+    rec["window"] = win
+    rec["hist_err"] = history_error(g["hist"], e["hist_clean"], win)
     # (3) true residual by the oracle's CSR product
     tr = np.linalg.norm(y - op.apply(g["x"])) / np.linalg.norm(y)
     rec["true_rel_res"] = tr
-    assert tr <= 10 * gold["tol"], rec
-    assert abs(tr - g["true_rel_res"]) <= 1e-3 * tr + 1e-15, rec
     # (2) x at equal k
+    xerr = {}
     for k, D in e["D"].items():
-        err = relerr(xk[int(k)], _oracle_x(op, y, method, int(k)))
-        rec[f"x_err_k{k}"] = err
-        assert err <= max(1e-9, 2 * D), rec
-    _record(**rec)
+        xerr[k] = relerr(xk[int(k)], _oracle_x(op, y, method, int(k)))
+        rec[f"x_err_k{k}"] = xerr[k]
+    _record(**rec)                     # recorded before the verdict
+    assert g["status"] == "CONVERGED", rec
+    assert e["k_min"] - 2 <= g["iterations"] <= e["k_max"] + 2, rec           # (1)
+    assert rec["hist_err"] <= gold["H"], rec                                     # (4)
+    assert tr <= 10 * gold["tol"], rec                                           # (3)
+    assert abs(tr - g["true_rel_res"]) <= 1e-3 * tr + 1e-15, rec
+    for k, D in e["D"].items():                                                  # (2)
+        assert xerr[k] <= max(1e-9, 2 * D), rec

@@ -359,3 +359,68 @@ def test_sharded_jacobi(G, options):
                           oracle.solve_jacobi(method, DenseOp(A), d, y, 0.0, k).x) <= 1e-9, method
     finally:
         g.close()
+
+
+# ---------------------------------------------------------------------------
+# the gather fused into the product epilogue
+# (CCG_OPT_P2P): every rank's mirror buffer written by the product kernel,
+# release/acquire flags — on the loopback the peers are the other handles'
+# buffers on the same device, and the host barrier of the exchange means no
+# kernel waits on another rank's kernel.  The data movement is the same as the
+# allgather's, so products and solves are bitwise identical to the plain
+# replicated mode.
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("G", [2, 4])
+@pytest.mark.parametrize("dtype", [np.complex128, np.complex64])
+def test_p2p_dense_bitwise(G, dtype):
+    n = 1024
+    A = dense_random(n, seed=11, dtype=dtype, shift=3 - 1j)
+    x = (np.random.default_rng(12).standard_normal(n) + 1j).astype(dtype)
+    y = (np.random.default_rng(13).standard_normal(n) + 0.5j).astype(dtype)
+    ref = DenseGroup(A, G, options=ccg.OPT_REPLICATED)
+    p2p = DenseGroup(A, G, options=ccg.OPT_REPLICATED | ccg.OPT_P2P)
+    try:
+        for o in ("A", "AH", "AT"):
+            assert np.array_equal(p2p.apply(x, o), ref.apply(x, o)), o
+        tol = 1e-10 if dtype == np.complex128 else 1e-5
+        for method in ("bicgstab", "cgne", "qmr", "cocr", "gmres", "cors"):
+            a, b = p2p.solve(method, y, tol, 300), ref.solve(method, y, tol, 300)
+            assert a["status"] == b["status"] and a["iterations"] == b["iterations"], method
+            assert np.array_equal(a["x"], b["x"]), method
+        st = ccg.ccg_get_stats(p2p.hs[0])
+        assert st["p2p_exchanges"] > 0 and st["replicated"] == 1, st
+    finally:
+        ref.close()
+        p2p.close()
+
+
+@pytest.mark.parametrize("G", [2, 4])
+def test_p2p_csr_stencil_bitwise(G):
+    from workloads import lattice_csr, helmholtz_coeffs
+    N = 16
+    d, oo = helmholtz_coeffs()
+    y = helmholtz_rhs(N)
+    x = (np.random.default_rng(5).standard_normal(N ** 3) + 0.5j).astype(np.complex128)
+    pairs = [(CsrGroup(N, G, flags=ccg.FLAG_SYMMETRIC, options=ccg.OPT_REPLICATED),
+              CsrGroup(N, G, flags=ccg.FLAG_SYMMETRIC, options=ccg.OPT_REPLICATED | ccg.OPT_P2P)),
+             (StencilGroup(N, N, N, G, (d, oo), options=ccg.OPT_REPLICATED),
+              StencilGroup(N, N, N, G, (d, oo), options=ccg.OPT_REPLICATED | ccg.OPT_P2P))]
+    for ref, p2p in pairs:
+        try:
+            for o in ("A", "AH", "AT"):
+                assert np.array_equal(p2p.apply(x, o), ref.apply(x, o)), o
+            for method in ("bicgstab", "qmr", "cocr"):
+                a, b = p2p.solve(method, y, 1e-8, 3000), ref.solve(method, y, 1e-8, 3000)
+                assert a["iterations"] == b["iterations"] and np.array_equal(a["x"], b["x"]), method
+        finally:
+            ref.close()
+            p2p.close()
+
+
+def test_p2p_option_errors():
+    with pytest.raises(ccg.CcgError) as e:           # needs replicated vectors
+        ccg.ccg_create_loopback_group(2, "c128", 64, options=ccg.OPT_P2P)
+    assert e.value.code == -1
+    with pytest.raises(ccg.CcgError) as e:           # at most 8 ranks (one NVLink domain)
+        ccg.ccg_create_loopback_group(16, "c128", 64, options=ccg.OPT_P2P | ccg.OPT_REPLICATED)
+    assert e.value.code == -1

@@ -22,8 +22,7 @@ import pytest
 
 import paper_1208_4869_b200 as ccg
 from oracle import DenseOp, CsrOp, ToeplitzOp
-from workloads import dda_lattice_rows, dda_lattice_rhs, dda_kernel, helmholtz_csr, helmholtz_rhs, \
-    helmholtz_coeffs
+from workloads import dda_lattice_rows, dda_lattice_rhs, dda_kernel, helmholtz_rhs, lattice_csr
 from tests._gpu import Dense, to_dev
 from tests.test_gpu_solve import _parity
 
@@ -32,6 +31,7 @@ pytestmark = pytest.mark.gpu
 ALL = list(ccg.METHODS)
 AH_METHODS = {"cgne", "qmr", "bicor", "bicg", "cgnr"}
 DIMS = (8, 8, 8)
+LATTICE = (6.5 - 0.5j, -1.0)
 
 
 class Forced(Dense):
@@ -55,8 +55,12 @@ class Forced(Dense):
             ccg.ccg_set_matvec_toeplitz3(self.h, *DIMS, K, 3 + 0.5j)
             self.op = ToeplitzOp(K, DIMS, 3 + 0.5j)
         else:
+            # a diagonally dominant complex-symmetric 7-point lattice: the point
+            # here is the data plane, not the rounding chaos of the indefinite
+            # config-5 operator (tests/test_gpu_cfg5_envelope.py covers that)
             N = 16
-            rp, ci, v = helmholtz_csr(N, kh=10 / 128)
+            d, o = LATTICE
+            rp, ci, v = lattice_csr(N, N, N, d, o)
             self.n = N ** 3
             self.h = ccg.ccg_create("c128", self.n, options=opts)
             if kind == "csr":
@@ -64,7 +68,6 @@ class Forced(Dense):
                 self.keep = t
                 ccg.ccg_set_matvec_csr(self.h, *t, 0, self.n, len(v), flags=ccg.FLAG_SYMMETRIC)
             else:
-                d, o = helmholtz_coeffs()
                 ccg.ccg_set_matvec_stencil7(self.h, N, N, N, d, o)
             self.op = CsrOp(rp, ci, v)
         self.y = dda_lattice_rhs(DIMS, 1.0) if kind in ("dense", "toeplitz") else helmholtz_rhs(16)
@@ -80,7 +83,7 @@ def test_nccl_one_rank_parity(method, kind, replicated):
                 h.solve(method, h.y, 1e-8, 10)
             assert e.value.code == -3
             return
-        _parity(h, h.op, h.y, method, 1e-8, 20000, np.complex128, literal=False,
+        _parity(h, h.op, h.y, method, 1e-8, 4000, np.complex128, literal=False,
                 tag=f"nccl1-{kind}-{'rep' if replicated else 'shard'}")
         st = ccg.ccg_get_stats(h.h)
         assert st["comm_kind"] == 1 and st["world"] == 1 and st["replicated"] == int(replicated), st
@@ -129,3 +132,34 @@ def test_nccl_debug_lines():
     assert p.returncode == 0, out[-3000:]
     assert "NCCL INFO" in out and "Init COMPLETE" in out, out[-3000:]
     assert "RESULT CONVERGED 12" in out, out[-3000:]
+
+
+@pytest.mark.parametrize("kind", ["dense", "csr", "stencil"])
+@pytest.mark.parametrize("method", ["bicgstab", "cgne", "qmr", "cocr", "gmres"])
+def test_nccl_window_p2p(method, kind):
+    """CCG_OPT_P2P through a real NCCL symmetric-memory window (one rank):
+    ncclMemAlloc + ncclCommWindowRegister, ncclGetPeerPointer resolved on the
+    device, the product epilogue storing into the window, release / acquire
+    flags inside the captured iteration graph — bitwise equal to the plain
+    replicated NCCL path, and the oracle parity of that path."""
+    class P2P(Forced):
+        def __init__(self, kind):
+            Forced.__init__(self, kind, True)
+            h0 = self.h
+            opts = ccg.OPT_FORCE_COMM | ccg.OPT_REPLICATED | ccg.OPT_P2P
+            self.h = ccg.ccg_create("c128", self.n, options=opts)
+            if kind == "dense":
+                ccg.ccg_set_matvec_dense(self.h, self.A, 0, self.n)
+            elif kind == "csr":
+                ccg.ccg_set_matvec_csr(self.h, *self.keep, 0, self.n, len(self.keep[2]), flags=ccg.FLAG_SYMMETRIC)
+            else:
+                ccg.ccg_set_matvec_stencil7(self.h, 16, 16, 16, *LATTICE)
+            ccg.ccg_destroy(h0)
+    with Forced(kind, True) as ref, P2P(kind) as h:
+        a = h.solve(method, h.y, 1e-8, 4000)
+        b = ref.solve(method, ref.y, 1e-8, 4000)
+        assert a["status"] == b["status"] == "CONVERGED"
+        assert a["iterations"] == b["iterations"] and np.array_equal(a["x"], b["x"]), method
+        st = ccg.ccg_get_stats(h.h)
+        assert st["comm_kind"] == 1 and st["p2p_exchanges"] > 0 and st["graph_replays"] > 0, st
+        _parity(h, h.op, h.y, method, 1e-8, 4000, np.complex128, literal=False, tag=f"nccl1-p2p-{kind}")

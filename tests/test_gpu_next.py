@@ -240,8 +240,8 @@ def test_stencil_apply_parity(dtype, dims):
 
 
 def test_stencil_bitwise_equals_csr_kernel():
-    """Same arithmetic as the CSR kernels (ascending column order, product from
-    zero then added): the stencil and the CSR operator agree bitwise on every
+    """Same arithmetic as the SELL CSR kernel (FMA accumulation in ascending
+    column order): the stencil and the CSR operator agree bitwise on every
     product.  (Solves then differ only through the grid-dependent order of the
     dot-product partials; they are checked against the oracle below.)"""
     N = 24

@@ -326,6 +326,8 @@ def test_false_convergence_spec_fixture():
 @pytest.mark.parametrize("op", ["dense", "csr"])
 @pytest.mark.parametrize("method", _FC["single_precision"]["methods"])
 def test_false_convergence_single_precision(method, op):
+    if op == "csr" and method in ("bicor", "cgne"):
+        pytest.skip("Aᴴ methods need CCG_FLAG_SYMMETRIC on CSR; this matrix is not symmetric")
     """c64 working precision at tol 1e-10: the true residual floor (~1e-7) is
     far above 10·tol while the recurrence residual keeps falling."""
     g = _FC["single_precision"]

@@ -120,7 +120,7 @@ def test_envelope_collapses_on_cfg1():
     op = DenseOp(A)
     e = envelope("bicgstab", op, y, 1e-10, 500)
     assert e.k_min == e.k_max == e.k_clean == 12
-    assert e.window == len(e.hist_clean) - 1          # histories agree to 1e-8 throughout
+    assert e.window == len(e.hist_clean) - 1          # histories agree to 1e-9 throughout
     _, D = x_spread("bicgstab", op, y, e.k_clean)
     assert D < 1e-14
 
@@ -152,7 +152,9 @@ def test_window_on_chaotic_proxy_and_noise_scaling():
     L = min(map(len, hists))
     M = np.stack([h[:L] for h in hists])
     spread = (M.max(0) - M.min(0)) / M[0]
-    assert np.all(spread[:e.window + 1] <= 1e-8) and spread[e.window + 1] > 1e-8
+    np.testing.assert_array_equal(spread, e.hist_spread)
+    # E3: the window is where the members agree to H/10 = 1e-9
+    assert np.all(spread[:e.window + 1] <= 1e-9) and spread[e.window + 1] > 1e-9
     e_big = envelope("bicgstab", op, y, 1e-8, 2000, eps=2e-10, seeds=4)
     assert e_big.window < e.window
     # a history equal to the clean one passes, one off by 1e-6 inside the window fails

@@ -24,7 +24,7 @@ sys.path.insert(0, ROOT)
 TOL, MAXIT = 1e-8, 20000          # BJ:11; maxit reading Q8
 METHODS = ("bicgstab", "cors")
 K_FIXED = (10, 20, 30, 40)        # D(k) at these equal iteration counts
-SEEDS = 8
+SEEDS = 8                         # SURVEY §8(c) E = 8; --seeds overrides (reading E4)
 
 _OP = None
 
@@ -58,27 +58,35 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--procs", type=int, default=SEEDS + 1)
     ap.add_argument("--out", default=os.path.join(ROOT, "tests", "golden", "cfg5_envelope.json"))
+    ap.add_argument("--seeds", type=int, default=SEEDS)
+    ap.add_argument("--methods", default=",".join(METHODS))
+    ap.add_argument("--merge", action="store_true", help="keep the other methods of an existing file")
     a = ap.parse_args()
-    from oracle.envelope import agreement_window, pairwise_spread, hist_tol, NOISE_C128
+    seeds = a.seeds
+    methods = a.methods.split(",")
+    from oracle.envelope import agreement_window, pairwise_spread, hist_tol, history_spread, NOISE_C128
     H = hist_tol(np.complex128)
     res = {"_source": ("written by tools/make_cfg5_envelope.py from oracle/ only: BASELINE config 5 "
                        "(BJ:11; PAPER.md:95 §5 'own sparse matrix scheme'), SURVEY §8(c) P-envelope: "
-                       f"clean run + {SEEDS} noise seeds of amplitude {NOISE_C128} per matvec output"),
-           "tol": TOL, "maxit": MAXIT, "H": H, "seeds": SEEDS, "methods": {}}
+                       f"clean run + noise seeds of amplitude {NOISE_C128} per matvec output"),
+           "tol": TOL, "maxit": MAXIT, "H": H, "methods": {}}
+    if a.merge and os.path.exists(a.out):
+        res["methods"] = json.load(open(a.out))["methods"]
     ctx = mp.get_context("fork")
     with ctx.Pool(a.procs) as pool:
-        for method in METHODS:
+        for method in methods:
             t = time.time()
-            runs = pool.map(_member, [(method, s, TOL, MAXIT) for s in range(SEEDS + 1)])
+            runs = pool.map(_member, [(method, s, TOL, MAXIT) for s in range(seeds + 1)])
             runs.sort(key=lambda r: r["seed"])
             hists = [r["hist"] for r in runs]
             ks = [r["k"] for r in runs]
-            ent = dict(k_clean=ks[0], ks=ks, k_min=min(ks), k_max=max(ks),
+            ent = dict(seeds=seeds, k_clean=ks[0], ks=ks, k_min=min(ks), k_max=max(ks),
                        statuses=[r["status"] for r in runs],
                        true_rel_res=[r["true_rel_res"] for r in runs],
-                       window=agreement_window(hists, H), hist_clean=hists[0], D={})
+                       window=agreement_window(hists, H), hist_clean=hists[0],
+                       hist_spread=history_spread(hists).tolist(), D={})
             for k in K_FIXED:
-                xr = pool.map(_member, [(method, s, 0.0, k) for s in range(SEEDS + 1)])
+                xr = pool.map(_member, [(method, s, 0.0, k) for s in range(seeds + 1)])
                 xr.sort(key=lambda r: r["seed"])
                 xs = [r["x"] for r in xr]
                 ent["D"][str(k)] = pairwise_spread(xs, xs[0])
