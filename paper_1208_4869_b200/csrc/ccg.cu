@@ -137,6 +137,18 @@ static int choose_launch(ccg_ctx* c) {
     }
     nrb = std::min<int64_t>(nrb, std::max<int64_t>(1, c->mnloc / 8));
     c->split_nrb = (int)nrb;
+    const char* bf = getenv("CCG_BS_FUSE");
+    c->bs_fuse = bf ? atoi(bf) != 0 : 1;
+    const char* fu = getenv("CCG_SPLIT_FUSE");
+    c->split_fuse = fu ? atoi(fu) != 0 : 0;   // off: cfg3 1.3 % slower (last-CTA tail), cfg2 neutral
+    if (c->rb_ticket_cap < c->split_nrb) {
+      if (c->rb_ticket) cudaFree(c->rb_ticket);
+      c->rb_ticket = nullptr;
+      c->rb_ticket_cap = 0;
+      CK(c, cudaMalloc(&c->rb_ticket, sizeof(unsigned) * c->split_nrb));
+      CK(c, cudaMemsetAsync(c->rb_ticket, 0, sizeof(unsigned) * c->split_nrb, c->stream));
+      c->rb_ticket_cap = c->split_nrb;
+    }
     c->nstage2_grid =
         (int)std::max<int64_t>(1, std::min<int64_t>((c->mnloc + NT - 1) / NT, (int64_t)c->sm_count * 4));
     size_t need = c->split_strips > 1 ? (size_t)c->split_strips * c->mnloc * sizeof(C) : 0;
@@ -591,6 +603,15 @@ int ccg_set_matvec_dense(ccg_handle c, const void* A_local, int64_t row0, int64_
   c->flags = flags;
   c->vec_ok = (c->esz == 16) || (((uintptr_t)A_local % 16) == 0 && (lda % 2) == 0);
   {
+    // L2-resident rows (matvec.cuh): ~80 MB of A kept in the
+    // 126 MB L2 between the products of a solve; 0 when A is >> L2
+    const char* pe = getenv("CCG_L2_PIN_MB");
+    const double pin_bytes = (pe ? atof(pe) : 80.0) * 1e6;
+    const double abytes = (double)nloc * (double)c->n * (double)c->esz;
+    c->l2_pin = pin_bytes <= 0 || abytes < 32e6 ? 0      // small A stays in L2 without help
+                : abytes <= pin_bytes ? 64 : (int)floor(64.0 * pin_bytes / abytes);
+  }
+  {
     // small L2-resident systems: the whole loop in one cluster (cluster.cuh)
     const char* ce = getenv("CCG_CLUSTER");
     const char* cb = getenv("CCG_CLUSTER_MAXBYTES");
@@ -1040,6 +1061,11 @@ int ccg_apply(ccg_handle c, ccg_op op, const void* x_local, void* y_local) {
   if (c->opk == OPK_CALLBACK && !(c->cb_caps & (op == CCG_OP_A ? CCG_CB_A : op == CCG_OP_AH ? CCG_CB_AH : CCG_CB_AT)))
     FAIL(c, CCG_E_CAPABILITY, "the user callback does not provide this product");
   CK(c, cudaSetDevice(c->device));
+  struct PinGuard {
+    ccg_ctx* c;
+    ~PinGuard() { c->pin_on = false; }
+  } pin_guard{c};
+  c->pin_on = c->opk == OPK_DENSE && c->l2_pin > 0;
   c->launches = 0;
   c->ms_a = c->ms_ah = 0;
   c->n_a = c->n_ah = 0;
@@ -1069,6 +1095,11 @@ int ccg_solve(ccg_handle c, ccg_method method, const void* x0_local, const void*
   if (c->opk == OPK_CALLBACK && (!(c->cb_caps & CCG_CB_A) || (needs_ah(method) && !(c->cb_caps & CCG_CB_AH))))
     FAIL(c, CCG_E_CAPABILITY, "the user callback does not provide the products this method needs");
   CK(c, cudaSetDevice(c->device));
+  struct PinGuard {
+    ccg_ctx* c;
+    ~PinGuard() { c->pin_on = false; }
+  } pin_guard{c};
+  c->pin_on = c->opk == OPK_DENSE && c->l2_pin > 0;
   c->launches = 0;
   c->ms_a = c->ms_ah = 0;
   c->n_a = c->n_ah = 0;
@@ -1139,6 +1170,17 @@ int ccg_solve(ccg_handle c, ccg_method method, const void* x0_local, const void*
     c->jac_active = false;
     rc = c->dtype == CCG_C64 ? Engine<float>::jac_out(c) : Engine<double>::jac_out(c);
     if (rc) return rc;
+  }
+  if (c->pin_on) {   // the pinned rows of A back to normal L2 priority
+    const int g = c->sm_count * 8;
+    if (c->dtype == CCG_C64)
+      l2_demote<float><<<g, 256, 0, c->stream>>>(reinterpret_cast<const float2*>(c->A), c->lda, c->mnloc, c->n, c->l2_pin);
+    else
+      l2_demote<double><<<g, 256, 0, c->stream>>>(reinterpret_cast<const double2*>(c->A), c->lda, c->mnloc, c->n,
+                                                  c->l2_pin);
+    CK(c, cudaGetLastError());
+    c->launches++;
+    c->pin_on = false;
   }
   CK(c, cudaMemcpyAsync(c->st_host, c->st, sizeof(State), cudaMemcpyDeviceToHost, c->stream));
   TRY(vec_out(c, x_local_out, c->loc[0]));
@@ -1230,6 +1272,7 @@ int ccg_destroy(ccg_handle c) {
     c->mirror = nullptr;
   }
   if (c->p2p_ctr) cudaFree(c->p2p_ctr);
+  if (c->rb_ticket) cudaFree(c->rb_ticket);
   delete c->comm;
   c->comm = nullptr;
   for (int i = 0; i < NLOCAL; ++i) if (c->loc[i]) cudaFree(c->loc[i]);

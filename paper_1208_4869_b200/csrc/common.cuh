@@ -237,12 +237,14 @@ __device__ __forceinline__ unsigned block_linear_id() {
 }
 __device__ __forceinline__ unsigned grid_blocks() { return gridDim.x * gridDim.y * gridDim.z; }
 
+// the CTA's K partial sums go to slot `bid` of `nb` (every slot written once
+// per launch); the CTA that arrives last sums the slots in slot order
 template <int K, int NT, class Fin>
-__device__ __forceinline__ void finish_reduction(double2 (&v)[K], const Red& red, State* st) {
+__device__ __forceinline__ void finish_reduction_at(double2 (&v)[K], const Red& red, State* st, unsigned bid,
+                                                    unsigned nb) {
   __shared__ double2 sm[(NT / 32) * K];
   __shared__ int am_last;
   block_sum<K, NT>(v, sm);
-  const unsigned bid = block_linear_id(), nb = grid_blocks();
   if (threadIdx.x == 0) {
 #pragma unroll
     for (int k = 0; k < K; ++k) red.part[(size_t)bid * K + k] = v[k];
@@ -273,6 +275,11 @@ __device__ __forceinline__ void finish_reduction(double2 (&v)[K], const Red& red
       for (int k = 0; k < K; ++k) red.rank_sum[k] = acc[k];
     }
   }
+}
+
+template <int K, int NT, class Fin>
+__device__ __forceinline__ void finish_reduction(double2 (&v)[K], const Red& red, State* st) {
+  finish_reduction_at<K, NT, Fin>(v, red, st, block_linear_id(), grid_blocks());
 }
 
 }  // namespace ccg

@@ -129,9 +129,15 @@ struct ccg_ctx {
   int bulk_grid = 0;
   int gemv_mode = 0;      // GEMV_SPLIT (default) | GEMV_BULK | GEMV_ROWS (env CCG_GEMV)
   int split_W = 0, split_strips = 1, split_nrb = 1, nstage2_grid = 1, split_ur = 8;
+  int bs_fuse = 1;        // BiCGSTAB P/S passes folded into the products (Engine::in_fuse_ok; CCG_BS_FUSE)
+  int split_fuse = 0;     // several strips: strip sum + epilogue by the last CTA of each row block (CCG_SPLIT_FUSE)
+  unsigned* rb_ticket = nullptr;   // [split_nrb] arrival tickets (zero between launches)
+  int rb_ticket_cap = 0;
   bool cols_ok = false;   // column-owner GEMV usable (vectorised layout, n % V == 0)
   int cols_strips = 1, cols_S = 1, dual_S = 1, cols_rg = 1;
   bool qmr_dual = true;   // QMR: A·p and Aᴴ·q in one pass over A (env CCG_QMR_DUAL=0 disables)
+  int l2_pin = 0;         // rows ((i>>3)&63) < l2_pin of A are kept L2-resident during a solve (CCG_L2_PIN_MB)
+  bool pin_on = false;    // inside ccg_solve (dense operator)
   void* npart = nullptr;  // [strips][nloc] partial row sums of the split / column-owner GEMV
   size_t npart_bytes = 0;
   // workspace
@@ -326,6 +332,8 @@ struct Engine {
   static C* Fs(ccg_ctx* c, int i) { return reinterpret_cast<C*>(c->full[i]) + c->row0; }  // own slice
 
   static CommType ndt() { return sizeof(T) == 4 ? CT_F32 : CT_F64; }
+  // L2-resident rows of A (matvec.cuh): only inside ccg_solve
+  static int pin(const ccg_ctx* c) { return c->pin_on ? c->l2_pin : 0; }
 
   // -------------------- collectives --------------------
   static int allgather(ccg_ctx* c, int fi) {
@@ -541,6 +549,41 @@ struct Engine {
     return matvec_rows(c, xfull, epi, gate);
   }
 
+  // the input transforms of matvec_a_in apply: single GPU, dense split GEMV
+  // with several strips and the strip sum in its own kernel (the epilogue that
+  // rewrites the transformed vectors runs after every CTA has staged them)
+  static bool in_fuse_ok(const ccg_ctx* c) {
+    return c->bs_fuse && c->opk == OPK_DENSE && c->gemv_mode == GEMV_SPLIT && c->split_strips > 1 &&
+           !c->split_fuse && !c->dist && !c->jac_active;
+  }
+
+  // y = A·x with x_j = xin(j) formed while the split GEMV stages its strips
+  template <class XIn, class Epi>
+  static int matvec_a_in(ccg_ctx* c, XIn xin, Epi epi, const int* gate) {
+    const C* A = reinterpret_cast<const C*>(c->A);
+    C* part = reinterpret_cast<C*>(c->npart);
+    dim3 g(c->split_strips, c->split_nrb);
+    const size_t smem = (size_t)c->split_W * sizeof(C);
+    Store<T> none{nullptr};
+    tev_begin(c, 0);
+    if (c->vec_ok)
+      launch_k(c, gemv_n_split<T, NT, SUR, true, false, Store<T>, XIn>, g, NT, smem, c->stream, A, c->lda,
+               static_cast<const C*>(nullptr), c->n, c->mnloc, c->split_W, part, none, make_red(c), c->st, gate, pin(c),
+               c->rb_ticket, xin);
+    else
+      launch_k(c, gemv_n_split<T, NT, SUR, false, false, Store<T>, XIn>, g, NT, smem, c->stream, A, c->lda,
+               static_cast<const C*>(nullptr), c->n, c->mnloc, c->split_W, part, none, make_red(c), c->st, gate, pin(c),
+               c->rb_ticket, xin);
+    c->launches++;
+    CK(c, cudaGetLastError());
+    launch_k(c, gemv_h_stage2<T, NT, Epi>, c->nstage2_grid, NT, 0, c->stream, part, c->split_strips, c->mnloc, 0,
+             c->mnloc, epi, make_red(c), c->st, gate);
+    c->launches++;
+    tev_end(c);
+    CK(c, cudaGetLastError());
+    return CCG_OK;
+  }
+
   // this rank's rows of A·x (all operators), epilogue per row
   template <class Epi>
   static int matvec_rows(ccg_ctx* c, const C* xfull, Epi epi, const int* gate) {
@@ -554,27 +597,27 @@ struct Engine {
       C* part = reinterpret_cast<C*>(c->npart);
       dim3 g(c->split_strips, c->split_nrb);
       const size_t smem = (size_t)c->split_W * sizeof(C);
-      if (c->split_strips == 1) {
+      if (c->split_strips == 1 || c->split_fuse) {   // epilogue in the GEMV (last strip CTA per row block)
         if (c->vec_ok)
           launch_k(c, gemv_n_split<T, NT, SUR, true, true, Epi>, g, NT, smem, c->stream, 
-              A, c->lda, xfull, c->n, c->mnloc, c->split_W, part, epi, make_red(c), c->st, gate);
+              A, c->lda, xfull, c->n, c->mnloc, c->split_W, part, epi, make_red(c), c->st, gate, pin(c), c->rb_ticket, XLoad<T>{});
         else
           launch_k(c, gemv_n_split<T, NT, SUR, false, true, Epi>, g, NT, smem, c->stream, 
-              A, c->lda, xfull, c->n, c->mnloc, c->split_W, part, epi, make_red(c), c->st, gate);
+              A, c->lda, xfull, c->n, c->mnloc, c->split_W, part, epi, make_red(c), c->st, gate, pin(c), c->rb_ticket, XLoad<T>{});
       } else {
         Store<T> none{nullptr};
         if (c->vec_ok && c->split_ur == 16)
           launch_k(c, gemv_n_split<T, NT, 16, true, false, Store<T>>, g, NT, smem, c->stream, 
-              A, c->lda, xfull, c->n, c->mnloc, c->split_W, part, none, make_red(c), c->st, gate);
+              A, c->lda, xfull, c->n, c->mnloc, c->split_W, part, none, make_red(c), c->st, gate, pin(c), c->rb_ticket, XLoad<T>{});
         else if (c->vec_ok && c->split_ur == 4)
           launch_k(c, gemv_n_split<T, NT, 4, true, false, Store<T>>, g, NT, smem, c->stream, 
-              A, c->lda, xfull, c->n, c->mnloc, c->split_W, part, none, make_red(c), c->st, gate);
+              A, c->lda, xfull, c->n, c->mnloc, c->split_W, part, none, make_red(c), c->st, gate, pin(c), c->rb_ticket, XLoad<T>{});
         else if (c->vec_ok)
           launch_k(c, gemv_n_split<T, NT, SUR, true, false, Store<T>>, g, NT, smem, c->stream, 
-              A, c->lda, xfull, c->n, c->mnloc, c->split_W, part, none, make_red(c), c->st, gate);
+              A, c->lda, xfull, c->n, c->mnloc, c->split_W, part, none, make_red(c), c->st, gate, pin(c), c->rb_ticket, XLoad<T>{});
         else
           launch_k(c, gemv_n_split<T, NT, SUR, false, false, Store<T>>, g, NT, smem, c->stream, 
-              A, c->lda, xfull, c->n, c->mnloc, c->split_W, part, none, make_red(c), c->st, gate);
+              A, c->lda, xfull, c->n, c->mnloc, c->split_W, part, none, make_red(c), c->st, gate, pin(c), c->rb_ticket, XLoad<T>{});
         c->launches++;
         CK(c, cudaGetLastError());
         launch_k(c, gemv_h_stage2<T, NT, Epi>, c->nstage2_grid, NT, 0, c->stream, part, c->split_strips, c->mnloc, 0,
@@ -584,10 +627,10 @@ struct Engine {
       C* part = reinterpret_cast<C*>(c->npart);
       if (c->cols_rg == 4)
         launch_k(c, gemv_cols<T, NT, true, false, false, 4>, dim3(c->cols_strips, c->cols_S), NT, 0, c->stream, 
-            reinterpret_cast<const C*>(c->A), c->lda, xfull, nullptr, c->mnloc, c->n, part, nullptr, gate);
+            reinterpret_cast<const C*>(c->A), c->lda, xfull, nullptr, c->mnloc, c->n, part, nullptr, gate, pin(c));
       else
         launch_k(c, gemv_cols<T, NT, true, false, false, 1>, dim3(c->cols_strips, c->cols_S), NT, 0, c->stream, 
-            reinterpret_cast<const C*>(c->A), c->lda, xfull, nullptr, c->mnloc, c->n, part, nullptr, gate);
+            reinterpret_cast<const C*>(c->A), c->lda, xfull, nullptr, c->mnloc, c->n, part, nullptr, gate, pin(c));
       c->launches++;
       CK(c, cudaGetLastError());
       launch_k(c, gemv_h_stage2<T, NT, Epi>, c->nstage2_grid, NT, 0, c->stream, part, c->cols_strips, c->mnloc, 0, c->mnloc,
@@ -688,14 +731,14 @@ struct Engine {
     tev_begin(c, 1);
     if (c->vec_ok) {
       if (conj)
-        launch_k(c, gemv_h_stage1<T, true, NT, UR, true>, g1, NT, 0, c->stream, A, c->lda, xr, c->mnloc, c->n, part, gate);
+        launch_k(c, gemv_h_stage1<T, true, NT, UR, true>, g1, NT, 0, c->stream, A, c->lda, xr, c->mnloc, c->n, part, gate, pin(c));
       else
-        launch_k(c, gemv_h_stage1<T, false, NT, UR, true>, g1, NT, 0, c->stream, A, c->lda, xr, c->mnloc, c->n, part, gate);
+        launch_k(c, gemv_h_stage1<T, false, NT, UR, true>, g1, NT, 0, c->stream, A, c->lda, xr, c->mnloc, c->n, part, gate, pin(c));
     } else {
       if (conj)
-        launch_k(c, gemv_h_stage1<T, true, NT, UR, false>, g1, NT, 0, c->stream, A, c->lda, xr, c->mnloc, c->n, part, gate);
+        launch_k(c, gemv_h_stage1<T, true, NT, UR, false>, g1, NT, 0, c->stream, A, c->lda, xr, c->mnloc, c->n, part, gate, pin(c));
       else
-        launch_k(c, gemv_h_stage1<T, false, NT, UR, false>, g1, NT, 0, c->stream, A, c->lda, xr, c->mnloc, c->n, part, gate);
+        launch_k(c, gemv_h_stage1<T, false, NT, UR, false>, g1, NT, 0, c->stream, A, c->lda, xr, c->mnloc, c->n, part, gate, pin(c));
     }
     c->launches++;
     CK(c, cudaGetLastError());
@@ -748,7 +791,7 @@ struct Engine {
     C* hp = reinterpret_cast<C*>(c->hpart);
     tev_begin(c, 0);
     launch_k(c, gemv_cols<T, NT, true, true, true>, dim3(c->cols_strips, c->dual_S), NT, 0, c->stream, 
-        A, c->lda, pfull, qloc, c->nloc, c->n, np, hp, gate);
+        A, c->lda, pfull, qloc, c->nloc, c->n, np, hp, gate, 0);   // no L2 pinning: measured slower
     c->launches++;
     CK(c, cudaGetLastError());
     launch_k(c, gemv_h_stage2<T, NT, EpiA>, c->nstage2_grid, NT, 0, c->stream, np, c->cols_strips, c->nloc, 0, c->nloc, ea,

@@ -20,6 +20,75 @@ __device__ __forceinline__ float4 ld_stream(const float4* p) { return __ldcs(p);
 __device__ __forceinline__ double2 ld_stream(const double2* p) { return __ldcs(p); }
 __device__ __forceinline__ float2 ld_stream(const float2* p) { return __ldcs(p); }
 
+// ---------------------------------------------------------------------------
+// L2 residency of part of A (DESIGN.md §4 "L2-resident rows"): a matrix a
+// little larger than the 126 MB L2 (config 2: 268 MB) is re-read every
+// product, so during a solve the rows with ((i >> 3) & 63) < pin (pin/64 of
+// A, sized to ~80 MB) are loaded with an L2 evict_last policy and stay
+// resident from one product to the next, the other rows evict-first.  The
+// predicate takes groups of 8 consecutive rows, so every CTA's row range is
+// pinned in the same proportion (no CTA waits on HBM while others hit L2).
+// l2_demote() returns the lines to normal priority when the solve ends.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t l2_policy_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t l2_policy_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ bool row_pinned(int64_t i, int pin) { return (int)((i >> 3) & 63) < pin; }
+__device__ __forceinline__ float4 ld_hint(const float4* p, uint64_t pol) {
+  float4 v;
+  asm("ld.global.L1::no_allocate.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ double2 ld_hint(const double2* p, uint64_t pol) {
+  double2 v;
+  asm("ld.global.L1::no_allocate.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
+               : "=d"(v.x), "=d"(v.y) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ float2 ld_hint(const float2* p, uint64_t pol) {
+  float2 v;
+  asm("ld.global.L1::no_allocate.L2::cache_hint.v2.f32 {%0, %1}, [%2], %3;"
+               : "=f"(v.x), "=f"(v.y) : "l"(p), "l"(pol));
+  return v;
+}
+// A-load functors: LdA streams (evict-first); LdPin picks the policy per row
+struct LdA {
+  template <class LV>
+  __device__ __forceinline__ LV operator()(const LV* p, int64_t) const { return ld_stream(p); }
+};
+struct LdPin {
+  uint64_t keep, drop;
+  int pin;
+  template <class LV>
+  __device__ __forceinline__ LV operator()(const LV* p, int64_t row) const {
+    return ld_hint(p, row_pinned(row, pin) ? keep : drop);
+  }
+};
+__device__ __forceinline__ LdPin make_ldpin(int pin) { return LdPin{l2_policy_last(), l2_policy_first(), pin}; }
+
+// demote the pinned rows of A to normal L2 priority (one thread per 128-B line)
+template <typename T>
+__global__ void l2_demote(const typename CT<T>::c* A, int64_t lda, int64_t nrows, int64_t n, int pin) {
+  using C = typename CT<T>::c;
+  const int64_t lines = (n * (int64_t)sizeof(C) + 127) / 128 + 1;   // +1: row starts need not be 128-B aligned
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nrows * lines;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = k / lines;
+    if (!row_pinned(i, pin)) continue;
+    const uintptr_t row = reinterpret_cast<uintptr_t>(A + i * lda) & ~(uintptr_t)127;
+    const char* p = reinterpret_cast<const char*>(row) + (k % lines) * 128;
+    asm volatile("applypriority.global.L2::evict_normal [%0], 128;" ::"l"(p));
+  }
+}
+
 // unpack a 16-byte vector into V complex values
 __device__ __forceinline__ void unpack(const float4& v, float2 (&c)[2]) {
   c[0] = make_float2(v.x, v.y); c[1] = make_float2(v.z, v.w);
@@ -244,14 +313,29 @@ gemv_n_bulk(const typename CT<T>::c* __restrict__ A, int64_t lda,
 // 16-byte loads in flight per lane, ~40 registers => 8 CTAs/SM, >200 KB of
 // loads in flight per SM) and warp-reduces each row.  With one strip the row
 // sum is final and the epilogue runs here (FUSED); otherwise the partial
-// goes to part[c][i] and gemv_h_stage2 sums the strips in order (fixed
-// order => deterministic) and runs the epilogue.
+// goes to part[c][i] and either gemv_h_stage2 sums the strips in order (fixed
+// order => deterministic) and runs the epilogue, or (FUSED, several strips)
+// the last of the row block's strip CTAs to finish — an arrival ticket per
+// row block, rbt[b] — sums the strips of its rows in the same order as
+// gemv_h_stage2 (bitwise the same product), runs the epilogue and puts the
+// phase partials in reduction slot b: no second launch per product.
 // ---------------------------------------------------------------------------
-template <typename T, int NT, int UR, bool VEC, bool FUSED, class Epi>
+// x staging: XLoad reads the input vector; a method's input transform (e.g.
+// BiCGSTAB's p = r + β(p − ωv), methods.cuh BsPIn) forms each staged element
+// from other vectors instead, so that vector pass is not a launch of its own
+template <typename T>
+struct XLoad {
+  using C = typename CT<T>::c;
+  __device__ void load(const State*) {}
+  __device__ C operator()(const C* x, int64_t j) const { return x[j]; }
+};
+
+template <typename T, int NT, int UR, bool VEC, bool FUSED, class Epi, class XIn = XLoad<T>>
 __global__ void __launch_bounds__(NT)
 gemv_n_split(const typename CT<T>::c* __restrict__ A, int64_t lda,
              const typename CT<T>::c* __restrict__ x, int64_t n, int64_t nrows, int W,
-             typename CT<T>::c* __restrict__ part, Epi epi, Red red, State* st, const int* gate) {
+             typename CT<T>::c* __restrict__ part, Epi epi, Red red, State* st, const int* gate, int pin,
+             unsigned* rbt, XIn xin) {
   using C = typename CT<T>::c;
   constexpr int V = VEC ? CT<T>::V : 1;
   using LV = typename std::conditional<VEC, typename CT<T>::v, C>::type;
@@ -263,7 +347,8 @@ gemv_n_split(const typename CT<T>::c* __restrict__ A, int64_t lda,
   const int strip = blockIdx.x, nrb = gridDim.y, b = blockIdx.y;
   const int64_t c0 = (int64_t)strip * W;
   const int cw = (int)min((int64_t)W, n - c0);
-  for (int t = threadIdx.x; t < cw; t += NT) xs[t] = x[c0 + t];
+  xin.load(st);
+  for (int t = threadIdx.x; t < cw; t += NT) xs[t] = xin(x, c0 + t);
   __syncthreads();
   const int64_t i0 = nrows * b / nrb, i1 = nrows * (b + 1) / nrb;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -272,6 +357,7 @@ gemv_n_split(const typename CT<T>::c* __restrict__ A, int64_t lda,
   double2 dacc[KK];
 #pragma unroll
   for (int k = 0; k < KK; ++k) dacc[k] = make_double2(0.0, 0.0);
+  auto rows = [&](auto ld) {
   for (int64_t i = i0 + warp; i < i1; i += NT / 32) {
     const LV* a = reinterpret_cast<const LV*>(A + i * lda + c0);
     C acc = czero<C>();
@@ -279,7 +365,7 @@ gemv_n_split(const typename CT<T>::c* __restrict__ A, int64_t lda,
     for (; k + 32 * (UR - 1) < nvec; k += 32 * UR) {
       LV av[UR];
 #pragma unroll
-      for (int u = 0; u < UR; ++u) av[u] = ld_stream(a + k + 32 * u);
+      for (int u = 0; u < UR; ++u) av[u] = ld(a + k + 32 * u, i);
 #pragma unroll
       for (int u = 0; u < UR; ++u) {
         C ac[V], xc[V];
@@ -291,7 +377,7 @@ gemv_n_split(const typename CT<T>::c* __restrict__ A, int64_t lda,
     }
     for (; k < nvec; k += 32) {
       C ac[V], xc[V];
-      unpack(ld_stream(a + k), ac);
+      unpack(ld(a + k, i), ac);
       unpack(xv[k], xc);
 #pragma unroll
       for (int v = 0; v < V; ++v) cfma(acc, ac[v], xc[v]);
@@ -303,11 +389,38 @@ gemv_n_split(const typename CT<T>::c* __restrict__ A, int64_t lda,
       acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
     }
     if (lane == 0) {
-      if constexpr (FUSED) epi(i, acc, dacc);
+      if (FUSED && gridDim.x == 1) epi(i, acc, dacc);
       else part[(int64_t)strip * nrows + i] = acc;
     }
   }
-  if constexpr (FUSED && Epi::K > 0) finish_reduction<KK, NT, Epi>(dacc, red, st);
+  };
+  if (pin > 0) rows(make_ldpin(pin)); else rows(LdA{});
+  if constexpr (FUSED) {
+    if (gridDim.x > 1) {
+      // strip partials of this row block: the last CTA to arrive finishes them
+      __shared__ int am_last;
+      __threadfence();
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        am_last = atomicAdd(rbt + b, 1u) == gridDim.x - 1;
+        if (am_last) rbt[b] = 0u;   // ready for the next launch
+      }
+      __syncthreads();
+      if (!am_last) return;
+      __threadfence();
+      for (int64_t i = i0 + threadIdx.x; i < i1; i += NT) {
+        double2 w = make_double2(0.0, 0.0);
+        for (int c = 0; c < (int)gridDim.x; ++c) {
+          const C p = __ldcg(part + (int64_t)c * nrows + i);
+          w.x += (double)p.x; w.y += (double)p.y;
+        }
+        epi(i, fromd2<C>(w), dacc);
+      }
+      if constexpr (Epi::K > 0) finish_reduction_at<KK, NT, Epi>(dacc, red, st, (unsigned)b, (unsigned)nrb);
+    } else if constexpr (Epi::K > 0) {
+      finish_reduction<KK, NT, Epi>(dacc, red, st);
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -320,7 +433,7 @@ template <typename T, bool CONJ, int NT, int UR, bool VEC>
 __global__ void __launch_bounds__(NT)
 gemv_h_stage1(const typename CT<T>::c* __restrict__ A, int64_t lda,
               const typename CT<T>::c* __restrict__ x, int64_t nrows, int64_t n,
-              typename CT<T>::c* __restrict__ part, const int* gate) {
+              typename CT<T>::c* __restrict__ part, const int* gate, int pin) {
   using C = typename CT<T>::c;
   constexpr int V = VEC ? CT<T>::V : 1;
   using LV = typename std::conditional<VEC, typename CT<T>::v, C>::type;
@@ -337,6 +450,7 @@ gemv_h_stage1(const typename CT<T>::c* __restrict__ A, int64_t lda,
 #pragma unroll
   for (int v = 0; v < V; ++v) acc[v] = czero<C>();
 
+  auto chunks = [&](auto ld) {
   for (int64_t c0 = i0; c0 < i1; c0 += CH) {
     const int cn = (int)min((int64_t)CH, i1 - c0);
     __syncthreads();
@@ -348,7 +462,7 @@ gemv_h_stage1(const typename CT<T>::c* __restrict__ A, int64_t lda,
     for (; t + UR <= cn; t += UR) {
       LV a[UR];
 #pragma unroll
-      for (int u = 0; u < UR; ++u) a[u] = ld_stream(Ap + (int64_t)(t + u) * ldv);
+      for (int u = 0; u < UR; ++u) a[u] = ld(Ap + (int64_t)(t + u) * ldv, c0 + t + u);
 #pragma unroll
       for (int u = 0; u < UR; ++u) {
         C ac[V];
@@ -362,7 +476,7 @@ gemv_h_stage1(const typename CT<T>::c* __restrict__ A, int64_t lda,
     }
     for (; t < cn; ++t) {
       C ac[V];
-      unpack(ld_stream(Ap + (int64_t)t * ldv), ac);
+      unpack(ld(Ap + (int64_t)t * ldv, c0 + t), ac);
       const C xi = xs[t];
 #pragma unroll
       for (int v = 0; v < V; ++v) {
@@ -370,6 +484,8 @@ gemv_h_stage1(const typename CT<T>::c* __restrict__ A, int64_t lda,
       }
     }
   }
+  };
+  if (pin > 0) chunks(make_ldpin(pin)); else chunks(LdA{});
   if (active) {
 #pragma unroll
     for (int v = 0; v < V; ++v) part[(int64_t)s * n + jv * V + v] = acc[v];
@@ -439,7 +555,7 @@ __global__ void __launch_bounds__(NT)
 gemv_cols(const typename CT<T>::c* __restrict__ A, int64_t lda,
           const typename CT<T>::c* __restrict__ xn, const typename CT<T>::c* __restrict__ xh,
           int64_t nrows, int64_t n, typename CT<T>::c* __restrict__ npart,
-          typename CT<T>::c* __restrict__ hpart, const int* gate) {
+          typename CT<T>::c* __restrict__ hpart, const int* gate, int pin) {
   using C = typename CT<T>::c;
   using LV = typename CT<T>::v;
   constexpr int V = CT<T>::V;
@@ -467,6 +583,7 @@ gemv_cols(const typename CT<T>::c* __restrict__ A, int64_t lda,
   for (int v = 0; v < V; ++v) hacc[v] = czero<C>();
   const LV* Ab = reinterpret_cast<const LV*>(A) + jc;
   int buf = 0;
+  auto chunks = [&](auto ld) {
   for (int64_t c0 = i0; c0 < i1; c0 += CH) {
     const int cn = (int)min((int64_t)CH, i1 - c0);
     if constexpr (DO_H) {
@@ -481,7 +598,10 @@ gemv_cols(const typename CT<T>::c* __restrict__ A, int64_t lda,
       for (int g = 0; g < RG; ++g) {
         LV a[UR];
 #pragma unroll
-        for (int u = 0; u < UR; ++u) a[u] = ld_stream(Ab + (c0 + t + min(g * UR + u, nr - 1)) * ldv);
+        for (int u = 0; u < UR; ++u) {
+          const int64_t row = c0 + t + min(g * UR + u, nr - 1);
+          a[u] = ld(Ab + row * ldv, row);
+        }
 #pragma unroll
         for (int u = 0; u < UR; ++u) {
           C ac[V];
@@ -516,6 +636,8 @@ gemv_cols(const typename CT<T>::c* __restrict__ A, int64_t lda,
       }
     }
   }
+  };
+  if (pin > 0) chunks(make_ldpin(pin)); else chunks(LdA{});
   if (DO_H && active) {
 #pragma unroll
     for (int v = 0; v < V; ++v) hpart[(int64_t)s * n + jv * V + v] = hacc[v];

@@ -131,6 +131,13 @@ struct TrueRes {
 // ===========================================================================
 // O1 BiCGSTAB.  Per iteration: P → [A p → v, σ] → S → [A s → t, ⟨t,s⟩,⟨t,t⟩] → X
 // ===========================================================================
+// the direction update p = r (k=1) | r + β(p − ωv): one definition shared by
+// the pass (BsP) and the fused form (BsPIn / BsV2), so both give the same bits
+template <typename C>
+__device__ __forceinline__ C bs_pnew(C r, C p, C v, C beta, C omega, int first) {
+  return first ? r : caxpy(r, beta, caxmy(p, omega, v));
+}
+
 template <typename T>
 struct BsP {  // p = r (k=1) | p = r + β(p − ωv)
   static constexpr int K = 0;
@@ -141,9 +148,7 @@ struct BsP {  // p = r (k=1) | p = r + β(p − ωv)
     first = st->iter == 0;
     beta = fromd2<C>(st->beta); omega = fromd2<C>(st->omega);
   }
-  __device__ void operator()(int64_t i, double2*) {
-    p[i] = first ? r[i] : caxpy(r[i], beta, caxmy(p[i], omega, v[i]));
-  }
+  __device__ void operator()(int64_t i, double2*) { p[i] = bs_pnew(r[i], p[i], v[i], beta, omega, first); }
   static __device__ void finish(State*, const double2*) {}
 };
 
@@ -205,6 +210,80 @@ struct BsT {  // t = A s ; ⟨t,s⟩, ⟨t,t⟩ ; ω
     st->omega = make_double2(sm[0].x / tt, sm[0].y / tt);
     if (!zfinite(st->omega)) { set_done(st, ST_NONFINITE, k - 1); return; }
     if (zzero(st->omega)) { set_done(st, ST_BREAKDOWN, k - 1, BD_OMEGA); return; }
+  }
+};
+
+// ---- BiCGSTAB with the P and S passes folded into the products (single GPU,
+// dense split GEMV with several strips; Engine::matvec_a_in).  The GEMV forms
+// each staged x element with BsPIn / BsSIn while it loads the strip, and the
+// strip-sum epilogue (after every CTA has read the old vectors) recomputes the
+// same element for its own row and stores it: 5 launches per iteration
+// instead of 7, same recurrence values bit for bit except ‖s‖², whose partial
+// sums now run in the epilogue's grid order (it only feeds the half-step test).
+template <typename T>
+struct BsPIn {   // staged element of p = r + β(p − ωv)
+  using C = Cx<T>;
+  const C* r; const C* p; const C* v;
+  C beta, omega; int first;
+  __device__ void load(const State* st) {
+    first = st->iter == 0;
+    beta = fromd2<C>(st->beta); omega = fromd2<C>(st->omega);
+  }
+  __device__ C operator()(const C*, int64_t j) const { return bs_pnew(r[j], p[j], v[j], beta, omega, first); }
+};
+
+template <typename T>
+struct BsV2 {   // p_i stored, v = A p, σ = ⟨r̃, v⟩
+  static constexpr int K = 1;
+  using C = Cx<T>;
+  C* v; const C* rt; const C* r; C* p;
+  C beta, omega; int first;
+  __device__ void load(const State* st) {
+    first = st->iter == 0;
+    beta = fromd2<C>(st->beta); omega = fromd2<C>(st->omega);
+  }
+  __device__ void operator()(int64_t i, C val, double2* acc) {
+    p[i] = bs_pnew(r[i], p[i], v[i], beta, omega, first);
+    const C b = rt[i];
+    v[i] = val;
+    dotc_acc(acc[0], b, val);
+  }
+  static __device__ void finish(State* st, const double2* s) { BsV<T>::finish(st, s); }
+};
+
+template <typename T>
+struct BsSIn {   // staged element of s = r − αv
+  using C = Cx<T>;
+  const C* r; const C* v;
+  C alpha;
+  __device__ void load(const State* st) { alpha = fromd2<C>(st->alpha); }
+  __device__ C operator()(const C*, int64_t j) const { return caxmy(r[j], alpha, v[j]); }
+};
+
+template <typename T>
+struct BsT2 {   // s_i stored, t = A s ; ⟨t,s⟩, ⟨t,t⟩, ‖s‖² ; half-step test, then ω
+  static constexpr int K = 3;
+  using C = Cx<T>;
+  C* t; C* s; const C* r; const C* v;
+  C alpha;
+  __device__ void load(const State* st) { alpha = fromd2<C>(st->alpha); }
+  __device__ void operator()(int64_t i, C val, double2* acc) {
+    const C si = caxmy(r[i], alpha, v[i]);
+    s[i] = si;
+    t[i] = val;
+    dotc_acc(acc[0], val, si);
+    nrm_acc(acc[1], val);
+    nrm_acc(acc[2], si);
+  }
+  static __device__ void finish(State* st, const double2* sm) {
+    const int k = st->iter + 1;
+    const double ss = sm[2].x;
+    if (!isfinite(ss)) { set_done(st, ST_NONFINITE, k - 1); return; }
+    st->ss = ss;
+    // half-step exit (Q4): t = A s was formed but is not part of the method
+    // (not counted; BsX does x += αp)
+    if (ss <= st->tol2r0) { st->half = 1; st->gate2 = 1; return; }
+    BsT<T>::finish(st, sm);
   }
 };
 

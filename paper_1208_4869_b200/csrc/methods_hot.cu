@@ -13,6 +13,11 @@ template <typename T>
 int Engine<T>::bicgstab_iter(ccg_ctx* c) {
   const int* g = &c->st->done;
   const int* g2 = &c->st->gate2;
+  if (in_fuse_ok(c)) {   // P and S formed inside the products (methods.cuh BsPIn / BsSIn)
+    TRY(matvec_a_in(c, BsPIn<T>{L(c, 2), Fs(c, 0), L(c, 4)}, BsV2<T>{L(c, 4), L(c, 3), L(c, 2), Fs(c, 0)}, g));
+    TRY(matvec_a_in(c, BsSIn<T>{L(c, 2), L(c, 4)}, BsT2<T>{L(c, 5), Fs(c, 1), L(c, 2), L(c, 4)}, g));
+    return pass(c, BsX<T>{L(c, X), L(c, 2), Fs(c, 0), Fs(c, 1), L(c, 5), L(c, 3)}, g);
+  }
   TRY(pass(c, BsP<T>{L(c, 2), Fs(c, 0), L(c, 4)}, g));
   TRY(allgather(c, 0));
   TRY(matvec_a(c, F(c, 0), BsV<T>{L(c, 4), L(c, 3)}, g));

@@ -15,7 +15,7 @@ mkdir -p gpurun_out
 run() {
   local task=$1; shift
   case "$task" in
-    tests) timeout 3000 python -m pytest tests -m gpu -q -p no:cacheprovider "$@" > gpurun_out/pytest_gpu.log 2>&1
+    tests) CCG_PARITY_LOG=gpurun_out/parity.jsonl timeout 3000 python -m pytest tests -m gpu -q -p no:cacheprovider "$@" > gpurun_out/pytest_gpu.log 2>&1
            echo "tests rc=$?"; tail -5 gpurun_out/pytest_gpu.log ;;
     smoke) timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" ;;
     bench) timeout 900 python bench.py "$@" > gpurun_out/bench.log 2>&1; echo "bench rc=$?"; tail -1 gpurun_out/bench.log ;;
