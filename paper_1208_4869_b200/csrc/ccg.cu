@@ -764,7 +764,7 @@ int ccg_set_matvec_stencil7(ccg_handle c, int64_t nx, int64_t ny, int64_t nz, co
   c->flags = flags | CCG_FLAG_SYMMETRIC;
   c->vec_ok = true;
   const char* zc = getenv("CCG_STENCIL_ZC");
-  c->szc = zc ? std::max(1, atoi(zc)) : 4;
+  c->szc = zc ? std::max(1, atoi(zc)) : 8;   // 1024 CTAs at 128³: one wave, half the reduction slots of 4 (ab/cfg5_zc.jsonl)
   invalidate_graphs(c);
   return c->dtype == CCG_C64 ? choose_launch<float>(c) : choose_launch<double>(c);
 }

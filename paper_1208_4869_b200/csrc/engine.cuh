@@ -85,7 +85,7 @@ struct ccg_ctx {
   int sell_grid[2] = {0, 0};
   int sell_one = 0, sell_waves = 1;   // SELL load schedule / grid waves (CCG_SELL_ONE, CCG_SELL_WAVES)
   // matrix-free 7-point stencil (ccg_set_matvec_stencil7)
-  int snx = 0, sny = 0, snz = 0, sz0 = 0, snzl = 0, szc = 4;
+  int snx = 0, sny = 0, snz = 0, sz0 = 0, snzl = 0, szc = 8;
   double2 scoef[4] = {};  // d, ox, oy, oz
   // FFT block-Toeplitz operator (ccg_set_matvec_toeplitz3)
   FftGeo geo = {};

@@ -429,6 +429,268 @@ __global__ void __launch_bounds__(256 / R) v7_march_rows(const C* __restrict__ x
   }
 }
 
+// V9: V6 with a register queue of the next PD "above" planes (loads issued
+// PD planes ahead: PD + 4 loads in flight per thread instead of ~1 from HBM),
+// MINB CTAs/SM requested in the launch bounds.
+template <int ZC, int PD, int MINB>
+__global__ void __launch_bounds__(256, MINB) v9_prefetch(const C* __restrict__ x, C* __restrict__ y, int nx, int ny,
+                                                       int nz, Co k) {
+  const int ix = blockIdx.x * 32 + (threadIdx.x & 31);
+  const int iy = blockIdx.y * 8 + (threadIdx.x >> 5);
+  const int zb = blockIdx.z * ZC;
+  if (ix >= nx || iy >= ny) return;
+  const int plane = nx * ny;
+  const C zero = czero<C>();
+  const bool hxm = ix > 0, hxp = ix < nx - 1, hym = iy > 0, hyp = iy < ny - 1;
+  const C* xp = x + (int64_t)zb * plane + ix + nx * iy;
+  C* yp = y + (int64_t)zb * plane + ix + nx * iy;
+  C below = zb > 0 ? xp[-plane] : zero;
+  C cur = xp[0];
+  C q[PD];   // q[d] = plane zb + 1 + d (zero outside the lattice)
+#pragma unroll
+  for (int d = 0; d < PD; ++d) q[d] = zb + 1 + d < nz ? xp[(d + 1) * plane] : zero;
+#pragma unroll
+  for (int j = 0; j < ZC; ++j) {
+    const int z = zb + j;
+    if (z >= nz) break;
+    const C above = q[0];
+#pragma unroll
+    for (int d = 0; d + 1 < PD; ++d) q[d] = q[d + 1];
+    q[PD - 1] = (j + 1 + PD < ZC + 1 && z + 1 + PD < nz) ? xp[(1 + PD) * plane] : zero;
+    const C ym = hym ? xp[-nx] : zero;
+    const C xm = hxm ? xp[-1] : zero;
+    const C xq = hxp ? xp[1] : zero;
+    const C yq = hyp ? xp[nx] : zero;
+    C acc = zero;
+    mac(acc, k.oz, below);
+    mac(acc, k.oy, ym);
+    mac(acc, k.ox, xm);
+    mac(acc, k.d, cur);
+    mac(acc, k.ox, xq);
+    mac(acc, k.oy, yq);
+    mac(acc, k.oz, above);
+    yp[0] = acc;
+    below = cur;
+    cur = above;
+    xp += plane;
+    yp += plane;
+  }
+}
+
+// ---- with a BiCGSTAB BsT-like epilogue: t = A s stored, fp64 partials
+// <t,s> and ||t||^2, per-CTA slot + arrival ticket, the last CTA sums the
+// slots in order (the library's finish_reduction pattern)
+struct EpiOut { double2* part; unsigned* ticket; double2* result; };
+
+template <bool REL = false>
+__device__ __forceinline__ void epi_finish(double2 a0, double2 a1, EpiOut e, unsigned bid, unsigned nb) {
+  __shared__ double2 sm[8][2];
+  __shared__ int last;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int o = 16; o; o >>= 1) {
+    a0.x += __shfl_xor_sync(~0u, a0.x, o); a0.y += __shfl_xor_sync(~0u, a0.y, o);
+    a1.x += __shfl_xor_sync(~0u, a1.x, o); a1.y += __shfl_xor_sync(~0u, a1.y, o);
+  }
+  if (lane == 0) { sm[warp][0] = a0; sm[warp][1] = a1; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double2 s0 = make_double2(0, 0), s1 = make_double2(0, 0);
+    for (int w = 0; w < (int)(blockDim.x / 32); ++w) { s0.x += sm[w][0].x; s0.y += sm[w][0].y; s1.x += sm[w][1].x; }
+    e.part[2 * bid] = s0; e.part[2 * bid + 1] = s1;
+    if (REL) {   // release RMW: orders this CTA's partials before its arrival, no L1 flush
+      unsigned t;
+      asm volatile("atom.add.release.gpu.global.u32 %0, [%1], 1;" : "=r"(t) : "l"(e.ticket) : "memory");
+      last = t == nb - 1;
+    } else {
+      __threadfence();
+      last = atomicAdd(e.ticket, 1u) == nb - 1;
+    }
+  }
+  __syncthreads();
+  if (!last) return;
+  if (REL) asm volatile("fence.acq_rel.gpu;" ::: "memory");
+  else __threadfence();
+  double2 s0 = make_double2(0, 0), s1 = make_double2(0, 0);
+  for (unsigned b = threadIdx.x; b < nb; b += blockDim.x) {
+    const double2 p0 = __ldcg(e.part + 2 * b), p1 = __ldcg(e.part + 2 * b + 1);
+    s0.x += p0.x; s0.y += p0.y; s1.x += p1.x;
+  }
+  for (int o = 16; o; o >>= 1) {
+    s0.x += __shfl_xor_sync(~0u, s0.x, o); s0.y += __shfl_xor_sync(~0u, s0.y, o); s1.x += __shfl_xor_sync(~0u, s1.x, o);
+  }
+  __syncthreads();
+  if (lane == 0) { sm[warp][0] = s0; sm[warp][1] = s1; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double2 r0 = make_double2(0, 0), r1 = make_double2(0, 0);
+    for (int w = 0; w < (int)(blockDim.x / 32); ++w) { r0.x += sm[w][0].x; r0.y += sm[w][0].y; r1.x += sm[w][1].x; }
+    e.result[0] = r0; e.result[1] = r1;
+    *e.ticket = 0;
+  }
+}
+
+__device__ __forceinline__ void epi_acc(double2& a0, double2& a1, C t, C s) {
+  a0.x = fma(t.x, s.x, fma(t.y, s.y, a0.x));   // conj(t)·s
+  a0.y = fma(t.x, s.y, fma(-t.y, s.x, a0.y));
+  a1.x = fma(t.x, t.x, fma(t.y, t.y, a1.x));
+}
+
+// one z-marching tile (32 x 8 columns, ZC planes), BsT-like epilogue
+template <int ZC>
+__device__ __forceinline__ void tile_e(const C* __restrict__ x, C* __restrict__ y, int nx, int ny, int nz, Co k,
+                                       int bx, int by, int bz, double2& a0, double2& a1) {
+  const int ix = bx * 32 + (threadIdx.x & 31);
+  const int iy = by * 8 + (threadIdx.x >> 5);
+  const int zb = bz * ZC;
+  if (ix >= nx || iy >= ny) return;
+  const int plane = nx * ny;
+  const C zero = czero<C>();
+  const bool hxm = ix > 0, hxp = ix < nx - 1, hym = iy > 0, hyp = iy < ny - 1;
+  const C* xp = x + (int64_t)zb * plane + ix + nx * iy;
+  C* yp = y + (int64_t)zb * plane + ix + nx * iy;
+  C below = zb > 0 ? xp[-plane] : zero;
+  C cur = xp[0];
+#pragma unroll
+  for (int j = 0; j < ZC; ++j) {
+    const int z = zb + j;
+    if (z >= nz) break;
+    const C above = z < nz - 1 ? xp[plane] : zero;
+    const C ym = hym ? xp[-nx] : zero;
+    const C xm = hxm ? xp[-1] : zero;
+    const C xq = hxp ? xp[1] : zero;
+    const C yq = hyp ? xp[nx] : zero;
+    C acc = zero;
+    mac(acc, k.oz, below);
+    mac(acc, k.oy, ym);
+    mac(acc, k.ox, xm);
+    mac(acc, k.d, cur);
+    mac(acc, k.ox, xq);
+    mac(acc, k.oy, yq);
+    mac(acc, k.oz, above);
+    yp[0] = acc;
+    epi_acc(a0, a1, acc, cur);
+    below = cur;
+    cur = above;
+    xp += plane;
+    yp += plane;
+  }
+}
+
+// V10: one tile per CTA + epilogue (the library's structure)
+template <int ZC, bool REL = false>
+__global__ void __launch_bounds__(256) v10_epi(const C* __restrict__ x, C* __restrict__ y, int nx, int ny, int nz, Co k,
+                                               EpiOut e) {
+  double2 a0 = make_double2(0, 0), a1 = make_double2(0, 0);
+  tile_e<ZC>(x, y, nx, ny, nz, k, blockIdx.x, blockIdx.y, blockIdx.z, a0, a1);
+  epi_finish<REL>(a0, a1, e, blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z),
+             gridDim.x * gridDim.y * gridDim.z);
+}
+
+// V11: persistent — grid = SMs x occupancy, each CTA walks tiles (z fastest
+// within a column block so consecutive tiles of a CTA share L2 lines)
+template <int ZC, int MINB, bool REL = false>
+__global__ void __launch_bounds__(256, MINB) v11_persist(const C* __restrict__ x, C* __restrict__ y, int nx, int ny,
+                                                       int nz, Co k, EpiOut e) {
+  double2 a0 = make_double2(0, 0), a1 = make_double2(0, 0);
+  const int tx = (nx + 31) / 32, ty = (ny + 7) / 8, tz = (nz + ZC - 1) / ZC;
+  const int ntiles = tx * ty * tz;
+  for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const int bx = t % tx, by = (t / tx) % ty, bz = t / (tx * ty);
+    tile_e<ZC>(x, y, nx, ny, nz, k, bx, by, bz, a0, a1);
+  }
+  epi_finish<REL>(a0, a1, e, blockIdx.x, gridDim.x);
+}
+
+// V12: v10 without the arrival ticket (block sum + slot store only); V13: the
+// epilogue arithmetic only (no block sum) — to split the epilogue's cost
+template <int ZC, int MODE>
+__global__ void __launch_bounds__(256) v12_parts(const C* __restrict__ x, C* __restrict__ y, int nx, int ny, int nz,
+                                                 Co k, EpiOut e) {
+  double2 a0 = make_double2(0, 0), a1 = make_double2(0, 0);
+  tile_e<ZC>(x, y, nx, ny, nz, k, blockIdx.x, blockIdx.y, blockIdx.z, a0, a1);
+  const unsigned bid = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+  if (MODE == 1) {   // arithmetic only
+    if (a0.x == 12345.678) e.part[bid] = a1;
+    return;
+  }
+  __shared__ double2 sm[8][2];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int o = 16; o; o >>= 1) {
+    a0.x += __shfl_xor_sync(~0u, a0.x, o); a0.y += __shfl_xor_sync(~0u, a0.y, o);
+    a1.x += __shfl_xor_sync(~0u, a1.x, o);
+  }
+  if (lane == 0) { sm[warp][0] = a0; sm[warp][1] = a1; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double2 s0 = make_double2(0, 0), s1 = make_double2(0, 0);
+    for (int w = 0; w < 8; ++w) { s0.x += sm[w][0].x; s0.y += sm[w][0].y; s1.x += sm[w][1].x; }
+    e.part[2 * bid] = s0; e.part[2 * bid + 1] = s1;
+  }
+}
+
+// V14: v10 with a two-level arrival: groups of 32 CTAs each have their own
+// ticket (different L2 slices, so the same-address atomics do not serialise
+// over the whole grid); the last CTA of a group sums its 32 slots with one
+// warp into a group slot, and only those take the grid ticket; the last one
+// sums the group slots.  Fixed order at both levels (deterministic).
+struct EpiOut2 { double2* part; double2* gpart; unsigned* gticket; unsigned* ticket; double2* result; };
+
+__device__ __forceinline__ double2 warp_sum2(double2 v) {
+  for (int o = 16; o; o >>= 1) { v.x += __shfl_xor_sync(~0u, v.x, o); v.y += __shfl_xor_sync(~0u, v.y, o); }
+  return v;
+}
+
+template <int ZC>
+__global__ void __launch_bounds__(256) v14_epi2(const C* __restrict__ x, C* __restrict__ y, int nx, int ny, int nz,
+                                                Co k, EpiOut2 e) {
+  double2 a0 = make_double2(0, 0), a1 = make_double2(0, 0);
+  tile_e<ZC>(x, y, nx, ny, nz, k, blockIdx.x, blockIdx.y, blockIdx.z, a0, a1);
+  const unsigned bid = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+  const unsigned nb = gridDim.x * gridDim.y * gridDim.z;
+  __shared__ double2 sm[8][2];
+  __shared__ int flag;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  a0 = warp_sum2(a0);
+  a1 = warp_sum2(a1);
+  if (lane == 0) { sm[warp][0] = a0; sm[warp][1] = a1; }
+  __syncthreads();
+  const unsigned g = bid / 32, ng = (nb + 31) / 32, gs = min(32u, nb - g * 32);
+  if (threadIdx.x == 0) {
+    double2 s0 = make_double2(0, 0), s1 = make_double2(0, 0);
+    for (int w = 0; w < 8; ++w) { s0.x += sm[w][0].x; s0.y += sm[w][0].y; s1.x += sm[w][1].x; }
+    e.part[2 * bid] = s0; e.part[2 * bid + 1] = s1;
+    unsigned t;
+    asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(t) : "l"(e.gticket + g) : "memory");
+    flag = t == gs - 1;
+  }
+  __syncthreads();
+  if (!flag) return;
+  if (warp != 0) return;
+  // group finisher (one warp): slots of group g in order
+  double2 p0 = make_double2(0, 0), p1 = make_double2(0, 0);
+  if (lane < (int)gs) { p0 = __ldcg(e.part + 2 * (g * 32 + lane)); p1 = __ldcg(e.part + 2 * (g * 32 + lane) + 1); }
+  p0 = warp_sum2(p0);
+  p1 = warp_sum2(p1);
+  unsigned last = 0;
+  if (lane == 0) {
+    e.gpart[2 * g] = p0; e.gpart[2 * g + 1] = p1;
+    e.gticket[g] = 0;
+    unsigned t;
+    asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(t) : "l"(e.ticket) : "memory");
+    last = t == ng - 1;
+  }
+  last = __shfl_sync(~0u, last, 0);
+  if (!last) return;
+  double2 q0 = make_double2(0, 0), q1 = make_double2(0, 0);
+  for (unsigned b = lane; b < ng; b += 32) {
+    const double2 u0 = __ldcg(e.gpart + 2 * b), u1 = __ldcg(e.gpart + 2 * b + 1);
+    q0.x += u0.x; q0.y += u0.y; q1.x += u1.x;
+  }
+  q0 = warp_sum2(q0);
+  q1 = warp_sum2(q1);
+  if (lane == 0) { e.result[0] = q0; e.result[1] = q1; *e.ticket = 0; }
+}
+
 __device__ __forceinline__ C shfl_up1(C v) {
   C r; r.x = __shfl_up_sync(0xffffffffu, v.x, 1); r.y = __shfl_up_sync(0xffffffffu, v.y, 1); return r;
 }
@@ -539,6 +801,20 @@ int main(int argc, char** argv) {
     CKE(cudaDeviceSynchronize());
     return 0;
   }
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  EpiOut eo;
+  CKE(cudaMalloc(&eo.part, 2 * sizeof(double2) * 1 << 16));
+  CKE(cudaMalloc(&eo.ticket, sizeof(unsigned)));
+  CKE(cudaMemset(eo.ticket, 0, sizeof(unsigned)));
+  CKE(cudaMalloc(&eo.result, 2 * sizeof(double2)));
+  EpiOut2 eo2;
+  CKE(cudaMalloc(&eo2.part, sizeof(double2) * 2 * 65536));
+  CKE(cudaMalloc(&eo2.gpart, sizeof(double2) * 2 * 4096));
+  CKE(cudaMalloc(&eo2.gticket, sizeof(unsigned) * 4096));
+  CKE(cudaMemset(eo2.gticket, 0, sizeof(unsigned) * 4096));
+  eo2.ticket = eo.ticket;
+  eo2.result = eo.result;
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
@@ -625,6 +901,57 @@ int main(int argc, char** argv) {
     bench("v8 shfl fma zc=" #ZC, [&] { v8_march_shfl<ZC><<<g, 256>>>(x, y, nx, ny, nz, k); }, fl); \
   }
     V8(4) V8(8)
+#define V9(ZC, PD, MB)                                                                                     \
+  {                                                                                                        \
+    dim3 g((nx + 31) / 32, (ny + 7) / 8, (nz + ZC - 1) / ZC);                                              \
+    bench("v9 prefetch zc=" #ZC " pd=" #PD " minb=" #MB,                                                   \
+          [&] { v9_prefetch<ZC, PD, MB><<<g, 256>>>(x, y, nx, ny, nz, k); }, fl);                          \
+  }
+    V9(8, 2, 1) V9(8, 3, 1) V9(8, 4, 1) V9(16, 3, 1) V9(16, 4, 1) V9(16, 6, 1) V9(32, 4, 1) V9(8, 3, 4) V9(16, 4, 4)
+    V9(16, 4, 3) V9(32, 6, 3) V9(4, 2, 4) V9(4, 3, 4)
+#define V10(ZC)                                                                                    \
+  {                                                                                                \
+    dim3 g((nx + 31) / 32, (ny + 7) / 8, (nz + ZC - 1) / ZC);                                      \
+    bench("v10 epi zc=" #ZC, [&] { v10_epi<ZC><<<g, 256>>>(x, y, nx, ny, nz, k, eo); }, fl);         \
+  }
+    V10(2) V10(4) V10(8)
+#define V11(ZC, MB, W)                                                                                        \
+  {                                                                                                           \
+    int occ = 0;                                                                                              \
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, v11_persist<ZC, MB>, 256, 0);                        \
+    const int grid = sms * occ * W;                                                                           \
+    bench("v11 persist zc=" #ZC " minb=" #MB " waves=" #W,                                                    \
+          [&] { v11_persist<ZC, MB><<<grid, 256>>>(x, y, nx, ny, nz, k, eo); }, fl);                          \
+  }
+    V11(2, 1, 1) V11(4, 1, 1) V11(8, 1, 1) V11(4, 3, 1) V11(4, 4, 1) V11(2, 4, 1) V11(4, 1, 2) V11(4, 4, 2)
+#define V10R(ZC)                                                                                          \
+  {                                                                                                       \
+    dim3 g((nx + 31) / 32, (ny + 7) / 8, (nz + ZC - 1) / ZC);                                             \
+    bench("v10 epi release zc=" #ZC, [&] { v10_epi<ZC, true><<<g, 256>>>(x, y, nx, ny, nz, k, eo); }, fl); \
+  }
+    V10R(2) V10R(4) V10R(8)
+#define V11R(ZC, MB)                                                                                          \
+  {                                                                                                           \
+    int occ = 0;                                                                                              \
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, v11_persist<ZC, MB, true>, 256, 0);                  \
+    const int grid = sms * occ;                                                                               \
+    bench("v11 persist release zc=" #ZC " minb=" #MB,                                                         \
+          [&] { v11_persist<ZC, MB, true><<<grid, 256>>>(x, y, nx, ny, nz, k, eo); }, fl);                    \
+  }
+    V11R(4, 1) V11R(4, 4) V11R(8, 1)
+    V11(4, 6, 1) V11(4, 8, 1) V11(8, 8, 1)
+#define V12(ZC, M)                                                                                          \
+  {                                                                                                         \
+    dim3 g((nx + 31) / 32, (ny + 7) / 8, (nz + ZC - 1) / ZC);                                               \
+    bench("v12 parts mode=" #M " zc=" #ZC, [&] { v12_parts<ZC, M><<<g, 256>>>(x, y, nx, ny, nz, k, eo); }, fl); \
+  }
+    V12(4, 1) V12(4, 2) V12(8, 1) V12(8, 2)
+#define V14(ZC)                                                                                          \
+  {                                                                                                      \
+    dim3 g((nx + 31) / 32, (ny + 7) / 8, (nz + ZC - 1) / ZC);                                            \
+    bench("v14 epi two-level zc=" #ZC, [&] { v14_epi2<ZC><<<g, 256>>>(x, y, nx, ny, nz, k, eo2); }, fl);  \
+  }
+    V14(2) V14(4) V14(8)
   }
   for (int fl = 1; fl >= 0; --fl) {
     bench("copy (cudaMemcpy d2d)", [&] { cudaMemcpyAsync(y, x, n * sizeof(C), cudaMemcpyDeviceToDevice); }, fl);
