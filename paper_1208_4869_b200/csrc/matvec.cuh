@@ -97,6 +97,30 @@ __device__ __forceinline__ void unpack(const double2& v, double2 (&c)[1]) { c[0]
 __device__ __forceinline__ void unpack(const float2& v, float2 (&c)[1]) { c[0] = v; }
 
 // ---------------------------------------------------------------------------
+// Early epilogue loads.  An epilogue that reads other vectors at the output
+// index (e.g. r̃_i for σ = ⟨r̃, v⟩) may declare `Pre`, `pre(i)` and
+// `post(i, val, pre, acc)`; the latency-bound products (stencil, SELL) then
+// issue pre(i) together with their own loads — a plane ahead in the stencil's
+// z-march — instead of after the product value is formed, which put one more
+// dependent DRAM round trip on every output (`cuobjdump -sass`: the r̃ load
+// sat between the last FMA and the store).  Same arithmetic, same bits.
+// ---------------------------------------------------------------------------
+template <class E, class = void>
+struct EpiPre {
+  struct P {};
+  static __device__ __forceinline__ P pre(const E&, int64_t) { return P{}; }
+  template <class C>
+  static __device__ __forceinline__ void post(E& e, int64_t i, C val, P, double2* acc) { e(i, val, acc); }
+};
+template <class E>
+struct EpiPre<E, std::void_t<typename E::Pre>> {
+  using P = typename E::Pre;
+  static __device__ __forceinline__ P pre(const E& e, int64_t i) { return e.pre(i); }
+  template <class C>
+  static __device__ __forceinline__ void post(E& e, int64_t i, C val, P p, double2* acc) { e.post(i, val, p, acc); }
+};
+
+// ---------------------------------------------------------------------------
 // K1 gemv_n: y_i = Σ_j A_ij x_j for local rows [0, nrows), row-major A.
 // Persistent, balanced: CTA b owns rows [b·nrows/G, (b+1)·nrows/G) and walks
 // them in groups of R rows.  Each thread keeps its x chunk in registers and
@@ -856,11 +880,15 @@ spmv_sell_kernel(const int64_t* __restrict__ soff, const int32_t* __restrict__ s
   int64_t i = (int64_t)blockIdx.x * NT + threadIdx.x;
   // two rows per step (i, i + stride) when their slices share the common
   // stencil width 7: twice the loads in flight per thread
+  using EP = EpiPre<Epi>;
   for (; !ONE && i + stride < nwarps_rows; i += 2 * stride) {
     const int64_t s1 = i >> 5, s2 = (i + stride) >> 5;
     const int lane = (int)(i & 31);
     const int w1 = __ldg(swidth + s1), w2 = __ldg(swidth + s2);
     if (w1 != 7 || w2 != 7) break;      // warp-uniform; the generic loop below finishes
+    typename EP::P p1{}, p2{};
+    if (i < nrows) p1 = EP::pre(epi, i);
+    if (i + stride < nrows) p2 = EP::pre(epi, i + stride);
     const int64_t b1 = __ldg(soff + s1) + lane, b2 = __ldg(soff + s2) + lane;
     int c1[7], c2[7];
 #pragma unroll
@@ -880,12 +908,14 @@ spmv_sell_kernel(const int64_t* __restrict__ soff, const int32_t* __restrict__ s
       a1.x = c1[u] >= 0 ? t1.x : a1.x; a1.y = c1[u] >= 0 ? t1.y : a1.y;
       a2.x = c2[u] >= 0 ? t2.x : a2.x; a2.y = c2[u] >= 0 ? t2.y : a2.y;
     }
-    if (i < nrows) epi(i, CONJ ? cconj(a1) : a1, dacc);
-    if (i + stride < nrows) epi(i + stride, CONJ ? cconj(a2) : a2, dacc);
+    if (i < nrows) EP::post(epi, i, CONJ ? cconj(a1) : a1, p1, dacc);
+    if (i + stride < nrows) EP::post(epi, i + stride, CONJ ? cconj(a2) : a2, p2, dacc);
   }
   for (; i < nwarps_rows; i += stride) {
     const int64_t s = i >> 5;
     const int lane = (int)(i & 31);
+    typename EP::P pr{};
+    if (i < nrows) pr = EP::pre(epi, i);
     const int w = __ldg(swidth + s);
     const int64_t base = __ldg(soff + s) + lane;
     C acc;
@@ -924,7 +954,7 @@ spmv_sell_kernel(const int64_t* __restrict__ soff, const int32_t* __restrict__ s
         }
       }
     }
-    if (i < nrows) epi(i, CONJ ? cconj(acc) : acc, dacc);
+    if (i < nrows) EP::post(epi, i, CONJ ? cconj(acc) : acc, pr, dacc);
   }
   if constexpr (Epi::K > 0) finish_reduction<KK, NT, Epi>(dacc, red, st);
 }
@@ -999,10 +1029,14 @@ stencil7_kernel(const typename CT<T>::c* __restrict__ x, int nx, int ny, int nz,
     int zg = z0 + zb;
     const C* xp = x + (int64_t)zg * plane + ix + nx * iy;
     int64_t li = (int64_t)zb * plane + ix + nx * iy;    // local (epilogue) index
+    using EP = EpiPre<Epi>;
+    typename EP::P pnext = EP::pre(epi, li);   // the epilogue's inputs, a plane ahead
     C below = zg > 0 ? xp[-plane] : zero;
     C cur = xp[0];
 #pragma unroll 4
     for (int zl = zb; zl < ze; ++zl, ++zg) {
+      const typename EP::P pcur = pnext;
+      if (zl + 1 < ze) pnext = EP::pre(epi, li + plane);
       const bool hzm = zg > 0, hzp = zg < nz - 1;
       // every load of the plane first (masked to zero), then the terms in
       // ascending column order
@@ -1019,7 +1053,7 @@ stencil7_kernel(const typename CT<T>::c* __restrict__ x, int nx, int ny, int nz,
       st_term(acc, ox, xq, hxp);
       st_term(acc, oy, yq, hyp);
       st_term(acc, oz, above, hzp);
-      epi(li, acc, dacc);
+      EP::post(epi, li, acc, pcur, dacc);
       below = cur;
       cur = above;
       xp += plane;

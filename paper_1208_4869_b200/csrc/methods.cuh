@@ -124,7 +124,10 @@ struct TrueRes {
   using C = Cx<T>;
   const C* y;
   __device__ void load(const State*) {}
-  __device__ void operator()(int64_t i, C ax, double2* acc) { nrm_acc(acc[0], csub(y[i], ax)); }
+  using Pre = C;   // early load (matvec.cuh EpiPre)
+  __device__ Pre pre(int64_t i) const { return y[i]; }
+  __device__ void post(int64_t, C ax, Pre yi, double2* acc) { nrm_acc(acc[0], csub(yi, ax)); }
+  __device__ void operator()(int64_t i, C ax, double2* acc) { post(i, ax, pre(i), acc); }
   static __device__ void finish(State* st, const double2* s) { st->true_rr = s[0].x; }
 };
 
@@ -158,7 +161,11 @@ struct BsV {  // v = A p ; σ = ⟨r̃, v⟩ ; α = ρ/σ
   using C = Cx<T>;
   C* v; const C* rt;
   __device__ void load(const State*) {}
-  __device__ void operator()(int64_t i, C val, double2* acc) { const C b = rt[i]; v[i] = val; dotc_acc(acc[0], b, val); }
+  // early load of the epilogue input (issued with the product's loads; matvec.cuh EpiPre)
+  using Pre = C;
+  __device__ Pre pre(int64_t i) const { return rt[i]; }
+  __device__ void post(int64_t i, C val, Pre b, double2* acc) { v[i] = val; dotc_acc(acc[0], b, val); }
+  __device__ void operator()(int64_t i, C val, double2* acc) { post(i, val, pre(i), acc); }
   static __device__ void finish(State* st, const double2* s) {
     const int k = st->iter + 1;
     st->matvecs_a++;
@@ -196,12 +203,14 @@ struct BsT {  // t = A s ; ⟨t,s⟩, ⟨t,t⟩ ; ω
   using C = Cx<T>;
   C* t; const C* s;
   __device__ void load(const State*) {}
-  __device__ void operator()(int64_t i, C val, double2* acc) {
-    const C si = s[i];
+  using Pre = C;   // early load (matvec.cuh EpiPre)
+  __device__ Pre pre(int64_t i) const { return s[i]; }
+  __device__ void post(int64_t i, C val, Pre si, double2* acc) {
     t[i] = val;
     dotc_acc(acc[0], val, si);
     nrm_acc(acc[1], val);
   }
+  __device__ void operator()(int64_t i, C val, double2* acc) { post(i, val, pre(i), acc); }
   static __device__ void finish(State* st, const double2* sm) {
     const int k = st->iter + 1;
     st->matvecs_a++;
@@ -567,7 +576,11 @@ struct RhoEpi {  // r̂ = A r ; ρ = ⟨shadow, r̂⟩   (BiCOR and CORS)
   using C = Cx<T>;
   C* rh; const C* sh;
   __device__ void load(const State*) {}
-  __device__ void operator()(int64_t i, C val, double2* acc) { const C b = sh[i]; rh[i] = val; dotc_acc(acc[0], b, val); }
+  // early load of the epilogue input (issued with the product's loads; matvec.cuh EpiPre)
+  using Pre = C;
+  __device__ Pre pre(int64_t i) const { return sh[i]; }
+  __device__ void post(int64_t i, C val, Pre b, double2* acc) { rh[i] = val; dotc_acc(acc[0], b, val); }
+  __device__ void operator()(int64_t i, C val, double2* acc) { post(i, val, pre(i), acc); }
   static __device__ void finish(State* st, const double2* s) { rho_step(st, s[0], true); }
 };
 
@@ -647,7 +660,11 @@ struct CoQ {  // q = A q̂ ; ξ = ⟨r₀*, q⟩ ; α = ρ/ξ
   using C = Cx<T>;
   C* q; const C* r0s;
   __device__ void load(const State*) {}
-  __device__ void operator()(int64_t i, C val, double2* acc) { const C b = r0s[i]; q[i] = val; dotc_acc(acc[0], b, val); }
+  // early load of the epilogue input (issued with the product's loads; matvec.cuh EpiPre)
+  using Pre = C;
+  __device__ Pre pre(int64_t i) const { return r0s[i]; }
+  __device__ void post(int64_t i, C val, Pre b, double2* acc) { q[i] = val; dotc_acc(acc[0], b, val); }
+  __device__ void operator()(int64_t i, C val, double2* acc) { post(i, val, pre(i), acc); }
   static __device__ void finish(State* st, const double2* s) { st->matvecs_a++; xi_step(st, s[0]); }
 };
 
@@ -772,7 +789,11 @@ struct CsV {  // v = A p ; σ = ⟨r̃, v⟩ ; α = ρ/σ
   using C = Cx<T>;
   C* v; const C* rt;
   __device__ void load(const State*) {}
-  __device__ void operator()(int64_t i, C val, double2* acc) { const C b = rt[i]; v[i] = val; dotc_acc(acc[0], b, val); }
+  // early load of the epilogue input (issued with the product's loads; matvec.cuh EpiPre)
+  using Pre = C;
+  __device__ Pre pre(int64_t i) const { return rt[i]; }
+  __device__ void post(int64_t i, C val, Pre b, double2* acc) { v[i] = val; dotc_acc(acc[0], b, val); }
+  __device__ void operator()(int64_t i, C val, double2* acc) { post(i, val, pre(i), acc); }
   static __device__ void finish(State* st, const double2* s) { st->matvecs_a++; sigma_step(st, s[0]); }
 };
 
@@ -801,13 +822,15 @@ struct CsR {  // r −= α A(u + q) ; ‖r‖², ⟨r̃, r⟩
   C* r; const C* rt;
   C alpha;
   __device__ void load(const State* st) { alpha = fromd2<C>(st->alpha); }
-  __device__ void operator()(int64_t i, C w, double2* acc) {
-    const C rold = r[i], rti = rt[i];
-    const C ri = caxmy(rold, alpha, w);
+  struct Pre { C r, rt; };   // early loads (matvec.cuh EpiPre)
+  __device__ Pre pre(int64_t i) const { return Pre{r[i], rt[i]}; }
+  __device__ void post(int64_t i, C w, Pre q, double2* acc) {
+    const C ri = caxmy(q.r, alpha, w);
     r[i] = ri;
     nrm_acc(acc[0], ri);
-    dotc_acc(acc[1], rti, ri);
+    dotc_acc(acc[1], q.rt, ri);
   }
+  __device__ void operator()(int64_t i, C w, double2* acc) { post(i, w, pre(i), acc); }
   static __device__ void finish(State* st, const double2* s) {
     st->matvecs_a++;
     next_rho(st, st->iter + 1, s[0].x, s[1]);
@@ -832,7 +855,11 @@ struct CrAr {  // Ar = A r ; μ' = [r, Ar] ; β = μ'/μ   (end of iteration k =
   using C = Cx<T>;
   C* ar; const C* r;
   __device__ void load(const State*) {}
-  __device__ void operator()(int64_t i, C val, double2* acc) { const C b = r[i]; ar[i] = val; dotu_acc(acc[0], b, val); }
+  // early load of the epilogue input (issued with the product's loads; matvec.cuh EpiPre)
+  using Pre = C;
+  __device__ Pre pre(int64_t i) const { return r[i]; }
+  __device__ void post(int64_t i, C val, Pre b, double2* acc) { ar[i] = val; dotu_acc(acc[0], b, val); }
+  __device__ void operator()(int64_t i, C val, double2* acc) { post(i, val, pre(i), acc); }
   static __device__ void finish(State* st, const double2* s) {
     st->matvecs_a++;
     const int kc = st->iter - 1;   // the oracle raises inside iteration iter

@@ -101,7 +101,11 @@ def test_split_fuse(request, monkeypatch, sysname):
         k = a["iterations"]
         a = _solve(monkeypatch, env0, A, y, method, 0.0, k)
         b = _solve(monkeypatch, env1, A, y, method, 0.0, k)
-        assert relerr(b["x"], a["x"]) <= (1e-12 if A.dtype == np.complex128 else 1e-5)
+        # the phase sums run in another fixed order: a rounding-level change.
+        # CGNE on config 2 amplifies it to ~1e-9 (its oracle envelope D(k) is
+        # 3.7e-9), BiCGSTAB does not
+        bar = 1e-5 if A.dtype == np.complex64 else (2 * 3.7e-9 if method == "cgne" else 1e-12)
+        assert relerr(b["x"], a["x"]) <= bar, (method, relerr(b["x"], a["x"]))
     # the product itself (ccg_apply takes the same kernels) is bitwise equal
     for k, v in env1.items():
         monkeypatch.setenv(k, v)
