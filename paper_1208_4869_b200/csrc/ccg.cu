@@ -121,12 +121,17 @@ static int choose_launch(ccg_ctx* c) {
     c->split_W = (int)std::min<int64_t>(c->n, strip_bytes / (int64_t)sizeof(C));
     c->split_strips = (int)((c->n + c->split_W - 1) / c->split_W);
     int occs = 0;
+    const int wbytes = (int)((size_t)c->split_W * sizeof(C));
+    auto kv = gemv_n_split<T, E::NT, E::SUR, true, false, Store<T>>;
+    auto ks = gemv_n_split<T, E::NT, E::SUR, false, false, Store<T>>;
+    if (wbytes > 48 * 1024) {   // strips above 48 KiB (CCG_SPLIT_KB): opt-in shared memory
+      cudaFuncSetAttribute(kv, cudaFuncAttributeMaxDynamicSharedMemorySize, wbytes);
+      cudaFuncSetAttribute(ks, cudaFuncAttributeMaxDynamicSharedMemorySize, wbytes);
+    }
     if (c->vec_ok)
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occs, gemv_n_split<T, E::NT, E::SUR, true, false, Store<T>>,
-                                                    NT, (size_t)c->split_W * sizeof(C));
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occs, kv, NT, (size_t)wbytes);
     else
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occs, gemv_n_split<T, E::NT, E::SUR, false, false, Store<T>>,
-                                                    NT, (size_t)c->split_W * sizeof(C));
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occs, ks, NT, (size_t)wbytes);
     if (occs < 1) occs = 1;
     const int64_t slots = (int64_t)c->sm_count * occs;
     // waves k: row blocks of >= 64 rows (x-strip reuse), CTAs = k·slots

@@ -232,6 +232,13 @@ enum { CCG_FALLBACK = 1000 };
 template <typename... KArgs, typename... Args>
 static void launch_k(ccg_ctx* c, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
                      Args&&... args) {
+  if (smem > 48 * 1024) {   // opt-in dynamic shared memory, once per kernel and handle (device)
+    int& big = c->occ_cache[reinterpret_cast<const void*>(kern)];
+    if (!(big & 2)) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      big |= 2;
+    }
+  }
   if (!c->pdl) {
     kern<<<grid, block, smem, s>>>(std::forward<Args>(args)...);
     return;
