@@ -142,8 +142,6 @@ static int choose_launch(ccg_ctx* c) {
     }
     nrb = std::min<int64_t>(nrb, std::max<int64_t>(1, c->mnloc / 8));
     c->split_nrb = (int)nrb;
-    const char* bf = getenv("CCG_BS_FUSE");
-    c->bs_fuse = bf ? atoi(bf) != 0 : 1;
     const char* fu = getenv("CCG_SPLIT_FUSE");
     c->split_fuse = fu ? atoi(fu) != 0 : 0;   // off: cfg3 1.3 % slower (last-CTA tail), cfg2 neutral
     if (c->rb_ticket_cap < c->split_nrb) {
@@ -204,8 +202,51 @@ static int choose_launch(ccg_ctx* c) {
     if (occ3 < 1) occ3 = 1;
     c->spmv_grid = (int)std::max<int64_t>(1, std::min<int64_t>(c->csr_nblocks, (int64_t)c->sm_count * occ3));
   }
+  size_t need_sym_h = 0;
+  if (c->opk == OPK_DENSE && c->sym_ok) {
+    // upper-triangle tiles: strips of NT·V columns × row blocks of H rows; the
+    // largest H (≤ SYM_HMAX) that still gives two waves of tiles (CCG_SYM_H)
+    const int64_t CW = (int64_t)NT * CT<T>::V;
+    c->sym_strips = (int)((c->n + CW - 1) / CW);
+    int occ_s = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_s, gemv_sym<T, E::NT, false>, NT, 0);
+    occ_s = std::max(1, occ_s);
+    auto ntiles = [&](int64_t H) {
+      int64_t t = 0;
+      for (int64_t cc = 0; cc < c->sym_strips; ++cc) t += (std::min((cc + 1) * CW, c->n) + H - 1) / H;
+      return t;
+    };
+    const char* he = getenv("CCG_SYM_H");
+    int64_t H = he ? atoi(he) : SYM_HMAX;
+    if (!he)
+      while (H > 32 && ntiles(H) < 2 * (int64_t)c->sm_count * occ_s) H /= 2;
+    H = std::max<int64_t>(8, std::min<int64_t>(SYM_HMAX, (H / 8) * 8));
+    c->sym_H = (int)H;
+    std::vector<int2> tl;
+    const int64_t nblk = (c->n + H - 1) / H;
+    for (int64_t I = 0; I < nblk; ++I)        // row-block major: concurrent CTAs read whole rows
+      for (int64_t cc = 0; cc < c->sym_strips; ++cc)
+        if (I * H < std::min((cc + 1) * CW, c->n)) tl.push_back(make_int2((int)cc, (int)I));
+    c->sym_ntiles = (int)tl.size();
+    if (c->sym_tiles) cudaFree(c->sym_tiles);
+    c->sym_tiles = nullptr;
+    CK(c, cudaMalloc(&c->sym_tiles, tl.size() * sizeof(int2)));
+    CK(c, cudaMemcpyAsync(c->sym_tiles, tl.data(), tl.size() * sizeof(int2), cudaMemcpyHostToDevice, c->stream));
+    CK(c, cudaStreamSynchronize(c->stream));
+    if (c->nstage2_grid <= 1)
+      c->nstage2_grid = (int)std::max<int64_t>(1, std::min<int64_t>((c->n + NT - 1) / NT, (int64_t)c->sm_count * 4));
+    const size_t need = (size_t)c->sym_strips * c->n * sizeof(C);
+    if (need > c->npart_bytes) {
+      if (c->npart) cudaFree(c->npart);
+      c->npart = nullptr;
+      CK(c, cudaMalloc(&c->npart, need));
+      c->npart_bytes = need;
+    }
+    need_sym_h = (size_t)nblk * c->n * sizeof(C);
+  }
   // workspace sized for the chosen grids
-  size_t need_hpart = (size_t)std::max(c->ah_S, c->cols_ok ? c->dual_S : 1) * (size_t)c->n * sizeof(C);
+  size_t need_hpart = std::max((size_t)std::max(c->ah_S, c->cols_ok ? c->dual_S : 1) * (size_t)c->n * sizeof(C),
+                               need_sym_h);
   if (c->opk == OPK_DENSE && need_hpart > c->hpart_bytes) {
     if (c->hpart) cudaFree(c->hpart);
     c->hpart = nullptr;
@@ -447,6 +488,13 @@ static int create_impl(ccg_handle* h, ccg_dtype dt, int64_t n, int world, int ra
   {
     const char* pe = getenv("CCG_PDL");
     c->pdl = !(pe && !strcmp(pe, "0"));
+    const char* bf = getenv("CCG_BS_FUSE");   // BiCGSTAB P/S folds into the dense split GEMV
+    c->bs_fuse = bf ? atoi(bf) != 0 : 1;
+    // the S fold on the stencil / SELL SpMV: measured slower at config 5
+    // (stencil 132 -> 155 us/it, CSR 211 -> 216: the latency-bound gathers
+    // take two loads per neighbour), so opt-in
+    const char* br = getenv("CCG_BS_FUSE_RO");
+    c->bs_fuse_ro = br ? atoi(br) != 0 : 0;
   }
   auto bail = [&](int code) {
     g_create_err = c->err;
@@ -608,11 +656,18 @@ int ccg_set_matvec_dense(ccg_handle c, const void* A_local, int64_t row0, int64_
   c->flags = flags;
   c->vec_ok = (c->esz == 16) || (((uintptr_t)A_local % 16) == 0 && (lda % 2) == 0);
   {
+    // complex-symmetric A (caller's assertion, one rank): products from the
+    // upper triangle only (matvec.cuh gemv_sym; CCG_SYMV=0 reads all of A)
+    const char* sv = getenv("CCG_SYMV");
+    c->sym_ok = (flags & CCG_FLAG_SYMMETRIC) && !c->dist && c->vec_ok && (c->n % (16 / c->esz == 2 ? 2 : 1)) == 0 &&
+                !(sv && !strcmp(sv, "0"));
+  }
+  {
     // L2-resident rows (matvec.cuh): ~80 MB of A kept in the
     // 126 MB L2 between the products of a solve; 0 when A is >> L2
     const char* pe = getenv("CCG_L2_PIN_MB");
     const double pin_bytes = (pe ? atof(pe) : 80.0) * 1e6;
-    const double abytes = (double)nloc * (double)c->n * (double)c->esz;
+    const double abytes = (double)nloc * (double)c->n * (double)c->esz * (c->sym_ok ? 0.5 : 1.0);
     c->l2_pin = pin_bytes <= 0 || abytes < 32e6 ? 0      // small A stays in L2 without help
                 : abytes <= pin_bytes ? 64 : (int)floor(64.0 * pin_bytes / abytes);
   }
@@ -1287,6 +1342,7 @@ int ccg_destroy(ccg_handle c) {
   if (c->rep_parts) cudaFree(c->rep_parts);
   if (c->hpart) cudaFree(c->hpart);
   if (c->npart) cudaFree(c->npart);
+  if (c->sym_tiles) cudaFree(c->sym_tiles);
   free_csr_copies(c);
   if (c->part) cudaFree(c->part);
   if (c->hist) cudaFree(c->hist);

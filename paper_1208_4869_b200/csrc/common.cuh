@@ -48,16 +48,34 @@ template <typename C> __device__ __forceinline__ C czero() { C r; r.x = 0; r.y =
 template <typename C> __device__ __forceinline__ C cadd(C a, C b) { C r; r.x = a.x + b.x; r.y = a.y + b.y; return r; }
 template <typename C> __device__ __forceinline__ C csub(C a, C b) { C r; r.x = a.x - b.x; r.y = a.y - b.y; return r; }
 template <typename C> __device__ __forceinline__ C cconj(C a) { C r; r.x = a.x; r.y = -a.y; return r; }
+// Real products that the compiler may not contract into an FMA (__fmul_rn /
+// __dmul_rn): the vector updates below then round the same way in every
+// kernel that inlines them, so a value formed in one kernel (a fused input
+// transform, methods.cuh BsSIn) and recomputed in another (its epilogue) are
+// the same bits — with plain `a*b - c*d` nvcc picks the contraction per call
+// site.
+__device__ __forceinline__ float rmul(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ double rmul(double a, double b) { return __dmul_rn(a, b); }
 template <typename C> __device__ __forceinline__ C cmul(C a, C b) {
+  C r; r.x = rmul(a.x, b.x) - rmul(a.y, b.y); r.y = rmul(a.x, b.y) + rmul(a.y, b.x); return r;
+}
+// contractible product (FFT butterflies: no value there is recomputed elsewhere)
+template <typename C> __device__ __forceinline__ C cmulc(C a, C b) {
   C r; r.x = a.x * b.x - a.y * b.y; r.y = a.x * b.y + a.y * b.x; return r;
 }
 // a + s*b
 template <typename C> __device__ __forceinline__ C caxpy(C a, C s, C b) {
-  C r; r.x = a.x + (s.x * b.x - s.y * b.y); r.y = a.y + (s.x * b.y + s.y * b.x); return r;
+  C r;
+  r.x = a.x + (rmul(s.x, b.x) - rmul(s.y, b.y));
+  r.y = a.y + (rmul(s.x, b.y) + rmul(s.y, b.x));
+  return r;
 }
 // a - s*b
 template <typename C> __device__ __forceinline__ C caxmy(C a, C s, C b) {
-  C r; r.x = a.x - (s.x * b.x - s.y * b.y); r.y = a.y - (s.x * b.y + s.y * b.x); return r;
+  C r;
+  r.x = a.x - (rmul(s.x, b.x) - rmul(s.y, b.y));
+  r.y = a.y - (rmul(s.x, b.y) + rmul(s.y, b.x));
+  return r;
 }
 // acc += a*b (4 FMAs)
 template <typename C> __device__ __forceinline__ void cfma(C& acc, C a, C b) {

@@ -130,6 +130,7 @@ struct ccg_ctx {
   int gemv_mode = 0;      // GEMV_SPLIT (default) | GEMV_BULK | GEMV_ROWS (env CCG_GEMV)
   int split_W = 0, split_strips = 1, split_nrb = 1, nstage2_grid = 1, split_ur = 8;
   int bs_fuse = 1;        // BiCGSTAB P/S passes folded into the products (Engine::in_fuse_ok; CCG_BS_FUSE)
+  int bs_fuse_ro = 0;     // the S fold on the stencil / SELL SpMV (Engine::in_fuse_ro_ok; CCG_BS_FUSE_RO)
   int split_fuse = 0;     // several strips: strip sum + epilogue by the last CTA of each row block (CCG_SPLIT_FUSE)
   unsigned* rb_ticket = nullptr;   // [split_nrb] arrival tickets (zero between launches)
   int rb_ticket_cap = 0;
@@ -140,6 +141,11 @@ struct ccg_ctx {
   bool pin_on = false;    // inside ccg_solve (dense operator)
   void* npart = nullptr;  // [strips][nloc] partial row sums of the split / column-owner GEMV
   size_t npart_bytes = 0;
+  // complex-symmetric dense A (CCG_FLAG_SYMMETRIC, one rank): upper-triangle
+  // products (matvec.cuh gemv_sym; CCG_SYMV=0 disables)
+  bool sym_ok = false;
+  int sym_H = 64, sym_ntiles = 0, sym_strips = 1;
+  int2* sym_tiles = nullptr;
   // workspace
   State* st = nullptr;
   State* st_host = nullptr;  // pinned
@@ -406,7 +412,7 @@ struct Engine {
       auto k = c->sell_one ? spmv_sell_kernel<T, NT, CONJ, true, Epi> : spmv_sell_kernel<T, NT, CONJ, false, Epi>;
       launch_k(c, k, c->sell_grid[c->sell_one], NT, 0, c->stream,
           c->sell_off, c->sell_width, c->sell_col, reinterpret_cast<const C*>(c->sell_val), x, c->mnloc, epi,
-          make_red(c), c->st, gate);
+          make_red(c), c->st, gate, XLoad<T>{});
     }
     else if (c->csr_blocks)
       launch_k(c, spmv_stream_kernel<T, NT, SNNZ, CONJ, Epi>, c->spmv_grid, NT, 0, c->stream, 
@@ -427,7 +433,7 @@ struct Engine {
     }
     dim3 g((c->snx + 31) / 32, (c->sny + 7) / 8, (c->snzl + c->szc - 1) / c->szc);
     launch_k(c, stencil7_kernel<T, Epi>, g, 256, 0, c->stream, xfull, c->snx, c->sny, c->snz, c->sz0, c->snzl, c->szc,
-                                                       k[0], k[1], k[2], k[3], epi, make_red(c), c->st, gate);
+                                                       k[0], k[1], k[2], k[3], epi, make_red(c), c->st, gate, XLoad<T>{});
   }
 
   // FFT block-Toeplitz product (fft.cuh); op: 0 = A, 1 = Aᴴ, 2 = Aᵀ.  Every
@@ -560,13 +566,42 @@ struct Engine {
   // with several strips and the strip sum in its own kernel (the epilogue that
   // rewrites the transformed vectors runs after every CTA has staged them)
   static bool in_fuse_ok(const ccg_ctx* c) {
-    return c->bs_fuse && c->opk == OPK_DENSE && c->gemv_mode == GEMV_SPLIT && c->split_strips > 1 &&
+    return c->bs_fuse && c->opk == OPK_DENSE && !c->sym_ok && c->gemv_mode == GEMV_SPLIT && c->split_strips > 1 &&
            !c->split_fuse && !c->dist && !c->jac_active;
+  }
+  // input transforms that read only vectors the product does not write
+  // (BiCGSTAB's s = r − αv): also the stencil and the SELL SpMV, whose
+  // neighbouring CTAs read the same inputs — single GPU (no halo of r, v)
+  static bool in_fuse_ro_ok(const ccg_ctx* c) {
+    if (in_fuse_ok(c)) return true;
+    return c->bs_fuse_ro && !c->dist && !c->jac_active &&
+           (c->opk == OPK_STENCIL || (c->opk == OPK_CSR && c->sell_col));
   }
 
   // y = A·x with x_j = xin(j) formed while the split GEMV stages its strips
+  // (or, for in_fuse_ro_ok transforms, while the stencil / SELL SpMV loads it)
   template <class XIn, class Epi>
   static int matvec_a_in(ccg_ctx* c, XIn xin, Epi epi, const int* gate) {
+    if (c->opk == OPK_STENCIL || c->opk == OPK_CSR) {
+      tev_begin(c, 0);
+      if (c->opk == OPK_STENCIL) {
+        C k[4];
+        for (int i = 0; i < 4; ++i) { k[i].x = (T)c->scoef[i].x; k[i].y = (T)c->scoef[i].y; }
+        dim3 g((c->snx + 31) / 32, (c->sny + 7) / 8, (c->snzl + c->szc - 1) / c->szc);
+        launch_k(c, stencil7_kernel<T, Epi, XIn>, g, 256, 0, c->stream, static_cast<const C*>(nullptr), c->snx,
+                 c->sny, c->snz, c->sz0, c->snzl, c->szc, k[0], k[1], k[2], k[3], epi, make_red(c), c->st, gate, xin);
+      } else {
+        auto k = c->sell_one ? spmv_sell_kernel<T, NT, false, true, Epi, XIn>
+                             : spmv_sell_kernel<T, NT, false, false, Epi, XIn>;
+        launch_k(c, k, c->sell_grid[c->sell_one], NT, 0, c->stream, c->sell_off, c->sell_width, c->sell_col,
+                 reinterpret_cast<const C*>(c->sell_val), static_cast<const C*>(nullptr), c->mnloc, epi, make_red(c),
+                 c->st, gate, xin);
+      }
+      c->launches++;
+      tev_end(c);
+      CK(c, cudaGetLastError());
+      return CCG_OK;
+    }
     const C* A = reinterpret_cast<const C*>(c->A);
     C* part = reinterpret_cast<C*>(c->npart);
     dim3 g(c->split_strips, c->split_nrb);
@@ -591,6 +626,23 @@ struct Engine {
     return CCG_OK;
   }
 
+  // complex-symmetric dense product from the upper triangle (gemv_sym):
+  // conj => Aᴴx = conj(A)·x; Aᵀ = A
+  template <class Epi>
+  static void sym_product(ccg_ctx* c, const C* x, bool conj, Epi epi, const int* gate) {
+    const C* A = reinterpret_cast<const C*>(c->A);
+    C* np = reinterpret_cast<C*>(c->npart);
+    C* hp = reinterpret_cast<C*>(c->hpart);
+    if (conj)
+      launch_k(c, gemv_sym<T, NT, true>, c->sym_ntiles, NT, 0, c->stream, A, c->lda, x, c->n, c->sym_H,
+               static_cast<const int2*>(c->sym_tiles), np, hp, gate, pin(c));
+    else
+      launch_k(c, gemv_sym<T, NT, false>, c->sym_ntiles, NT, 0, c->stream, A, c->lda, x, c->n, c->sym_H,
+               static_cast<const int2*>(c->sym_tiles), np, hp, gate, pin(c));
+    launch_k(c, gemv_sym_stage2<T, NT, Epi>, c->nstage2_grid, NT, 0, c->stream, static_cast<const C*>(np),
+             static_cast<const C*>(hp), c->n, c->sym_H, NT * CT<T>::V, c->sym_strips, epi, make_red(c), c->st, gate);
+  }
+
   // this rank's rows of A·x (all operators), epilogue per row
   template <class Epi>
   static int matvec_rows(ccg_ctx* c, const C* xfull, Epi epi, const int* gate) {
@@ -599,6 +651,9 @@ struct Engine {
       toeplitz(c, xfull, 0, epi, gate);
     } else if (c->opk == OPK_STENCIL) {
       stencil(c, xfull, false, epi, gate);
+    } else if (c->opk == OPK_DENSE && c->sym_ok) {
+      sym_product(c, xfull, false, epi, gate);
+      c->launches++;   // + the stage-2 launch counted below
     } else if (c->opk == OPK_DENSE && c->gemv_mode == GEMV_SPLIT) {
       const C* A = reinterpret_cast<const C*>(c->A);
       C* part = reinterpret_cast<C*>(c->npart);
@@ -730,6 +785,14 @@ struct Engine {
       CK(c, cudaGetLastError());
       if (c->rep) return rep_finish_rows(c, epi, gate);
       return post<Epi>(c, gate);
+    }
+    if (c->sym_ok) {   // one rank, A = Aᵀ: Aᵀx = A·x, Aᴴx = conj(A)·x from the upper triangle
+      tev_begin(c, 1);
+      sym_product(c, xloc, conj, epi, gate);
+      c->launches += 2;
+      tev_end(c);
+      CK(c, cudaGetLastError());
+      return CCG_OK;
     }
     const C* A = reinterpret_cast<const C*>(c->A);
     C* part = reinterpret_cast<C*>(c->hpart);

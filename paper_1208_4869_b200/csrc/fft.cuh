@@ -69,9 +69,9 @@ __device__ void fft_dit(C* buf, int logL, int TX, bool inv, const C* __restrict_
       const C w3 = twiddle(tw, (m + h) << (logL - s - 2), twstride, inv);
       const C x0 = buf[i0 * TX + t], x1 = buf[(i0 + h) * TX + t];
       const C x2 = buf[(i0 + 2 * h) * TX + t], x3 = buf[(i0 + 3 * h) * TX + t];
-      const C p1 = cmul(x1, w1), p3 = cmul(x3, w1);
+      const C p1 = cmulc(x1, w1), p3 = cmulc(x3, w1);
       const C a0 = cadd(x0, p1), a1 = csub(x0, p1), a2 = cadd(x2, p3), a3 = csub(x2, p3);
-      const C q2 = cmul(a2, w2), q3 = cmul(a3, w3);
+      const C q2 = cmulc(a2, w2), q3 = cmulc(a3, w3);
       buf[i0 * TX + t] = cadd(a0, q2);
       buf[(i0 + 2 * h) * TX + t] = csub(a0, q2);
       buf[(i0 + h) * TX + t] = cadd(a1, q3);
@@ -88,7 +88,7 @@ __device__ void fft_dit(C* buf, int logL, int TX, bool inv, const C* __restrict_
       const int i0 = ((q >> s) << (s + 1)) + m, i1 = i0 + h;
       const C w = twiddle(tw, m << (logL - s - 1), twstride, inv);
       const C a = buf[i0 * TX + t];
-      const C bb = cmul(buf[i1 * TX + t], w);
+      const C bb = cmulc(buf[i1 * TX + t], w);
       buf[i0 * TX + t] = cadd(a, bb);
       buf[i1 * TX + t] = csub(a, bb);
     }
@@ -115,12 +115,12 @@ __device__ void fft_dif(C* buf, int logL, int TX, bool inv, const C* __restrict_
       const C wc = twiddle(tw, m << (logL - s), twstride, inv);
       const C x0 = buf[i0 * TX + t], x1 = buf[(i0 + hh) * TX + t];
       const C x2 = buf[(i0 + H) * TX + t], x3 = buf[(i0 + H + hh) * TX + t];
-      const C a0 = cadd(x0, x2), a2 = cmul(csub(x0, x2), wa);
-      const C a1 = cadd(x1, x3), a3 = cmul(csub(x1, x3), wb);
+      const C a0 = cadd(x0, x2), a2 = cmulc(csub(x0, x2), wa);
+      const C a1 = cadd(x1, x3), a3 = cmulc(csub(x1, x3), wb);
       buf[i0 * TX + t] = cadd(a0, a1);
-      buf[(i0 + hh) * TX + t] = cmul(csub(a0, a1), wc);
+      buf[(i0 + hh) * TX + t] = cmulc(csub(a0, a1), wc);
       buf[(i0 + H) * TX + t] = cadd(a2, a3);
-      buf[(i0 + H + hh) * TX + t] = cmul(csub(a2, a3), wc);
+      buf[(i0 + H + hh) * TX + t] = cmulc(csub(a2, a3), wc);
     }
   }
   if (s == 0) {                         // odd last stage
@@ -133,7 +133,7 @@ __device__ void fft_dif(C* buf, int logL, int TX, bool inv, const C* __restrict_
       const C a = buf[i0 * TX + t];
       const C bb = buf[i1 * TX + t];
       buf[i0 * TX + t] = cadd(a, bb);
-      buf[i1 * TX + t] = cmul(csub(a, bb), w);
+      buf[i1 * TX + t] = cmulc(csub(a, bb), w);
     }
   }
   __syncthreads();
@@ -223,7 +223,7 @@ fft_z_mul(typename CT<T>::c* __restrict__ W, const typename CT<T>::c* __restrict
     } else {
       ki = ((int64_t)k * g.Y2 + ky) * g.X2 + kx0 + t;
     }
-    buf[k * TX + t] = cmul(buf[k * TX + t], __ldg(Kh + ki));
+    buf[k * TX + t] = cmulc(buf[k * TX + t], __ldg(Kh + ki));
   }
   fft_dif(buf, g.lz, TX, true, tw, twstride);
   for (int e = threadIdx.x; e < TX * g.nz; e += blockDim.x) {

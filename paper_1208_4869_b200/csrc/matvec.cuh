@@ -353,6 +353,15 @@ struct XLoad {
   __device__ void load(const State*) {}
   __device__ C operator()(const C* x, int64_t j) const { return x[j]; }
 };
+template <class XIn> struct is_xload : std::false_type {};
+template <typename T> struct is_xload<XLoad<T>> : std::true_type {};
+// a gathered input element: the read-only-path load for the plain vector,
+// else the method's input transform
+template <class XIn, typename C>
+__device__ __forceinline__ C xgather(const XIn& xin, const C* __restrict__ x, int64_t j) {
+  if constexpr (is_xload<XIn>::value) return __ldg(x + j);
+  else return xin(x, j);
+}
 
 template <typename T, int NT, int UR, bool VEC, bool FUSED, class Epi, class XIn = XLoad<T>>
 __global__ void __launch_bounds__(NT)
@@ -668,6 +677,136 @@ gemv_cols(const typename CT<T>::c* __restrict__ A, int64_t lda,
   }
 }
 
+// ---------------------------------------------------------------------------
+// K1s gemv_sym: y = A·x (CONJ: y = conj(A)·x = Aᴴx) for complex-symmetric
+// A = Aᵀ (CCG_FLAG_SYMMETRIC, one rank holding every row), reading only the
+// upper triangle j ≥ i — half of A's bytes per product:
+//   y_i = Σ_{j ≥ i} A_ij x_j + Σ_{j < i} A_ji x_j     (A_ij = A_ji).
+// Tiles (strip c of CW = NT·V columns, row block I of H rows) of the upper
+// triangle only (host table `tiles`, row-block major).  As in gemv_cols, thread
+// t owns the 16-byte column chunk t of the strip and walks the tile's rows 8 at
+// a time (8 independent 16-B loads in flight); each element feeds
+//   N: the row dot Σ_j A_ij x_j of row i   (j ≥ i)      -> npart[c][i]
+//   H: the column sum Σ_i A_ij x_i of col j (i < j)      -> hpart[I][j]
+// (the diagonal-straddling tiles mask by selects; the others do not test).
+// gemv_sym_stage2 sums both in a fixed order (deterministic).
+// ---------------------------------------------------------------------------
+constexpr int SYM_HMAX = 512;
+template <typename T, int NT, bool CONJ>
+__global__ void __launch_bounds__(NT)
+gemv_sym(const typename CT<T>::c* __restrict__ A, int64_t lda, const typename CT<T>::c* __restrict__ x, int64_t n,
+         int H, const int2* __restrict__ tiles, typename CT<T>::c* __restrict__ npart,
+         typename CT<T>::c* __restrict__ hpart, const int* gate, int pin) {
+  using C = typename CT<T>::c;
+  using LV = typename CT<T>::v;
+  constexpr int V = CT<T>::V;
+  constexpr int UR = 8;
+  constexpr int CW = NT * V;
+  if (pdl_gate(gate)) return;
+  __shared__ C xs[SYM_HMAX];
+  __shared__ C red[2][NT / 32][UR];
+  const int2 tl = tiles[blockIdx.x];
+  const int c = tl.x, I = tl.y;
+  const int64_t cbeg = (int64_t)c * CW, cend = min(cbeg + CW, n);
+  const int64_t r0 = (int64_t)I * H, r1 = min(r0 + H, cend);
+  const int rn = (int)(r1 - r0);
+  const int64_t jv = (int64_t)c * NT + threadIdx.x;   // 16-byte chunk index
+  const bool active = jv < n / V;
+  const int64_t jc = active ? jv : 0;
+  const int64_t j0 = jc * V;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t ldv = lda / V;
+  C xr[V], hacc[V];
+#pragma unroll
+  for (int v = 0; v < V; ++v) { xr[v] = x[j0 + v]; hacc[v] = czero<C>(); }
+  for (int t = threadIdx.x; t < rn; t += NT) xs[t] = x[r0 + t];
+  __syncthreads();
+  const LV* Ab = reinterpret_cast<const LV*>(A) + jc;
+  int buf = 0;
+  auto body = [&](auto ld, auto dg) {
+    constexpr bool DG = decltype(dg)::value;
+    for (int t = 0; t < rn; t += UR) {
+      const int nr = min(UR, rn - t);
+      LV a[UR];
+#pragma unroll
+      for (int u = 0; u < UR; ++u) {
+        const int64_t row = r0 + t + min(u, nr - 1);
+        a[u] = ld(Ab + row * ldv, row);
+      }
+      C rp[UR];
+#pragma unroll
+      for (int u = 0; u < UR; ++u) {
+        C ac[V];
+        unpack(a[u], ac);
+        const int64_t row = r0 + t + u;
+        const C xi = xs[t + min(u, nr - 1)];
+        rp[u] = czero<C>();
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+          const bool n_ok = active && (!DG || j0 + v >= row);
+          const bool h_ok = active && u < nr && (!DG || j0 + v > row);
+          C tn = rp[u], th = hacc[v];
+          if (CONJ) { cfmac(tn, ac[v], xr[v]); cfmac(th, ac[v], xi); }
+          else { cfma(tn, ac[v], xr[v]); cfma(th, ac[v], xi); }
+          rp[u].x = n_ok ? tn.x : rp[u].x; rp[u].y = n_ok ? tn.y : rp[u].y;
+          hacc[v].x = h_ok ? th.x : hacc[v].x; hacc[v].y = h_ok ? th.y : hacc[v].y;
+        }
+      }
+      warp_transpose_reduce<UR>(rp, lane);   // lane L: warp sum of row L >> 2
+      if ((lane & 3) == 0) red[buf][warp][lane >> 2] = rp[0];
+      __syncthreads();
+      if (threadIdx.x < nr) {
+        C sum = red[buf][0][threadIdx.x];
+#pragma unroll
+        for (int w = 1; w < NT / 32; ++w) sum = cadd(sum, red[buf][w][threadIdx.x]);
+        npart[(int64_t)c * n + r0 + t + threadIdx.x] = sum;
+      }
+      buf ^= 1;
+    }
+  };
+  const bool diag = r1 > cbeg;   // the tile reaches the diagonal: masks
+  if (pin > 0) {
+    if (diag) body(make_ldpin(pin), std::true_type{}); else body(make_ldpin(pin), std::false_type{});
+  } else {
+    if (diag) body(LdA{}, std::true_type{}); else body(LdA{}, std::false_type{});
+  }
+  if (active) {
+#pragma unroll
+    for (int v = 0; v < V; ++v) hpart[(int64_t)I * n + j0 + v] = hacc[v];
+  }
+}
+
+// y_i = Σ_{c ≥ c(i)} npart[c][i] + Σ_{I < nb(c(i))} hpart[I][i] (fp64, fixed
+// order), then the epilogue; c(i) = i / CW, nb(c) = the row blocks of strip c
+template <typename T, int NT, class Epi>
+__global__ void __launch_bounds__(NT)
+gemv_sym_stage2(const typename CT<T>::c* __restrict__ npart, const typename CT<T>::c* __restrict__ hpart, int64_t n,
+                int H, int CW, int nstrips, Epi epi, Red red, State* st, const int* gate) {
+  using C = typename CT<T>::c;
+  constexpr int KK = Epi::K > 0 ? Epi::K : 1;
+  if (pdl_gate(gate)) return;
+  epi.load(st);
+  double2 dacc[KK];
+#pragma unroll
+  for (int k = 0; k < KK; ++k) dacc[k] = make_double2(0.0, 0.0);
+  for (int64_t i = (int64_t)blockIdx.x * NT + threadIdx.x; i < n; i += (int64_t)gridDim.x * NT) {
+    const int ci = (int)(i / CW);
+    double2 w = make_double2(0.0, 0.0);
+    for (int c = ci; c < nstrips; ++c) {
+      const C p = __ldcs(npart + (int64_t)c * n + i);
+      w.x += (double)p.x; w.y += (double)p.y;
+    }
+    const int64_t cend = min((int64_t)(ci + 1) * CW, n);
+    const int nb = (int)((cend + H - 1) / H);
+    for (int b = 0; b < nb; ++b) {
+      const C p = __ldcs(hpart + (int64_t)b * n + i);
+      w.x += (double)p.x; w.y += (double)p.y;
+    }
+    epi(i, fromd2<C>(w), dacc);
+  }
+  if constexpr (Epi::K > 0) finish_reduction<KK, NT, Epi>(dacc, red, st);
+}
+
 // K2 stage 2: w_j = Σ_s part[s][off + j] in split order, then epilogue.
 template <typename T, int NT, class Epi>
 __global__ void __launch_bounds__(NT)
@@ -832,9 +971,9 @@ spmv_stream_kernel(const int32_t* __restrict__ rowptr, const int32_t* __restrict
 // values and x gathers are issued before any arithmetic (padding: col = −1,
 // gather clamped to index 0 and its product skipped), then the products are
 // accumulated by FMA in CSR column order
-template <int W, bool CONJ, typename C>
+template <int W, bool CONJ, typename C, class XIn>
 __device__ __forceinline__ C sell_row(const int32_t* __restrict__ scol, const C* __restrict__ sval,
-                                      const C* __restrict__ x, int64_t base) {
+                                      const C* __restrict__ x, int64_t base, const XIn& xin) {
   int col[W];
 #pragma unroll
   for (int u = 0; u < W; ++u) col[u] = __ldcs(scol + base + 32 * (int64_t)u);
@@ -842,7 +981,7 @@ __device__ __forceinline__ C sell_row(const int32_t* __restrict__ scol, const C*
 #pragma unroll
   for (int u = 0; u < W; ++u) {
     v[u] = __ldcs(sval + base + 32 * (int64_t)u);
-    xv[u] = __ldg(x + max(col[u], 0));
+    xv[u] = xgather(xin, x, max(col[u], 0));
   }
   C acc = czero<C>();
 #pragma unroll
@@ -861,17 +1000,19 @@ __device__ __forceinline__ C sell_row(const int32_t* __restrict__ scol, const C*
 // ONE = true — one row per step with "≥ 3 CTAs/SM" in the launch bounds, under
 // which ptxas issues all 14 loads of a row before its arithmetic (78-94
 // registers): c128 SpMV 64.6 → 57.9 µs at config 5 (cold ncu), the default.
-template <typename T, int NT, bool CONJ, bool ONE, class Epi>
+// XIn: input transform of the gathered x (see stencil7_kernel); CONJ = false only
+template <typename T, int NT, bool CONJ, bool ONE, class Epi, class XIn = XLoad<T>>
 __global__ void __launch_bounds__(NT, ONE ? 3 : 0)
 spmv_sell_kernel(const int64_t* __restrict__ soff, const int32_t* __restrict__ swidth,
                  const int32_t* __restrict__ scol, const typename CT<T>::c* __restrict__ sval,
                  const typename CT<T>::c* __restrict__ x, int64_t nrows, Epi epi, Red red, State* st,
-                 const int* gate) {
+                 const int* gate, XIn xin) {
   using C = typename CT<T>::c;
   constexpr int KK = Epi::K > 0 ? Epi::K : 1;
   constexpr int U = 8;
   if (pdl_gate(gate)) return;
   epi.load(st);
+  xin.load(st);
   double2 dacc[KK];
 #pragma unroll
   for (int k = 0; k < KK; ++k) dacc[k] = make_double2(0.0, 0.0);
@@ -896,8 +1037,8 @@ spmv_sell_kernel(const int64_t* __restrict__ soff, const int32_t* __restrict__ s
     C v1[7], v2[7], x1[7], x2[7];
 #pragma unroll
     for (int u = 0; u < 7; ++u) {
-      v1[u] = __ldcs(sval + b1 + 32 * u); x1[u] = __ldg(x + max(c1[u], 0));
-      v2[u] = __ldcs(sval + b2 + 32 * u); x2[u] = __ldg(x + max(c2[u], 0));
+      v1[u] = __ldcs(sval + b1 + 32 * u); x1[u] = xgather(xin, x, max(c1[u], 0));
+      v2[u] = __ldcs(sval + b2 + 32 * u); x2[u] = xgather(xin, x, max(c2[u], 0));
     }
     C a1 = czero<C>(), a2 = czero<C>();
 #pragma unroll
@@ -921,14 +1062,14 @@ spmv_sell_kernel(const int64_t* __restrict__ soff, const int32_t* __restrict__ s
     C acc;
     switch (w) {   // warp-uniform: the whole slice shares its width
       case 0: acc = czero<C>(); break;
-      case 1: acc = sell_row<1, CONJ>(scol, sval, x, base); break;
-      case 2: acc = sell_row<2, CONJ>(scol, sval, x, base); break;
-      case 3: acc = sell_row<3, CONJ>(scol, sval, x, base); break;
-      case 4: acc = sell_row<4, CONJ>(scol, sval, x, base); break;
-      case 5: acc = sell_row<5, CONJ>(scol, sval, x, base); break;
-      case 6: acc = sell_row<6, CONJ>(scol, sval, x, base); break;
-      case 7: acc = sell_row<7, CONJ>(scol, sval, x, base); break;
-      case 8: acc = sell_row<8, CONJ>(scol, sval, x, base); break;
+      case 1: acc = sell_row<1, CONJ>(scol, sval, x, base, xin); break;
+      case 2: acc = sell_row<2, CONJ>(scol, sval, x, base, xin); break;
+      case 3: acc = sell_row<3, CONJ>(scol, sval, x, base, xin); break;
+      case 4: acc = sell_row<4, CONJ>(scol, sval, x, base, xin); break;
+      case 5: acc = sell_row<5, CONJ>(scol, sval, x, base, xin); break;
+      case 6: acc = sell_row<6, CONJ>(scol, sval, x, base, xin); break;
+      case 7: acc = sell_row<7, CONJ>(scol, sval, x, base, xin); break;
+      case 8: acc = sell_row<8, CONJ>(scol, sval, x, base, xin); break;
       default: {
         acc = czero<C>();
         for (int j0 = 0; j0 < w; j0 += U) {
@@ -942,7 +1083,7 @@ spmv_sell_kernel(const int64_t* __restrict__ soff, const int32_t* __restrict__ s
           }
           C xv[U];
 #pragma unroll
-          for (int u = 0; u < U; ++u) xv[u] = col[u] >= 0 ? __ldg(x + col[u]) : czero<C>();
+          for (int u = 0; u < U; ++u) xv[u] = col[u] >= 0 ? xgather(xin, x, col[u]) : czero<C>();
 #pragma unroll
           for (int u = 0; u < U; ++u) {
             if (col[u] >= 0) {
@@ -1006,15 +1147,22 @@ __device__ __forceinline__ void st_term(C& acc, C coef, C v, bool has) {
   acc.y = has ? t.y : acc.y;
 }
 
-template <typename T, class Epi>
+// XIn: input transform (as in gemv_n_split) — each lattice value is formed as
+// xin(x, j) from other vectors (BiCGSTAB's s = r − αv, methods.cuh BsSIn), so
+// the vector pass that would store it first is not a launch of its own; the
+// epilogue stores the element for its own point.  Only transforms that read
+// vectors this kernel does not write (no ping-pong needed between CTAs).
+template <typename T, class Epi, class XIn = XLoad<T>>
 __global__ void __launch_bounds__(256)
 stencil7_kernel(const typename CT<T>::c* __restrict__ x, int nx, int ny, int nz, int z0, int nzl, int zc,
                 typename CT<T>::c d, typename CT<T>::c ox, typename CT<T>::c oy, typename CT<T>::c oz,
-                Epi epi, Red red, State* st, const int* gate) {
+                Epi epi, Red red, State* st, const int* gate, XIn xin) {
   using C = typename CT<T>::c;
   constexpr int KK = Epi::K > 0 ? Epi::K : 1;
+  constexpr bool PLAIN = std::is_same<XIn, XLoad<T>>::value;
   if (pdl_gate(gate)) return;
   epi.load(st);
+  xin.load(st);
   double2 dacc[KK];
 #pragma unroll
   for (int k = 0; k < KK; ++k) dacc[k] = make_double2(0.0, 0.0);
@@ -1028,11 +1176,17 @@ stencil7_kernel(const typename CT<T>::c* __restrict__ x, int nx, int ny, int nz,
     const C zero = czero<C>();
     int zg = z0 + zb;
     const C* xp = x + (int64_t)zg * plane + ix + nx * iy;
+    int64_t gi = (int64_t)zg * plane + ix + nx * iy;    // global (input) index
     int64_t li = (int64_t)zb * plane + ix + nx * iy;    // local (epilogue) index
+    // lattice value at offset o from the current point
+    auto X = [&](int o) -> C {
+      if constexpr (PLAIN) return xp[o];
+      else return xin(x, gi + o);
+    };
     using EP = EpiPre<Epi>;
     typename EP::P pnext = EP::pre(epi, li);   // the epilogue's inputs, a plane ahead
-    C below = zg > 0 ? xp[-plane] : zero;
-    C cur = xp[0];
+    C below = zg > 0 ? X(-plane) : zero;
+    C cur = X(0);
 #pragma unroll 4
     for (int zl = zb; zl < ze; ++zl, ++zg) {
       const typename EP::P pcur = pnext;
@@ -1040,11 +1194,11 @@ stencil7_kernel(const typename CT<T>::c* __restrict__ x, int nx, int ny, int nz,
       const bool hzm = zg > 0, hzp = zg < nz - 1;
       // every load of the plane first (masked to zero), then the terms in
       // ascending column order
-      const C above = hzp ? xp[plane] : zero;
-      const C ym = hym ? xp[-nx] : zero;
-      const C xm = hxm ? xp[-1] : zero;
-      const C xq = hxp ? xp[1] : zero;
-      const C yq = hyp ? xp[nx] : zero;
+      const C above = hzp ? X(plane) : zero;
+      const C ym = hym ? X(-nx) : zero;
+      const C xm = hxm ? X(-1) : zero;
+      const C xq = hxp ? X(1) : zero;
+      const C yq = hyp ? X(nx) : zero;
       C acc = zero;
       st_term(acc, oz, below, hzm);
       st_term(acc, oy, ym, hym);
@@ -1057,6 +1211,7 @@ stencil7_kernel(const typename CT<T>::c* __restrict__ x, int nx, int ny, int nz,
       below = cur;
       cur = above;
       xp += plane;
+      gi += plane;
       li += plane;
     }
   }

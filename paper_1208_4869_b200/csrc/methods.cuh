@@ -223,7 +223,8 @@ struct BsT {  // t = A s ; ⟨t,s⟩, ⟨t,t⟩ ; ω
 };
 
 // ---- BiCGSTAB with the P and S passes folded into the products (single GPU,
-// dense split GEMV with several strips; Engine::matvec_a_in).  The GEMV forms
+// dense split GEMV with several strips; Engine::matvec_a_in; the S fold alone
+// also on the stencil and the SELL SpMV, Engine::in_fuse_ro_ok).  The GEMV forms
 // each staged x element with BsPIn / BsSIn while it loads the strip, and the
 // strip-sum epilogue (after every CTA has read the old vectors) recomputes the
 // same element for its own row and stores it: 5 launches per iteration
@@ -266,7 +267,8 @@ struct BsSIn {   // staged element of s = r − αv
   const C* r; const C* v;
   C alpha;
   __device__ void load(const State* st) { alpha = fromd2<C>(st->alpha); }
-  __device__ C operator()(const C*, int64_t j) const { return caxmy(r[j], alpha, v[j]); }
+  // r and v are read-only for the whole product (the non-coherent path)
+  __device__ C operator()(const C*, int64_t j) const { return caxmy(__ldg(r + j), alpha, __ldg(v + j)); }
 };
 
 template <typename T>

@@ -21,6 +21,10 @@ int Engine<T>::bicgstab_iter(ccg_ctx* c) {
   TRY(pass(c, BsP<T>{L(c, 2), Fs(c, 0), L(c, 4)}, g));
   TRY(allgather(c, 0));
   TRY(matvec_a(c, F(c, 0), BsV<T>{L(c, 4), L(c, 3)}, g));
+  if (in_fuse_ro_ok(c)) {   // stencil / SELL: s = r − αv formed inside t = A s (BsSIn / BsT2)
+    TRY(matvec_a_in(c, BsSIn<T>{L(c, 2), L(c, 4)}, BsT2<T>{L(c, 5), Fs(c, 1), L(c, 2), L(c, 4)}, g));
+    return pass(c, BsX<T>{L(c, X), L(c, 2), Fs(c, 0), Fs(c, 1), L(c, 5), L(c, 3)}, g);
+  }
   TRY(pass(c, BsS<T>{L(c, 2), L(c, 4), Fs(c, 1)}, g));
   TRY(allgather(c, 1));
   TRY(matvec_a(c, F(c, 1), BsT<T>{L(c, 5), Fs(c, 1)}, g2));

@@ -45,6 +45,8 @@ VARIANTS = [
     ("stencil", {"CCG_STENCIL_ZC": "4"}),     # matrix-free operator (NEXT-4), z-chunks
     ("stencil", {"CCG_STENCIL_ZC": "8"}),
     ("stencil", {"CCG_STENCIL_ZC": "16"}),
+    ("csr", {"CCG_BS_FUSE_RO": "1"}),         # BiCGSTAB's S pass folded into t = A s
+    ("stencil", {"CCG_BS_FUSE_RO": "1"}),
 ]
 
 

@@ -5,6 +5,10 @@
   GEMV's x staging and strip-sum epilogue (methods.cuh BsPIn / BsV2 / BsSIn /
   BsT2): the recurrence vectors and scalars are bitwise those of the separate
   passes (only ‖s‖², which feeds the half-step test, is summed in another order);
+* CCG_BS_FUSE_RO (opt-in; slower at config 5) — on the matrix-free stencil
+  and the SELL CSR SpMV only the S pass is folded (s = r − αv formed while
+  t = A s loads its inputs; r and v are not written by that product, so
+  neighbouring CTAs need no ping-pong): same bits;
 * CCG_L2_PIN_MB — L2 evict_last residency of part of A during a solve
   (matvec.cuh LdPin): a cache policy, so bitwise the same results;
 * CCG_SPLIT_FUSE — strip sum + epilogue by the last CTA of each row block:
@@ -74,6 +78,74 @@ def test_bs_fuse_half_step(monkeypatch):
     assert g["status"] == "CONVERGED" and g["iterations"] == 1 and g["matvecs_a"] == 1
     assert g.get("half_step", 1) == 1
     assert relerr(g["x"], y / c) <= 1e-6
+
+
+def _lattice_handle(kind, dims):
+    from workloads import lattice_csr, helmholtz_coeffs
+    from tests._gpu import Csr
+    from tests.test_gpu_next import Stencil
+    nx, ny, nz = dims
+    d, o = helmholtz_coeffs()
+    if kind == "stencil":
+        return Stencil(nx, ny, nz, d, o)
+    rp, ci, v = lattice_csr(nx, ny, nz, d, o)
+    return Csr(rp, ci, v, nx * ny * nz)
+
+
+def _lattice_solve(monkeypatch, env, kind, dims, y, tol, maxit):
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    with _lattice_handle(kind, dims) as h:
+        return h.solve("bicgstab", y, tol, maxit)
+
+
+@pytest.mark.parametrize("k", [1, 2, 7, 20])
+@pytest.mark.parametrize("dims", [(24, 24, 24), (31, 17, 12)])
+@pytest.mark.parametrize("kind", ["stencil", "csr"])
+def test_bs_fuse_s_lattice_bitwise(monkeypatch, kind, dims, k):
+    rng = np.random.default_rng(5)
+    n = dims[0] * dims[1] * dims[2]
+    y = (rng.standard_normal(n) + 1j * rng.standard_normal(n)) / np.sqrt(2)
+    a = _lattice_solve(monkeypatch, {"CCG_BS_FUSE_RO": "0"}, kind, dims, y, 0.0, k)
+    b = _lattice_solve(monkeypatch, {"CCG_BS_FUSE_RO": "1"}, kind, dims, y, 0.0, k)
+    assert a["iterations"] == b["iterations"] == k
+    assert a["matvecs_a"] == b["matvecs_a"]
+    assert np.array_equal(a["x"], b["x"])
+    assert np.array_equal(np.asarray(a["hist"]), np.asarray(b["hist"]))
+
+
+@pytest.mark.parametrize("kind", ["stencil", "csr"])
+def test_bs_fuse_s_lattice_converges_like_oracle(monkeypatch, kind):
+    """Tolerance-driven BiCGSTAB through the fused S path on a 16³ shifted
+    Helmholtz lattice (config 5's operator family) against the oracle's
+    rounding envelope."""
+    from workloads import lattice_csr, helmholtz_coeffs, helmholtz_rhs
+    from oracle import CsrOp
+    from tests._gpu import envelope_parity
+    N = 16
+    d, o = helmholtz_coeffs()
+    op = CsrOp(*lattice_csr(N, N, N, d, o))
+    y = helmholtz_rhs(N)
+    g = _lattice_solve(monkeypatch, {"CCG_BS_FUSE_RO": "1"}, kind, (N, N, N), y, 1e-8, 4000)
+    # this indefinite operator is rounding-chaotic: the P-envelope (SURVEY §8(c))
+    envelope_parity("bicgstab", op, y, 1e-8, 4000, np.complex128, g,
+                    lambda k: _lattice_solve(monkeypatch, {"CCG_BS_FUSE_RO": "1"}, kind, (N, N, N), y, 0.0, k)["x"])
+
+
+def test_bs_fuse_s_half_step_csr(monkeypatch):
+    """A = cI as a CSR matrix (SURVEY §8(c) pin): the half-step exit of
+    iteration 1 through the fused S product: 1 counted matvec, x = y/c."""
+    from tests._gpu import Csr
+    n, c = 5000, 3 - 4j
+    rp = np.arange(n + 1, dtype=np.int32)
+    ci = np.arange(n, dtype=np.int32)
+    v = np.full(n, c, dtype=np.complex128)
+    y = np.exp(1j * np.arange(n) * 0.1)
+    monkeypatch.setenv("CCG_BS_FUSE_RO", "1")
+    with Csr(rp, ci, v, n) as h:
+        g = h.solve("bicgstab", y, 1e-8, 50)
+    assert g["status"] == "CONVERGED" and g["iterations"] == 1 and g["matvecs_a"] == 1
+    assert relerr(g["x"], y / c) <= 1e-14
 
 
 @pytest.mark.parametrize("method", ["bicgstab", "cgne", "bicor", "qmr"])

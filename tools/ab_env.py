@@ -28,6 +28,7 @@ def main():
     ap.add_argument("--methods", default="bicgstab,cocr")
     ap.add_argument("--rounds", type=int, default=7)
     ap.add_argument("--tol", type=float, default=1e-8)
+    ap.add_argument("--sym", action="store_true", help="dense: pass CCG_FLAG_SYMMETRIC (A = Aᵀ)")
     a = ap.parse_args()
     dev = torch.device("cuda:0")
     if a.config == 4:                    # the FFT lattice operator (64 × 32 × 32)
@@ -55,7 +56,7 @@ def main():
         if a.config == 4:
             ccg.ccg_set_matvec_toeplitz3(h, 64, 32, 32, kern, 2.5 + 0.2j)
         elif a.config in (1, 2):
-            ccg.ccg_set_matvec_dense(h, A, 0, n)
+            ccg.ccg_set_matvec_dense(h, A, 0, n, flags=ccg.FLAG_SYMMETRIC if a.sym else 0)
         elif a.op == "csr":
             ccg.ccg_set_matvec_csr(h, rpd, cid, vd, 0, n, vd.numel())
         else:

@@ -16,6 +16,12 @@ import os
 import sys
 import time
 
+# one BLAS thread per member: the dot products' summation order (and so, on
+# this rounding-chaotic problem, the members' iteration counts) depends on the
+# BLAS thread count; the committed golden was written this way
+for _v in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
+    os.environ[_v] = "1"
+
 import numpy as np
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
