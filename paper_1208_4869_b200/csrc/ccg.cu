@@ -233,8 +233,8 @@ static int choose_launch(ccg_ctx* c) {
     CK(c, cudaMalloc(&c->sym_tiles, tl.size() * sizeof(int2)));
     CK(c, cudaMemcpyAsync(c->sym_tiles, tl.data(), tl.size() * sizeof(int2), cudaMemcpyHostToDevice, c->stream));
     CK(c, cudaStreamSynchronize(c->stream));
-    if (c->nstage2_grid <= 1)
-      c->nstage2_grid = (int)std::max<int64_t>(1, std::min<int64_t>((c->n + NT - 1) / NT, (int64_t)c->sm_count * 4));
+    // stage 2: one CTA per 32 outputs, at most 8 CTAs per SM
+    c->sym_s2_grid = (int)std::max<int64_t>(1, std::min<int64_t>((c->n + 31) / 32, (int64_t)c->sm_count * 8));
     const size_t need = (size_t)c->sym_strips * c->n * sizeof(C);
     if (need > c->npart_bytes) {
       if (c->npart) cudaFree(c->npart);
@@ -256,6 +256,7 @@ static int choose_launch(ccg_ctx* c) {
   int64_t maxgrid = std::max<int64_t>({(int64_t)c->gemv_grid, (int64_t)c->ah_strips * c->ah_S,
                                        (int64_t)c->stage2_grid, (int64_t)c->pass_grid, (int64_t)c->spmv_grid,
                                        (int64_t)c->split_strips * c->split_nrb, (int64_t)c->nstage2_grid,
+                                       (int64_t)c->sym_s2_grid,
                                        (int64_t)c->bulk_grid, (int64_t)std::max(c->sell_grid[0], c->sell_grid[1]),
                                        (int64_t)c->cols_strips * std::max(c->cols_S, c->dual_S),
                                        c->opk == OPK_STENCIL ? (int64_t)((c->snx + 31) / 32) * ((c->sny + 7) / 8) *

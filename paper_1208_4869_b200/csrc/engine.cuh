@@ -144,7 +144,7 @@ struct ccg_ctx {
   // complex-symmetric dense A (CCG_FLAG_SYMMETRIC, one rank): upper-triangle
   // products (matvec.cuh gemv_sym; CCG_SYMV=0 disables)
   bool sym_ok = false;
-  int sym_H = 64, sym_ntiles = 0, sym_strips = 1;
+  int sym_H = 64, sym_ntiles = 0, sym_strips = 1, sym_s2_grid = 1;
   int2* sym_tiles = nullptr;
   // workspace
   State* st = nullptr;
@@ -639,7 +639,7 @@ struct Engine {
     else
       launch_k(c, gemv_sym<T, NT, false>, c->sym_ntiles, NT, 0, c->stream, A, c->lda, x, c->n, c->sym_H,
                static_cast<const int2*>(c->sym_tiles), np, hp, gate, pin(c));
-    launch_k(c, gemv_sym_stage2<T, NT, Epi>, c->nstage2_grid, NT, 0, c->stream, static_cast<const C*>(np),
+    launch_k(c, gemv_sym_stage2<T, NT, Epi>, c->sym_s2_grid, NT, 0, c->stream, static_cast<const C*>(np),
              static_cast<const C*>(hp), c->n, c->sym_H, NT * CT<T>::V, c->sym_strips, epi, make_red(c), c->st, gate);
   }
 

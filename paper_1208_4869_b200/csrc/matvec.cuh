@@ -682,86 +682,100 @@ gemv_cols(const typename CT<T>::c* __restrict__ A, int64_t lda,
 // A = Aᵀ (CCG_FLAG_SYMMETRIC, one rank holding every row), reading only the
 // upper triangle j ≥ i — half of A's bytes per product:
 //   y_i = Σ_{j ≥ i} A_ij x_j + Σ_{j < i} A_ji x_j     (A_ij = A_ji).
-// Tiles (strip c of CW = NT·V columns, row block I of H rows) of the upper
-// triangle only (host table `tiles`, row-block major).  As in gemv_cols, thread
-// t owns the 16-byte column chunk t of the strip and walks the tile's rows 8 at
-// a time (8 independent 16-B loads in flight); each element feeds
-//   N: the row dot Σ_j A_ij x_j of row i   (j ≥ i)      -> npart[c][i]
-//   H: the column sum Σ_i A_ij x_i of col j (i < j)      -> hpart[I][j]
-// (the diagonal-straddling tiles mask by selects; the others do not test).
-// gemv_sym_stage2 sums both in a fixed order (deterministic).
+// Tiles (strip c of CW = 256·V columns = 4 KiB of a row, row block I of H
+// rows) of the upper triangle only (host table `tiles`, row-block major).  A
+// warp takes whole 4-KiB row segments: lane l loads the 16-byte chunks
+// l + 32u (u < 8) of row i — 8 independent loads — and each
+// element feeds
+//   N: the row dot Σ_j A_ij x_j (j ≥ i): FMAs, then a shuffle tree per row,
+//      lane 0 stores npart[c][i];
+//   H: the column sums Σ_i A_ij x_i (i < j): per-lane accumulators for the
+//      lane's 8 chunks over the warp's rows; the 8 warps' accumulators are
+//      added in warp order through shared memory once per tile -> hpart[I][j].
+// No block barrier inside the row loop.  x of the strip's columns and of the
+// tile's rows are staged in shared memory.  The diagonal-straddling tiles mask
+// by selects and skip the chunks wholly left of the diagonal (not loaded).
+// gemv_sym_stage2 sums both partial sets in a fixed order (deterministic).
 // ---------------------------------------------------------------------------
 constexpr int SYM_HMAX = 512;
 template <typename T, int NT, bool CONJ>
-__global__ void __launch_bounds__(NT)
+__global__ void __launch_bounds__(NT, 2)
 gemv_sym(const typename CT<T>::c* __restrict__ A, int64_t lda, const typename CT<T>::c* __restrict__ x, int64_t n,
          int H, const int2* __restrict__ tiles, typename CT<T>::c* __restrict__ npart,
          typename CT<T>::c* __restrict__ hpart, const int* gate, int pin) {
   using C = typename CT<T>::c;
   using LV = typename CT<T>::v;
   constexpr int V = CT<T>::V;
-  constexpr int UR = 8;
-  constexpr int CW = NT * V;
+  constexpr int U = 8;                 // chunks per lane per row
+  constexpr int CW = 32 * U * V;       // strip width in columns (4 KiB)
+  constexpr int NW = NT / 32;
+  static_assert(NT == 256, "gemv_sym: 8 warps");
   if (pdl_gate(gate)) return;
-  __shared__ C xs[SYM_HMAX];
-  __shared__ C red[2][NT / 32][UR];
+  __shared__ __align__(16) C xcol[CW];
+  __shared__ C xrow[SYM_HMAX];
+  __shared__ __align__(16) C hred[NW][CW];
   const int2 tl = tiles[blockIdx.x];
   const int c = tl.x, I = tl.y;
   const int64_t cbeg = (int64_t)c * CW, cend = min(cbeg + CW, n);
   const int64_t r0 = (int64_t)I * H, r1 = min(r0 + H, cend);
   const int rn = (int)(r1 - r0);
-  const int64_t jv = (int64_t)c * NT + threadIdx.x;   // 16-byte chunk index
-  const bool active = jv < n / V;
-  const int64_t jc = active ? jv : 0;
-  const int64_t j0 = jc * V;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t ldv = lda / V;
-  C xr[V], hacc[V];
-#pragma unroll
-  for (int v = 0; v < V; ++v) { xr[v] = x[j0 + v]; hacc[v] = czero<C>(); }
-  for (int t = threadIdx.x; t < rn; t += NT) xs[t] = x[r0 + t];
+  for (int t = threadIdx.x; t < CW; t += NT) xcol[t] = cbeg + t < n ? x[cbeg + t] : czero<C>();
+  for (int t = threadIdx.x; t < rn; t += NT) xrow[t] = x[r0 + t];
   __syncthreads();
-  const LV* Ab = reinterpret_cast<const LV*>(A) + jc;
-  int buf = 0;
+  // this lane's chunks: k = lane + 32u, columns cbeg + kV .. + V − 1
+  bool act[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) act[u] = cbeg + (int64_t)(lane + 32 * u) * V < cend;
+  C hacc[U][V];
+#pragma unroll
+  for (int u = 0; u < U; ++u)
+#pragma unroll
+    for (int v = 0; v < V; ++v) hacc[u][v] = czero<C>();
+  const LV* Ab = reinterpret_cast<const LV*>(A + cbeg) + lane;
+  const int64_t ldv = lda / V;
+  const LV* xv = reinterpret_cast<const LV*>(xcol) + lane;
   auto body = [&](auto ld, auto dg) {
     constexpr bool DG = decltype(dg)::value;
-    for (int t = 0; t < rn; t += UR) {
-      const int nr = min(UR, rn - t);
-      LV a[UR];
+    for (int t = warp; t < rn; t += NW) {   // (unroll 2 spills at 128 registers)
+      const int64_t row = r0 + t;
+      LV a[U];
 #pragma unroll
-      for (int u = 0; u < UR; ++u) {
-        const int64_t row = r0 + t + min(u, nr - 1);
-        a[u] = ld(Ab + row * ldv, row);
+      for (int u = 0; u < U; ++u) {
+        const int64_t j0 = cbeg + (int64_t)(lane + 32 * u) * V;
+        const bool need = act[u] && (!DG || j0 + V - 1 >= row);
+        a[u] = need ? ld(Ab + row * ldv + 32 * u, row) : LV{};
       }
-      C rp[UR];
+      const C xi = xrow[t];
+      C acc = czero<C>();
 #pragma unroll
-      for (int u = 0; u < UR; ++u) {
-        C ac[V];
+      for (int u = 0; u < U; ++u) {
+        C ac[V], xc[V];
         unpack(a[u], ac);
-        const int64_t row = r0 + t + u;
-        const C xi = xs[t + min(u, nr - 1)];
-        rp[u] = czero<C>();
+        unpack(xv[32 * u], xc);
+        const int64_t j0 = cbeg + (int64_t)(lane + 32 * u) * V;
 #pragma unroll
         for (int v = 0; v < V; ++v) {
-          const bool n_ok = active && (!DG || j0 + v >= row);
-          const bool h_ok = active && u < nr && (!DG || j0 + v > row);
-          C tn = rp[u], th = hacc[v];
-          if (CONJ) { cfmac(tn, ac[v], xr[v]); cfmac(th, ac[v], xi); }
-          else { cfma(tn, ac[v], xr[v]); cfma(th, ac[v], xi); }
-          rp[u].x = n_ok ? tn.x : rp[u].x; rp[u].y = n_ok ? tn.y : rp[u].y;
-          hacc[v].x = h_ok ? th.x : hacc[v].x; hacc[v].y = h_ok ? th.y : hacc[v].y;
+          if (!DG) {
+            if (CONJ) { cfmac(acc, ac[v], xc[v]); cfmac(hacc[u][v], ac[v], xi); }
+            else { cfma(acc, ac[v], xc[v]); cfma(hacc[u][v], ac[v], xi); }
+          } else {
+            C tn = acc, th = hacc[u][v];
+            if (CONJ) { cfmac(tn, ac[v], xc[v]); cfmac(th, ac[v], xi); }
+            else { cfma(tn, ac[v], xc[v]); cfma(th, ac[v], xi); }
+            const bool n_ok = j0 + v >= row, h_ok = j0 + v > row;
+            acc.x = n_ok ? tn.x : acc.x; acc.y = n_ok ? tn.y : acc.y;
+            hacc[u][v].x = h_ok ? th.x : hacc[u][v].x; hacc[u][v].y = h_ok ? th.y : hacc[u][v].y;
+          }
         }
       }
-      warp_transpose_reduce<UR>(rp, lane);   // lane L: warp sum of row L >> 2
-      if ((lane & 3) == 0) red[buf][warp][lane >> 2] = rp[0];
-      __syncthreads();
-      if (threadIdx.x < nr) {
-        C sum = red[buf][0][threadIdx.x];
 #pragma unroll
-        for (int w = 1; w < NT / 32; ++w) sum = cadd(sum, red[buf][w][threadIdx.x]);
-        npart[(int64_t)c * n + r0 + t + threadIdx.x] = sum;
+      for (int o = 16; o > 0; o >>= 1) {   // butterfly: every lane ends with the same sum
+        C t = acc;
+        shfl_c(t, o);
+        acc = cadd(acc, t);
       }
-      buf ^= 1;
+      if (lane == 0) npart[(int64_t)c * n + row] = acc;
     }
   };
   const bool diag = r1 > cbeg;   // the tile reaches the diagonal: masks
@@ -770,39 +784,67 @@ gemv_sym(const typename CT<T>::c* __restrict__ A, int64_t lda, const typename CT
   } else {
     if (diag) body(LdA{}, std::true_type{}); else body(LdA{}, std::false_type{});
   }
-  if (active) {
+  // column sums: the warps' accumulators in warp order
 #pragma unroll
-    for (int v = 0; v < V; ++v) hpart[(int64_t)I * n + j0 + v] = hacc[v];
+  for (int u = 0; u < U; ++u)
+#pragma unroll
+    for (int v = 0; v < V; ++v) hred[warp][(lane + 32 * u) * V + v] = hacc[u][v];
+  __syncthreads();
+  for (int t = threadIdx.x; t < CW; t += NT) {
+    if (cbeg + t >= n) break;
+    C s = hred[0][t];
+#pragma unroll
+    for (int w = 1; w < NW; ++w) s = cadd(s, hred[w][t]);
+    hpart[(int64_t)I * n + cbeg + t] = s;
   }
 }
 
-// y_i = Σ_{c ≥ c(i)} npart[c][i] + Σ_{I < nb(c(i))} hpart[I][i] (fp64, fixed
-// order), then the epilogue; c(i) = i / CW, nb(c) = the row blocks of strip c
+// y_i = Σ_{c ≥ c(i)} npart[c][i] + Σ_{I < nb(c(i))} hpart[I][i] (fp64), then
+// the epilogue; c(i) = i / CW, nb(c) = the row blocks of strip c.  A CTA takes
+// 32 consecutive outputs (one strip: CW is a multiple of 32), lane = output;
+// warp w sums the partials p ≡ w (mod NT/32) of the list [npart strips ...,
+// hpart blocks ...] in order, then warp 0 adds the warp sums in warp order —
+// a fixed order (deterministic) with NT/32 independent load streams per
+// output (one thread per output walking ~n/H partials was latency-bound).
 template <typename T, int NT, class Epi>
 __global__ void __launch_bounds__(NT)
 gemv_sym_stage2(const typename CT<T>::c* __restrict__ npart, const typename CT<T>::c* __restrict__ hpart, int64_t n,
                 int H, int CW, int nstrips, Epi epi, Red red, State* st, const int* gate) {
   using C = typename CT<T>::c;
   constexpr int KK = Epi::K > 0 ? Epi::K : 1;
+  constexpr int NW = NT / 32;
   if (pdl_gate(gate)) return;
   epi.load(st);
+  __shared__ double2 sh[NW][32];
   double2 dacc[KK];
 #pragma unroll
   for (int k = 0; k < KK; ++k) dacc[k] = make_double2(0.0, 0.0);
-  for (int64_t i = (int64_t)blockIdx.x * NT + threadIdx.x; i < n; i += (int64_t)gridDim.x * NT) {
-    const int ci = (int)(i / CW);
-    double2 w = make_double2(0.0, 0.0);
-    for (int c = ci; c < nstrips; ++c) {
-      const C p = __ldcs(npart + (int64_t)c * n + i);
-      w.x += (double)p.x; w.y += (double)p.y;
-    }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int64_t base = (int64_t)blockIdx.x * 32; base < n; base += (int64_t)gridDim.x * 32) {
+    const int64_t i = base + lane;
+    const bool valid = i < n;
+    const int ci = (int)(base / CW);
+    const int nN = nstrips - ci;
     const int64_t cend = min((int64_t)(ci + 1) * CW, n);
-    const int nb = (int)((cend + H - 1) / H);
-    for (int b = 0; b < nb; ++b) {
-      const C p = __ldcs(hpart + (int64_t)b * n + i);
-      w.x += (double)p.x; w.y += (double)p.y;
+    const int P = nN + (int)((cend + H - 1) / H);
+    double2 w = make_double2(0.0, 0.0);
+#pragma unroll 4
+    for (int p = warp; p < P; p += NW) {
+      const C* src = p < nN ? npart + (int64_t)(ci + p) * n : hpart + (int64_t)(p - nN) * n;
+      if (valid) {
+        const C v = __ldcs(src + i);
+        w.x += (double)v.x; w.y += (double)v.y;
+      }
     }
-    epi(i, fromd2<C>(w), dacc);
+    sh[warp][lane] = w;
+    __syncthreads();
+    if (warp == 0) {
+      double2 y = sh[0][lane];
+#pragma unroll
+      for (int k = 1; k < NW; ++k) { y.x += sh[k][lane].x; y.y += sh[k][lane].y; }
+      if (valid) epi(i, fromd2<C>(y), dacc);
+    }
+    __syncthreads();
   }
   if constexpr (Epi::K > 0) finish_reduction<KK, NT, Epi>(dacc, red, st);
 }

@@ -51,11 +51,18 @@ def timed(h, method, y, x, tol, maxit, reps, stream):
     return r, its, ms
 
 
+SYM_FLAG = False   # --sym: configs 2 / 4 dense with CCG_FLAG_SYMMETRIC (upper-triangle products)
+
+
 def run_dense(cfg, A, y, methods, tol, maxit, reps, dtype, toeplitz=None):
     n = y.shape[0]
     s = 8 if dtype == "c64" else 16
     h = ccg.ccg_create(dtype, n)
-    if toeplitz is None:
+    if toeplitz is None and SYM_FLAG and cfg in (2, 4):
+        ccg.ccg_set_matvec_dense(h, A, 0, n, flags=ccg.FLAG_SYMMETRIC)
+        b_mat = n * (n + 1) // 2 * s       # the upper triangle: what the product reads
+        opname = "dense-sym"
+    elif toeplitz is None:
         ccg.ccg_set_matvec_dense(h, A, 0, n)
         b_mat = n * n * s
         opname = "dense"
@@ -88,8 +95,11 @@ def main():
     ap.add_argument("--no-dense4", action="store_true", help="config 4: FFT operator only")
     ap.add_argument("--ops", default="csr,stencil", help="config 5 operators")
     ap.add_argument("--ops2", default="dense,toeplitz", help="config 2 operators")
+    ap.add_argument("--sym", action="store_true", help="configs 2/4 dense: CCG_FLAG_SYMMETRIC")
+    ap.add_argument("--no-fft4", action="store_true", help="config 4: dense only")
     a = ap.parse_args()
-    global SEL
+    global SEL, SYM_FLAG
+    SYM_FLAG = a.sym
     SEL = set(a.methods.split(",")) if a.methods else set()
     dev = "cuda:0"
     for c in [int(v) for v in a.configs.split(",")]:
@@ -119,8 +129,9 @@ def main():
             del Ad
         elif c == 4:
             n = cf["n"]
-            run_dense(4, None, torch.from_numpy(cfg4_rhs()).to(dev), SYM, cf["tol"], cf["maxit"], a.reps or 5,
-                      "c128", toeplitz=(64, 32, 32, dda_kernel((64, 32, 32), 0.5), 2.5 + 0.2j))
+            if not a.no_fft4:
+                run_dense(4, None, torch.from_numpy(cfg4_rhs()).to(dev), SYM, cf["tol"], cf["maxit"], a.reps or 5,
+                          "c128", toeplitz=(64, 32, 32, dda_kernel((64, 32, 32), 0.5), 2.5 + 0.2j))
             if a.no_dense4:
                 continue
             Ad = torch.empty((n, n), dtype=torch.complex128, device=dev)

@@ -21,13 +21,14 @@ ap.add_argument("--methods", default="bicgstab")
 ap.add_argument("--its", type=int, default=20)
 ap.add_argument("--reps", type=int, default=2)
 ap.add_argument("--timing", action="store_true", help="per-product CUDA events (library timing mode)")
+ap.add_argument("--sym", action="store_true", help="CCG_FLAG_SYMMETRIC (upper-triangle products)")
 a = ap.parse_args()
 A, y = cfg2()
 Ad = torch.from_numpy(A).cuda()
 yd = torch.from_numpy(y).cuda()
 x = torch.empty_like(yd)
 h = ccg.ccg_create("c128", A.shape[0])
-ccg.ccg_set_matvec_dense(h, Ad, 0, A.shape[0])
+ccg.ccg_set_matvec_dense(h, Ad, 0, A.shape[0], flags=ccg.FLAG_SYMMETRIC if a.sym else 0)
 ccg.ccg_set_timing(h, a.timing)
 for m in a.methods.split(","):
     for _ in range(a.reps):
