@@ -204,45 +204,55 @@ static int choose_launch(ccg_ctx* c) {
   }
   size_t need_sym_h = 0;
   if (c->opk == OPK_DENSE && c->sym_ok) {
-    // upper-triangle tiles: strips of NT·V columns × row blocks of H rows; the
-    // largest H (≤ SYM_HMAX) that still gives two waves of tiles (CCG_SYM_H)
-    const int64_t CW = (int64_t)NT * CT<T>::V;
-    c->sym_strips = (int)((c->n + CW - 1) / CW);
-    int occ_s = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_s, gemv_sym<T, E::NT, false>, NT, 0);
-    occ_s = std::max(1, occ_s);
-    auto ntiles = [&](int64_t H) {
-      int64_t t = 0;
-      for (int64_t cc = 0; cc < c->sym_strips; ++cc) t += (std::min((cc + 1) * CW, c->n) + H - 1) / H;
-      return t;
+    // upper-triangle tiles: strips of CW columns × row blocks of H rows; the
+    // largest H (≤ SYM_HMAX) that still gives two waves of tiles (CCG_SYM_H).
+    // Single products: CW = 256·V (gemv_sym); the dual product: 128·V.
+    auto plan = [&](int64_t CW, int occ, int& strips, int& Hout, int& ntl, int2*& dtiles) -> int64_t {
+      strips = (int)((c->n + CW - 1) / CW);
+      auto ntiles = [&](int64_t H) {
+        int64_t t = 0;
+        for (int64_t cc = 0; cc < strips; ++cc) t += (std::min((cc + 1) * CW, c->n) + H - 1) / H;
+        return t;
+      };
+      const char* he = getenv("CCG_SYM_H");
+      int64_t H = he ? atoi(he) : SYM_HMAX;
+      if (!he)
+        while (H > 32 && ntiles(H) < 2 * (int64_t)c->sm_count * std::max(1, occ)) H /= 2;
+      H = std::max<int64_t>(8, std::min<int64_t>(SYM_HMAX, (H / 8) * 8));
+      Hout = (int)H;
+      std::vector<int2> tl;
+      const int64_t nblk = (c->n + H - 1) / H;
+      for (int64_t I = 0; I < nblk; ++I)        // row-block major: concurrent CTAs read whole rows
+        for (int64_t cc = 0; cc < strips; ++cc)
+          if (I * H < std::min((cc + 1) * CW, c->n)) tl.push_back(make_int2((int)cc, (int)I));
+      ntl = (int)tl.size();
+      if (dtiles) cudaFree(dtiles);
+      dtiles = nullptr;
+      if (cudaMalloc(&dtiles, tl.size() * sizeof(int2)) != cudaSuccess) return -1;
+      if (cudaMemcpyAsync(dtiles, tl.data(), tl.size() * sizeof(int2), cudaMemcpyHostToDevice, c->stream) !=
+          cudaSuccess)
+        return -1;
+      return nblk;
     };
-    const char* he = getenv("CCG_SYM_H");
-    int64_t H = he ? atoi(he) : SYM_HMAX;
-    if (!he)
-      while (H > 32 && ntiles(H) < 2 * (int64_t)c->sm_count * occ_s) H /= 2;
-    H = std::max<int64_t>(8, std::min<int64_t>(SYM_HMAX, (H / 8) * 8));
-    c->sym_H = (int)H;
-    std::vector<int2> tl;
-    const int64_t nblk = (c->n + H - 1) / H;
-    for (int64_t I = 0; I < nblk; ++I)        // row-block major: concurrent CTAs read whole rows
-      for (int64_t cc = 0; cc < c->sym_strips; ++cc)
-        if (I * H < std::min((cc + 1) * CW, c->n)) tl.push_back(make_int2((int)cc, (int)I));
-    c->sym_ntiles = (int)tl.size();
-    if (c->sym_tiles) cudaFree(c->sym_tiles);
-    c->sym_tiles = nullptr;
-    CK(c, cudaMalloc(&c->sym_tiles, tl.size() * sizeof(int2)));
-    CK(c, cudaMemcpyAsync(c->sym_tiles, tl.data(), tl.size() * sizeof(int2), cudaMemcpyHostToDevice, c->stream));
+    int occ1 = 0, occ2 = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1, gemv_sym<T, E::NT, false>, NT, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, gemv_sym_dual<T, E::NT>, NT, 0);
+    const int64_t nblk1 = plan((int64_t)256 * CT<T>::V, occ1, c->sym_strips, c->sym_H, c->sym_ntiles, c->sym_tiles);
+    const int64_t nblk2 = plan((int64_t)128 * CT<T>::V, occ2, c->sym2_strips, c->sym2_H, c->sym2_ntiles,
+                               c->sym2_tiles);
+    if (nblk1 < 0 || nblk2 < 0) FAIL(c, CCG_E_CUDA, "symmetric tile tables");
     CK(c, cudaStreamSynchronize(c->stream));
     // stage 2: one CTA per 32 outputs, at most 8 CTAs per SM
     c->sym_s2_grid = (int)std::max<int64_t>(1, std::min<int64_t>((c->n + 31) / 32, (int64_t)c->sm_count * 8));
-    const size_t need = (size_t)c->sym_strips * c->n * sizeof(C);
+    // npart: [strips][n] (single) or 2 × [strips2][n] (dual); hpart likewise
+    const size_t need = std::max((size_t)c->sym_strips, 2 * (size_t)c->sym2_strips) * c->n * sizeof(C);
     if (need > c->npart_bytes) {
       if (c->npart) cudaFree(c->npart);
       c->npart = nullptr;
       CK(c, cudaMalloc(&c->npart, need));
       c->npart_bytes = need;
     }
-    need_sym_h = (size_t)nblk * c->n * sizeof(C);
+    need_sym_h = std::max((size_t)nblk1, 2 * (size_t)nblk2) * c->n * sizeof(C);
   }
   // workspace sized for the chosen grids
   size_t need_hpart = std::max((size_t)std::max(c->ah_S, c->cols_ok ? c->dual_S : 1) * (size_t)c->n * sizeof(C),
@@ -1344,6 +1354,7 @@ int ccg_destroy(ccg_handle c) {
   if (c->hpart) cudaFree(c->hpart);
   if (c->npart) cudaFree(c->npart);
   if (c->sym_tiles) cudaFree(c->sym_tiles);
+  if (c->sym2_tiles) cudaFree(c->sym2_tiles);
   free_csr_copies(c);
   if (c->part) cudaFree(c->part);
   if (c->hist) cudaFree(c->hist);

@@ -146,6 +146,8 @@ struct ccg_ctx {
   bool sym_ok = false;
   int sym_H = 64, sym_ntiles = 0, sym_strips = 1, sym_s2_grid = 1;
   int2* sym_tiles = nullptr;
+  int sym2_H = 64, sym2_ntiles = 0, sym2_strips = 1;   // the dual product's tiles (gemv_sym_dual)
+  int2* sym2_tiles = nullptr;
   // workspace
   State* st = nullptr;
   State* st_host = nullptr;  // pinned
@@ -859,6 +861,21 @@ struct Engine {
     const C* A = reinterpret_cast<const C*>(c->A);
     C* np = reinterpret_cast<C*>(c->npart);
     C* hp = reinterpret_cast<C*>(c->hpart);
+    if (c->sym_ok) {   // complex-symmetric A: both products from one upper-triangle pass
+      const int64_t ns = (int64_t)c->sym2_strips * c->n, nh = (int64_t)((c->n + c->sym2_H - 1) / c->sym2_H) * c->n;
+      const int CW2 = 128 * CT<T>::V;
+      tev_begin(c, 0);
+      launch_k(c, gemv_sym_dual<T, NT>, c->sym2_ntiles, NT, 0, c->stream, A, c->lda, pfull, qloc, c->n, c->sym2_H,
+               static_cast<const int2*>(c->sym2_tiles), np, hp, np + ns, hp + nh, gate);
+      launch_k(c, gemv_sym_stage2<T, NT, EpiA>, c->sym_s2_grid, NT, 0, c->stream, static_cast<const C*>(np),
+               static_cast<const C*>(hp), c->n, c->sym2_H, CW2, c->sym2_strips, ea, make_red(c), c->st, gate);
+      launch_k(c, gemv_sym_stage2<T, NT, EpiH>, c->sym_s2_grid, NT, 0, c->stream, static_cast<const C*>(np + ns),
+               static_cast<const C*>(hp + nh), c->n, c->sym2_H, CW2, c->sym2_strips, eh, make_red(c), c->st, gate);
+      c->launches += 3;
+      tev_end(c);
+      CK(c, cudaGetLastError());
+      return CCG_OK;
+    }
     tev_begin(c, 0);
     launch_k(c, gemv_cols<T, NT, true, true, true>, dim3(c->cols_strips, c->dual_S), NT, 0, c->stream, 
         A, c->lda, pfull, qloc, c->nloc, c->n, np, hp, gate, 0);   // no L2 pinning: measured slower

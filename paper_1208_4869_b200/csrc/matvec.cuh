@@ -799,6 +799,134 @@ gemv_sym(const typename CT<T>::c* __restrict__ A, int64_t lda, const typename CT
   }
 }
 
+// K1s' gemv_sym_dual: A·p and Aᴴ·q of one QMR / BiCG iteration (independent,
+// SURVEY §8(a) a7; §8(f) NEXT-1) from ONE pass over the upper triangle of a
+// complex-symmetric A — half of the full dual pass's bytes, the same as one
+// gemv_sym.  Each loaded element feeds four sums:
+//   (A p)_i:  N Σ_{j≥i} A_ij p_j,        H Σ_{i<j} A_ij p_i      -> np1 / hp1
+//   (Aᴴq)_i:  N Σ_{j≥i} conj(A_ij) q_j,  H Σ_{i<j} conj(A_ij) q_i -> np2 / hp2
+// Same layout as gemv_sym with 4 chunks per lane (2-KiB strips: CW = 128·V)
+// so the two sets of column accumulators fit the register budget.
+template <typename T, int NT>
+__global__ void __launch_bounds__(NT, 2)
+gemv_sym_dual(const typename CT<T>::c* __restrict__ A, int64_t lda, const typename CT<T>::c* __restrict__ p,
+              const typename CT<T>::c* __restrict__ q, int64_t n, int H, const int2* __restrict__ tiles,
+              typename CT<T>::c* __restrict__ np1, typename CT<T>::c* __restrict__ hp1,
+              typename CT<T>::c* __restrict__ np2, typename CT<T>::c* __restrict__ hp2, const int* gate) {
+  using C = typename CT<T>::c;
+  using LV = typename CT<T>::v;
+  constexpr int V = CT<T>::V;
+  constexpr int U = 4;
+  constexpr int CW = 32 * U * V;
+  constexpr int NW = NT / 32;
+  static_assert(NT == 256, "gemv_sym_dual: 8 warps");
+  if (pdl_gate(gate)) return;
+  __shared__ __align__(16) C pcol[CW];
+  __shared__ __align__(16) C qcol[CW];
+  __shared__ C prow[SYM_HMAX];
+  __shared__ C qrow[SYM_HMAX];
+  __shared__ __align__(16) C hred[NW][CW];
+  const int2 tl = tiles[blockIdx.x];
+  const int c = tl.x, I = tl.y;
+  const int64_t cbeg = (int64_t)c * CW, cend = min(cbeg + CW, n);
+  const int64_t r0 = (int64_t)I * H, r1 = min(r0 + H, cend);
+  const int rn = (int)(r1 - r0);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int t = threadIdx.x; t < CW; t += NT) {
+    pcol[t] = cbeg + t < n ? p[cbeg + t] : czero<C>();
+    qcol[t] = cbeg + t < n ? q[cbeg + t] : czero<C>();
+  }
+  for (int t = threadIdx.x; t < rn; t += NT) { prow[t] = p[r0 + t]; qrow[t] = q[r0 + t]; }
+  __syncthreads();
+  bool act[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) act[u] = cbeg + (int64_t)(lane + 32 * u) * V < cend;
+  C h1[U][V], h2[U][V];
+#pragma unroll
+  for (int u = 0; u < U; ++u)
+#pragma unroll
+    for (int v = 0; v < V; ++v) { h1[u][v] = czero<C>(); h2[u][v] = czero<C>(); }
+  const LV* Ab = reinterpret_cast<const LV*>(A + cbeg) + lane;
+  const int64_t ldv = lda / V;
+  const LV* pv = reinterpret_cast<const LV*>(pcol) + lane;
+  const LV* qv = reinterpret_cast<const LV*>(qcol) + lane;
+  auto body = [&](auto dg) {
+    constexpr bool DG = decltype(dg)::value;
+    for (int t = warp; t < rn; t += NW) {
+      const int64_t row = r0 + t;
+      LV a[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t j0 = cbeg + (int64_t)(lane + 32 * u) * V;
+        const bool need = act[u] && (!DG || j0 + V - 1 >= row);
+        a[u] = need ? ld_stream(Ab + row * ldv + 32 * u) : LV{};
+      }
+      const C pi = prow[t], qi = qrow[t];
+      C n1 = czero<C>(), n2 = czero<C>();
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        C ac[V], pc[V], qc[V];
+        unpack(a[u], ac);
+        unpack(pv[32 * u], pc);
+        unpack(qv[32 * u], qc);
+        const int64_t j0 = cbeg + (int64_t)(lane + 32 * u) * V;
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+          C t1 = n1, t2 = n2, t3 = h1[u][v], t4 = h2[u][v];
+          cfma(t1, ac[v], pc[v]);
+          cfmac(t2, ac[v], qc[v]);
+          cfma(t3, ac[v], pi);
+          cfmac(t4, ac[v], qi);
+          const bool n_ok = !DG || j0 + v >= row, h_ok = !DG || j0 + v > row;
+          n1.x = n_ok ? t1.x : n1.x; n1.y = n_ok ? t1.y : n1.y;
+          n2.x = n_ok ? t2.x : n2.x; n2.y = n_ok ? t2.y : n2.y;
+          h1[u][v].x = h_ok ? t3.x : h1[u][v].x; h1[u][v].y = h_ok ? t3.y : h1[u][v].y;
+          h2[u][v].x = h_ok ? t4.x : h2[u][v].x; h2[u][v].y = h_ok ? t4.y : h2[u][v].y;
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        C t1 = n1, t2 = n2;
+        shfl_c(t1, o);
+        shfl_c(t2, o);
+        n1 = cadd(n1, t1);
+        n2 = cadd(n2, t2);
+      }
+      if (lane == 0) {
+        np1[(int64_t)c * n + row] = n1;
+        np2[(int64_t)c * n + row] = n2;
+      }
+    }
+  };
+  if (r1 > cbeg) body(std::true_type{}); else body(std::false_type{});
+  // column sums of both products, warps in order, through the same buffer
+#pragma unroll
+  for (int u = 0; u < U; ++u)
+#pragma unroll
+    for (int v = 0; v < V; ++v) hred[warp][(lane + 32 * u) * V + v] = h1[u][v];
+  __syncthreads();
+  for (int t = threadIdx.x; t < CW; t += NT) {
+    if (cbeg + t >= n) break;
+    C s = hred[0][t];
+#pragma unroll
+    for (int w = 1; w < NW; ++w) s = cadd(s, hred[w][t]);
+    hp1[(int64_t)I * n + cbeg + t] = s;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int u = 0; u < U; ++u)
+#pragma unroll
+    for (int v = 0; v < V; ++v) hred[warp][(lane + 32 * u) * V + v] = h2[u][v];
+  __syncthreads();
+  for (int t = threadIdx.x; t < CW; t += NT) {
+    if (cbeg + t >= n) break;
+    C s = hred[0][t];
+#pragma unroll
+    for (int w = 1; w < NW; ++w) s = cadd(s, hred[w][t]);
+    hp2[(int64_t)I * n + cbeg + t] = s;
+  }
+}
+
 // y_i = Σ_{c ≥ c(i)} npart[c][i] + Σ_{I < nb(c(i))} hpart[I][i] (fp64), then
 // the epilogue; c(i) = i / CW, nb(c) = the row blocks of strip c.  A CTA takes
 // 32 consecutive outputs (one strip: CW is a multiple of 32), lane = output;

@@ -243,14 +243,17 @@ def test_cfg4_device_generator_matches_numpy():
         assert np.max(np.abs(got - ref) / np.maximum(np.abs(ref), 1e-300)) <= 4 * np.finfo(float).eps
 
 
-def test_cfg4_dense_full_size():
+@pytest.mark.parametrize("flags", [0, ccg.FLAG_SYMMETRIC], ids=["full", "sym"])
+def test_cfg4_dense_full_size(flags):
     """BASELINE config 4 at its full size as a DENSE matrix (n = 65536 c128,
     68.7 GB in HBM, the bench_all launch configuration): sampled rows of A·x
     against the oracle's own rows, Aᴴ·x against the oracle's lattice operator,
     and BiCGSTAB inside the rounding envelope of SURVEY §8(c) — the problem is
     rounding-chaotic (noise-seed iteration counts 102-110), so the P-envelope
     criterion applies: k within [k_min − 2, k_max + 2], x at equal k within
-    max(1e-9, 2D), and the true residual recomputed by the oracle ≤ 10·tol."""
+    max(1e-9, 2D), and the true residual recomputed by the oracle ≤ 10·tol.
+    `sym`: the same with CCG_FLAG_SYMMETRIC (A = Aᵀ bitwise):
+    the products read only the upper triangle (matvec.cuh gemv_sym)."""
     import torch
     from oracle import ToeplitzOp
     from oracle.operators import reference_apply
@@ -266,7 +269,7 @@ def test_cfg4_dense_full_size():
     y = cfg4_rhs()
     h = ccg.ccg_create("c128", n)
     try:
-        ccg.ccg_set_matvec_dense(h, Ad, 0, n)
+        ccg.ccg_set_matvec_dense(h, Ad, 0, n, flags=flags)
         rng = np.random.default_rng(9)
         x = rng.standard_normal(n) + 1j * rng.standard_normal(n)
         xd = torch.from_numpy(x).to("cuda:0")
@@ -292,7 +295,8 @@ def test_cfg4_dense_full_size():
         def at_k(k):
             ccg.ccg_solve(h, "bicgstab", None, yv, xo, 0.0, k)
             return xo.cpu().numpy()
-        rec = dict(test="cfg4-full-dense", method="bicgstab", k_gpu=g["iterations"], true_rel_res=tr)
+        rec = dict(test="cfg4-full-dense" + ("-sym" if flags else ""), method="bicgstab", k_gpu=g["iterations"],
+                   true_rel_res=tr)
         envelope_parity("bicgstab", op, y, 1e-8, 2000, np.complex128, g, at_k, rec)
         _record(**rec)
     finally:

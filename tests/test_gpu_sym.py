@@ -122,3 +122,23 @@ def test_sym_off_matches_full(monkeypatch):
     with Dense(A, flags=ccg.FLAG_SYMMETRIC) as hf:
         yf = hf.apply(y)
     assert relerr(ys, yf) <= TOL[np.complex128]
+
+
+@pytest.mark.parametrize("dtype", [np.complex128, np.complex64])
+def test_sym_dual_qmr(monkeypatch, dtype):
+    """QMR's A·p and Aᴴ·q from one upper-triangle pass (gemv_sym_dual) against
+    the same iteration with two single symmetric products (CCG_QMR_DUAL=0):
+    rounding-level agreement at equal k, and both against the oracle."""
+    n = 1536 if dtype == np.complex128 else 2048
+    A = _sym(n, dtype, seed=31)
+    y = _x(n, dtype, seed=32)
+    k = 12
+    with Dense(A, flags=ccg.FLAG_SYMMETRIC) as h:
+        a = h.solve("qmr", y, 0.0, k)
+    monkeypatch.setenv("CCG_QMR_DUAL", "0")
+    with Dense(A, flags=ccg.FLAG_SYMMETRIC) as h:
+        b = h.solve("qmr", y, 0.0, k)
+    o = oracle.solve("qmr", DenseOp(A), y, 0.0, k)
+    bar = 1e-12 if dtype == np.complex128 else 1e-4
+    assert relerr(a["x"], b["x"]) <= bar
+    assert relerr(a["x"], o.x) <= (1e-9 if dtype == np.complex128 else 1e-4)
