@@ -87,8 +87,11 @@ typedef enum {
 typedef enum { CCG_OP_A = 0, CCG_OP_AH = 1, CCG_OP_AT = 2 } ccg_op;
 
 /* Flags for ccg_set_matvec_*.  CCG_FLAG_SYMMETRIC: caller asserts A == Aᵀ
- * (complex symmetric, unconjugated).  Not verified by the
- * library.  For CSR it enables Aᴴ·x = conj(A·conj(x)) (single GPU only). */
+ * (complex symmetric, unconjugated; the DDA matrices of P:47 §1
+ * and the COCG/COCR family of P:69 §2.4, §3.4).  Not verified by the
+ * library.  For CSR it enables Aᴴ·x = conj(A·conj(x)) (single GPU only); for
+ * a dense matrix on one rank the products read only the upper triangle
+ * j ≥ i (half of A's bytes; the strictly-lower triangle is never read). */
 enum { CCG_FLAG_SYMMETRIC = 1 };
 
 typedef enum {
@@ -196,7 +199,11 @@ int ccg_create_loopback_group_ex(ccg_handle* hs, int world, ccg_dtype dt, int64_
  *             leading dimension lda ≥ n (elements).  Borrowed: the caller keeps
  *             it alive and unmodified until ccg_destroy or the next set_matvec.
  *   row0, nloc : must equal the handle's row range (rank·n/world, n/world).
- *   flags   : CCG_FLAG_SYMMETRIC or 0 (informational for dense).
+ *   flags   : CCG_FLAG_SYMMETRIC or 0.  With the flag and world == 1 every
+ *             product (A, Aᴴ, Aᵀ; QMR's A·p and Aᴴ·q in one pass) reads only
+ *             the upper triangle j ≥ i: y_i = Σ_{j≥i} A_ij x_j + Σ_{j<i} A_ji x_j
+ *             (same products up to summation order; env CCG_SYMV=0 reads all
+ *             of A).  With world > 1 the flag is informational.
  * Supports CCG_OP_A, CCG_OP_AH, CCG_OP_AT. */
 int ccg_set_matvec_dense(ccg_handle h, const void* A_local, int64_t row0, int64_t nloc,
                          int64_t lda, uint32_t flags);
