@@ -698,8 +698,11 @@ gemv_cols(const typename CT<T>::c* __restrict__ A, int64_t lda,
 // gemv_sym_stage2 sums both partial sets in a fixed order (deterministic).
 // ---------------------------------------------------------------------------
 constexpr int SYM_HMAX = 512;
+#ifndef CCG_SYM_MINB
+#define CCG_SYM_MINB 2
+#endif
 template <typename T, int NT, bool CONJ>
-__global__ void __launch_bounds__(NT, 2)
+__global__ void __launch_bounds__(NT, CCG_SYM_MINB)
 gemv_sym(const typename CT<T>::c* __restrict__ A, int64_t lda, const typename CT<T>::c* __restrict__ x, int64_t n,
          int H, const int2* __restrict__ tiles, typename CT<T>::c* __restrict__ npart,
          typename CT<T>::c* __restrict__ hpart, const int* gate, int pin) {
