@@ -143,6 +143,7 @@ struct ccg_ctx {
   size_t npart_bytes = 0;
   // complex-symmetric dense A (CCG_FLAG_SYMMETRIC, one rank): upper-triangle
   // products (matvec.cuh gemv_sym; CCG_SYMV=0 disables)
+  int stencil_minb = 4;   // stencil7_kernel launch bound: 4 CTAs/SM (≤ 64 registers); CCG_STENCIL_MINB=1: none
   bool sym_ok = false;
   int sym_H = 64, sym_ntiles = 0, sym_strips = 1, sym_s2_grid = 1;
   int2* sym_tiles = nullptr;
@@ -434,7 +435,8 @@ struct Engine {
       k[i].y = (T)(conj ? -c->scoef[i].y : c->scoef[i].y);
     }
     dim3 g((c->snx + 31) / 32, (c->sny + 7) / 8, (c->snzl + c->szc - 1) / c->szc);
-    launch_k(c, stencil7_kernel<T, Epi>, g, 256, 0, c->stream, xfull, c->snx, c->sny, c->snz, c->sz0, c->snzl, c->szc,
+    auto kern = c->stencil_minb == 4 ? stencil7_kernel<T, Epi, XLoad<T>, 4> : stencil7_kernel<T, Epi, XLoad<T>, 1>;
+    launch_k(c, kern, g, 256, 0, c->stream, xfull, c->snx, c->sny, c->snz, c->sz0, c->snzl, c->szc,
                                                        k[0], k[1], k[2], k[3], epi, make_red(c), c->st, gate, XLoad<T>{});
   }
 

@@ -1325,8 +1325,8 @@ __device__ __forceinline__ void st_term(C& acc, C coef, C v, bool has) {
 // the vector pass that would store it first is not a launch of its own; the
 // epilogue stores the element for its own point.  Only transforms that read
 // vectors this kernel does not write (no ping-pong needed between CTAs).
-template <typename T, class Epi, class XIn = XLoad<T>>
-__global__ void __launch_bounds__(256)
+template <typename T, class Epi, class XIn = XLoad<T>, int MINB = 1>
+__global__ void __launch_bounds__(256, MINB)
 stencil7_kernel(const typename CT<T>::c* __restrict__ x, int nx, int ny, int nz, int z0, int nzl, int zc,
                 typename CT<T>::c d, typename CT<T>::c ox, typename CT<T>::c oy, typename CT<T>::c oz,
                 Epi epi, Red red, State* st, const int* gate, XIn xin) {
