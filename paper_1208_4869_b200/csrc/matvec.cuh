@@ -853,51 +853,73 @@ gemv_sym_dual(const typename CT<T>::c* __restrict__ A, int64_t lda, const typena
   const int64_t ldv = lda / V;
   const LV* pv = reinterpret_cast<const LV*>(pcol) + lane;
   const LV* qv = reinterpret_cast<const LV*>(qcol) + lane;
+  // two rows per step (t, t + 1): 8 loads in flight per lane, and the row sums
+  // of the pair share one transposed shuffle level (lanes 0-15 keep row t,
+  // lanes 16-31 row t + 1), then a 4-level butterfly inside each half
   auto body = [&](auto dg) {
     constexpr bool DG = decltype(dg)::value;
-    for (int t = warp; t < rn; t += NW) {
-      const int64_t row = r0 + t;
-      LV a[U];
+    for (int t = 2 * warp; t < rn; t += 2 * NW) {
+      LV a[2][U];
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int64_t j0 = cbeg + (int64_t)(lane + 32 * u) * V;
-        const bool need = act[u] && (!DG || j0 + V - 1 >= row);
-        a[u] = need ? ld_stream(Ab + row * ldv + 32 * u) : LV{};
-      }
-      const C pi = prow[t], qi = qrow[t];
-      C n1 = czero<C>(), n2 = czero<C>();
+      for (int r = 0; r < 2; ++r) {
+        const int tr = min(t + r, rn - 1);
+        const int64_t row = r0 + tr;
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        C ac[V], pc[V], qc[V];
-        unpack(a[u], ac);
-        unpack(pv[32 * u], pc);
-        unpack(qv[32 * u], qc);
-        const int64_t j0 = cbeg + (int64_t)(lane + 32 * u) * V;
-#pragma unroll
-        for (int v = 0; v < V; ++v) {
-          C t1 = n1, t2 = n2, t3 = h1[u][v], t4 = h2[u][v];
-          cfma(t1, ac[v], pc[v]);
-          cfmac(t2, ac[v], qc[v]);
-          cfma(t3, ac[v], pi);
-          cfmac(t4, ac[v], qi);
-          const bool n_ok = !DG || j0 + v >= row, h_ok = !DG || j0 + v > row;
-          n1.x = n_ok ? t1.x : n1.x; n1.y = n_ok ? t1.y : n1.y;
-          n2.x = n_ok ? t2.x : n2.x; n2.y = n_ok ? t2.y : n2.y;
-          h1[u][v].x = h_ok ? t3.x : h1[u][v].x; h1[u][v].y = h_ok ? t3.y : h1[u][v].y;
-          h2[u][v].x = h_ok ? t4.x : h2[u][v].x; h2[u][v].y = h_ok ? t4.y : h2[u][v].y;
+        for (int u = 0; u < U; ++u) {
+          const int64_t j0 = cbeg + (int64_t)(lane + 32 * u) * V;
+          const bool need = act[u] && (t + r < rn) && (!DG || j0 + V - 1 >= row);
+          a[r][u] = need ? ld_stream(Ab + row * ldv + 32 * u) : LV{};
         }
       }
+      C n1[2], n2[2];
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        C t1 = n1, t2 = n2;
+      for (int r = 0; r < 2; ++r) {
+        const int tr = min(t + r, rn - 1);
+        const int64_t row = r0 + tr;
+        const C pi = prow[tr], qi = qrow[tr];
+        const bool live = t + r < rn;
+        n1[r] = czero<C>(); n2[r] = czero<C>();
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          C ac[V], pc[V], qc[V];
+          unpack(a[r][u], ac);
+          unpack(pv[32 * u], pc);
+          unpack(qv[32 * u], qc);
+          const int64_t j0 = cbeg + (int64_t)(lane + 32 * u) * V;
+#pragma unroll
+          for (int v = 0; v < V; ++v) {
+            C t1 = n1[r], t2 = n2[r], t3 = h1[u][v], t4 = h2[u][v];
+            cfma(t1, ac[v], pc[v]);
+            cfmac(t2, ac[v], qc[v]);
+            cfma(t3, ac[v], pi);
+            cfmac(t4, ac[v], qi);
+            const bool n_ok = !DG || j0 + v >= row, h_ok = live && (!DG || j0 + v > row);
+            n1[r].x = n_ok ? t1.x : n1[r].x; n1[r].y = n_ok ? t1.y : n1[r].y;
+            n2[r].x = n_ok ? t2.x : n2[r].x; n2[r].y = n_ok ? t2.y : n2[r].y;
+            h1[u][v].x = h_ok ? t3.x : h1[u][v].x; h1[u][v].y = h_ok ? t3.y : h1[u][v].y;
+            h2[u][v].x = h_ok ? t4.x : h2[u][v].x; h2[u][v].y = h_ok ? t4.y : h2[u][v].y;
+          }
+        }
+      }
+      const bool up = lane & 16;
+      C s1 = up ? n1[0] : n1[1], s2 = up ? n2[0] : n2[1];
+      C k1 = up ? n1[1] : n1[0], k2 = up ? n2[1] : n2[0];
+      shfl_c(s1, 16);
+      shfl_c(s2, 16);
+      k1 = up ? cadd(s1, k1) : cadd(k1, s1);   // lane l and l ^ 16 add in the same order
+      k2 = up ? cadd(s2, k2) : cadd(k2, s2);
+#pragma unroll
+      for (int o = 8; o > 0; o >>= 1) {
+        C t1 = k1, t2 = k2;
         shfl_c(t1, o);
         shfl_c(t2, o);
-        n1 = cadd(n1, t1);
-        n2 = cadd(n2, t2);
+        k1 = cadd(k1, t1);
+        k2 = cadd(k2, t2);
       }
-      if (lane == 0) {
-        np1[(int64_t)c * n + row] = n1;
-        np2[(int64_t)c * n + row] = n2;
+      const int r = up ? 1 : 0;
+      if ((lane & 15) == 0 && t + r < rn) {
+        np1[(int64_t)c * n + r0 + t + r] = k1;
+        np2[(int64_t)c * n + r0 + t + r] = k2;
       }
     }
   };
