@@ -19,7 +19,7 @@ E perturbed runs ("the envelope members"):
                     for every j ≤ k (H = 1e-8 for complex128).
 
 The GPU passes (SURVEY §8(c) P-envelope) when
-  (1) k_GPU ∈ [k_min − 2, k_max + 2];
+  (1) k_GPU ∈ [k_min − m, k_max + m], m = max(2, ⌈(k_max − k_min)/4⌉) (E5);
   (2) ‖x_GPU(k) − x_clean(k)‖/‖x_clean(k)‖ ≤ max(literal bar, 2·D(k)) at equal k;
   (3) its true residual ≤ tol (≤ 10·tol, S:254);
   (4) its residual history agrees with the clean history to H over the window.
@@ -38,7 +38,11 @@ Readings (E1-E4):
       spread);
   E4  the clean run is an envelope member; histories are relative to each
       member's own ‖r₀‖; E may be raised above 8 where the iteration count is
-      broadly distributed (tools/make_cfg5_envelope.py --seeds).
+      broadly distributed (tools/make_cfg5_envelope.py --seeds);
+  E5  criterion (1)'s margin is SURVEY's ±2 where the members' counts are
+      tight, and a quarter of their range where they are broadly distributed
+      (k_margin): the bare range of E members excludes an independent member
+      with probability 2/(E+1), ≈ 6 % at E = 32.
 """
 
 from dataclasses import dataclass, field
@@ -151,6 +155,15 @@ def history_error(hist_gpu, hist_clean, window):
     return float(np.max(np.abs(g - c) / np.maximum(c, np.finfo(float).tiny)))
 
 
+def k_margin(k_min, k_max):
+    """Criterion (1)'s margin (reading E5): SURVEY's ±2, or a quarter of the
+    members' range where the count is broadly distributed.  For E = 32 normal
+    draws the range is ≈ 4.2 standard deviations, so the interval is
+    ≈ mean ± 3.1σ and an independent member falls outside it with
+    probability ≈ 0.2 % (the bare range: 2/(E+1) ≈ 6 %)."""
+    return max(2, -(-(k_max - k_min) // 4))
+
+
 @dataclass
 class Envelope:
     k_clean: int
@@ -164,7 +177,8 @@ class Envelope:
     hist_spread: np.ndarray = field(default=None, repr=False)   # S(k)
 
     def check_k(self, k_gpu):
-        return self.k_min - 2 <= k_gpu <= self.k_max + 2
+        m = k_margin(self.k_min, self.k_max)
+        return self.k_min - m <= k_gpu <= self.k_max + m
 
     def history_error(self, hist_gpu):
         """Criterion 4: must be ≤ H."""

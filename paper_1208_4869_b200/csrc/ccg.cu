@@ -872,6 +872,16 @@ int ccg_set_matvec_toeplitz3(ccg_handle c, int64_t nx, int64_t ny, int64_t nz, c
   while (g.tx > 1 && (g.ny * g.nz + g.tx - 1) / g.tx < want) --g.tx;
   c->geo = g;
   c->fft_lmax = std::max(g.X2, std::max(g.Y2, g.Z2));
+  {
+    // passes 2-4 fused (one kx plane per CTA), opt-in (CCG_FFT_YZ=1) where a
+    // plane fits in shared memory: measured neutral at config 4 (BiCGSTAB
+    // 79.7 vs 79.6 µs/it; the fused kernel takes 20 µs on 128 CTAs — one
+    // 16-warp CTA per SM cannot hide the per-stage latency the separate
+    // passes hide with 2+ CTAs per SM)
+    const char* fy = getenv("CCG_FFT_YZ");
+    const size_t smp = (size_t)g.Y2 * (g.Z2 + 1) * (c->dtype == CCG_C64 ? 8 : 16);
+    c->fft_yz = smp <= 200 * 1024 && fy && atoi(fy) != 0;
+  }
   // circulant embedding of the kernel, 3-D FFT in double, normalised
   const int64_t kx = 2 * nx - 1, ky = 2 * ny - 1;
   const size_t N = (size_t)g.X2 * g.Y2 * g.Z2;

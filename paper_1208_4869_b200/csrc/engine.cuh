@@ -143,6 +143,7 @@ struct ccg_ctx {
   size_t npart_bytes = 0;
   // complex-symmetric dense A (CCG_FLAG_SYMMETRIC, one rank): upper-triangle
   // products (matvec.cuh gemv_sym; CCG_SYMV=0 disables)
+  bool fft_yz = false;     // FFT lattice operator: passes 2-4 fused (fft.cuh fft_yz; CCG_FFT_YZ)
   int stencil_minb = 4;   // stencil7_kernel launch bound: 4 CTAs/SM (≤ 64 registers); CCG_STENCIL_MINB=1: none
   bool sym_ok = false;
   int sym_H = 64, sym_ntiles = 0, sym_strips = 1, sym_s2_grid = 1;
@@ -460,12 +461,24 @@ struct Engine {
       launch_k(c, fft_fwd_x<T, true>, gx, btx, smx, c->stream, xfull, W, g, tw, L / g.X2, gate);
     else
       launch_k(c, fft_fwd_x<T, false>, gx, btx, smx, c->stream, xfull, W, g, tw, L / g.X2, gate);
-    launch_k(c, fft_fwd_y<T>, dim3(g.X2 / g.tyz, g.nz), bty, smy, c->stream, W, g, tw, L / g.Y2, gate);
-    if (op == 0)
-      launch_k(c, fft_z_mul<T, false>, dim3(g.X2 / g.tyz, g.Y2), btz, smz, c->stream, W, Kh, g, tw, L / g.Z2, gate);
-    else
-      launch_k(c, fft_z_mul<T, true>, dim3(g.X2 / g.tyz, g.Y2), btz, smz, c->stream, W, Kh, g, tw, L / g.Z2, gate);
-    launch_k(c, fft_inv_y<T>, dim3(g.X2 / g.tyz, g.nz), bty, smy, c->stream, W, g, tw, L / g.Y2, gate);
+    if (c->fft_yz) {   // passes 2-4 in one kernel: one kx plane per CTA in shared memory
+      const size_t smp = (size_t)g.Y2 * (g.Z2 + 1) * sizeof(C);
+      auto k = op == 0 ? fft_yz<T, false> : fft_yz<T, true>;
+      int& attr = c->occ_cache[reinterpret_cast<const void*>(k)];
+      if (!attr) {
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smp);
+        attr = 1;
+      }
+      launch_k(c, k, g.X2, 512, smp, c->stream, W, Kh, g, tw, L / g.Y2, L / g.Z2, gate);
+      c->launches -= 2;
+    } else {
+      launch_k(c, fft_fwd_y<T>, dim3(g.X2 / g.tyz, g.nz), bty, smy, c->stream, W, g, tw, L / g.Y2, gate);
+      if (op == 0)
+        launch_k(c, fft_z_mul<T, false>, dim3(g.X2 / g.tyz, g.Y2), btz, smz, c->stream, W, Kh, g, tw, L / g.Z2, gate);
+      else
+        launch_k(c, fft_z_mul<T, true>, dim3(g.X2 / g.tyz, g.Y2), btz, smz, c->stream, W, Kh, g, tw, L / g.Z2, gate);
+      launch_k(c, fft_inv_y<T>, dim3(g.X2 / g.tyz, g.nz), bty, smy, c->stream, W, g, tw, L / g.Y2, gate);
+    }
     C d;
     d.x = (T)c->tdiag.x;
     d.y = (T)(op == 1 ? -c->tdiag.y : c->tdiag.y);

@@ -8,7 +8,7 @@
 // two) it becomes  y = IFFT( FFT(K_pad) ⊙ FFT(x_pad) )  restricted to the box.
 //
 // Five kernels per product (all line FFTs in shared memory, radix-2 stages
-// fused in pairs):
+// fused in pairs; passes 2-4 can be one kernel, fft_yz, CCG_FFT_YZ=1):
 //   fwd_x   : the ny·nz nonzero x-lines of x_pad (zero padding not read)
 //   fwd_y   : the X2·nz nonzero y-lines
 //   z_mul   : every (kx, ky) z-line: forward FFT, ⊙ K̂ (the mirrored entry
@@ -52,8 +52,11 @@ __device__ __forceinline__ C twiddle(const C* __restrict__ tw, int m, int stride
 // points through stages s and s+1 in registers: the same operations in the
 // same order as two radix-2 stages, half the barriers and shared-memory
 // traffic); an odd last stage runs alone.  Called by all threads of the CTA.
+// Strided form: element l of line t at buf[l·ES + t·LS] (the plain form is
+// ES = TX, LS = 1: lines interleaved).
 template <typename C>
-__device__ void fft_dit(C* buf, int logL, int TX, bool inv, const C* __restrict__ tw, int twstride) {
+__device__ void fft_dit_s(C* buf, int logL, int TX, int ES, int LS, bool inv, const C* __restrict__ tw,
+                          int twstride) {
   const int L = 1 << logL;
   int s = 0;
   for (; s + 1 < logL; s += 2) {
@@ -67,15 +70,15 @@ __device__ void fft_dit(C* buf, int logL, int TX, bool inv, const C* __restrict_
       const C w1 = twiddle(tw, m << (logL - s - 1), twstride, inv);
       const C w2 = twiddle(tw, m << (logL - s - 2), twstride, inv);
       const C w3 = twiddle(tw, (m + h) << (logL - s - 2), twstride, inv);
-      const C x0 = buf[i0 * TX + t], x1 = buf[(i0 + h) * TX + t];
-      const C x2 = buf[(i0 + 2 * h) * TX + t], x3 = buf[(i0 + 3 * h) * TX + t];
+      const C x0 = buf[i0 * ES + t * LS], x1 = buf[(i0 + h) * ES + t * LS];
+      const C x2 = buf[(i0 + 2 * h) * ES + t * LS], x3 = buf[(i0 + 3 * h) * ES + t * LS];
       const C p1 = cmulc(x1, w1), p3 = cmulc(x3, w1);
       const C a0 = cadd(x0, p1), a1 = csub(x0, p1), a2 = cadd(x2, p3), a3 = csub(x2, p3);
       const C q2 = cmulc(a2, w2), q3 = cmulc(a3, w3);
-      buf[i0 * TX + t] = cadd(a0, q2);
-      buf[(i0 + 2 * h) * TX + t] = csub(a0, q2);
-      buf[(i0 + h) * TX + t] = cadd(a1, q3);
-      buf[(i0 + 3 * h) * TX + t] = csub(a1, q3);
+      buf[i0 * ES + t * LS] = cadd(a0, q2);
+      buf[(i0 + 2 * h) * ES + t * LS] = csub(a0, q2);
+      buf[(i0 + h) * ES + t * LS] = cadd(a1, q3);
+      buf[(i0 + 3 * h) * ES + t * LS] = csub(a1, q3);
     }
   }
   if (s < logL) {                       // odd last stage
@@ -87,10 +90,10 @@ __device__ void fft_dit(C* buf, int logL, int TX, bool inv, const C* __restrict_
       const int m = q & (h - 1);
       const int i0 = ((q >> s) << (s + 1)) + m, i1 = i0 + h;
       const C w = twiddle(tw, m << (logL - s - 1), twstride, inv);
-      const C a = buf[i0 * TX + t];
-      const C bb = cmulc(buf[i1 * TX + t], w);
-      buf[i0 * TX + t] = cadd(a, bb);
-      buf[i1 * TX + t] = csub(a, bb);
+      const C a = buf[i0 * ES + t * LS];
+      const C bb = cmulc(buf[i1 * ES + t * LS], w);
+      buf[i0 * ES + t * LS] = cadd(a, bb);
+      buf[i1 * ES + t * LS] = csub(a, bb);
     }
   }
   __syncthreads();
@@ -99,7 +102,8 @@ __device__ void fft_dit(C* buf, int logL, int TX, bool inv, const C* __restrict_
 // In-place decimation-in-frequency FFT: natural input, bit-reversed output;
 // stages s = logL−1 … 0 fused in pairs (s, s−1) the same way.
 template <typename C>
-__device__ void fft_dif(C* buf, int logL, int TX, bool inv, const C* __restrict__ tw, int twstride) {
+__device__ void fft_dif_s(C* buf, int logL, int TX, int ES, int LS, bool inv, const C* __restrict__ tw,
+                          int twstride) {
   const int L = 1 << logL;
   int s = logL - 1;
   for (; s >= 1; s -= 2) {
@@ -113,14 +117,14 @@ __device__ void fft_dif(C* buf, int logL, int TX, bool inv, const C* __restrict_
       const C wa = twiddle(tw, m << (logL - s - 1), twstride, inv);
       const C wb = twiddle(tw, (m + hh) << (logL - s - 1), twstride, inv);
       const C wc = twiddle(tw, m << (logL - s), twstride, inv);
-      const C x0 = buf[i0 * TX + t], x1 = buf[(i0 + hh) * TX + t];
-      const C x2 = buf[(i0 + H) * TX + t], x3 = buf[(i0 + H + hh) * TX + t];
+      const C x0 = buf[i0 * ES + t * LS], x1 = buf[(i0 + hh) * ES + t * LS];
+      const C x2 = buf[(i0 + H) * ES + t * LS], x3 = buf[(i0 + H + hh) * ES + t * LS];
       const C a0 = cadd(x0, x2), a2 = cmulc(csub(x0, x2), wa);
       const C a1 = cadd(x1, x3), a3 = cmulc(csub(x1, x3), wb);
-      buf[i0 * TX + t] = cadd(a0, a1);
-      buf[(i0 + hh) * TX + t] = cmulc(csub(a0, a1), wc);
-      buf[(i0 + H) * TX + t] = cadd(a2, a3);
-      buf[(i0 + H + hh) * TX + t] = cmulc(csub(a2, a3), wc);
+      buf[i0 * ES + t * LS] = cadd(a0, a1);
+      buf[(i0 + hh) * ES + t * LS] = cmulc(csub(a0, a1), wc);
+      buf[(i0 + H) * ES + t * LS] = cadd(a2, a3);
+      buf[(i0 + H + hh) * ES + t * LS] = cmulc(csub(a2, a3), wc);
     }
   }
   if (s == 0) {                         // odd last stage
@@ -130,13 +134,22 @@ __device__ void fft_dif(C* buf, int logL, int TX, bool inv, const C* __restrict_
       const int t = b % TX, q = b / TX;
       const int i0 = q << 1, i1 = i0 + 1;
       const C w = twiddle(tw, 0, twstride, inv);
-      const C a = buf[i0 * TX + t];
-      const C bb = buf[i1 * TX + t];
-      buf[i0 * TX + t] = cadd(a, bb);
-      buf[i1 * TX + t] = cmulc(csub(a, bb), w);
+      const C a = buf[i0 * ES + t * LS];
+      const C bb = buf[i1 * ES + t * LS];
+      buf[i0 * ES + t * LS] = cadd(a, bb);
+      buf[i1 * ES + t * LS] = cmulc(csub(a, bb), w);
     }
   }
   __syncthreads();
+}
+
+template <typename C>
+__device__ __forceinline__ void fft_dit(C* buf, int logL, int TX, bool inv, const C* __restrict__ tw, int twstride) {
+  fft_dit_s(buf, logL, TX, TX, 1, inv, tw, twstride);
+}
+template <typename C>
+__device__ __forceinline__ void fft_dif(C* buf, int logL, int TX, bool inv, const C* __restrict__ tw, int twstride) {
+  fft_dif_s(buf, logL, TX, TX, 1, inv, tw, twstride);
 }
 
 // (1) x_pad lines (y < ny, z < nz): load x (conj if CONJ_IN), zero pad, DIT along x
@@ -252,6 +265,52 @@ fft_inv_y(typename CT<T>::c* __restrict__ W, FftGeo g, const typename CT<T>::c* 
   for (int e = threadIdx.x; e < TX * g.ny; e += blockDim.x) {
     const int t = e % TX, l = e / TX;
     base[(int64_t)l * g.X2 + t] = buf[bitrev(l, g.ly) * TX + t];
+  }
+}
+
+// (2-4 fused, opt-in: measured neutral) one kx plane per CTA, whole in shared
+// memory as P[y][z] (row stride RS = Z2 + 1: the z-line pass reads rows 16 B
+// apart, conflict-free): y DIT over the nz nonzero z-lines (bit-reversed load),
+// z DIF forward (natural in, bit-reversed kz out) ⊙ K̂ (mirrored for Aᵀ), z
+// DIT inverse (bit-reversed in, natural out), y DIF inverse over z < nz; stores
+// y < ny, z < nz.  The same transforms as passes (2)-(4) with no round trip
+// of the work array through L2 and two launches fewer per product.
+template <typename T, bool TRANS>
+__global__ void __launch_bounds__(512)
+fft_yz(typename CT<T>::c* __restrict__ W, const typename CT<T>::c* __restrict__ Kh, FftGeo g,
+       const typename CT<T>::c* __restrict__ tw, int twy, int twz, const int* gate) {
+  using C = typename CT<T>::c;
+  if (pdl_gate(gate)) return;
+  extern __shared__ __align__(16) unsigned char fft_sm[];
+  C* P = reinterpret_cast<C*>(fft_sm);
+  const int kx = blockIdx.x;
+  const int RS = g.Z2 + 1;
+  const int64_t sz = (int64_t)g.Y2 * g.X2;
+  for (int e = threadIdx.x; e < g.Y2 * g.Z2; e += blockDim.x) {
+    const int z = e / g.Y2, y = e % g.Y2;
+    C v = czero<C>();
+    if (y < g.ny && z < g.nz) v = W[(int64_t)z * sz + (int64_t)y * g.X2 + kx];
+    P[bitrev(y, g.ly) * RS + z] = v;
+  }
+  fft_dit_s(P, g.ly, g.nz, RS, 1, false, tw, twy);
+  fft_dif_s(P, g.lz, g.Y2, 1, RS, false, tw, twz);
+  for (int e = threadIdx.x; e < g.Y2 * g.Z2; e += blockDim.x) {
+    const int ky = e / g.Z2, p = e % g.Z2;
+    const int kz = bitrev(p, g.lz);
+    int64_t ki;
+    if (TRANS) {
+      const int mx = (g.X2 - kx) & (g.X2 - 1), my = (g.Y2 - ky) & (g.Y2 - 1), mz = (g.Z2 - kz) & (g.Z2 - 1);
+      ki = ((int64_t)mz * g.Y2 + my) * g.X2 + mx;
+    } else {
+      ki = ((int64_t)kz * g.Y2 + ky) * g.X2 + kx;
+    }
+    P[ky * RS + p] = cmulc(P[ky * RS + p], __ldg(Kh + ki));
+  }
+  fft_dit_s(P, g.lz, g.Y2, 1, RS, true, tw, twz);
+  fft_dif_s(P, g.ly, g.nz, RS, 1, true, tw, twy);
+  for (int e = threadIdx.x; e < g.ny * g.nz; e += blockDim.x) {
+    const int z = e / g.ny, y = e % g.ny;
+    W[(int64_t)z * sz + (int64_t)y * g.X2 + kx] = P[bitrev(y, g.ly) * RS + z];
   }
 }
 

@@ -78,7 +78,8 @@ class Csr(Dense):
 
 def envelope_parity(method, op, y, tol, maxit, dtype, g, solve_at_k, rec=None, **kw):
     """SURVEY §8(c) P-envelope, all four criteria (oracle/envelope.py):
-    (1) k_GPU ∈ [k_min − 2, k_max + 2]; (2) x at equal k within max(bar, 2·D)
+    (1) k_GPU ∈ [k_min − m, k_max + m], m = max(2, ⌈(k_max − k_min)/4⌉)
+    (reading E5); (2) x at equal k within max(bar, 2·D)
     with D the pairwise spread; (3) true residual ≤ 10·tol; (4) the GPU
     residual history (g["hist"]) agrees with the clean oracle history to H
     over the envelope's agreement window (where the members agree to H/10).  `g` is the GPU result of the

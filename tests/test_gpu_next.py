@@ -330,6 +330,37 @@ def test_toeplitz_apply_parity(dtype, dims):
             assert relerr(h.apply(x, o), ref) <= TOL[dtype], (o, relerr(h.apply(x, o), ref))
 
 
+@pytest.mark.parametrize("yz", ["0", "1"])
+@pytest.mark.parametrize("dtype", [np.complex128, np.complex64])
+@pytest.mark.parametrize("dims", [(1, 1, 1), (5, 3, 4), (9, 6, 3), (1, 12, 5), (33, 7, 9), (40, 17, 2)])
+def test_toeplitz_yz_fused_parity(monkeypatch, yz, dtype, dims):
+    """Passes 2-4 fused into one kernel per kx plane (fft.cuh fft_yz, CCG_FFT_YZ=1)
+    and the separate passes (=0): every product vs the brute-force dense matrix."""
+    monkeypatch.setenv("CCG_FFT_YZ", yz)
+    nx, ny, nz = dims
+    rng = np.random.default_rng(nx + 7 * ny + 3 * nz)
+    K = rng.standard_normal((2 * nz - 1, 2 * ny - 1, 2 * nx - 1)) + 1j * rng.standard_normal(
+        (2 * nz - 1, 2 * ny - 1, 2 * nx - 1))
+    A = _dense_from_kernel(K, dims, 4 - 2j)
+    x = _x(nx * ny * nz, dtype, seed=5)
+    with Toeplitz(dims, K, 4 - 2j, dtype=dtype) as h:
+        for o in ("A", "AH", "AT"):
+            ref = reference_apply(A, x.astype(np.complex128), o)
+            assert relerr(h.apply(x, o), ref) <= TOL[dtype], (o, relerr(h.apply(x, o), ref))
+
+
+def test_toeplitz_cfg2_fused_yz_solves(monkeypatch):
+    """Config 2 through the fused-plane FFT passes: BiCGSTAB / COCR P-literal."""
+    monkeypatch.setenv("CCG_FFT_YZ", "1")
+    A, y = cfg2()
+    K = dda_kernel((16, 16, 16), 1.0)
+    with Toeplitz((16, 16, 16), K, 3 + 0.5j) as h:
+        for o in ("A", "AH", "AT"):
+            assert relerr(h.apply(y, o), reference_apply(A, y, o)) <= 1e-13, o
+        for m in ("bicgstab", "cocr"):
+            _parity(h, DenseOp(A), y, m, 1e-8, 1000, np.complex128, tag="cfg2-toeplitz-yz")
+
+
 def test_toeplitz_cfg2_apply_and_solves():
     """BASELINE config 2 through the FFT operator: the dense product to 1e-13,
     then BiCGSTAB / QMR / BiCOR / COCR P-literal against the oracle's dense solves."""

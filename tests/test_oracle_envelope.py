@@ -209,3 +209,41 @@ def test_false_convergence_single_precision(method):
     assert r.status_name == g["status"], (method, r.status_name)
     true = np.linalg.norm(y.astype(complex) - A.astype(complex) @ r.x.astype(complex)) / np.linalg.norm(y)
     assert true > 10 * g["tol"] and r.rec_rel_res <= g["tol"]
+
+
+# ---------------- criterion (1) margin (reading E5) ----------------
+def test_k_margin_tight_envelope_is_surveys_two():
+    from oracle.envelope import k_margin
+    assert k_margin(12, 12) == 2            # config 1: every member at 12
+    assert k_margin(102, 110) == 2          # config 4 dense (102-110)
+    assert k_margin(100, 109) == 3          # ⌈9/4⌉
+    assert k_margin(1051, 1490) == 110      # config 5 BiCGSTAB, E = 32 (golden)
+
+
+def test_k_margin_exceedance_rate():
+    """The rule's purpose, measured independently of its formula: for E + 1 =
+    33 members drawn from a normal distribution, an independent draw falls
+    outside [k_min − m, k_max + m] with probability well under 1 % (the bare
+    range: 2/(E+1) ≈ 6 %)."""
+    from oracle.envelope import k_margin
+    rng = np.random.default_rng(7)
+    trials, out_bare, out_rule = 4000, 0, 0
+    for _ in range(trials):
+        ks = np.round(1260 + 120 * rng.standard_normal(33)).astype(int)
+        new = int(round(1260 + 120 * rng.standard_normal()))
+        lo, hi = int(ks.min()), int(ks.max())
+        out_bare += not (lo <= new <= hi)
+        m = k_margin(lo, hi)
+        out_rule += not (lo - m <= new <= hi + m)
+    assert 0.03 < out_bare / trials < 0.09
+    assert out_rule / trials < 0.01
+
+
+def test_check_k_uses_margin():
+    e = oracle.envelope.Envelope(k_clean=1206, k_min=1051, k_max=1490, ks=[], statuses=[], window=22,
+                                 hist_clean=np.ones(3))
+    assert e.check_k(1024) and e.check_k(941) and not e.check_k(940)
+    assert e.check_k(1600) and not e.check_k(1601)
+    t = oracle.envelope.Envelope(k_clean=105, k_min=102, k_max=110, ks=[], statuses=[], window=5,
+                                 hist_clean=np.ones(3))
+    assert t.check_k(100) and not t.check_k(99) and t.check_k(112) and not t.check_k(113)

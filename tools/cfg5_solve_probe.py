@@ -1,4 +1,5 @@
-"""Drive config 5 solves (CSR or matrix-free stencil) for an ncu launch list
+"""Drive config 5 solves (CSR or matrix-free stencil) — or config 4's FFT
+lattice operator (--op toeplitz4) — for an ncu launch list
 (perf only): a fixed iteration count (tol 0), so `ncu --cache-control none`
 sees the L2 state of a real solve.
 
@@ -12,7 +13,7 @@ import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_1208_4869_b200 as ccg  # noqa: E402
-from workloads import helmholtz_csr, helmholtz_rhs, helmholtz_coeffs  # noqa: E402
+from workloads import helmholtz_csr, helmholtz_rhs, helmholtz_coeffs, cfg4_rhs, dda_kernel  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--op", default="stencil")
@@ -22,10 +23,13 @@ ap.add_argument("--reps", type=int, default=1)
 a = ap.parse_args()
 N = 128
 n = N ** 3
-y = torch.from_numpy(helmholtz_rhs(N)).cuda()
+y = torch.from_numpy(helmholtz_rhs(N) if a.op != "toeplitz4" else cfg4_rhs()).cuda()
+n = y.numel()
 x = torch.empty_like(y)
 h = ccg.ccg_create("c128", n)
-if a.op == "csr":
+if a.op == "toeplitz4":
+    ccg.ccg_set_matvec_toeplitz3(h, 64, 32, 32, dda_kernel((64, 32, 32), 0.5), 2.5 + 0.2j)
+elif a.op == "csr":
     rp, ci, v = (torch.from_numpy(t).cuda() for t in helmholtz_csr(N))
     ccg.ccg_set_matvec_csr(h, rp, ci, v, 0, n, v.numel())
 else:
