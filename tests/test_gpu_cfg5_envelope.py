@@ -107,3 +107,53 @@ def test_cfg5_full_size_envelope(problem, method, kind, env, monkeypatch):
     assert abs(tr - g["true_rel_res"]) <= 1e-3 * tr + 1e-15, rec
     for k, D in e["D"].items():                                                  # (2)
         assert xerr[k] <= max(1e-9, 2 * D), rec
+
+
+# ---------------------------------------------------------------------------
+# N = 64 proxy of config 5 (262 144 unknowns, the same k·h = 10/128): the FULL
+# P-envelope computed in-test by the oracle (8 noise seeds) —
+# k-range, x at equal k against the clean iterate within max(1e-9, 2·D(k)),
+# history agreement over the window, true residual — for both operators.
+# ---------------------------------------------------------------------------
+_ENV64 = {}
+
+
+def _env64(method):
+    from oracle.envelope import envelope, x_spread
+    if method not in _ENV64:
+        N64 = 64
+        rp, ci, v = helmholtz_csr(N64, kh=10 / 128)
+        y = helmholtz_rhs(N64)
+        op = CsrOp(rp, ci, v)
+        env = envelope(method, op, y, 1e-8, 4000)
+        xs = {k: x_spread(method, op, y, k) for k in (15, 40)}   # a tight and a loose D(k)
+        _ENV64[method] = (rp, ci, v, y, op, env, xs)
+    return _ENV64[method]
+
+
+@pytest.mark.parametrize("kind", ["csr", "stencil"])
+@pytest.mark.parametrize("method", ["bicgstab", "cors"])
+def test_cfg5_proxy64_full_envelope(method, kind):
+    rp, ci, v, y, op, env, xs = _env64(method)
+    N64 = 64
+    if kind == "csr":
+        h = Csr(rp, ci, v, N64 ** 3)
+    else:
+        d, o = helmholtz_coeffs(10 / 128)
+        h = Stencil(N64, N64, N64, d, o)
+    with h:
+        g = h.solve(method, y, 1e-8, 4000)
+        xk = {k: h.solve(method, y, 0.0, k)["x"] for k in xs}
+    tr = np.linalg.norm(y - op.apply(g["x"])) / np.linalg.norm(y)
+    rec = dict(test="cfg5-proxy64-envelope", op=kind, method=method, k_gpu=g["iterations"],
+               envelope_k=[env.k_min, env.k_max], hist_err=env.history_error(g["hist"]), window=env.window,
+               true_rel_res=tr)
+    for k, (xc, D) in xs.items():
+        rec[f"D{k}"], rec[f"x_err{k}"] = D, relerr(xk[k], xc)
+    _record(**rec)
+    assert g["status"] == "CONVERGED", rec
+    assert env.check_k(g["iterations"]), rec                      # (1)
+    for k, (xc, D) in xs.items():                                  # (2)
+        assert rec[f"x_err{k}"] <= max(1e-9, 2 * D), rec
+    assert tr <= 10 * 1e-8, rec                                    # (3)
+    assert rec["hist_err"] <= env.H, rec                           # (4)
