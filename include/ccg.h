@@ -203,7 +203,11 @@ int ccg_create_loopback_group_ex(ccg_handle* hs, int world, ccg_dtype dt, int64_
  *             product (A, Aᴴ, Aᵀ; QMR's A·p and Aᴴ·q in one pass) reads only
  *             the upper triangle j ≥ i: y_i = Σ_{j≥i} A_ij x_j + Σ_{j<i} A_ji x_j
  *             (same products up to summation order; env CCG_SYMV=0 reads all
- *             of A).  With world > 1 the flag is informational.
+ *             of A).  Without the flag (world == 1) the call tests A = Aᵀ bit
+ *             for bit on the device — one read of A if it holds, a few tiles
+ *             if not — and takes the same path when it holds
+ *             (CCG_STAT_SYMMETRIC tells which; env CCG_SYM_DETECT=0 skips the
+ *             test).  With world > 1 the flag is informational.
  * Supports CCG_OP_A, CCG_OP_AH, CCG_OP_AT. */
 int ccg_set_matvec_dense(ccg_handle h, const void* A_local, int64_t row0, int64_t nloc,
                          int64_t lda, uint32_t flags);
@@ -351,7 +355,9 @@ int64_t ccg_last_launch_count(ccg_handle h);
  * Returns CCG_E_ARG for an unknown key or NULL value. */
 enum { CCG_STAT_COMM_KIND = 0, CCG_STAT_GRAPH_REPLAYS = 1, CCG_STAT_GRAPH_COLLECTIVES = 2,
        CCG_STAT_EAGER_COLLECTIVES = 3, CCG_STAT_WORLD = 4, CCG_STAT_REPLICATED = 5,
-       CCG_STAT_P2P_EXCHANGES = 6 /* P2P mirror exchanges issued (host side, since create) */ };
+       CCG_STAT_P2P_EXCHANGES = 6 /* P2P mirror exchanges issued (host side, since create) */,
+       CCG_STAT_SYMMETRIC = 7 /* dense, one rank: 0 the general products, 1 upper-triangle products
+                                 (CCG_FLAG_SYMMETRIC), 2 upper-triangle products, A = Aᵀ detected */ };
 int ccg_get_stat(ccg_handle h, int32_t key, int64_t* value);
 
 /* cudaStream_t of the handle (for callers that order their own work). */

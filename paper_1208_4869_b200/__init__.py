@@ -316,7 +316,7 @@ def ccg_last_launch_count(h):
 
 
 STATS = {"comm_kind": 0, "graph_replays": 1, "graph_collectives": 2, "eager_collectives": 3,
-         "world": 4, "replicated": 5, "p2p_exchanges": 6}
+         "world": 4, "replicated": 5, "p2p_exchanges": 6, "symmetric": 7}
 
 
 def ccg_get_stat(h, key):

@@ -670,11 +670,38 @@ int ccg_set_matvec_dense(ccg_handle c, const void* A_local, int64_t row0, int64_
   c->flags = flags;
   c->vec_ok = (c->esz == 16) || (((uintptr_t)A_local % 16) == 0 && (lda % 2) == 0);
   {
-    // complex-symmetric A (caller's assertion, one rank): products from the
-    // upper triangle only (matvec.cuh gemv_sym; CCG_SYMV=0 reads all of A)
+    // complex-symmetric A, one rank: products from the upper triangle only
+    // (matvec.cuh gemv_sym; CCG_SYMV=0 reads all of A).  Declared by the caller
+    // (CCG_FLAG_SYMMETRIC) or detected exactly here: A = Aᵀ bit for bit, one
+    // read of A when it holds, a few tiles when it does not (CCG_SYM_DETECT=0
+    // skips the test).  The matrix is borrowed unmodified until the next
+    // set_matvec (ccg.h), so the property holds for every product.
     const char* sv = getenv("CCG_SYMV");
-    c->sym_ok = (flags & CCG_FLAG_SYMMETRIC) && !c->dist && c->vec_ok && (c->n % (16 / c->esz == 2 ? 2 : 1)) == 0 &&
-                !(sv && !strcmp(sv, "0"));
+    const char* sd = getenv("CCG_SYM_DETECT");
+    const bool usable = !c->dist && c->vec_ok && (c->n % (c->esz == 8 ? 2 : 1)) == 0 && !(sv && !strcmp(sv, "0"));
+    c->sym_state = 0;
+    if (usable && (flags & CCG_FLAG_SYMMETRIC)) {
+      c->sym_state = 1;
+    } else if (usable && !(sd && !strcmp(sd, "0"))) {
+      int* bad = nullptr;
+      CK(c, cudaMalloc(&bad, sizeof(int)));
+      CK(c, cudaMemsetAsync(bad, 0, sizeof(int), c->stream));
+      const int grid = c->sm_count * 8;
+      if (c->dtype == CCG_C64)
+        sym_check<float><<<grid, 256, 0, c->stream>>>(static_cast<const float2*>(A_local), lda, c->n, bad);
+      else
+        sym_check<double><<<grid, 256, 0, c->stream>>>(static_cast<const double2*>(A_local), lda, c->n, bad);
+      int hbad = 1;
+      const cudaError_t e1 = cudaGetLastError();
+      const cudaError_t e2 = cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, c->stream);
+      const cudaError_t e3 = cudaStreamSynchronize(c->stream);
+      cudaFree(bad);
+      CK(c, e1);
+      CK(c, e2);
+      CK(c, e3);
+      if (!hbad) c->sym_state = 2;
+    }
+    c->sym_ok = c->sym_state != 0;
   }
   {
     // L2-resident rows (matvec.cuh): ~80 MB of A kept in the
@@ -1337,6 +1364,7 @@ int ccg_get_stat(ccg_handle c, int32_t key, int64_t* value) {
     case CCG_STAT_WORLD: *value = c->world; break;
     case CCG_STAT_REPLICATED: *value = c->rep ? 1 : 0; break;
     case CCG_STAT_P2P_EXCHANGES: *value = c->p2p_calls; break;
+    case CCG_STAT_SYMMETRIC: *value = c->opk == OPK_DENSE ? c->sym_state : 0; break;
     default: FAIL(c, CCG_E_ARG, "unknown stat key");
   }
   return CCG_OK;

@@ -146,6 +146,7 @@ struct ccg_ctx {
   bool fft_yz = false;     // FFT lattice operator: passes 2-4 fused (fft.cuh fft_yz; CCG_FFT_YZ)
   int stencil_minb = 4;   // stencil7_kernel launch bound: 4 CTAs/SM (≤ 64 registers); CCG_STENCIL_MINB=1: none
   bool sym_ok = false;
+  int sym_state = 0;      // 0 general, 1 declared (CCG_FLAG_SYMMETRIC), 2 detected (A = Aᵀ bitwise)
   int sym_H = 64, sym_ntiles = 0, sym_strips = 1, sym_s2_grid = 1;
   int2* sym_tiles = nullptr;
   int sym2_H = 64, sym2_ntiles = 0, sym2_strips = 1;   // the dual product's tiles (gemv_sym_dual)

@@ -802,6 +802,56 @@ gemv_sym(const typename CT<T>::c* __restrict__ A, int64_t lda, const typename CT
   }
 }
 
+// bitwise equality of two complex values (their stored bit patterns)
+__device__ __forceinline__ bool memcmp_c(float2 a, float2 b) {
+  return __float_as_uint(a.x) == __float_as_uint(b.x) && __float_as_uint(a.y) == __float_as_uint(b.y);
+}
+__device__ __forceinline__ bool memcmp_c(double2 a, double2 b) {
+  return __double_as_longlong(a.x) == __double_as_longlong(b.x) &&
+         __double_as_longlong(a.y) == __double_as_longlong(b.y);
+}
+
+// Exact symmetry test A = Aᵀ (ccg_set_matvec_dense without CCG_FLAG_SYMMETRIC,
+// one rank): 32×32 tile pairs (I ≤ J) of the upper triangle, the lower tile
+// transposed through shared memory, the 16-byte patterns compared bitwise.
+// The first mismatch sets *bad and every CTA stops at its next tile, so a
+// general matrix costs a few tiles; a symmetric one one read of A.
+template <typename T>
+__global__ void __launch_bounds__(256)
+sym_check(const typename CT<T>::c* __restrict__ A, int64_t lda, int64_t n, int* bad) {
+  using C = typename CT<T>::c;
+  __shared__ C lo[32][33];
+  __shared__ int stop;
+  const int64_t NTL = (n + 31) / 32;
+  const int64_t pairs = NTL * (NTL + 1) / 2;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;   // 32 × 8
+  for (int64_t p = blockIdx.x; p < pairs; p += gridDim.x) {
+    if (threadIdx.x == 0) stop = *(volatile int*)bad;
+    __syncthreads();
+    if (stop) return;
+    // p -> (I, J), I ≤ J: row-major enumeration of the upper triangle of tiles
+    int64_t I = (int64_t)((2 * NTL + 1 - sqrt((double)(2 * NTL + 1) * (2 * NTL + 1) - 8.0 * (double)p)) / 2);
+    while (I > 0 && I * NTL - I * (I - 1) / 2 > p) --I;
+    while ((I + 1) * NTL - (I + 1) * I / 2 <= p) ++I;
+    const int64_t J = I + (p - (I * NTL - I * (I - 1) / 2));
+    bool ok = true;
+    for (int r = ty; r < 32; r += 8) {   // lower tile (J, I) -> shared, transposed on read
+      const int64_t i = J * 32 + r, j = I * 32 + tx;
+      if (i < n && j < n) lo[r][tx] = A[i * lda + j];
+    }
+    __syncthreads();
+    for (int r = ty; r < 32; r += 8) {   // upper tile (I, J): A[I*32+r][J*32+tx] vs A[J*32+tx][I*32+r]
+      const int64_t i = I * 32 + r, j = J * 32 + tx;
+      if (i < n && j < n) {
+        const C a = A[i * lda + j], b = lo[tx][r];
+        ok &= memcmp_c(a, b);
+      }
+    }
+    if (!ok) atomicExch(bad, 1);
+    __syncthreads();
+  }
+}
+
 // K1s' gemv_sym_dual: A·p and Aᴴ·q of one QMR / BiCG iteration (independent,
 // SURVEY §8(a) a7; §8(f) NEXT-1) from ONE pass over the upper triangle of a
 // complex-symmetric A — half of the full dual pass's bytes, the same as one

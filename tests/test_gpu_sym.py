@@ -142,3 +142,48 @@ def test_sym_dual_qmr(monkeypatch, dtype):
     bar = 1e-12 if dtype == np.complex128 else 1e-4
     assert relerr(a["x"], b["x"]) <= bar
     assert relerr(a["x"], o.x) <= (1e-9 if dtype == np.complex128 else 1e-4)
+
+
+def test_sym_detected_without_flag(monkeypatch):
+    """Without CCG_FLAG_SYMMETRIC a bitwise-symmetric A is detected on the
+    device (CCG_STAT_SYMMETRIC = 2) and takes the upper-triangle products; one
+    changed element (or CCG_SYM_DETECT=0) keeps the general path (0)."""
+    monkeypatch.setenv("CCG_SYM_DETECT", "1")   # the library default (conftest pins 0)
+    A, y = cfg2()
+    with Dense(A) as h:
+        assert ccg.ccg_get_stat(h.h, "symmetric") == 2
+        assert relerr(h.apply(y), reference_apply(A, y, "A")) <= TOL[np.complex128]
+        _parity(h, DenseOp(A), y, "bicgstab", 1e-8, 1000, np.complex128, tag="cfg2-sym-detected")
+    with Dense(A, flags=ccg.FLAG_SYMMETRIC) as h:
+        assert ccg.ccg_get_stat(h.h, "symmetric") == 1
+    for (i, j) in ((4095, 0), (0, 4095), (2000, 2001), (17, 3)):
+        B = A.copy()
+        B[i, j] += 1e-3
+        with Dense(B) as h:
+            assert ccg.ccg_get_stat(h.h, "symmetric") == 0, (i, j)
+            assert relerr(h.apply(y), reference_apply(B, y, "A")) <= TOL[np.complex128]
+    monkeypatch.setenv("CCG_SYM_DETECT", "0")
+    with Dense(A) as h:
+        assert ccg.ccg_get_stat(h.h, "symmetric") == 0
+
+
+@pytest.mark.parametrize("dtype", [np.complex128, np.complex64])
+@pytest.mark.parametrize("n", [1, 2, 31, 33, 100, 1000])
+def test_sym_detect_ragged(monkeypatch, dtype, n):
+    """Ragged n (partial 32×32 tiles): symmetric detected, a single flipped
+    entry anywhere in the last partial tile row is not; products exact."""
+    monkeypatch.setenv("CCG_SYM_DETECT", "1")
+    if dtype == np.complex64 and n % 2:
+        n += 1
+    A = _sym(n, dtype, seed=40 + n)
+    x = _x(n, dtype, seed=41)
+    with Dense(A) as h:
+        assert ccg.ccg_get_stat(h.h, "symmetric") == 2
+        assert relerr(h.apply(x), reference_apply(A.astype(np.complex128), x.astype(np.complex128), "A")) \
+            <= TOL[dtype]
+    if n > 1:
+        B = A.copy()
+        j = (n - 1) // 2                       # off the diagonal (j < n − 1)
+        B[n - 1, j] = B[n - 1, j] * (1 + 1e-3)
+        with Dense(B) as h:
+            assert ccg.ccg_get_stat(h.h, "symmetric") == 0

@@ -58,14 +58,17 @@ def run_dense(cfg, A, y, methods, tol, maxit, reps, dtype, toeplitz=None):
     n = y.shape[0]
     s = 8 if dtype == "c64" else 16
     h = ccg.ccg_create(dtype, n)
-    if toeplitz is None and SYM_FLAG and cfg in (2, 4):
-        ccg.ccg_set_matvec_dense(h, A, 0, n, flags=ccg.FLAG_SYMMETRIC)
-        b_mat = n * (n + 1) // 2 * s       # the upper triangle: what the product reads
-        opname = "dense-sym"
-    elif toeplitz is None:
-        ccg.ccg_set_matvec_dense(h, A, 0, n)
-        b_mat = n * n * s
-        opname = "dense"
+    if toeplitz is None:
+        # the library detects A = Aᵀ itself (CCG_SYM_DETECT=0: general kernels);
+        # --sym declares it (CCG_FLAG_SYMMETRIC)
+        ccg.ccg_set_matvec_dense(h, A, 0, n, flags=ccg.FLAG_SYMMETRIC if (SYM_FLAG and cfg in (2, 4)) else 0)
+        sym = ccg.ccg_get_stat(h, "symmetric")
+        if sym:
+            b_mat = n * (n + 1) // 2 * s   # the upper triangle: what the product reads
+            opname = "dense-sym" if sym == 1 else "dense-sym-detected"
+        else:
+            b_mat = n * n * s
+            opname = "dense"
     else:
         ccg.ccg_set_matvec_toeplitz3(h, *toeplitz)
         b_mat = 2 * n * s                  # x read + y written: the FFT operator's irreducible bytes
