@@ -202,6 +202,24 @@ static int choose_launch(ccg_ctx* c) {
     if (occ3 < 1) occ3 = 1;
     c->spmv_grid = (int)std::max<int64_t>(1, std::min<int64_t>(c->csr_nblocks, (int64_t)c->sm_count * occ3));
   }
+  // QMR/BiCG dual product in the warp-per-row layout (gemv_dual_rows; one rank)
+  size_t need_dual_h = 0;
+  {
+    const char* dr = getenv("CCG_DUAL_ROWS");
+    // default on: config 3 QMR 687 -> 725 it/s, BiCG 663 -> 725; config 2 QMR
+    // 86.0 -> 83.9 us/it (CCG_DUAL_ROWS=0: the column-owner dual)
+    c->dual_rows = c->opk == OPK_DENSE && c->cols_ok && !c->dist && (dr ? atoi(dr) != 0 : true);
+    if (c->dual_rows) {
+      int occd2 = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occd2, gemv_dual_rows<T, E::NT>, NT, 0);
+      const int64_t CW = (int64_t)256 * CT<T>::V;
+      const int64_t nstr = (c->n + CW - 1) / CW;
+      int64_t H = SYM_HMAX;
+      while (H > 32 && nstr * ((c->nloc + H - 1) / H) < 2 * (int64_t)c->sm_count * std::max(1, occd2)) H /= 2;
+      c->dual_H = (int)H;
+      need_dual_h = (size_t)((c->nloc + H - 1) / H) * c->n * sizeof(C);
+    }
+  }
   size_t need_sym_h = 0;
   if (c->opk == OPK_DENSE && c->sym_ok) {
     // upper-triangle tiles: strips of CW columns × row blocks of H rows; the
@@ -258,8 +276,8 @@ static int choose_launch(ccg_ctx* c) {
     need_sym_h = std::max((size_t)nblk1, 2 * (size_t)nblk2) * c->n * sizeof(C);
   }
   // workspace sized for the chosen grids
-  size_t need_hpart = std::max((size_t)std::max(c->ah_S, c->cols_ok ? c->dual_S : 1) * (size_t)c->n * sizeof(C),
-                               need_sym_h);
+  size_t need_hpart = std::max({(size_t)std::max(c->ah_S, c->cols_ok ? c->dual_S : 1) * (size_t)c->n * sizeof(C),
+                                need_sym_h, need_dual_h});
   if (c->opk == OPK_DENSE && need_hpart > c->hpart_bytes) {
     if (c->hpart) cudaFree(c->hpart);
     c->hpart = nullptr;

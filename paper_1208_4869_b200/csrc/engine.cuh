@@ -143,6 +143,7 @@ struct ccg_ctx {
   size_t npart_bytes = 0;
   // complex-symmetric dense A (CCG_FLAG_SYMMETRIC, one rank): upper-triangle
   // products (matvec.cuh gemv_sym; CCG_SYMV=0 disables)
+  bool dual_rows = false; int dual_H = 512;   // QMR/BiCG dual product in the warp-per-row layout (CCG_DUAL_ROWS)
   bool fft_yz = false;     // FFT lattice operator: passes 2-4 fused (fft.cuh fft_yz; CCG_FFT_YZ)
   int stencil_minb = 4;   // stencil7_kernel launch bound: 4 CTAs/SM (≤ 64 registers); CCG_STENCIL_MINB=1: none
   bool sym_ok = false;
@@ -887,6 +888,22 @@ struct Engine {
                static_cast<const C*>(hp), c->n, c->sym2_H, CW2, c->sym2_strips, ea, make_red(c), c->st, gate);
       launch_k(c, gemv_sym_stage2<T, NT, EpiH>, c->sym_s2_grid, NT, 0, c->stream, static_cast<const C*>(np + ns),
                static_cast<const C*>(hp + nh), c->n, c->sym2_H, CW2, c->sym2_strips, eh, make_red(c), c->st, gate);
+      c->launches += 3;
+      tev_end(c);
+      CK(c, cudaGetLastError());
+      return CCG_OK;
+    }
+    if (c->dual_rows && !c->dist) {   // general A, warp-per-row dual (gemv_dual_rows)
+      const int CW = 256 * CT<T>::V;
+      const int nstrips = (int)((c->n + CW - 1) / CW);
+      const int nblk = (int)((c->nloc + c->dual_H - 1) / c->dual_H);
+      tev_begin(c, 0);
+      launch_k(c, gemv_dual_rows<T, NT>, nstrips * nblk, NT, 0, c->stream, A, c->lda, pfull, qloc, c->nloc, c->n,
+               c->dual_H, nstrips, np, hp, gate);
+      launch_k(c, gemv_h_stage2<T, NT, EpiA>, c->nstage2_grid, NT, 0, c->stream, static_cast<const C*>(np), nstrips,
+               c->nloc, 0, c->nloc, ea, make_red(c), c->st, gate);
+      launch_k(c, gemv_h_stage2<T, NT, EpiH>, c->stage2_grid, NT, 0, c->stream, static_cast<const C*>(hp), nblk, c->n,
+               0, c->n, eh, make_red(c), c->st, gate);
       c->launches += 3;
       tev_end(c);
       CK(c, cudaGetLastError());

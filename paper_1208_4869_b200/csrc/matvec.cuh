@@ -1002,6 +1002,90 @@ gemv_sym_dual(const typename CT<T>::c* __restrict__ A, int64_t lda, const typena
   }
 }
 
+// K2D' gemv_dual_rows: A·p and Aᴴ·q of one QMR / BiCG iteration from ONE pass
+// over a GENERAL A, in gemv_sym's warp-per-row layout:
+// tile = (strip c of CW = 256·V columns, row block I of H rows); a warp takes
+// whole 4-KiB row segments (8 independent 16-B loads per lane), forms the row
+// dot with p (shuffle tree, lane 0 stores np[c][i]) and keeps per-lane column
+// accumulators Σ_i conj(A_ij) q_i added over the tile's warps once (hp[I][j]).
+// No barrier in the row loop (the column-owner dual, gemv_cols<DO_N, DO_H>,
+// reduces its row sums across warps every 8 rows).  gemv_h_stage2 sums np over
+// the strips and hp over the row blocks, each in a fixed order.
+template <typename T, int NT>
+__global__ void __launch_bounds__(NT, 2)
+gemv_dual_rows(const typename CT<T>::c* __restrict__ A, int64_t lda, const typename CT<T>::c* __restrict__ p,
+               const typename CT<T>::c* __restrict__ q, int64_t nrows, int64_t n, int H, int nstrips,
+               typename CT<T>::c* __restrict__ np, typename CT<T>::c* __restrict__ hp, const int* gate) {
+  using C = typename CT<T>::c;
+  using LV = typename CT<T>::v;
+  constexpr int V = CT<T>::V;
+  constexpr int U = 8;
+  constexpr int CW = 32 * U * V;
+  constexpr int NW = NT / 32;
+  static_assert(NT == 256, "gemv_dual_rows: 8 warps");
+  if (pdl_gate(gate)) return;
+  __shared__ __align__(16) C pcol[CW];
+  __shared__ C qrow[SYM_HMAX];
+  __shared__ __align__(16) C hred[NW][CW];
+  const int c = (int)(blockIdx.x % nstrips), I = (int)(blockIdx.x / nstrips);   // row-block major
+  const int64_t cbeg = (int64_t)c * CW, cend = min(cbeg + CW, n);
+  const int64_t r0 = (int64_t)I * H, r1 = min(r0 + H, nrows);
+  const int rn = (int)(r1 - r0);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int t = threadIdx.x; t < CW; t += NT) pcol[t] = cbeg + t < n ? p[cbeg + t] : czero<C>();
+  for (int t = threadIdx.x; t < rn; t += NT) qrow[t] = q[r0 + t];
+  __syncthreads();
+  bool act[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) act[u] = cbeg + (int64_t)(lane + 32 * u) * V < cend;
+  C hacc[U][V];
+#pragma unroll
+  for (int u = 0; u < U; ++u)
+#pragma unroll
+    for (int v = 0; v < V; ++v) hacc[u][v] = czero<C>();
+  const LV* Ab = reinterpret_cast<const LV*>(A + cbeg) + lane;
+  const int64_t ldv = lda / V;
+  const LV* pv = reinterpret_cast<const LV*>(pcol) + lane;
+  for (int t = warp; t < rn; t += NW) {
+    const int64_t row = r0 + t;
+    LV a[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) a[u] = act[u] ? ld_stream(Ab + row * ldv + 32 * u) : LV{};
+    const C qi = qrow[t];
+    C acc = czero<C>();
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      C ac[V], pc[V];
+      unpack(a[u], ac);
+      unpack(pv[32 * u], pc);
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        cfma(acc, ac[v], pc[v]);
+        cfmac(hacc[u][v], ac[v], qi);
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      C tt = acc;
+      shfl_c(tt, o);
+      acc = cadd(acc, tt);
+    }
+    if (lane == 0) np[(int64_t)c * nrows + row] = acc;
+  }
+#pragma unroll
+  for (int u = 0; u < U; ++u)
+#pragma unroll
+    for (int v = 0; v < V; ++v) hred[warp][(lane + 32 * u) * V + v] = hacc[u][v];
+  __syncthreads();
+  for (int t = threadIdx.x; t < CW; t += NT) {
+    if (cbeg + t >= n) break;
+    C sum = hred[0][t];
+#pragma unroll
+    for (int w = 1; w < NW; ++w) sum = cadd(sum, hred[w][t]);
+    hp[(int64_t)I * n + cbeg + t] = sum;
+  }
+}
+
 // y_i = Σ_{c ≥ c(i)} npart[c][i] + Σ_{I < nb(c(i))} hpart[I][i] (fp64), then
 // the epilogue; c(i) = i / CW, nb(c) = the row blocks of strip c.  A CTA takes
 // 32 consecutive outputs (one strip: CW is a multiple of 32), lane = output;

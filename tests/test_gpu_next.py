@@ -733,3 +733,42 @@ def test_pipelined_chunks_bitwise(monkeypatch, method):
     assert a["status"] == b["status"] == "CONVERGED"
     assert a["iterations"] == b["iterations"] and np.array_equal(a["x"], b["x"])
     assert a["true_rel_res"] == b["true_rel_res"]
+
+
+# ---------------------------------------------------------------------------
+# QMR / BiCG dual product in the warp-per-row layout (matvec.cuh
+# gemv_dual_rows, CCG_DUAL_ROWS=1): against the oracle and the column-owner dual
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("method", ["qmr", "bicg"])
+@pytest.mark.parametrize("sysname", ["cfg2", "c64"])
+def test_dual_rows_parity(monkeypatch, method, sysname):
+    monkeypatch.setenv("CCG_DUAL_ROWS", "1")
+    if sysname == "cfg2":
+        A, y = cfg2()
+        tol, dt = 1e-8, np.complex128
+    else:
+        n = 4096
+        A = gauss_shifted_rows(n, 0, n, seed=1)
+        y = cfg3_rhs(n)
+        tol, dt = 1e-5, np.complex64
+    with Dense(A) as h:
+        _parity(h, DenseOp(A), y, method, tol, 1000, dt, literal=False, tag=f"dual-rows-{sysname}")
+
+
+@pytest.mark.parametrize("n", [7, 257, 1000, 1537])
+def test_dual_rows_ragged(monkeypatch, n):
+    """Ragged n (partial strips and row blocks): QMR x after k iterations equal
+    to the column-owner dual's to rounding, and to the oracle's."""
+    A = dense_random(n, seed=n, dtype=np.complex128, shift=3 - 1j)
+    y = dense_random(n, seed=n + 1)[:, 0] * 3
+    k = 6
+    monkeypatch.setenv("CCG_CLUSTER", "0")
+    monkeypatch.setenv("CCG_DUAL_ROWS", "1")
+    with Dense(A) as h:
+        a = h.solve("qmr", y, 0.0, k)
+    monkeypatch.setenv("CCG_DUAL_ROWS", "0")
+    with Dense(A) as h:
+        b = h.solve("qmr", y, 0.0, k)
+    o = oracle.solve("qmr", DenseOp(A), y, 0.0, k)
+    assert relerr(a["x"], b["x"]) <= 1e-12
+    assert relerr(a["x"], o.x) <= 1e-9
