@@ -585,6 +585,7 @@ struct Engine {
   // with several strips and the strip sum in its own kernel (the epilogue that
   // rewrites the transformed vectors runs after every CTA has staged them)
   static bool in_fuse_ok(const ccg_ctx* c) {
+    if (c->bs_fuse && c->opk == OPK_DENSE && c->sym_ok && !c->dist && !c->jac_active) return true;   // gemv_sym
     return c->bs_fuse && c->opk == OPK_DENSE && !c->sym_ok && c->gemv_mode == GEMV_SPLIT && c->split_strips > 1 &&
            !c->split_fuse && !c->dist && !c->jac_active;
   }
@@ -621,6 +622,14 @@ struct Engine {
       CK(c, cudaGetLastError());
       return CCG_OK;
     }
+    if (c->opk == OPK_DENSE && c->sym_ok) {   // upper-triangle product, x staged through xin
+      tev_begin(c, 0);
+      sym_product(c, static_cast<const C*>(nullptr), false, epi, gate, xin);
+      c->launches += 2;
+      tev_end(c);
+      CK(c, cudaGetLastError());
+      return CCG_OK;
+    }
     const C* A = reinterpret_cast<const C*>(c->A);
     C* part = reinterpret_cast<C*>(c->npart);
     dim3 g(c->split_strips, c->split_nrb);
@@ -647,17 +656,18 @@ struct Engine {
 
   // complex-symmetric dense product from the upper triangle (gemv_sym):
   // conj => Aᴴx = conj(A)·x; Aᵀ = A
-  template <class Epi>
-  static void sym_product(ccg_ctx* c, const C* x, bool conj, Epi epi, const int* gate) {
+  template <class Epi, class XIn = XLoad<T>>
+  static void sym_product(ccg_ctx* c, const C* x, bool conj, Epi epi, const int* gate, XIn xin = XIn{}) {
     const C* A = reinterpret_cast<const C*>(c->A);
     C* np = reinterpret_cast<C*>(c->npart);
     C* hp = reinterpret_cast<C*>(c->hpart);
+    const State* stc = c->st;
     if (conj)
-      launch_k(c, gemv_sym<T, NT, true>, c->sym_ntiles, NT, 0, c->stream, A, c->lda, x, c->n, c->sym_H,
-               static_cast<const int2*>(c->sym_tiles), np, hp, gate, pin(c));
+      launch_k(c, gemv_sym<T, NT, true, XIn>, c->sym_ntiles, NT, 0, c->stream, A, c->lda, x, c->n, c->sym_H,
+               static_cast<const int2*>(c->sym_tiles), np, hp, gate, pin(c), stc, xin);
     else
-      launch_k(c, gemv_sym<T, NT, false>, c->sym_ntiles, NT, 0, c->stream, A, c->lda, x, c->n, c->sym_H,
-               static_cast<const int2*>(c->sym_tiles), np, hp, gate, pin(c));
+      launch_k(c, gemv_sym<T, NT, false, XIn>, c->sym_ntiles, NT, 0, c->stream, A, c->lda, x, c->n, c->sym_H,
+               static_cast<const int2*>(c->sym_tiles), np, hp, gate, pin(c), stc, xin);
     launch_k(c, gemv_sym_stage2<T, NT, Epi>, c->sym_s2_grid, NT, 0, c->stream, static_cast<const C*>(np),
              static_cast<const C*>(hp), c->n, c->sym_H, NT * CT<T>::V, c->sym_strips, epi, make_red(c), c->st, gate);
   }

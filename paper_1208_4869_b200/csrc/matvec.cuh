@@ -701,11 +701,13 @@ constexpr int SYM_HMAX = 512;
 #ifndef CCG_SYM_MINB
 #define CCG_SYM_MINB 2
 #endif
-template <typename T, int NT, bool CONJ>
+// XIn: input transform applied while staging x (BiCGSTAB's P / S folds,
+// methods.cuh BsPIn / BsSIn; the stage-2 epilogue stores the element)
+template <typename T, int NT, bool CONJ, class XIn = XLoad<T>>
 __global__ void __launch_bounds__(NT, CCG_SYM_MINB)
 gemv_sym(const typename CT<T>::c* __restrict__ A, int64_t lda, const typename CT<T>::c* __restrict__ x, int64_t n,
          int H, const int2* __restrict__ tiles, typename CT<T>::c* __restrict__ npart,
-         typename CT<T>::c* __restrict__ hpart, const int* gate, int pin) {
+         typename CT<T>::c* __restrict__ hpart, const int* gate, int pin, const State* st, XIn xin) {
   using C = typename CT<T>::c;
   using LV = typename CT<T>::v;
   constexpr int V = CT<T>::V;
@@ -723,8 +725,9 @@ gemv_sym(const typename CT<T>::c* __restrict__ A, int64_t lda, const typename CT
   const int64_t r0 = (int64_t)I * H, r1 = min(r0 + H, cend);
   const int rn = (int)(r1 - r0);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int t = threadIdx.x; t < CW; t += NT) xcol[t] = cbeg + t < n ? x[cbeg + t] : czero<C>();
-  for (int t = threadIdx.x; t < rn; t += NT) xrow[t] = x[r0 + t];
+  xin.load(st);
+  for (int t = threadIdx.x; t < CW; t += NT) xcol[t] = cbeg + t < n ? xin(x, cbeg + t) : czero<C>();
+  for (int t = threadIdx.x; t < rn; t += NT) xrow[t] = xin(x, r0 + t);
   __syncthreads();
   // this lane's chunks: k = lane + 32u, columns cbeg + kV .. + V − 1
   bool act[U];

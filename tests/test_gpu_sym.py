@@ -187,3 +187,20 @@ def test_sym_detect_ragged(monkeypatch, dtype, n):
         B[n - 1, j] = B[n - 1, j] * (1 + 1e-3)
         with Dense(B) as h:
             assert ccg.ccg_get_stat(h.h, "symmetric") == 0
+
+
+@pytest.mark.parametrize("k", [1, 2, 7, 20])
+def test_sym_bs_fuse_bitwise(monkeypatch, k):
+    """BiCGSTAB's P and S passes folded into the upper-triangle product (x
+    staged through BsPIn / BsSIn, the stage-2 epilogue stores p / s): the same
+    recurrence bit for bit as the separate passes (CCG_BS_FUSE=0)."""
+    A, y = cfg2()
+    res = []
+    for f in ("0", "1"):
+        monkeypatch.setenv("CCG_BS_FUSE", f)
+        with Dense(A, flags=ccg.FLAG_SYMMETRIC) as h:
+            res.append(h.solve("bicgstab", y, 0.0, k))
+    a, b = res
+    assert a["iterations"] == b["iterations"] == k
+    assert np.array_equal(a["x"], b["x"])
+    assert np.array_equal(np.asarray(a["hist"]), np.asarray(b["hist"]))
