@@ -520,6 +520,8 @@ static int create_impl(ccg_handle* h, ccg_dtype dt, int64_t n, int world, int ra
   {
     const char* pe = getenv("CCG_PDL");
     c->pdl = !(pe && !strcmp(pe, "0"));
+    const char* clr = getenv("CCG_CL_REDUNDANT");
+    c->cl_redundant = !(clr && !strcmp(clr, "0"));
     const char* bf = getenv("CCG_BS_FUSE");   // BiCGSTAB P/S folds into the dense split GEMV
     c->bs_fuse = bf ? atoi(bf) != 0 : 1;
     // the S fold on the stencil / SELL SpMV: measured slower at config 5

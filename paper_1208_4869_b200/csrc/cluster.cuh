@@ -88,6 +88,26 @@ struct ClusterCtx {
     }
   }
 
+  // the same pass over ALL rows in every CTA, its sums over all rows formed
+  // in-CTA (fixed order, identical in every CTA) and its scalar step run on the
+  // CTA's own State: no barrier, no DSMEM.  Only for passes whose outputs do
+  // not alias their inputs (every CTA writes the same values) and whose inputs
+  // are complete (written by this CTA, or before the last barrier).
+  template <class Op>
+  __device__ void rpass(Op op) {
+    constexpr int KK = Op::K > 0 ? Op::K : 1;
+    op.load(st);
+    double2 d[KK];
+#pragma unroll
+    for (int k = 0; k < KK; ++k) d[k] = make_double2(0.0, 0.0);
+    for (int64_t i = threadIdx.x; i < n; i += CL_NT) op(i, d);
+    if constexpr (Op::K > 0) {
+      block_sum<Op::K, CL_NT>(d, red_sm);
+      if (threadIdx.x == 0) Op::finish(st, d);
+    }
+    __syncthreads();
+  }
+
   // fused vector pass over this CTA's rows
   template <class Op>
   __device__ void pass(Op op) {
@@ -192,6 +212,73 @@ struct ClBicgstab {
     CL_PH(cx.pass(x));
   }
 };
+// BiCGSTAB with 2 cluster barriers per iteration instead of 5: the P and S
+// passes, the σ / ⟨t,s⟩,⟨t,t⟩ sums and the X pass run redundantly over all rows
+// in every CTA (rpass); barriers only after each product (its rows come from
+// every CTA).  P writes p out of place into the other of two buffers
+// (iteration parity), so no CTA reads a p another CTA is overwriting; the X
+// pass writes x only for this CTA's rows (x is updated in place), r for all
+// rows.  Same arithmetic as the multi-kernel path, sums in another fixed order.
+template <typename T>
+struct BsPo {   // p_out = r (k = 1) | r + β(p_in − ωv)   (BsP out of place)
+  static constexpr int K = 0;
+  using C = Cx<T>;
+  const C* r; const C* pin; C* pout; const C* v;
+  C beta, omega; int first;
+  __device__ void load(const State* st) {
+    first = st->iter == 0;
+    beta = fromd2<C>(st->beta); omega = fromd2<C>(st->omega);
+  }
+  __device__ void operator()(int64_t i, double2*) { pout[i] = bs_pnew(r[i], pin[i], v[i], beta, omega, first); }
+  static __device__ void finish(State*, const double2*) {}
+};
+template <typename T>
+struct BsXc {
+  static constexpr int K = 2;
+  using C = Cx<T>;
+  BsX<T> b;
+  int64_t r0, r1;
+  __device__ void load(const State* st) { b.load(st); }
+  __device__ void operator()(int64_t i, double2* acc) {
+    const bool own = i >= r0 && i < r1;
+    if (b.half) {
+      if (own) b.x[i] = caxpy(b.x[i], b.alpha, b.p[i]);
+      return;
+    }
+    const C si = b.s[i], ti = b.t[i], rti = b.rt[i];
+    if (own) b.x[i] = caxpy(caxpy(b.x[i], b.alpha, b.p[i]), b.omega, si);   // BsX's arithmetic
+    const C ri = caxmy(si, b.omega, ti);
+    b.r[i] = ri;
+    nrm_acc(acc[0], ri);
+    dotc_acc(acc[1], rti, ri);
+  }
+  static __device__ void finish(State* st, const double2* sm) { BsX<T>::finish(st, sm); }
+};
+template <typename T>
+struct ClBicgstabR {
+  BsP<T> p; BsV<T> v; BsS<T> s; BsT<T> t; BsX<T> x;
+  const typename CT<T>::c *pf, *sf;
+  typename CT<T>::c* p2;   // the second p buffer
+  __device__ void setup(ClusterCtx<T>&) {}
+  __device__ void iter(ClusterCtx<T>& cx) {
+    using C = typename CT<T>::c;
+    C* pa = const_cast<C*>(pf);
+    C* pin = (cx.st->iter & 1) ? p2 : pa;
+    C* pout = (cx.st->iter & 1) ? pa : p2;
+    CL_PH(cx.rpass(BsPo<T>{p.r, pin, pout, p.v}));       // p (all rows) into the other buffer
+    CL_PH(cx.gemv(Store<T>{v.v}, pout));                  // own rows of v; barrier
+    CL_PH(cx.rpass(EpiPass<C, BsV<T>>{v, v.v}));          // σ over all rows -> α
+    CL_PH(cx.rpass(s));                                   // s (all rows), ‖s‖², half-step test
+    if (!cx.st->gate2) {
+      cx.gemv(Store<T>{t.t}, sf);                         // own rows of t; barrier
+      cx.rpass(EpiPass<C, BsT<T>>{t, t.t});               // ⟨t,s⟩, ⟨t,t⟩ -> ω
+    }
+    BsX<T> xb = x;
+    xb.p = pout;
+    CL_PH(cx.rpass(BsXc<T>{xb, cx.r0, cx.r1}));
+  }
+};
+
 template <typename T>
 struct ClCgne {
   CgQ<T> q; CgP<T> p; CgP0<T> p0;

@@ -144,6 +144,7 @@ struct ccg_ctx {
   // complex-symmetric dense A (CCG_FLAG_SYMMETRIC, one rank): upper-triangle
   // products (matvec.cuh gemv_sym; CCG_SYMV=0 disables)
   bool dual_rows = false; int dual_H = 512;   // QMR/BiCG dual product in the warp-per-row layout (CCG_DUAL_ROWS)
+  bool cl_redundant = true;  // cluster BiCGSTAB with redundant all-row passes (3 barriers/it; CCG_CL_REDUNDANT)
   bool fft_yz = false;     // FFT lattice operator: passes 2-4 fused (fft.cuh fft_yz; CCG_FFT_YZ)
   int stencil_minb = 4;   // stencil7_kernel launch bound: 4 CTAs/SM (≤ 64 registers); CCG_STENCIL_MINB=1: none
   bool sym_ok = false;

@@ -10,6 +10,11 @@ template <typename T>
 int Engine<T>::cluster_run(ccg_ctx* c, int m) {
   switch (m) {
     case M_BICGSTAB:
+      if (c->cl_redundant)
+        return launch_cluster(c, ClBicgstabR<T>{BsP<T>{L(c, 2), Fs(c, 0), L(c, 4)}, BsV<T>{L(c, 4), L(c, 3)},
+                                                BsS<T>{L(c, 2), L(c, 4), Fs(c, 1)}, BsT<T>{L(c, 5), Fs(c, 1)},
+                                                BsX<T>{L(c, X), L(c, 2), Fs(c, 0), Fs(c, 1), L(c, 5), L(c, 3)},
+                                                F(c, 0), F(c, 1), F(c, 2)});
       return launch_cluster(c, ClBicgstab<T>{BsP<T>{L(c, 2), Fs(c, 0), L(c, 4)}, BsV<T>{L(c, 4), L(c, 3)},
                                              BsS<T>{L(c, 2), L(c, 4), Fs(c, 1)}, BsT<T>{L(c, 5), Fs(c, 1)},
                                              BsX<T>{L(c, X), L(c, 2), Fs(c, 0), Fs(c, 1), L(c, 5), L(c, 3)},
