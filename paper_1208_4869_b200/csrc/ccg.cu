@@ -562,18 +562,18 @@ static int create_impl(ccg_handle* h, ccg_dtype dt, int64_t n, int world, int ra
   }
   for (auto& e : c->done_ev) CKC(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   CKC(cudaMalloc(&c->ticket, sizeof(unsigned)));
-  CKC(cudaMemset(c->ticket, 0, sizeof(unsigned)));
+  CKC(cudaMemsetAsync(c->ticket, 0, sizeof(unsigned), c->stream));
   CKC(cudaMalloc(&c->rank_sum, 16 * sizeof(double2)));
   CKC(cudaMalloc(&c->all_sums, (size_t)16 * world * sizeof(double2)));
   CKC(cudaMalloc(&c->zero_gate, sizeof(int)));
-  CKC(cudaMemset(c->zero_gate, 0, sizeof(int)));
+  CKC(cudaMemsetAsync(c->zero_gate, 0, sizeof(int), c->stream));
   for (int i = 0; i < NLOCAL; ++i) {
     CKC(cudaMalloc(&c->loc[i], (size_t)c->nloc * c->esz));
-    CKC(cudaMemset(c->loc[i], 0, (size_t)c->nloc * c->esz));
+    CKC(cudaMemsetAsync(c->loc[i], 0, (size_t)c->nloc * c->esz, c->stream));
   }
   for (int i = 0; i < NFULL; ++i) {
     CKC(cudaMalloc(&c->full[i], (size_t)n * c->esz));
-    CKC(cudaMemset(c->full[i], 0, (size_t)n * c->esz));
+    CKC(cudaMemsetAsync(c->full[i], 0, (size_t)n * c->esz, c->stream));
   }
   if (c->rep) {
     CKC(cudaMalloc(&c->rep_tmp, (size_t)n * c->esz));
@@ -1076,13 +1076,13 @@ static int bicgstabl_workspace(ccg_ctx* c) {
     c->bl_buf = nullptr;
     c->bl_bytes = 0;
     CK(c, cudaMalloc(&c->bl_buf, need));
-    CK(c, cudaMemset(c->bl_buf, 0, need));
+    CK(c, cudaMemsetAsync(c->bl_buf, 0, need, c->stream));
     c->bl_bytes = need;
   }
   invalidate_graphs(c);   // buffer layout depends on ℓ
   if (!c->gm_dev) {
     CK(c, cudaMalloc(&c->gm_dev, sizeof(GmDev)));
-    CK(c, cudaMemset(c->gm_dev, 0, sizeof(GmDev)));
+    CK(c, cudaMemsetAsync(c->gm_dev, 0, sizeof(GmDev), c->stream));
   }
   return CCG_OK;
 }
@@ -1100,7 +1100,7 @@ static int gmres_workspace(ccg_ctx* c) {
   }
   if (!c->gm_dev) {   // (BiCGstab(ℓ) may have allocated the scratch already)
     CK(c, cudaMalloc(&c->gm_dev, sizeof(GmDev)));
-    CK(c, cudaMemset(c->gm_dev, 0, sizeof(GmDev)));
+    CK(c, cudaMemsetAsync(c->gm_dev, 0, sizeof(GmDev), c->stream));
   }
   if (!c->gm_part) {
     // one full wave of the multi-dot passes: CTAs per SM = their occupancy
@@ -1141,7 +1141,7 @@ static int gmres_workspace(ccg_ctx* c) {
         1, std::min<int64_t>((c->nloc + 255) / 256, (int64_t)c->sm_count * std::max(1, std::min(on, ox))));
     CK(c, cudaMalloc(&c->gm_part, (size_t)c->gm_grid * (GM_MAX + 1) * sizeof(double2)));
     CK(c, cudaMalloc(&c->gm_ticket, sizeof(unsigned)));
-    CK(c, cudaMemset(c->gm_ticket, 0, sizeof(unsigned)));
+    CK(c, cudaMemsetAsync(c->gm_ticket, 0, sizeof(unsigned), c->stream));
     CK(c, cudaMalloc(&c->gm_rank, (size_t)(GM_MAX + 1) * sizeof(double2)));
     CK(c, cudaMalloc(&c->gm_all, (size_t)c->world * (GM_MAX + 1) * sizeof(double2)));
   }
@@ -1352,7 +1352,10 @@ int ccg_get_history(ccg_handle c, double* rel_res, int32_t cap, int32_t* len) {
   if (!c || !len) return CCG_E_ARG;
   if (!c->hist || c->hist_len == 0) { *len = 0; return CCG_OK; }
   int32_t m = std::min<int32_t>(cap, c->hist_len);
-  if (m > 0 && rel_res) CK(c, cudaMemcpy(rel_res, c->hist, sizeof(double) * m, cudaMemcpyDeviceToHost));
+  if (m > 0 && rel_res) {   // ordered after the solve's kernels on the (non-blocking) library stream
+    CK(c, cudaMemcpyAsync(rel_res, c->hist, sizeof(double) * m, cudaMemcpyDeviceToHost, c->stream));
+    CK(c, cudaStreamSynchronize(c->stream));
+  }
   *len = m;
   return CCG_OK;
 }
