@@ -218,6 +218,9 @@ static int choose_launch(ccg_ctx* c) {
       while (H > 32 && nstr * ((c->nloc + H - 1) / H) < 2 * (int64_t)c->sm_count * std::max(1, occd2)) H /= 2;
       c->dual_H = (int)H;
       need_dual_h = (size_t)((c->nloc + H - 1) / H) * c->n * sizeof(C);
+      // part_sum_stage2: one CTA per 32 outputs, at most 8 CTAs per SM
+      c->sym_s2_grid = std::max(c->sym_s2_grid,
+                                (int)std::max<int64_t>(1, std::min<int64_t>((c->n + 31) / 32, (int64_t)c->sm_count * 8)));
     }
   }
   size_t need_sym_h = 0;

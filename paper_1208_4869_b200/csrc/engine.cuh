@@ -911,10 +911,10 @@ struct Engine {
       tev_begin(c, 0);
       launch_k(c, gemv_dual_rows<T, NT>, nstrips * nblk, NT, 0, c->stream, A, c->lda, pfull, qloc, c->nloc, c->n,
                c->dual_H, nstrips, np, hp, gate);
-      launch_k(c, gemv_h_stage2<T, NT, EpiA>, c->nstage2_grid, NT, 0, c->stream, static_cast<const C*>(np), nstrips,
-               c->nloc, 0, c->nloc, ea, make_red(c), c->st, gate);
-      launch_k(c, gemv_h_stage2<T, NT, EpiH>, c->stage2_grid, NT, 0, c->stream, static_cast<const C*>(hp), nblk, c->n,
-               0, c->n, eh, make_red(c), c->st, gate);
+      launch_k(c, part_sum_stage2<T, NT, EpiA>, c->sym_s2_grid, NT, 0, c->stream, static_cast<const C*>(np), nstrips,
+               c->nloc, c->nloc, ea, make_red(c), c->st, gate);
+      launch_k(c, part_sum_stage2<T, NT, EpiH>, c->sym_s2_grid, NT, 0, c->stream, static_cast<const C*>(hp), nblk, c->n,
+               c->n, eh, make_red(c), c->st, gate);
       c->launches += 3;
       tev_end(c);
       CK(c, cudaGetLastError());

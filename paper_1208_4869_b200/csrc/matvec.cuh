@@ -850,8 +850,9 @@ sym_check(const typename CT<T>::c* __restrict__ A, int64_t lda, int64_t n, int* 
         ok &= memcmp_c(a, b);
       }
     }
-    if (!ok) atomicExch(bad, 1);
-    __syncthreads();
+    // one atomic per CTA (a per-thread atomic on one address serialised
+    // ~300 k of them on a general matrix: 220 µs instead of a few)
+    if (__syncthreads_or(!ok) && threadIdx.x == 0) atomicExch(bad, 1);
   }
 }
 
@@ -1133,6 +1134,50 @@ gemv_sym_stage2(const typename CT<T>::c* __restrict__ npart, const typename CT<T
 #pragma unroll
       for (int k = 1; k < NW; ++k) { y.x += sh[k][lane].x; y.y += sh[k][lane].y; }
       if (valid) epi(i, fromd2<C>(y), dacc);
+    }
+    __syncthreads();
+  }
+  if constexpr (Epi::K > 0) finish_reduction<KK, NT, Epi>(dacc, red, st);
+}
+
+// w_j = Σ_s part[s][off + j] (fp64) with NT/32 load streams per output: a CTA
+// takes 32 consecutive outputs (lane = output), warp w sums the partials
+// s ≡ w (mod NT/32) in order, warp 0 adds the warp sums in warp order — a fixed
+// order; for the many-partial sums of the warp-per-row dual (64 strips / row
+// blocks at config 3) where one thread per output walking them was
+// latency-bound (18 µs per launch)
+template <typename T, int NT, class Epi>
+__global__ void __launch_bounds__(NT)
+part_sum_stage2(const typename CT<T>::c* __restrict__ part, int S, int64_t n, int64_t nout, Epi epi, Red red,
+                State* st, const int* gate) {
+  using C = typename CT<T>::c;
+  constexpr int KK = Epi::K > 0 ? Epi::K : 1;
+  constexpr int NW = NT / 32;
+  if (pdl_gate(gate)) return;
+  epi.load(st);
+  __shared__ double2 sh[NW][32];
+  double2 dacc[KK];
+#pragma unroll
+  for (int k = 0; k < KK; ++k) dacc[k] = make_double2(0.0, 0.0);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int64_t base = (int64_t)blockIdx.x * 32; base < nout; base += (int64_t)gridDim.x * 32) {
+    const int64_t j = base + lane;
+    const bool valid = j < nout;
+    double2 w = make_double2(0.0, 0.0);
+#pragma unroll 4
+    for (int sidx = warp; sidx < S; sidx += NW) {
+      if (valid) {
+        const C v = __ldcs(part + (int64_t)sidx * n + j);
+        w.x += (double)v.x; w.y += (double)v.y;
+      }
+    }
+    sh[warp][lane] = w;
+    __syncthreads();
+    if (warp == 0) {
+      double2 y = sh[0][lane];
+#pragma unroll
+      for (int k = 1; k < NW; ++k) { y.x += sh[k][lane].x; y.y += sh[k][lane].y; }
+      if (valid) epi(j, fromd2<C>(y), dacc);
     }
     __syncthreads();
   }
