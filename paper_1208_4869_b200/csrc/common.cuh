@@ -276,11 +276,25 @@ __device__ __forceinline__ void finish_reduction_at(double2 (&v)[K], const Red& 
   double2 acc[K];
 #pragma unroll
   for (int k = 0; k < K; ++k) acc[k] = make_double2(0.0, 0.0);
-  for (unsigned b = threadIdx.x; b < nb; b += NT) {
+  // slots b = tid, tid + NT, … summed in that order; the loads of U slots are
+  // issued together (one L2 round trip per U slots instead of one per slot —
+  // this serial tail runs on one SM while the rest of the GPU waits)
+  constexpr int U = K >= 8 ? 1 : 8 / K;   // <= 32 registers of loads in flight
+  for (unsigned b0 = threadIdx.x; b0 < nb; b0 += U * NT) {
+    double2 p[U][K];
 #pragma unroll
-    for (int k = 0; k < K; ++k) {
-      double2 p = __ldcg(red.part + (size_t)b * K + k);
-      acc[k].x += p.x; acc[k].y += p.y;
+    for (int u = 0; u < U; ++u) {
+      const unsigned b = b0 + u * NT;
+#pragma unroll
+      for (int k = 0; k < K; ++k)
+        p[u][k] = b < nb ? __ldcg(red.part + (size_t)b * K + k) : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (b0 + u * NT < nb) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) { acc[k].x += p[u][k].x; acc[k].y += p[u][k].y; }
+      }
     }
   }
   block_sum<K, NT>(acc, sm);

@@ -147,6 +147,7 @@ struct ccg_ctx {
   bool cl_redundant = true;  // cluster BiCGSTAB with redundant all-row passes (3 barriers/it; CCG_CL_REDUNDANT)
   bool fft_yz = false;     // FFT lattice operator: passes 2-4 fused (fft.cuh fft_yz; CCG_FFT_YZ)
   int stencil_minb = 4;   // stencil7_kernel launch bound: 4 CTAs/SM (≤ 64 registers); CCG_STENCIL_MINB=1: none
+  bool stencil_realo = true;   // skip the FMAs by exactly-zero imaginary parts of ox, oy, oz (CCG_STENCIL_REALO=0: keep them)
   bool sym_ok = false;
   int sym_state = 0;      // 0 general, 1 declared (CCG_FLAG_SYMMETRIC), 2 detected (A = Aᵀ bitwise)
   int sym_H = 64, sym_ntiles = 0, sym_strips = 1, sym_s2_grid = 1;
@@ -439,7 +440,16 @@ struct Engine {
       k[i].y = (T)(conj ? -c->scoef[i].y : c->scoef[i].y);
     }
     dim3 g((c->snx + 31) / 32, (c->sny + 7) / 8, (c->snzl + c->szc - 1) / c->szc);
-    auto kern = c->stencil_minb == 4 ? stencil7_kernel<T, Epi, XLoad<T>, 4> : stencil7_kernel<T, Epi, XLoad<T>, 1>;
+    // real off-diagonal coefficients (config 5's Laplacian): half the FMAs per neighbour term
+    const bool realo = c->stencil_realo && k[1].y == (T)0 && k[2].y == (T)0 && k[3].y == (T)0;
+    auto kern = c->stencil_minb != 4 ? stencil7_kernel<T, Epi, XLoad<T>, 1, false>
+                : realo              ? stencil7_kernel<T, Epi, XLoad<T>, 4, true>
+                                     : stencil7_kernel<T, Epi, XLoad<T>, 3, false>;
+    // the epilogue's early load is this product's own input (BsT, CrAr): the variant without it
+    if constexpr (EpiPreSrc<Epi>::has) {
+      if (c->stencil_minb == 4 && EpiPreSrc<Epi>::get(epi) == static_cast<const void*>(xfull + (int64_t)c->sz0 * c->snx * c->sny))
+        kern = realo ? stencil7_kernel<T, Epi, XLoad<T>, 4, true, true> : stencil7_kernel<T, Epi, XLoad<T>, 3, false, true>;
+    }
     launch_k(c, kern, g, 256, 0, c->stream, xfull, c->snx, c->sny, c->snz, c->sz0, c->snzl, c->szc,
                                                        k[0], k[1], k[2], k[3], epi, make_red(c), c->st, gate, XLoad<T>{});
   }

@@ -10,6 +10,7 @@
 // which finish_reduction() turns into the phase's recurrence scalars.
 #pragma once
 #include <type_traits>
+#include <utility>
 #include "bulk.cuh"
 #include "common.cuh"
 
@@ -85,6 +86,10 @@ __global__ void l2_demote(const typename CT<T>::c* A, int64_t lda, int64_t nrows
     if (!row_pinned(i, pin)) continue;
     const uintptr_t row = reinterpret_cast<uintptr_t>(A + i * lda) & ~(uintptr_t)127;
     const char* p = reinterpret_cast<const char*>(row) + (k % lines) * 128;
+    // the extra line of an aligned row starts at or past the row's end — for
+    // the last row that is past the end of A (an unmapped address when A ends
+    // its allocation: intermittent illegal access with every row pinned)
+    if (p >= reinterpret_cast<const char*>(A + i * lda + n)) continue;
     asm volatile("applypriority.global.L2::evict_normal [%0], 128;" ::"l"(p));
   }
 }
@@ -118,6 +123,21 @@ struct EpiPre<E, std::void_t<typename E::Pre>> {
   static __device__ __forceinline__ P pre(const E& e, int64_t i) { return e.pre(i); }
   template <class C>
   static __device__ __forceinline__ void post(E& e, int64_t i, C val, P p, double2* acc) { e.post(i, val, p, acc); }
+};
+
+// An epilogue whose early load is the product's own input at the output index
+// (BsT: ⟨t, s⟩ with t = A s; CrAr: [r, A r]) says so with `pre_src()`; the
+// stencil, which holds that element in a register already, then runs the
+// PREX variant without the load (its active phase is L1-bound: 6 → 5 16-byte loads per point).
+template <class E, class = void>
+struct EpiPreSrc {
+  static constexpr bool has = false;
+  static const void* get(const E&) { return nullptr; }
+};
+template <class E>
+struct EpiPreSrc<E, std::void_t<decltype(std::declval<const E&>().pre_src())>> {
+  static constexpr bool has = true;
+  static const void* get(const E& e) { return e.pre_src(); }
 };
 
 // ---------------------------------------------------------------------------
@@ -1513,15 +1533,29 @@ __global__ void csr_to_sell(const int32_t* __restrict__ rowptr, const int32_t* _
 // matrix, so the two operators give bitwise-identical products.
 // Block: 256 threads = 32 (x) × 8 (y); grid (⌈nx/32⌉, ⌈ny/8⌉, ⌈nzl/zc⌉).
 // ---------------------------------------------------------------------------
-// acc += coef·v (4 FMAs) where the neighbour exists; a select, not a branch,
-// so the loads of a plane stay batched and a missing neighbour leaves acc
-// bitwise untouched (the CSR row simply has no such entry)
-template <typename C>
-__device__ __forceinline__ void st_term(C& acc, C coef, C v, bool has) {
-  C t = acc;
-  cfma(t, coef, v);
-  acc.x = has ? t.x : acc.x;
-  acc.y = has ? t.y : acc.y;
+// Boundary handling without per-term selects (round 2; the select version was
+// issue-bound: 129 SASS instructions per point with the BsT epilogue, 24 FSEL
+// + 10 CS2R + ~12 predicate ops of them).  A missing x/y neighbour is handled
+// once per thread, outside the z loop: its load offset is clamped to 0 (the
+// thread re-reads its own point — always in bounds, and finite whenever the
+// point itself is) and its coefficient is a per-thread register set to 0, so
+// the loop body is 5 unconditional loads and 7 unconditional complex FMAs.
+// fma(0, v, acc) leaves acc bitwise unchanged for finite v unless acc is −0,
+// and acc (started at +0) can only be −0 after an underflow to −0: the product
+// stays bitwise equal to the CSR one except for the sign of such a zero
+// (DESIGN §4.3).  z: the plane below the lattice is a zero value; the plane
+// above is a predicated load (uniform per CTA).
+// REALO: ox, oy, oz have exactly zero imaginary parts (the Laplacian of
+// config 5): the two FMAs per term that multiply by it are skipped (same
+// caveat: they could only flip the sign of a zero component).
+template <bool REALO, typename C>
+__device__ __forceinline__ void st_fma(C& acc, C coef, C v) {
+  if constexpr (REALO) {
+    acc.x = fma(coef.x, v.x, acc.x);
+    acc.y = fma(coef.x, v.y, acc.y);
+  } else {
+    cfma(acc, coef, v);
+  }
 }
 
 // XIn: input transform (as in gemv_n_split) — each lattice value is formed as
@@ -1529,7 +1563,7 @@ __device__ __forceinline__ void st_term(C& acc, C coef, C v, bool has) {
 // the vector pass that would store it first is not a launch of its own; the
 // epilogue stores the element for its own point.  Only transforms that read
 // vectors this kernel does not write (no ping-pong needed between CTAs).
-template <typename T, class Epi, class XIn = XLoad<T>, int MINB = 1>
+template <typename T, class Epi, class XIn = XLoad<T>, int MINB = 1, bool REALO = false, bool PREX = false>
 __global__ void __launch_bounds__(256, MINB)
 stencil7_kernel(const typename CT<T>::c* __restrict__ x, int nx, int ny, int nz, int z0, int nzl, int zc,
                 typename CT<T>::c d, typename CT<T>::c ox, typename CT<T>::c oy, typename CT<T>::c oz,
@@ -1551,6 +1585,9 @@ stencil7_kernel(const typename CT<T>::c* __restrict__ x, int nx, int ny, int nz,
     const int plane = nx * ny;
     const bool hxm = ix > 0, hxp = ix < nx - 1, hym = iy > 0, hyp = iy < ny - 1;
     const C zero = czero<C>();
+    // per-thread clamped offsets and coefficients of the in-plane neighbours
+    const int oxm = hxm ? -1 : 0, oxq = hxp ? 1 : 0, oym = hym ? -nx : 0, oyq = hyp ? nx : 0;
+    const C cxm = hxm ? ox : zero, cxq = hxp ? ox : zero, cym = hym ? oy : zero, cyq = hyp ? oy : zero;
     int zg = z0 + zb;
     const C* xp = x + (int64_t)zg * plane + ix + nx * iy;
     int64_t gi = (int64_t)zg * plane + ix + nx * iy;    // global (input) index
@@ -1561,29 +1598,32 @@ stencil7_kernel(const typename CT<T>::c* __restrict__ x, int nx, int ny, int nz,
       else return xin(x, gi + o);
     };
     using EP = EpiPre<Epi>;
-    typename EP::P pnext = EP::pre(epi, li);   // the epilogue's inputs, a plane ahead
+    // PREX: the epilogue's early load is this product's own input element
+    // (chosen by the launcher from pre_src()): taken from `cur`, not loaded
+    typename EP::P pnext{};
+    if constexpr (!PREX) pnext = EP::pre(epi, li);   // the epilogue's inputs, a plane ahead
     C below = zg > 0 ? X(-plane) : zero;
     C cur = X(0);
 #pragma unroll 4
     for (int zl = zb; zl < ze; ++zl, ++zg) {
-      const typename EP::P pcur = pnext;
-      if (zl + 1 < ze) pnext = EP::pre(epi, li + plane);
-      const bool hzm = zg > 0, hzp = zg < nz - 1;
-      // every load of the plane first (masked to zero), then the terms in
-      // ascending column order
-      const C above = hzp ? X(plane) : zero;
-      const C ym = hym ? X(-nx) : zero;
-      const C xm = hxm ? X(-1) : zero;
-      const C xq = hxp ? X(1) : zero;
-      const C yq = hyp ? X(nx) : zero;
+      typename EP::P pcur = pnext;
+      if constexpr (PREX) pcur = cur;
+      else if (zl + 1 < ze) pnext = EP::pre(epi, li + plane);
+      // every load of the plane first, then the terms in ascending column order
+      C above = zero;
+      if (zg < nz - 1) above = X(plane);
+      const C ym = X(oym);
+      const C xm = X(oxm);
+      const C xq = X(oxq);
+      const C yq = X(oyq);
       C acc = zero;
-      st_term(acc, oz, below, hzm);
-      st_term(acc, oy, ym, hym);
-      st_term(acc, ox, xm, hxm);
-      st_term(acc, d, cur, true);
-      st_term(acc, ox, xq, hxp);
-      st_term(acc, oy, yq, hyp);
-      st_term(acc, oz, above, hzp);
+      st_fma<REALO>(acc, oz, below);
+      st_fma<REALO>(acc, cym, ym);
+      st_fma<REALO>(acc, cxm, xm);
+      cfma(acc, d, cur);
+      st_fma<REALO>(acc, cxq, xq);
+      st_fma<REALO>(acc, cyq, yq);
+      st_fma<REALO>(acc, oz, above);
       EP::post(epi, li, acc, pcur, dacc);
       below = cur;
       cur = above;

@@ -205,6 +205,7 @@ struct BsT {  // t = A s ; ⟨t,s⟩, ⟨t,t⟩ ; ω
   __device__ void load(const State*) {}
   using Pre = C;   // early load (matvec.cuh EpiPre)
   __device__ Pre pre(int64_t i) const { return s[i]; }
+  __host__ __device__ const void* pre_src() const { return s; }   // the product's own input: no second load (EpiPreSrc)
   __device__ void post(int64_t i, C val, Pre si, double2* acc) {
     t[i] = val;
     dotc_acc(acc[0], val, si);
@@ -860,6 +861,7 @@ struct CrAr {  // Ar = A r ; μ' = [r, Ar] ; β = μ'/μ   (end of iteration k =
   // early load of the epilogue input (issued with the product's loads; matvec.cuh EpiPre)
   using Pre = C;
   __device__ Pre pre(int64_t i) const { return r[i]; }
+  __host__ __device__ const void* pre_src() const { return r; }   // the product's own input (EpiPreSrc)
   __device__ void post(int64_t i, C val, Pre b, double2* acc) { ar[i] = val; dotu_acc(acc[0], b, val); }
   __device__ void operator()(int64_t i, C val, double2* acc) { post(i, val, pre(i), acc); }
   static __device__ void finish(State* st, const double2* s) {

@@ -157,6 +157,37 @@ def test_l2_pin_bitwise(monkeypatch, cfg2_sys, method):
     assert np.array_equal(a["x"], b["x"]) and np.array_equal(a["x"], c["x"])
 
 
+def test_l2_pin_all_rows_default_stays_inside_A():
+    """A between 32 MB and the default 80 MB pin budget has every row pinned by
+    default; l2_demote's extra (unaligned-row) line of the LAST row then lay
+    past the end of A — an illegal access whenever A ends its mapping.  c128
+    n = 1536 is exactly 18 × 2 MiB, so a fresh allocation ends on a mapping
+    boundary; several fresh allocations make an unmapped neighbour likely."""
+    import torch
+    import paper_1208_4869_b200 as ccg
+    n = 1536
+    A = gauss_shifted_rows(n, 0, n, seed=5).astype(np.complex128) + 2.0 * np.eye(n)
+    y = cfg3_rhs(n).astype(np.complex128)
+    ref = None
+    for _ in range(4):
+        torch.cuda.empty_cache()
+        Ad = torch.from_numpy(A).cuda()
+        yd = torch.from_numpy(y).cuda()
+        xd = torch.empty_like(yd)
+        h = ccg.ccg_create("c128", n)
+        try:
+            ccg.ccg_set_matvec_dense(h, Ad, 0, n)
+            r = ccg.ccg_solve(h, "bicgstab", None, yd, xd, 1e-10, 200)
+        finally:
+            ccg.ccg_destroy(h)
+        assert r["status"] == "CONVERGED"
+        x = xd.cpu().numpy()
+        assert ref is None or np.array_equal(x, ref)
+        ref = x
+        del Ad
+    assert relerr(A @ ref, y) <= 1e-9
+
+
 @pytest.mark.parametrize("sysname", ["cfg2_sys", "c64_sys"])
 def test_split_fuse(request, monkeypatch, sysname):
     A, y = request.getfixturevalue(sysname)
