@@ -239,6 +239,27 @@ def test_stencil_apply_parity(dtype, dims):
             assert relerr(h.apply(x, o), reference_apply(op, x, o)) <= TOL[dtype], o
 
 
+@pytest.mark.parametrize("dtype", [np.complex128, np.complex64])
+@pytest.mark.parametrize("dims", [(1, 1, 1), (1, 5, 1), (2, 3, 4), (33, 9, 5), (31, 17, 12), (128, 8, 9), (65, 10, 17)])
+def test_stencil_apply_parity_real_offdiagonals(dtype, dims):
+    """Real ox, oy, oz (a Laplacian-type operator, as config 5's) run the REALO
+    kernel variant (matvec.cuh stencil7_kernel: the FMAs by the zero imaginary
+    part are skipped): same parity bar at ragged sizes, and — the CSR kernel
+    keeps those FMAs — equal values element by element."""
+    nx, ny, nz = dims
+    d, ox, oy, oz = 5.5 - 0.25j, -1.0, -0.5, 0.75
+    rp, ci, v = lattice_csr(nx, ny, nz, d, ox, oy, oz, dtype=dtype)
+    op = CsrOp(rp, ci, v)
+    x = _x(nx * ny * nz, dtype, seed=nx + 7)
+    with Stencil(nx, ny, nz, d, ox, oy, oz, dtype=dtype) as h:
+        for o in ("A", "AH", "AT"):
+            assert relerr(h.apply(x, o), reference_apply(op, x, o)) <= TOL[dtype], o
+        ys = h.apply(x, "A")
+    if nx * ny * nz >= 1000:   # the SELL CSR kernel (same FMA order; tiny matrices take other CSR kernels)
+        with Csr(rp, ci, v, nx * ny * nz) as hc:
+            assert np.array_equal(hc.apply(x, "A"), ys)
+
+
 def test_stencil_bitwise_equals_csr_kernel():
     """Same arithmetic as the SELL CSR kernel (FMA accumulation in ascending
     column order): the stencil and the CSR operator agree bitwise on every
