@@ -240,7 +240,14 @@ int ccg_set_matvec_csr(ccg_handle h, const int32_t* rowptr, const int32_t* colin
  *            (copied; finite, else CCG_E_ARG).
  *   flags  : unused (A is complex symmetric by construction).
  * Supports CCG_OP_A, CCG_OP_AT (= A) and CCG_OP_AH (conjugated coefficients),
- * hence every method, on any world size. */
+ * hence every method, on any world size.
+ *   Arithmetic: the terms are accumulated by FMA in ascending column order, as
+ *   the CSR kernel does on the equivalent matrix; an omitted term is a zero
+ *   coefficient times the point's own value, so the result equals the CSR
+ *   product bit for bit except the sign of a component that underflowed to −0,
+ *   and a non-finite u_i makes (A u)_i non-finite (as d·u_i already does).
+ *   Off-diagonal coefficients with exactly zero imaginary parts (the
+ *   Laplacian case) take a kernel that skips the multiplications by them. */
 int ccg_set_matvec_stencil7(ccg_handle h, int64_t nx, int64_t ny, int64_t nz, const double* coeffs,
                             uint32_t flags);
 
