@@ -892,7 +892,7 @@ int ccg_set_matvec_stencil7(ccg_handle c, int64_t nx, int64_t ny, int64_t nz, co
   // latency-bound; interleaved A/B at config 5 (ab/cfg5_stencil_minb.jsonl):
   // BiCGSTAB 142.9 -> 129.8 us/it, CORS 174.3 -> 155.8, COCR 101.5 -> 93.4
   const char* smb = getenv("CCG_STENCIL_MINB");
-  c->stencil_minb = smb && atoi(smb) == 1 ? 1 : 4;
+  c->stencil_minb = smb && atoi(smb) == 1 ? 1 : smb && atoi(smb) == 3 ? 3 : 4;
   const char* sro = getenv("CCG_STENCIL_REALO");
   c->stencil_realo = !(sro && atoi(sro) == 0);
   c->szc = zc ? std::max(1, atoi(zc)) : 8;   // 1024 CTAs at 128³: one wave, half the reduction slots of 4 (ab/cfg5_zc.jsonl)

@@ -430,6 +430,18 @@ struct Engine {
           c->rowptr, c->colind, vals, x, c->mnloc, epi, make_red(c), c->st, gate);
   }
 
+  // does this kernel use more than a few words of local memory per thread (register spills)?  Asked once
+  // per kernel and handle; bits 4 (asked) and 8 (yes) of the handle's per-kernel flags
+  static bool kernel_spills(ccg_ctx* c, const void* kern) {
+    int& f = c->occ_cache[kern];
+    if (!(f & 4)) {
+      cudaFuncAttributes a;
+      f |= 4;
+      if (cudaFuncGetAttributes(&a, kern) == cudaSuccess && a.localSizeBytes > 96) f |= 8;
+    }
+    return (f & 8) != 0;
+  }
+
   // matrix-free stencil; conj => Aᴴ (= the stencil with conjugated
   // coefficients, A being complex symmetric)
   template <class Epi>
@@ -442,13 +454,25 @@ struct Engine {
     dim3 g((c->snx + 31) / 32, (c->sny + 7) / 8, (c->snzl + c->szc - 1) / c->szc);
     // real off-diagonal coefficients (config 5's Laplacian): half the FMAs per neighbour term
     const bool realo = c->stencil_realo && k[1].y == (T)0 && k[2].y == (T)0 && k[3].y == (T)0;
-    auto kern = c->stencil_minb != 4 ? stencil7_kernel<T, Epi, XLoad<T>, 1, false>
-                : realo              ? stencil7_kernel<T, Epi, XLoad<T>, 4, true>
-                                     : stencil7_kernel<T, Epi, XLoad<T>, 3, false>;
     // the epilogue's early load is this product's own input (BsT, CrAr): the variant without it
-    if constexpr (EpiPreSrc<Epi>::has) {
-      if (c->stencil_minb == 4 && EpiPreSrc<Epi>::get(epi) == static_cast<const void*>(xfull + (int64_t)c->sz0 * c->snx * c->sny))
-        kern = realo ? stencil7_kernel<T, Epi, XLoad<T>, 4, true, true> : stencil7_kernel<T, Epi, XLoad<T>, 3, false, true>;
+    bool prex = false;
+    if constexpr (EpiPreSrc<Epi>::has)
+      prex = EpiPreSrc<Epi>::get(epi) == static_cast<const void*>(xfull + (int64_t)c->sz0 * c->snx * c->sny);
+    auto kern = stencil7_kernel<T, Epi, XLoad<T>, 1, false>;
+    if (c->stencil_minb == 3 && realo) {   // CCG_STENCIL_MINB=3: every epilogue at 3 CTAs/SM (A/B)
+      kern = stencil7_kernel<T, Epi, XLoad<T>, 3, true>;
+      if constexpr (EpiPreSrc<Epi>::has) { if (prex) kern = stencil7_kernel<T, Epi, XLoad<T>, 3, true, true>; }
+    } else if (c->stencil_minb >= 3) {
+      if (realo) {
+        // 4 CTAs/SM (64 registers) unless the epilogue then spills (TFQMR's TfO: 256 B, CGS's CsR: 128 B
+        // of local memory per thread; the others ≤ 32) — those run at 3 CTAs/SM (80 registers, no spills)
+        kern = stencil7_kernel<T, Epi, XLoad<T>, 4, true>;
+        if constexpr (EpiPreSrc<Epi>::has) { if (prex) kern = stencil7_kernel<T, Epi, XLoad<T>, 4, true, true>; }
+        if (kernel_spills(c, reinterpret_cast<const void*>(kern))) kern = stencil7_kernel<T, Epi, XLoad<T>, 3, true>;
+      } else {
+        kern = stencil7_kernel<T, Epi, XLoad<T>, 3, false>;
+        if constexpr (EpiPreSrc<Epi>::has) { if (prex) kern = stencil7_kernel<T, Epi, XLoad<T>, 3, false, true>; }
+      }
     }
     launch_k(c, kern, g, 256, 0, c->stream, xfull, c->snx, c->sny, c->snz, c->sz0, c->snzl, c->szc,
                                                        k[0], k[1], k[2], k[3], epi, make_red(c), c->st, gate, XLoad<T>{});
