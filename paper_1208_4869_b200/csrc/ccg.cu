@@ -895,7 +895,18 @@ int ccg_set_matvec_stencil7(ccg_handle c, int64_t nx, int64_t ny, int64_t nz, co
   c->stencil_minb = smb && atoi(smb) == 1 ? 1 : smb && atoi(smb) == 3 ? 3 : 4;
   const char* sro = getenv("CCG_STENCIL_REALO");
   c->stencil_realo = !(sro && atoi(sro) == 0);
-  c->szc = zc ? std::max(1, atoi(zc)) : 8;   // 1024 CTAs at 128³: one wave, half the reduction slots of 4 (ab/cfg5_zc.jsonl)
+  if (zc) {
+    c->szc = std::max(1, atoi(zc));
+  } else {
+    // the longest z-march of 16, 8, 4 planes that still gives ≥ 3 CTAs per SM (fewer z-chunk halo planes
+    // re-read, fewer reduction slots; with the loop unrolled by 2 — ab/cfg5_stencil_zc_unroll2.jsonl —
+    // 16 beats 8 at 128³: BiCGSTAB 121.0 → 119.3 µs/it, CORS 149.4 → 144.6, CGS 117.8 → 112.1)
+    const int64_t tiles = ((nx + 31) / 32) * ((ny + 7) / 8);
+    c->szc = 4;
+    for (int z : {16, 8}) {
+      if (tiles * ((c->snzl + z - 1) / z) >= 3 * (int64_t)c->sm_count) { c->szc = z; break; }
+    }
+  }
   invalidate_graphs(c);
   return c->dtype == CCG_C64 ? choose_launch<float>(c) : choose_launch<double>(c);
 }

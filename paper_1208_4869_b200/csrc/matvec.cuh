@@ -1604,7 +1604,7 @@ stencil7_kernel(const typename CT<T>::c* __restrict__ x, int nx, int ny, int nz,
     if constexpr (!PREX) pnext = EP::pre(epi, li);   // the epilogue's inputs, a plane ahead
     C below = zg > 0 ? X(-plane) : zero;
     C cur = X(0);
-#pragma unroll 4
+#pragma unroll 2
     for (int zl = zb; zl < ze; ++zl, ++zg) {
       typename EP::P pcur = pnext;
       if constexpr (PREX) pcur = cur;
