@@ -532,6 +532,8 @@ static int create_impl(ccg_handle* h, ccg_dtype dt, int64_t n, int world, int ra
     // take two loads per neighbour), so opt-in
     const char* br = getenv("CCG_BS_FUSE_RO");
     c->bs_fuse_ro = br ? atoi(br) != 0 : 0;
+    const char* bm = getenv("CCG_BS_MERGE");
+    c->bs_merge = bm ? atoi(bm) != 0 : 0;
   }
   auto bail = [&](int code) {
     g_create_err = c->err;

@@ -130,6 +130,7 @@ struct ccg_ctx {
   int gemv_mode = 0;      // GEMV_SPLIT (default) | GEMV_BULK | GEMV_ROWS (env CCG_GEMV)
   int split_W = 0, split_strips = 1, split_nrb = 1, nstage2_grid = 1, split_ur = 8;
   int bs_fuse = 1;        // BiCGSTAB P/S passes folded into the products (Engine::in_fuse_ok; CCG_BS_FUSE)
+  int bs_merge = 0;       // BiCGSTAB X and P passes merged on the stencil / SELL SpMV (Engine::bs_merge_ok; CCG_BS_MERGE)
   int bs_fuse_ro = 0;     // the S fold on the stencil / SELL SpMV (Engine::in_fuse_ro_ok; CCG_BS_FUSE_RO)
   int split_fuse = 0;     // several strips: strip sum + epilogue by the last CTA of each row block (CCG_SPLIT_FUSE)
   unsigned* rb_ticket = nullptr;   // [split_nrb] arrival tickets (zero between launches)
@@ -630,6 +631,12 @@ struct Engine {
   static bool in_fuse_ro_ok(const ccg_ctx* c) {
     if (in_fuse_ok(c)) return true;
     return c->bs_fuse_ro && !c->dist && !c->jac_active &&
+           (c->opk == OPK_STENCIL || (c->opk == OPK_CSR && c->sell_col));
+  }
+
+  // BiCGSTAB with the X and P passes merged (methods.cuh BsTm / BsXP): single GPU, sparse operators
+  static bool bs_merge_ok(const ccg_ctx* c) {
+    return c->bs_merge && !c->dist && !c->jac_active && !c->bs_fuse_ro &&
            (c->opk == OPK_STENCIL || (c->opk == OPK_CSR && c->sell_col));
   }
 

@@ -338,6 +338,81 @@ struct BsX {  // x += αp + ωs ; r = s − ωt ; ‖r‖², ⟨r̃, r⟩   (hal
   }
 };
 
+// ---- BiCGSTAB with the X and P passes merged (single GPU, stencil / SELL
+// SpMV; Engine::bs_merge_ok, CCG_BS_MERGE=1).  ρ' = ⟨r̃, r'⟩ with r' = s − ωt
+// is linear in r', so the t = A s product, which already reduces ⟨t,s⟩ and
+// ⟨t,t⟩, also reduces ⟨r̃,s⟩ and ⟨r̃,t⟩ and its scalar step forms
+// ρ' = ⟨r̃,s⟩ − ω⟨r̃,t⟩ and β right after ω.  The x / r update and the next
+// direction p = r' + β(p − ωv) are then ONE pass (5 vectors read, 3 written)
+// instead of BsX (5 + 2) followed by BsP (3 + 1): 4 launches and 16 instead of
+// 19 vector streams per iteration.  Same recurrence in exact arithmetic; ρ'
+// differs from the directly summed ⟨r̃, r'⟩ by rounding (a cancellation of
+// relative size ‖s‖/‖r'‖), so this path is compared with the oracle by the
+// P-envelope, not bit for bit with the default path.  The ρ' = 0 / non-finite
+// tests stay where the literal recurrence has them — after the convergence
+// test of the merged pass.
+template <typename T>
+struct BsTm {   // t = A s ; ⟨t,s⟩, ⟨t,t⟩, ⟨r̃,s⟩, ⟨r̃,t⟩ ; ω, ρ', β
+  static constexpr int K = 4;
+  using C = Cx<T>;
+  C* t; const C* s; const C* rt;
+  __device__ void load(const State*) {}
+  struct Pre { C s, rt; };
+  __device__ Pre pre(int64_t i) const { return Pre{s[i], rt[i]}; }
+  __device__ void post(int64_t i, C val, Pre b, double2* acc) {
+    t[i] = val;
+    dotc_acc(acc[0], val, b.s);
+    nrm_acc(acc[1], val);
+    dotc_acc(acc[2], b.rt, b.s);
+    dotc_acc(acc[3], b.rt, val);
+  }
+  __device__ void operator()(int64_t i, C val, double2* acc) { post(i, val, pre(i), acc); }
+  static __device__ void finish(State* st, const double2* sm) {
+    BsT<T>::finish(st, sm);
+    if (st->done) return;
+    const double2 wt = zmul(st->omega, sm[3]);
+    const double2 rho_new = make_double2(sm[2].x - wt.x, sm[2].y - wt.y);
+    st->pb_rho = rho_new;   // tested in BsXP::finish, after the convergence test
+    st->beta = zmul(zdiv(rho_new, st->rho), zdiv(st->alpha, st->omega));
+  }
+};
+
+template <typename T>
+struct BsXP {   // x += αp + ωs ; r = s − ωt ; p = r + β(p − ωv) ; ‖r‖²   (half-step: x += αp)
+  static constexpr int K = 1;
+  using C = Cx<T>;
+  C* x; C* r; C* p; const C* s; const C* t; const C* v;
+  C alpha, omega, beta; int half;
+  __device__ void load(const State* st) {
+    alpha = fromd2<C>(st->alpha); omega = fromd2<C>(st->omega); beta = fromd2<C>(st->beta); half = st->half;
+  }
+  __device__ void operator()(int64_t i, double2* acc) {
+    if (half) { x[i] = caxpy(x[i], alpha, p[i]); return; }
+    const C xi = x[i], pi = p[i], si = s[i], ti = t[i], vi = v[i];
+    x[i] = caxpy(caxpy(xi, alpha, pi), omega, si);
+    const C ri = caxmy(si, omega, ti);
+    r[i] = ri;
+    p[i] = bs_pnew(ri, pi, vi, beta, omega, 0);
+    nrm_acc(acc[0], ri);
+  }
+  static __device__ void finish(State* st, const double2* sm) {
+    const int k = st->iter + 1;
+    if (st->half) {
+      push_hist(st, k, st->ss);
+      set_done(st, ST_CONVERGED, k);
+      return;
+    }
+    bool stop;
+    conv_check_common(st, k, sm[0].x, stop);
+    if (stop) return;
+    const double2 rho_new = st->pb_rho;
+    if (!zfinite(rho_new)) { set_done(st, ST_NONFINITE, k); return; }
+    if (zzero(rho_new)) { set_done(st, ST_BREAKDOWN, k, BD_RHO); return; }
+    st->rho = rho_new;
+    st->iter = k;
+  }
+};
+
 // ===========================================================================
 // O2 CGNE (Craig).  Setup: AH r → P0 (π, α).  Per iteration:
 // [A p → r −= αAp, x += αp, ‖r‖²] → [Aᴴ r → p = Aᴴr + βp, ‖p‖²]

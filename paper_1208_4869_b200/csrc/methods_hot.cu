@@ -7,12 +7,22 @@
 #endif
 
 template <typename T>
-int Engine<T>::bicgstab_setup(ccg_ctx* c, bool x0) { return init_residual(c, x0, L(c, 2), L(c, 3), nullptr, nullptr); }
+int Engine<T>::bicgstab_setup(ccg_ctx* c, bool x0) {
+  TRY(init_residual(c, x0, L(c, 2), L(c, 3), nullptr, nullptr));
+  if (bs_merge_ok(c)) return pass(c, BsP<T>{L(c, 2), Fs(c, 0), L(c, 4)}, &c->st->done);   // p = r; later p's come from BsXP
+  return CCG_OK;
+}
 
 template <typename T>
 int Engine<T>::bicgstab_iter(ccg_ctx* c) {
   const int* g = &c->st->done;
   const int* g2 = &c->st->gate2;
+  if (bs_merge_ok(c)) {   // X and P passes merged, ρ' from the t = A s reduction (methods.cuh BsTm / BsXP)
+    TRY(matvec_a(c, F(c, 0), BsV<T>{L(c, 4), L(c, 3)}, g));
+    TRY(pass(c, BsS<T>{L(c, 2), L(c, 4), Fs(c, 1)}, g));
+    TRY(matvec_a(c, F(c, 1), BsTm<T>{L(c, 5), Fs(c, 1), L(c, 3)}, g2));
+    return pass(c, BsXP<T>{L(c, X), L(c, 2), Fs(c, 0), Fs(c, 1), L(c, 5), L(c, 4)}, g);
+  }
   if (in_fuse_ok(c)) {   // P and S formed inside the products (methods.cuh BsPIn / BsSIn)
     TRY(matvec_a_in(c, BsPIn<T>{L(c, 2), Fs(c, 0), L(c, 4)}, BsV2<T>{L(c, 4), L(c, 3), L(c, 2), Fs(c, 0)}, g));
     TRY(matvec_a_in(c, BsSIn<T>{L(c, 2), L(c, 4)}, BsT2<T>{L(c, 5), Fs(c, 1), L(c, 2), L(c, 4)}, g));

@@ -188,6 +188,46 @@ def test_l2_pin_all_rows_default_stays_inside_A():
     assert relerr(A @ ref, y) <= 1e-9
 
 
+@pytest.mark.parametrize("kind", ["stencil", "csr"])
+def test_bs_merge_opt_in(monkeypatch, kind):
+    """CCG_BS_MERGE=1 (opt-in; methods.cuh BsTm / BsXP: the X and P passes of
+    BiCGSTAB merged, ρ' = ⟨r̃,s⟩ − ω⟨r̃,t⟩ from the t = A s reduction): the same
+    recurrence up to rounding — x equal to the default path's at a small fixed
+    k, and a full solve that converges in about as many iterations with the
+    same true residual bar."""
+    import paper_1208_4869_b200 as ccg
+    from tests._gpu import to_dev
+    from workloads import lattice_csr, helmholtz_coeffs, helmholtz_rhs
+    N = 16
+    d, o = helmholtz_coeffs()
+    rp, ci, v = lattice_csr(N, N, N, d, o)
+    y = helmholtz_rhs(N)
+    out = {}
+    for m in ("0", "1"):
+        monkeypatch.setenv("CCG_BS_MERGE", m)
+        h = ccg.ccg_create("c128", N ** 3)
+        try:
+            if kind == "stencil":
+                ccg.ccg_set_matvec_stencil7(h, N, N, N, d, o)
+            else:
+                keep = [to_dev(a) for a in (rp, ci, v)]
+                ccg.ccg_set_matvec_csr(h, *keep, 0, N ** 3, len(v))
+            yd = to_dev(y)
+            xd = to_dev(np.zeros_like(y))
+            r8 = ccg.ccg_solve(h, "bicgstab", None, yd, xd, 0.0, 8)
+            x8 = xd.cpu().numpy().copy()
+            rf = ccg.ccg_solve(h, "bicgstab", None, yd, xd, 1e-8, 4000)
+            out[m] = (r8, x8, rf)
+        finally:
+            ccg.ccg_destroy(h)
+    (a8, xa, af), (b8, xb, bf) = out["0"], out["1"]
+    assert a8["iterations"] == b8["iterations"] == 8 and a8["matvecs_a"] == b8["matvecs_a"]
+    assert relerr(xb, xa) <= 1e-9
+    assert af["status"] == bf["status"] == "CONVERGED"
+    assert abs(af["iterations"] - bf["iterations"]) <= 4
+    assert bf["true_rel_res"] <= 1.001e-8
+
+
 @pytest.mark.parametrize("sysname", ["cfg2_sys", "c64_sys"])
 def test_split_fuse(request, monkeypatch, sysname):
     A, y = request.getfixturevalue(sysname)
