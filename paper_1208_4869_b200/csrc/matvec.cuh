@@ -140,6 +140,13 @@ struct EpiPreSrc<E, std::void_t<decltype(std::declval<const E&>().pre_src())>> {
   static const void* get(const E& e) { return e.pre_src(); }
 };
 
+// An epilogue with `WANTS_X` and `post_x(i, val, pre, x_i, acc)` takes the product's own input element
+// from the stencil's register (BsTm; valid where the caller guarantees input == that vector)
+template <class E, class = void>
+struct EpiWantsX : std::false_type {};
+template <class E>
+struct EpiWantsX<E, std::enable_if_t<E::WANTS_X>> : std::true_type {};
+
 // ---------------------------------------------------------------------------
 // K1 gemv_n: y_i = Σ_j A_ij x_j for local rows [0, nrows), row-major A.
 // Persistent, balanced: CTA b owns rows [b·nrows/G, (b+1)·nrows/G) and walks
@@ -1624,7 +1631,8 @@ stencil7_kernel(const typename CT<T>::c* __restrict__ x, int nx, int ny, int nz,
       st_fma<REALO>(acc, cxq, xq);
       st_fma<REALO>(acc, cyq, yq);
       st_fma<REALO>(acc, oz, above);
-      EP::post(epi, li, acc, pcur, dacc);
+      if constexpr (PLAIN && EpiWantsX<Epi>::value) epi.post_x(li, acc, pcur, cur, dacc);
+      else EP::post(epi, li, acc, pcur, dacc);
       below = cur;
       cur = above;
       xp += plane;

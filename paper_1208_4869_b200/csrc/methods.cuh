@@ -357,15 +357,19 @@ struct BsTm {   // t = A s ; ⟨t,s⟩, ⟨t,t⟩, ⟨r̃,s⟩, ⟨r̃,t⟩ ; ω
   using C = Cx<T>;
   C* t; const C* s; const C* rt;
   __device__ void load(const State*) {}
-  struct Pre { C s, rt; };
-  __device__ Pre pre(int64_t i) const { return Pre{s[i], rt[i]}; }
-  __device__ void post(int64_t i, C val, Pre b, double2* acc) {
+  using Pre = C;   // early load of r̃ (matvec.cuh EpiPre)
+  __device__ Pre pre(int64_t i) const { return rt[i]; }
+  // the stencil passes the product's own input element (s, by construction of bicgstab_iter's
+  // merged path: single GPU, no preconditioner) from its register instead of a second load
+  static constexpr bool WANTS_X = true;
+  __device__ void post_x(int64_t i, C val, Pre rti, C si, double2* acc) {
     t[i] = val;
-    dotc_acc(acc[0], val, b.s);
+    dotc_acc(acc[0], val, si);
     nrm_acc(acc[1], val);
-    dotc_acc(acc[2], b.rt, b.s);
-    dotc_acc(acc[3], b.rt, val);
+    dotc_acc(acc[2], rti, si);
+    dotc_acc(acc[3], rti, val);
   }
+  __device__ void post(int64_t i, C val, Pre rti, double2* acc) { post_x(i, val, rti, s[i], acc); }
   __device__ void operator()(int64_t i, C val, double2* acc) { post(i, val, pre(i), acc); }
   static __device__ void finish(State* st, const double2* sm) {
     BsT<T>::finish(st, sm);
